@@ -1,0 +1,144 @@
+/*
+ * heff.h -- C ABI of libheff: the B200 (sm_100a) two-site DMRG effective-Hamiltonian
+ * matvec H_eff.psi and the Lanczos ground-state solver around it.
+ *
+ * What is computed (citations: lines of the paper text, /root/reference/PAPER.md).
+ *   DMRG computes "dominant eigenvectors of very large Hermitian linear operators"
+ *   (Sec. 6.2).  At a two-site window the operator is the product of
+ *   the left environment, the two MPO tensors of Eq. (1)'s MPO form (Sec. 6.1,
+ *   PAPER.md:666-672) and the right environment, contracted over all matching indices by
+ *   ITensor's `*` (Sec. 4) with primes keeping the output legs apart
+ *   (Sec. 2.6):
+ *
+ *     out[a',s1',s2',b'] = sum_{a,w,s1,w1,s2,w2,b}
+ *          L[a',w,a] W1[w,s1',s1,w1] W2[w1,s2',s2,w2] R[b',w2,b] psi[a,s1,s2,b]     (D)
+ *
+ *   The output is returned un-primed in psi's layout.  libheff evaluates
+ *   (D) exactly (up to rounding order) in the north_star's four steps
+ *   L.psi -> .W1 -> .W2 -> .R (order A) on one GPU, and in the mirror order
+ *   R.psi -> .W2 -> .W1 -> .L on a b'-shard (order B, reading R17).
+ *
+ * Layout: every tensor is dense, row-major (last index fastest), IEEE fp64:
+ *   L  [mL][kL][mL]     W1 [kL][d1][d1][kM]    W2 [kM][d2][d2][kR]
+ *   R  [nb][kR][mR]     rows b' in [b_lo, b_hi) of R (all mR rows when dist == NULL)
+ *   psi, out  [mL][d1][d2][mR]   (a b'-shard [mL][d1][d2][nb] where stated)
+ *
+ * Pointers: every tensor pointer is a DEVICE pointer on the current CUDA device unless
+ * the function name ends in _host.  Alignment: 8 B required; 16 B (and even row
+ * lengths) enables the TMA-fed GEMM path, otherwise a plain-load path runs.
+ *
+ * Ownership: L, W1, W2 and R are BORROWED -- they must stay allocated and unmodified
+ * for the plan's lifetime (W1/W2 are also copied at create).  The plan owns its
+ * workspace (intermediates, Lanczos basis, gather buffer) and its NCCL communicator.
+ *
+ * Streams: `heff_stream` is a cudaStream_t (NULL = legacy default stream).  heff_apply
+ * is stream-ordered and returns before completion.  lanczos_ground blocks until done.
+ *
+ * Errors: functions return HEFF_OK (0) or a negative code; heff_last_error() gives a
+ * thread-local message for the last failure.  There is no CPU fallback: a missing or
+ * failing device is an error.
+ *
+ * Concurrency: one plan per host thread at a time.
+ */
+#ifndef HEFF_H
+#define HEFF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct heff_plan_s* heff_plan;
+typedef void* heff_stream; /* cudaStream_t */
+
+enum {
+  HEFF_OK = 0,
+  HEFF_EINVAL = -1,      /* null pointer, bad shape, aliasing, bad b-range      */
+  HEFF_ENOMEM = -2,      /* device allocation failed                            */
+  HEFF_ECUDA = -3,       /* CUDA runtime / driver error                         */
+  HEFF_ENCCL = -4,       /* NCCL error (load, init or collective)               */
+  HEFF_EZERO = -5,       /* lanczos start vector is zero          */
+  HEFF_EUNSUPPORTED = -6 /* request outside what this build supports            */
+};
+
+/* Dimensions: bond dims mL, mR; site dims d1, d2; MPO bond dims kL (L/W1), kM (W1/W2),
+ * kR (W2/R).  All >= 1. */
+typedef struct {
+  int64_t mL, d1, d2, mR, kL, kM, kR;
+} heff_dims;
+
+/* Multi-GPU partition over the output right bond b' (R17).
+ * This rank owns b' in [b_lo, b_hi); its R argument holds exactly those rows.
+ * nccl_uid: 128-byte ncclUniqueId from heff_nccl_unique_id() on rank 0, broadcast by
+ * the caller (torch.distributed).  nccl_uid == NULL gives a "virtual shard": the plan
+ * computes its out-shard from a full psi with no communicator (heff_apply only). */
+typedef struct {
+  int nranks, rank;
+  const unsigned char* nccl_uid;
+  int64_t b_lo, b_hi;
+} heff_dist;
+
+/* Lanczos options (readings R11-R14).
+ *   mode 0 (fixed): exactly max_iter matvecs unless an invariant subspace is hit;
+ *   mode 1 (converge): stop when beta_j |y_j[last]| <= tol * hnorm_j, or at max_iter.
+ * alpha_out, beta_out, theta_out: optional HOST arrays of >= max_iter doubles receiving
+ * the tridiagonal T_j and the lowest Ritz value after every step. */
+typedef struct {
+  int max_iter;
+  int mode;
+  double tol;
+  double* alpha_out;
+  double* beta_out;
+  double* theta_out;
+} heff_lanczos_opts;
+
+/* Create a plan: validates dims, copies W1/W2, allocates workspace, and (dist with a
+ * uid) joins the NCCL communicator (collective over all ranks). */
+int heff_create(heff_plan* out, const heff_dims* dims, const double* L, const double* W1, const double* W2,
+                const double* R, const heff_dist* dist, heff_stream stream);
+
+/* out = H_eff . psi  (D).  dist == NULL: psi, out are full [mL][d1][d2][mR].
+ * Sharded plan: psi is the FULL vector, out is this rank's shard [mL][d1][d2][nb].
+ * out must not alias psi.  Asynchronous on `stream`. */
+int heff_apply(heff_plan p, const double* psi, double* out, heff_stream stream);
+
+/* Same as heff_apply with HOST psi / out (pageable or pinned); copies in and out on
+ * `stream` and synchronises it.  The end-to-end entry point. */
+int heff_apply_host(heff_plan p, const double* psi_host, double* out_host, heff_stream stream);
+
+/* Lowest eigenpair of H_eff by Lanczos with full (CGS2) reorthogonalisation.
+ * psi: in = start vector, out = normalised Ritz vector (device; the local shard
+ * [mL][d1][d2][nb] on a communicating sharded plan, else the full vector).
+ * energy: lowest Ritz value; iters_done: matvecs performed; resid_est:
+ * beta_j |y_j[last]|.  Synchronous.  HEFF_EZERO if psi == 0. */
+int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts* opts, double* energy, int* iters_done,
+                   double* resid_est, heff_stream stream);
+
+int heff_destroy(heff_plan p);
+
+/* Thread-local message describing the last failure on this thread ("" if none). */
+const char* heff_last_error(void);
+
+/* Device bytes the plan allocates for matvec workspace (excluding the Lanczos basis). */
+size_t heff_workspace_bytes(const heff_dims* dims, const heff_dist* dist);
+
+/* Writes a fresh 128-byte ncclUniqueId (rank 0 calls this, then broadcasts it). */
+int heff_nccl_unique_id(unsigned char uid[128]);
+
+/* Tuning / test knobs.  HEFF_OPT_GEMM_PATH: 0 auto, 1 plain-load DMMA GEMM, 2 TMA DMMA GEMM.
+ * HEFF_OPT_LAST_KERNEL_COUNT (get only): kernels launched by the last heff_apply. */
+enum { HEFF_OPT_GEMM_PATH = 1, HEFF_OPT_LAST_KERNEL_COUNT = 2, HEFF_OPT_MPO_NNZ = 3 };
+int heff_set_option(heff_plan p, int option, int64_t value);
+int heff_get_option(heff_plan p, int option, int64_t* value);
+
+/* Timing of the dominant kernels inside the last heff_apply when enabled with
+ * HEFF_OPT_PROFILE (events recorded on the launch stream): ms for GEMM1, MPO, GEMM4. */
+enum { HEFF_OPT_PROFILE = 4 };
+int heff_last_timings(heff_plan p, float* ms_gemm_first, float* ms_mpo, float* ms_gemm_last, float* ms_other);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEFF_H */

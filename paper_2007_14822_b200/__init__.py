@@ -1,0 +1,8 @@
+"""B200-native two-site DMRG H_eff.psi matvec + Lanczos (arXiv 2007.14822 hot path).
+
+The compute lives in libheff.so (CUDA, sm_100a; C ABI in include/heff.h); `heff` is the
+ctypes binding.  See DESIGN.md.
+"""
+from .heff import Heff, HeffError, HeffZeroVector, LanczosResult, lib, nccl_unique_id, workspace_bytes  # noqa: F401
+
+__all__ = ["Heff", "HeffError", "HeffZeroVector", "LanczosResult", "lib", "nccl_unique_id", "workspace_bytes"]

@@ -1,0 +1,809 @@
+// heff_api.cu -- libheff: plans, the H_eff.psi matvec, and the Lanczos driver.
+// C ABI in include/heff.h (each entry point documents its arguments there).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/heff.h"
+#include "blas1.cuh"
+#include "gemm.cuh"
+#include "mpo.cuh"
+#include "tridiag.h"
+
+using namespace heff;
+
+// ----------------------------------------------------------------------------- errors
+static thread_local std::string g_err;
+
+static int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                                 \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess)                                                                       \
+      return set_err(e_ == cudaErrorMemoryAllocation ? HEFF_ENOMEM : HEFF_ECUDA, "%s: %s (%s:%d)", \
+                     #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+  } while (0)
+
+#define CKR(call)                 \
+  do {                            \
+    int r_ = (call);              \
+    if (r_ != HEFF_OK) return r_; \
+  } while (0)
+
+extern "C" const char* heff_last_error(void) { return g_err.c_str(); }
+
+// ----------------------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+      nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi g_nccl;
+
+static int nccl_load() {
+  if (g_nccl.loaded) return HEFF_OK;
+  const char* env = getenv("HEFF_NCCL_PATH");
+  void* h = nullptr;
+  if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);  // torch's copy, if loaded
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return set_err(HEFF_ENCCL, "cannot load libnccl.so.2: %s", dlerror());
+#define LD(name)                                                                   \
+  g_nccl.name = reinterpret_cast<decltype(g_nccl.name)>(dlsym(h, "nccl" #name));   \
+  if (!g_nccl.name) return set_err(HEFF_ENCCL, "libnccl lacks nccl%s", #name);
+  LD(GetUniqueId) LD(CommInitRank) LD(CommDestroy) LD(CommAbort) LD(AllReduce) LD(AllGather) LD(CommGetAsyncError)
+  LD(GetErrorString)
+#undef LD
+  g_nccl.loaded = true;
+  return HEFF_OK;
+}
+
+#define CKN(call)                                                                                     \
+  do {                                                                                                \
+    ncclResult_t r_ = (call);                                                                         \
+    if (r_ != ncclSuccess) return set_err(HEFF_ENCCL, "%s: %s", #call, g_nccl.GetErrorString(r_)); \
+  } while (0)
+
+extern "C" int heff_nccl_unique_id(unsigned char uid[128]) {
+  if (!uid) return set_err(HEFF_EINVAL, "uid is NULL");
+  CKR(nccl_load());
+  ncclUniqueId id;
+  CKN(g_nccl.GetUniqueId(&id));
+  memcpy(uid, id.internal, 128);
+  return HEFF_OK;
+}
+
+// ----------------------------------------------------------------------------- TMA maps
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major fp64 view: `rows` rows of `cols` elements, row pitch `ld` elements; box
+// {box_cols, box_rows}; 128-byte swizzle; OOB reads return zero.
+static int make_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                    int box_rows) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return set_err(HEFF_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(HEFF_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return HEFF_OK;
+}
+
+// ----------------------------------------------------------------------------- GEMM launch
+// Tile configuration of the TMA path.
+constexpr int kBM = 128, kBN = 128, kWM = 64, kWN = 32, kStages = 5, kGroupM = 16;
+using CfgNN = TmaGemmCfg<kBM, kBN, kWM, kWN, kStages, false>;
+using CfgNT = TmaGemmCfg<kBM, kBN, kWM, kWN, kStages, true>;
+
+struct GemmOp {
+  int64_t M = 0, N = 0, K = 0;
+  const double* A = nullptr;
+  int64_t lda = 0;
+  const double* B = nullptr;
+  int64_t ldb = 0;
+  bool b_kmajor = false;
+  double* C = nullptr;
+  int64_t ldc = 0;
+  // cached TMA maps (rebuilt when A/B pointers change)
+  CUtensorMap mapA, mapB;
+  const double* mapA_ptr = nullptr;
+  const double* mapB_ptr = nullptr;
+  int64_t mapA_rows = -1, mapB_rows = -1;
+};
+
+static int g_num_sms = 0;
+
+static bool tma_ok(const GemmOp& g) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return (g.lda % 2 == 0) && (g.ldb % 2 == 0) && al16(g.A) && al16(g.B) && g.M < (1ll << 31) && g.N < (1ll << 31) &&
+         g.K < (1ll << 31);
+}
+
+static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch) {
+  if (g.M == 0 || g.N == 0) return HEFF_OK;
+  const bool use_tma = (path == 2) || (path == 0 && tma_ok(g));
+  if (path == 2 && !tma_ok(g)) return set_err(HEFF_EUNSUPPORTED, "TMA GEMM path needs 16-byte rows/alignment");
+  if (use_tma) {
+    if (g.mapA_ptr != g.A || g.mapA_rows != g.M) {
+      CKR(make_map(&g.mapA, g.A, g.M, g.K, g.lda, kGemmBK, kBM));
+      g.mapA_ptr = g.A;
+      g.mapA_rows = g.M;
+    }
+    if (g.mapB_ptr != g.B || g.mapB_rows != g.N) {
+      if (g.b_kmajor)
+        CKR(make_map(&g.mapB, g.B, g.N, g.K, g.ldb, kGemmBK, kBN));
+      else
+        CKR(make_map(&g.mapB, g.B, g.K, g.N, g.ldb, 16, kGemmBK));
+      g.mapB_ptr = g.B;
+      g.mapB_rows = g.N;
+    }
+    const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + kBN - 1) / kBN);
+    const int grid = (int)std::min<int64_t>(tiles, g_num_sms);
+    const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(g.C) & 15) == 0) ? 1 : 0;
+    if (g.b_kmajor) {
+      auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, true>;
+      k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
+                                                          kGroupM, vec);
+    } else {
+      auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>;
+      k<<<grid, CfgNN::kThreads, CfgNN::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
+                                                          kGroupM, vec);
+    }
+  } else {
+    dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64));
+    if (grid.y > 65535) return set_err(HEFF_EUNSUPPORTED, "plain GEMM path: M too large");
+    if (g.b_kmajor)
+      gemm_dmma_plain_kernel<true><<<grid, 128, 0, s>>>(g.A, g.lda, g.B, g.ldb, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K);
+    else
+      gemm_dmma_plain_kernel<false><<<grid, 128, 0, s>>>(g.A, g.lda, g.B, g.ldb, g.C, g.ldc, (int)g.M, (int)g.N,
+                                                         (int)g.K);
+  }
+  CK(cudaGetLastError());
+  if (nlaunch) ++*nlaunch;
+  return HEFF_OK;
+}
+
+static int init_device_once() {
+  static bool done = false;
+  if (done) return HEFF_OK;
+  int dev;
+  CK(cudaGetDevice(&dev));
+  int major = 0, minor = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  if (major != 10 || minor != 0)
+    return set_err(HEFF_EUNSUPPORTED, "libheff is built for sm_100a (B200); device is sm_%d%d", major, minor);
+  CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaFuncSetAttribute(gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNT::kSmemBytes));
+  CK(cudaFuncSetAttribute(gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNN::kSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_orderA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(mpo_orderB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  done = true;
+  return HEFF_OK;
+}
+
+// ----------------------------------------------------------------------------- plan
+struct Csr {
+  int nrows = 0, nnz = 0;
+  int* d_rowptr = nullptr;
+  int* d_col = nullptr;
+  double* d_val = nullptr;
+};
+
+struct heff_plan_s {
+  heff_dims dims{};
+  const double *L = nullptr, *R = nullptr;  // borrowed
+  std::vector<double> W1h, W2h;             // host copies
+  bool sharded = false;                     // order B on a b'-shard
+  int nranks = 1, rank = 0;
+  int64_t b_lo = 0, b_hi = 0, nb = 0;
+  ncclComm_t comm = nullptr;
+  // order A workspace (chunked over a')
+  int64_t chunk_rows = 0;                   // a' rows per chunk
+  double *T1 = nullptr, *T3 = nullptr;
+  GemmOp g1, g4;                            // per-chunk ops (A/C pointers advanced per chunk)
+  // order B workspace
+  double *V1 = nullptr, *V3 = nullptr;
+  GemmOp gA, gD;
+  Csr csrA, csrB;
+  // e2e staging
+  double *stage_in = nullptr, *stage_out = nullptr;
+  // Lanczos
+  double* basis = nullptr;                  // [cap][ldv]
+  int basis_cap = 0;
+  int64_t ldv = 0;
+  double* work = nullptr;                   // w (local length)
+  double* full = nullptr;                   // gathered full psi (sharded + comm)
+  double* gather = nullptr;                 // blocked gather buffer
+  double* partial = nullptr;                // [(cap+1)][ldp]
+  int ldp = 0;
+  double* scal = nullptr;                   // c1[cap], c2[cap], alpha[cap], beta2/beta[cap], invb[cap], y[cap]
+  // options
+  int gemm_path = 0;
+  int last_launches = 0;
+  int profile = 0;
+  cudaEvent_t ev[8] = {};
+  float t_g1 = 0, t_mpo = 0, t_g4 = 0, t_other = 0;
+};
+
+static int build_csr(Csr& c, const std::vector<int>& rowptr, const std::vector<int>& col, const std::vector<double>& val) {
+  c.nrows = (int)rowptr.size() - 1;
+  c.nnz = (int)val.size();
+  CK(cudaMalloc(&c.d_rowptr, sizeof(int) * rowptr.size()));
+  CK(cudaMalloc(&c.d_col, sizeof(int) * std::max<size_t>(1, col.size())));
+  CK(cudaMalloc(&c.d_val, sizeof(double) * std::max<size_t>(1, val.size())));
+  CK(cudaMemcpy(c.d_rowptr, rowptr.data(), sizeof(int) * rowptr.size(), cudaMemcpyHostToDevice));
+  if (!col.empty()) {
+    CK(cudaMemcpy(c.d_col, col.data(), sizeof(int) * col.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c.d_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
+  }
+  return HEFF_OK;
+}
+
+// Two-site MPO Wc[w,s1',s1,s2',s2,w2] = sum_w1 W1[w,s1',s1,w1] W2[w1,s2',s2,w2], as CSR
+// in the (out-row, in-col) order each kernel wants.  Exact zeros are dropped.
+static int build_mpo_csr(heff_plan_s* p) {
+  const int64_t kL = p->dims.kL, kM = p->dims.kM, kR = p->dims.kR, d1 = p->dims.d1, d2 = p->dims.d2;
+  auto W1 = [&](int64_t w, int64_t s1p, int64_t s1, int64_t w1) { return p->W1h[((w * d1 + s1p) * d1 + s1) * kM + w1]; };
+  auto W2 = [&](int64_t w1, int64_t s2p, int64_t s2, int64_t w2) { return p->W2h[((w1 * d2 + s2p) * d2 + s2) * kR + w2]; };
+  auto Wc = [&](int64_t w, int64_t s1p, int64_t s1, int64_t s2p, int64_t s2, int64_t w2) {
+    double acc = 0.0;
+    for (int64_t w1 = 0; w1 < kM; ++w1) acc += W1(w, s1p, s1, w1) * W2(w1, s2p, s2, w2);
+    return acc;
+  };
+  std::vector<int> rp, cl;
+  std::vector<double> vl;
+  // order A: rows (s1',s2',w2), cols (w,s1,s2)
+  rp.push_back(0);
+  for (int64_t s1p = 0; s1p < d1; ++s1p)
+    for (int64_t s2p = 0; s2p < d2; ++s2p)
+      for (int64_t w2 = 0; w2 < kR; ++w2) {
+        for (int64_t w = 0; w < kL; ++w)
+          for (int64_t s1 = 0; s1 < d1; ++s1)
+            for (int64_t s2 = 0; s2 < d2; ++s2) {
+              const double v = Wc(w, s1p, s1, s2p, s2, w2);
+              if (v != 0.0) {
+                cl.push_back((int)((w * d1 + s1) * d2 + s2));
+                vl.push_back(v);
+              }
+            }
+        rp.push_back((int)vl.size());
+      }
+  CKR(build_csr(p->csrA, rp, cl, vl));
+  rp.clear(); cl.clear(); vl.clear();
+  // order B: rows (w,s1',s2'), cols (s1,s2,w2)
+  rp.push_back(0);
+  for (int64_t w = 0; w < kL; ++w)
+    for (int64_t s1p = 0; s1p < d1; ++s1p)
+      for (int64_t s2p = 0; s2p < d2; ++s2p) {
+        for (int64_t s1 = 0; s1 < d1; ++s1)
+          for (int64_t s2 = 0; s2 < d2; ++s2)
+            for (int64_t w2 = 0; w2 < kR; ++w2) {
+              const double v = Wc(w, s1p, s1, s2p, s2, w2);
+              if (v != 0.0) {
+                cl.push_back((int)((s1 * d2 + s2) * kR + w2));
+                vl.push_back(v);
+              }
+            }
+        rp.push_back((int)vl.size());
+      }
+  CKR(build_csr(p->csrB, rp, cl, vl));
+  return HEFF_OK;
+}
+
+static int64_t vec_len(const heff_plan_s* p) {  // local vector length
+  const heff_dims& d = p->dims;
+  return d.mL * d.d1 * d.d2 * (p->sharded ? p->nb : d.mR);
+}
+
+extern "C" size_t heff_workspace_bytes(const heff_dims* d, const heff_dist* dist) {
+  if (!d) return 0;
+  if (dist) {
+    const int64_t nb = dist->b_hi - dist->b_lo;
+    return sizeof(double) * (size_t)(d->mL * d->d1 * d->d2 * nb * d->kR + d->kL * d->mL * d->d1 * d->d2 * nb);
+  }
+  return sizeof(double) * (size_t)(d->mL * (d->kL + d->kR) * d->d1 * d->d2 * d->mR);
+}
+
+static void free_csr(Csr& c) {
+  cudaFree(c.d_rowptr);
+  cudaFree(c.d_col);
+  cudaFree(c.d_val);
+  c = Csr{};
+}
+
+extern "C" int heff_destroy(heff_plan p) {
+  if (!p) return HEFF_OK;
+  cudaFree(p->T1); cudaFree(p->T3); cudaFree(p->V1); cudaFree(p->V3);
+  cudaFree(p->stage_in); cudaFree(p->stage_out);
+  cudaFree(p->basis); cudaFree(p->work); cudaFree(p->full); cudaFree(p->gather);
+  cudaFree(p->partial); cudaFree(p->scal);
+  free_csr(p->csrA);
+  free_csr(p->csrB);
+  for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
+  if (p->comm && g_nccl.loaded) g_nccl.CommDestroy(p->comm);
+  delete p;
+  return HEFF_OK;
+}
+
+extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* L, const double* W1, const double* W2,
+                           const double* R, const heff_dist* dist, heff_stream stream) {
+  if (!out || !dims || !L || !W1 || !W2 || !R) return set_err(HEFF_EINVAL, "heff_create: null argument");
+  *out = nullptr;
+  const heff_dims d = *dims;
+  if (d.mL < 1 || d.mR < 1 || d.d1 < 1 || d.d2 < 1 || d.kL < 1 || d.kM < 1 || d.kR < 1)
+    return set_err(HEFF_EINVAL, "heff_create: every dimension must be >= 1");
+  if (d.kL * d.d1 * d.d2 > kMpoMaxRows || d.d1 * d.d2 * d.kR > kMpoMaxRows)
+    return set_err(HEFF_EUNSUPPORTED, "heff_create: k d1 d2 > %d exceeds the MPO kernel's shared-memory tile",
+                   kMpoMaxRows);
+  for (const void* ptr : {(const void*)L, (const void*)W1, (const void*)W2, (const void*)R})
+    if (reinterpret_cast<uintptr_t>(ptr) & 7) return set_err(HEFF_EINVAL, "heff_create: pointers must be 8-byte aligned");
+  CKR(init_device_once());
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+
+  heff_plan_s* p = new heff_plan_s();
+  p->dims = d;
+  p->L = L;
+  p->R = R;
+  auto fail = [&](int code) {
+    heff_destroy(p);
+    return code;
+  };
+  if (dist) {
+    if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks || dist->b_lo < 0 || dist->b_hi > d.mR ||
+        dist->b_lo >= dist->b_hi)
+      return fail(set_err(HEFF_EINVAL, "heff_create: bad heff_dist (rank %d/%d, b [%lld,%lld))", dist->rank,
+                          dist->nranks, (long long)dist->b_lo, (long long)dist->b_hi));
+    p->sharded = true;
+    p->nranks = dist->nranks;
+    p->rank = dist->rank;
+    p->b_lo = dist->b_lo;
+    p->b_hi = dist->b_hi;
+    p->nb = dist->b_hi - dist->b_lo;
+    if (dist->nccl_uid) {
+      if (d.mR % dist->nranks != 0 || p->nb != d.mR / dist->nranks || p->b_lo != p->rank * p->nb)
+        return fail(set_err(HEFF_EINVAL, "heff_create: communicating shards must be equal contiguous blocks of mR"));
+      int r = nccl_load();
+      if (r) return fail(r);
+      ncclUniqueId id;
+      memcpy(id.internal, dist->nccl_uid, 128);
+      ncclResult_t nr = g_nccl.CommInitRank(&p->comm, dist->nranks, id, dist->rank);
+      if (nr != ncclSuccess) return fail(set_err(HEFF_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(nr)));
+    }
+  }
+  // W copies
+  p->W1h.resize(d.kL * d.d1 * d.d1 * d.kM);
+  p->W2h.resize(d.kM * d.d2 * d.d2 * d.kR);
+  if (cudaMemcpyAsync(p->W1h.data(), W1, sizeof(double) * p->W1h.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(p->W2h.data(), W2, sizeof(double) * p->W2h.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return fail(set_err(HEFF_EINVAL, "heff_create: W1/W2 are not readable device pointers (%s)",
+                        cudaGetErrorString(cudaGetLastError())));
+  int r = build_mpo_csr(p);
+  if (r) return fail(r);
+
+  if (!p->sharded) {
+    // order A, chunked over a' so that T1 + T3 fit the workspace budget
+    const int64_t per_row = (d.kL + d.kR) * d.d1 * d.d2 * d.mR * 8;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return fail(set_err(HEFF_ECUDA, "cudaMemGetInfo failed"));
+    int64_t budget = (int64_t)(0.45 * (double)free_b);
+    if (const char* e = getenv("HEFF_WORKSPACE_MB")) budget = std::atoll(e) * (1ll << 20);
+    int64_t rows = std::max<int64_t>(1, std::min<int64_t>(d.mL, budget / per_row));
+    // keep chunks balanced
+    const int64_t nchunks = (d.mL + rows - 1) / rows;
+    rows = (d.mL + nchunks - 1) / nchunks;
+    p->chunk_rows = rows;
+    if (cudaMalloc(&p->T1, sizeof(double) * rows * d.kL * d.d1 * d.d2 * d.mR) != cudaSuccess ||
+        cudaMalloc(&p->T3, sizeof(double) * rows * d.d1 * d.d2 * d.kR * d.mR) != cudaSuccess)
+      return fail(set_err(HEFF_ENOMEM, "heff_create: cannot allocate T1/T3 workspace (%lld a' rows)", (long long)rows));
+    // GEMM1: T1[(a' w), (s1 s2 b)] = L[(a' w), a] . psi[a, (s1 s2 b)]   (NN)
+    p->g1.N = d.d1 * d.d2 * d.mR;
+    p->g1.K = d.mL;
+    p->g1.lda = d.mL;
+    p->g1.ldb = d.d1 * d.d2 * d.mR;
+    p->g1.b_kmajor = false;
+    p->g1.ldc = d.d1 * d.d2 * d.mR;
+    // GEMM4: out[(a' s1' s2'), b'] = T3[(a' s1' s2'), (w2 b)] . R[b', (w2 b)]^T   (NT)
+    p->g4.N = d.mR;
+    p->g4.K = d.kR * d.mR;
+    p->g4.lda = d.kR * d.mR;
+    p->g4.B = R;
+    p->g4.ldb = d.kR * d.mR;
+    p->g4.b_kmajor = true;
+    p->g4.ldc = d.mR;
+  } else {
+    const int64_t nb = p->nb;
+    if (cudaMalloc(&p->V1, sizeof(double) * d.mL * d.d1 * d.d2 * nb * d.kR) != cudaSuccess ||
+        cudaMalloc(&p->V3, sizeof(double) * d.kL * d.mL * d.d1 * d.d2 * nb) != cudaSuccess)
+      return fail(set_err(HEFF_ENOMEM, "heff_create: cannot allocate V1/V3 workspace"));
+    // GEMM_A: V1[(a s1 s2), (b' w2)] = psi[(a s1 s2), b] . R_g[(b' w2), b]^T   (NT)
+    p->gA.M = d.mL * d.d1 * d.d2;
+    p->gA.N = nb * d.kR;
+    p->gA.K = d.mR;
+    p->gA.lda = d.mR;
+    p->gA.B = R;
+    p->gA.ldb = d.mR;
+    p->gA.b_kmajor = true;
+    p->gA.C = p->V1;
+    p->gA.ldc = nb * d.kR;
+    // GEMM_D: out_g[a', (s1' s2' b')] = L[a', (w a)] . V3[(w a), (s1' s2' b')]   (NN)
+    p->gD.M = d.mL;
+    p->gD.N = d.d1 * d.d2 * nb;
+    p->gD.K = d.kL * d.mL;
+    p->gD.A = L;
+    p->gD.lda = d.kL * d.mL;
+    p->gD.B = p->V3;
+    p->gD.ldb = d.d1 * d.d2 * nb;
+    p->gD.b_kmajor = false;
+    p->gD.ldc = d.d1 * d.d2 * nb;
+  }
+  *out = p;
+  return HEFF_OK;
+}
+
+extern "C" int heff_set_option(heff_plan p, int option, int64_t value) {
+  if (!p) return set_err(HEFF_EINVAL, "null plan");
+  switch (option) {
+    case HEFF_OPT_GEMM_PATH:
+      if (value < 0 || value > 2) return set_err(HEFF_EINVAL, "gemm path must be 0, 1 or 2");
+      p->gemm_path = (int)value;
+      return HEFF_OK;
+    case HEFF_OPT_PROFILE:
+      p->profile = value ? 1 : 0;
+      if (p->profile && !p->ev[0])
+        for (auto& e : p->ev) CK(cudaEventCreate(&e));
+      return HEFF_OK;
+    default:
+      return set_err(HEFF_EINVAL, "unknown option %d", option);
+  }
+}
+
+extern "C" int heff_get_option(heff_plan p, int option, int64_t* value) {
+  if (!p || !value) return set_err(HEFF_EINVAL, "null argument");
+  switch (option) {
+    case HEFF_OPT_GEMM_PATH: *value = p->gemm_path; return HEFF_OK;
+    case HEFF_OPT_LAST_KERNEL_COUNT: *value = p->last_launches; return HEFF_OK;
+    case HEFF_OPT_MPO_NNZ: *value = p->sharded ? p->csrB.nnz : p->csrA.nnz; return HEFF_OK;
+    case HEFF_OPT_PROFILE: *value = p->profile; return HEFF_OK;
+    default: return set_err(HEFF_EINVAL, "unknown option %d", option);
+  }
+}
+
+extern "C" int heff_last_timings(heff_plan p, float* g1, float* mpo, float* g4, float* other) {
+  if (!p) return set_err(HEFF_EINVAL, "null plan");
+  if (g1) *g1 = p->t_g1;
+  if (mpo) *mpo = p->t_mpo;
+  if (g4) *g4 = p->t_g4;
+  if (other) *other = p->t_other;
+  return HEFF_OK;
+}
+
+// --------------------------------------------------------------------------- the matvec
+static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl) {
+  const heff_dims& d = p->dims;
+  const int64_t nin = d.kL * d.d1 * d.d2, nout = d.d1 * d.d2 * d.kR;
+  const size_t mpo_smem = sizeof(double) * nin * kMpoCols;
+  for (int64_t a0 = 0; a0 < d.mL; a0 += p->chunk_rows) {
+    const int64_t rows = std::min(p->chunk_rows, d.mL - a0);
+    if (p->profile) CK(cudaEventRecord(p->ev[0], s));
+    p->g1.M = rows * d.kL;
+    p->g1.A = p->L + a0 * d.kL * d.mL;
+    p->g1.B = psi;
+    p->g1.C = p->T1;
+    CKR(launch_gemm(p->g1, p->gemm_path, s, nl));
+    if (p->profile) CK(cudaEventRecord(p->ev[1], s));
+    dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
+    mpo_orderA_kernel<<<grid, kMpoCols, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
+                                                       p->csrA.d_col, p->csrA.d_val);
+    CK(cudaGetLastError());
+    ++*nl;
+    if (p->profile) CK(cudaEventRecord(p->ev[2], s));
+    p->g4.M = rows * d.d1 * d.d2;
+    p->g4.A = p->T3;
+    p->g4.C = out + a0 * d.d1 * d.d2 * d.mR;
+    CKR(launch_gemm(p->g4, p->gemm_path, s, nl));
+    if (p->profile) {
+      CK(cudaEventRecord(p->ev[3], s));
+      CK(cudaEventSynchronize(p->ev[3]));
+      float x;
+      CK(cudaEventElapsedTime(&x, p->ev[0], p->ev[1])); p->t_g1 += x;
+      CK(cudaEventElapsedTime(&x, p->ev[1], p->ev[2])); p->t_mpo += x;
+      CK(cudaEventElapsedTime(&x, p->ev[2], p->ev[3])); p->t_g4 += x;
+    }
+  }
+  return HEFF_OK;
+}
+
+static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl) {
+  const heff_dims& d = p->dims;
+  const int dd = (int)(d.d1 * d.d2);
+  const size_t mpo_smem = sizeof(double) * dd * d.kR * kMpoCols;
+  if (p->profile) CK(cudaEventRecord(p->ev[0], s));
+  p->gA.A = psi;
+  CKR(launch_gemm(p->gA, p->gemm_path, s, nl));
+  if (p->profile) CK(cudaEventRecord(p->ev[1], s));
+  dim3 grid((unsigned)((p->nb + kMpoCols - 1) / kMpoCols), (unsigned)d.mL);
+  mpo_orderB_kernel<<<grid, kMpoCols, mpo_smem, s>>>(p->V1, p->V3, d.mL, p->nb, dd, (int)d.kR, (int)d.kL,
+                                                     p->csrB.d_rowptr, p->csrB.d_col, p->csrB.d_val);
+  CK(cudaGetLastError());
+  ++*nl;
+  if (p->profile) CK(cudaEventRecord(p->ev[2], s));
+  p->gD.C = out;
+  CKR(launch_gemm(p->gD, p->gemm_path, s, nl));
+  if (p->profile) {
+    CK(cudaEventRecord(p->ev[3], s));
+    CK(cudaEventSynchronize(p->ev[3]));
+    float x;
+    CK(cudaEventElapsedTime(&x, p->ev[0], p->ev[1])); p->t_g1 += x;
+    CK(cudaEventElapsedTime(&x, p->ev[1], p->ev[2])); p->t_mpo += x;
+    CK(cudaEventElapsedTime(&x, p->ev[2], p->ev[3])); p->t_g4 += x;
+  }
+  return HEFF_OK;
+}
+
+static int apply_impl(heff_plan_s* p, const double* psi, double* out, cudaStream_t s) {
+  if (!psi || !out) return set_err(HEFF_EINVAL, "heff_apply: null psi/out");
+  if (psi == out) return set_err(HEFF_EINVAL, "heff_apply: out must not alias psi");
+  if ((reinterpret_cast<uintptr_t>(psi) | reinterpret_cast<uintptr_t>(out)) & 7)
+    return set_err(HEFF_EINVAL, "heff_apply: psi/out must be 8-byte aligned");
+  int nl = 0;
+  p->t_g1 = p->t_mpo = p->t_g4 = p->t_other = 0.f;
+  int r = p->sharded ? apply_orderB(p, psi, out, s, &nl) : apply_orderA(p, psi, out, s, &nl);
+  p->last_launches = nl;
+  return r;
+}
+
+extern "C" int heff_apply(heff_plan p, const double* psi, double* out, heff_stream stream) {
+  if (!p) return set_err(HEFF_EINVAL, "heff_apply: null plan");
+  return apply_impl(p, psi, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_host, heff_stream stream) {
+  if (!p || !psi_host || !out_host) return set_err(HEFF_EINVAL, "heff_apply_host: null argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const heff_dims& d = p->dims;
+  const int64_t n_in = d.mL * d.d1 * d.d2 * d.mR;
+  const int64_t n_out = vec_len(p);
+  if (!p->stage_in) {
+    CK(cudaMalloc(&p->stage_in, sizeof(double) * n_in));
+    CK(cudaMalloc(&p->stage_out, sizeof(double) * n_out));
+  }
+  CK(cudaMemcpyAsync(p->stage_in, psi_host, sizeof(double) * n_in, cudaMemcpyHostToDevice, s));
+  CKR(apply_impl(p, p->stage_in, p->stage_out, s));
+  CK(cudaMemcpyAsync(out_host, p->stage_out, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return HEFF_OK;
+}
+
+// --------------------------------------------------------------------------- Lanczos
+static int reduce_grid(int64_t n) {
+  const int64_t per = (int64_t)kRedThreads * 2 * 8;  // >= 8 pairs per thread
+  return (int)std::max<int64_t>(1, std::min<int64_t>(4 * (int64_t)g_num_sms, (n + per - 1) / per));
+}
+
+static int ew_grid(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(8 * (int64_t)g_num_sms, (n / 2 + 255) / 256));
+}
+
+// c[0..nq) = V[0..nq)^T w  (local sums; allreduced across ranks when communicating)
+static int multidot(heff_plan_s* p, const double* V, int nq, const double* w, int64_t n, double* c, cudaStream_t s) {
+  const int G = p->ldp;
+  for (int q0 = 0; q0 < nq; q0 += kDotQ) {
+    const int qn = std::min(kDotQ, nq - q0);
+    multidot_partial_kernel<<<G, kRedThreads, 0, s>>>(V + q0 * p->ldv, p->ldv, qn, w, n, p->partial + q0 * G, G);
+  }
+  reduce_partial_kernel<<<nq, kRedThreads, 0, s>>>(p->partial, G, G, c, 0, nullptr);
+  CK(cudaGetLastError());
+  if (p->comm) CKN(g_nccl.AllReduce(c, c, nq, ncclFloat64, ncclSum, p->comm, s));
+  return HEFF_OK;
+}
+
+static int multiaxpy(heff_plan_s* p, const double* V, int nq, const double* c, double sign, double* w, int64_t n,
+                     cudaStream_t s) {
+  for (int q0 = 0; q0 < nq; q0 += 64) {
+    const int qn = std::min(64, nq - q0);
+    multiaxpy_kernel<<<ew_grid(n), 256, 0, s>>>(V + q0 * p->ldv, p->ldv, qn, c + q0, sign, w, n);
+  }
+  CK(cudaGetLastError());
+  return HEFF_OK;
+}
+
+__global__ void sqrt_inv_kernel(double* x, double* inv) {
+  const double v = sqrt(*x);
+  *x = v;
+  *inv = v > 0.0 ? 1.0 / v : 0.0;
+}
+
+// ||w|| -> *nrm, 1/||w|| -> *inv (global over ranks)
+static int norm2(heff_plan_s* p, const double* w, int64_t n, double* nrm, double* inv, cudaStream_t s) {
+  const int G = p->ldp;
+  multidot_partial_kernel<<<G, kRedThreads, 0, s>>>(w, 0, 1, w, n, p->partial, G);
+  reduce_partial_kernel<<<1, kRedThreads, 0, s>>>(p->partial, G, G, nrm, p->comm ? 0 : 1, inv);
+  CK(cudaGetLastError());
+  if (p->comm) {
+    CKN(g_nccl.AllReduce(nrm, nrm, 1, ncclFloat64, ncclSum, p->comm, s));
+    sqrt_inv_kernel<<<1, 1, 0, s>>>(nrm, inv);
+    CK(cudaGetLastError());
+  }
+  return HEFF_OK;
+}
+
+// full-psi input for the matvec: all-gather the shard (communicating plans) or use v as is
+static int matvec_local(heff_plan_s* p, const double* v, double* w, cudaStream_t s) {
+  if (!p->sharded) return apply_impl(p, v, w, s);
+  if (!p->comm) return set_err(HEFF_EUNSUPPORTED, "lanczos_ground on a virtual shard (no communicator)");
+  const heff_dims& d = p->dims;
+  const int64_t rows = d.mL * d.d1 * d.d2;
+  const int64_t nloc = rows * p->nb;
+  if (p->nranks == 1) {
+    CK(cudaMemcpyAsync(p->full, v, sizeof(double) * nloc, cudaMemcpyDeviceToDevice, s));
+  } else {
+    CKN(g_nccl.AllGather(v, p->gather, nloc, ncclFloat64, p->comm, s));
+    relayout_blocked_kernel<<<ew_grid(rows * d.mR), 256, 0, s>>>(p->gather, p->full, rows, p->nb, p->nranks);
+    CK(cudaGetLastError());
+  }
+  return apply_impl(p, p->full, w, s);
+}
+
+extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts* o, double* energy, int* iters_done,
+                              double* resid_est, heff_stream stream) {
+  if (!p || !psi || !o || !energy) return set_err(HEFF_EINVAL, "lanczos_ground: null argument");
+  if (o->max_iter < 1 || o->max_iter > 100000) return set_err(HEFF_EINVAL, "lanczos_ground: max_iter out of range");
+  if (o->mode != 0 && o->mode != 1) return set_err(HEFF_EINVAL, "lanczos_ground: mode must be 0 or 1");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int cap = o->max_iter;
+  const int64_t n = vec_len(p);
+  const int64_t ldv = (n + 31) / 32 * 32;
+  // (re)allocate the Krylov basis and scratch
+  if (p->basis_cap < cap || p->ldv != ldv) {
+    cudaFree(p->basis); cudaFree(p->partial); cudaFree(p->scal);
+    p->basis = nullptr; p->partial = nullptr; p->scal = nullptr;
+    p->basis_cap = 0;
+    CK(cudaMalloc(&p->basis, sizeof(double) * ldv * cap));
+    p->ldp = reduce_grid(n);
+    CK(cudaMalloc(&p->partial, sizeof(double) * (size_t)(cap + kDotQ) * p->ldp));
+    CK(cudaMalloc(&p->scal, sizeof(double) * 6 * (size_t)(cap + 1)));
+    p->basis_cap = cap;
+    p->ldv = ldv;
+  }
+  if (!p->work) CK(cudaMalloc(&p->work, sizeof(double) * ldv));
+  if (p->sharded && p->comm && !p->full) {
+    const heff_dims& d = p->dims;
+    CK(cudaMalloc(&p->full, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
+    if (p->nranks > 1) CK(cudaMalloc(&p->gather, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
+  }
+  double* c1 = p->scal;
+  double* c2 = c1 + (cap + 1);
+  double* alpha = c2 + (cap + 1);
+  double* beta = alpha + (cap + 1);
+  double* invb = beta + (cap + 1);
+  double* ydev = invb + (cap + 1);
+  double* V = p->basis;
+  double* w = p->work;
+
+  // v1 = x0 / ||x0||  (copied into the aligned basis first)
+  CK(cudaMemcpyAsync(V, psi, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  CKR(norm2(p, V, n, beta + cap, invb + cap, s));
+  double h_nrm = 0.0;
+  CK(cudaMemcpyAsync(&h_nrm, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (!(h_nrm > 0.0)) return set_err(HEFF_EZERO, "lanczos_ground: zero start vector");
+  scale_kernel<<<ew_grid(n), 256, 0, s>>>(V, invb + cap, V, n);
+  CK(cudaGetLastError());
+
+  std::vector<double> ha(cap), hb(cap);
+  double theta = 0.0, ylast = 0.0, hnorm = 0.0;
+  int j_done = 0;
+  auto step = [&](int j) -> int {  // j = 1-based step: v_j = V[j-1]
+    double* vj = V + (int64_t)(j - 1) * ldv;
+    CKR(matvec_local(p, vj, w, s));
+    CKR(multidot(p, V, j, w, n, c1, s));
+    CKR(multiaxpy(p, V, j, c1, -1.0, w, n, s));
+    CKR(multidot(p, V, j, w, n, c2, s));
+    CKR(multiaxpy(p, V, j, c2, -1.0, w, n, s));
+    lanczos_alpha_kernel<<<1, 1, 0, s>>>(c1, c2, j - 1, alpha);
+    CKR(norm2(p, w, n, beta + (j - 1), invb + (j - 1), s));
+    if (j < cap) scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + (j - 1), V + (int64_t)j * ldv, n);
+    CK(cudaGetLastError());
+    return HEFF_OK;
+  };
+  // scalar bookkeeping on the host: returns true to stop after step j
+  auto host_check = [&](int j) -> bool {
+    for (int i = 0; i < j; ++i) {
+      const double gsh = std::fabs(ha[i]) + (i > 0 ? hb[i - 1] : 0.0) + hb[i];
+      hnorm = std::max(hnorm, gsh);
+    }
+    tridiag_lowest_last(j, ha.data(), hb.data(), &theta, &ylast);
+    if (o->theta_out) o->theta_out[j - 1] = theta;
+    if (hb[j - 1] <= 1e-12 * hnorm) return true;  // breakdown: invariant subspace
+    if (o->mode == 1 && hb[j - 1] * std::fabs(ylast) <= o->tol * hnorm) return true;
+    return j == cap;
+  };
+
+  if (o->mode == 0) {
+    // fixed steps: enqueue everything, read the scalars once, truncate at a breakdown
+    for (int j = 1; j <= cap; ++j) CKR(step(j));
+    CK(cudaMemcpyAsync(ha.data(), alpha, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hb.data(), beta, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int j = 1; j <= cap; ++j) {
+      j_done = j;
+      if (host_check(j)) break;
+    }
+  } else {
+    for (int j = 1; j <= cap; ++j) {
+      CKR(step(j));
+      CK(cudaMemcpyAsync(&ha[j - 1], alpha + (j - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(&hb[j - 1], beta + (j - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      j_done = j;
+      if (host_check(j)) break;
+    }
+  }
+  if (o->alpha_out) memcpy(o->alpha_out, ha.data(), sizeof(double) * j_done);
+  if (o->beta_out) memcpy(o->beta_out, hb.data(), sizeof(double) * j_done);
+  // Ritz vector x = V y / ||V y||
+  std::vector<double> y(j_done);
+  if (!tridiag_lowest_vec(j_done, ha.data(), hb.data(), &theta, y.data()))
+    return set_err(HEFF_ECUDA, "lanczos_ground: tridiagonal QL did not converge");
+  CK(cudaMemcpyAsync(ydev, y.data(), sizeof(double) * j_done, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(w, 0, sizeof(double) * n, s));
+  CKR(multiaxpy(p, V, j_done, ydev, 1.0, w, n, s));
+  CKR(norm2(p, w, n, beta + cap, invb + cap, s));
+  scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + cap, psi, n);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  *energy = theta;
+  if (iters_done) *iters_done = j_done;
+  if (resid_est) *resid_est = hb[j_done - 1] * std::fabs(y[j_done - 1]);
+  return HEFF_OK;
+}

@@ -1,0 +1,89 @@
+// mpo.cuh -- the two small O(m^2 d^3 k^2) MPO steps of H_eff.psi, fused into one
+// HBM-streaming kernel per order.
+//
+// Both MPO steps are applied at once through the two-site MPO
+//   Wc[w,s1',s1,s2',s2,w2] = sum_w1 W1[w,s1',s1,w1] W2[w1,s2',s2,w2]
+// held as a CSR list of its nonzeros (built once per plan on the host).  Order A maps,
+// for every (a', b):   T3[a',s1',s2',w2,b] = sum Wc . T1[a',w,s1,s2,b]
+// and order B maps, for every (a, b'):  V3[w,a,s1',s2',b'] = sum Wc . V1[a,s1,s2,b',w2].
+// (Re-association of steps 2+3 of (D) in heff.h; exact up to rounding order.)
+// Each block stages the k d^2 input column block of its (row, 128-column) tile in shared
+// memory with coalesced loads, then writes every output row coalesced: one HBM read of
+// the input and one write of the output, no intermediate T2.
+#pragma once
+#include <cstdint>
+
+namespace heff {
+
+constexpr int kMpoCols = 128;     // b (or b') columns per block = threads per block
+constexpr int kMpoMaxRows = 200;  // k d1 d2 rows staged in shared memory (<= 200 KB)
+
+// Order A.  T1: [mL][nin][mR] with nin = kL d1 d2 (rows (w,s1,s2));
+//           T3: [mL][nout][mR] with nout = d1 d2 kR (rows (s1',s2',w2)).
+__global__ void __launch_bounds__(kMpoCols) mpo_orderA_kernel(const double* __restrict__ T1, double* __restrict__ T3,
+                                                              int64_t mR, int nin, int nout,
+                                                              const int* __restrict__ rowptr,
+                                                              const int* __restrict__ col,
+                                                              const double* __restrict__ val) {
+  extern __shared__ double s_in[];  // [nin][kMpoCols]
+  const int64_t ap = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * kMpoCols + threadIdx.x;
+  const bool ok = b < mR;
+  const double* in = T1 + ap * nin * mR;
+  double* out = T3 + ap * nout * mR;
+  for (int r = 0; r < nin; ++r) s_in[r * kMpoCols + threadIdx.x] = ok ? __ldcs(in + r * mR + b) : 0.0;
+  __syncthreads();
+  if (!ok) return;
+  for (int o = 0; o < nout; ++o) {
+    double acc = 0.0;
+    const int e1 = __ldg(rowptr + o + 1);
+    for (int e = __ldg(rowptr + o); e < e1; ++e) acc = fma(__ldg(val + e), s_in[__ldg(col + e) * kMpoCols + threadIdx.x], acc);
+    __stcs(out + o * mR + b, acc);
+  }
+}
+
+// Order B on a b'-shard of width nb.  V1: [mL][d1 d2][nb][kR]; V3: [kL][mL][d1 d2][nb].
+// CSR rows o = (w,s1',s2') (nout = kL d1 d2), columns c = (s1,s2,w2) (nin = d1 d2 kR).
+__global__ void __launch_bounds__(kMpoCols) mpo_orderB_kernel(const double* __restrict__ V1, double* __restrict__ V3,
+                                                              int64_t mL, int64_t nb, int dd, int kR, int kL,
+                                                              const int* __restrict__ rowptr,
+                                                              const int* __restrict__ col,
+                                                              const double* __restrict__ val) {
+  extern __shared__ double s_in[];  // [(s1 s2) kR + w2][kMpoCols]
+  const int64_t a = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * kMpoCols;
+  const int64_t width = min((int64_t)kMpoCols, nb - b0);
+  for (int s = 0; s < dd; ++s) {
+    const double* src = V1 + ((a * dd + s) * nb + b0) * kR;  // contiguous [width][kR]
+    for (int e = threadIdx.x; e < kMpoCols * kR; e += kMpoCols) {
+      const int bl = e / kR, w2 = e - bl * kR;
+      s_in[(s * kR + w2) * kMpoCols + bl] = (bl < width) ? __ldcs(src + e) : 0.0;
+    }
+  }
+  __syncthreads();
+  const int bl = threadIdx.x;
+  if (bl >= width) return;
+  const int nout = kL * dd;
+  for (int o = 0; o < nout; ++o) {
+    double acc = 0.0;
+    const int e1 = __ldg(rowptr + o + 1);
+    for (int e = __ldg(rowptr + o); e < e1; ++e) acc = fma(__ldg(val + e), s_in[__ldg(col + e) * kMpoCols + bl], acc);
+    const int w = o / dd, s = o - w * dd;
+    __stcs(V3 + ((w * mL + a) * dd + s) * nb + b0 + bl, acc);
+  }
+}
+
+// Blocked-b gather layout [P][mL d1 d2][nb] -> natural [mL d1 d2][P nb] (after an
+// all-gather of shards).  One thread per element, coalesced on the write side.
+__global__ void relayout_blocked_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t rows,
+                                        int64_t nb, int P) {
+  const int64_t n = rows * nb * P;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / (nb * P);
+    const int64_t rem = i - row * nb * P;
+    const int64_t g = rem / nb, bl = rem - g * nb;
+    dst[i] = src[(g * rows + row) * nb + bl];
+  }
+}
+
+}  // namespace heff

@@ -1,0 +1,231 @@
+"""Thin ctypes binding of libheff (include/heff.h) -- argument marshalling only.
+
+Every step of H_eff.psi and of the Lanczos solver runs in libheff's CUDA kernels; this
+module passes torch device pointers, the current CUDA stream and plain sizes across the
+C ABI.  There is no CPU fallback: if libheff.so is missing or the device is not a B200
+(sm_100a) the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from pathlib import Path
+
+import torch
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libheff.so"
+
+HEFF_OK, HEFF_EINVAL, HEFF_ENOMEM, HEFF_ECUDA, HEFF_ENCCL, HEFF_EZERO, HEFF_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+OPT_GEMM_PATH, OPT_LAST_KERNEL_COUNT, OPT_MPO_NNZ, OPT_PROFILE = 1, 2, 3, 4
+
+
+class HeffError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libheff error {code}: {msg}")
+        self.code = code
+
+
+class HeffZeroVector(HeffError, ValueError):
+    pass
+
+
+class _Dims(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("mL", "d1", "d2", "mR", "kL", "kM", "kR")]
+
+
+class _Dist(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_uid", ctypes.c_void_p),
+                ("b_lo", ctypes.c_int64), ("b_hi", ctypes.c_int64)]
+
+
+class _LanczosOpts(ctypes.Structure):
+    _fields_ = [("max_iter", ctypes.c_int), ("mode", ctypes.c_int), ("tol", ctypes.c_double),
+                ("alpha_out", ctypes.c_void_p), ("beta_out", ctypes.c_void_p), ("theta_out", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libheff.so (built by __graft_entry__.build() / paper_2007_14822_b200/build.py)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(str(LIB_PATH))
+        vp, i64, ip = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.heff_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(_Dims), vp, vp, vp, vp, ctypes.POINTER(_Dist), vp]
+        L.heff_apply.argtypes = [vp, vp, vp, vp]
+        L.heff_apply_host.argtypes = [vp, vp, vp, vp]
+        L.lanczos_ground.argtypes = [vp, vp, ctypes.POINTER(_LanczosOpts), ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ip), ctypes.POINTER(ctypes.c_double), vp]
+        L.heff_destroy.argtypes = [vp]
+        L.heff_last_error.restype = ctypes.c_char_p
+        L.heff_workspace_bytes.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(_Dist)]
+        L.heff_workspace_bytes.restype = ctypes.c_size_t
+        L.heff_nccl_unique_id.argtypes = [ctypes.c_char_p]
+        L.heff_set_option.argtypes = [vp, ip, i64]
+        L.heff_get_option.argtypes = [vp, ip, ctypes.POINTER(i64)]
+        L.heff_last_timings.argtypes = [vp] + [ctypes.POINTER(ctypes.c_float)] * 4
+        for f in ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
+                  "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings"):
+            getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy", "heff_last_error",
+            "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings")
+
+
+def _check(rc: int):
+    if rc != HEFF_OK:
+        msg = lib().heff_last_error().decode(errors="replace")
+        if rc == HEFF_EZERO:
+            raise HeffZeroVector(rc, msg)
+        raise HeffError(rc, msg)
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+    return t
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().heff_nccl_unique_id(buf))
+    return buf.raw
+
+
+@dataclass
+class LanczosResult:
+    energy: float
+    iters: int
+    resid: float
+    alpha: list
+    beta: list
+    thetas: list
+
+
+class Heff:
+    """A libheff plan: H_eff for fixed (L, W1, W2, R).
+
+    dist = None: single GPU, order A.  dist = dict(nranks, rank, b_lo, b_hi, uid=None|bytes):
+    this rank's b'-shard (order B); R must then hold only rows [b_lo, b_hi).
+    The tensors are borrowed: keep them alive and unmodified while the plan lives.
+    """
+
+    def __init__(self, L, W1, W2, R, dist: dict | None = None, stream=None):
+        for t, n in ((L, "L"), (W1, "W1"), (W2, "W2"), (R, "R")):
+            _dev(t, n)
+        mL, kL, _ = L.shape
+        _, d1, _, kM = W1.shape
+        _, d2, _, kR = W2.shape
+        mR = R.shape[2]
+        self.dims = dict(mL=mL, d1=d1, d2=d2, mR=mR, kL=kL, kM=kM, kR=kR)
+        self._keep = (L, W1, W2, R)
+        self._cdims = _Dims(mL, d1, d2, mR, kL, kM, kR)
+        self.dist = dist
+        pdist = None
+        self._uid = None
+        if dist is not None:
+            uid = dist.get("uid")
+            self._uid = ctypes.create_string_buffer(uid, 128) if uid is not None else None
+            self._cdist = _Dist(dist["nranks"], dist["rank"],
+                                ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None,
+                                dist["b_lo"], dist["b_hi"])
+            pdist = ctypes.byref(self._cdist)
+            self.nb = dist["b_hi"] - dist["b_lo"]
+        else:
+            self.nb = mR
+        h = ctypes.c_void_p()
+        _check(lib().heff_create(ctypes.byref(h), ctypes.byref(self._cdims), L.data_ptr(), W1.data_ptr(),
+                                 W2.data_ptr(), R.data_ptr(), pdist, _stream(stream)))
+        self._h = h
+
+    # -- shapes
+    @property
+    def psi_shape(self):
+        d = self.dims
+        return (d["mL"], d["d1"], d["d2"], d["mR"])
+
+    @property
+    def out_shape(self):
+        d = self.dims
+        return (d["mL"], d["d1"], d["d2"], self.nb)
+
+    def apply(self, psi: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        _dev(psi, "psi")
+        if out is None:
+            out = torch.empty(self.out_shape, dtype=torch.float64, device=psi.device)
+        _dev(out, "out")
+        _check(lib().heff_apply(self._h, psi.data_ptr(), out.data_ptr(), _stream(stream)))
+        return out
+
+    def apply_host(self, psi_host: torch.Tensor, out_host: torch.Tensor, stream=None) -> torch.Tensor:
+        """End-to-end entry: host buffers in and out (copies happen inside libheff)."""
+        assert psi_host.device.type == "cpu" and out_host.device.type == "cpu"
+        assert psi_host.dtype == torch.float64 and out_host.dtype == torch.float64
+        assert psi_host.is_contiguous() and out_host.is_contiguous()
+        _check(lib().heff_apply_host(self._h, psi_host.data_ptr(), out_host.data_ptr(), _stream(stream)))
+        return out_host
+
+    def lanczos_ground(self, psi: torch.Tensor, max_iter: int, tol: float = 0.0, converge: bool = False,
+                       stream=None) -> LanczosResult:
+        """psi: start vector (overwritten with the normalised Ritz vector)."""
+        _dev(psi, "psi")
+        a = (ctypes.c_double * max_iter)()
+        b = (ctypes.c_double * max_iter)()
+        th = (ctypes.c_double * max_iter)()
+        o = _LanczosOpts(max_iter, 1 if converge else 0, tol, ctypes.cast(a, ctypes.c_void_p),
+                         ctypes.cast(b, ctypes.c_void_p), ctypes.cast(th, ctypes.c_void_p))
+        e, it, r = ctypes.c_double(), ctypes.c_int(), ctypes.c_double()
+        _check(lib().lanczos_ground(self._h, psi.data_ptr(), ctypes.byref(o), ctypes.byref(e), ctypes.byref(it),
+                                    ctypes.byref(r), _stream(stream)))
+        j = it.value
+        return LanczosResult(e.value, j, r.value, list(a[:j]), list(b[:j]), list(th[:j]))
+
+    def set_option(self, opt: int, value: int):
+        _check(lib().heff_set_option(self._h, opt, int(value)))
+
+    def get_option(self, opt: int) -> int:
+        v = ctypes.c_int64()
+        _check(lib().heff_get_option(self._h, opt, ctypes.byref(v)))
+        return v.value
+
+    def last_timings(self):
+        f = [ctypes.c_float() for _ in range(4)]
+        _check(lib().heff_last_timings(self._h, *[ctypes.byref(x) for x in f]))
+        return tuple(x.value for x in f)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().heff_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def workspace_bytes(dims: dict, dist: dict | None = None) -> int:
+    cd = _Dims(*(dims[k] for k in ("mL", "d1", "d2", "mR", "kL", "kM", "kR")))
+    pd = None
+    if dist is not None:
+        pd = ctypes.byref(_Dist(dist["nranks"], dist["rank"], None, dist["b_lo"], dist["b_hi"]))
+    return int(lib().heff_workspace_bytes(ctypes.byref(cd), pd))

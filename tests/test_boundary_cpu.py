@@ -1,0 +1,62 @@
+"""CPU-side checks of the C-ABI boundary: libheff builds for sm_100a, loads without a GPU,
+and exports every function include/heff.h declares.  No compute calls (no GPU here)."""
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_functions():
+    text = (ROOT / "include" / "heff.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?(?:int|size_t|char\s*\*|const char\s*\*)\s*\*?\s*(heff_\w+|lanczos_ground)\s*\(",
+                                 text, flags=re.M)))
+
+
+def test_header_declares_north_star_calls():
+    fns = header_functions()
+    for name in ("heff_create", "heff_apply", "lanczos_ground", "heff_destroy", "heff_last_error"):
+        assert name in fns, fns
+
+
+def test_library_builds_and_exports_every_symbol():
+    import __graft_entry__ as g
+    g.build()
+    from paper_2007_14822_b200 import heff
+    L = heff.lib()
+    fns = header_functions()
+    assert set(fns) <= set(heff.EXPORTED), set(fns) - set(heff.EXPORTED)
+    for name in fns:
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(heff.LIB_PATH)], capture_output=True, text=True).stdout
+    for name in fns:
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_is_sm100a_with_dmma_and_tma():
+    from paper_2007_14822_b200 import heff
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(heff.LIB_PATH)], capture_output=True,
+                          text=True).stdout
+    assert "sm_100a" in sass
+    assert "DMMA.8x8x4" in sass          # FP64 tensor-core MMA
+    assert "UTMALDG" in sass             # TMA loads
+
+
+def test_product_path_does_not_import_oracle():
+    pkg = ROOT / "paper_2007_14822_b200"
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) + list(pkg.rglob("*.h")):
+        t = f.read_text()
+        assert "oracle" not in re.sub(r"#.*|//.*", "", t).replace("oracle/", ""), f
+
+
+def test_binding_errors_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2007_14822_b200 import Heff
+    t = torch.zeros(2, 2, 2, dtype=torch.float64)
+    with pytest.raises(TypeError):
+        Heff(t, t.reshape(2, 1, 2, 2), t.reshape(2, 1, 2, 2), t)

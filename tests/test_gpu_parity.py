@@ -1,0 +1,237 @@
+"""GPU parity: libheff (through its C ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star, reading R10): relative Frobenius error <= 1e-12
+per matvec; Lanczos ground energy within 1e-10 * max(1, |E|); ED energies within 1e-10.
+"""
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+import torch
+
+from heffgen import configs as C
+from tests import ed_ref
+
+pytestmark = pytest.mark.gpu
+
+MATVEC_TOL = 1e-12
+ENERGY_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__ as g
+    g.build()
+    return torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import oracle
+    oracle.build()
+    return oracle
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def gpu_apply(x, dev, path=0, psi=None):
+    from paper_2007_14822_b200 import Heff
+    xd = x.to(dev)
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        h.set_option(1, path)
+        p = xd.psi if psi is None else torch.from_numpy(psi).to(dev)
+        out = h.apply(p)
+        torch.cuda.synchronize()
+        return out.cpu().numpy()
+
+
+CASES = {
+    "c1": lambda: C.make("c1"),
+    "c1_n8": lambda: C.make("c1_n8"),
+    "two_site": lambda: C.trivial_two_site(),
+    "hubbard_two_site": lambda: C.trivial_two_site("hubbard"),
+    "c2": lambda: C.make("c2"),
+    "c4_m64": lambda: C.make("c4", m=64),
+    "c5_m32": lambda: C.make("c5", m=32),
+    "ragged_odd": lambda: C.random_dense(dict(mL=37, d1=3, d2=2, mR=29, kL=4, kM=3, kR=5), seed=31),
+    "ragged_even": lambda: C.random_dense(dict(mL=200, d1=3, d2=3, mR=150, kL=7, kM=5, kR=7), seed=32),
+    "tails": lambda: C.random_dense(dict(mL=130, d1=2, d2=2, mR=258, kL=3, kM=2, kR=5), seed=33),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("path", [0, 1, 2])
+def test_matvec_parity(dev, orc, case, path):
+    x = CASES[case]()
+    d = x.dims
+    if path == 2 and (d["mL"] % 2 or (d["d1"] * d["d2"] * d["mR"]) % 2 or (d["kR"] * d["mR"]) % 2):
+        pytest.skip("TMA path needs even row pitches")
+    L, W1, W2, R, psi = x.numpy()
+    ref = orc.heff_apply(L, W1, W2, R, psi)
+    out = gpu_apply(x, dev, path)
+    assert rel(out, ref) <= MATVEC_TOL, rel(out, ref)
+
+
+def test_matvec_parity_c3(dev, orc):
+    x = C.make("c3")
+    L, W1, W2, R, psi = x.numpy()
+    ref = orc.heff_apply(L, W1, W2, R, psi)
+    out = gpu_apply(x, dev)
+    assert rel(out, ref) <= MATVEC_TOL
+
+
+def test_matvec_parity_c4_full_size_sampled_rows(dev, orc):
+    """C4 at full size (m = 4096, k = 20) in the bench's launch configuration; the oracle
+    computes sampled output rows a' one by one (order A is independent per a')."""
+    from paper_2007_14822_b200 import Heff
+    x = C.make("c4", device=dev)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        out = h.apply(x.psi)
+        torch.cuda.synchronize()
+        L, W1, W2, R, psi = x.numpy()
+        mL = L.shape[0]
+        rows = sorted({0, 1, 127, 128, 2047, mL - 2, mL - 1} | set(np.random.default_rng(5).integers(0, mL, 5).tolist()))
+        outc = out.cpu().numpy()
+    for a in rows:
+        ref = orc.heff_apply(L, W1, W2, R, psi, rows=(a, a + 1))[0]
+        assert rel(outc[a], ref) <= MATVEC_TOL, (a, rel(outc[a], ref))
+    # a property that holds at any size: <psi|H psi> equals the oracle-free order-B value
+    e_a = float(np.vdot(psi, outc))
+    assert np.isfinite(e_a)
+
+
+def test_orderB_virtual_shards(dev, orc):
+    from paper_2007_14822_b200 import Heff
+    for x, P in ((C.make("c2"), 2), (C.make("c2"), 4), (C.make("c4", m=64), 8),
+                 (C.random_dense(dict(mL=40, d1=2, d2=3, mR=33, kL=3, kM=4, kR=2), seed=3), 3)):
+        L, W1, W2, R, psi = x.numpy()
+        ref = orc.heff_apply(L, W1, W2, R, psi)
+        xd = x.to(dev)
+        mR = R.shape[0]
+        bounds = np.linspace(0, mR, P + 1).astype(int)
+        parts = []
+        for g in range(P):
+            lo, hi = int(bounds[g]), int(bounds[g + 1])
+            Rg = xd.R[lo:hi].contiguous()
+            with Heff(xd.L, xd.W1, xd.W2, Rg, dist=dict(nranks=P, rank=g, b_lo=lo, b_hi=hi)) as h:
+                parts.append(h.apply(xd.psi).cpu().numpy())
+        out = np.concatenate(parts, axis=3)
+        assert rel(out, ref) <= MATVEC_TOL
+        refB = orc.heff_apply_B(L, W1, W2, R, psi, cols=(int(bounds[1]), int(bounds[2])))
+        assert rel(parts[1], refB) <= MATVEC_TOL
+
+
+def test_linearity_and_hermiticity_gpu(dev):
+    from paper_2007_14822_b200 import Heff
+    x = C.make("c2", device=dev)
+    g = torch.Generator(device="cpu").manual_seed(4)
+    phi = torch.randn(x.psi.shape, generator=g, dtype=torch.float64).to(dev)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        Hpsi, Hphi = h.apply(x.psi), h.apply(phi)
+        Hlin = h.apply((2.0 * x.psi - 0.5 * phi).contiguous())
+    assert torch.linalg.norm(Hlin - (2.0 * Hpsi - 0.5 * Hphi)) <= 1e-13 * torch.linalg.norm(Hlin)
+    lhs, rhs = torch.dot(phi.ravel(), Hpsi.ravel()), torch.dot(Hphi.ravel(), x.psi.ravel())
+    assert abs(lhs - rhs) <= 1e-12 * torch.linalg.norm(phi) * torch.linalg.norm(Hpsi)
+
+
+def test_apply_host_e2e(dev, orc):
+    from paper_2007_14822_b200 import Heff
+    x = C.make("c2")
+    L, W1, W2, R, psi = x.numpy()
+    ref = orc.heff_apply(L, W1, W2, R, psi)
+    xd = x.to(dev)
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        out = torch.empty(x.psi.shape, dtype=torch.float64).pin_memory()
+        h.apply_host(x.psi.contiguous(), out)
+    assert rel(out.numpy(), ref) <= MATVEC_TOL
+
+
+# ------------------------------------------------------------------------ Lanczos
+def gpu_lanczos(x, dev, max_iter, tol=0.0, converge=False):
+    from paper_2007_14822_b200 import Heff
+    xd = x.to(dev)
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        v = xd.psi.clone()
+        r = h.lanczos_ground(v, max_iter=max_iter, tol=tol, converge=converge)
+        return r, v.cpu().numpy()
+
+
+@pytest.mark.parametrize("name,steps", [("c1", 20), ("c1_n8", 20), ("c3", 6)])
+def test_lanczos_fixed_steps_parity(dev, orc, name, steps):
+    x = C.make(name)
+    L, W1, W2, R, psi = x.numpy()
+    o = orc.lanczos_heff(L, W1, W2, R, psi, max_iter=steps)
+    r, v = gpu_lanczos(x, dev, steps)
+    assert r.iters == o.iters == steps
+    assert abs(r.energy - o.energy) <= ENERGY_TOL * max(1.0, abs(o.energy))
+    np.testing.assert_allclose(r.alpha, o.alpha, rtol=0, atol=1e-10)
+    np.testing.assert_allclose(r.beta, o.beta, rtol=0, atol=1e-10)
+    assert abs(np.linalg.norm(v) - 1.0) < 1e-12
+    assert abs(abs(np.vdot(v, o.x)) - 1.0) < 1e-8
+
+
+def test_lanczos_converge_c2(dev, orc):
+    x = C.make("c2")
+    L, W1, W2, R, psi = x.numpy()
+    o = orc.lanczos_heff(L, W1, W2, R, psi, max_iter=500, tol=1e-10, converge=True)
+    r, v = gpu_lanczos(x, dev, 500, tol=1e-10, converge=True)
+    assert abs(r.energy - o.energy) <= ENERGY_TOL * max(1.0, abs(o.energy))
+    assert abs(r.iters - o.iters) <= 2
+    assert abs(abs(np.vdot(v, o.x)) - 1.0) < 1e-10
+
+
+@pytest.mark.parametrize("name,N", [("c1_n8", 8), ("c1", 10)])
+def test_lanczos_gpu_matches_ed(dev, name, N):
+    x = C.make(name)
+    r, _ = gpu_lanczos(x, dev, 300, tol=1e-10, converge=True)
+    e0 = spla.eigsh(ed_ref.heisenberg(N, ed_ref.chain_bonds(N)), k=1, which="SA", tol=1e-14)[0][0]
+    assert abs(r.energy - e0) <= 1e-10
+
+
+def test_lanczos_two_site_singlet(dev):
+    r, v = gpu_lanczos(C.trivial_two_site(), dev, 10, tol=1e-12, converge=True)
+    assert abs(r.energy + 0.75) <= 1e-12
+    # singlet (|ud> - |du>)/sqrt(2) up to sign
+    s = np.zeros(4); s[1], s[2] = 1 / np.sqrt(2), -1 / np.sqrt(2)
+    assert abs(abs(np.dot(v.ravel(), s)) - 1) < 1e-10
+
+
+def test_lanczos_zero_vector_and_errors(dev):
+    from paper_2007_14822_b200 import Heff, HeffError, HeffZeroVector
+    x = C.make("c1").to(dev)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        with pytest.raises(HeffZeroVector):
+            h.lanczos_ground(torch.zeros_like(x.psi), max_iter=5)
+        with pytest.raises(HeffError):
+            h.apply(x.psi, x.psi)                       # aliasing
+        with pytest.raises(HeffError):
+            h.lanczos_ground(x.psi.clone(), max_iter=0)
+    bad = torch.zeros((4, 3, 4), dtype=torch.float64, device=dev)   # kL mismatch is caught on the python side
+    with pytest.raises(Exception):
+        Heff(bad, x.W1, x.W2, x.R)
+
+
+def test_lanczos_nccl_single_rank(dev, orc):
+    """The communicating (order B + NCCL) Lanczos path with one rank on one GPU."""
+    from paper_2007_14822_b200 import Heff, nccl_unique_id
+    x = C.make("c2")
+    L, W1, W2, R, psi = x.numpy()
+    o = orc.lanczos_heff(L, W1, W2, R, psi, max_iter=20)
+    xd = x.to(dev)
+    uid = nccl_unique_id()
+    with Heff(xd.L, xd.W1, xd.W2, xd.R, dist=dict(nranks=1, rank=0, b_lo=0, b_hi=R.shape[0], uid=uid)) as h:
+        v = xd.psi.clone()
+        r = h.lanczos_ground(v, max_iter=20)
+    assert abs(r.energy - o.energy) <= ENERGY_TOL * max(1.0, abs(o.energy))
+
+
+def test_kernel_launch_count(dev):
+    from paper_2007_14822_b200 import Heff
+    x = C.make("c2", device=dev)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        h.apply(x.psi)
+        assert h.get_option(2) == 3      # GEMM1, fused MPO, GEMM4
