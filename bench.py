@@ -1,0 +1,321 @@
+"""Benchmark of the hot path: FP64 two-site H_eff.psi inside Lanczos, at C4 (m = 4096).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl heff|reference]
+
+A step is one Lanczos iteration through the C ABI (lanczos_ground, fixed-step mode):
+one H_eff.psi matvec (GEMM1 L.psi -> fused MPO W1.W2 -> GEMM4 .R^T; at N > 1 order B
+on a b'-shard plus the NCCL all-gather of psi), CGS2 reorthogonalisation, the norm and
+the host tridiagonal solve.  value = matvecs/s of the whole job (strong scaling: one
+fixed m = 4096 problem split over N GPUs).  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, plain C loops, all host cores) on a
+bounded sample of the same workload (rows a' of the output), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "H_eff·ψ matvecs/s and FP64 TFLOP/s vs B200 FP64 peak at m=4096, 1/2/4/8 GPU"
+# FP64 peak: 148 SM x 128 flop/clk/SM x 1.965 GHz; the DMMA microbenchmark measured 37.16 TF/s
+# sustained at 1965 MHz (profiles/r01_fp64_peaks.txt).  MEASURED_PEAKS.json has no FP64 entry.
+FP64_PEAK_TFLOPS = 148 * 128 * 1.965e9 / 1e12
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (clocks + throttle reasons)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
+        pw = [float(r[2]) for r in self.rows if len(r) >= 7 and r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+def workload_name(cfg: str, dims: dict) -> str:
+    model = {"c1": "heisenberg_chain", "c2": "heisenberg_chain", "c3": "heisenberg_chain", "c4": "cylinder6",
+             "c5": "hubbard"}[cfg]
+    return f"{cfg}_{model}_m{dims['mL']}_d{dims['d1']}_k{dims['kL']}"
+
+
+def cpu_baseline(x, budget_s: float = 12.0) -> dict:
+    """The oracle as it stands, on rows a' of the same C4 inputs, for ~budget_s seconds."""
+    from oracle import oracle
+    oracle.build()
+    L, W1, W2, R, psi = x.numpy()
+    mL = L.shape[0]
+    cores = oracle.max_threads()
+    rows_done, t0 = 0, time.perf_counter()
+    while True:
+        lo = rows_done % mL
+        hi = min(mL, lo + cores)
+        oracle.heff_apply(L, W1, W2, R, psi, rows=(lo, hi))
+        rows_done += hi - lo
+        el = time.perf_counter() - t0
+        if el >= budget_s or rows_done >= mL:
+            break
+    return {"value": rows_done / mL / el, "unit": "matvec/s", "cores": cores, "kind": "oracle",
+            "sample": f"{rows_done} of {mL} output rows a' (order A, independent per a'), {el:.1f} s; "
+                      f"value = rows/s / mL", "seconds": el}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on bounded samples of the same workload."""
+    import numpy as np  # noqa: F401
+    import torch
+    from heffgen import configs as C
+    from oracle import oracle
+
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    oracle.build()
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    x = C.make(args.config, device=dev).to("cpu")
+    L, W1, W2, R, psi = x.numpy()
+    mL = L.shape[0]
+    cores = oracle.max_threads()
+    rows = cores  # one row per thread per step
+    for _ in range(args.warmup):
+        oracle.heff_apply(L, W1, W2, R, psi, rows=(0, rows))
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        lo = (s * rows) % mL
+        oracle.heff_apply(L, W1, W2, R, psi, rows=(lo, min(mL, lo + rows)))
+    el = time.perf_counter() - t0
+    frac = rows / mL
+    value = args.steps * frac / el
+    flops = C.flops_per_matvec(x.dims)
+    line = {"metric": METRIC, "value": value, "unit": "matvec/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3 / frac,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config, x.dims), **x.dims, "parallelism": "cpu_oracle"},
+            "tflops": value * flops / 1e12,
+            "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle",
+                             "sample": f"each step = {rows} of {mL} output rows a' of one matvec (order A oracle)"},
+            "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def load_ncu_traffic(kernel_key: str):
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if not f.exists():
+        return None
+    try:
+        d = json.loads(f.read_text())
+        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="heff", choices=["heff", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from heffgen import configs as C
+    from paper_2007_14822_b200 import Heff
+    from paper_2007_14822_b200.heff import OPT_PROFILE, OPT_TOTAL_LAUNCHES, nccl_unique_id
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- inputs (seeded, synthetic; generated on the GPU, then broadcast from rank 0)
+    x = C.make(args.config, device=dev)
+    dims = x.dims
+    if world > 1:
+        for t in (x.L, x.W1, x.W2, x.R, x.psi):
+            dist.broadcast(t, 0)
+    mR = dims["mR"]
+    flops = C.flops_per_matvec(dims)
+    gemm_flops = C.gemm_flops_per_matvec(dims)
+    if world > 1:
+        assert mR % world == 0
+        nb = mR // world
+        lo, hi = rank * nb, (rank + 1) * nb
+        uid_t = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid_t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid_t, 0)
+        uid = bytes(uid_t.cpu().tolist())
+        Rg = x.R[lo:hi].contiguous()
+        plan = Heff(x.L, x.W1, x.W2, Rg, dist=dict(nranks=world, rank=rank, b_lo=lo, b_hi=hi, uid=uid))
+        psi0 = x.psi[..., lo:hi].contiguous()
+        order = "B (R-first) on b'-shards"
+    else:
+        plan = Heff(x.L, x.W1, x.W2, x.R)
+        psi0 = x.psi.clone()
+        order = "A (L-first)"
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up: W Lanczos steps
+    v = psi0.clone()
+    plan.lanczos_ground(v, max_iter=max(1, args.warmup))
+    barrier()
+
+    # ---- timed: K Lanczos steps (one lanczos_ground call, fixed-step mode)
+    plan.set_option(OPT_PROFILE, 1)
+    plan.set_option(OPT_TOTAL_LAUNCHES, 0)
+    clk = Clocks(local)
+    v = psi0.clone()
+    barrier()
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = plan.lanczos_ground(v, max_iter=args.steps)
+    e1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    launches = plan.get_option(OPT_TOTAL_LAUNCHES)
+    g1_ms, mpo_ms, g4_ms, nrec = plan.last_timings()
+    plan.set_option(OPT_PROFILE, 0)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = args.steps / (ms_max / 1e3)
+
+    # ---- e2e: heff_apply_host (pinned host psi in, host out) per step
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        hin = x.psi.cpu().pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        plan.apply_host(hin, hout)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            plan.apply_host(hin, hout)
+        el = time.perf_counter() - t0
+        e2e = {"value": args.e2e_steps / el, "unit": "matvec/s", "h2d_bytes_per_step": hin.numel() * 8,
+               "d2h_bytes_per_step": hout.numel() * 8,
+               "what": "heff_apply_host: pinned-host psi -> device, H_eff.psi, device -> pinned-host out"}
+    elif world > 1:
+        e2e = {"value": None, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "what": "not measured at N>1 (sharded Lanczos keeps vectors on device)"}
+
+    # ---- roofline of the dominant kernel (a GEMM step; the two GEMMs are ~50/50)
+    n_mv = max(1.0, nrec)
+    d = dims
+    g1_flop = 2.0 * d["mL"] * d["kL"] * d["mL"] * d["d1"] * d["d2"] * d["mR"]
+    g4_flop = gemm_flops - g1_flop
+    if world > 1:
+        g1_flop /= world
+        g4_flop /= world
+    k1 = ("gemm_first", g1_ms, g1_flop)
+    k4 = ("gemm_last", g4_ms, g4_flop)
+    dom = max((k1, k4), key=lambda k: k[1])
+    per_launch_ms = dom[1] / n_mv
+    achieved = dom[2] / (per_launch_ms / 1e3) / 1e12 if per_launch_ms > 0 else None
+    kernel_names = {"gemm_first": "gemm_dmma_tma_kernel NN (L.psi)" if world == 1 else "gemm_dmma_tma_kernel NT (psi.R^T)",
+                    "gemm_last": "gemm_dmma_tma_kernel NT (T3.R^T)" if world == 1 else "gemm_dmma_tma_kernel NN (L.V3)"}
+    roofline = {"bound": "tensor", "kernel": kernel_names[dom[0]], "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
+                "traffic": load_ncu_traffic(dom[0] + ("_A" if world == 1 else "_B")),
+                "peak_source": "derived FP64 DMMA peak 148 SM x 128 flop/clk x 1.965 GHz = 37.2 TF/s (no FP64 entry "
+                               "in MEASURED_PEAKS.json); DMMA microbenchmark 37.16 TF/s sustained",
+                "per_launch_ms": per_launch_ms,
+                "gemm_steps": {"gemm_first_tflops": g1_flop * n_mv / (g1_ms / 1e3) / 1e12 if g1_ms else None,
+                               "gemm_last_tflops": g4_flop * n_mv / (g4_ms / 1e3) / 1e12 if g4_ms else None,
+                               "gemm_both_frac": ((g1_flop + g4_flop) * n_mv / ((g1_ms + g4_ms) / 1e3) / 1e12
+                                                  / FP64_PEAK_TFLOPS) if (g1_ms + g4_ms) else None,
+                               "mpo_ms_per_matvec": mpo_ms / n_mv,
+                               "share_of_step": {"gemm_first": g1_ms / ms, "mpo": mpo_ms / ms, "gemm_last": g4_ms / ms}}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        del plan
+        torch.cuda.empty_cache()
+        cpu = cpu_baseline(x.to("cpu"))
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_name(args.config, dims), **dims, "order": order,
+                           "parallelism": f"b'-shard x{world}" if world > 1 else "single GPU",
+                           "flops_per_matvec": flops, "l2": "inputs larger than L2 (psi 0.54 GB, L and R 2.7 GB each)",
+                           "step": "one Lanczos iteration (matvec + CGS2 + norm + host tridiagonal)"},
+                "tflops": value * flops / 1e12, "frac_fp64_peak": value * flops / 1e12 / (FP64_PEAK_TFLOPS * world),
+                "lanczos": {"energy": res.energy, "iters": res.iters},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -133,10 +133,13 @@ enum { HEFF_OPT_GEMM_PATH = 1, HEFF_OPT_LAST_KERNEL_COUNT = 2, HEFF_OPT_MPO_NNZ 
 int heff_set_option(heff_plan p, int option, int64_t value);
 int heff_get_option(heff_plan p, int option, int64_t* value);
 
-/* Timing of the dominant kernels inside the last heff_apply when enabled with
- * HEFF_OPT_PROFILE (events recorded on the launch stream): ms for GEMM1, MPO, GEMM4. */
-enum { HEFF_OPT_PROFILE = 4 };
-int heff_last_timings(heff_plan p, float* ms_gemm_first, float* ms_mpo, float* ms_gemm_last, float* ms_other);
+/* Kernel timing.  With HEFF_OPT_PROFILE = 1 every matvec (chunk) records CUDA events on
+ * its launch stream around its first GEMM, the fused MPO kernel and its last GEMM, with
+ * no host synchronisation.  heff_last_timings waits for them, returns the summed ms of
+ * each of the three since the previous call (n_recorded = matvec chunks) and resets.
+ * HEFF_OPT_TOTAL_LAUNCHES: kernels launched on this plan (set resets the counter). */
+enum { HEFF_OPT_PROFILE = 4, HEFF_OPT_TOTAL_LAUNCHES = 5 };
+int heff_last_timings(heff_plan p, float* ms_gemm_first, float* ms_mpo, float* ms_gemm_last, float* n_recorded);
 
 #ifdef __cplusplus
 }

@@ -268,9 +268,10 @@ struct heff_plan_s {
   // options
   int gemm_path = 0;
   int last_launches = 0;
+  int64_t total_launches = 0;              // every libheff kernel launched on this plan
   int profile = 0;
-  cudaEvent_t ev[8] = {};
-  float t_g1 = 0, t_mpo = 0, t_g4 = 0, t_other = 0;
+  std::vector<cudaEvent_t> prof_ev;         // 4 events per recorded (chunk of a) matvec
+  size_t prof_used = 0;
 };
 
 static int build_csr(Csr& c, const std::vector<int>& rowptr, const std::vector<int>& col, const std::vector<double>& val) {
@@ -367,8 +368,7 @@ extern "C" int heff_destroy(heff_plan p) {
   cudaFree(p->partial); cudaFree(p->scal);
   free_csr(p->csrA);
   free_csr(p->csrB);
-  for (auto& e : p->ev)
-    if (e) cudaEventDestroy(e);
+  for (auto& e : p->prof_ev) cudaEventDestroy(e);
   if (p->comm && g_nccl.loaded) g_nccl.CommDestroy(p->comm);
   delete p;
   return HEFF_OK;
@@ -499,8 +499,10 @@ extern "C" int heff_set_option(heff_plan p, int option, int64_t value) {
       return HEFF_OK;
     case HEFF_OPT_PROFILE:
       p->profile = value ? 1 : 0;
-      if (p->profile && !p->ev[0])
-        for (auto& e : p->ev) CK(cudaEventCreate(&e));
+      p->prof_used = 0;
+      return HEFF_OK;
+    case HEFF_OPT_TOTAL_LAUNCHES:
+      p->total_launches = value;
       return HEFF_OK;
     default:
       return set_err(HEFF_EINVAL, "unknown option %d", option);
@@ -514,16 +516,42 @@ extern "C" int heff_get_option(heff_plan p, int option, int64_t* value) {
     case HEFF_OPT_LAST_KERNEL_COUNT: *value = p->last_launches; return HEFF_OK;
     case HEFF_OPT_MPO_NNZ: *value = p->sharded ? p->csrB.nnz : p->csrA.nnz; return HEFF_OK;
     case HEFF_OPT_PROFILE: *value = p->profile; return HEFF_OK;
+    case HEFF_OPT_TOTAL_LAUNCHES: *value = p->total_launches; return HEFF_OK;
     default: return set_err(HEFF_EINVAL, "unknown option %d", option);
   }
 }
 
+// profiling: 4 events around (GEMM first, MPO, GEMM last) per recorded matvec chunk;
+// no host synchronisation until heff_last_timings collects and resets them.
+static int prof_mark(heff_plan_s* p, int k, cudaStream_t s) {
+  if (!p->profile) return HEFF_OK;
+  const size_t idx = p->prof_used * 4 + k;
+  while (p->prof_ev.size() <= idx) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    p->prof_ev.push_back(e);
+  }
+  CK(cudaEventRecord(p->prof_ev[idx], s));
+  if (k == 3) ++p->prof_used;
+  return HEFF_OK;
+}
+
 extern "C" int heff_last_timings(heff_plan p, float* g1, float* mpo, float* g4, float* other) {
   if (!p) return set_err(HEFF_EINVAL, "null plan");
-  if (g1) *g1 = p->t_g1;
-  if (mpo) *mpo = p->t_mpo;
-  if (g4) *g4 = p->t_g4;
-  if (other) *other = p->t_other;
+  float a = 0, b = 0, c = 0;
+  for (size_t i = 0; i < p->prof_used; ++i) {
+    cudaEvent_t* e = &p->prof_ev[i * 4];
+    CK(cudaEventSynchronize(e[3]));
+    float x;
+    CK(cudaEventElapsedTime(&x, e[0], e[1])); a += x;
+    CK(cudaEventElapsedTime(&x, e[1], e[2])); b += x;
+    CK(cudaEventElapsedTime(&x, e[2], e[3])); c += x;
+  }
+  if (g1) *g1 = a;
+  if (mpo) *mpo = b;
+  if (g4) *g4 = c;
+  if (other) *other = (float)p->prof_used;
+  p->prof_used = 0;
   return HEFF_OK;
 }
 
@@ -534,31 +562,24 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
   const size_t mpo_smem = sizeof(double) * nin * kMpoCols;
   for (int64_t a0 = 0; a0 < d.mL; a0 += p->chunk_rows) {
     const int64_t rows = std::min(p->chunk_rows, d.mL - a0);
-    if (p->profile) CK(cudaEventRecord(p->ev[0], s));
+    CKR(prof_mark(p, 0, s));
     p->g1.M = rows * d.kL;
     p->g1.A = p->L + a0 * d.kL * d.mL;
     p->g1.B = psi;
     p->g1.C = p->T1;
     CKR(launch_gemm(p->g1, p->gemm_path, s, nl));
-    if (p->profile) CK(cudaEventRecord(p->ev[1], s));
+    CKR(prof_mark(p, 1, s));
     dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
     mpo_orderA_kernel<<<grid, kMpoCols, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
                                                        p->csrA.d_col, p->csrA.d_val);
     CK(cudaGetLastError());
     ++*nl;
-    if (p->profile) CK(cudaEventRecord(p->ev[2], s));
+    CKR(prof_mark(p, 2, s));
     p->g4.M = rows * d.d1 * d.d2;
     p->g4.A = p->T3;
     p->g4.C = out + a0 * d.d1 * d.d2 * d.mR;
     CKR(launch_gemm(p->g4, p->gemm_path, s, nl));
-    if (p->profile) {
-      CK(cudaEventRecord(p->ev[3], s));
-      CK(cudaEventSynchronize(p->ev[3]));
-      float x;
-      CK(cudaEventElapsedTime(&x, p->ev[0], p->ev[1])); p->t_g1 += x;
-      CK(cudaEventElapsedTime(&x, p->ev[1], p->ev[2])); p->t_mpo += x;
-      CK(cudaEventElapsedTime(&x, p->ev[2], p->ev[3])); p->t_g4 += x;
-    }
+    CKR(prof_mark(p, 3, s));
   }
   return HEFF_OK;
 }
@@ -567,26 +588,19 @@ static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStre
   const heff_dims& d = p->dims;
   const int dd = (int)(d.d1 * d.d2);
   const size_t mpo_smem = sizeof(double) * dd * d.kR * kMpoCols;
-  if (p->profile) CK(cudaEventRecord(p->ev[0], s));
+  CKR(prof_mark(p, 0, s));
   p->gA.A = psi;
   CKR(launch_gemm(p->gA, p->gemm_path, s, nl));
-  if (p->profile) CK(cudaEventRecord(p->ev[1], s));
+  CKR(prof_mark(p, 1, s));
   dim3 grid((unsigned)((p->nb + kMpoCols - 1) / kMpoCols), (unsigned)d.mL);
   mpo_orderB_kernel<<<grid, kMpoCols, mpo_smem, s>>>(p->V1, p->V3, d.mL, p->nb, dd, (int)d.kR, (int)d.kL,
                                                      p->csrB.d_rowptr, p->csrB.d_col, p->csrB.d_val);
   CK(cudaGetLastError());
   ++*nl;
-  if (p->profile) CK(cudaEventRecord(p->ev[2], s));
+  CKR(prof_mark(p, 2, s));
   p->gD.C = out;
   CKR(launch_gemm(p->gD, p->gemm_path, s, nl));
-  if (p->profile) {
-    CK(cudaEventRecord(p->ev[3], s));
-    CK(cudaEventSynchronize(p->ev[3]));
-    float x;
-    CK(cudaEventElapsedTime(&x, p->ev[0], p->ev[1])); p->t_g1 += x;
-    CK(cudaEventElapsedTime(&x, p->ev[1], p->ev[2])); p->t_mpo += x;
-    CK(cudaEventElapsedTime(&x, p->ev[2], p->ev[3])); p->t_g4 += x;
-  }
+  CKR(prof_mark(p, 3, s));
   return HEFF_OK;
 }
 
@@ -596,9 +610,9 @@ static int apply_impl(heff_plan_s* p, const double* psi, double* out, cudaStream
   if ((reinterpret_cast<uintptr_t>(psi) | reinterpret_cast<uintptr_t>(out)) & 7)
     return set_err(HEFF_EINVAL, "heff_apply: psi/out must be 8-byte aligned");
   int nl = 0;
-  p->t_g1 = p->t_mpo = p->t_g4 = p->t_other = 0.f;
   int r = p->sharded ? apply_orderB(p, psi, out, s, &nl) : apply_orderA(p, psi, out, s, &nl);
   p->last_launches = nl;
+  p->total_launches += nl;
   return r;
 }
 
@@ -640,8 +654,10 @@ static int multidot(heff_plan_s* p, const double* V, int nq, const double* w, in
   for (int q0 = 0; q0 < nq; q0 += kDotQ) {
     const int qn = std::min(kDotQ, nq - q0);
     multidot_partial_kernel<<<G, kRedThreads, 0, s>>>(V + q0 * p->ldv, p->ldv, qn, w, n, p->partial + q0 * G, G);
+    ++p->total_launches;
   }
   reduce_partial_kernel<<<nq, kRedThreads, 0, s>>>(p->partial, G, G, c, 0, nullptr);
+  ++p->total_launches;
   CK(cudaGetLastError());
   if (p->comm) CKN(g_nccl.AllReduce(c, c, nq, ncclFloat64, ncclSum, p->comm, s));
   return HEFF_OK;
@@ -652,6 +668,7 @@ static int multiaxpy(heff_plan_s* p, const double* V, int nq, const double* c, d
   for (int q0 = 0; q0 < nq; q0 += 64) {
     const int qn = std::min(64, nq - q0);
     multiaxpy_kernel<<<ew_grid(n), 256, 0, s>>>(V + q0 * p->ldv, p->ldv, qn, c + q0, sign, w, n);
+    ++p->total_launches;
   }
   CK(cudaGetLastError());
   return HEFF_OK;
@@ -668,10 +685,12 @@ static int norm2(heff_plan_s* p, const double* w, int64_t n, double* nrm, double
   const int G = p->ldp;
   multidot_partial_kernel<<<G, kRedThreads, 0, s>>>(w, 0, 1, w, n, p->partial, G);
   reduce_partial_kernel<<<1, kRedThreads, 0, s>>>(p->partial, G, G, nrm, p->comm ? 0 : 1, inv);
+  p->total_launches += 2;
   CK(cudaGetLastError());
   if (p->comm) {
     CKN(g_nccl.AllReduce(nrm, nrm, 1, ncclFloat64, ncclSum, p->comm, s));
     sqrt_inv_kernel<<<1, 1, 0, s>>>(nrm, inv);
+    ++p->total_launches;
     CK(cudaGetLastError());
   }
   return HEFF_OK;
@@ -689,6 +708,7 @@ static int matvec_local(heff_plan_s* p, const double* v, double* w, cudaStream_t
   } else {
     CKN(g_nccl.AllGather(v, p->gather, nloc, ncclFloat64, p->comm, s));
     relayout_blocked_kernel<<<ew_grid(rows * d.mR), 256, 0, s>>>(p->gather, p->full, rows, p->nb, p->nranks);
+    ++p->total_launches;
     CK(cudaGetLastError());
   }
   return apply_impl(p, p->full, w, s);
@@ -738,6 +758,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   CK(cudaStreamSynchronize(s));
   if (!(h_nrm > 0.0)) return set_err(HEFF_EZERO, "lanczos_ground: zero start vector");
   scale_kernel<<<ew_grid(n), 256, 0, s>>>(V, invb + cap, V, n);
+  ++p->total_launches;
   CK(cudaGetLastError());
 
   std::vector<double> ha(cap), hb(cap);
@@ -751,8 +772,12 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     CKR(multidot(p, V, j, w, n, c2, s));
     CKR(multiaxpy(p, V, j, c2, -1.0, w, n, s));
     lanczos_alpha_kernel<<<1, 1, 0, s>>>(c1, c2, j - 1, alpha);
+    ++p->total_launches;
     CKR(norm2(p, w, n, beta + (j - 1), invb + (j - 1), s));
-    if (j < cap) scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + (j - 1), V + (int64_t)j * ldv, n);
+    if (j < cap) {
+      scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + (j - 1), V + (int64_t)j * ldv, n);
+      ++p->total_launches;
+    }
     CK(cudaGetLastError());
     return HEFF_OK;
   };
@@ -800,6 +825,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   CKR(multiaxpy(p, V, j_done, ydev, 1.0, w, n, s));
   CKR(norm2(p, w, n, beta + cap, invb + cap, s));
   scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + cap, psi, n);
+  ++p->total_launches;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
   *energy = theta;

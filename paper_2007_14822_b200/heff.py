@@ -17,7 +17,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libheff.so"
 
 HEFF_OK, HEFF_EINVAL, HEFF_ENOMEM, HEFF_ECUDA, HEFF_ENCCL, HEFF_EZERO, HEFF_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
-OPT_GEMM_PATH, OPT_LAST_KERNEL_COUNT, OPT_MPO_NNZ, OPT_PROFILE = 1, 2, 3, 4
+OPT_GEMM_PATH, OPT_LAST_KERNEL_COUNT, OPT_MPO_NNZ, OPT_PROFILE, OPT_TOTAL_LAUNCHES = 1, 2, 3, 4, 5
 
 
 class HeffError(RuntimeError):
@@ -125,10 +125,17 @@ class Heff:
     def __init__(self, L, W1, W2, R, dist: dict | None = None, stream=None):
         for t, n in ((L, "L"), (W1, "W1"), (W2, "W2"), (R, "R")):
             _dev(t, n)
+        if L.dim() != 3 or W1.dim() != 4 or W2.dim() != 4 or R.dim() != 3:
+            raise ValueError("expected L[mL,kL,mL], W1[kL,d1,d1,kM], W2[kM,d2,d2,kR], R[nb,kR,mR]")
         mL, kL, _ = L.shape
         _, d1, _, kM = W1.shape
         _, d2, _, kR = W2.shape
         mR = R.shape[2]
+        nb = (dist["b_hi"] - dist["b_lo"]) if dist is not None else mR
+        if (tuple(L.shape) != (mL, kL, mL) or tuple(W1.shape) != (kL, d1, d1, kM)
+                or tuple(W2.shape) != (kM, d2, d2, kR) or tuple(R.shape) != (nb, kR, mR)):
+            raise ValueError(f"inconsistent shapes L{tuple(L.shape)} W1{tuple(W1.shape)} W2{tuple(W2.shape)} "
+                             f"R{tuple(R.shape)}")
         self.dims = dict(mL=mL, d1=d1, d2=d2, mR=mR, kL=kL, kM=kM, kR=kR)
         self._keep = (L, W1, W2, R)
         self._cdims = _Dims(mL, d1, d2, mR, kL, kM, kR)
@@ -166,6 +173,9 @@ class Heff:
         if out is None:
             out = torch.empty(self.out_shape, dtype=torch.float64, device=psi.device)
         _dev(out, "out")
+        n_in = self.dims["mL"] * self.dims["d1"] * self.dims["d2"] * self.dims["mR"]
+        if psi.numel() != n_in or out.numel() != n_in // self.dims["mR"] * self.nb:
+            raise ValueError(f"psi must have {self.psi_shape} elements and out {self.out_shape}")
         _check(lib().heff_apply(self._h, psi.data_ptr(), out.data_ptr(), _stream(stream)))
         return out
 
