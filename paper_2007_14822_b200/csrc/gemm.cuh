@@ -53,7 +53,8 @@ struct TmaGemmCfg {
 template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR>
 __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::kThreads, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                         double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store) {
+                         double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store,
+                         int splits, int64_t split_stride) {
   using Cfg = TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>;
   constexpr int MI = WM / 8, NJ = WN / 8;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -65,6 +66,10 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int ktiles = (K + kGemmBK - 1) / kGemmBK;
+  // split-K: work unit u = (tile, split); split s covers k blocks [s*kper, min((s+1)*kper, ktiles))
+  // and writes its partial tile to C + s*split_stride (reduced by splitk_reduce_kernel).
+  const int kper = (ktiles + splits - 1) / splits;
+  const int units = tiles * splits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -83,10 +88,11 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
       tma_prefetch_desc(&tmB);
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, group_m, mb, nb);
-        for (int kb = 0; kb < ktiles; ++kb) {
+        tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
+        const int kb0 = (u % splits) * kper, kb1 = min(ktiles, kb0 + kper);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* sA = smem + stage * Cfg::kStageBytes;
           unsigned char* sB = sA + Cfg::kTileABytes;
@@ -118,16 +124,18 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
     int mb, nb;
-    tile_coords(tile, num_m, num_n, group_m, mb, nb);
+    tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
+    const int kb0 = (u % splits) * kper, kb1 = min(ktiles, kb0 + kper);
+    double* Cu = C + (int64_t)(u % splits) * split_stride;
     double acc[MI][NJ][2];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int kb = 0; kb < ktiles; ++kb) {
+    for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(&full[stage], phase);
       const uint32_t sA = smem_base + stage * Cfg::kStageBytes;
       const uint32_t sB = sA + Cfg::kTileABytes;
@@ -169,7 +177,7 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
     for (int i = 0; i < MI; ++i) {
       const int row = mb * BM + wm0 + 8 * i + g;
       if (row >= M) continue;
-      double* crow = C + (int64_t)row * ldc;
+      double* crow = Cu + (int64_t)row * ldc;
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         const int col = nb * BN + wn0 + 8 * j + 2 * t;
@@ -181,6 +189,19 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
         }
       }
     }
+  }
+}
+
+// C[r][c] = sum_s W[s][r][c] over the split-K partial tiles, in fixed order (deterministic).
+__global__ void splitk_reduce_kernel(const double* __restrict__ W, int splits, int64_t split_stride,
+                                     double* __restrict__ C, int64_t ldc, int M, int N) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / N, c = i - r * N;
+    const int64_t off = r * ldc + c;
+    double acc = W[off];
+    for (int s = 1; s < splits; ++s) acc += W[s * split_stride + off];
+    C[off] = acc;
   }
 }
 

@@ -158,13 +158,41 @@ struct GemmOp {
 
 static int g_num_sms = 0;
 
+// split-K factor: enough (tile, split) units to fill the 148 SMs in whole waves when the
+// tile count alone would leave most of the last wave idle; each split keeps >= 4 k blocks.
+static int choose_splits(int64_t tiles, int64_t ktiles) {
+  if (tiles >= 4 * (int64_t)g_num_sms) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 16; ++s) {
+    const int64_t kper = (ktiles + s - 1) / s;
+    if (s > 1 && kper < 4) break;
+    const int64_t units = tiles * s;
+    const int64_t waves = (units + g_num_sms - 1) / g_num_sms;
+    const double eff = (double)units / (double)(waves * g_num_sms);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = s;
+    }
+    if (eff >= 0.95) break;
+  }
+  // no empty splits
+  const int64_t kper = (ktiles + best - 1) / best;
+  return (int)((ktiles + kper - 1) / kper);
+}
+
 static bool tma_ok(const GemmOp& g) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   return (g.lda % 2 == 0) && (g.ldb % 2 == 0) && al16(g.A) && al16(g.B) && g.M < (1ll << 31) && g.N < (1ll << 31) &&
          g.K < (1ll << 31);
 }
 
-static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch) {
+struct SplitWs {  // split-K partial-tile workspace, grown on demand
+  double* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitWs* ws) {
   if (g.M == 0 || g.N == 0) return HEFF_OK;
   const bool use_tma = (path == 2) || (path == 0 && tma_ok(g));
   if (path == 2 && !tma_ok(g)) return set_err(HEFF_EUNSUPPORTED, "TMA GEMM path needs 16-byte rows/alignment");
@@ -183,16 +211,42 @@ static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch) {
       g.mapB_rows = g.N;
     }
     const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + kBN - 1) / kBN);
-    const int grid = (int)std::min<int64_t>(tiles, g_num_sms);
-    const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(g.C) & 15) == 0) ? 1 : 0;
+    const int64_t ktiles = (g.K + kGemmBK - 1) / kGemmBK;
+    int splits = ws ? choose_splits(tiles, ktiles) : 1;
+    double* Cdst = g.C;
+    const int64_t split_stride = g.M * g.ldc;
+    if (splits > 1) {
+      const size_t need = sizeof(double) * (size_t)splits * (size_t)split_stride;
+      if (ws->bytes < need) {
+        cudaFree(ws->ptr);
+        ws->ptr = nullptr;
+        ws->bytes = 0;
+        if (cudaMalloc(&ws->ptr, need) != cudaSuccess) {
+          cudaGetLastError();
+          splits = 1;  // no room for partials: run unsplit
+        } else {
+          ws->bytes = need;
+        }
+      }
+      if (splits > 1) Cdst = ws->ptr;
+    }
+    const int grid = (int)std::min<int64_t>(tiles * splits, g_num_sms);
+    const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(Cdst) & 15) == 0) ? 1 : 0;
     if (g.b_kmajor) {
       auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, true>;
-      k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec);
+      k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(g.mapA, g.mapB, Cdst, g.ldc, (int)g.M, (int)g.N, (int)g.K,
+                                                          kGroupM, vec, splits, split_stride);
     } else {
       auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>;
-      k<<<grid, CfgNN::kThreads, CfgNN::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec);
+      k<<<grid, CfgNN::kThreads, CfgNN::kSmemBytes, s>>>(g.mapA, g.mapB, Cdst, g.ldc, (int)g.M, (int)g.N, (int)g.K,
+                                                          kGroupM, vec, splits, split_stride);
+    }
+    if (splits > 1) {
+      CK(cudaGetLastError());
+      if (nlaunch) ++*nlaunch;
+      const int64_t total = g.M * g.N;
+      const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * (int64_t)g_num_sms, (total + 255) / 256));
+      splitk_reduce_kernel<<<rgrid, 256, 0, s>>>(Cdst, splits, split_stride, g.C, g.ldc, (int)g.M, (int)g.N);
     }
   } else {
     dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64));
@@ -253,6 +307,7 @@ struct heff_plan_s {
   double *V1 = nullptr, *V3 = nullptr;
   GemmOp gA, gD;
   Csr csrA, csrB;
+  SplitWs splitws;
   // e2e staging
   double *stage_in = nullptr, *stage_out = nullptr;
   // Lanczos
@@ -329,7 +384,7 @@ static int build_mpo_csr(heff_plan_s* p) {
             for (int64_t w2 = 0; w2 < kR; ++w2) {
               const double v = Wc(w, s1p, s1, s2p, s2, w2);
               if (v != 0.0) {
-                cl.push_back((int)((s1 * d2 + s2) * kR + w2));
+                cl.push_back((int)((s1 * d2 + s2) * kMpoCols * kR + w2));  // shared-memory offset, see mpo.cuh
                 vl.push_back(v);
               }
             }
@@ -366,6 +421,7 @@ extern "C" int heff_destroy(heff_plan p) {
   cudaFree(p->stage_in); cudaFree(p->stage_out);
   cudaFree(p->basis); cudaFree(p->work); cudaFree(p->full); cudaFree(p->gather);
   cudaFree(p->partial); cudaFree(p->scal);
+  cudaFree(p->splitws.ptr);
   free_csr(p->csrA);
   free_csr(p->csrB);
   for (auto& e : p->prof_ev) cudaEventDestroy(e);
@@ -567,10 +623,10 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     p->g1.A = p->L + a0 * d.kL * d.mL;
     p->g1.B = psi;
     p->g1.C = p->T1;
-    CKR(launch_gemm(p->g1, p->gemm_path, s, nl));
+    CKR(launch_gemm(p->g1, p->gemm_path, s, nl, &p->splitws));
     CKR(prof_mark(p, 1, s));
     dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
-    mpo_orderA_kernel<<<grid, kMpoCols, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
+    mpo_orderA_kernel<<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
                                                        p->csrA.d_col, p->csrA.d_val);
     CK(cudaGetLastError());
     ++*nl;
@@ -578,7 +634,7 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     p->g4.M = rows * d.d1 * d.d2;
     p->g4.A = p->T3;
     p->g4.C = out + a0 * d.d1 * d.d2 * d.mR;
-    CKR(launch_gemm(p->g4, p->gemm_path, s, nl));
+    CKR(launch_gemm(p->g4, p->gemm_path, s, nl, &p->splitws));
     CKR(prof_mark(p, 3, s));
   }
   return HEFF_OK;
@@ -590,16 +646,16 @@ static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStre
   const size_t mpo_smem = sizeof(double) * dd * d.kR * kMpoCols;
   CKR(prof_mark(p, 0, s));
   p->gA.A = psi;
-  CKR(launch_gemm(p->gA, p->gemm_path, s, nl));
+  CKR(launch_gemm(p->gA, p->gemm_path, s, nl, &p->splitws));
   CKR(prof_mark(p, 1, s));
   dim3 grid((unsigned)((p->nb + kMpoCols - 1) / kMpoCols), (unsigned)d.mL);
-  mpo_orderB_kernel<<<grid, kMpoCols, mpo_smem, s>>>(p->V1, p->V3, d.mL, p->nb, dd, (int)d.kR, (int)d.kL,
+  mpo_orderB_kernel<<<grid, kMpoThreads, mpo_smem, s>>>(p->V1, p->V3, d.mL, p->nb, dd, (int)d.kR, (int)d.kL,
                                                      p->csrB.d_rowptr, p->csrB.d_col, p->csrB.d_val);
   CK(cudaGetLastError());
   ++*nl;
   CKR(prof_mark(p, 2, s));
   p->gD.C = out;
-  CKR(launch_gemm(p->gD, p->gemm_path, s, nl));
+  CKR(launch_gemm(p->gD, p->gemm_path, s, nl, &p->splitws));
   CKR(prof_mark(p, 3, s));
   return HEFF_OK;
 }

@@ -13,61 +13,104 @@
 #pragma once
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace heff {
 
-constexpr int kMpoCols = 128;     // b (or b') columns per block = threads per block
+constexpr int kMpoCols = 128;     // b (or b') columns per block
+constexpr int kMpoSplit = 4;      // threads per column (each computes every kMpoSplit-th output row)
+constexpr int kMpoThreads = kMpoCols * kMpoSplit;
 constexpr int kMpoMaxRows = 200;  // k d1 d2 rows staged in shared memory (<= 200 KB)
 
 // Order A.  T1: [mL][nin][mR] with nin = kL d1 d2 (rows (w,s1,s2));
 //           T3: [mL][nout][mR] with nout = d1 d2 kR (rows (s1',s2',w2)).
-__global__ void __launch_bounds__(kMpoCols) mpo_orderA_kernel(const double* __restrict__ T1, double* __restrict__ T3,
+// Block (b-tile, a'): the nin x width input tile arrives by nin 1-D bulk async copies
+// (one thread issues them, one mbarrier counts the bytes), so the whole tile is in flight
+// at once; odd row pitches fall back to plain coalesced loads.
+__global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* __restrict__ T1, double* __restrict__ T3,
                                                               int64_t mR, int nin, int nout,
                                                               const int* __restrict__ rowptr,
                                                               const int* __restrict__ col,
                                                               const double* __restrict__ val) {
-  extern __shared__ double s_in[];  // [nin][kMpoCols]
+  extern __shared__ __align__(16) double s_in[];  // [nin][kMpoCols]
+  __shared__ uint64_t bar;
   const int64_t ap = blockIdx.y;
-  const int64_t b = (int64_t)blockIdx.x * kMpoCols + threadIdx.x;
-  const bool ok = b < mR;
-  const double* in = T1 + ap * nin * mR;
-  double* out = T3 + ap * nout * mR;
-  for (int r = 0; r < nin; ++r) s_in[r * kMpoCols + threadIdx.x] = ok ? __ldcs(in + r * mR + b) : 0.0;
-  __syncthreads();
-  if (!ok) return;
-  for (int o = 0; o < nout; ++o) {
+  const int64_t b0 = (int64_t)blockIdx.x * kMpoCols;
+  const int width = (int)min((int64_t)kMpoCols, mR - b0);
+  const double* in = T1 + ap * nin * mR + b0;
+  double* out = T3 + ap * nout * mR + b0;
+  const bool bulk = ((mR & 1) == 0) && ((width & 1) == 0);
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&bar, (uint32_t)(nin * width * 8));
+      for (int r = 0; r < nin; ++r) bulk_load(s_in + r * kMpoCols, in + r * mR, (uint32_t)(width * 8), &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
+    for (int e = threadIdx.x; e < nin * kMpoCols; e += kMpoThreads) {
+      const int r = e / kMpoCols, c = e - r * kMpoCols;
+      if (c < width) s_in[e] = __ldcs(in + r * mR + c);
+    }
+    __syncthreads();
+  }
+  const int t = threadIdx.x % kMpoCols;
+  if (t >= width) return;
+  for (int o = threadIdx.x / kMpoCols; o < nout; o += kMpoSplit) {
     double acc = 0.0;
     const int e1 = __ldg(rowptr + o + 1);
-    for (int e = __ldg(rowptr + o); e < e1; ++e) acc = fma(__ldg(val + e), s_in[__ldg(col + e) * kMpoCols + threadIdx.x], acc);
-    __stcs(out + o * mR + b, acc);
+    for (int e = __ldg(rowptr + o); e < e1; ++e) acc = fma(__ldg(val + e), s_in[__ldg(col + e) * kMpoCols + t], acc);
+    __stcs(out + o * mR + t, acc);
   }
 }
 
 // Order B on a b'-shard of width nb.  V1: [mL][d1 d2][nb][kR]; V3: [kL][mL][d1 d2][nb].
-// CSR rows o = (w,s1',s2') (nout = kL d1 d2), columns c = (s1,s2,w2) (nin = d1 d2 kR).
-__global__ void __launch_bounds__(kMpoCols) mpo_orderB_kernel(const double* __restrict__ V1, double* __restrict__ V3,
+// CSR rows o = (w,s1',s2') (nout = kL d1 d2).  The host stores each CSR column already as
+// its shared-memory offset (s*kMpoCols + 0)*kR + w2 for input (s = (s1,s2), w2), so the
+// [s][b'][w2] tile lands by dd bulk copies of contiguous width*kR runs.
+__global__ void __launch_bounds__(kMpoThreads) mpo_orderB_kernel(const double* __restrict__ V1, double* __restrict__ V3,
                                                               int64_t mL, int64_t nb, int dd, int kR, int kL,
                                                               const int* __restrict__ rowptr,
                                                               const int* __restrict__ col,
                                                               const double* __restrict__ val) {
-  extern __shared__ double s_in[];  // [(s1 s2) kR + w2][kMpoCols]
+  extern __shared__ __align__(16) double s_in[];  // [(s1 s2)][kMpoCols][kR]
+  __shared__ uint64_t bar;
   const int64_t a = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * kMpoCols;
-  const int64_t width = min((int64_t)kMpoCols, nb - b0);
-  for (int s = 0; s < dd; ++s) {
-    const double* src = V1 + ((a * dd + s) * nb + b0) * kR;  // contiguous [width][kR]
-    for (int e = threadIdx.x; e < kMpoCols * kR; e += kMpoCols) {
-      const int bl = e / kR, w2 = e - bl * kR;
-      s_in[(s * kR + w2) * kMpoCols + bl] = (bl < width) ? __ldcs(src + e) : 0.0;
+  const int width = (int)min((int64_t)kMpoCols, nb - b0);
+  const int run = width * kR;  // doubles per (s1,s2) block
+  const bool bulk = (((nb * kR) & 1) == 0) && (((b0 * kR) & 1) == 0) && ((run & 1) == 0);
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      fence_barrier_init();
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&bar, (uint32_t)(dd * run * 8));
+      for (int s = 0; s < dd; ++s)
+        bulk_load(s_in + s * kMpoCols * kR, V1 + ((a * dd + s) * nb + b0) * kR, (uint32_t)(run * 8), &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
+    for (int s = 0; s < dd; ++s) {
+      const double* src = V1 + ((a * dd + s) * nb + b0) * kR;
+      for (int e = threadIdx.x; e < run; e += kMpoThreads) s_in[s * kMpoCols * kR + e] = __ldcs(src + e);
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  const int bl = threadIdx.x;
+  const int bl = threadIdx.x % kMpoCols;
   if (bl >= width) return;
   const int nout = kL * dd;
-  for (int o = 0; o < nout; ++o) {
+  const double* my = s_in + bl * kR;
+  for (int o = threadIdx.x / kMpoCols; o < nout; o += kMpoSplit) {
     double acc = 0.0;
     const int e1 = __ldg(rowptr + o + 1);
-    for (int e = __ldg(rowptr + o); e < e1; ++e) acc = fma(__ldg(val + e), s_in[__ldg(col + e) * kMpoCols + bl], acc);
+    for (int e = __ldg(rowptr + o); e < e1; ++e) acc = fma(__ldg(val + e), my[__ldg(col + e)], acc);
     const int w = o / dd, s = o - w * dd;
     __stcs(V3 + ((w * mL + a) * dd + s) * nb + b0 + bl, acc);
   }
