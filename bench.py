@@ -163,6 +163,8 @@ def main():
     ap.add_argument("--impl", default="heff", choices=["heff", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the b'-sharded NCCL plan even at N=1 (exercises the multi-GPU code path)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -173,6 +175,7 @@ def main():
 
     from heffgen import configs as C
     from paper_2007_14822_b200 import Heff
+    from paper_2007_14822_b200 import dist as hdist
     from paper_2007_14822_b200.heff import OPT_PROFILE, OPT_TOTAL_LAUNCHES, nccl_unique_id
 
     world = env_int("WORLD_SIZE", 1)
@@ -182,28 +185,26 @@ def main():
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
 
     # ---- inputs (seeded, synthetic; generated on the GPU, then broadcast from rank 0)
     x = C.make(args.config, device=dev)
     dims = x.dims
-    if world > 1:
+    if sharded:
         for t in (x.L, x.W1, x.W2, x.R, x.psi):
             dist.broadcast(t, 0)
     mR = dims["mR"]
     flops = C.flops_per_matvec(dims)
     gemm_flops = C.gemm_flops_per_matvec(dims)
-    if world > 1:
-        assert mR % world == 0
-        nb = mR // world
-        lo, hi = rank * nb, (rank + 1) * nb
-        uid_t = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            uid_t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid_t, 0)
-        uid = bytes(uid_t.cpu().tolist())
+    if sharded:
+        lo, hi = hdist.shard_range(mR, world, rank)
+        uid = hdist.broadcast_uid(nccl_unique_id() if rank == 0 else None, device=dev)
         Rg = x.R[lo:hi].contiguous()
         plan = Heff(x.L, x.W1, x.W2, Rg, dist=dict(nranks=world, rank=rank, b_lo=lo, b_hi=hi, uid=uid))
         psi0 = x.psi[..., lo:hi].contiguous()
@@ -215,7 +216,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -241,36 +242,34 @@ def main():
     launches = plan.get_option(OPT_TOTAL_LAUNCHES)
     g1_ms, mpo_ms, g4_ms, nrec = plan.last_timings()
     plan.set_option(OPT_PROFILE, 0)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = hdist.max_over_ranks(ms, device=dev) if sharded else ms
     value = args.steps / (ms_max / 1e3)
 
     # ---- e2e: heff_apply_host (pinned host psi in, host out) per step
+    # every rank copies the full psi in (pinned host) and its out-shard back, per step
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
+    if args.e2e_steps > 0:
         hin = x.psi.cpu().pin_memory()
-        hout = torch.empty_like(hin).pin_memory()
+        hout = torch.empty(plan.out_shape, dtype=torch.float64).pin_memory()
         plan.apply_host(hin, hout)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             plan.apply_host(hin, hout)
         el = time.perf_counter() - t0
-        e2e = {"value": args.e2e_steps / el, "unit": "matvec/s", "h2d_bytes_per_step": hin.numel() * 8,
-               "d2h_bytes_per_step": hout.numel() * 8,
-               "what": "heff_apply_host: pinned-host psi -> device, H_eff.psi, device -> pinned-host out"}
-    elif world > 1:
-        e2e = {"value": None, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-               "what": "not measured at N>1 (sharded Lanczos keeps vectors on device)"}
+        if sharded:
+            el = hdist.max_over_ranks(el, device=dev)
+        e2e = {"value": args.e2e_steps / el, "unit": "matvec/s", "h2d_bytes_per_step": hin.numel() * 8 * world,
+               "d2h_bytes_per_step": hout.numel() * 8 * world,
+               "what": "heff_apply_host on every rank: pinned-host psi -> device, H_eff.psi (its b'-shard at N>1), "
+                       "device -> pinned-host out; bytes summed over ranks"}
 
     # ---- roofline of the dominant kernel (a GEMM step; the two GEMMs are ~50/50)
     n_mv = max(1.0, nrec)
     d = dims
     g1_flop = 2.0 * d["mL"] * d["kL"] * d["mL"] * d["d1"] * d["d2"] * d["mR"]
     g4_flop = gemm_flops - g1_flop
-    if world > 1:
+    if sharded:
         g1_flop /= world
         g4_flop /= world
     k1 = ("gemm_first", g1_ms, g1_flop)
@@ -278,11 +277,11 @@ def main():
     dom = max((k1, k4), key=lambda k: k[1])
     per_launch_ms = dom[1] / n_mv
     achieved = dom[2] / (per_launch_ms / 1e3) / 1e12 if per_launch_ms > 0 else None
-    kernel_names = {"gemm_first": "gemm_dmma_tma_kernel NN (L.psi)" if world == 1 else "gemm_dmma_tma_kernel NT (psi.R^T)",
-                    "gemm_last": "gemm_dmma_tma_kernel NT (T3.R^T)" if world == 1 else "gemm_dmma_tma_kernel NN (L.V3)"}
+    kernel_names = {"gemm_first": "gemm_dmma_tma_kernel NT (psi.R_g^T)" if sharded else "gemm_dmma_tma_kernel NN (L.psi)",
+                    "gemm_last": "gemm_dmma_tma_kernel NN (L.V3)" if sharded else "gemm_dmma_tma_kernel NT (T3.R^T)"}
     roofline = {"bound": "tensor", "kernel": kernel_names[dom[0]], "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
-                "traffic": load_ncu_traffic(dom[0] + ("_A" if world == 1 else "_B")),
+                "traffic": load_ncu_traffic(dom[0] + ("_B" if sharded else "_A")),
                 "peak_source": "derived FP64 DMMA peak 148 SM x 128 flop/clk x 1.965 GHz = 37.2 TF/s (no FP64 entry "
                                "in MEASURED_PEAKS.json); DMMA microbenchmark 37.16 TF/s sustained",
                 "per_launch_ms": per_launch_ms,
@@ -304,14 +303,14 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_name(args.config, dims), **dims, "order": order,
-                           "parallelism": f"b'-shard x{world}" if world > 1 else "single GPU",
+                           "parallelism": f"b'-shard x{world} (NCCL)" if sharded else "single GPU",
                            "flops_per_matvec": flops, "l2": "inputs larger than L2 (psi 0.54 GB, L and R 2.7 GB each)",
                            "step": "one Lanczos iteration (matvec + CGS2 + norm + host tridiagonal)"},
                 "tflops": value * flops / 1e12, "frac_fp64_peak": value * flops / 1e12 / (FP64_PEAK_TFLOPS * world),
                 "lanczos": {"energy": res.energy, "iters": res.iters},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
         dist.destroy_process_group()
     return 0

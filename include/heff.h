@@ -124,6 +124,11 @@ const char* heff_last_error(void);
 /* Device bytes the plan allocates for matvec workspace (excluding the Lanczos basis). */
 size_t heff_workspace_bytes(const heff_dims* dims, const heff_dist* dist);
 
+/* The layout map applied after the all-gather of b'-shards: src [P][rows][nb] ->
+ * dst [rows][P*nb] (device pointers, no aliasing).  Exposed for tests and for callers
+ * that gather shards themselves.  Asynchronous on `stream`. */
+int heff_relayout_blocked(const double* src, double* dst, int64_t rows, int64_t nb, int P, heff_stream stream);
+
 /* Writes a fresh 128-byte ncclUniqueId (rank 0 calls this, then broadcasts it). */
 int heff_nccl_unique_id(unsigned char uid[128]);
 

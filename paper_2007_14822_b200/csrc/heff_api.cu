@@ -770,6 +770,18 @@ static int matvec_local(heff_plan_s* p, const double* v, double* w, cudaStream_t
   return apply_impl(p, p->full, w, s);
 }
 
+extern "C" int heff_relayout_blocked(const double* src, double* dst, int64_t rows, int64_t nb, int P,
+                                     heff_stream stream) {
+  if (!src || !dst || rows < 0 || nb < 0 || P < 1) return set_err(HEFF_EINVAL, "heff_relayout_blocked: bad argument");
+  if (src == dst) return set_err(HEFF_EINVAL, "heff_relayout_blocked: dst must not alias src");
+  CKR(init_device_once());
+  if (rows * nb == 0) return HEFF_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  relayout_blocked_kernel<<<ew_grid(rows * nb * P), 256, 0, s>>>(src, dst, rows, nb, P);
+  CK(cudaGetLastError());
+  return HEFF_OK;
+}
+
 extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts* o, double* energy, int* iters_done,
                               double* resid_est, heff_stream stream) {
   if (!p || !psi || !o || !energy) return set_err(HEFF_EINVAL, "lanczos_ground: null argument");

@@ -68,15 +68,18 @@ def lib() -> ctypes.CDLL:
         L.heff_set_option.argtypes = [vp, ip, i64]
         L.heff_get_option.argtypes = [vp, ip, ctypes.POINTER(i64)]
         L.heff_last_timings.argtypes = [vp] + [ctypes.POINTER(ctypes.c_float)] * 4
+        L.heff_relayout_blocked.argtypes = [vp, vp, i64, i64, ip, vp]
         for f in ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
-                  "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings"):
+                  "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
+                  "heff_relayout_blocked"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
 
 
 EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy", "heff_last_error",
-            "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings")
+            "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
+            "heff_relayout_blocked")
 
 
 def _check(rc: int):
@@ -96,6 +99,15 @@ def _dev(t: torch.Tensor, name: str) -> torch.Tensor:
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
     return t
+
+
+def relayout_blocked(src: torch.Tensor, P: int, stream=None) -> torch.Tensor:
+    """[P][rows][nb] -> [rows][P*nb] on the device (libheff's post-all-gather map)."""
+    _dev(src, "src")
+    _, rows, nb = src.shape
+    dst = torch.empty((rows, P * nb), dtype=torch.float64, device=src.device)
+    _check(lib().heff_relayout_blocked(src.data_ptr(), dst.data_ptr(), rows, nb, P, _stream(stream)))
+    return dst
 
 
 def nccl_unique_id() -> bytes:

@@ -235,3 +235,25 @@ def test_kernel_launch_count(dev):
     with Heff(x.L, x.W1, x.W2, x.R) as h:
         h.apply(x.psi)
         assert h.get_option(2) >= 3      # GEMM1, fused MPO, GEMM4 (+ split-K reductions)
+
+
+def test_relayout_kernel(dev):
+    from paper_2007_14822_b200 import dist as hdist
+    from paper_2007_14822_b200.heff import relayout_blocked
+    for P, rows, nb in ((4, 37, 33), (8, 64, 512), (1, 5, 7)):
+        src = torch.randn(P, rows, nb, dtype=torch.float64, device=dev)
+        assert torch.equal(relayout_blocked(src, P), hdist.blocked_to_natural(src, P))
+
+
+def test_sharded_plan_matvec_full_c3_with_nccl(dev, orc):
+    """A communicating 1-rank plan computes the full out through order B (all-gather path
+    is the identity at P = 1); compare with the oracle at C3."""
+    from paper_2007_14822_b200 import Heff, nccl_unique_id
+    x = C.make("c3")
+    L, W1, W2, R, psi = x.numpy()
+    ref = orc.heff_apply(L, W1, W2, R, psi)
+    xd = x.to(dev)
+    with Heff(xd.L, xd.W1, xd.W2, xd.R, dist=dict(nranks=1, rank=0, b_lo=0, b_hi=R.shape[0],
+                                                   uid=nccl_unique_id())) as h:
+        out = h.apply(xd.psi).cpu().numpy()
+    assert rel(out, ref) <= MATVEC_TOL
