@@ -2,7 +2,10 @@
 // normalisation, all HBM-streaming with deterministic warp-shuffle reductions
 // (fixed grid, fixed summation order, no fp64 atomics).
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
+
+namespace cg = cooperative_groups;
 
 namespace heff {
 
@@ -118,6 +121,105 @@ __global__ void scale_kernel(const double* __restrict__ x, const double* __restr
 __global__ void lanczos_alpha_kernel(const double* __restrict__ c1, const double* __restrict__ c2, int j,
                                      double* __restrict__ alpha) {
   if (threadIdx.x == 0 && blockIdx.x == 0) alpha[j] = c1[j] + c2[j];
+}
+
+// ------------------------------------------------------------------------------------
+// One fused CGS2 Lanczos step (single device, no communicator), cooperative launch.
+// Given w = H v_j and the basis V[0..j):
+//   c1 = V^T w ; w -= V c1 ; c2 = V^T w ; w -= V c2 ; alpha = c1[j-1] + c2[j-1] ;
+//   beta = ||w|| ; vnext = w / beta   (vnext may be null)
+// Each block owns one contiguous chunk of the vectors for all phases; the three
+// grid-wide reductions are per-block partials + a grid sync + the same fixed-order sum in
+// every block (deterministic, no atomics).  Replaces ~16 launches per step with one.
+// partial: [2*jmax + 1][gridDim.x].
+// ------------------------------------------------------------------------------------
+constexpr int kStepThreads = 512;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int k = 0; k < kStepThreads / 32; ++k) t += red[k];
+  return t;
+}
+
+// partial[q][b] <- block b's sum over its chunk of V[q][i] w[i], q < j (8 vectors per pass)
+__device__ __forceinline__ void chunk_dots(const double* __restrict__ V, int64_t ldv, int j,
+                                           const double* __restrict__ w, int64_t lo, int64_t hi,
+                                           double* __restrict__ partial, double* red) {
+  for (int q0 = 0; q0 < j; q0 += kDotQ) {
+    const int nq = min(kDotQ, j - q0);
+    double acc[kDotQ];
+#pragma unroll
+    for (int q = 0; q < kDotQ; ++q) acc[q] = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) {
+      const double x = w[i];
+#pragma unroll
+      for (int q = 0; q < kDotQ; ++q)
+        if (q < nq) acc[q] = fma(V[(q0 + q) * ldv + i], x, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kDotQ; ++q)
+      if (q < nq) {
+        const double s = block_sum(acc[q], red);
+        if (threadIdx.x == 0) partial[(q0 + q) * gridDim.x + blockIdx.x] = s;
+      }
+  }
+}
+
+__global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* __restrict__ V, int64_t ldv, int j,
+                                                                  double* __restrict__ w, int64_t n,
+                                                                  double* __restrict__ partial, int jmax,
+                                                                  double* __restrict__ c1, double* __restrict__ c2,
+                                                                  double* __restrict__ alpha, double* __restrict__ beta,
+                                                                  double* __restrict__ invb,
+                                                                  double* __restrict__ vnext) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double s_c[];  // [j]
+  __shared__ double red[kStepThreads / 32];
+  const int G = gridDim.x;
+  const int64_t chunk = ((n + G - 1) / G + 1) / 2 * 2;
+  const int64_t lo = min(n, (int64_t)blockIdx.x * chunk), hi = min(n, lo + chunk);
+  double* p1 = partial;
+  double* p2 = partial + (int64_t)jmax * G;
+  double* p3 = partial + 2 * (int64_t)jmax * G;
+  for (int pass = 0; pass < 2; ++pass) {
+    double* pp = pass ? p2 : p1;
+    double* cc = pass ? c2 : c1;
+    chunk_dots(V, ldv, j, w, lo, hi, pp, red);
+    grid.sync();
+    for (int q = threadIdx.x; q < j; q += kStepThreads) {  // same fixed-order sum in every block
+      double s = 0.0;
+      for (int b = 0; b < G; ++b) s += pp[q * G + b];
+      s_c[q] = s;
+      if (blockIdx.x == 0) cc[q] = s;
+    }
+    __syncthreads();
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) {
+      double x = w[i];
+      for (int q = 0; q < j; ++q) x = fma(-s_c[q], V[q * ldv + i], x);
+      w[i] = x;
+    }
+  }
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) acc = fma(w[i], w[i], acc);
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) p3[blockIdx.x] = s;
+  grid.sync();
+  double nrm2 = 0.0;
+  for (int b = 0; b < G; ++b) nrm2 += p3[b];  // every thread, same order
+  const double bt = sqrt(nrm2);
+  const double ib = bt > 0.0 ? 1.0 / bt : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    alpha[j - 1] = c1[j - 1] + c2[j - 1];
+    beta[j - 1] = bt;
+    invb[j - 1] = ib;
+  }
+  if (vnext)
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) vnext[i] = w[i] * ib;
 }
 
 }  // namespace heff

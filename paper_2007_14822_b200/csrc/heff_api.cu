@@ -278,6 +278,7 @@ static int init_device_once() {
   CK(cudaFuncSetAttribute(gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNN::kSmemBytes));
   CK(cudaFuncSetAttribute(mpo_orderA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   CK(cudaFuncSetAttribute(mpo_orderB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   done = true;
   return HEFF_OK;
@@ -695,6 +696,8 @@ extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_
 }
 
 // --------------------------------------------------------------------------- Lanczos
+static int g_step_grid = 0;  // co-resident blocks of cgs2_step_kernel (cooperative launch)
+
 static int reduce_grid(int64_t n) {
   const int64_t per = (int64_t)kRedThreads * 2 * 8;  // >= 8 pairs per thread
   return (int)std::max<int64_t>(1, std::min<int64_t>(4 * (int64_t)g_num_sms, (n + per - 1) / per));
@@ -798,7 +801,8 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     p->basis_cap = 0;
     CK(cudaMalloc(&p->basis, sizeof(double) * ldv * cap));
     p->ldp = reduce_grid(n);
-    CK(cudaMalloc(&p->partial, sizeof(double) * (size_t)(cap + kDotQ) * p->ldp));
+    const size_t pcols = std::max<size_t>((size_t)p->ldp, (size_t)8 * g_num_sms);  // also the fused step's grid
+    CK(cudaMalloc(&p->partial, sizeof(double) * (size_t)(2 * cap + kDotQ + 1) * pcols));
     CK(cudaMalloc(&p->scal, sizeof(double) * 6 * (size_t)(cap + 1)));
     p->basis_cap = cap;
     p->ldv = ldv;
@@ -832,9 +836,35 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   std::vector<double> ha(cap), hb(cap);
   double theta = 0.0, ylast = 0.0, hnorm = 0.0;
   int j_done = 0;
+  // fused single-launch CGS2 step when there is no communicator and the coefficients fit
+  // (launch-bound sizes only: above ~2M elements the separate vectorised kernels stream faster)
+  const bool fused = (p->comm == nullptr) && (cap <= 4096) && (n <= (int64_t(1) << 21) || getenv("HEFF_FUSED_STEP")) &&
+                     getenv("HEFF_NO_FUSED_STEP") == nullptr;
+  int step_grid = 0;
+  if (fused) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs2_step_kernel, kStepThreads,
+                                                     sizeof(double) * (size_t)cap));
+    const int64_t want = std::max<int64_t>(1, (n + 4 * kStepThreads - 1) / (4 * kStepThreads));
+    step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * g_num_sms, want));
+  }
   auto step = [&](int j) -> int {  // j = 1-based step: v_j = V[j-1]
     double* vj = V + (int64_t)(j - 1) * ldv;
     CKR(matvec_local(p, vj, w, s));
+    if (fused) {
+      const double* Vc = V;
+      int64_t ldv_ = ldv;
+      int jj = j, jmax = cap;
+      double* partial = p->partial;
+      double* vnext = (j < cap) ? V + (int64_t)j * ldv : nullptr;
+      int64_t nn = n;
+      double* wp = w;
+      void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &alpha, &beta, &invb, &vnext};
+      CK(cudaLaunchCooperativeKernel((const void*)cgs2_step_kernel, dim3(step_grid), dim3(kStepThreads), args,
+                                     sizeof(double) * (size_t)j, s));
+      ++p->total_launches;
+      return HEFF_OK;
+    }
     CKR(multidot(p, V, j, w, n, c1, s));
     CKR(multiaxpy(p, V, j, c1, -1.0, w, n, s));
     CKR(multidot(p, V, j, w, n, c2, s));
