@@ -68,6 +68,34 @@ def model_inputs(Ws: list[np.ndarray], window: int, m: int, seed: int, device="c
                       psi.contiguous(), m_)
 
 
+def model_inputs_terms(Ws_terms: list, window: int, m: int, seed: int, device="cpu") -> list:
+    """Environments of ONE random orthonormal MPS for several MPOs (an MPO sum,
+    P:L739-750).  Ws_terms[t][j] is term t's MPO tensor at site j.  The MPS draws are the
+    same as model_inputs' for the same seed; psi is shared."""
+    N = len(Ws_terms[0])
+    d = Ws_terms[0][0].shape[1]
+    rng = np.random.default_rng(seed)
+    As = env.draw_left_block(rng, window, d, m, device)
+    Bs = env.draw_right_block(rng, N - window - 2, d, m, device)
+    out = []
+    psi = None
+    for Ws in Ws_terms:
+        k = Ws[0].shape[0]
+        tW = [torch.from_numpy(np.ascontiguousarray(W)).to(device) for W in Ws]
+        L = env.build_left_env(As, tW[:window], k, device)
+        R = env.build_right_env(Bs, tW[window + 2:], k, device)
+        if psi is None:
+            psi = random_psi(seed + 1, (L.shape[0], d, d, R.shape[0]), device)
+        out.append(HeffInputs(L.contiguous(), tW[window].contiguous(), tW[window + 1].contiguous(), R.contiguous(),
+                              psi, dict(N=N, window=window, m_cap=m, seed=seed, k=k)))
+    return out
+
+
+def heisenberg_chain_split(N: int, window: int, m: int, seed: int, device="cpu") -> list:
+    """Eq. (1) as the MPO sum [Sz Sz terms, flip terms] (SPEC.md:771's dmrg([H1,H2]) example)."""
+    return model_inputs_terms([[mpo.heisenberg_zz_W()] * N, [mpo.heisenberg_flip_W()] * N], window, m, seed, device)
+
+
 def heisenberg_chain(N: int, window: int, m: int, seed: int, device="cpu") -> HeffInputs:
     W = mpo.heisenberg_chain_W()
     return model_inputs([W] * N, window, m, seed, device, dict(model="heisenberg_chain"))

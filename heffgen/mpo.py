@@ -39,6 +39,30 @@ def heisenberg_chain_W() -> np.ndarray:
     return W
 
 
+def heisenberg_zz_W() -> np.ndarray:
+    """The Sz Sz part of Eq. (1) alone (k = 3): one term of an MPO sum."""
+    k = 3
+    W = np.zeros((k, 2, 2, k))
+    W[2, :, :, 2] = I2
+    W[0, :, :, 0] = I2
+    W[2, :, :, 1] = SZ
+    W[1, :, :, 0] = SZ
+    return W
+
+
+def heisenberg_flip_W() -> np.ndarray:
+    """The 1/2 (S+S- + S-S+) part of Eq. (1) alone (k = 4)."""
+    k = 4
+    W = np.zeros((k, 2, 2, k))
+    W[3, :, :, 3] = I2
+    W[0, :, :, 0] = I2
+    W[3, :, :, 1] = 0.5 * SM
+    W[3, :, :, 2] = 0.5 * SP
+    W[1, :, :, 0] = SP
+    W[2, :, :, 0] = SM
+    return W
+
+
 CYL_WIDTH = 6
 
 

@@ -116,6 +116,19 @@ int heff_apply_host(heff_plan p, const double* psi_host, double* out_host, heff_
 int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts* opts, double* energy, int* iters_done,
                    double* resid_est, heff_stream stream);
 
+/* MPO sums ("loops over them internally as if they were summed"):
+ * a composite plan whose matvec is sum_t H_eff^(t) psi over borrowed term plans (same
+ * mL, d1, d2, mR; single-GPU, non-composite).  The terms must outlive the composite;
+ * heff_destroy(composite) does not destroy them.  Usable with heff_apply,
+ * heff_apply_host, lanczos_ground and heff_set_penalty. */
+int heff_create_sum(heff_plan* out, const heff_plan* terms, int nterms);
+
+/* Excited states by energy penalty: after this call every matvec of `p`
+ * computes H_eff psi + weight * sum_i phi_i <phi_i|psi>.  phis: DEVICE array
+ * [nphi][mL*d1*d2*mR] (copied; may be freed after the call).  nphi = 0 removes the
+ * penalty.  Not supported on b'-sharded plans (HEFF_EUNSUPPORTED). */
+int heff_set_penalty(heff_plan p, const double* phis, int nphi, double weight, heff_stream stream);
+
 int heff_destroy(heff_plan p);
 
 /* Thread-local message describing the last failure on this thread ("" if none). */

@@ -124,6 +124,26 @@ def heff_apply_B(L, W1, W2, R, psi, cols: tuple[int, int] | None = None) -> np.n
     return out
 
 
+def heff_apply_penalty(L, W1, W2, R, psi, phis, weight: float) -> np.ndarray:
+    """H_eff psi + weight * sum_i phi_i <phi_i|psi> -- the excited-state energy penalty
+    "projectors onto the previous states ... added to the Hamiltonian times an energy
+    penalty" (Sec. 6.2, PAPER.md:752-762).  phis: [nphi, *psi.shape]."""
+    out = heff_apply(L, W1, W2, R, psi)
+    for phi in np.asarray(phis, dtype=np.float64):
+        out += weight * phi * float(np.sum(phi * psi))
+    return out
+
+
+def heff_apply_sum(terms, psi) -> np.ndarray:
+    """sum_t H_eff^(t) psi over (L, W1, W2, R) terms -- an MPO sum "as if they were summed"
+    (Sec. 6.2)."""
+    out = None
+    for (L, W1, W2, R) in terms:
+        y = heff_apply(L, W1, W2, R, psi)
+        out = y if out is None else out + y
+    return out
+
+
 def tridiag_lowest(alpha, beta):
     alpha = _c(alpha)
     j = alpha.size

@@ -27,9 +27,10 @@ __global__ void __launch_bounds__(kRedThreads) multidot_partial_kernel(const dou
   double acc[kDotQ];
 #pragma unroll
   for (int q = 0; q < kDotQ; ++q) acc[q] = 0.0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(V) | (uintptr_t)(ldv * 8)) & 15) == 0;
   const int64_t stride = (int64_t)gridDim.x * kRedThreads * 2;
   for (int64_t i = ((int64_t)blockIdx.x * kRedThreads + threadIdx.x) * 2; i < n; i += stride) {
-    if (i + 1 < n) {
+    if (vec && i + 1 < n) {
       const double2 x = __ldg(reinterpret_cast<const double2*>(w + i));
 #pragma unroll
       for (int q = 0; q < kDotQ; ++q)
@@ -39,10 +40,12 @@ __global__ void __launch_bounds__(kRedThreads) multidot_partial_kernel(const dou
           acc[q] = fma(v.y, x.y, acc[q]);
         }
     } else {
-      const double x = w[i];
+      for (int64_t ii = i; ii < min(i + 2, n); ++ii) {
+        const double x = w[ii];
 #pragma unroll
-      for (int q = 0; q < kDotQ; ++q)
-        if (q < nq) acc[q] = fma(V[q * ldv + i], x, acc[q]);
+        for (int q = 0; q < kDotQ; ++q)
+          if (q < nq) acc[q] = fma(V[q * ldv + ii], x, acc[q]);
+      }
     }
   }
   __shared__ double red[kDotQ][kRedThreads / 32];
@@ -91,9 +94,10 @@ __global__ void __launch_bounds__(256) multiaxpy_kernel(const double* __restrict
   __shared__ double sc[64];
   if (threadIdx.x < nq) sc[threadIdx.x] = sign * c[threadIdx.x];
   __syncthreads();
+  const bool vec = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(V) | (uintptr_t)(ldv * 8)) & 15) == 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i < n; i += stride) {
-    if (i + 1 < n) {
+    if (vec && i + 1 < n) {
       double2 x = *reinterpret_cast<double2*>(w + i);
       for (int q = 0; q < nq; ++q) {
         const double2 v = __ldcs(reinterpret_cast<const double2*>(V + q * ldv + i));
@@ -102,9 +106,11 @@ __global__ void __launch_bounds__(256) multiaxpy_kernel(const double* __restrict
       }
       *reinterpret_cast<double2*>(w + i) = x;
     } else {
-      double x = w[i];
-      for (int q = 0; q < nq; ++q) x = fma(sc[q], V[q * ldv + i], x);
-      w[i] = x;
+      for (int64_t ii = i; ii < min(i + 2, n); ++ii) {
+        double x = w[ii];
+        for (int q = 0; q < nq; ++q) x = fma(sc[q], V[q * ldv + ii], x);
+        w[ii] = x;
+      }
     }
   }
 }

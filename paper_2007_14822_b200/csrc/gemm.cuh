@@ -54,7 +54,7 @@ template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR>
 __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::kThreads, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store,
-                         int splits, int64_t split_stride) {
+                         int splits, int64_t split_stride, int accumulate) {
   using Cfg = TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>;
   constexpr int MI = WM / 8, NJ = WN / 8;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -182,26 +182,32 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
       for (int j = 0; j < NJ; ++j) {
         const int col = nb * BN + wn0 + 8 * j + 2 * t;
         if (vec_store && col + 1 < N) {
-          *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+          double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+          if (accumulate) {
+            const double2 o = *reinterpret_cast<const double2*>(crow + col);
+            v.x += o.x;
+            v.y += o.y;
+          }
+          *reinterpret_cast<double2*>(crow + col) = v;
         } else {
-          if (col < N) crow[col] = acc[i][j][0];
-          if (col + 1 < N) crow[col + 1] = acc[i][j][1];
+          if (col < N) crow[col] = acc[i][j][0] + (accumulate ? crow[col] : 0.0);
+          if (col + 1 < N) crow[col + 1] = acc[i][j][1] + (accumulate ? crow[col + 1] : 0.0);
         }
       }
     }
   }
 }
 
-// C[r][c] = sum_s W[s][r][c] over the split-K partial tiles, in fixed order (deterministic).
+// C[r][c] (+)= sum_s W[s][r][c] over the split-K partial tiles, in fixed order (deterministic).
 __global__ void splitk_reduce_kernel(const double* __restrict__ W, int splits, int64_t split_stride,
-                                     double* __restrict__ C, int64_t ldc, int M, int N) {
+                                     double* __restrict__ C, int64_t ldc, int M, int N, int accumulate) {
   const int64_t total = (int64_t)M * N;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / N, c = i - r * N;
     const int64_t off = r * ldc + c;
     double acc = W[off];
     for (int s = 1; s < splits; ++s) acc += W[s * split_stride + off];
-    C[off] = acc;
+    C[off] = accumulate ? C[off] + acc : acc;
   }
 }
 
@@ -213,7 +219,7 @@ template <bool B_KMAJOR>
 __global__ void __launch_bounds__(128) gemm_dmma_plain_kernel(const double* __restrict__ A, int64_t lda,
                                                                const double* __restrict__ B, int64_t ldb,
                                                                double* __restrict__ C, int64_t ldc, int M, int N,
-                                                               int K) {
+                                                               int K, int accumulate) {
   constexpr int BM = 64, BN = 64, BK = 16, PITCH = BK + 1;
   __shared__ double sA[BM][PITCH];
   __shared__ double sB[BN][PITCH];  // stored [n][k]
@@ -266,8 +272,9 @@ __global__ void __launch_bounds__(128) gemm_dmma_plain_kernel(const double* __re
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = n0 + wn0 + 8 * j + 2 * t;
-      if (col < N) C[(int64_t)row * ldc + col] = acc[i][j][0];
-      if (col + 1 < N) C[(int64_t)row * ldc + col + 1] = acc[i][j][1];
+      double* c = C + (int64_t)row * ldc + col;
+      if (col < N) c[0] = acc[i][j][0] + (accumulate ? c[0] : 0.0);
+      if (col + 1 < N) c[1] = acc[i][j][1] + (accumulate ? c[1] : 0.0);
     }
   }
 }

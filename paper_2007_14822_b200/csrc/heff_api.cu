@@ -149,6 +149,7 @@ struct GemmOp {
   bool b_kmajor = false;
   double* C = nullptr;
   int64_t ldc = 0;
+  int accumulate = 0;  // C += A.B instead of C = A.B
   // cached TMA maps (rebuilt when A/B pointers change)
   CUtensorMap mapA, mapB;
   const double* mapA_ptr = nullptr;
@@ -235,27 +236,29 @@ static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitW
     if (g.b_kmajor) {
       auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, true>;
       k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(g.mapA, g.mapB, Cdst, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec, splits, split_stride);
+                                                          kGroupM, vec, splits, split_stride, splits > 1 ? 0 : g.accumulate);
     } else {
       auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>;
       k<<<grid, CfgNN::kThreads, CfgNN::kSmemBytes, s>>>(g.mapA, g.mapB, Cdst, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec, splits, split_stride);
+                                                          kGroupM, vec, splits, split_stride, splits > 1 ? 0 : g.accumulate);
     }
     if (splits > 1) {
       CK(cudaGetLastError());
       if (nlaunch) ++*nlaunch;
       const int64_t total = g.M * g.N;
       const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * (int64_t)g_num_sms, (total + 255) / 256));
-      splitk_reduce_kernel<<<rgrid, 256, 0, s>>>(Cdst, splits, split_stride, g.C, g.ldc, (int)g.M, (int)g.N);
+      splitk_reduce_kernel<<<rgrid, 256, 0, s>>>(Cdst, splits, split_stride, g.C, g.ldc, (int)g.M, (int)g.N,
+                                                 g.accumulate);
     }
   } else {
     dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64));
     if (grid.y > 65535) return set_err(HEFF_EUNSUPPORTED, "plain GEMM path: M too large");
     if (g.b_kmajor)
-      gemm_dmma_plain_kernel<true><<<grid, 128, 0, s>>>(g.A, g.lda, g.B, g.ldb, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K);
+      gemm_dmma_plain_kernel<true><<<grid, 128, 0, s>>>(g.A, g.lda, g.B, g.ldb, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
+                                                        g.accumulate);
     else
       gemm_dmma_plain_kernel<false><<<grid, 128, 0, s>>>(g.A, g.lda, g.B, g.ldb, g.C, g.ldc, (int)g.M, (int)g.N,
-                                                         (int)g.K);
+                                                         (int)g.K, g.accumulate);
   }
   CK(cudaGetLastError());
   if (nlaunch) ++*nlaunch;
@@ -294,6 +297,15 @@ struct Csr {
 
 struct heff_plan_s {
   heff_dims dims{};
+  // composite plan (MPO sum): borrowed term plans, applied and summed
+  std::vector<heff_plan_s*> terms;
+  // energy penalty: out += weight * sum_i phi_i <phi_i|psi>
+  double* phis = nullptr;                   // [nphi][ldv_phi], plan-owned copy
+  int nphi = 0;
+  int64_t ldv_phi = 0;
+  double pen_weight = 0.0;
+  double* pen_scratch = nullptr;            // partials [nphi][pen_G] + coefficients [nphi]
+  int pen_G = 0;
   const double *L = nullptr, *R = nullptr;  // borrowed
   std::vector<double> W1h, W2h;             // host copies
   bool sharded = false;                     // order B on a b'-shard
@@ -423,6 +435,7 @@ extern "C" int heff_destroy(heff_plan p) {
   cudaFree(p->basis); cudaFree(p->work); cudaFree(p->full); cudaFree(p->gather);
   cudaFree(p->partial); cudaFree(p->scal);
   cudaFree(p->splitws.ptr);
+  cudaFree(p->phis); cudaFree(p->pen_scratch);
   free_csr(p->csrA);
   free_csr(p->csrB);
   for (auto& e : p->prof_ev) cudaEventDestroy(e);
@@ -613,7 +626,7 @@ extern "C" int heff_last_timings(heff_plan p, float* g1, float* mpo, float* g4, 
 }
 
 // --------------------------------------------------------------------------- the matvec
-static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl) {
+static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl, int accumulate) {
   const heff_dims& d = p->dims;
   const int64_t nin = d.kL * d.d1 * d.d2, nout = d.d1 * d.d2 * d.kR;
   const size_t mpo_smem = sizeof(double) * nin * kMpoCols;
@@ -635,13 +648,14 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     p->g4.M = rows * d.d1 * d.d2;
     p->g4.A = p->T3;
     p->g4.C = out + a0 * d.d1 * d.d2 * d.mR;
+    p->g4.accumulate = accumulate;
     CKR(launch_gemm(p->g4, p->gemm_path, s, nl, &p->splitws));
     CKR(prof_mark(p, 3, s));
   }
   return HEFF_OK;
 }
 
-static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl) {
+static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl, int accumulate) {
   const heff_dims& d = p->dims;
   const int dd = (int)(d.d1 * d.d2);
   const size_t mpo_smem = sizeof(double) * dd * d.kR * kMpoCols;
@@ -656,21 +670,101 @@ static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStre
   ++*nl;
   CKR(prof_mark(p, 2, s));
   p->gD.C = out;
+  p->gD.accumulate = accumulate;
   CKR(launch_gemm(p->gD, p->gemm_path, s, nl, &p->splitws));
   CKR(prof_mark(p, 3, s));
   return HEFF_OK;
 }
 
-static int apply_impl(heff_plan_s* p, const double* psi, double* out, cudaStream_t s) {
+static int64_t vec_len(const heff_plan_s* p);
+static int ew_grid(int64_t n);
+
+// out += weight * Phi (Phi^T psi): the excited-state energy penalty
+static int apply_penalty(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl) {
+  const int64_t n = vec_len(p);
+  const int G = p->pen_G;
+  double* part = p->pen_scratch;
+  double* c = part + (size_t)p->nphi * G;
+  for (int q0 = 0; q0 < p->nphi; q0 += kDotQ) {
+    const int qn = std::min(kDotQ, p->nphi - q0);
+    // psi (caller's buffer, maybe only 8-byte aligned) is the single "w" vector read by the scalar tail
+    multidot_partial_kernel<<<G, kRedThreads, 0, s>>>(p->phis + q0 * p->ldv_phi, p->ldv_phi, qn, psi, n,
+                                                      part + q0 * G, G);
+    ++*nl;
+  }
+  reduce_partial_kernel<<<p->nphi, kRedThreads, 0, s>>>(part, G, G, c, 0, nullptr);
+  ++*nl;
+  for (int q0 = 0; q0 < p->nphi; q0 += 64) {
+    multiaxpy_kernel<<<ew_grid(n), 256, 0, s>>>(p->phis + q0 * p->ldv_phi, p->ldv_phi, std::min(64, p->nphi - q0),
+                                                c + q0, p->pen_weight, out, n);
+    ++*nl;
+  }
+  CK(cudaGetLastError());
+  return HEFF_OK;
+}
+
+static int apply_impl(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int accumulate = 0) {
   if (!psi || !out) return set_err(HEFF_EINVAL, "heff_apply: null psi/out");
   if (psi == out) return set_err(HEFF_EINVAL, "heff_apply: out must not alias psi");
   if ((reinterpret_cast<uintptr_t>(psi) | reinterpret_cast<uintptr_t>(out)) & 7)
     return set_err(HEFF_EINVAL, "heff_apply: psi/out must be 8-byte aligned");
   int nl = 0;
-  int r = p->sharded ? apply_orderB(p, psi, out, s, &nl) : apply_orderA(p, psi, out, s, &nl);
+  int r = HEFF_OK;
+  if (!p->terms.empty()) {
+    for (size_t t = 0; t < p->terms.size() && r == HEFF_OK; ++t) {
+      r = apply_impl(p->terms[t], psi, out, s, (t > 0 || accumulate) ? 1 : 0);
+      nl += p->terms[t]->last_launches;
+    }
+  } else {
+    r = p->sharded ? apply_orderB(p, psi, out, s, &nl, accumulate) : apply_orderA(p, psi, out, s, &nl, accumulate);
+  }
+  if (r == HEFF_OK && p->nphi > 0) r = apply_penalty(p, psi, out, s, &nl);
   p->last_launches = nl;
   p->total_launches += nl;
   return r;
+}
+
+extern "C" int heff_create_sum(heff_plan* out, const heff_plan* terms, int nterms) {
+  if (!out || !terms || nterms < 1) return set_err(HEFF_EINVAL, "heff_create_sum: need >= 1 term plan");
+  *out = nullptr;
+  const heff_dims& d0 = terms[0]->dims;
+  for (int t = 0; t < nterms; ++t) {
+    const heff_plan_s* q = terms[t];
+    if (!q) return set_err(HEFF_EINVAL, "heff_create_sum: null term");
+    if (q->sharded || q->comm || !q->terms.empty())
+      return set_err(HEFF_EUNSUPPORTED, "heff_create_sum: terms must be single-GPU, non-composite plans");
+    if (q->dims.mL != d0.mL || q->dims.mR != d0.mR || q->dims.d1 != d0.d1 || q->dims.d2 != d0.d2)
+      return set_err(HEFF_EINVAL, "heff_create_sum: terms must share mL, d1, d2, mR");
+  }
+  heff_plan_s* p = new heff_plan_s();
+  p->dims = d0;
+  p->terms.assign(terms, terms + nterms);
+  *out = p;
+  return HEFF_OK;
+}
+
+extern "C" int heff_set_penalty(heff_plan p, const double* phis, int nphi, double weight, heff_stream stream) {
+  if (!p || nphi < 0 || (nphi > 0 && !phis)) return set_err(HEFF_EINVAL, "heff_set_penalty: bad argument");
+  if (p->sharded) return set_err(HEFF_EUNSUPPORTED, "heff_set_penalty: not supported on b'-sharded plans");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaFree(p->phis);
+  cudaFree(p->pen_scratch);
+  p->phis = nullptr;
+  p->pen_scratch = nullptr;
+  p->nphi = 0;
+  if (nphi == 0) return HEFF_OK;
+  CKR(init_device_once());
+  const int64_t n = vec_len(p);
+  p->ldv_phi = (n + 31) / 32 * 32;
+  p->pen_G = (int)std::max<int64_t>(1, std::min<int64_t>(4 * (int64_t)g_num_sms, (n + 4095) / 4096));
+  CK(cudaMalloc(&p->phis, sizeof(double) * (size_t)nphi * p->ldv_phi));
+  CK(cudaMalloc(&p->pen_scratch, sizeof(double) * (size_t)nphi * (p->pen_G + 1)));
+  CK(cudaMemset2DAsync(p->phis, sizeof(double) * p->ldv_phi, 0, sizeof(double) * p->ldv_phi, nphi, s));
+  CK(cudaMemcpy2DAsync(p->phis, sizeof(double) * p->ldv_phi, phis, sizeof(double) * n, sizeof(double) * n, nphi,
+                       cudaMemcpyDeviceToDevice, s));
+  p->nphi = nphi;
+  p->pen_weight = weight;
+  return HEFF_OK;
 }
 
 extern "C" int heff_apply(heff_plan p, const double* psi, double* out, heff_stream stream) {

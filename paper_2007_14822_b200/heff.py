@@ -69,9 +69,11 @@ def lib() -> ctypes.CDLL:
         L.heff_get_option.argtypes = [vp, ip, ctypes.POINTER(i64)]
         L.heff_last_timings.argtypes = [vp] + [ctypes.POINTER(ctypes.c_float)] * 4
         L.heff_relayout_blocked.argtypes = [vp, vp, i64, i64, ip, vp]
+        L.heff_create_sum.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), ip]
+        L.heff_set_penalty.argtypes = [vp, vp, ip, ctypes.c_double, vp]
         for f in ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
-                  "heff_relayout_blocked"):
+                  "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -79,7 +81,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy", "heff_last_error",
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
-            "heff_relayout_blocked")
+            "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty")
 
 
 def _check(rc: int):
@@ -169,6 +171,20 @@ class Heff:
                                  W2.data_ptr(), R.data_ptr(), pdist, _stream(stream)))
         self._h = h
 
+    def set_penalty(self, phis: torch.Tensor | None, weight: float = 0.0, stream=None):
+        """Energy penalty: matvec becomes H psi + weight * sum_i phi_i <phi_i|psi>.
+        phis: [nphi, *psi_shape] float64 CUDA tensor (copied), or None to remove."""
+        if phis is None:
+            _check(lib().heff_set_penalty(self._h, None, 0, 0.0, _stream(stream)))
+            return
+        _dev(phis, "phis")
+        n = 1
+        for x in self.psi_shape:
+            n *= x
+        if phis.numel() % n:
+            raise ValueError("phis must hold whole psi-shaped vectors")
+        _check(lib().heff_set_penalty(self._h, phis.data_ptr(), phis.numel() // n, float(weight), _stream(stream)))
+
     # -- shapes
     @property
     def psi_shape(self):
@@ -243,6 +259,23 @@ class Heff:
 
     def __exit__(self, *a):
         self.close()
+
+
+class HeffSum(Heff):
+    """sum_t H_eff^(t) over term plans ("as if they were summed").  The terms
+    must share mL, d1, d2, mR and stay alive while the sum is used."""
+
+    def __init__(self, terms: list):
+        if not terms:
+            raise ValueError("need at least one term")
+        self._terms = list(terms)
+        self.dims = dict(terms[0].dims)
+        self.dist = None
+        self.nb = self.dims["mR"]
+        arr = (ctypes.c_void_p * len(terms))(*[t._h.value for t in terms])
+        h = ctypes.c_void_p()
+        _check(lib().heff_create_sum(ctypes.byref(h), arr, len(terms)))
+        self._h = h
 
 
 def workspace_bytes(dims: dict, dist: dict | None = None) -> int:
