@@ -159,6 +159,26 @@ int heff_get_option(heff_plan p, int option, int64_t* value);
 enum { HEFF_OPT_PROFILE = 4, HEFF_OPT_TOTAL_LAUNCHES = 5 };
 int heff_last_timings(heff_plan p, float* ms_gemm_first, float* ms_mpo, float* ms_gemm_last, float* n_recorded);
 
+/* ---- Environment update --------------------------------------
+ * After each local eigensolve a DMRG sweep moves the window one site and grows the
+ * environment by that site (Sec. 6.2; SPEC ProjMPO):
+ *   left:  Lout[a',w',a] = sum A[x',s',a'] L[x',w,x] W[w,s',s,w'] A[x,s,a]
+ *          L [mi][kl][mi], A [mi][d][mo] (left-orthonormal site tensor), W [kl][d][d][kr]
+ *          -> Lout [mo][kr][mo]
+ *   right: Rout[b',w,b]  = sum B[b',s',y'] R[y',w',y] W[w,s',s,w'] B[b,s,y]
+ *          R [mi][kr][mi], B [mo][d][mi] (right-orthonormal), W [kl][d][d][kr]
+ *          -> Rout [mo][kl][mo]
+ * Device pointers, row-major fp64; Lout/Rout must not alias the inputs.  Workspace
+ * (about 2 mi k d mo doubles) lives in a per-thread arena that grows on demand and is
+ * reused by later calls; the call synchronises `stream` before returning. */
+typedef struct {
+  int64_t mi, d, mo, kl, kr;
+} heff_env_dims;
+int heff_env_update_left(const heff_env_dims* dims, const double* L, const double* A, const double* W, double* Lout,
+                         heff_stream stream);
+int heff_env_update_right(const heff_env_dims* dims, const double* R, const double* B, const double* W, double* Rout,
+                          heff_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -455,3 +455,93 @@ int ref_lanczos_heff(const oracle_dims* D, const double* L, const double* W1, co
   return ref_lanczos(oracle_heff_matvec, &c, n, x0, max_iter, tol, mode, energy, x_out, iters_done, alpha_out,
                      beta_out, theta_hist);
 }
+
+/* ---------------------------------------------------------------------------------
+ * Environment update.  SPEC's ProjMPO keeps "L[j] equals
+ * contraction of psi-dag.H.psi over sites 1..j" (projmpo_position
+ * S:747-755); DMRG moves it one site per bond step (Sec. 6.2):
+ *   Lout[a',w',a] = sum_{x',s',w,s,x} A[x',s',a'] L[x',w,x] W[w,s',s,w'] A[x,s,a]
+ *   Rout[b',w,b]  = sum_{y',s',w',s,y} B[b',s',y'] R[y',w',y] W[w,s',s,w'] B[b,s,y]
+ * evaluated as the pairwise `*` chain L*A -> *W -> *A-dagger (and mirrored for R).
+ * Shapes: L [mi][kl][mi], A [mi][d][mo], W [kl][d][d][kr] -> Lout [mo][kr][mo];
+ *         R [mi][kr][mi], B [mo][d][mi], W [kl][d][d][kr] -> Rout [mo][kl][mo].
+ * ------------------------------------------------------------------------------- */
+int ref_env_left(int64_t mi, int64_t d, int64_t mo, int64_t kl, int64_t kr, const double* L, const double* A,
+                 const double* W, double* Lout) {
+  double* X = (double*)calloc((size_t)(mi * kl * d * mo), sizeof(double)); /* [x'][w][s][a]  */
+  double* Y = (double*)calloc((size_t)(mi * d * kr * mo), sizeof(double)); /* [x'][s'][w'][a] */
+  if (!X || !Y) { free(X); free(Y); return -2; }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t xp = 0; xp < mi; ++xp) {
+    for (int64_t w = 0; w < kl; ++w)
+      for (int64_t x = 0; x < mi; ++x) {
+        const double l = L[IDX3(xp, w, x, kl, mi)];
+        double* xr = X + IDX3(xp, w, 0, kl, d * mo);
+        const double* ar = A + x * d * mo;
+        for (int64_t sa = 0; sa < d * mo; ++sa) xr[sa] += l * ar[sa]; /* sa = (s,a) */
+      }
+    for (int64_t sp = 0; sp < d; ++sp)
+      for (int64_t wp = 0; wp < kr; ++wp)
+        for (int64_t w = 0; w < kl; ++w)
+          for (int64_t s = 0; s < d; ++s) {
+            const double c = W[IDX4(w, sp, s, wp, d, d, kr)];
+            double* yr = Y + IDX4(xp, sp, wp, 0, d, kr, mo);
+            const double* xr = X + IDX4(xp, w, s, 0, kl, d, mo);
+            for (int64_t a = 0; a < mo; ++a) yr[a] += c * xr[a];
+          }
+  }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t ap = 0; ap < mo; ++ap)
+    for (int64_t wp = 0; wp < kr; ++wp) {
+      double* o = Lout + IDX3(ap, wp, 0, kr, mo);
+      for (int64_t a = 0; a < mo; ++a) o[a] = 0.0;
+      for (int64_t xp = 0; xp < mi; ++xp)
+        for (int64_t sp = 0; sp < d; ++sp) {
+          const double c = A[IDX3(xp, sp, ap, d, mo)];
+          const double* yr = Y + IDX4(xp, sp, wp, 0, d, kr, mo);
+          for (int64_t a = 0; a < mo; ++a) o[a] += c * yr[a];
+        }
+    }
+  free(X);
+  free(Y);
+  return 0;
+}
+
+int ref_env_right(int64_t mi, int64_t d, int64_t mo, int64_t kl, int64_t kr, const double* R, const double* B,
+                  const double* W, double* Rout) {
+  double* X = (double*)calloc((size_t)(mo * d * kr * mi), sizeof(double)); /* [b'][s'][w'][y] */
+  double* Y = (double*)calloc((size_t)(mo * kl * d * mi), sizeof(double)); /* [b'][w][s][y]   */
+  if (!X || !Y) { free(X); free(Y); return -2; }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t bp = 0; bp < mo; ++bp) {
+    for (int64_t sp = 0; sp < d; ++sp)
+      for (int64_t yp = 0; yp < mi; ++yp) {
+        const double b = B[IDX3(bp, sp, yp, d, mi)];
+        double* xr = X + IDX3(bp, sp, 0, d, kr * mi);
+        const double* rr = R + yp * kr * mi;
+        for (int64_t wy = 0; wy < kr * mi; ++wy) xr[wy] += b * rr[wy]; /* wy = (w',y) */
+      }
+    for (int64_t w = 0; w < kl; ++w)
+      for (int64_t s = 0; s < d; ++s)
+        for (int64_t sp = 0; sp < d; ++sp)
+          for (int64_t wp = 0; wp < kr; ++wp) {
+            const double c = W[IDX4(w, sp, s, wp, d, d, kr)];
+            double* yr = Y + IDX4(bp, w, s, 0, kl, d, mi);
+            const double* xr = X + IDX4(bp, sp, wp, 0, d, kr, mi);
+            for (int64_t y = 0; y < mi; ++y) yr[y] += c * xr[y];
+          }
+  }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t bp = 0; bp < mo; ++bp)
+    for (int64_t w = 0; w < kl; ++w)
+      for (int64_t b = 0; b < mo; ++b) {
+        double acc = 0.0;
+        const double* yr = Y + IDX3(bp, w, 0, kl, d * mi);
+        const double* br = B + b * d * mi;
+        for (int64_t sy = 0; sy < d * mi; ++sy) acc += yr[sy] * br[sy]; /* sy = (s,y) */
+        Rout[IDX3(bp, w, b, kl, mo)] = acc;
+      }
+  free(X);
+  free(Y);
+  return 0;
+}

@@ -60,6 +60,10 @@ def lib():
         _lib.ref_lanczos_heff.argtypes = [ctypes.POINTER(_Dims), dp, dp, dp, dp, dp, ctypes.c_int, ctypes.c_double,
                                           ctypes.c_int, dp, dp, ctypes.POINTER(ctypes.c_int), dp, dp, dp]
         _lib.ref_lanczos_heff.restype = ctypes.c_int
+        i64 = ctypes.c_int64
+        for f in (_lib.ref_env_left, _lib.ref_env_right):
+            f.argtypes = [i64, i64, i64, i64, i64, dp, dp, dp, dp]
+            f.restype = ctypes.c_int
         _lib.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib.oracle_max_threads.restype = ctypes.c_int
     return _lib
@@ -141,6 +145,32 @@ def heff_apply_sum(terms, psi) -> np.ndarray:
     for (L, W1, W2, R) in terms:
         y = heff_apply(L, W1, W2, R, psi)
         out = y if out is None else out + y
+    return out
+
+
+def env_left(L, A, W) -> np.ndarray:
+    """Lout[a',w',a] = sum A[x',s',a'] L[x',w,x] W[w,s',s,w'] A[x,s,a]  (heff_oracle.c ref_env_left)."""
+    L, A, W = map(_c, (L, A, W))
+    mi, kl, _ = L.shape
+    _, d, mo = A.shape
+    kr = W.shape[3]
+    assert A.shape[0] == mi and W.shape[:3] == (kl, d, d)
+    out = np.empty((mo, kr, mo))
+    if lib().ref_env_left(mi, d, mo, kl, kr, _p(L), _p(A), _p(W), _p(out)) != 0:
+        raise RuntimeError("ref_env_left failed")
+    return out
+
+
+def env_right(R, B, W) -> np.ndarray:
+    """Rout[b',w,b] = sum B[b',s',y'] R[y',w',y] W[w,s',s,w'] B[b,s,y]  (heff_oracle.c ref_env_right)."""
+    R, B, W = map(_c, (R, B, W))
+    mi, kr, _ = R.shape
+    mo, d, _ = B.shape
+    kl = W.shape[0]
+    assert B.shape[2] == mi and W.shape[1:] == (d, d, kr)
+    out = np.empty((mo, kl, mo))
+    if lib().ref_env_right(mi, d, mo, kl, kr, _p(R), _p(B), _p(W), _p(out)) != 0:
+        raise RuntimeError("ref_env_right failed")
     return out
 
 

@@ -1025,3 +1025,180 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   if (resid_est) *resid_est = hb[j_done - 1] * std::fabs(y[j_done - 1]);
   return HEFF_OK;
 }
+
+// --------------------------------------------------------------------------- environments
+// NEXT-1: the environment update that follows each eigensolve in a sweep
+// (Sec. 6.2; SPEC ProjMPO S:L737-755), built from the same kernels:
+//   left:  X = L.A (NN GEMM) -> Y = W.X (MPO kernel, single-site CSR) -> Lout = A^T.Y (NN GEMM
+//          on an explicitly transposed A)
+//   right: X = B.R (NN GEMM) -> Y = W.X (MPO kernel) -> Rout = Y.B^T (NT GEMM)
+static thread_local SplitWs t_env_splitws;
+
+// Per-thread workspace of the environment updates, grown on demand and kept (no
+// cudaMalloc/cudaFree per call; each call synchronises its stream before returning).
+struct EnvArena {
+  double* buf = nullptr;
+  size_t bytes = 0;
+  int* rowptr = nullptr;
+  int* col = nullptr;
+  double* val = nullptr;
+  size_t csr_cap = 0;
+};
+static thread_local EnvArena t_env_arena;
+
+static int env_reserve(size_t doubles) {
+  EnvArena& a = t_env_arena;
+  if (a.bytes >= doubles * sizeof(double)) return HEFF_OK;
+  cudaFree(a.buf);
+  a.buf = nullptr;
+  a.bytes = 0;
+  CK(cudaMalloc(&a.buf, doubles * sizeof(double)));
+  a.bytes = doubles * sizeof(double);
+  return HEFF_OK;
+}
+
+static int upload_csr(Csr& c, const std::vector<int>& rp, const std::vector<int>& cl, const std::vector<double>& vl,
+                      cudaStream_t s) {
+  EnvArena& a = t_env_arena;
+  const size_t need = std::max(rp.size(), std::max<size_t>(1, vl.size()));
+  if (a.csr_cap < need) {
+    cudaFree(a.rowptr); cudaFree(a.col); cudaFree(a.val);
+    a.csr_cap = 0;
+    CK(cudaMalloc(&a.rowptr, sizeof(int) * need));
+    CK(cudaMalloc(&a.col, sizeof(int) * need));
+    CK(cudaMalloc(&a.val, sizeof(double) * need));
+    a.csr_cap = need;
+  }
+  CK(cudaMemcpyAsync(a.rowptr, rp.data(), sizeof(int) * rp.size(), cudaMemcpyHostToDevice, s));
+  if (!vl.empty()) {
+    CK(cudaMemcpyAsync(a.col, cl.data(), sizeof(int) * cl.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(a.val, vl.data(), sizeof(double) * vl.size(), cudaMemcpyHostToDevice, s));
+  }
+  c.d_rowptr = a.rowptr;
+  c.d_col = a.col;
+  c.d_val = a.val;
+  c.nrows = (int)rp.size() - 1;
+  c.nnz = (int)vl.size();
+  return HEFF_OK;
+}
+
+static int env_common_check(const heff_env_dims* d, const void* a, const void* b, const void* w, const void* o) {
+  if (!d || !a || !b || !w || !o) return set_err(HEFF_EINVAL, "heff_env_update: null argument");
+  if (d->mi < 1 || d->mo < 1 || d->d < 1 || d->kl < 1 || d->kr < 1)
+    return set_err(HEFF_EINVAL, "heff_env_update: every dimension must be >= 1");
+  if (d->kl * d->d > kMpoMaxRows || d->kr * d->d > kMpoMaxRows)
+    return set_err(HEFF_EUNSUPPORTED, "heff_env_update: k d > %d", kMpoMaxRows);
+  return init_device_once();
+}
+
+extern "C" int heff_env_update_left(const heff_env_dims* dims, const double* L, const double* A, const double* W,
+                                    double* Lout, heff_stream stream) {
+  CKR(env_common_check(dims, L, A, W, Lout));
+  const heff_env_dims d = *dims;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<double> Wh(d.kl * d.d * d.d * d.kr);
+  CK(cudaMemcpyAsync(Wh.data(), W, sizeof(double) * Wh.size(), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // CSR: rows (s',w'), cols (w,s)
+  std::vector<int> rp{0}, cl;
+  std::vector<double> vl;
+  for (int64_t sp = 0; sp < d.d; ++sp)
+    for (int64_t wp = 0; wp < d.kr; ++wp) {
+      for (int64_t w = 0; w < d.kl; ++w)
+        for (int64_t ss = 0; ss < d.d; ++ss) {
+          const double v = Wh[((w * d.d + sp) * d.d + ss) * d.kr + wp];
+          if (v != 0.0) {
+            cl.push_back((int)(w * d.d + ss));
+            vl.push_back(v);
+          }
+        }
+      rp.push_back((int)vl.size());
+    }
+  Csr csr;
+  auto pad = [](int64_t x) { return (x + 31) / 32 * 32; };  // keep every sub-buffer 256-byte aligned
+  const int64_t nX = pad(d.mi * d.kl * d.d * d.mo), nY = pad(d.mi * d.d * d.kr * d.mo), nA = pad(d.mi * d.d * d.mo);
+  CKR(env_reserve((size_t)(nX + nY + nA)));
+  CKR(upload_csr(csr, rp, cl, vl, s));
+  double* X = t_env_arena.buf;
+  double* Y = X + nX;
+  double* At = Y + nY;
+  auto cleanup = [&]() { cudaStreamSynchronize(s); };
+  int r = HEFF_OK;
+  int nl = 0;
+  GemmOp g1;  // X[(x' w), (s a)] = L[(x' w), x] . A[x, (s a)]
+  g1.M = d.mi * d.kl; g1.N = d.d * d.mo; g1.K = d.mi;
+  g1.A = L; g1.lda = d.mi; g1.B = A; g1.ldb = d.d * d.mo; g1.b_kmajor = false; g1.C = X; g1.ldc = d.d * d.mo;
+  r = launch_gemm(g1, 0, s, &nl, &t_env_splitws);
+  if (!r) {
+    const int nin = (int)(d.kl * d.d), nout = (int)(d.d * d.kr);
+    dim3 grid((unsigned)((d.mo + kMpoCols - 1) / kMpoCols), (unsigned)d.mi);
+    mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mo, nin, nout, csr.d_rowptr,
+                                                                                 csr.d_col, csr.d_val);
+    dim3 tg((unsigned)((d.mo + 31) / 32), (unsigned)((d.mi * d.d + 31) / 32));
+    transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, At, d.mi * d.d, d.mo);
+    if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_left: launch failed");
+  }
+  if (!r) {
+    GemmOp g3;  // Lout[a', (w' a)] = At[a', (x' s')] . Y[(x' s'), (w' a)]
+    g3.M = d.mo; g3.N = d.kr * d.mo; g3.K = d.mi * d.d;
+    g3.A = At; g3.lda = d.mi * d.d; g3.B = Y; g3.ldb = d.kr * d.mo; g3.b_kmajor = false; g3.C = Lout;
+    g3.ldc = d.kr * d.mo;
+    r = launch_gemm(g3, 0, s, &nl, &t_env_splitws);
+  }
+  cleanup();
+  return r;
+}
+
+extern "C" int heff_env_update_right(const heff_env_dims* dims, const double* R, const double* B, const double* W,
+                                     double* Rout, heff_stream stream) {
+  CKR(env_common_check(dims, R, B, W, Rout));
+  const heff_env_dims d = *dims;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<double> Wh(d.kl * d.d * d.d * d.kr);
+  CK(cudaMemcpyAsync(Wh.data(), W, sizeof(double) * Wh.size(), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // CSR: rows (w,s), cols (s',w')
+  std::vector<int> rp{0}, cl;
+  std::vector<double> vl;
+  for (int64_t w = 0; w < d.kl; ++w)
+    for (int64_t ss = 0; ss < d.d; ++ss) {
+      for (int64_t sp = 0; sp < d.d; ++sp)
+        for (int64_t wp = 0; wp < d.kr; ++wp) {
+          const double v = Wh[((w * d.d + sp) * d.d + ss) * d.kr + wp];
+          if (v != 0.0) {
+            cl.push_back((int)(sp * d.kr + wp));
+            vl.push_back(v);
+          }
+        }
+      rp.push_back((int)vl.size());
+    }
+  Csr csr;
+  auto pad = [](int64_t x) { return (x + 31) / 32 * 32; };
+  const int64_t nX = pad(d.mo * d.d * d.kr * d.mi), nY = pad(d.mo * d.kl * d.d * d.mi);
+  CKR(env_reserve((size_t)(nX + nY)));
+  CKR(upload_csr(csr, rp, cl, vl, s));
+  double* X = t_env_arena.buf;
+  double* Y = X + nX;
+  auto cleanup = [&]() { cudaStreamSynchronize(s); };
+  int r = HEFF_OK;
+  int nl = 0;
+  GemmOp g1;  // X[(b' s'), (w' y)] = B[(b' s'), y'] . R[y', (w' y)]
+  g1.M = d.mo * d.d; g1.N = d.kr * d.mi; g1.K = d.mi;
+  g1.A = B; g1.lda = d.mi; g1.B = R; g1.ldb = d.kr * d.mi; g1.b_kmajor = false; g1.C = X; g1.ldc = d.kr * d.mi;
+  r = launch_gemm(g1, 0, s, &nl, &t_env_splitws);
+  if (!r) {
+    const int nin = (int)(d.d * d.kr), nout = (int)(d.kl * d.d);
+    dim3 grid((unsigned)((d.mi + kMpoCols - 1) / kMpoCols), (unsigned)d.mo);
+    mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mi, nin, nout, csr.d_rowptr,
+                                                                                 csr.d_col, csr.d_val);
+    if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_right: launch failed");
+  }
+  if (!r) {
+    GemmOp g3;  // Rout[(b' w), b] = Y[(b' w), (s y)] . B[b, (s y)]^T
+    g3.M = d.mo * d.kl; g3.N = d.mo; g3.K = d.d * d.mi;
+    g3.A = Y; g3.lda = d.d * d.mi; g3.B = B; g3.ldb = d.d * d.mi; g3.b_kmajor = true; g3.C = Rout; g3.ldc = d.mo;
+    r = launch_gemm(g3, 0, s, &nl, &t_env_splitws);
+  }
+  cleanup();
+  return r;
+}

@@ -129,4 +129,20 @@ __global__ void relayout_blocked_kernel(const double* __restrict__ src, double* 
   }
 }
 
+// dst[c][r] = src[r][c] for a rows x cols row-major matrix (32x32 shared-memory tiles,
+// coalesced on both sides).  Used once per environment update for A-dagger.
+__global__ void transpose_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t rows, int64_t cols) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = src[r * cols + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * rows + r] = tile[threadIdx.x][k];
+  }
+}
+
 }  // namespace heff

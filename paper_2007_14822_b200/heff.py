@@ -39,6 +39,10 @@ class _Dist(ctypes.Structure):
                 ("b_lo", ctypes.c_int64), ("b_hi", ctypes.c_int64)]
 
 
+class _EnvDims(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("mi", "d", "mo", "kl", "kr")]
+
+
 class _LanczosOpts(ctypes.Structure):
     _fields_ = [("max_iter", ctypes.c_int), ("mode", ctypes.c_int), ("tol", ctypes.c_double),
                 ("alpha_out", ctypes.c_void_p), ("beta_out", ctypes.c_void_p), ("theta_out", ctypes.c_void_p)]
@@ -71,9 +75,12 @@ def lib() -> ctypes.CDLL:
         L.heff_relayout_blocked.argtypes = [vp, vp, i64, i64, ip, vp]
         L.heff_create_sum.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), ip]
         L.heff_set_penalty.argtypes = [vp, vp, ip, ctypes.c_double, vp]
+        L.heff_env_update_left.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
+        L.heff_env_update_right.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         for f in ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
-                  "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty"):
+                  "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
+                  "heff_env_update_right"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -81,7 +88,8 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy", "heff_last_error",
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
-            "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty")
+            "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
+            "heff_env_update_right")
 
 
 def _check(rc: int):
@@ -110,6 +118,36 @@ def relayout_blocked(src: torch.Tensor, P: int, stream=None) -> torch.Tensor:
     dst = torch.empty((rows, P * nb), dtype=torch.float64, device=src.device)
     _check(lib().heff_relayout_blocked(src.data_ptr(), dst.data_ptr(), rows, nb, P, _stream(stream)))
     return dst
+
+
+def env_update_left(L: torch.Tensor, A: torch.Tensor, W: torch.Tensor, stream=None) -> torch.Tensor:
+    """Lout[a',w',a] = sum A[x',s',a'] L[x',w,x] W[w,s',s,w'] A[x,s,a] (heff_env_update_left)."""
+    for t, n in ((L, "L"), (A, "A"), (W, "W")):
+        _dev(t, n)
+    mi, kl, _ = L.shape
+    _, d, mo = A.shape
+    kr = W.shape[3]
+    if tuple(L.shape) != (mi, kl, mi) or tuple(A.shape) != (mi, d, mo) or tuple(W.shape) != (kl, d, d, kr):
+        raise ValueError("expected L[mi,kl,mi], A[mi,d,mo], W[kl,d,d,kr]")
+    out = torch.empty((mo, kr, mo), dtype=torch.float64, device=L.device)
+    _check(lib().heff_env_update_left(ctypes.byref(_EnvDims(mi, d, mo, kl, kr)), L.data_ptr(), A.data_ptr(),
+                                      W.data_ptr(), out.data_ptr(), _stream(stream)))
+    return out
+
+
+def env_update_right(R: torch.Tensor, B: torch.Tensor, W: torch.Tensor, stream=None) -> torch.Tensor:
+    """Rout[b',w,b] = sum B[b',s',y'] R[y',w',y] W[w,s',s,w'] B[b,s,y] (heff_env_update_right)."""
+    for t, n in ((R, "R"), (B, "B"), (W, "W")):
+        _dev(t, n)
+    mi, kr, _ = R.shape
+    mo, d, _ = B.shape
+    kl = W.shape[0]
+    if tuple(R.shape) != (mi, kr, mi) or tuple(B.shape) != (mo, d, mi) or tuple(W.shape) != (kl, d, d, kr):
+        raise ValueError("expected R[mi,kr,mi], B[mo,d,mi], W[kl,d,d,kr]")
+    out = torch.empty((mo, kl, mo), dtype=torch.float64, device=R.device)
+    _check(lib().heff_env_update_right(ctypes.byref(_EnvDims(mi, d, mo, kl, kr)), R.data_ptr(), B.data_ptr(),
+                                       W.data_ptr(), out.data_ptr(), _stream(stream)))
+    return out
 
 
 def nccl_unique_id() -> bytes:
