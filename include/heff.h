@@ -159,6 +159,12 @@ int heff_get_option(heff_plan p, int option, int64_t* value);
 enum { HEFF_OPT_PROFILE = 4, HEFF_OPT_TOTAL_LAUNCHES = 5 };
 int heff_last_timings(heff_plan p, float* ms_gemm_first, float* ms_mpo, float* ms_gemm_last, float* n_recorded);
 
+/* Host-only (no device work): lowest eigenpair of the symmetric tridiagonal T with
+ * diagonal alpha[0..j) and off-diagonal beta[0..j-1) by implicit-shift QL -- the solver
+ * lanczos_ground runs on T_j.  y (optional, j doubles): unit eigenvector, largest-|.|
+ * component positive (reading R14). */
+int heff_tridiag_lowest(int j, const double* alpha, const double* beta, double* theta, double* y);
+
 /* ---- Environment update --------------------------------------
  * After each local eigensolve a DMRG sweep moves the window one site and grows the
  * environment by that site (Sec. 6.2; SPEC ProjMPO):

@@ -1202,3 +1202,13 @@ extern "C" int heff_env_update_right(const heff_env_dims* dims, const double* R,
   cleanup();
   return r;
 }
+
+// Host-only: the tridiagonal eigen-solve lanczos_ground uses (implicit QL, tridiag.h).
+extern "C" int heff_tridiag_lowest(int j, const double* alpha, const double* beta, double* theta, double* y) {
+  if (j < 1 || !alpha || !theta || (j > 1 && !beta)) return set_err(HEFF_EINVAL, "heff_tridiag_lowest: bad argument");
+  std::vector<double> yy(j);
+  if (!tridiag_lowest_vec(j, alpha, beta, theta, yy.data()))
+    return set_err(HEFF_ECUDA, "heff_tridiag_lowest: QL iteration did not converge");
+  if (y) memcpy(y, yy.data(), sizeof(double) * j);
+  return HEFF_OK;
+}

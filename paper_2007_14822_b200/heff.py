@@ -75,12 +75,14 @@ def lib() -> ctypes.CDLL:
         L.heff_relayout_blocked.argtypes = [vp, vp, i64, i64, ip, vp]
         L.heff_create_sum.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), ip]
         L.heff_set_penalty.argtypes = [vp, vp, ip, ctypes.c_double, vp]
+        dp = ctypes.POINTER(ctypes.c_double)
+        L.heff_tridiag_lowest.argtypes = [ip, dp, dp, dp, dp]
         L.heff_env_update_left.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         L.heff_env_update_right.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         for f in ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-                  "heff_env_update_right"):
+                  "heff_env_update_right", "heff_tridiag_lowest"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -89,7 +91,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy", "heff_last_error",
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-            "heff_env_update_right")
+            "heff_env_update_right", "heff_tridiag_lowest")
 
 
 def _check(rc: int):
@@ -118,6 +120,20 @@ def relayout_blocked(src: torch.Tensor, P: int, stream=None) -> torch.Tensor:
     dst = torch.empty((rows, P * nb), dtype=torch.float64, device=src.device)
     _check(lib().heff_relayout_blocked(src.data_ptr(), dst.data_ptr(), rows, nb, P, _stream(stream)))
     return dst
+
+
+def tridiag_lowest(alpha, beta):
+    """libheff's host QL solve of the Lanczos tridiagonal (no GPU needed)."""
+    import numpy as np
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    j = a.size
+    b = np.ascontiguousarray(np.append(np.asarray(beta, dtype=np.float64)[: max(0, j - 1)], 0.0), dtype=np.float64)
+    y = np.empty(j)
+    th = ctypes.c_double()
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(lib().heff_tridiag_lowest(j, a.ctypes.data_as(dp), b.ctypes.data_as(dp), ctypes.byref(th),
+                                     y.ctypes.data_as(dp)))
+    return th.value, y
 
 
 def env_update_left(L: torch.Tensor, A: torch.Tensor, W: torch.Tensor, stream=None) -> torch.Tensor:

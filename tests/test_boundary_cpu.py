@@ -60,3 +60,27 @@ def test_binding_errors_without_gpu():
     t = torch.zeros(2, 2, 2, dtype=torch.float64)
     with pytest.raises(TypeError):
         Heff(t, t.reshape(2, 1, 2, 2), t.reshape(2, 1, 2, 2), t)
+
+
+def test_library_tridiagonal_ql_vs_oracle_bisection_and_numpy(oracle_lib):
+    """P10: libheff's host QL (used by lanczos_ground) vs the oracle's Sturm bisection vs
+    numpy.linalg.eigh, no GPU needed."""
+    import numpy as np
+    from paper_2007_14822_b200 import heff
+    rng = np.random.default_rng(11)
+    for j in (1, 2, 5, 20, 150, 400):
+        a = rng.standard_normal(j) * 3.0
+        b = np.abs(rng.standard_normal(j - 1))
+        th_q, y_q = heff.tridiag_lowest(a, b)
+        th_b, y_b = oracle_lib.tridiag_lowest(a, b)
+        T = np.diag(a) + np.diag(b, 1) + np.diag(b, -1)
+        ev = np.linalg.eigvalsh(T)[0]
+        scale = max(1.0, np.abs(a).max() + 2 * (b.max() if j > 1 else 0))
+        assert abs(th_q - ev) <= 1e-14 * scale * 4
+        assert abs(th_q - th_b) <= 1e-14 * scale * 4
+        assert np.linalg.norm(T @ y_q - th_q * y_q) <= 1e-12 * scale
+        assert abs(abs(np.dot(y_q, y_b)) - 1.0) <= 1e-9
+        assert y_q[np.argmax(np.abs(y_q))] > 0
+    # split matrix (a zero off-diagonal) and a 1x1
+    th, y = heff.tridiag_lowest([2.0, -1.0, 3.0], [0.0, 0.5])
+    assert abs(th - np.linalg.eigvalsh(np.diag([2.0, -1.0, 3.0]) + np.diag([0.0, 0.5], 1) + np.diag([0.0, 0.5], -1))[0]) < 1e-15
