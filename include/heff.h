@@ -159,6 +159,12 @@ int heff_get_option(heff_plan p, int option, int64_t* value);
 enum { HEFF_OPT_PROFILE = 4, HEFF_OPT_TOTAL_LAUNCHES = 5 };
 int heff_last_timings(heff_plan p, float* ms_gemm_first, float* ms_mpo, float* ms_gemm_last, float* n_recorded);
 
+/* The FP64 tensor-core GEMM of the hot path as a primitive: C[M][N] (+)= A[M][K] . op(B),
+ * op(B) = B[K][N] (b_kmajor = 0, row pitch ldb) or B[N][K]^T (b_kmajor = 1).  Row-major
+ * device pointers; accumulate != 0 adds into C; path as HEFF_OPT_GEMM_PATH.  Async. */
+int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb, int b_kmajor,
+              double* C, int64_t ldc, int accumulate, int path, heff_stream stream);
+
 /* Host-only (no device work): lowest eigenpair of the symmetric tridiagonal T with
  * diagonal alpha[0..j) and off-diagonal beta[0..j-1) by implicit-shift QL -- the solver
  * lanczos_ground runs on T_j.  y (optional, j doubles): unit eigenvector, largest-|.|

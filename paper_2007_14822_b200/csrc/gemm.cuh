@@ -50,11 +50,47 @@ struct TmaGemmCfg {
   static_assert(BM <= 256 && (B_KMAJOR ? BN <= 256 : BN % 16 == 0), "TMA box limits");
 };
 
+// Work assignment (hybrid data-parallel + stream-K).  Tiles [0, dp_tiles) are taken whole,
+// round-robin (CTA b: b, b+G, ...), so concurrently running CTAs work on neighbouring
+// tiles of the GROUP_M raster and share L2.  The remaining tiles' (tile, k-block)
+// iterations are cut into G equal contiguous ranges, one per CTA, so the last wave is
+// balanced to the k-block.  A tile whose k-range is split between CTAs is written as
+// partial tiles (slot 2b for CTA b's first stream-K tile, 2b+1 for its last) and summed by
+// streamk_fixup_kernel in CTA order (deterministic).  dp_tiles == tiles: plain persistent.
+struct WorkRange {
+  int64_t it, it_end;  // stream-K iteration range (iterations counted from dp_tiles*ktiles)
+  int tile;            // data-parallel cursor
+  int dp_tiles, ktiles;
+  __device__ WorkRange(int tiles, int dp_tiles_, int ktiles_) : dp_tiles(dp_tiles_), ktiles(ktiles_) {
+    const int64_t total = (int64_t)(tiles - dp_tiles_) * ktiles_;
+    it = total * blockIdx.x / gridDim.x;
+    it_end = total * (blockIdx.x + 1) / gridDim.x;
+    tile = blockIdx.x;
+  }
+  // next (tile, [kb0, kb1)) segment; false when done
+  __device__ bool next(int& t, int& kb0, int& kb1) {
+    if (tile < dp_tiles) {
+      t = tile;
+      kb0 = 0;
+      kb1 = ktiles;
+      tile += gridDim.x;
+      return true;
+    }
+    if (it >= it_end) return false;
+    const int local = (int)(it / ktiles);
+    t = dp_tiles + local;
+    kb0 = (int)(it - (int64_t)local * ktiles);
+    kb1 = (int)min((int64_t)ktiles, (int64_t)kb0 + (it_end - it));
+    it += kb1 - kb0;
+    return true;
+  }
+};
+
 template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR>
 __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::kThreads, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store,
-                         int splits, int64_t split_stride, int accumulate) {
+                         int dp_tiles, double* __restrict__ partial_ws, int accumulate) {
   using Cfg = TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>;
   constexpr int MI = WM / 8, NJ = WN / 8;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -66,10 +102,6 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int ktiles = (K + kGemmBK - 1) / kGemmBK;
-  // split-K: work unit u = (tile, split); split s covers k blocks [s*kper, min((s+1)*kper, ktiles))
-  // and writes its partial tile to C + s*split_stride (reduced by splitk_reduce_kernel).
-  const int kper = (ktiles + splits - 1) / splits;
-  const int units = tiles * splits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -88,10 +120,11 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
       tma_prefetch_desc(&tmB);
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      WorkRange wr(tiles, dp_tiles, ktiles);
+      int tile, kb0, kb1;
+      while (wr.next(tile, kb0, kb1)) {
         int mb, nb;
-        tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
-        const int kb0 = (u % splits) * kper, kb1 = min(ktiles, kb0 + kper);
+        tile_coords(tile, num_m, num_n, group_m, mb, nb);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* sA = smem + stage * Cfg::kStageBytes;
@@ -124,11 +157,12 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+  WorkRange wr(tiles, dp_tiles, ktiles);
+  int tile, kb0, kb1;
+  bool first_seg = true;  // first stream-K segment of this CTA
+  while (wr.next(tile, kb0, kb1)) {
     int mb, nb;
-    tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
-    const int kb0 = (u % splits) * kper, kb1 = min(ktiles, kb0 + kper);
-    double* Cu = C + (int64_t)(u % splits) * split_stride;
+    tile_coords(tile, num_m, num_n, group_m, mb, nb);
     double acc[MI][NJ][2];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -167,47 +201,120 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
 #pragma unroll
             for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][q], b[j][q]);
       }
+      // Release the stage.  The fragments were read by the generic proxy (ld.shared) and the
+      // producer's next TMA write comes through the async proxy: without a proxy fence ptxas
+      // may issue the arrive while the last ld.shared are still in flight and the refill
+      // can overtake them (observed: stale rows 48-63 with short stream-K segments).
+      fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
 
-    // epilogue: fragments straight to global (row-major C)
+    if (kb0 == 0 && kb1 == ktiles) {
+      // whole tile: fragments straight to global (row-major C)
 #pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int row = mb * BM + wm0 + 8 * i + g;
-      if (row >= M) continue;
-      double* crow = Cu + (int64_t)row * ldc;
+      for (int i = 0; i < MI; ++i) {
+        const int row = mb * BM + wm0 + 8 * i + g;
+        if (row >= M) continue;
+        double* crow = C + (int64_t)row * ldc;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        const int col = nb * BN + wn0 + 8 * j + 2 * t;
-        if (vec_store && col + 1 < N) {
-          double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
-          if (accumulate) {
-            const double2 o = *reinterpret_cast<const double2*>(crow + col);
-            v.x += o.x;
-            v.y += o.y;
+        for (int j = 0; j < NJ; ++j) {
+          const int col = nb * BN + wn0 + 8 * j + 2 * t;
+          if (vec_store && col + 1 < N) {
+            double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+            if (accumulate) {
+              const double2 o = *reinterpret_cast<const double2*>(crow + col);
+              v.x += o.x;
+              v.y += o.y;
+            }
+            *reinterpret_cast<double2*>(crow + col) = v;
+          } else {
+            if (col < N) crow[col] = acc[i][j][0] + (accumulate ? crow[col] : 0.0);
+            if (col + 1 < N) crow[col + 1] = acc[i][j][1] + (accumulate ? crow[col + 1] : 0.0);
           }
-          *reinterpret_cast<double2*>(crow + col) = v;
-        } else {
-          if (col < N) crow[col] = acc[i][j][0] + (accumulate ? crow[col] : 0.0);
-          if (col + 1 < N) crow[col + 1] = acc[i][j][1] + (accumulate ? crow[col + 1] : 0.0);
         }
       }
+    } else {
+      // stream-K partial tile -> workspace slot (full BM x BN, row-major)
+      double* ws = partial_ws + ((int64_t)blockIdx.x * 2 + (first_seg ? 0 : 1)) * (BM * BN);
+      first_seg = false;
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          *reinterpret_cast<double2*>(ws + (wm0 + 8 * i + g) * BN + wn0 + 8 * j + 2 * t) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
     }
+    if (tile >= dp_tiles) first_seg = false;
   }
 }
 
-// C[r][c] (+)= sum_s W[s][r][c] over the split-K partial tiles, in fixed order (deterministic).
-__global__ void splitk_reduce_kernel(const double* __restrict__ W, int splits, int64_t split_stride,
-                                     double* __restrict__ C, int64_t ldc, int M, int N, int accumulate) {
-  const int64_t total = (int64_t)M * N;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / N, c = i - r * N;
-    const int64_t off = r * ldc + c;
-    double acc = W[off];
-    for (int s = 1; s < splits; ++s) acc += W[s * split_stride + off];
-    C[off] = accumulate ? C[off] + acc : acc;
+// Stream-K fixup: every stream-K tile whose k-range was split across CTAs is the sum, in
+// CTA order, of their partial slots.  One block per stream-K tile; the slot list is
+// computed once per block (no per-element integer division), then the tile is summed with
+// 16-byte loads.
+constexpr int kFixupMaxParts = 256;
+constexpr int kFixupSplit = 16;  // blocks per tile (parallelism for small problems)
+
+template <int BM, int BN>
+__global__ void __launch_bounds__(256) streamk_fixup_kernel(const double* __restrict__ ws, double* __restrict__ C,
+                                                            int64_t ldc, int M, int N, int ktiles, int group_m,
+                                                            int grid, int dp_tiles, int accumulate) {
+  __shared__ int s_slot[kFixupMaxParts];
+  __shared__ int s_n;
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const int local = blockIdx.x / kFixupSplit;  // stream-K tile index
+  const int part = blockIdx.x % kFixupSplit;    // this block's 1/kFixupSplit of the tile
+  const int tile = dp_tiles + local;
+  if (threadIdx.x == 0) {
+    const int64_t total = (int64_t)(num_m * num_n - dp_tiles) * ktiles;
+    // CTA b owns stream-K iterations [total*b/grid, total*(b+1)/grid)
+    auto cta_of = [&](int64_t it) {
+      int64_t b = (it * grid) / total;
+      while (b + 1 < grid && total * (b + 1) / grid <= it) ++b;
+      while (b > 0 && total * b / grid > it) --b;
+      return (int)b;
+    };
+    const int64_t it_first = (int64_t)local * ktiles;
+    const int b0 = cta_of(it_first), b1 = cta_of(it_first + ktiles - 1);
+    int n = 0;
+    if (b0 != b1)
+      for (int b = b0; b <= b1 && n < kFixupMaxParts; ++b) {
+        const int first_local_of_b = (int)((total * b / grid) / ktiles);
+        s_slot[n++] = 2 * b + (first_local_of_b == local ? 0 : 1);
+      }
+    s_n = n;  // 0: the tile was written whole by one CTA
+  }
+  __syncthreads();
+  const int n = s_n;
+  if (n == 0) return;
+  int mb, nb;
+  tile_coords(tile, num_m, num_n, group_m, mb, nb);
+  const bool vec = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+  constexpr int kPer = BM * BN / kFixupSplit;
+  for (int e = part * kPer + threadIdx.x * 2; e < (part + 1) * kPer; e += blockDim.x * 2) {
+    const int r = e / BN, c = e - r * BN;  // c even
+    const int row = mb * BM + r, col = nb * BN + c;
+    if (row >= M || col >= N) continue;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < n; ++k) {
+      const double2 v = *reinterpret_cast<const double2*>(ws + (int64_t)s_slot[k] * (BM * BN) + e);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    double* cp = C + (int64_t)row * ldc + col;
+    if (vec && col + 1 < N) {
+      if (accumulate) {
+        const double2 o = *reinterpret_cast<const double2*>(cp);
+        acc.x += o.x;
+        acc.y += o.y;
+      }
+      *reinterpret_cast<double2*>(cp) = acc;
+    } else {
+      cp[0] = accumulate ? cp[0] + acc.x : acc.x;
+      if (col + 1 < N) cp[1] = accumulate ? cp[1] + acc.y : acc.y;
+    }
   }
 }
 

@@ -159,36 +159,13 @@ struct GemmOp {
 
 static int g_num_sms = 0;
 
-// split-K factor: enough (tile, split) units to fill the 148 SMs in whole waves when the
-// tile count alone would leave most of the last wave idle; each split keeps >= 4 k blocks.
-static int choose_splits(int64_t tiles, int64_t ktiles) {
-  if (tiles >= 4 * (int64_t)g_num_sms) return 1;
-  int best = 1;
-  double best_eff = 0.0;
-  for (int s = 1; s <= 16; ++s) {
-    const int64_t kper = (ktiles + s - 1) / s;
-    if (s > 1 && kper < 4) break;
-    const int64_t units = tiles * s;
-    const int64_t waves = (units + g_num_sms - 1) / g_num_sms;
-    const double eff = (double)units / (double)(waves * g_num_sms);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
-      best = s;
-    }
-    if (eff >= 0.95) break;
-  }
-  // no empty splits
-  const int64_t kper = (ktiles + best - 1) / best;
-  return (int)((ktiles + kper - 1) / kper);
-}
-
 static bool tma_ok(const GemmOp& g) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   return (g.lda % 2 == 0) && (g.ldb % 2 == 0) && al16(g.A) && al16(g.B) && g.M < (1ll << 31) && g.N < (1ll << 31) &&
          g.K < (1ll << 31);
 }
 
-struct SplitWs {  // split-K partial-tile workspace, grown on demand
+struct SplitWs {  // stream-K partial-tile workspace, grown on demand
   double* ptr = nullptr;
   size_t bytes = 0;
 };
@@ -213,42 +190,49 @@ static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitW
     }
     const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + kBN - 1) / kBN);
     const int64_t ktiles = (g.K + kGemmBK - 1) / kGemmBK;
-    int splits = ws ? choose_splits(tiles, ktiles) : 1;
-    double* Cdst = g.C;
-    const int64_t split_stride = g.M * g.ldc;
-    if (splits > 1) {
-      const size_t need = sizeof(double) * (size_t)splits * (size_t)split_stride;
+    // Hybrid schedule: whole tiles round-robin for all but the last one-to-two waves, whose
+    // (tile, k-block) iterations are balanced across the SMs by stream-K.
+    int grid = (int)std::min<int64_t>(tiles, g_num_sms);
+    int64_t dp_tiles = tiles;
+    const int64_t waves = (tiles + g_num_sms - 1) / g_num_sms;
+    const double eff = (double)tiles / (double)(waves * g_num_sms);
+    if (ws && eff < 0.995 && getenv("HEFF_NO_STREAMK") == nullptr) {
+      dp_tiles = (tiles >= 2 * (int64_t)g_num_sms) ? (tiles / g_num_sms - 1) * g_num_sms : 0;
+      const int64_t sk_iters = (tiles - dp_tiles) * ktiles;
+      grid = (int)std::max<int64_t>(1, std::min<int64_t>(g_num_sms, sk_iters / 4));  // >= 4 k-blocks per CTA
+      // every split tile must have <= kFixupMaxParts contributing CTAs
+      while (grid > 1 && ktiles / std::max<int64_t>(1, sk_iters / grid) + 2 > kFixupMaxParts) grid /= 2;
+      if (dp_tiles > 0) grid = g_num_sms;
+      const size_t need = sizeof(double) * 2 * (size_t)grid * kBM * kBN;
       if (ws->bytes < need) {
         cudaFree(ws->ptr);
         ws->ptr = nullptr;
         ws->bytes = 0;
         if (cudaMalloc(&ws->ptr, need) != cudaSuccess) {
           cudaGetLastError();
-          splits = 1;  // no room for partials: run unsplit
+          dp_tiles = tiles;  // no room for partial tiles: plain persistent schedule
+          grid = (int)std::min<int64_t>(tiles, g_num_sms);
         } else {
           ws->bytes = need;
         }
       }
-      if (splits > 1) Cdst = ws->ptr;
     }
-    const int grid = (int)std::min<int64_t>(tiles * splits, g_num_sms);
-    const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(Cdst) & 15) == 0) ? 1 : 0;
+    const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(g.C) & 15) == 0) ? 1 : 0;
+    double* wsp = ws ? ws->ptr : nullptr;
     if (g.b_kmajor) {
       auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, true>;
-      k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(g.mapA, g.mapB, Cdst, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec, splits, split_stride, splits > 1 ? 0 : g.accumulate);
+      k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
+                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate);
     } else {
       auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>;
-      k<<<grid, CfgNN::kThreads, CfgNN::kSmemBytes, s>>>(g.mapA, g.mapB, Cdst, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec, splits, split_stride, splits > 1 ? 0 : g.accumulate);
+      k<<<grid, CfgNN::kThreads, CfgNN::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
+                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate);
     }
-    if (splits > 1) {
+    if (dp_tiles < tiles) {
       CK(cudaGetLastError());
       if (nlaunch) ++*nlaunch;
-      const int64_t total = g.M * g.N;
-      const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * (int64_t)g_num_sms, (total + 255) / 256));
-      splitk_reduce_kernel<<<rgrid, 256, 0, s>>>(Cdst, splits, split_stride, g.C, g.ldc, (int)g.M, (int)g.N,
-                                                 g.accumulate);
+      streamk_fixup_kernel<kBM, kBN><<<(unsigned)((tiles - dp_tiles) * kFixupSplit), 256, 0, s>>>(
+          wsp, g.C, g.ldc, (int)g.M, (int)g.N, (int)ktiles, kGroupM, grid, (int)dp_tiles, g.accumulate);
     }
   } else {
     dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64));
@@ -1210,5 +1194,27 @@ extern "C" int heff_tridiag_lowest(int j, const double* alpha, const double* bet
   if (!tridiag_lowest_vec(j, alpha, beta, theta, yy.data()))
     return set_err(HEFF_ECUDA, "heff_tridiag_lowest: QL iteration did not converge");
   if (y) memcpy(y, yy.data(), sizeof(double) * j);
+  return HEFF_OK;
+}
+
+// The FP64 GEMM primitive of the hot path, exposed for kernel-level tests and reuse:
+// C[M][N] (+)= A[M][K] . op(B), op(B) = B[K][N] (b_kmajor = 0) or B[N][K]^T (b_kmajor = 1).
+static thread_local SplitWs t_gemm_ws;
+extern "C" int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                         int b_kmajor, double* C, int64_t ldc, int accumulate, int path, heff_stream stream) {
+  if (M < 0 || N < 0 || K < 0 || !A || !B || !C || path < 0 || path > 2)
+    return set_err(HEFF_EINVAL, "heff_gemm: bad argument");
+  CKR(init_device_once());
+  GemmOp g;
+  g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.b_kmajor = b_kmajor != 0;
+  g.C = C; g.ldc = ldc; g.accumulate = accumulate ? 1 : 0;
+  int nl = 0;
+  return launch_gemm(g, path, reinterpret_cast<cudaStream_t>(stream), &nl, &t_gemm_ws);
+}
+
+// debug: copy the calling thread's heff_gemm stream-K workspace (partial tiles) to dst
+extern "C" int heff_debug_gemm_ws(double* dst, size_t bytes) {
+  if (!t_gemm_ws.ptr) return set_err(HEFF_EINVAL, "no workspace");
+  CK(cudaMemcpy(dst, t_gemm_ws.ptr, std::min(bytes, t_gemm_ws.bytes), cudaMemcpyDeviceToDevice));
   return HEFF_OK;
 }

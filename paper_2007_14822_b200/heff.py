@@ -77,12 +77,13 @@ def lib() -> ctypes.CDLL:
         L.heff_set_penalty.argtypes = [vp, vp, ip, ctypes.c_double, vp]
         dp = ctypes.POINTER(ctypes.c_double)
         L.heff_tridiag_lowest.argtypes = [ip, dp, dp, dp, dp]
+        L.heff_gemm.argtypes = [i64, i64, i64, vp, i64, vp, i64, ip, vp, i64, ip, ip, vp]
         L.heff_env_update_left.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         L.heff_env_update_right.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         for f in ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-                  "heff_env_update_right", "heff_tridiag_lowest"):
+                  "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -91,7 +92,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy", "heff_last_error",
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-            "heff_env_update_right", "heff_tridiag_lowest")
+            "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm")
 
 
 def _check(rc: int):
@@ -120,6 +121,23 @@ def relayout_blocked(src: torch.Tensor, P: int, stream=None) -> torch.Tensor:
     dst = torch.empty((rows, P * nb), dtype=torch.float64, device=src.device)
     _check(lib().heff_relayout_blocked(src.data_ptr(), dst.data_ptr(), rows, nb, P, _stream(stream)))
     return dst
+
+
+def gemm(A: torch.Tensor, B: torch.Tensor, b_kmajor: bool = False, C: torch.Tensor | None = None,
+         accumulate: bool = False, path: int = 0, stream=None) -> torch.Tensor:
+    """C (+)= A @ B (B [K,N]) or A @ B.T (b_kmajor, B [N,K]) on libheff's FP64 DMMA GEMM."""
+    _dev(A, "A")
+    _dev(B, "B")
+    M, K = A.shape
+    N = B.shape[0] if b_kmajor else B.shape[1]
+    if (B.shape[1] if b_kmajor else B.shape[0]) != K:
+        raise ValueError("inner dimensions differ")
+    if C is None:
+        C = torch.zeros((M, N), dtype=torch.float64, device=A.device)
+    _dev(C, "C")
+    _check(lib().heff_gemm(M, N, K, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), int(b_kmajor),
+                           C.data_ptr(), C.stride(0), int(accumulate), int(path), _stream(stream)))
+    return C
 
 
 def tridiag_lowest(alpha, beta):

@@ -257,3 +257,15 @@ def test_sharded_plan_matvec_full_c3_with_nccl(dev, orc):
                                                    uid=nccl_unique_id())) as h:
         out = h.apply(xd.psi).cpu().numpy()
     assert rel(out, ref) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("sk", ["on", "off"])
+def test_streamk_and_data_parallel_schedules(dev, orc, sk, monkeypatch):
+    """Hybrid stream-K (partial tiles + fixup) and the plain persistent schedule give the same
+    parity on shapes with ragged last waves (pure stream-K and DP + stream-K tails)."""
+    if sk == "off":
+        monkeypatch.setenv("HEFF_NO_STREAMK", "1")
+    for x in (C.make("c2"), C.random_dense(dict(mL=600, d1=2, d2=2, mR=520, kL=5, kM=5, kR=5), seed=12)):
+        L, W1, W2, R, psi = x.numpy()
+        ref = orc.heff_apply(L, W1, W2, R, psi)
+        assert rel(gpu_apply(x, dev), ref) <= MATVEC_TOL
