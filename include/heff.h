@@ -171,6 +171,28 @@ int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, con
  * component positive (reading R14). */
 int heff_tridiag_lowest(int j, const double* alpha, const double* beta, double* theta, double* y);
 
+/* ---- U(1) block sparsity (Sec. 7) -----------------
+ * Declares conserved charges so heff_apply skips the GEMM k-blocks that are zero by
+ * symmetry.  Conventions (reading R18): a bond index carries the total charge to
+ * its left; L[a',w,a] = 0 unless qa[a'] - qa[a] = cL[w]; R[b',w,b] = 0 unless
+ * qb[b'] - qb[b] = cR[w]; psi[a,s1,s2,b] = 0 unless qb[b] = qa[a] + qs1[s1] + qs2[s2]
+ * (W1/W2 must conserve charge with channel charges cL -> cM -> cR).  qa (mL) and qb (mR)
+ * are nondecreasing (sector-sorted bonds).  All arrays are HOST int arrays, copied.
+ * Tensors stay dense; entries the declaration says are zero must be zero, otherwise the
+ * result is undefined.  qn == NULL returns the plan to dense.  Single-GPU, unchunked
+ * order-A plans only (HEFF_EUNSUPPORTED otherwise). */
+typedef struct {
+  const int* qa;
+  const int* qb;
+  const int* qs1;
+  const int* qs2;
+  const int* cL;
+  const int* cM;
+  const int* cR;
+} heff_qn;
+int heff_set_qn(heff_plan p, const heff_qn* qn);
+enum { HEFF_OPT_SPARSE_KBLOCKS = 6 }; /* get: scheduled (tile, 16-wide k-block) products per matvec */
+
 /* ---- Environment update --------------------------------------
  * After each local eigensolve a DMRG sweep moves the window one site and grows the
  * environment by that site (Sec. 6.2; SPEC ProjMPO):

@@ -24,11 +24,11 @@ namespace heff {
 
 constexpr int kGemmBK = 16;  // doubles per k block = one 128-byte swizzle row
 
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group_m, int& mb, int& nb) {
+__host__ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group_m, int& mb, int& nb) {
   const int per_group = group_m * num_n;
   const int group = tile / per_group;
   const int first_m = group * group_m;
-  const int gm = min(group_m, num_m - first_m);
+  const int gm = (group_m < num_m - first_m) ? group_m : (num_m - first_m);
   const int local = tile - group * per_group;
   mb = first_m + local % gm;
   nb = local / gm;
@@ -61,27 +61,37 @@ struct WorkRange {
   int64_t it, it_end;  // stream-K iteration range (iterations counted from dp_tiles*ktiles)
   int tile;            // data-parallel cursor
   int dp_tiles, ktiles;
-  __device__ WorkRange(int tiles, int dp_tiles_, int ktiles_) : dp_tiles(dp_tiles_), ktiles(ktiles_) {
+  // block-sparse mode (kb_list != null): tiles taken whole in `order`, each over the
+  // k-blocks kb_list[kb_ptr[t] .. kb_ptr[t+1])
+  const int* order;
+  const int* kb_ptr;
+  __device__ WorkRange(int tiles, int dp_tiles_, int ktiles_, const int* order_, const int* kb_ptr_)
+      : dp_tiles(dp_tiles_), ktiles(ktiles_), order(order_), kb_ptr(kb_ptr_) {
     const int64_t total = (int64_t)(tiles - dp_tiles_) * ktiles_;
     it = total * blockIdx.x / gridDim.x;
     it_end = total * (blockIdx.x + 1) / gridDim.x;
     tile = blockIdx.x;
   }
-  // next (tile, [kb0, kb1)) segment; false when done
-  __device__ bool next(int& t, int& kb0, int& kb1) {
+  // next (tile, [i0, i1)) segment; i indexes k-blocks (dense) or kb_list (sparse)
+  __device__ bool next(int& t, int& i0, int& i1) {
     if (tile < dp_tiles) {
-      t = tile;
-      kb0 = 0;
-      kb1 = ktiles;
+      t = order ? __ldg(order + tile) : tile;
+      if (kb_ptr) {
+        i0 = __ldg(kb_ptr + t);
+        i1 = __ldg(kb_ptr + t + 1);
+      } else {
+        i0 = 0;
+        i1 = ktiles;
+      }
       tile += gridDim.x;
       return true;
     }
     if (it >= it_end) return false;
     const int local = (int)(it / ktiles);
     t = dp_tiles + local;
-    kb0 = (int)(it - (int64_t)local * ktiles);
-    kb1 = (int)min((int64_t)ktiles, (int64_t)kb0 + (it_end - it));
-    it += kb1 - kb0;
+    i0 = (int)(it - (int64_t)local * ktiles);
+    i1 = (int)min((int64_t)ktiles, (int64_t)i0 + (it_end - it));
+    it += i1 - i0;
     return true;
   }
 };
@@ -90,7 +100,9 @@ template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR>
 __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::kThreads, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store,
-                         int dp_tiles, double* __restrict__ partial_ws, int accumulate) {
+                         int dp_tiles, double* __restrict__ partial_ws, int accumulate,
+                         const int* __restrict__ tile_order, const int* __restrict__ kb_ptr,
+                         const int* __restrict__ kb_list) {
   using Cfg = TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>;
   constexpr int MI = WM / 8, NJ = WN / 8;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -120,12 +132,13 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
       tma_prefetch_desc(&tmB);
       int stage = 0;
       uint32_t phase = 0;
-      WorkRange wr(tiles, dp_tiles, ktiles);
-      int tile, kb0, kb1;
-      while (wr.next(tile, kb0, kb1)) {
+      WorkRange wr(tiles, dp_tiles, ktiles, tile_order, kb_ptr);
+      int tile, i0, i1;
+      while (wr.next(tile, i0, i1)) {
         int mb, nb;
         tile_coords(tile, num_m, num_n, group_m, mb, nb);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int idx = i0; idx < i1; ++idx) {
+          const int kb = kb_list ? __ldg(kb_list + idx) : idx;
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* sA = smem + stage * Cfg::kStageBytes;
           unsigned char* sB = sA + Cfg::kTileABytes;
@@ -157,7 +170,7 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
 
   int stage = 0;
   uint32_t phase = 0;
-  WorkRange wr(tiles, dp_tiles, ktiles);
+  WorkRange wr(tiles, dp_tiles, ktiles, tile_order, kb_ptr);
   int tile, kb0, kb1;
   bool first_seg = true;  // first stream-K segment of this CTA
   while (wr.next(tile, kb0, kb1)) {
@@ -169,7 +182,7 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int kb = kb0; kb < kb1; ++kb) {
+    for (int idx = kb0; idx < kb1; ++idx) {  // the consumers only count k-blocks; the producer picks them
       mbar_wait(&full[stage], phase);
       const uint32_t sA = smem_base + stage * Cfg::kStageBytes;
       const uint32_t sB = sA + Cfg::kTileABytes;
@@ -211,7 +224,7 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
 
-    if (kb0 == 0 && kb1 == ktiles) {
+    if (kb_list || (kb0 == 0 && kb1 == ktiles)) {
       // whole tile: fragments straight to global (row-major C)
 #pragma unroll
       for (int i = 0; i < MI; ++i) {

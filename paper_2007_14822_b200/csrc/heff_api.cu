@@ -150,6 +150,10 @@ struct GemmOp {
   double* C = nullptr;
   int64_t ldc = 0;
   int accumulate = 0;  // C += A.B instead of C = A.B
+  // block-sparse schedule (heff_set_qn): tile order + per-tile k-block lists, device arrays
+  const int* sp_order = nullptr;
+  const int* sp_ptr = nullptr;
+  const int* sp_list = nullptr;
   // cached TMA maps (rebuilt when A/B pointers change)
   CUtensorMap mapA, mapB;
   const double* mapA_ptr = nullptr;
@@ -196,7 +200,9 @@ static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitW
     int64_t dp_tiles = tiles;
     const int64_t waves = (tiles + g_num_sms - 1) / g_num_sms;
     const double eff = (double)tiles / (double)(waves * g_num_sms);
-    if (ws && eff < 0.995 && getenv("HEFF_NO_STREAMK") == nullptr) {
+    const bool sparse = g.sp_list != nullptr;
+    if (sparse) grid = (int)std::min<int64_t>(tiles, g_num_sms);
+    if (!sparse && ws && eff < 0.995 && getenv("HEFF_NO_STREAMK") == nullptr) {
       dp_tiles = (tiles >= 2 * (int64_t)g_num_sms) ? (tiles / g_num_sms - 1) * g_num_sms : 0;
       const int64_t sk_iters = (tiles - dp_tiles) * ktiles;
       grid = (int)std::max<int64_t>(1, std::min<int64_t>(g_num_sms, sk_iters / 4));  // >= 4 k-blocks per CTA
@@ -222,11 +228,13 @@ static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitW
     if (g.b_kmajor) {
       auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, true>;
       k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate);
+                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order,
+                                                          g.sp_ptr, g.sp_list);
     } else {
       auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>;
       k<<<grid, CfgNN::kThreads, CfgNN::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate);
+                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order,
+                                                          g.sp_ptr, g.sp_list);
     }
     if (dp_tiles < tiles) {
       CK(cudaGetLastError());
@@ -305,6 +313,11 @@ struct heff_plan_s {
   GemmOp gA, gD;
   Csr csrA, csrB;
   SplitWs splitws;
+  // U(1) block-sparse schedules of the two GEMMs (heff_set_qn); one device allocation each
+  int* sp1 = nullptr;
+  int* sp4 = nullptr;
+  int64_t sp_kblocks = 0;  // k-block x tile products scheduled per matvec (both GEMMs)
+  unsigned char* mpo_live = nullptr;  // [mL][b-tiles]: MPO blocks that can be nonzero (U(1) plans)
   // e2e staging
   double *stage_in = nullptr, *stage_out = nullptr;
   // Lanczos
@@ -420,6 +433,7 @@ extern "C" int heff_destroy(heff_plan p) {
   cudaFree(p->partial); cudaFree(p->scal);
   cudaFree(p->splitws.ptr);
   cudaFree(p->phis); cudaFree(p->pen_scratch);
+  cudaFree(p->sp1); cudaFree(p->sp4);
   free_csr(p->csrA);
   free_csr(p->csrB);
   for (auto& e : p->prof_ev) cudaEventDestroy(e);
@@ -571,6 +585,7 @@ extern "C" int heff_get_option(heff_plan p, int option, int64_t* value) {
     case HEFF_OPT_MPO_NNZ: *value = p->sharded ? p->csrB.nnz : p->csrA.nnz; return HEFF_OK;
     case HEFF_OPT_PROFILE: *value = p->profile; return HEFF_OK;
     case HEFF_OPT_TOTAL_LAUNCHES: *value = p->total_launches; return HEFF_OK;
+    case HEFF_OPT_SPARSE_KBLOCKS: *value = p->sp_kblocks; return HEFF_OK;
     default: return set_err(HEFF_EINVAL, "unknown option %d", option);
   }
 }
@@ -625,7 +640,7 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     CKR(prof_mark(p, 1, s));
     dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
     mpo_orderA_kernel<<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
-                                                       p->csrA.d_col, p->csrA.d_val);
+                                                       p->csrA.d_col, p->csrA.d_val, p->mpo_live);
     CK(cudaGetLastError());
     ++*nl;
     CKR(prof_mark(p, 2, s));
@@ -1117,7 +1132,7 @@ extern "C" int heff_env_update_left(const heff_env_dims* dims, const double* L, 
     const int nin = (int)(d.kl * d.d), nout = (int)(d.d * d.kr);
     dim3 grid((unsigned)((d.mo + kMpoCols - 1) / kMpoCols), (unsigned)d.mi);
     mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mo, nin, nout, csr.d_rowptr,
-                                                                                 csr.d_col, csr.d_val);
+                                                                                 csr.d_col, csr.d_val, nullptr);
     dim3 tg((unsigned)((d.mo + 31) / 32), (unsigned)((d.mi * d.d + 31) / 32));
     transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, At, d.mi * d.d, d.mo);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_left: launch failed");
@@ -1174,7 +1189,7 @@ extern "C" int heff_env_update_right(const heff_env_dims* dims, const double* R,
     const int nin = (int)(d.d * d.kr), nout = (int)(d.kl * d.d);
     dim3 grid((unsigned)((d.mi + kMpoCols - 1) / kMpoCols), (unsigned)d.mo);
     mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mi, nin, nout, csr.d_rowptr,
-                                                                                 csr.d_col, csr.d_val);
+                                                                                 csr.d_col, csr.d_val, nullptr);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_right: launch failed");
   }
   if (!r) {
@@ -1216,5 +1231,205 @@ extern "C" int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64
 extern "C" int heff_debug_gemm_ws(double* dst, size_t bytes) {
   if (!t_gemm_ws.ptr) return set_err(HEFF_EINVAL, "no workspace");
   CK(cudaMemcpy(dst, t_gemm_ws.ptr, std::min(bytes, t_gemm_ws.bytes), cudaMemcpyDeviceToDevice));
+  return HEFF_OK;
+}
+
+// --------------------------------------------------------------------------- U(1) block sparsity
+// NEXT-3: QN-conserving H_eff (Sec. 7).  The tensors stay
+// dense and sector-sorted; heff_set_qn builds, per GEMM output tile, the list of k-blocks
+// whose (row, column) charge constraints can both be met, and the GEMM kernel visits only
+// those (tiles in descending-work order, round-robin over the SMs).  Tiles with an empty
+// list are written as zeros.
+static std::vector<std::vector<int>> kblocks_by_value(const std::vector<int>& kval_lo, const std::vector<int>& kval_hi,
+                                                      const std::vector<std::vector<int>>& kvals, int vmin, int vmax) {
+  (void)kval_lo;
+  (void)kval_hi;
+  std::vector<std::vector<int>> inv(vmax - vmin + 1);
+  for (size_t kb = 0; kb < kvals.size(); ++kb)
+    for (int v : kvals[kb]) inv[v - vmin].push_back((int)kb);
+  return inv;
+}
+
+// rowv[r], colv[c]: the charge each output row / column requires of the contracted index;
+// kvals[kb]: the charges present in k-block kb.  Returns order | ptr | list in one buffer.
+static int build_sparse_schedule(int64_t M, int64_t N, const std::vector<int>& rowv, const std::vector<int>& colv,
+                                 const std::vector<std::vector<int>>& kvals, int** d_out, int64_t* total_kb,
+                                 const int** order, const int** ptr, const int** list, int64_t* makespan) {
+  const int num_m = (int)((M + kBM - 1) / kBM), num_n = (int)((N + kBN - 1) / kBN);
+  const int tiles = num_m * num_n;
+  int vmin = INT32_MAX, vmax = INT32_MIN;
+  for (auto& kv : kvals)
+    for (int v : kv) { vmin = std::min(vmin, v); vmax = std::max(vmax, v); }
+  if (vmin > vmax) { vmin = 0; vmax = 0; }
+  auto inv = kblocks_by_value({}, {}, kvals, vmin, vmax);
+  auto tile_set = [&](const std::vector<int>& vals, int64_t lo, int64_t hi) {
+    std::vector<int> v(vals.begin() + lo, vals.begin() + hi);
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    return v;
+  };
+  std::vector<std::vector<int>> setM(num_m), setN(num_n);
+  for (int mb = 0; mb < num_m; ++mb) setM[mb] = tile_set(rowv, (int64_t)mb * kBM, std::min<int64_t>(M, (int64_t)(mb + 1) * kBM));
+  for (int nb = 0; nb < num_n; ++nb) setN[nb] = tile_set(colv, (int64_t)nb * kBN, std::min<int64_t>(N, (int64_t)(nb + 1) * kBN));
+  std::vector<std::vector<int>> lists(tiles);
+  int64_t tot = 0;
+  std::vector<int> I, kb;
+  for (int t = 0; t < tiles; ++t) {
+    int mb, nb;
+    tile_coords(t, num_m, num_n, kGroupM, mb, nb);
+    I.clear();
+    std::set_intersection(setM[mb].begin(), setM[mb].end(), setN[nb].begin(), setN[nb].end(), std::back_inserter(I));
+    kb.clear();
+    for (int v : I)
+      if (v >= vmin && v <= vmax) kb.insert(kb.end(), inv[v - vmin].begin(), inv[v - vmin].end());
+    std::sort(kb.begin(), kb.end());
+    kb.erase(std::unique(kb.begin(), kb.end()), kb.end());
+    lists[t] = kb;
+    tot += (int64_t)kb.size();
+  }
+  std::vector<int> ord(tiles);
+  for (int t = 0; t < tiles; ++t) ord[t] = t;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return lists[a].size() > lists[b].size(); });
+  {  // k-blocks of the busiest CTA under the kernel's round-robin over `ord` (+ per-tile overhead ~2 k-blocks)
+    const int G = std::min<int>(tiles, g_num_sms);
+    std::vector<int64_t> load(G, 0);
+    for (int i = 0; i < tiles; ++i) load[i % G] += (int64_t)lists[ord[i]].size() + 2;
+    *makespan = *std::max_element(load.begin(), load.end());
+  }
+  std::vector<int> buf;
+  buf.reserve((size_t)tiles * 2 + 1 + (size_t)tot);
+  buf.insert(buf.end(), ord.begin(), ord.end());
+  int64_t acc = 0;
+  for (int t = 0; t < tiles; ++t) { buf.push_back((int)acc); acc += (int64_t)lists[t].size(); }
+  buf.push_back((int)acc);
+  for (int t = 0; t < tiles; ++t) buf.insert(buf.end(), lists[t].begin(), lists[t].end());
+  if (acc > INT32_MAX) return set_err(HEFF_EUNSUPPORTED, "heff_set_qn: schedule too large");
+  cudaFree(*d_out);
+  *d_out = nullptr;
+  CK(cudaMalloc(d_out, sizeof(int) * buf.size()));
+  CK(cudaMemcpy(*d_out, buf.data(), sizeof(int) * buf.size(), cudaMemcpyHostToDevice));
+  *order = *d_out;
+  *ptr = *d_out + tiles;
+  *list = *d_out + 2 * tiles + 1;
+  *total_kb = tot;
+  return HEFF_OK;
+}
+
+static int64_t dense_kblock_tiles(int64_t M, int64_t N, int64_t K) {
+  return ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN) * ((K + kGemmBK - 1) / kGemmBK);
+}
+
+// The block-sparse schedule runs whole tiles data-parallel (no stream-K): use it when it
+// removes at least 30% of the work and there are enough tiles to fill the SMs.
+// Estimated critical path (busiest SM's k-blocks) of the sparse round-robin schedule vs
+// the perfectly balanced dense stream-K schedule.
+static bool sparse_worth_it(int64_t M, int64_t N, int64_t K, int64_t makespan) {
+  if (getenv("HEFF_QN_FORCE_SPARSE")) return true;
+  const double dense_span = (double)dense_kblock_tiles(M, N, K) / g_num_sms;
+  return (double)makespan < 0.85 * dense_span;
+}
+
+extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
+  if (!p) return set_err(HEFF_EINVAL, "heff_set_qn: null plan");
+  if (!qn) {  // back to dense
+    cudaFree(p->sp1); cudaFree(p->sp4); cudaFree(p->mpo_live);
+    p->sp1 = p->sp4 = nullptr;
+    p->mpo_live = nullptr;
+    p->g1.sp_order = p->g1.sp_ptr = p->g1.sp_list = nullptr;
+    p->g4.sp_order = p->g4.sp_ptr = p->g4.sp_list = nullptr;
+    p->sp_kblocks = 0;
+    return HEFF_OK;
+  }
+  if (p->sharded || !p->terms.empty())
+    return set_err(HEFF_EUNSUPPORTED, "heff_set_qn: single-GPU order-A plans only (set it on each term of a sum)");
+  const heff_dims& d = p->dims;
+  if (p->chunk_rows != d.mL) return set_err(HEFF_EUNSUPPORTED, "heff_set_qn: plan is chunked over a' (workspace budget)");
+  if (!qn->qa || !qn->qb || !qn->qs1 || !qn->qs2 || !qn->cL || !qn->cR)
+    return set_err(HEFF_EINVAL, "heff_set_qn: null charge array");
+  for (int64_t i = 1; i < d.mL; ++i)
+    if (qn->qa[i] < qn->qa[i - 1]) return set_err(HEFF_EINVAL, "heff_set_qn: qa must be nondecreasing");
+  for (int64_t i = 1; i < d.mR; ++i)
+    if (qn->qb[i] < qn->qb[i - 1]) return set_err(HEFF_EINVAL, "heff_set_qn: qb must be nondecreasing");
+  // GEMM1: rows (a',w) need q(a) = qa[a'] - cL[w]; columns (s1,s2,b) need q(a) = qb[b] - qs1 - qs2
+  {
+    const int64_t M = d.mL * d.kL, N = d.d1 * d.d2 * d.mR, K = d.mL;
+    std::vector<int> rowv(M), colv(N);
+    for (int64_t ap = 0; ap < d.mL; ++ap)
+      for (int64_t w = 0; w < d.kL; ++w) rowv[ap * d.kL + w] = qn->qa[ap] - qn->cL[w];
+    for (int64_t s1 = 0; s1 < d.d1; ++s1)
+      for (int64_t s2 = 0; s2 < d.d2; ++s2)
+        for (int64_t b = 0; b < d.mR; ++b) colv[(s1 * d.d2 + s2) * d.mR + b] = qn->qb[b] - qn->qs1[s1] - qn->qs2[s2];
+    std::vector<std::vector<int>> kvals((K + kGemmBK - 1) / kGemmBK);
+    for (int64_t a = 0; a < K; ++a) {
+      auto& v = kvals[a / kGemmBK];
+      if (v.empty() || v.back() != qn->qa[a]) v.push_back(qn->qa[a]);
+    }
+    int64_t tot = 0, span = 0;
+    CKR(build_sparse_schedule(M, N, rowv, colv, kvals, &p->sp1, &tot, &p->g1.sp_order, &p->g1.sp_ptr, &p->g1.sp_list,
+                              &span));
+    p->sp_kblocks = tot;
+    if (!sparse_worth_it(M, N, K, span)) {  // dense (stream-K) schedule is faster here
+      p->g1.sp_order = p->g1.sp_ptr = p->g1.sp_list = nullptr;
+      p->sp_kblocks = dense_kblock_tiles(M, N, K);
+    }
+  }
+  // GEMM4: rows (a',s1',s2') and columns b' both fix q(b) + cR[w2] for the contracted (w2, b)
+  {
+    const int64_t M = d.mL * d.d1 * d.d2, N = d.mR, K = d.kR * d.mR;
+    std::vector<int> rowv(M), colv(N);
+    for (int64_t ap = 0; ap < d.mL; ++ap)
+      for (int64_t s1 = 0; s1 < d.d1; ++s1)
+        for (int64_t s2 = 0; s2 < d.d2; ++s2) rowv[(ap * d.d1 + s1) * d.d2 + s2] = qn->qa[ap] + qn->qs1[s1] + qn->qs2[s2];
+    for (int64_t b = 0; b < d.mR; ++b) colv[b] = qn->qb[b];
+    std::vector<std::vector<int>> kvals((K + kGemmBK - 1) / kGemmBK);
+    for (int64_t w2 = 0; w2 < d.kR; ++w2)
+      for (int64_t b = 0; b < d.mR; ++b) {
+        auto& v = kvals[(w2 * d.mR + b) / kGemmBK];
+        const int val = qn->qb[b] + qn->cR[w2];
+        if (std::find(v.begin(), v.end(), val) == v.end()) v.push_back(val);
+      }
+    int64_t tot = 0, span = 0;
+    CKR(build_sparse_schedule(M, N, rowv, colv, kvals, &p->sp4, &tot, &p->g4.sp_order, &p->g4.sp_ptr, &p->g4.sp_list,
+                              &span));
+    if (!sparse_worth_it(M, N, K, span)) {
+      p->g4.sp_order = p->g4.sp_ptr = p->g4.sp_list = nullptr;
+      tot = dense_kblock_tiles(M, N, K);
+    }
+    p->sp_kblocks += tot;
+  }
+  // MPO blocks (a', 128-column b tile): live iff some (w,s1,s2) input or (s1',s2',w2) output
+  // entry of the block is allowed; the rest are skipped and their T3 entries stay zero.
+  {
+    const int nbt = (int)((d.mR + kMpoCols - 1) / kMpoCols);
+    std::vector<unsigned char> live((size_t)d.mL * nbt, 0);
+    std::vector<int> in_off, out_off;  // charge offsets: q(b) must equal qa[a'] + off
+    for (int64_t w = 0; w < d.kL; ++w)
+      for (int64_t s1 = 0; s1 < d.d1; ++s1)
+        for (int64_t s2 = 0; s2 < d.d2; ++s2) in_off.push_back(qn->qs1[s1] + qn->qs2[s2] - qn->cL[w]);
+    for (int64_t s1 = 0; s1 < d.d1; ++s1)
+      for (int64_t s2 = 0; s2 < d.d2; ++s2)
+        for (int64_t w2 = 0; w2 < d.kR; ++w2) out_off.push_back(qn->qs1[s1] + qn->qs2[s2] - qn->cR[w2]);
+    std::vector<int> offs(in_off);
+    offs.insert(offs.end(), out_off.begin(), out_off.end());
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    for (int t = 0; t < nbt; ++t) {
+      const int64_t b0 = (int64_t)t * kMpoCols, b1 = std::min<int64_t>(d.mR, b0 + kMpoCols);
+      std::vector<int> tq(qn->qb + b0, qn->qb + b1);
+      tq.erase(std::unique(tq.begin(), tq.end()), tq.end());  // qb sorted
+      for (int64_t ap = 0; ap < d.mL; ++ap) {
+        bool on = false;
+        for (int o : offs) {
+          if (std::binary_search(tq.begin(), tq.end(), qn->qa[ap] + o)) { on = true; break; }
+        }
+        live[(size_t)ap * nbt + t] = on ? 1 : 0;
+      }
+    }
+    cudaFree(p->mpo_live);
+    p->mpo_live = nullptr;
+    CK(cudaMalloc(&p->mpo_live, live.size()));
+    CK(cudaMemcpy(p->mpo_live, live.data(), live.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemset(p->T3, 0, sizeof(double) * d.mL * d.d1 * d.d2 * d.kR * d.mR));
+  }
   return HEFF_OK;
 }

@@ -31,10 +31,14 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
                                                               int64_t mR, int nin, int nout,
                                                               const int* __restrict__ rowptr,
                                                               const int* __restrict__ col,
-                                                              const double* __restrict__ val) {
+                                                              const double* __restrict__ val,
+                                                              const unsigned char* __restrict__ live) {
   extern __shared__ __align__(16) double s_in[];  // [nin][kMpoCols]
   __shared__ uint64_t bar;
   const int64_t ap = blockIdx.y;
+  // U(1) plans: blocks whose input and output are zero by symmetry are skipped (their T3
+  // entries were zeroed once by heff_set_qn)
+  if (live && !live[ap * gridDim.x + blockIdx.x]) return;
   const int64_t b0 = (int64_t)blockIdx.x * kMpoCols;
   const int width = (int)min((int64_t)kMpoCols, mR - b0);
   const double* in = T1 + ap * nin * mR + b0;

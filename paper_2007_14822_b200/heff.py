@@ -17,7 +17,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libheff.so"
 
 HEFF_OK, HEFF_EINVAL, HEFF_ENOMEM, HEFF_ECUDA, HEFF_ENCCL, HEFF_EZERO, HEFF_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
-OPT_GEMM_PATH, OPT_LAST_KERNEL_COUNT, OPT_MPO_NNZ, OPT_PROFILE, OPT_TOTAL_LAUNCHES = 1, 2, 3, 4, 5
+OPT_GEMM_PATH, OPT_LAST_KERNEL_COUNT, OPT_MPO_NNZ, OPT_PROFILE, OPT_TOTAL_LAUNCHES, OPT_SPARSE_KBLOCKS = 1, 2, 3, 4, 5, 6
 
 
 class HeffError(RuntimeError):
@@ -41,6 +41,10 @@ class _Dist(ctypes.Structure):
 
 class _EnvDims(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("mi", "d", "mo", "kl", "kr")]
+
+
+class _QN(ctypes.Structure):
+    _fields_ = [(n, ctypes.POINTER(ctypes.c_int)) for n in ("qa", "qb", "qs1", "qs2", "cL", "cM", "cR")]
 
 
 class _LanczosOpts(ctypes.Structure):
@@ -77,13 +81,14 @@ def lib() -> ctypes.CDLL:
         L.heff_set_penalty.argtypes = [vp, vp, ip, ctypes.c_double, vp]
         dp = ctypes.POINTER(ctypes.c_double)
         L.heff_tridiag_lowest.argtypes = [ip, dp, dp, dp, dp]
+        L.heff_set_qn.argtypes = [vp, ctypes.POINTER(_QN)]
         L.heff_gemm.argtypes = [i64, i64, i64, vp, i64, vp, i64, ip, vp, i64, ip, ip, vp]
         L.heff_env_update_left.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         L.heff_env_update_right.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         for f in ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-                  "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm"):
+                  "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -92,7 +97,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy", "heff_last_error",
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-            "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm")
+            "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn")
 
 
 def _check(rc: int):
@@ -256,6 +261,17 @@ class Heff:
         if phis.numel() % n:
             raise ValueError("phis must hold whole psi-shaped vectors")
         _check(lib().heff_set_penalty(self._h, phis.data_ptr(), phis.numel() // n, float(weight), _stream(stream)))
+
+    def set_qn(self, qn: dict | None):
+        """Declare U(1) charges (keys qa, qb, qs1, qs2, cL, cM, cR; see heff.h) so the GEMMs
+        skip k-blocks that vanish by symmetry; None returns to dense."""
+        if qn is None:
+            _check(lib().heff_set_qn(self._h, None))
+            return
+        import numpy as np
+        arrs = {k: np.ascontiguousarray(qn[k], dtype=np.int32) for k in ("qa", "qb", "qs1", "qs2", "cL", "cM", "cR")}
+        c = _QN(*[a.ctypes.data_as(ctypes.POINTER(ctypes.c_int)) for a in arrs.values()])
+        _check(lib().heff_set_qn(self._h, ctypes.byref(c)))
 
     # -- shapes
     @property
