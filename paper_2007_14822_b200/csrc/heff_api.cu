@@ -318,6 +318,11 @@ struct heff_plan_s {
   int* sp4 = nullptr;
   int64_t sp_kblocks = 0;  // k-block x tile products scheduled per matvec (both GEMMs)
   unsigned char* mpo_live = nullptr;  // [mL][b-tiles]: MPO blocks that can be nonzero (U(1) plans)
+  // U(1) plans: Lanczos keeps only the sector's entries (positions qn_idx into psi)
+  int* qn_idx = nullptr;
+  int64_t qn_n = 0;
+  double* dense_in = nullptr;               // zero outside the sector
+  double* dense_out = nullptr;
   // e2e staging
   double *stage_in = nullptr, *stage_out = nullptr;
   // Lanczos
@@ -325,6 +330,7 @@ struct heff_plan_s {
   int basis_cap = 0;
   int64_t ldv = 0;
   double* work = nullptr;                   // w (local length)
+  int64_t work_len = 0;
   double* full = nullptr;                   // gathered full psi (sharded + comm)
   double* gather = nullptr;                 // blocked gather buffer
   double* partial = nullptr;                // [(cap+1)][ldp]
@@ -790,6 +796,10 @@ extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_
 
 // --------------------------------------------------------------------------- Lanczos
 static int g_step_grid = 0;  // co-resident blocks of cgs2_step_kernel (cooperative launch)
+__global__ void gather_kernel(const double* __restrict__ dense, const int* __restrict__ idx, int64_t n,
+                              double* __restrict__ compact);
+__global__ void scatter_kernel(const double* __restrict__ compact, const int* __restrict__ idx, int64_t n,
+                               double* __restrict__ dense);
 
 static int reduce_grid(int64_t n) {
   const int64_t per = (int64_t)kRedThreads * 2 * 8;  // >= 8 pairs per thread
@@ -885,8 +895,16 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   if (o->mode != 0 && o->mode != 1) return set_err(HEFF_EINVAL, "lanczos_ground: mode must be 0 or 1");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int cap = o->max_iter;
-  const int64_t n = vec_len(p);
+  // U(1) plans iterate on the sector's entries only (gather/scatter around each matvec)
+  const bool compact = p->qn_idx != nullptr && !p->sharded && p->terms.empty();
+  const int64_t n_dense = vec_len(p);
+  const int64_t n = compact ? p->qn_n : n_dense;
   const int64_t ldv = (n + 31) / 32 * 32;
+  if (compact && !p->dense_in) {
+    CK(cudaMalloc(&p->dense_in, sizeof(double) * n_dense));
+    CK(cudaMalloc(&p->dense_out, sizeof(double) * n_dense));
+    CK(cudaMemsetAsync(p->dense_in, 0, sizeof(double) * n_dense, s));
+  }
   // (re)allocate the Krylov basis and scratch
   if (p->basis_cap < cap || p->ldv != ldv) {
     cudaFree(p->basis); cudaFree(p->partial); cudaFree(p->scal);
@@ -900,7 +918,12 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     p->basis_cap = cap;
     p->ldv = ldv;
   }
-  if (!p->work) CK(cudaMalloc(&p->work, sizeof(double) * ldv));
+  if (!p->work || p->work_len < ldv) {
+    cudaFree(p->work);
+    p->work = nullptr;
+    CK(cudaMalloc(&p->work, sizeof(double) * ldv));
+    p->work_len = ldv;
+  }
   if (p->sharded && p->comm && !p->full) {
     const heff_dims& d = p->dims;
     CK(cudaMalloc(&p->full, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
@@ -916,7 +939,13 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   double* w = p->work;
 
   // v1 = x0 / ||x0||  (copied into the aligned basis first)
-  CK(cudaMemcpyAsync(V, psi, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  if (compact) {
+    gather_kernel<<<ew_grid(n), 256, 0, s>>>(psi, p->qn_idx, n, V);
+    ++p->total_launches;
+    CK(cudaGetLastError());
+  } else {
+    CK(cudaMemcpyAsync(V, psi, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  }
   CKR(norm2(p, V, n, beta + cap, invb + cap, s));
   double h_nrm = 0.0;
   CK(cudaMemcpyAsync(&h_nrm, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -943,7 +972,15 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   }
   auto step = [&](int j) -> int {  // j = 1-based step: v_j = V[j-1]
     double* vj = V + (int64_t)(j - 1) * ldv;
-    CKR(matvec_local(p, vj, w, s));
+    if (compact) {
+      scatter_kernel<<<ew_grid(n), 256, 0, s>>>(vj, p->qn_idx, n, p->dense_in);
+      CKR(matvec_local(p, p->dense_in, p->dense_out, s));
+      gather_kernel<<<ew_grid(n), 256, 0, s>>>(p->dense_out, p->qn_idx, n, w);
+      p->total_launches += 2;
+      CK(cudaGetLastError());
+    } else {
+      CKR(matvec_local(p, vj, w, s));
+    }
     if (fused) {
       const double* Vc = V;
       int64_t ldv_ = ldv;
@@ -1015,7 +1052,14 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   CK(cudaMemsetAsync(w, 0, sizeof(double) * n, s));
   CKR(multiaxpy(p, V, j_done, ydev, 1.0, w, n, s));
   CKR(norm2(p, w, n, beta + cap, invb + cap, s));
-  scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + cap, psi, n);
+  if (compact) {  // psi = scatter(x), zero outside the sector
+    scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + cap, w, n);
+    CK(cudaMemsetAsync(psi, 0, sizeof(double) * n_dense, s));
+    scatter_kernel<<<ew_grid(n), 256, 0, s>>>(w, p->qn_idx, n, psi);
+    p->total_launches += 1;
+  } else {
+    scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + cap, psi, n);
+  }
   ++p->total_launches;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
@@ -1333,8 +1377,12 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
   if (!p) return set_err(HEFF_EINVAL, "heff_set_qn: null plan");
   if (!qn) {  // back to dense
     cudaFree(p->sp1); cudaFree(p->sp4); cudaFree(p->mpo_live);
+    cudaFree(p->qn_idx); cudaFree(p->dense_in); cudaFree(p->dense_out);
     p->sp1 = p->sp4 = nullptr;
     p->mpo_live = nullptr;
+    p->qn_idx = nullptr;
+    p->dense_in = p->dense_out = nullptr;
+    p->qn_n = 0;
     p->g1.sp_order = p->g1.sp_ptr = p->g1.sp_list = nullptr;
     p->g4.sp_order = p->g4.sp_ptr = p->g4.sp_list = nullptr;
     p->sp_kblocks = 0;
@@ -1431,5 +1479,43 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
     CK(cudaMemcpy(p->mpo_live, live.data(), live.size(), cudaMemcpyHostToDevice));
     CK(cudaMemset(p->T3, 0, sizeof(double) * d.mL * d.d1 * d.d2 * d.kR * d.mR));
   }
+  // sector positions of psi: for each (a,s1,s2) the b-range with qb[b] = qa[a] + qs1 + qs2
+  {
+    std::vector<int> idx;
+    const int64_t n = d.mL * d.d1 * d.d2 * d.mR;
+    if (n <= INT32_MAX) {
+      for (int64_t a = 0; a < d.mL; ++a)
+        for (int64_t s1 = 0; s1 < d.d1; ++s1)
+          for (int64_t s2 = 0; s2 < d.d2; ++s2) {
+            const int q = qn->qa[a] + qn->qs1[s1] + qn->qs2[s2];
+            const int* lo = std::lower_bound(qn->qb, qn->qb + d.mR, q);
+            const int* hi = std::upper_bound(qn->qb, qn->qb + d.mR, q);
+            const int64_t base = ((a * d.d1 + s1) * d.d2 + s2) * d.mR;
+            for (const int* b = lo; b < hi; ++b) idx.push_back((int)(base + (b - qn->qb)));
+          }
+      cudaFree(p->qn_idx);
+      cudaFree(p->dense_in);
+      cudaFree(p->dense_out);
+      p->qn_idx = nullptr;
+      p->dense_in = p->dense_out = nullptr;
+      p->qn_n = (int64_t)idx.size();
+      if (p->qn_n > 0) {
+        CK(cudaMalloc(&p->qn_idx, sizeof(int) * idx.size()));
+        CK(cudaMemcpy(p->qn_idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice));
+      }
+    }
+  }
   return HEFF_OK;
+}
+
+__global__ void gather_kernel(const double* __restrict__ dense, const int* __restrict__ idx, int64_t n,
+                              double* __restrict__ compact) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    compact[i] = dense[idx[i]];
+}
+
+__global__ void scatter_kernel(const double* __restrict__ compact, const int* __restrict__ idx, int64_t n,
+                               double* __restrict__ dense) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dense[idx[i]] = compact[i];
 }

@@ -94,3 +94,22 @@ def test_qn_errors(dev):
         h.set_qn(z.qn_dict())
         h.set_qn(None)                      # back to dense
         h.apply(xd.psi)
+
+
+@pytest.mark.parametrize("case", ["chain_m256", "cylinder_m256"])
+def test_qn_lanczos_fixed_steps_parity(dev, orc, case):
+    """Sector-compact Lanczos on the GPU vs the oracle's dense Lanczos on the same inputs."""
+    from paper_2007_14822_b200 import Heff
+    z = CASES[case]()
+    L, W1, W2, R, psi = z.x.numpy()
+    o = orc.lanczos_heff(L, W1, W2, R, psi, max_iter=12)
+    xd = z.x.to(dev)
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        h.set_qn(z.qn_dict())
+        v = xd.psi.clone()
+        r = h.lanczos_ground(v, max_iter=12)
+    assert r.iters == o.iters == 12
+    assert abs(r.energy - o.energy) <= 1e-10 * max(1.0, abs(o.energy))
+    vc = v.cpu().numpy()
+    assert np.abs(vc[~z.mask()]).max() == 0.0
+    assert abs(abs(np.vdot(vc, o.x)) - 1.0) < 1e-8

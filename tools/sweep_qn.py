@@ -65,13 +65,20 @@ def main():
             h.set_option(OPT_PROFILE, 1)
             h.apply(x.psi, out)
             g1, mpo_ms, g4, _ = h.last_timings()
+            h.set_option(OPT_PROFILE, 0)
+            steps = 3 if d["mL"] >= 4096 else 20
+            h.lanczos_ground(x.psi.clone(), max_iter=steps)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            h.lanczos_ground(x.psi.clone(), max_iter=steps)
+            lz_sparse = (time.perf_counter() - t1) / steps * 1e3
         sched_flops = nkb * 2.0 * 128 * 128 * 16        # tile-padded work actually scheduled
         row = {"config": name, **d, "gen_s": round(gen, 1), "sector_dim": int(z.mask().sum()),
                "dense_elems": int(z.mask().size), "dense_ms": ms_dense, "sparse_ms": ms_sparse,
                "speedup": ms_dense / ms_sparse, "rel_diff_vs_dense": err, "sched_kblock_tiles": nkb,
                "sched_gemm_tflops": sched_flops / ((g1 + g4) / 1e3) / 1e12 if (g1 + g4) else None,
                "sparse_gemm_first_ms": g1, "sparse_mpo_ms": mpo_ms, "sparse_gemm_last_ms": g4,
-               "dense_equiv_tflops": flops / ms_sparse / 1e9}
+               "dense_equiv_tflops": flops / ms_sparse / 1e9, "sparse_lanczos_step_ms": lz_sparse}
         print(json.dumps(row), flush=True)
         rows.append(row)
         del x, z
