@@ -68,6 +68,31 @@ def model_inputs(Ws: list[np.ndarray], window: int, m: int, seed: int, device="c
                       psi.contiguous(), m_)
 
 
+def model_inputs_complex(Ws: list, window: int, m: int, seed: int, device="cpu") -> HeffInputs:
+    """Complex analogue of model_inputs: random complex orthonormal MPS (real and imaginary
+    parts N(0,1) from default_rng(seed)), environments with the bra side conjugated, psi
+    complex N(0,1) from default_rng(seed+1), unit norm."""
+    N = len(Ws)
+    d = Ws[0].shape[1]
+    k = Ws[0].shape[0]
+    rng = np.random.default_rng(seed)
+    tW = [torch.from_numpy(np.ascontiguousarray(W, dtype=np.complex128)).to(device) for W in Ws]
+    As = env.draw_left_block(rng, window, d, m, device, complex_=True)
+    Bs = env.draw_right_block(rng, N - window - 2, d, m, device, complex_=True)
+    L = env.build_left_env(As, tW[:window], k, device)
+    R = env.build_right_env(Bs, tW[window + 2:], k, device)
+    r2 = np.random.default_rng(seed + 1)
+    shape = (L.shape[0], d, d, R.shape[0])
+    x = r2.standard_normal(shape) + 1j * r2.standard_normal(shape)
+    x /= np.linalg.norm(x)
+    return HeffInputs(L.contiguous(), tW[window].contiguous(), tW[window + 1].contiguous(), R.contiguous(),
+                      torch.from_numpy(x).to(device), dict(N=N, window=window, m_cap=m, seed=seed, complex=True))
+
+
+def dm_chain(N: int, window: int, m: int, seed: int, D: float = 0.5, device="cpu") -> HeffInputs:
+    return model_inputs_complex([mpo.dm_chain_W(D)] * N, window, m, seed, device)
+
+
 def model_inputs_terms(Ws_terms: list, window: int, m: int, seed: int, device="cpu") -> list:
     """Environments of ONE random orthonormal MPS for several MPOs (an MPO sum,
     P:L739-750).  Ws_terms[t][j] is term t's MPO tensor at site j.  The MPS draws are the

@@ -39,6 +39,25 @@ def heisenberg_chain_W() -> np.ndarray:
     return W
 
 
+def dm_chain_W(D: float = 0.5) -> np.ndarray:
+    """Complex Hermitian MPO (k = 5): Eq. (1) plus a Dzyaloshinskii-Moriya term
+    D (Sx_i Sy_{i+1} - Sy_i Sx_{i+1}) = (iD/2)(S+_i S-_{i+1} - S-_i S+_{i+1}), i.e. bond
+    1/2 (1 + iD) S+_i S-_{i+1} + 1/2 (1 - iD) S-_i S+_{i+1} + Sz_i Sz_{i+1}
+    (the NEXT-4 complex workload; reading R19)."""
+    k = 5
+    W = np.zeros((k, 2, 2, k), dtype=np.complex128)
+    start, done = k - 1, 0
+    W[start, :, :, start] = I2
+    W[done, :, :, done] = I2
+    W[start, :, :, 1] = 0.5 * (1 - 1j * D) * SM
+    W[start, :, :, 2] = 0.5 * (1 + 1j * D) * SP
+    W[start, :, :, 3] = SZ
+    W[1, :, :, done] = SP
+    W[2, :, :, done] = SM
+    W[3, :, :, done] = SZ
+    return W
+
+
 def heisenberg_zz_W() -> np.ndarray:
     """The Sz Sz part of Eq. (1) alone (k = 3): one term of an MPO sum."""
     k = 3

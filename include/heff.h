@@ -99,6 +99,15 @@ typedef struct {
 int heff_create(heff_plan* out, const heff_dims* dims, const double* L, const double* W1, const double* W2,
                 const double* R, const heff_dist* dist, heff_stream stream);
 
+/* Complex plans (ITensor's Dense{ComplexF64}/zgemm):
+ * same as heff_create with L, W1, W2, R -- and later psi/out -- as interleaved complex
+ * (re, im) fp64 arrays, 16-byte aligned.  (D) is evaluated without conjugation, so a
+ * Hermitian H_eff needs environments built with the bra tensors conjugated.
+ * heff_apply / heff_apply_host / lanczos_ground (Hermitian Lanczos, <v,w> = sum conj(v) w)
+ * accept complex plans; sharding, U(1) sparsity, penalties and sums do not (EUNSUPPORTED). */
+int heff_create_z(heff_plan* out, const heff_dims* dims, const double* L, const double* W1, const double* W2,
+                  const double* R, const heff_dist* dist, heff_stream stream);
+
 /* out = H_eff . psi  (D).  dist == NULL: psi, out are full [mL][d1][d2][mR].
  * Sharded plan: psi is the FULL vector, out is this rank's shard [mL][d1][d2][nb].
  * out must not alias psi.  Asynchronous on `stream`. */

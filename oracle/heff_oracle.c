@@ -545,3 +545,173 @@ int ref_env_right(int64_t mi, int64_t d, int64_t mo, int64_t kl, int64_t kr, con
   free(Y);
   return 0;
 }
+
+/* ---------------------------------------------------------------------------------
+ * Complex variant (ITensor's Dense{ComplexF64} storage and zgemm,
+ * PAPER.md:583).  (D) is unchanged -- no conjugation inside the
+ * contraction; Hermiticity comes from environments built with the bra tensors
+ * conjugated.  Arrays are interleaved complex (double _Complex).  Order A, a' range.
+ * ------------------------------------------------------------------------------- */
+#include <complex.h>
+
+int ref_heff_apply_A_z(const oracle_dims* D, const double _Complex* L, const double _Complex* W1,
+                       const double _Complex* W2, const double _Complex* R, const double _Complex* psi, int64_t a_lo,
+                       int64_t a_hi, double _Complex* out_rows) {
+  const int64_t mL = D->mL, d1 = D->d1, d2 = D->d2, mR = D->mR, kL = D->kL, kM = D->kM, kR = D->kR;
+  if (a_lo < 0 || a_hi > mL || a_lo > a_hi) return -1;
+  int err = 0;
+#pragma omp parallel
+  {
+    double _Complex* T1 = (double _Complex*)malloc(sizeof(double _Complex) * kL * d1 * d2 * mR);
+    double _Complex* T2 = (double _Complex*)malloc(sizeof(double _Complex) * d1 * kM * d2 * mR);
+    double _Complex* T3 = (double _Complex*)malloc(sizeof(double _Complex) * d1 * d2 * kR * mR);
+    if (!T1 || !T2 || !T3) {
+#pragma omp atomic write
+      err = -2;
+    } else {
+#pragma omp for schedule(dynamic, 1)
+      for (int64_t ap = a_lo; ap < a_hi; ++ap) {
+        for (int64_t x = 0; x < kL * d1 * d2 * mR; ++x) T1[x] = 0;
+        for (int64_t w = 0; w < kL; ++w)
+          for (int64_t a = 0; a < mL; ++a) {
+            const double _Complex l = L[IDX3(ap, w, a, kL, mL)];
+            double _Complex* t = T1 + w * d1 * d2 * mR;
+            const double _Complex* p = psi + a * d1 * d2 * mR;
+            for (int64_t x = 0; x < d1 * d2 * mR; ++x) t[x] += l * p[x];
+          }
+        for (int64_t x = 0; x < d1 * kM * d2 * mR; ++x) T2[x] = 0;
+        for (int64_t s1p = 0; s1p < d1; ++s1p)
+          for (int64_t w1 = 0; w1 < kM; ++w1)
+            for (int64_t w = 0; w < kL; ++w)
+              for (int64_t s1 = 0; s1 < d1; ++s1) {
+                const double _Complex c = W1[IDX4(w, s1p, s1, w1, d1, d1, kM)];
+                double _Complex* t2 = T2 + IDX3(s1p, w1, 0, kM, d2 * mR);
+                const double _Complex* t1 = T1 + IDX3(w, s1, 0, d1, d2 * mR);
+                for (int64_t x = 0; x < d2 * mR; ++x) t2[x] += c * t1[x];
+              }
+        for (int64_t x = 0; x < d1 * d2 * kR * mR; ++x) T3[x] = 0;
+        for (int64_t s1p = 0; s1p < d1; ++s1p)
+          for (int64_t s2p = 0; s2p < d2; ++s2p)
+            for (int64_t w2 = 0; w2 < kR; ++w2)
+              for (int64_t w1 = 0; w1 < kM; ++w1)
+                for (int64_t s2 = 0; s2 < d2; ++s2) {
+                  const double _Complex c = W2[IDX4(w1, s2p, s2, w2, d2, d2, kR)];
+                  double _Complex* t3 = T3 + IDX4(s1p, s2p, w2, 0, d2, kR, mR);
+                  const double _Complex* t2 = T2 + IDX4(s1p, w1, s2, 0, kM, d2, mR);
+                  for (int64_t b = 0; b < mR; ++b) t3[b] += c * t2[b];
+                }
+        double _Complex* o = out_rows + (ap - a_lo) * d1 * d2 * mR;
+        for (int64_t s = 0; s < d1 * d2; ++s)
+          for (int64_t bp = 0; bp < mR; ++bp) {
+            double _Complex acc = 0;
+            const double _Complex* t3 = T3 + s * kR * mR;
+            const double _Complex* r = R + bp * kR * mR;
+            for (int64_t x = 0; x < kR * mR; ++x) acc += t3[x] * r[x];
+            o[s * mR + bp] = acc;
+          }
+      }
+    }
+    free(T1);
+    free(T2);
+    free(T3);
+  }
+  return err;
+}
+
+/* Hermitian Lanczos with CGS2 (same readings as ref_lanczos; <v,w> = sum conj(v) w).
+ * matvec(ctx, in, out) on interleaved complex vectors of n complex entries. */
+typedef void (*oracle_zmatvec_fn)(void* ctx, const double _Complex* in, double _Complex* out);
+
+static double _Complex zdotc(int64_t n, const double _Complex* x, const double _Complex* y) {
+  double _Complex s = 0;
+  for (int64_t i = 0; i < n; ++i) s += conj(x[i]) * y[i];
+  return s;
+}
+
+int ref_lanczos_z(oracle_zmatvec_fn matvec, void* ctx, int64_t n, const double _Complex* x0, int max_iter, double tol,
+                  int mode, double* energy, double _Complex* x_out, int* iters_done, double* alpha_out,
+                  double* beta_out, double* theta_hist) {
+  if (n <= 0 || max_iter <= 0) return -1;
+  double nrm = sqrt(creal(zdotc(n, x0, x0)));
+  if (!(nrm > 0.0)) return -5;
+  double _Complex* V = (double _Complex*)malloc(sizeof(double _Complex) * n * (size_t)(max_iter + 1));
+  double _Complex* w = (double _Complex*)malloc(sizeof(double _Complex) * n);
+  double* alpha = (double*)calloc(max_iter + 1, sizeof(double));
+  double* beta = (double*)calloc(max_iter + 1, sizeof(double));
+  double* y = (double*)calloc(max_iter + 1, sizeof(double));
+  double _Complex* c = (double _Complex*)calloc(max_iter + 1, sizeof(double _Complex));
+  if (!V || !w || !alpha || !beta || !y || !c) {
+    free(V); free(w); free(alpha); free(beta); free(y); free(c);
+    return -2;
+  }
+  for (int64_t i = 0; i < n; ++i) V[i] = x0[i] / nrm;
+  double hnorm = 0.0, theta = 0.0;
+  int j = 0;
+  for (j = 1; j <= max_iter; ++j) {
+    const double _Complex* vj = V + (int64_t)(j - 1) * n;
+    matvec(ctx, vj, w);
+    alpha[j - 1] = creal(zdotc(n, vj, w));
+    for (int64_t i = 0; i < n; ++i) w[i] -= alpha[j - 1] * vj[i];
+    if (j > 1) {
+      const double _Complex* vjm = V + (int64_t)(j - 2) * n;
+      for (int64_t i = 0; i < n; ++i) w[i] -= beta[j - 2] * vjm[i];
+    }
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int q = 0; q < j; ++q) c[q] = zdotc(n, V + (int64_t)q * n, w);
+      for (int q = 0; q < j; ++q) {
+        const double _Complex* vq = V + (int64_t)q * n;
+        for (int64_t i = 0; i < n; ++i) w[i] -= c[q] * vq[i];
+      }
+    }
+    beta[j - 1] = sqrt(creal(zdotc(n, w, w)));
+    ref_tridiag_lowest(j, alpha, beta, &theta, y);
+    if (theta_hist) theta_hist[j - 1] = theta;
+    for (int i = 0; i < j; ++i) {
+      const double g = fabs(alpha[i]) + ((i > 0) ? beta[i - 1] : 0.0) + beta[i];
+      if (g > hnorm) hnorm = g;
+    }
+    if (beta[j - 1] <= 1e-12 * hnorm) break;
+    if (mode == 1 && beta[j - 1] * fabs(y[j - 1]) <= tol * hnorm) break;
+    if (j == max_iter) break;
+    double _Complex* vn = V + (int64_t)j * n;
+    for (int64_t i = 0; i < n; ++i) vn[i] = w[i] / beta[j - 1];
+  }
+  if (j > max_iter) j = max_iter;
+  if (x_out) {
+    for (int64_t i = 0; i < n; ++i) x_out[i] = 0;
+    for (int q = 0; q < j; ++q) {
+      const double _Complex* vq = V + (int64_t)q * n;
+      for (int64_t i = 0; i < n; ++i) x_out[i] += y[q] * vq[i];
+    }
+    const double xn = sqrt(creal(zdotc(n, x_out, x_out)));
+    for (int64_t i = 0; i < n; ++i) x_out[i] /= xn;
+  }
+  *energy = theta;
+  *iters_done = j;
+  if (alpha_out) memcpy(alpha_out, alpha, sizeof(double) * j);
+  if (beta_out) memcpy(beta_out, beta, sizeof(double) * j);
+  free(V); free(w); free(alpha); free(beta); free(y); free(c);
+  return 0;
+}
+
+typedef struct {
+  oracle_dims dims;
+  const double _Complex *L, *W1, *W2, *R;
+} oracle_heff_z_ctx;
+
+void oracle_heff_matvec_z(void* vctx, const double _Complex* in, double _Complex* out) {
+  oracle_heff_z_ctx* c = (oracle_heff_z_ctx*)vctx;
+  ref_heff_apply_A_z(&c->dims, c->L, c->W1, c->W2, c->R, in, 0, c->dims.mL, out);
+}
+
+int ref_lanczos_heff_z(const oracle_dims* D, const double _Complex* L, const double _Complex* W1,
+                       const double _Complex* W2, const double _Complex* R, const double _Complex* x0, int max_iter,
+                       double tol, int mode, double* energy, double _Complex* x_out, int* iters_done,
+                       double* alpha_out, double* beta_out, double* theta_hist) {
+  oracle_heff_z_ctx c;
+  c.dims = *D;
+  c.L = L; c.W1 = W1; c.W2 = W2; c.R = R;
+  const int64_t n = D->mL * D->d1 * D->d2 * D->mR;
+  return ref_lanczos_z(oracle_heff_matvec_z, &c, n, x0, max_iter, tol, mode, energy, x_out, iters_done, alpha_out,
+                       beta_out, theta_hist);
+}

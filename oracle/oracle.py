@@ -60,6 +60,12 @@ def lib():
         _lib.ref_lanczos_heff.argtypes = [ctypes.POINTER(_Dims), dp, dp, dp, dp, dp, ctypes.c_int, ctypes.c_double,
                                           ctypes.c_int, dp, dp, ctypes.POINTER(ctypes.c_int), dp, dp, dp]
         _lib.ref_lanczos_heff.restype = ctypes.c_int
+        _lib.ref_heff_apply_A_z.argtypes = [ctypes.POINTER(_Dims), dp, dp, dp, dp, dp, ctypes.c_int64,
+                                            ctypes.c_int64, dp]
+        _lib.ref_heff_apply_A_z.restype = ctypes.c_int
+        _lib.ref_lanczos_heff_z.argtypes = [ctypes.POINTER(_Dims), dp, dp, dp, dp, dp, ctypes.c_int, ctypes.c_double,
+                                            ctypes.c_int, dp, dp, ctypes.POINTER(ctypes.c_int), dp, dp, dp]
+        _lib.ref_lanczos_heff_z.restype = ctypes.c_int
         i64 = ctypes.c_int64
         for f in (_lib.ref_env_left, _lib.ref_env_right):
             f.argtypes = [i64, i64, i64, i64, i64, dp, dp, dp, dp]
@@ -126,6 +132,41 @@ def heff_apply_B(L, W1, W2, R, psi, cols: tuple[int, int] | None = None) -> np.n
     if rc != 0:
         raise RuntimeError(f"ref_heff_apply_B failed: {rc}")
     return out
+
+
+def _cz(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+def _pz(a: np.ndarray):
+    assert a.dtype == np.complex128 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def heff_apply_z(L, W1, W2, R, psi, rows: tuple[int, int] | None = None) -> np.ndarray:
+    """Complex order A (heff_oracle.c ref_heff_apply_A_z); no conjugation inside (D)."""
+    L, W1, W2, R, psi = map(_cz, (L, W1, W2, R, psi))
+    D = dims_of(L, W1, W2, R)
+    a_lo, a_hi = rows if rows is not None else (0, D.mL)
+    out = np.empty((a_hi - a_lo, D.d1, D.d2, D.mR), dtype=np.complex128)
+    rc = lib().ref_heff_apply_A_z(ctypes.byref(D), _pz(L), _pz(W1), _pz(W2), _pz(R), _pz(psi), a_lo, a_hi, _pz(out))
+    if rc != 0:
+        raise RuntimeError(f"ref_heff_apply_A_z failed: {rc}")
+    return out
+
+
+def lanczos_heff_z(L, W1, W2, R, x0, max_iter: int, tol: float = 0.0, converge: bool = False) -> "LanczosResult":
+    """Hermitian Lanczos (CGS2, <v,w> = sum conj(v) w) on the complex H_eff, all in C."""
+    L, W1, W2, R = map(_cz, (L, W1, W2, R))
+    D = dims_of(L, W1, W2, R)
+    x0 = _cz(x0)
+    e, it = ctypes.c_double(), ctypes.c_int()
+    x = np.empty_like(x0)
+    al, be, th = np.zeros(max_iter + 1), np.zeros(max_iter + 1), np.zeros(max_iter + 1)
+    rc = lib().ref_lanczos_heff_z(ctypes.byref(D), _pz(L), _pz(W1), _pz(W2), _pz(R), _pz(x0), max_iter, tol,
+                                  1 if converge else 0, ctypes.byref(e), _pz(x), ctypes.byref(it), _p(al), _p(be),
+                                  _p(th))
+    return _lanczos_out(rc, e, x, it, al, be, th)
 
 
 def heff_apply_penalty(L, W1, W2, R, psi, phis, weight: float) -> np.ndarray:

@@ -123,10 +123,91 @@ __global__ void scale_kernel(const double* __restrict__ x, const double* __restr
     y[i] = x[i] * f;
 }
 
-// alpha[j] = c1[j] + c2[j]  (the two CGS passes' coefficient on v_j)
+// alpha[j] = Re(c1[j] + c2[j])  (the two CGS passes' coefficient on v_j; stride 2 for
+// interleaved complex coefficients, whose real part is read)
 __global__ void lanczos_alpha_kernel(const double* __restrict__ c1, const double* __restrict__ c2, int j,
-                                     double* __restrict__ alpha) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) alpha[j] = c1[j] + c2[j];
+                                     double* __restrict__ alpha, int stride) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) alpha[j] = c1[stride * j] + c2[stride * j];
+}
+
+// ---- complex (interleaved) vectors: <v,w> = sum conj(v) w -----------------------------
+// partial[2q][b] / partial[2q+1][b] = Re / Im of block b's sum of conj(V_q[i]) w[i],
+// i over n complex entries; V rows are ldv doubles apart (16-byte aligned).
+__global__ void __launch_bounds__(kRedThreads) zmultidot_partial_kernel(const double* __restrict__ V, int64_t ldv,
+                                                                        int nq, const double* __restrict__ w,
+                                                                        int64_t n, double* __restrict__ partial,
+                                                                        int ldp) {
+  double re[kDotQ], im[kDotQ];
+#pragma unroll
+  for (int q = 0; q < kDotQ; ++q) re[q] = im[q] = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kRedThreads) {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(w) + i);
+#pragma unroll
+    for (int q = 0; q < kDotQ; ++q)
+      if (q < nq) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(V + q * ldv) + i);
+        re[q] = fma(v.x, x.x, fma(v.y, x.y, re[q]));
+        im[q] = fma(v.x, x.y, fma(-v.y, x.x, im[q]));
+      }
+  }
+  __shared__ double red[2 * kDotQ][kRedThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < kDotQ; ++q) {
+    const double a = warp_sum(re[q]), b = warp_sum(im[q]);
+    if (lane == 0) {
+      red[2 * q][warp] = a;
+      red[2 * q + 1][warp] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * nq) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRedThreads / 32; ++k) t += red[threadIdx.x][k];
+    partial[threadIdx.x * ldp + blockIdx.x] = t;
+  }
+}
+
+// w[i] += sign * sum_q c_q V_q[i]; c interleaved complex (nq <= 64), w and V interleaved
+__global__ void __launch_bounds__(256) zmultiaxpy_kernel(const double* __restrict__ V, int64_t ldv, int nq,
+                                                         const double* __restrict__ c, double sign,
+                                                         double* __restrict__ w, int64_t n) {
+  __shared__ double sc[128];
+  if (threadIdx.x < 2 * nq) sc[threadIdx.x] = sign * c[threadIdx.x];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 x = reinterpret_cast<double2*>(w)[i];
+    for (int q = 0; q < nq; ++q) {
+      const double2 v = __ldcs(reinterpret_cast<const double2*>(V + q * ldv) + i);
+      const double cr = sc[2 * q], ci = sc[2 * q + 1];
+      x.x = fma(cr, v.x, fma(-ci, v.y, x.x));
+      x.y = fma(cr, v.y, fma(ci, v.x, x.y));
+    }
+    reinterpret_cast<double2*>(w)[i] = x;
+  }
+}
+
+// planes[0][i] = Re z[i], planes[1][i] = Im z[i]  (and back)
+__global__ void deinterleave_kernel(const double* __restrict__ z, double* __restrict__ re, double* __restrict__ im,
+                                    int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = reinterpret_cast<const double2*>(z)[i];
+    re[i] = v.x;
+    im[i] = v.y;
+  }
+}
+
+__global__ void interleave_kernel(const double* __restrict__ re, const double* __restrict__ im, double* __restrict__ z,
+                                  int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<double2*>(z)[i] = make_double2(re[i], im[i]);
+}
+
+// out = -x (the negated imaginary planes of the complex environments)
+__global__ void negate_kernel(const double* __restrict__ x, double* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = -x[i];
 }
 
 // ------------------------------------------------------------------------------------

@@ -162,6 +162,7 @@ struct GemmOp {
 };
 
 static int g_num_sms = 0;
+static int ew_grid(int64_t n);
 
 static bool tma_ok(const GemmOp& g) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -291,6 +292,14 @@ struct heff_plan_s {
   heff_dims dims{};
   // composite plan (MPO sum): borrowed term plans, applied and summed
   std::vector<heff_plan_s*> terms;
+  // complex plans (heff_create_z): planar copies [re, im, -im] of L and R, planar T1/T3
+  bool is_complex = false;
+  double* Lp = nullptr;
+  double* Rp = nullptr;
+  double* zin = nullptr;                    // psi planes [2][n]
+  double* zout = nullptr;                   // out planes [2][n]
+  int64_t t1_plane = 0, t3_plane = 0;
+  GemmOp gz1[4], gz4[4];
   // energy penalty: out += weight * sum_i phi_i <phi_i|psi>
   double* phis = nullptr;                   // [nphi][ldv_phi], plan-owned copy
   int nphi = 0;
@@ -564,6 +573,124 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
   return HEFF_OK;
 }
 
+// --------------------------------------------------------------------------- complex plans
+// NEXT-4: ITensor's Dense{ComplexF64} + zgemm.  (D) has no
+// conjugation; each complex GEMM is four real DMMA GEMMs on planar copies (the negated
+// imaginary planes of L and R turn the subtraction into an accumulating GEMM) and the two
+// MPO steps run as one real MPO kernel on stacked [re; im] rows with the 2x2 blocks
+// [[Re, -Im], [Im, Re]] of the complex two-site MPO.
+static int build_mpo_csr_complex(heff_plan_s* p, const std::vector<double>& W1z, const std::vector<double>& W2z) {
+  const int64_t kL = p->dims.kL, kM = p->dims.kM, kR = p->dims.kR, d1 = p->dims.d1, d2 = p->dims.d2;
+  auto W1 = [&](int64_t w, int64_t s1p, int64_t s1, int64_t w1, int c) {
+    return W1z[2 * (((w * d1 + s1p) * d1 + s1) * kM + w1) + c];
+  };
+  auto W2 = [&](int64_t w1, int64_t s2p, int64_t s2, int64_t w2, int c) {
+    return W2z[2 * (((w1 * d2 + s2p) * d2 + s2) * kR + w2) + c];
+  };
+  const int64_t nin = kL * d1 * d2, nout = d1 * d2 * kR;
+  std::vector<std::vector<std::pair<int, double>>> rows(2 * nout);
+  for (int64_t s1p = 0; s1p < d1; ++s1p)
+    for (int64_t s2p = 0; s2p < d2; ++s2p)
+      for (int64_t w2 = 0; w2 < kR; ++w2)
+        for (int64_t w = 0; w < kL; ++w)
+          for (int64_t s1 = 0; s1 < d1; ++s1)
+            for (int64_t s2 = 0; s2 < d2; ++s2) {
+              double re = 0.0, im = 0.0;
+              for (int64_t w1 = 0; w1 < kM; ++w1) {
+                const double ar = W1(w, s1p, s1, w1, 0), ai = W1(w, s1p, s1, w1, 1);
+                const double br = W2(w1, s2p, s2, w2, 0), bi = W2(w1, s2p, s2, w2, 1);
+                re += ar * br - ai * bi;
+                im += ar * bi + ai * br;
+              }
+              const int o = (int)((s1p * d2 + s2p) * kR + w2), c = (int)((w * d1 + s1) * d2 + s2);
+              if (re != 0.0) {
+                rows[o].push_back({c, re});                          // Re out <- Re in
+                rows[nout + o].push_back({(int)nin + c, re});        // Im out <- Im in
+              }
+              if (im != 0.0) {
+                rows[o].push_back({(int)nin + c, -im});              // Re out <- -Im * Im in
+                rows[nout + o].push_back({c, im});                   // Im out <- Im * Re in
+              }
+            }
+  std::vector<int> rp{0}, cl;
+  std::vector<double> vl;
+  for (auto& r : rows) {
+    for (auto& e : r) {
+      cl.push_back(e.first);
+      vl.push_back(e.second);
+    }
+    rp.push_back((int)vl.size());
+  }
+  return build_csr(p->csrA, rp, cl, vl);
+}
+
+extern "C" int heff_create_z(heff_plan* out, const heff_dims* dims, const double* L, const double* W1,
+                             const double* W2, const double* R, const heff_dist* dist, heff_stream stream) {
+  if (!out || !dims || !L || !W1 || !W2 || !R) return set_err(HEFF_EINVAL, "heff_create_z: null argument");
+  *out = nullptr;
+  if (dist) return set_err(HEFF_EUNSUPPORTED, "heff_create_z: complex plans are single-GPU");
+  const heff_dims d = *dims;
+  if (d.mL < 1 || d.mR < 1 || d.d1 < 1 || d.d2 < 1 || d.kL < 1 || d.kM < 1 || d.kR < 1)
+    return set_err(HEFF_EINVAL, "heff_create_z: every dimension must be >= 1");
+  if (2 * d.kL * d.d1 * d.d2 > kMpoMaxRows || 2 * d.d1 * d.d2 * d.kR > kMpoMaxRows)
+    return set_err(HEFF_EUNSUPPORTED, "heff_create_z: 2 k d1 d2 > %d exceeds the MPO kernel's tile", kMpoMaxRows);
+  for (const void* ptr : {(const void*)L, (const void*)W1, (const void*)W2, (const void*)R})
+    if (reinterpret_cast<uintptr_t>(ptr) & 15)
+      return set_err(HEFF_EINVAL, "heff_create_z: complex pointers must be 16-byte aligned");
+  CKR(init_device_once());
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  heff_plan_s* p = new heff_plan_s();
+  p->dims = d;
+  p->is_complex = true;
+  auto fail = [&](int code) {
+    heff_destroy(p);
+    return code;
+  };
+  std::vector<double> W1z(2 * d.kL * d.d1 * d.d1 * d.kM), W2z(2 * d.kM * d.d2 * d.d2 * d.kR);
+  if (cudaMemcpyAsync(W1z.data(), W1, sizeof(double) * W1z.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(W2z.data(), W2, sizeof(double) * W2z.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return fail(set_err(HEFF_EINVAL, "heff_create_z: W1/W2 are not readable device pointers"));
+  int r = build_mpo_csr_complex(p, W1z, W2z);
+  if (r) return fail(r);
+  const int64_t nL = d.mL * d.kL * d.mL, nR = d.mR * d.kR * d.mR, n = d.mL * d.d1 * d.d2 * d.mR;
+  if (cudaMalloc(&p->Lp, sizeof(double) * 3 * nL) != cudaSuccess ||
+      cudaMalloc(&p->Rp, sizeof(double) * 3 * nR) != cudaSuccess ||
+      cudaMalloc(&p->zin, sizeof(double) * 2 * n) != cudaSuccess ||
+      cudaMalloc(&p->zout, sizeof(double) * 2 * n) != cudaSuccess)
+    return fail(set_err(HEFF_ENOMEM, "heff_create_z: cannot allocate planar copies"));
+  deinterleave_kernel<<<ew_grid(2 * nL), 256, 0, s>>>(L, p->Lp, p->Lp + nL, nL);
+  negate_kernel<<<ew_grid(2 * nL), 256, 0, s>>>(p->Lp + nL, p->Lp + 2 * nL, nL);
+  deinterleave_kernel<<<ew_grid(2 * nR), 256, 0, s>>>(R, p->Rp, p->Rp + nR, nR);
+  negate_kernel<<<ew_grid(2 * nR), 256, 0, s>>>(p->Rp + nR, p->Rp + 2 * nR, nR);
+  if (cudaGetLastError() != cudaSuccess) return fail(set_err(HEFF_ECUDA, "heff_create_z: launch failed"));
+  // workspace: planar T1, T3, chunked over a'
+  const int64_t per_row = 2 * (d.kL + d.kR) * d.d1 * d.d2 * d.mR * 8;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return fail(set_err(HEFF_ECUDA, "cudaMemGetInfo failed"));
+  int64_t budget = (int64_t)(0.45 * (double)free_b);
+  if (const char* e = getenv("HEFF_WORKSPACE_MB")) budget = std::atoll(e) * (1ll << 20);
+  int64_t rows = std::max<int64_t>(1, std::min<int64_t>(d.mL, budget / per_row));
+  const int64_t nchunks = (d.mL + rows - 1) / rows;
+  rows = (d.mL + nchunks - 1) / nchunks;
+  p->chunk_rows = rows;
+  p->t1_plane = rows * d.kL * d.d1 * d.d2 * d.mR;
+  p->t3_plane = rows * d.d1 * d.d2 * d.kR * d.mR;
+  if (cudaMalloc(&p->T1, sizeof(double) * 2 * p->t1_plane) != cudaSuccess ||
+      cudaMalloc(&p->T3, sizeof(double) * 2 * p->t3_plane) != cudaSuccess)
+    return fail(set_err(HEFF_ENOMEM, "heff_create_z: cannot allocate T1/T3 workspace"));
+  for (int k = 0; k < 4; ++k) {
+    GemmOp& g1 = p->gz1[k];
+    g1.N = d.d1 * d.d2 * d.mR; g1.K = d.mL; g1.lda = d.mL; g1.ldb = g1.N; g1.b_kmajor = false; g1.ldc = g1.N;
+    GemmOp& g4 = p->gz4[k];
+    g4.N = d.mR; g4.K = d.kR * d.mR; g4.lda = g4.K; g4.ldb = g4.K; g4.b_kmajor = true; g4.ldc = d.mR;
+  }
+  p->L = p->Lp;
+  p->R = p->Rp;
+  *out = p;
+  return HEFF_OK;
+}
+
 extern "C" int heff_set_option(heff_plan p, int option, int64_t value) {
   if (!p) return set_err(HEFF_EINVAL, "null plan");
   switch (option) {
@@ -646,7 +773,7 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     CKR(prof_mark(p, 1, s));
     dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
     mpo_orderA_kernel<<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
-                                                       p->csrA.d_col, p->csrA.d_val, p->mpo_live);
+                                                       p->csrA.d_col, p->csrA.d_val, p->mpo_live, 1, 0, 0);
     CK(cudaGetLastError());
     ++*nl;
     CKR(prof_mark(p, 2, s));
@@ -682,7 +809,62 @@ static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStre
 }
 
 static int64_t vec_len(const heff_plan_s* p);
-static int ew_grid(int64_t n);
+static int apply_orderA_z(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl) {
+  const heff_dims& d = p->dims;
+  const int64_t n = d.mL * d.d1 * d.d2 * d.mR, nL = d.mL * d.kL * d.mL, nR = d.mR * d.kR * d.mR;
+  const double *pre = p->zin, *pim = p->zin + n;
+  deinterleave_kernel<<<ew_grid(2 * n), 256, 0, s>>>(psi, p->zin, p->zin + n, n);
+  ++*nl;
+  const int64_t nin = 2 * d.kL * d.d1 * d.d2, nout = 2 * d.d1 * d.d2 * d.kR;
+  const size_t mpo_smem = sizeof(double) * nin * kMpoCols;
+  for (int64_t a0 = 0; a0 < d.mL; a0 += p->chunk_rows) {
+    const int64_t rows = std::min(p->chunk_rows, d.mL - a0);
+    CKR(prof_mark(p, 0, s));
+    const int64_t lo = a0 * d.kL * d.mL;
+    const double* Lre = p->Lp + lo;
+    const double* Lim = p->Lp + nL + lo;
+    const double* Lneg = p->Lp + 2 * nL + lo;
+    double* T1re = p->T1;
+    double* T1im = p->T1 + p->t1_plane;
+    // T1re = Lre.psi_re - Lim.psi_im ; T1im = Lre.psi_im + Lim.psi_re
+    const double* A1[4] = {Lre, Lneg, Lre, Lim};
+    const double* B1[4] = {pre, pim, pim, pre};
+    double* C1[4] = {T1re, T1re, T1im, T1im};
+    for (int k = 0; k < 4; ++k) {
+      GemmOp& g = p->gz1[k];
+      g.M = rows * d.kL; g.A = A1[k]; g.B = B1[k]; g.C = C1[k]; g.accumulate = k & 1;
+      CKR(launch_gemm(g, p->gemm_path, s, nl, &p->splitws));
+    }
+    CKR(prof_mark(p, 1, s));
+    dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
+    mpo_orderA_kernel<<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
+                                                       p->csrA.d_col, p->csrA.d_val, nullptr, 2, p->t1_plane,
+                                                       p->t3_plane);
+    CK(cudaGetLastError());
+    ++*nl;
+    CKR(prof_mark(p, 2, s));
+    const double *T3re = p->T3, *T3im = p->T3 + p->t3_plane;
+    const double *Rre = p->Rp, *Rim = p->Rp + nR, *Rneg = p->Rp + 2 * nR;
+    double* ore = p->zout + a0 * d.d1 * d.d2 * d.mR;
+    double* oim = p->zout + n + a0 * d.d1 * d.d2 * d.mR;
+    // out_re = T3re.Rre^T - T3im.Rim^T ; out_im = T3re.Rim^T + T3im.Rre^T
+    const double* A4[4] = {T3re, T3im, T3re, T3im};
+    const double* B4[4] = {Rre, Rneg, Rim, Rre};
+    double* C4[4] = {ore, ore, oim, oim};
+    for (int k = 0; k < 4; ++k) {
+      GemmOp& g = p->gz4[k];
+      g.M = rows * d.d1 * d.d2; g.A = A4[k]; g.B = B4[k]; g.C = C4[k]; g.accumulate = k & 1;
+      CKR(launch_gemm(g, p->gemm_path, s, nl, &p->splitws));
+    }
+    CKR(prof_mark(p, 3, s));
+  }
+  interleave_kernel<<<ew_grid(2 * n), 256, 0, s>>>(p->zout, p->zout + n, out, n);
+  ++*nl;
+  CK(cudaGetLastError());
+  return HEFF_OK;
+}
+
+
 
 // out += weight * Phi (Phi^T psi): the excited-state energy penalty
 static int apply_penalty(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl) {
@@ -720,6 +902,11 @@ static int apply_impl(heff_plan_s* p, const double* psi, double* out, cudaStream
       r = apply_impl(p->terms[t], psi, out, s, (t > 0 || accumulate) ? 1 : 0);
       nl += p->terms[t]->last_launches;
     }
+  } else if (p->is_complex) {
+    if (accumulate) return set_err(HEFF_EUNSUPPORTED, "complex plans cannot be terms of a sum");
+    if ((reinterpret_cast<uintptr_t>(psi) | reinterpret_cast<uintptr_t>(out)) & 15)
+      return set_err(HEFF_EINVAL, "heff_apply: complex psi/out must be 16-byte aligned");
+    r = apply_orderA_z(p, psi, out, s, &nl);
   } else {
     r = p->sharded ? apply_orderB(p, psi, out, s, &nl, accumulate) : apply_orderA(p, psi, out, s, &nl, accumulate);
   }
@@ -736,8 +923,8 @@ extern "C" int heff_create_sum(heff_plan* out, const heff_plan* terms, int nterm
   for (int t = 0; t < nterms; ++t) {
     const heff_plan_s* q = terms[t];
     if (!q) return set_err(HEFF_EINVAL, "heff_create_sum: null term");
-    if (q->sharded || q->comm || !q->terms.empty())
-      return set_err(HEFF_EUNSUPPORTED, "heff_create_sum: terms must be single-GPU, non-composite plans");
+    if (q->sharded || q->comm || !q->terms.empty() || q->is_complex)
+      return set_err(HEFF_EUNSUPPORTED, "heff_create_sum: terms must be single-GPU, real, non-composite plans");
     if (q->dims.mL != d0.mL || q->dims.mR != d0.mR || q->dims.d1 != d0.d1 || q->dims.d2 != d0.d2)
       return set_err(HEFF_EINVAL, "heff_create_sum: terms must share mL, d1, d2, mR");
   }
@@ -750,7 +937,8 @@ extern "C" int heff_create_sum(heff_plan* out, const heff_plan* terms, int nterm
 
 extern "C" int heff_set_penalty(heff_plan p, const double* phis, int nphi, double weight, heff_stream stream) {
   if (!p || nphi < 0 || (nphi > 0 && !phis)) return set_err(HEFF_EINVAL, "heff_set_penalty: bad argument");
-  if (p->sharded) return set_err(HEFF_EUNSUPPORTED, "heff_set_penalty: not supported on b'-sharded plans");
+  if (p->sharded || p->is_complex)
+    return set_err(HEFF_EUNSUPPORTED, "heff_set_penalty: not supported on b'-sharded or complex plans");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaFree(p->phis);
   cudaFree(p->pen_scratch);
@@ -781,8 +969,9 @@ extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_
   if (!p || !psi_host || !out_host) return set_err(HEFF_EINVAL, "heff_apply_host: null argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const heff_dims& d = p->dims;
-  const int64_t n_in = d.mL * d.d1 * d.d2 * d.mR;
-  const int64_t n_out = vec_len(p);
+  const int64_t zf = p->is_complex ? 2 : 1;  // doubles per entry
+  const int64_t n_in = zf * d.mL * d.d1 * d.d2 * d.mR;
+  const int64_t n_out = zf * vec_len(p);
   if (!p->stage_in) {
     CK(cudaMalloc(&p->stage_in, sizeof(double) * n_in));
     CK(cudaMalloc(&p->stage_out, sizeof(double) * n_out));
@@ -830,6 +1019,31 @@ static int multiaxpy(heff_plan_s* p, const double* V, int nq, const double* c, d
   for (int q0 = 0; q0 < nq; q0 += 64) {
     const int qn = std::min(64, nq - q0);
     multiaxpy_kernel<<<ew_grid(n), 256, 0, s>>>(V + q0 * p->ldv, p->ldv, qn, c + q0, sign, w, n);
+    ++p->total_launches;
+  }
+  CK(cudaGetLastError());
+  return HEFF_OK;
+}
+
+// complex (interleaved) versions: c[2q], c[2q+1] = Re, Im of <V_q, w>, n complex entries
+static int zmultidot(heff_plan_s* p, const double* V, int nq, const double* w, int64_t n, double* c, cudaStream_t s) {
+  const int G = p->ldp;
+  for (int q0 = 0; q0 < nq; q0 += kDotQ) {
+    const int qn = std::min(kDotQ, nq - q0);
+    zmultidot_partial_kernel<<<G, kRedThreads, 0, s>>>(V + q0 * p->ldv, p->ldv, qn, w, n, p->partial + 2 * q0 * G, G);
+    ++p->total_launches;
+  }
+  reduce_partial_kernel<<<2 * nq, kRedThreads, 0, s>>>(p->partial, G, G, c, 0, nullptr);
+  ++p->total_launches;
+  CK(cudaGetLastError());
+  return HEFF_OK;
+}
+
+static int zmultiaxpy(heff_plan_s* p, const double* V, int nq, const double* c, double sign, double* w, int64_t n,
+                      cudaStream_t s) {
+  for (int q0 = 0; q0 < nq; q0 += 64) {
+    const int qn = std::min(64, nq - q0);
+    zmultiaxpy_kernel<<<ew_grid(2 * n), 256, 0, s>>>(V + q0 * p->ldv, p->ldv, qn, c + 2 * q0, sign, w, n);
     ++p->total_launches;
   }
   CK(cudaGetLastError());
@@ -898,8 +1112,10 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   // U(1) plans iterate on the sector's entries only (gather/scatter around each matvec)
   const bool compact = p->qn_idx != nullptr && !p->sharded && p->terms.empty();
   const int64_t n_dense = vec_len(p);
-  const int64_t n = compact ? p->qn_n : n_dense;
-  const int64_t ldv = (n + 31) / 32 * 32;
+  const int64_t n = compact ? p->qn_n : n_dense;     // entries per vector
+  const bool cplx = p->is_complex;                   // interleaved complex entries
+  const int64_t nr = cplx ? 2 * n : n;               // doubles per vector
+  const int64_t ldv = (nr + 31) / 32 * 32;
   if (compact && !p->dense_in) {
     CK(cudaMalloc(&p->dense_in, sizeof(double) * n_dense));
     CK(cudaMalloc(&p->dense_out, sizeof(double) * n_dense));
@@ -911,10 +1127,10 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     p->basis = nullptr; p->partial = nullptr; p->scal = nullptr;
     p->basis_cap = 0;
     CK(cudaMalloc(&p->basis, sizeof(double) * ldv * cap));
-    p->ldp = reduce_grid(n);
+    p->ldp = reduce_grid(nr);
     const size_t pcols = std::max<size_t>((size_t)p->ldp, (size_t)8 * g_num_sms);  // also the fused step's grid
-    CK(cudaMalloc(&p->partial, sizeof(double) * (size_t)(2 * cap + kDotQ + 1) * pcols));
-    CK(cudaMalloc(&p->scal, sizeof(double) * 6 * (size_t)(cap + 1)));
+    CK(cudaMalloc(&p->partial, sizeof(double) * (size_t)(2 * cap + 2 * kDotQ + 1) * pcols));
+    CK(cudaMalloc(&p->scal, sizeof(double) * 8 * (size_t)(cap + 1)));
     p->basis_cap = cap;
     p->ldv = ldv;
   }
@@ -929,9 +1145,9 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     CK(cudaMalloc(&p->full, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
     if (p->nranks > 1) CK(cudaMalloc(&p->gather, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
   }
-  double* c1 = p->scal;
-  double* c2 = c1 + (cap + 1);
-  double* alpha = c2 + (cap + 1);
+  double* c1 = p->scal;                              // 2 (cap+1): room for complex coefficients
+  double* c2 = c1 + 2 * (cap + 1);
+  double* alpha = c2 + 2 * (cap + 1);
   double* beta = alpha + (cap + 1);
   double* invb = beta + (cap + 1);
   double* ydev = invb + (cap + 1);
@@ -944,14 +1160,14 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     ++p->total_launches;
     CK(cudaGetLastError());
   } else {
-    CK(cudaMemcpyAsync(V, psi, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(V, psi, sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
   }
-  CKR(norm2(p, V, n, beta + cap, invb + cap, s));
+  CKR(norm2(p, V, nr, beta + cap, invb + cap, s));
   double h_nrm = 0.0;
   CK(cudaMemcpyAsync(&h_nrm, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (!(h_nrm > 0.0)) return set_err(HEFF_EZERO, "lanczos_ground: zero start vector");
-  scale_kernel<<<ew_grid(n), 256, 0, s>>>(V, invb + cap, V, n);
+  scale_kernel<<<ew_grid(nr), 256, 0, s>>>(V, invb + cap, V, nr);
   ++p->total_launches;
   CK(cudaGetLastError());
 
@@ -960,8 +1176,8 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   int j_done = 0;
   // fused single-launch CGS2 step when there is no communicator and the coefficients fit
   // (launch-bound sizes only: above ~2M elements the separate vectorised kernels stream faster)
-  const bool fused = (p->comm == nullptr) && (cap <= 4096) && (n <= (int64_t(1) << 21) || getenv("HEFF_FUSED_STEP")) &&
-                     getenv("HEFF_NO_FUSED_STEP") == nullptr;
+  const bool fused = !cplx && (p->comm == nullptr) && (cap <= 4096) &&
+                     (n <= (int64_t(1) << 21) || getenv("HEFF_FUSED_STEP")) && getenv("HEFF_NO_FUSED_STEP") == nullptr;
   int step_grid = 0;
   if (fused) {
     int per_sm = 0;
@@ -995,15 +1211,22 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       ++p->total_launches;
       return HEFF_OK;
     }
-    CKR(multidot(p, V, j, w, n, c1, s));
-    CKR(multiaxpy(p, V, j, c1, -1.0, w, n, s));
-    CKR(multidot(p, V, j, w, n, c2, s));
-    CKR(multiaxpy(p, V, j, c2, -1.0, w, n, s));
-    lanczos_alpha_kernel<<<1, 1, 0, s>>>(c1, c2, j - 1, alpha);
+    if (cplx) {
+      CKR(zmultidot(p, V, j, w, n, c1, s));
+      CKR(zmultiaxpy(p, V, j, c1, -1.0, w, n, s));
+      CKR(zmultidot(p, V, j, w, n, c2, s));
+      CKR(zmultiaxpy(p, V, j, c2, -1.0, w, n, s));
+    } else {
+      CKR(multidot(p, V, j, w, n, c1, s));
+      CKR(multiaxpy(p, V, j, c1, -1.0, w, n, s));
+      CKR(multidot(p, V, j, w, n, c2, s));
+      CKR(multiaxpy(p, V, j, c2, -1.0, w, n, s));
+    }
+    lanczos_alpha_kernel<<<1, 1, 0, s>>>(c1, c2, j - 1, alpha, cplx ? 2 : 1);
     ++p->total_launches;
-    CKR(norm2(p, w, n, beta + (j - 1), invb + (j - 1), s));
+    CKR(norm2(p, w, nr, beta + (j - 1), invb + (j - 1), s));
     if (j < cap) {
-      scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + (j - 1), V + (int64_t)j * ldv, n);
+      scale_kernel<<<ew_grid(nr), 256, 0, s>>>(w, invb + (j - 1), V + (int64_t)j * ldv, nr);
       ++p->total_launches;
     }
     CK(cudaGetLastError());
@@ -1049,16 +1272,16 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   if (!tridiag_lowest_vec(j_done, ha.data(), hb.data(), &theta, y.data()))
     return set_err(HEFF_ECUDA, "lanczos_ground: tridiagonal QL did not converge");
   CK(cudaMemcpyAsync(ydev, y.data(), sizeof(double) * j_done, cudaMemcpyHostToDevice, s));
-  CK(cudaMemsetAsync(w, 0, sizeof(double) * n, s));
-  CKR(multiaxpy(p, V, j_done, ydev, 1.0, w, n, s));
-  CKR(norm2(p, w, n, beta + cap, invb + cap, s));
+  CK(cudaMemsetAsync(w, 0, sizeof(double) * nr, s));
+  CKR(multiaxpy(p, V, j_done, ydev, 1.0, w, nr, s));   // real y: also right for complex V
+  CKR(norm2(p, w, nr, beta + cap, invb + cap, s));
   if (compact) {  // psi = scatter(x), zero outside the sector
     scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + cap, w, n);
     CK(cudaMemsetAsync(psi, 0, sizeof(double) * n_dense, s));
     scatter_kernel<<<ew_grid(n), 256, 0, s>>>(w, p->qn_idx, n, psi);
     p->total_launches += 1;
   } else {
-    scale_kernel<<<ew_grid(n), 256, 0, s>>>(w, invb + cap, psi, n);
+    scale_kernel<<<ew_grid(nr), 256, 0, s>>>(w, invb + cap, psi, nr);
   }
   ++p->total_launches;
   CK(cudaGetLastError());
@@ -1176,7 +1399,7 @@ extern "C" int heff_env_update_left(const heff_env_dims* dims, const double* L, 
     const int nin = (int)(d.kl * d.d), nout = (int)(d.d * d.kr);
     dim3 grid((unsigned)((d.mo + kMpoCols - 1) / kMpoCols), (unsigned)d.mi);
     mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mo, nin, nout, csr.d_rowptr,
-                                                                                 csr.d_col, csr.d_val, nullptr);
+                                                                                 csr.d_col, csr.d_val, nullptr, 1, 0, 0);
     dim3 tg((unsigned)((d.mo + 31) / 32), (unsigned)((d.mi * d.d + 31) / 32));
     transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, At, d.mi * d.d, d.mo);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_left: launch failed");
@@ -1233,7 +1456,7 @@ extern "C" int heff_env_update_right(const heff_env_dims* dims, const double* R,
     const int nin = (int)(d.d * d.kr), nout = (int)(d.kl * d.d);
     dim3 grid((unsigned)((d.mi + kMpoCols - 1) / kMpoCols), (unsigned)d.mo);
     mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mi, nin, nout, csr.d_rowptr,
-                                                                                 csr.d_col, csr.d_val, nullptr);
+                                                                                 csr.d_col, csr.d_val, nullptr, 1, 0, 0);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_right: launch failed");
   }
   if (!r) {
@@ -1388,8 +1611,8 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
     p->sp_kblocks = 0;
     return HEFF_OK;
   }
-  if (p->sharded || !p->terms.empty())
-    return set_err(HEFF_EUNSUPPORTED, "heff_set_qn: single-GPU order-A plans only (set it on each term of a sum)");
+  if (p->sharded || !p->terms.empty() || p->is_complex)
+    return set_err(HEFF_EUNSUPPORTED, "heff_set_qn: single-GPU real order-A plans only (set it on each term of a sum)");
   const heff_dims& d = p->dims;
   if (p->chunk_rows != d.mL) return set_err(HEFF_EUNSUPPORTED, "heff_set_qn: plan is chunked over a' (workspace budget)");
   if (!qn->qa || !qn->qb || !qn->qs1 || !qn->qs2 || !qn->cL || !qn->cR)

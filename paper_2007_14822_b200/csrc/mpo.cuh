@@ -32,17 +32,24 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
                                                               const int* __restrict__ rowptr,
                                                               const int* __restrict__ col,
                                                               const double* __restrict__ val,
-                                                              const unsigned char* __restrict__ live) {
+                                                              const unsigned char* __restrict__ live,
+                                                              int planes, int64_t in_plane, int64_t out_plane) {
+  // planes == 2 (complex plans): rows [0, nin/2) come from the real plane of T1 and
+  // [nin/2, nin) from the imaginary plane (in_plane doubles further); likewise for T3.
+  // The CSR then holds the real 2x2 blocks [[Re, -Im], [Im, Re]] of the complex MPO.
   extern __shared__ __align__(16) double s_in[];  // [nin][kMpoCols]
   __shared__ uint64_t bar;
   const int64_t ap = blockIdx.y;
   // U(1) plans: blocks whose input and output are zero by symmetry are skipped (their T3
   // entries were zeroed once by heff_set_qn)
   if (live && !live[ap * gridDim.x + blockIdx.x]) return;
+  const int nin_p = nin / planes, nout_p = nout / planes;
   const int64_t b0 = (int64_t)blockIdx.x * kMpoCols;
   const int width = (int)min((int64_t)kMpoCols, mR - b0);
-  const double* in = T1 + ap * nin * mR + b0;
-  double* out = T3 + ap * nout * mR + b0;
+  auto in_row = [&](int r) {
+    const int pl = r / nin_p;
+    return T1 + pl * in_plane + (ap * nin_p + (r - pl * nin_p)) * mR + b0;
+  };
   const bool bulk = ((mR & 1) == 0) && ((width & 1) == 0);
   if (bulk) {
     if (threadIdx.x == 0) {
@@ -52,13 +59,13 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
     __syncthreads();
     if (threadIdx.x == 0) {
       mbar_arrive_expect_tx(&bar, (uint32_t)(nin * width * 8));
-      for (int r = 0; r < nin; ++r) bulk_load(s_in + r * kMpoCols, in + r * mR, (uint32_t)(width * 8), &bar);
+      for (int r = 0; r < nin; ++r) bulk_load(s_in + r * kMpoCols, in_row(r), (uint32_t)(width * 8), &bar);
     }
     mbar_wait(&bar, 0);
   } else {
     for (int e = threadIdx.x; e < nin * kMpoCols; e += kMpoThreads) {
       const int r = e / kMpoCols, c = e - r * kMpoCols;
-      if (c < width) s_in[e] = __ldcs(in + r * mR + c);
+      if (c < width) s_in[e] = __ldcs(in_row(r) + c);
     }
     __syncthreads();
   }
@@ -68,7 +75,8 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
     double acc = 0.0;
     const int e1 = __ldg(rowptr + o + 1);
     for (int e = __ldg(rowptr + o); e < e1; ++e) acc = fma(__ldg(val + e), s_in[__ldg(col + e) * kMpoCols + t], acc);
-    __stcs(out + o * mR + t, acc);
+    const int pl = o / nout_p;
+    __stcs(T3 + pl * out_plane + (ap * nout_p + (o - pl * nout_p)) * mR + b0 + t, acc);
   }
 }
 

@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         L.heff_last_timings.argtypes = [vp] + [ctypes.POINTER(ctypes.c_float)] * 4
         L.heff_relayout_blocked.argtypes = [vp, vp, i64, i64, ip, vp]
         L.heff_create_sum.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), ip]
+        L.heff_create_z.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(_Dims), vp, vp, vp, vp, ctypes.POINTER(_Dist), vp]
         L.heff_set_penalty.argtypes = [vp, vp, ip, ctypes.c_double, vp]
         dp = ctypes.POINTER(ctypes.c_double)
         L.heff_tridiag_lowest.argtypes = [ip, dp, dp, dp, dp]
@@ -88,7 +89,7 @@ def lib() -> ctypes.CDLL:
         for f in ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-                  "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn"):
+                  "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -97,7 +98,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy", "heff_last_error",
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-            "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn")
+            "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z")
 
 
 def _check(rc: int):
@@ -113,9 +114,10 @@ def _stream(stream) -> int:
     return int(s.cuda_stream)
 
 
-def _dev(t: torch.Tensor, name: str) -> torch.Tensor:
-    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
-        raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+def _dev(t: torch.Tensor, name: str, cplx: bool = False) -> torch.Tensor:
+    dt = torch.complex128 if cplx else torch.float64
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dt and t.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous {dt} CUDA tensor")
     return t
 
 
@@ -214,8 +216,9 @@ class Heff:
     """
 
     def __init__(self, L, W1, W2, R, dist: dict | None = None, stream=None):
+        self.cplx = isinstance(L, torch.Tensor) and L.is_complex()
         for t, n in ((L, "L"), (W1, "W1"), (W2, "W2"), (R, "R")):
-            _dev(t, n)
+            _dev(t, n, self.cplx)
         if L.dim() != 3 or W1.dim() != 4 or W2.dim() != 4 or R.dim() != 3:
             raise ValueError("expected L[mL,kL,mL], W1[kL,d1,d1,kM], W2[kM,d2,d2,kR], R[nb,kR,mR]")
         mL, kL, _ = L.shape
@@ -244,8 +247,9 @@ class Heff:
         else:
             self.nb = mR
         h = ctypes.c_void_p()
-        _check(lib().heff_create(ctypes.byref(h), ctypes.byref(self._cdims), L.data_ptr(), W1.data_ptr(),
-                                 W2.data_ptr(), R.data_ptr(), pdist, _stream(stream)))
+        create = lib().heff_create_z if self.cplx else lib().heff_create
+        _check(create(ctypes.byref(h), ctypes.byref(self._cdims), L.data_ptr(), W1.data_ptr(), W2.data_ptr(),
+                      R.data_ptr(), pdist, _stream(stream)))
         self._h = h
 
     def set_penalty(self, phis: torch.Tensor | None, weight: float = 0.0, stream=None):
@@ -285,10 +289,11 @@ class Heff:
         return (d["mL"], d["d1"], d["d2"], self.nb)
 
     def apply(self, psi: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        _dev(psi, "psi")
+        cplx = getattr(self, "cplx", False)
+        _dev(psi, "psi", cplx)
         if out is None:
-            out = torch.empty(self.out_shape, dtype=torch.float64, device=psi.device)
-        _dev(out, "out")
+            out = torch.empty(self.out_shape, dtype=psi.dtype, device=psi.device)
+        _dev(out, "out", cplx)
         n_in = self.dims["mL"] * self.dims["d1"] * self.dims["d2"] * self.dims["mR"]
         if psi.numel() != n_in or out.numel() != n_in // self.dims["mR"] * self.nb:
             raise ValueError(f"psi must have {self.psi_shape} elements and out {self.out_shape}")
@@ -298,7 +303,8 @@ class Heff:
     def apply_host(self, psi_host: torch.Tensor, out_host: torch.Tensor, stream=None) -> torch.Tensor:
         """End-to-end entry: host buffers in and out (copies happen inside libheff)."""
         assert psi_host.device.type == "cpu" and out_host.device.type == "cpu"
-        assert psi_host.dtype == torch.float64 and out_host.dtype == torch.float64
+        dt = torch.complex128 if getattr(self, "cplx", False) else torch.float64
+        assert psi_host.dtype == dt and out_host.dtype == dt
         assert psi_host.is_contiguous() and out_host.is_contiguous()
         _check(lib().heff_apply_host(self._h, psi_host.data_ptr(), out_host.data_ptr(), _stream(stream)))
         return out_host
@@ -306,7 +312,7 @@ class Heff:
     def lanczos_ground(self, psi: torch.Tensor, max_iter: int, tol: float = 0.0, converge: bool = False,
                        stream=None) -> LanczosResult:
         """psi: start vector (overwritten with the normalised Ritz vector)."""
-        _dev(psi, "psi")
+        _dev(psi, "psi", getattr(self, "cplx", False))
         a = (ctypes.c_double * max_iter)()
         b = (ctypes.c_double * max_iter)()
         th = (ctypes.c_double * max_iter)()
@@ -358,6 +364,7 @@ class HeffSum(Heff):
             raise ValueError("need at least one term")
         self._terms = list(terms)
         self.dims = dict(terms[0].dims)
+        self.cplx = False
         self.dist = None
         self.nb = self.dims["mR"]
         arr = (ctypes.c_void_p * len(terms))(*[t._h.value for t in terms])
