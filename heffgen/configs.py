@@ -46,6 +46,19 @@ def random_psi(seed: int, shape, device="cpu") -> torch.Tensor:
     return torch.from_numpy(x).to(device)
 
 
+def graded_matrix(M: int, N: int, seed: int, decades: float = 12.0) -> np.ndarray:
+    """Synthetic two-site matrix with a DMRG-like decaying spectrum: Q1 diag(s) Q2^T with
+    Q1, Q2 the orthonormal factors of N(0,1) matrices (default_rng(seed)) and
+    s_i = 10^(-decades * i / (k-1)), k = min(M, N), then unit Frobenius norm."""
+    rng = np.random.default_rng(seed)
+    k = min(M, N)
+    Q1, _ = np.linalg.qr(rng.standard_normal((M, k)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((N, k)))
+    s = 10.0 ** (-decades * np.arange(k) / max(1, k - 1))
+    A = (Q1 * s[None, :]) @ Q2.T
+    return A / np.linalg.norm(A)
+
+
 def model_inputs(Ws: list[np.ndarray], window: int, m: int, seed: int, device="cpu", meta=None) -> HeffInputs:
     """Environments of a random orthonormal MPS around the two-site window (window, window+1).
 

@@ -60,7 +60,8 @@ enum {
   HEFF_ECUDA = -3,       /* CUDA runtime / driver error                         */
   HEFF_ENCCL = -4,       /* NCCL error (load, init or collective)               */
   HEFF_EZERO = -5,       /* lanczos start vector is zero          */
-  HEFF_EUNSUPPORTED = -6 /* request outside what this build supports            */
+  HEFF_EUNSUPPORTED = -6, /* request outside what this build supports           */
+  HEFF_ENOCONV = -7       /* an iterative decomposition did not converge          */
 };
 
 /* Dimensions: bond dims mL, mR; site dims d1, d2; MPO bond dims kL (L/W1), kM (W1/W2),
@@ -221,6 +222,33 @@ int heff_env_update_left(const heff_env_dims* dims, const double* L, const doubl
                          heff_stream stream);
 int heff_env_update_right(const heff_env_dims* dims, const double* R, const double* B, const double* W, double* Rout,
                           heff_stream stream);
+
+/* ---- Two-site split ---------------------------------------------
+ * After each local eigensolve a sweep splits the two-site wavefunction with a truncated SVD
+ * (Sec. 5: "U,S,V = svd(W,(j,i);cutoff=1E-8,maxdim=10)"; Sec. 6.2,
+ * PAPER.md:705-737).  psi is viewed as the matrix Psi[(a s1)][(s2 b)] of M = mL*d1 rows and
+ * N = d2*mR columns (row-major, no copy) and factored Psi ~= U diag(s) V^T, keeping n values:
+ *   dir 0 (moving right): Q = U [M][n] (left-orthonormal A[a][s1][k]),  C = diag(s) V^T [n][N]
+ *   dir 1 (moving left):  Q = V^T [n][N] (right-orthonormal B[k][s2][b]), C = U diag(s) [M][n]
+ * Truncation (readings R20-R22): n is the smallest count whose discarded weight
+ * sum_{i>=n} s_i^2 <= cutoff * sum_i s_i^2, raised to mindim, capped at maxdim (<= 0:
+ * unlimited); s_i <= 1e-12 s_1 are numerical zeros and never kept.  Each kept vector's sign
+ * makes the largest-|.| entry of Q's vector positive (first on ties).
+ * Arguments: psi, Q, S, C are DEVICE pointers (fp64; psi is not modified; Q and C are
+ * written compactly with row pitch n resp. N -- allocate for n <= min(M, N, maxdim)).
+ * S receives all min(M, N) singular values, descending.  n_kept, trunc_err (relative
+ * discarded weight) and sweeps (Jacobi sweeps used; may be NULL) are HOST pointers.
+ * trunc == NULL: cutoff 0, maxdim unlimited, mindim 1.  Errors: HEFF_EINVAL (bad sizes,
+ * cutoff < 0, dir not 0/1), HEFF_EZERO (psi == 0), HEFF_ENOCONV (Jacobi sweep cap).
+ * Workspace lives in a per-thread arena (about (2 max(M,N) + n) min(M,N)... doubles,
+ * grown on demand, reused).  Synchronous on `stream`. */
+typedef struct {
+  double cutoff;
+  int64_t maxdim;
+  int64_t mindim;
+} heff_trunc;
+int heff_svd_split(int64_t M, int64_t N, const double* psi, const heff_trunc* trunc, int dir, double* Q, double* S,
+                   double* C, int64_t* n_kept, double* trunc_err, int* sweeps, heff_stream stream);
 
 #ifdef __cplusplus
 }

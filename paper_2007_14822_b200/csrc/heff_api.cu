@@ -18,6 +18,7 @@
 #include "blas1.cuh"
 #include "gemm.cuh"
 #include "mpo.cuh"
+#include "svd.cuh"
 #include "tridiag.h"
 
 using namespace heff;
@@ -1741,4 +1742,213 @@ __global__ void scatter_kernel(const double* __restrict__ compact, const int* __
                                double* __restrict__ dense) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dense[idx[i]] = compact[i];
+}
+
+// --------------------------------------------------------------------------- two-site split
+// NEXT-2: truncated SVD of Psi[(a s1)][(s2 b)] (Sec. 5) by
+// block one-sided Jacobi (svd.cuh), then the sort / truncation rule (host, over min(M,N)
+// norms), the gauge + gather kernels and one DMMA GEMM for the next centre.
+struct SvdArena {
+  double* buf = nullptr;
+  size_t bytes = 0;
+};
+static thread_local SvdArena t_svd_arena;
+static thread_local SplitWs t_svd_splitws;
+
+static int svd_reserve(size_t bytes) {
+  SvdArena& a = t_svd_arena;
+  if (a.bytes >= bytes) return HEFF_OK;
+  cudaFree(a.buf);
+  a.buf = nullptr;
+  a.bytes = 0;
+  CK(cudaMalloc(&a.buf, bytes));
+  a.bytes = bytes;
+  return HEFF_OK;
+}
+
+// round-robin (circle method) schedule of nblk (even) blocks: rounds nblk-1, nblk/2 pairs each
+static std::vector<int2> svd_pair_schedule(int nblk) {
+  std::vector<int> idx(nblk);
+  for (int i = 0; i < nblk; ++i) idx[i] = i;
+  std::vector<int2> out;
+  out.reserve((size_t)(nblk - 1) * (nblk / 2));
+  for (int r = 0; r < nblk - 1; ++r) {
+    for (int k = 0; k < nblk / 2; ++k) out.push_back(make_int2(idx[k], idx[nblk - 1 - k]));
+    const int last = idx[nblk - 1];
+    for (int i = nblk - 1; i > 1; --i) idx[i] = idx[i - 1];
+    idx[1] = last;
+  }
+  return out;
+}
+
+static constexpr int kSvdMaxSweeps = 80;
+static constexpr double kSvdRankEps = 1e-12;   // reading R21
+static constexpr double kSvdNegligible = 1e-15; // columns below this fraction of ||Psi||_F are not rotated
+
+extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const heff_trunc* trunc, int dir, double* Qout,
+                              double* S, double* Cout, int64_t* n_kept, double* trunc_err, int* sweeps_out,
+                              heff_stream stream) {
+  if (M < 1 || N < 1 || !psi || !Qout || !S || !Cout || !n_kept || !trunc_err || (dir != 0 && dir != 1))
+    return set_err(HEFF_EINVAL, "heff_svd_split: bad argument");
+  const double cutoff = trunc ? trunc->cutoff : 0.0;
+  const int64_t maxdim = trunc ? trunc->maxdim : 0;
+  const int64_t mindim = trunc ? std::max<int64_t>(1, trunc->mindim) : 1;
+  if (!(cutoff >= 0.0)) return set_err(HEFF_EINVAL, "heff_svd_split: cutoff < 0");
+  if (M * N >= (1ll << 40) || std::max(M, N) >= (1ll << 31)) return set_err(HEFF_EUNSUPPORTED, "heff_svd_split: too large");
+  CKR(init_device_once());
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t R = dir == 0 ? M : N;          // rows of X
+  const int64_t ncols = dir == 0 ? N : M;      // columns of X (orthogonalised)
+  const int64_t kmin = std::min(M, N);
+  int64_t nblk = (ncols + kSvdB - 1) / kSvdB;
+  if (nblk & 1) ++nblk;
+  if (nblk < 2) nblk = 2;
+  const int npairs = (int)(nblk / 2), rounds = (int)(nblk - 1);
+  // row splits: about 4 CTAs per SM for the Gram, 8 for the rotation
+  const int64_t rs1 = std::max<int64_t>(1, std::min<int64_t>((4 * g_num_sms + npairs - 1) / npairs, (R + 127) / 128));
+  const int rows1 = (int)(((R + rs1 - 1) / rs1 + 127) / 128 * 128);
+  const int rsplit = (int)((R + rows1 - 1) / rows1);
+  const int64_t rs2 = std::max<int64_t>(1, std::min<int64_t>((8 * g_num_sms + npairs - 1) / npairs, (R + 31) / 32));
+  const int rows2 = (int)(((R + rs2 - 1) / rs2 + 31) / 32 * 32);
+  const int rsplit2 = (int)((R + rows2 - 1) / rows2);
+  const int red_blocks = 4 * g_num_sms;
+
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t bX = al(sizeof(double) * nblk * kSvdB * R);
+  const size_t bG = al(sizeof(double) * (size_t)npairs * rsplit * kSvdPair * kSvdPair);
+  const size_t bNorm = al(sizeof(double) * nblk * kSvdB);
+  const size_t bPairs = al(sizeof(int2) * (size_t)rounds * npairs);
+  const size_t bStat = al(sizeof(unsigned long long) * kSvdMaxSweeps + sizeof(int) * kSvdMaxSweeps);
+  const size_t bRed = al(sizeof(double) * (red_blocks + 1));
+  const size_t bPerm = al(sizeof(int) * kmin) + 2 * al(sizeof(double) * kmin);
+  const size_t bUt = dir == 0 ? al(sizeof(double) * kmin * M) : 0;
+  const size_t bQ = al(sizeof(double) * (size_t)npairs * kSvdPair * kSvdPair) + al(sizeof(int) * npairs);
+  const size_t bSortPerm = al(sizeof(int) * nblk * kSvdB);
+  CKR(svd_reserve(2 * bX + bG + bNorm + bPairs + bStat + bRed + bPerm + bUt + bQ + bSortPerm));
+  unsigned char* w = reinterpret_cast<unsigned char*>(t_svd_arena.buf);
+  double* Xb = reinterpret_cast<double*>(w); w += bX;
+  double* Xb2 = reinterpret_cast<double*>(w); w += bX;
+  double* d_Qg = reinterpret_cast<double*>(w); w += al(sizeof(double) * (size_t)npairs * kSvdPair * kSvdPair);
+  int* d_flag = reinterpret_cast<int*>(w); w += al(sizeof(int) * npairs);
+  int* d_sortperm = reinterpret_cast<int*>(w); w += bSortPerm;
+  double* Gp = reinterpret_cast<double*>(w); w += bG;
+  double* d_norm = reinterpret_cast<double*>(w); w += bNorm;
+  int2* d_pairs = reinterpret_cast<int2*>(w); w += bPairs;
+  unsigned long long* d_maxoff = reinterpret_cast<unsigned long long*>(w);
+  int* d_nrot = reinterpret_cast<int*>(w + sizeof(unsigned long long) * kSvdMaxSweeps); w += bStat;
+  double* d_red = reinterpret_cast<double*>(w); w += bRed;
+  int* d_perm = reinterpret_cast<int*>(w); w += al(sizeof(int) * kmin);
+  double* d_skept = reinterpret_cast<double*>(w); w += al(sizeof(double) * kmin);
+  double* d_scale = reinterpret_cast<double*>(w); w += al(sizeof(double) * kmin);
+  double* d_Ut = reinterpret_cast<double*>(w);
+
+  const std::vector<int2> sched = svd_pair_schedule((int)nblk);
+  CK(cudaMemcpyAsync(d_pairs, sched.data(), sizeof(int2) * sched.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(d_maxoff, 0, bStat, s));
+  // ||Psi||_F^2 (deterministic two-pass) and the packed working copy
+  svd_sumsq_partial_kernel<<<red_blocks, 256, 0, s>>>(psi, M * N, d_red);
+  svd_sum_kernel<<<1, 32, 0, s>>>(d_red, red_blocks, d_red + red_blocks);
+  if (dir == 0) {
+    svd_pack_kernel<<<ew_grid(nblk * kSvdB * R), 256, 0, s>>>(psi, Xb, R, ncols, nblk);
+  } else {
+    dim3 grid((unsigned)((R + 31) / 32), (unsigned)(nblk * kSvdB / 32));
+    svd_pack_t_kernel<<<grid, dim3(32, 8), 0, s>>>(psi, Xb, R, ncols);
+  }
+  CK(cudaGetLastError());
+  double fro2 = 0.0;
+  CK(cudaMemcpyAsync(&fro2, d_red + red_blocks, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (!(fro2 > 0.0)) return set_err(HEFF_EZERO, "heff_svd_split: psi is zero");
+  const double eps = 1.1102230246251565e-16;
+  const double tol = std::max(4.0 * eps * std::sqrt((double)R), 8.0 * eps);
+  const double negl = kSvdNegligible * kSvdNegligible * fro2;
+
+  // Jacobi sweeps until a sweep rotates no pair
+  int sweeps = 0;
+  bool converged = false;
+  const bool sort_cols = getenv("HEFF_SVD_NO_SORT") == nullptr;
+  std::vector<double> nrm(nblk * kSvdB);
+  std::vector<int> order(nblk * kSvdB);
+  for (int sw = 0; sw < kSvdMaxSweeps && !converged; ++sw) {
+    if (sort_cols && ncols > kSvdPair) {  // descending-norm column order for this sweep
+      svd_colnorm_kernel<<<(unsigned)nblk, 256, 0, s>>>(Xb, R, ncols, d_norm);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(nrm.data(), d_norm, sizeof(double) * ncols, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int64_t i = 0; i < ncols; ++i) order[i] = (int)i;
+      std::stable_sort(order.begin(), order.begin() + ncols, [&](int a, int b) { return nrm[a] > nrm[b]; });
+      CK(cudaMemcpyAsync(d_sortperm, order.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice, s));
+      svd_permute_kernel<<<ew_grid(nblk * kSvdB * R), 256, 0, s>>>(Xb, Xb2, R, ncols, nblk, d_sortperm);
+      std::swap(Xb, Xb2);
+    }
+    for (int r = 0; r < rounds; ++r) {
+      const int2* pr = d_pairs + (size_t)r * npairs;
+      svd_gram_kernel<<<dim3(npairs, rsplit), kSvdGramThreads, 0, s>>>(Xb, R, pr, rows1, Gp);
+      svd_pair_eig_kernel<<<npairs, kSvdEigThreads, 0, s>>>(Gp, rsplit, tol, negl, d_Qg, d_flag, d_maxoff + sw,
+                                                           d_nrot + sw);
+      svd_rotate_kernel<<<dim3(npairs, rsplit2), kSvdRotThreads, 0, s>>>(Xb, R, pr, d_Qg, d_flag, rows2);
+    }
+    CK(cudaGetLastError());
+    int nrot = 0;
+    CK(cudaMemcpyAsync(&nrot, d_nrot + sw, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    sweeps = sw + 1;
+    converged = nrot == 0;
+  }
+  if (sweeps_out) *sweeps_out = sweeps;
+  if (!converged) return set_err(HEFF_ENOCONV, "heff_svd_split: Jacobi did not converge in %d sweeps", kSvdMaxSweeps);
+
+  // singular values = column norms; sort (descending, stable) and truncate on the host
+  svd_colnorm_kernel<<<(unsigned)nblk, 256, 0, s>>>(Xb, R, ncols, d_norm);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(nrm.data(), d_norm, sizeof(double) * ncols, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < ncols; ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.begin() + ncols, [&](int a, int b) { return nrm[a] > nrm[b]; });
+  std::vector<double> sv(kmin);
+  for (int64_t i = 0; i < kmin; ++i) sv[i] = nrm[order[i]];
+  double total = 0.0;
+  for (int64_t i = kmin - 1; i >= 0; --i) total += sv[i] * sv[i];
+  if (!(sv[0] > 0.0)) return set_err(HEFF_EZERO, "heff_svd_split: psi is zero");
+  int64_t rank = 0;
+  while (rank < kmin && sv[rank] > kSvdRankEps * sv[0]) ++rank;
+  int64_t n = kmin;
+  double disc = 0.0;
+  while (n > 1 && disc + sv[n - 1] * sv[n - 1] <= cutoff * total) {
+    disc += sv[n - 1] * sv[n - 1];
+    --n;
+  }
+  n = std::min(n, rank);
+  n = std::max(n, std::min(mindim, rank));
+  if (maxdim > 0) n = std::min(n, maxdim);
+  double err = 0.0;
+  for (int64_t i = kmin - 1; i >= n; --i) err += sv[i] * sv[i];
+  err /= total;
+  CK(cudaMemcpyAsync(S, sv.data(), sizeof(double) * kmin, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_perm, order.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_skept, sv.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  svd_sign_kernel<<<(unsigned)n, 256, 0, s>>>(Xb, R, d_perm, d_skept, d_scale);
+  dim3 gg((unsigned)std::min<int64_t>((R + 255) / 256, 1024), (unsigned)n);
+  int nl = 0;
+  int r = HEFF_OK;
+  if (dir == 0) {
+    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, d_Ut);   // U^T [n][M]
+    dim3 tg((unsigned)((M + 31) / 32), (unsigned)((n + 31) / 32));
+    transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(d_Ut, Qout, n, M);            // U [M][n]
+    CK(cudaGetLastError());
+    GemmOp g;  // C[n][N] = U^T[n][M] . Psi[M][N]
+    g.M = n; g.N = N; g.K = M; g.A = d_Ut; g.lda = M; g.B = psi; g.ldb = N; g.b_kmajor = false; g.C = Cout; g.ldc = N;
+    r = launch_gemm(g, 0, s, &nl, &t_svd_splitws);
+  } else {
+    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, Qout);   // V^T [n][N]
+    CK(cudaGetLastError());
+    GemmOp g;  // C[M][n] = Psi[M][N] . (V^T)^T
+    g.M = M; g.N = n; g.K = N; g.A = psi; g.lda = N; g.B = Qout; g.ldb = N; g.b_kmajor = true; g.C = Cout; g.ldc = n;
+    r = launch_gemm(g, 0, s, &nl, &t_svd_splitws);
+  }
+  CK(cudaStreamSynchronize(s));
+  if (r != HEFF_OK) return r;
+  *n_kept = n;
+  *trunc_err = err;
+  return HEFF_OK;
 }

@@ -1,0 +1,426 @@
+// svd.cuh -- the two-site split: truncated SVD of the two-site
+// wavefunction Psi[(a s1)][(s2 b)] (Sec. 5) by block one-sided (Hestenes)
+// Jacobi on FP64 tensor cores.
+//
+// The columns of a working copy X (Psi moving right, Psi^T moving left) are made mutually
+// orthogonal by orthogonal rotations X <- X Q; at convergence X = U S (column norms = the
+// singular values, normalised columns = the singular vectors) -- no V is accumulated, the
+// next centre is one GEMM with the original Psi afterwards.
+//
+// Work unit: a PAIR of 16-column blocks (I, J).  Per round of the round-robin ordering all
+// nblk/2 pairs are disjoint and run in parallel, two kernels per round:
+//   svd_gram_kernel   G = [X_I X_J]^T [X_I X_J] (32 x 32), DMMA over a row range, one
+//                     partial per (pair, row split); the 4 loaded values per lane feed 10
+//                     DMMA (upper triangle of 4x4 tiles; columns permuted c = 4g + i so one
+//                     lane loads 32 contiguous bytes).
+//   svd_pair_eig_kernel one CTA per pair: sums the partials (fixed order), tests the pair
+//                     for convergence (max |g_ij| / sqrt(g_ii g_jj) over non-negligible
+//                     columns) and diagonalises G in shared memory by cyclic two-sided Jacobi
+//                     (relative accuracy for graded G) -> Q (32 x 32).
+//   svd_rotate_kernel streams a row range of each rotated pair through Y <- Y Q on DMMA,
+//                     Q's fragments held in registers.
+// Columns are re-sorted by norm at the start of every sweep.  All reductions are
+// fixed-order: the result is bitwise deterministic.
+//
+// Layout: X is stored block-column-major, Xb[blk][r][16] (a block's rows are 128-byte
+// contiguous lines), zero-padded to an even number of blocks.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+
+namespace heff {
+
+constexpr int kSvdB = 16;              // columns per block
+constexpr int kSvdPair = 2 * kSvdB;    // columns per pair
+constexpr int kSvdGramThreads = 256;
+constexpr int kSvdRotThreads = 128;
+constexpr int kSvdMaxInnerSweeps = 24;
+
+// ---------------------------------------------------------------- packing
+// Moving right: X = Psi [R][ncols] -> Xb (zero beyond ncols).
+__global__ void svd_pack_kernel(const double* __restrict__ psi, double* __restrict__ Xb, int64_t R, int64_t ncols,
+                                int64_t nblk) {
+  const int64_t total = nblk * R * kSvdB;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e & (kSvdB - 1));
+    const int64_t rb = e >> 4;
+    const int64_t blk = rb / R, r = rb - blk * R;
+    const int64_t c = blk * kSvdB + j;
+    Xb[e] = c < ncols ? psi[r * ncols + c] : 0.0;
+  }
+}
+
+// Moving left: X = Psi^T, Psi is [ncols][R] -> Xb[blk][r][16] = Psi[blk*16+j][r]; 32x32 tiles.
+__global__ void svd_pack_t_kernel(const double* __restrict__ psi, double* __restrict__ Xb, int64_t R, int64_t ncols) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t c = c0 + k, r = r0 + tx;
+    tile[k][tx] = (c < ncols && r < R) ? psi[c * R + r] : 0.0;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t r = r0 + k, c = c0 + tx;
+    if (r < R) Xb[((c >> 4) * R + r) * kSvdB + (c & 15)] = tile[tx][k];
+  }
+}
+
+// ---------------------------------------------------------------- sum of squares (deterministic)
+__global__ void svd_sumsq_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    s = fma(v, v, s);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void svd_sum_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    *out = s;
+  }
+}
+
+// ---------------------------------------------------------------- Gram partials
+// Gp[(p * gridDim.y + split)][32][32] = sum over rows of the split of Y[r]^T Y[r],
+// Y = [X_I | X_J].  Lane (g, t) of a warp loads row (t) columns 4g..4g+3 (32 B): tile i of
+// the DMMA A/B operands is column 4g + i, so tile (i, j) accumulates G[4m+i][4n+j].
+__global__ void __launch_bounds__(kSvdGramThreads) svd_gram_kernel(const double* __restrict__ Xb, int64_t R,
+                                                                   const int2* __restrict__ pairs, int rows_per_cta,
+                                                                   double* __restrict__ Gp) {
+  __shared__ double red[kSvdGramThreads / 32][10 * 64];
+  const int p = blockIdx.x, split = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int2 pr = pairs[p];
+  const double* base = Xb + (int64_t)(g < 4 ? pr.x : pr.y) * R * kSvdB + (g & 3) * 4;
+  double acc[10][2];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const int64_t r_begin = (int64_t)split * rows_per_cta;
+  const int64_t r_end = min(R, r_begin + (int64_t)rows_per_cta);
+  for (int64_t rb = r_begin; rb < r_end; rb += 128) {
+    double v[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t r = rb + u * 32 + warp * 4 + t;
+      if (r < r_end) {
+        const double2* src = reinterpret_cast<const double2*>(base + r * kSvdB);
+        const double2 a = __ldg(src), b = __ldg(src + 1);
+        v[u][0] = a.x; v[u][1] = a.y; v[u][2] = b.x; v[u][3] = b.y;
+      } else {
+        v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int idx = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = i; j < 4; ++j, ++idx) dmma_8x8x4(acc[idx][0], acc[idx][1], v[u][i], v[u][j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    red[warp][i * 64 + lane * 2] = acc[i][0];
+    red[warp][i * 64 + lane * 2 + 1] = acc[i][1];
+  }
+  __syncthreads();
+  double* out = Gp + ((int64_t)p * gridDim.y + split) * (kSvdPair * kSvdPair);
+  for (int e = threadIdx.x; e < 10 * 64; e += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kSvdGramThreads / 32; ++w) s += red[w][e];
+    const int idx = e >> 6, l = (e >> 1) & 31, h = e & 1;
+    int i = 0, j = 0, k = idx;  // idx -> (i, j), i <= j, row-major over the upper triangle
+    for (i = 0; i < 4; ++i) {
+      if (k < 4 - i) { j = i + k; break; }
+      k -= 4 - i;
+    }
+    const int gm = l >> 2, tn = l & 3;
+    const int row = 4 * gm + i, col = 4 * (2 * tn + h) + j;
+    out[row * kSvdPair + col] = s;
+    if (i != j) out[col * kSvdPair + row] = s;
+  }
+}
+
+// ---------------------------------------------------------------- pair eigen-solve
+// One CTA per pair: sum the Gram partials (fixed order), test the pair (max |g_ij| /
+// sqrt(g_ii g_jj) over non-negligible columns), and if it is not converged diagonalise G by
+// cyclic two-sided Jacobi in shared memory (parallel round-robin ordering, 16 disjoint
+// rotations per round).  Each round is one parameter phase and one update phase: every
+// 2x2 block (pair k rows, pair k' columns) of G <- J^T G J depends only on its old values,
+// so a thread updates a whole block at once (the diagonal blocks get the exact rotated
+// 2x2 values), and Q <- Q J by columns.  Output: Qg[p] (row-major 32x32), flag[p].
+constexpr int kSvdEigThreads = 256;
+
+__global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const double* __restrict__ Gp, int rsplit,
+                                                                     double tol, double negl,
+                                                                     double* __restrict__ Qg, int* __restrict__ flag,
+                                                                     unsigned long long* __restrict__ stat_maxoff,
+                                                                     int* __restrict__ stat_nrot) {
+  __shared__ double G[kSvdPair][kSvdPair + 1];
+  __shared__ double Q[kSvdPair][kSvdPair + 1];
+  __shared__ double s_c[16], s_s[16], s_na[16], s_nb[16];
+  __shared__ int s_do[16], s_neg[kSvdPair];
+  __shared__ unsigned char s_pa[31][16], s_pb[31][16];
+  __shared__ int s_any;
+  __shared__ double s_off[kSvdEigThreads / 32];
+  const int p = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* gsrc = Gp + (int64_t)p * rsplit * (kSvdPair * kSvdPair);
+  for (int e = tid; e < kSvdPair * kSvdPair; e += blockDim.x) {
+    double v = 0.0;
+    for (int sp = 0; sp < rsplit; ++sp) v += gsrc[(int64_t)sp * (kSvdPair * kSvdPair) + e];
+    const int r = e >> 5, c = e & 31;
+    G[r][c] = v;
+    Q[r][c] = (r == c) ? 1.0 : 0.0;
+  }
+  for (int e = tid; e < 31 * 16; e += blockDim.x) {  // round-robin (circle method) over 32 columns
+    const int rr = e >> 4, k = e & 15;
+    auto idx = [&](int i) { return i == 0 ? 0 : ((i - 1 + rr) % 31) + 1; };
+    s_pa[rr][k] = (unsigned char)idx(k);
+    s_pb[rr][k] = (unsigned char)idx(31 - k);
+  }
+  __syncthreads();
+  if (tid < kSvdPair) s_neg[tid] = !(G[tid][tid] > negl);
+  __syncthreads();
+  double off = 0.0;
+  for (int e = tid; e < kSvdPair * kSvdPair; e += blockDim.x) {
+    const int r = e >> 5, c = e & 31;
+    if (r < c && !s_neg[r] && !s_neg[c]) off = fmax(off, fabs(G[r][c]) / sqrt(G[r][r] * G[c][c]));
+  }
+  for (int o = 16; o > 0; o >>= 1) off = fmax(off, __shfl_xor_sync(0xffffffffu, off, o));
+  if (lane == 0) s_off[warp] = off;
+  __syncthreads();
+  off = s_off[0];
+  for (int w = 1; w < kSvdEigThreads / 32; ++w) off = fmax(off, s_off[w]);
+  const bool rotate = off > tol;
+  if (tid == 0) {
+    flag[p] = rotate ? 1 : 0;
+    atomicMax(stat_maxoff, (unsigned long long)__double_as_longlong(off));
+    if (rotate) atomicAdd(stat_nrot, 1);
+  }
+  if (!rotate) return;
+
+  for (int sweep = 0; sweep < kSvdMaxInnerSweeps; ++sweep) {
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    for (int rr = 0; rr < 31; ++rr) {
+      if (tid < 16) {
+        const int a = s_pa[rr][tid], b = s_pb[rr][tid];
+        const double app = G[a][a], aqq = G[b][b], apq = G[a][b];
+        const bool d = !s_neg[a] && !s_neg[b] && fabs(apq) > tol * sqrt(app * aqq);
+        s_do[tid] = d;
+        if (d) {
+          const double zeta = (aqq - app) / (2.0 * apq);
+          const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+          const double c = 1.0 / sqrt(1.0 + tt * tt);
+          s_c[tid] = c;
+          s_s[tid] = c * tt;
+          s_na[tid] = app - tt * apq;   // exact rotated diagonal
+          s_nb[tid] = aqq + tt * apq;
+          s_any = 1;
+        }
+      }
+      __syncthreads();
+      {  // G <- J^T G J: one 2x2 block (pair k rows, pair kk columns) per thread
+        const int k = tid >> 4, kk = tid & 15;
+        const bool dk = s_do[k], dkk = s_do[kk];
+        if (dk || dkk) {
+          const int a = s_pa[rr][k], b = s_pb[rr][k];
+          const int a2 = s_pa[rr][kk], b2 = s_pb[rr][kk];
+          if (k == kk) {
+            G[a][a] = s_na[k];
+            G[b][b] = s_nb[k];
+            G[a][b] = G[b][a] = 0.0;
+          } else {
+            double x00 = G[a][a2], x01 = G[a][b2], x10 = G[b][a2], x11 = G[b][b2];
+            if (dkk) {  // columns: [x.0 x.1] <- [x.0 x.1] [[c, s], [-s, c]]
+              const double c = s_c[kk], s = s_s[kk];
+              const double y00 = c * x00 - s * x01, y01 = s * x00 + c * x01;
+              const double y10 = c * x10 - s * x11, y11 = s * x10 + c * x11;
+              x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+            }
+            if (dk) {   // rows: [x0. ; x1.] <- [[c, -s], [s, c]] [x0. ; x1.]
+              const double c = s_c[k], s = s_s[k];
+              const double y00 = c * x00 - s * x10, y10 = s * x00 + c * x10;
+              const double y01 = c * x01 - s * x11, y11 = s * x01 + c * x11;
+              x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+            }
+            G[a][a2] = x00; G[a][b2] = x01; G[b][a2] = x10; G[b][b2] = x11;
+          }
+        }
+      }
+      for (int task = tid; task < 32 * 16; task += blockDim.x) {  // Q <- Q J
+        const int k = task & 15, r = task >> 4;
+        if (!s_do[k]) continue;
+        const int a = s_pa[rr][k], b = s_pb[rr][k];
+        const double c = s_c[k], s = s_s[k];
+        const double qa = Q[r][a], qb = Q[r][b];
+        Q[r][a] = c * qa - s * qb;
+        Q[r][b] = s * qa + c * qb;
+      }
+      __syncthreads();
+    }
+    const int any = s_any;
+    __syncthreads();  // every thread has read s_any before thread 0 resets it
+    if (!any) break;
+  }
+  double* q = Qg + (int64_t)p * (kSvdPair * kSvdPair);
+  for (int e = tid; e < kSvdPair * kSvdPair; e += blockDim.x) q[e] = Q[e >> 5][e & 31];
+}
+
+// ---------------------------------------------------------------- rotation
+// Y <- Y Q on a row range of a rotated pair.  A = Y (row g, k-slice kk of lane t = column
+// 8t + kk), B = Q fragments held in registers, D tile n = output columns 8n + {2t, 2t+1}.
+__global__ void __launch_bounds__(kSvdRotThreads) svd_rotate_kernel(double* __restrict__ Xb, int64_t R,
+                                                                   const int2* __restrict__ pairs,
+                                                                   const double* __restrict__ Qg,
+                                                                   const int* __restrict__ flag, int rows_per_cta) {
+  const int p = blockIdx.x;
+  if (!flag[p]) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const double* q = Qg + (int64_t)p * (kSvdPair * kSvdPair);
+  double qf[8][4];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) qf[kk][n] = __ldg(q + (8 * t + kk) * kSvdPair + 8 * n + g);
+  const int2 pr = pairs[p];
+  double* XI = Xb + (int64_t)pr.x * R * kSvdB;
+  double* XJ = Xb + (int64_t)pr.y * R * kSvdB;
+  const double* src_base = (t < 2 ? XI : XJ) + (t & 1) * 8;
+  const int64_t r_begin = (int64_t)blockIdx.y * rows_per_cta;
+  const int64_t r_end = min(R, r_begin + (int64_t)rows_per_cta);
+#pragma unroll 2
+  for (int64_t rb = r_begin + warp * 8; rb < r_end; rb += 8 * (kSvdRotThreads / 32)) {
+    const int64_t row = rb + g;
+    const bool ok = row < r_end;
+    double y[8];
+    if (ok) {
+      const double2* s2 = reinterpret_cast<const double2*>(src_base + row * kSvdB);
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        const double2 v = s2[qq];
+        y[2 * qq] = v.x;
+        y[2 * qq + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) y[qq] = 0.0;
+    }
+    double acc[4][2];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) acc[n][0] = acc[n][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[n][0], acc[n][1], y[kk], qf[kk][n]);
+    if (ok) {
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        double* dst = (n < 2 ? XI : XJ) + row * kSvdB + (((8 * n) & 15) + 2 * t);
+        *reinterpret_cast<double2*>(dst) = make_double2(acc[n][0], acc[n][1]);
+      }
+    }
+  }
+}
+
+// X columns permuted into descending-norm order at the start of a sweep (de Rijk-style
+// ordering: the round-robin then meets the dominant columns first):
+// dst[blk][r][j] = src column perm[blk*16 + j] (zero for padding columns >= ncols).
+__global__ void svd_permute_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t R, int64_t ncols,
+                                   int64_t nblk, const int* __restrict__ perm) {
+  const int64_t total = nblk * R * kSvdB;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e & (kSvdB - 1));
+    const int64_t rb = e >> 4;
+    const int64_t blk = rb / R, r = rb - blk * R;
+    const int64_t c = blk * kSvdB + j;
+    double v = 0.0;
+    if (c < ncols) {
+      const int sc = perm[c];
+      v = src[(((int64_t)(sc >> 4)) * R + r) * kSvdB + (sc & 15)];
+    }
+    dst[e] = v;
+  }
+}
+
+// ---------------------------------------------------------------- extraction
+// norms[c] = ||X[:, c]|| for c < ncols; one CTA (256 threads) per 16-column block
+__global__ void svd_colnorm_kernel(const double* __restrict__ Xb, int64_t R, int64_t ncols, double* __restrict__ norms) {
+  __shared__ double red[256];
+  const int64_t blk = blockIdx.x;
+  const int j = threadIdx.x & 15, rl = threadIdx.x >> 4;
+  double s = 0.0;
+  for (int64_t r = rl; r < R; r += 16) {
+    const double x = Xb[(blk * R + r) * kSvdB + j];
+    s = fma(x, x, s);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    double tot = 0.0;
+    for (int q = 0; q < 16; ++q) tot += red[q * 16 + threadIdx.x];
+    const int64_t c = blk * kSvdB + threadIdx.x;
+    if (c < ncols) norms[c] = sqrt(tot);
+  }
+}
+
+// scale[k] = sign / s_k, sign making the largest-|.| entry of column perm[k] positive (first on ties)
+__global__ void svd_sign_kernel(const double* __restrict__ Xb, int64_t R, const int* __restrict__ perm,
+                                const double* __restrict__ s, double* __restrict__ scale) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  const int k = blockIdx.x;
+  const int c = perm[k];
+  const double* col = Xb + (int64_t)(c >> 4) * R * kSvdB + (c & 15);
+  double best = -1.0;
+  int64_t bi = 0;
+  for (int64_t r = threadIdx.x; r < R; r += blockDim.x) {
+    const double a = fabs(col[r * kSvdB]);
+    if (a > best) { best = a; bi = r; }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      const double o = sv[threadIdx.x + w];
+      const int64_t oi = si[threadIdx.x + w];
+      if (o > sv[threadIdx.x] || (o == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = o;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) scale[k] = (col[si[0] * kSvdB] < 0.0 ? -1.0 : 1.0) / s[k];
+}
+
+// out[k][r] = X[r][perm k] * scale[k]   (k < n: grid.y; r < R)
+__global__ void svd_gather_t_kernel(const double* __restrict__ Xb, int64_t R, const int* __restrict__ perm,
+                                    const double* __restrict__ scale, double* __restrict__ out) {
+  const int k = blockIdx.y;
+  const int c = perm[k];
+  const double sc = scale[k];
+  const double* col = Xb + (int64_t)(c >> 4) * R * kSvdB + (c & 15);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x)
+    out[(int64_t)k * R + r] = col[r * kSvdB] * sc;
+}
+
+}  // namespace heff

@@ -17,6 +17,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libheff.so"
 
 HEFF_OK, HEFF_EINVAL, HEFF_ENOMEM, HEFF_ECUDA, HEFF_ENCCL, HEFF_EZERO, HEFF_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+HEFF_ENOCONV = -7
 OPT_GEMM_PATH, OPT_LAST_KERNEL_COUNT, OPT_MPO_NNZ, OPT_PROFILE, OPT_TOTAL_LAUNCHES, OPT_SPARSE_KBLOCKS = 1, 2, 3, 4, 5, 6
 
 
@@ -45,6 +46,10 @@ class _EnvDims(ctypes.Structure):
 
 class _QN(ctypes.Structure):
     _fields_ = [(n, ctypes.POINTER(ctypes.c_int)) for n in ("qa", "qb", "qs1", "qs2", "cL", "cM", "cR")]
+
+
+class _Trunc(ctypes.Structure):
+    _fields_ = [("cutoff", ctypes.c_double), ("maxdim", ctypes.c_int64), ("mindim", ctypes.c_int64)]
 
 
 class _LanczosOpts(ctypes.Structure):
@@ -86,7 +91,9 @@ def lib() -> ctypes.CDLL:
         L.heff_gemm.argtypes = [i64, i64, i64, vp, i64, vp, i64, ip, vp, i64, ip, ip, vp]
         L.heff_env_update_left.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         L.heff_env_update_right.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
-        for f in ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
+        L.heff_svd_split.argtypes = [i64, i64, vp, ctypes.POINTER(_Trunc), ip, vp, vp, vp, ctypes.POINTER(i64),
+                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ip), vp]
+        for f in ("heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
                   "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z"):
@@ -98,7 +105,8 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy", "heff_last_error",
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-            "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z")
+            "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z",
+            "heff_svd_split")
 
 
 def _check(rc: int):
@@ -189,6 +197,46 @@ def env_update_right(R: torch.Tensor, B: torch.Tensor, W: torch.Tensor, stream=N
     _check(lib().heff_env_update_right(ctypes.byref(_EnvDims(mi, d, mo, kl, kr)), R.data_ptr(), B.data_ptr(),
                                        W.data_ptr(), out.data_ptr(), _stream(stream)))
     return out
+
+
+@dataclass
+class SplitResult:
+    Q: torch.Tensor       # dir 0: U [M, n]; dir 1: V^T [n, N]
+    S: torch.Tensor       # all min(M, N) singular values, descending
+    C: torch.Tensor       # dir 0: S V^T [n, N]; dir 1: U S [M, n]
+    n: int
+    trunc_err: float
+    sweeps: int
+
+
+def svd_split(psi: torch.Tensor, cutoff: float = 0.0, maxdim: int = 0, mindim: int = 1, direction: int = 0,
+              stream=None) -> SplitResult:
+    """Two-site split (heff_svd_split): psi [mL, d1, d2, mR] is viewed as Psi[(a s1), (s2 b)]
+    (a 2-D tensor is taken as Psi itself) and factored by the truncated SVD."""
+    _dev(psi, "psi")
+    if psi.dim() == 4:
+        mL, d1, d2, mR = psi.shape
+        M, N = mL * d1, d2 * mR
+    elif psi.dim() == 2:
+        M, N = psi.shape
+    else:
+        raise ValueError("psi must be [mL, d1, d2, mR] or [M, N]")
+    kmax = min(M, N) if maxdim <= 0 else min(M, N, maxdim)
+    Q = torch.empty(max(1, M * kmax if direction == 0 else kmax * N), dtype=torch.float64, device=psi.device)
+    C = torch.empty(max(1, kmax * N if direction == 0 else M * kmax), dtype=torch.float64, device=psi.device)
+    S = torch.empty(min(M, N), dtype=torch.float64, device=psi.device)
+    n = ctypes.c_int64(0)
+    err = ctypes.c_double(0.0)
+    sw = ctypes.c_int(0)
+    tr = _Trunc(float(cutoff), int(maxdim), int(mindim))
+    _check(lib().heff_svd_split(M, N, psi.data_ptr(), ctypes.byref(tr), int(direction), Q.data_ptr(), S.data_ptr(),
+                                C.data_ptr(), ctypes.byref(n), ctypes.byref(err), ctypes.byref(sw), _stream(stream)))
+    k = n.value
+    if direction == 0:
+        Qv, Cv = Q[: M * k].view(M, k), C[: k * N].view(k, N)
+    else:
+        Qv, Cv = Q[: k * N].view(k, N), C[: M * k].view(M, k)
+    return SplitResult(Qv, S, Cv, k, err.value, sw.value)
 
 
 def nccl_unique_id() -> bytes:

@@ -1,0 +1,76 @@
+"""Time the two-site split (heff_svd_split) at the config sizes on one GPU.
+
+Psi is the two-site matrix (mL d) x (d mR) of configs C1..C4: the seeded N(0,1) psi of the
+config (reading R8) and a graded stand-in with a DMRG-like decaying spectrum
+(heffgen.configs.graded_matrix).  Reports ms per split (CUDA events on the launching
+stream, after one warm-up), Jacobi sweeps, and the per-sweep streaming figures.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from heffgen import configs as C  # noqa: E402
+from paper_2007_14822_b200 import heff  # noqa: E402
+
+SIZES = {"c1": 16, "c2": 256, "c3": 1024, "c4": 4096}
+
+
+def run(m: int, kind: str, reps: int, maxdim: int, direction: int):
+    dev = torch.device("cuda:0")
+    if kind == "random":
+        psi = C.random_psi(1000 + m, (m, 2, 2, m), dev)
+    else:
+        psi = torch.from_numpy(C.graded_matrix(2 * m, 2 * m, 7, 12.0)).to(dev).view(m, 2, 2, m)
+    heff.svd_split(psi, maxdim=maxdim, direction=direction)      # warm-up (arena, module load)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ts, sweeps = [], []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        r = heff.svd_split(psi, maxdim=maxdim, direction=direction)
+        b.record(s)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+        sweeps.append(r.sweeps)
+    ts.sort()
+    M = 2 * m
+    nblk = ((M + 15) // 16 + 1) // 2 * 2
+    # per sweep: every round streams X once for the Gram (read) and once for the rotation
+    # (read + write): 24 B per element, (nblk - 1) rounds
+    bytes_per_sweep = 24.0 * M * (nblk * 16) * (nblk - 1)
+    return dict(m=m, M=M, kind=kind, dir=direction, maxdim=maxdim, ms=ts[len(ts) // 2], ms_min=ts[0],
+                sweeps=sweeps[-1], n=r.n, trunc_err=r.trunc_err,
+                ms_per_sweep=ts[len(ts) // 2] / sweeps[-1],
+                stream_GBps=bytes_per_sweep * sweeps[-1] / (ts[len(ts) // 2] * 1e-3) / 1e9)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c1,c2,c3,c4")
+    ap.add_argument("--kinds", default="random,graded")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    rows = []
+    for c in a.configs.split(","):
+        m = SIZES[c]
+        for kind in a.kinds.split(","):
+            for d in (0, 1):
+                row = dict(config=c, **run(m, kind, a.reps if m < 4096 else max(1, a.reps - 1), m, d))
+                print(json.dumps(row), flush=True)
+                rows.append(row)
+    if a.out:
+        Path(a.out).write_text(json.dumps(rows, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -2,8 +2,9 @@
 hot path composes into the paper's algorithm (Sec. 6.2): at every bond the
 local eigensolve is libheff's lanczos_ground on H_eff (heff_create / heff_apply), the
 environments move with heff_env_update_left/right, and the two-site tensor is formed with
-heff_gemm.  The SVD split (not built in libheff yet) uses
-torch.linalg.svd (cuSOLVER) here, so this script is a test harness, not a product path.
+heff_gemm, and the two-site split is libheff's heff_svd_split (block one-sided Jacobi SVD,
+SURVEY 8(f) NEXT-2).  Every step of the sweep runs in libheff's kernels; this script only
+sequences them.
 
     python tools/dmrg_gpu.py --N 20 --maxdim 64 --sweeps 4
 """
@@ -21,7 +22,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from heffgen import mpo  # noqa: E402
-from paper_2007_14822_b200 import Heff, env_update_left, env_update_right  # noqa: E402
+from paper_2007_14822_b200 import Heff, env_update_left, env_update_right, svd_split  # noqa: E402
 from paper_2007_14822_b200.heff import gemm  # noqa: E402
 
 
@@ -43,21 +44,24 @@ def two_site(A, B):
     return gemm(A.reshape(a * d1, k), B.reshape(k, d2 * b)).reshape(a, d1, d2, b)
 
 
+SPLIT_STATS = {"calls": 0, "sweeps": 0, "max_sweeps": 0, "ms": 0.0}
+
+
 def split(psi, maxdim, cutoff, direction):
-    """Truncated SVD of psi reshaped (a s1) x (s2 b); keeps the largest singular values with
-    discarded weight <= cutoff (relative) and at most maxdim."""
+    """Truncated SVD of psi reshaped (a s1) x (s2 b) on libheff (heff_svd_split): keeps the
+    largest singular values with relative discarded weight <= cutoff and at most maxdim
+    (P:L521-546).  Moving right returns (U, S V^T), moving left (U S, V^T)."""
     a, d1, d2, b = psi.shape
-    U, S, Vh = torch.linalg.svd(psi.reshape(a * d1, d2 * b), full_matrices=False)
-    w = S * S
-    tot = w.sum()
-    tail = torch.flip(torch.cumsum(torch.flip(w, [0]), 0), [0])   # tail[i] = sum_{j >= i} w_j
-    keep = int((tail / tot > cutoff).sum().item())
-    keep = max(1, min(keep, maxdim))
-    U, S, Vh = U[:, :keep], S[:keep], Vh[:keep]
-    disc = float((tot - w[:keep].sum()) / tot)
+    t0 = time.perf_counter()
+    r = svd_split(psi, cutoff=cutoff, maxdim=maxdim, direction=0 if direction == "right" else 1)
+    SPLIT_STATS["calls"] += 1
+    SPLIT_STATS["sweeps"] += r.sweeps
+    SPLIT_STATS["max_sweeps"] = max(SPLIT_STATS["max_sweeps"], r.sweeps)
+    SPLIT_STATS["ms"] += 1e3 * (time.perf_counter() - t0)
+    k = r.n
     if direction == "right":
-        return U.reshape(a, d1, keep).contiguous(), (S[:, None] * Vh).reshape(keep, d2, b).contiguous(), disc
-    return (U * S[None, :]).reshape(a, d1, keep).contiguous(), Vh.reshape(keep, d2, b).contiguous(), disc
+        return r.Q.reshape(a, d1, k).contiguous(), r.C.reshape(k, d2, b).contiguous(), r.trunc_err
+    return r.C.reshape(a, d1, k).contiguous(), r.Q.reshape(k, d2, b).contiguous(), r.trunc_err
 
 
 def dmrg(Ws, maxdims, cutoff=1e-11, seed=0, lanczos_iter=40, init_dim=8, device="cuda", log=print):
@@ -96,7 +100,10 @@ def dmrg(Ws, maxdims, cutoff=1e-11, seed=0, lanczos_iter=40, init_dim=8, device=
                 else:
                     Rs[j + 1] = env_update_right(Rs[j + 2], As[j + 1], tW[j + 1])
         log(f"After sweep {sw + 1} energy={energy:.12f} maxlinkdim={max(a.shape[2] for a in As[:-1])} "
-            f"maxtrunc={maxdisc:.2e} time={time.perf_counter() - t0:.2f}")
+            f"maxtrunc={maxdisc:.2e} time={time.perf_counter() - t0:.2f} split: {SPLIT_STATS['calls']} calls, "
+            f"{SPLIT_STATS['sweeps'] / max(1, SPLIT_STATS['calls']):.1f} Jacobi sweeps avg "
+            f"(max {SPLIT_STATS['max_sweeps']}), {SPLIT_STATS['ms'] / 1e3:.2f} s")
+        SPLIT_STATS.update(calls=0, sweeps=0, max_sweeps=0, ms=0.0)
     return energy, As
 
 
@@ -105,10 +112,15 @@ def main():
     ap.add_argument("--N", type=int, default=20)
     ap.add_argument("--maxdim", type=int, default=64)
     ap.add_argument("--sweeps", type=int, default=4)
+    ap.add_argument("--model", default="chain", choices=["chain", "cylinder"])
+    ap.add_argument("--lanczos", type=int, default=40)
     args = ap.parse_args()
-    W = mpo.heisenberg_chain_W()
+    if args.model == "chain":
+        Ws = [mpo.heisenberg_chain_W()] * args.N
+    else:
+        Ws = [mpo.cylinder_W(j) for j in range(args.N)]
     maxdims = [min(args.maxdim, 10 * 2 ** s) for s in range(args.sweeps)]
-    e, _ = dmrg([W] * args.N, maxdims)
+    e, _ = dmrg(Ws, maxdims, lanczos_iter=args.lanczos)
     print(f"E0 = {e:.12f}  E0/N = {e / args.N:.8f}")
 
 
