@@ -1866,6 +1866,9 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   // Jacobi sweeps until a sweep rotates no pair
   int sweeps = 0;
   bool converged = false;
+  const char* it_env = getenv("HEFF_SVD_INNER_THRESH");
+  const double inner_thresh = it_env ? atof(it_env) : 1e-2;
+  int inner = inner_thresh > 1.0 ? kSvdMaxInnerSweeps : 1;
   const bool sort_cols = getenv("HEFF_SVD_NO_SORT") == nullptr;
   std::vector<double> nrm(nblk * kSvdB);
   std::vector<int> order(nblk * kSvdB);
@@ -1884,16 +1887,21 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     for (int r = 0; r < rounds; ++r) {
       const int2* pr = d_pairs + (size_t)r * npairs;
       svd_gram_kernel<<<dim3(npairs, rsplit), kSvdGramThreads, 0, s>>>(Xb, R, pr, rows1, Gp);
-      svd_pair_eig_kernel<<<npairs, kSvdEigThreads, 0, s>>>(Gp, rsplit, tol, negl, d_Qg, d_flag, d_maxoff + sw,
-                                                           d_nrot + sw);
+      svd_pair_eig_kernel<<<npairs, kSvdEigThreads, 0, s>>>(Gp, rsplit, tol, negl, inner, d_Qg, d_flag,
+                                                           d_maxoff + sw, d_nrot + sw);
       svd_rotate_kernel<<<dim3(npairs, rsplit2), kSvdRotThreads, 0, s>>>(Xb, R, pr, d_Qg, d_flag, rows2);
     }
     CK(cudaGetLastError());
     int nrot = 0;
+    unsigned long long offbits = 0;
     CK(cudaMemcpyAsync(&nrot, d_nrot + sw, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&offbits, d_maxoff + sw, sizeof(offbits), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     sweeps = sw + 1;
     converged = nrot == 0;
+    double maxoff;
+    memcpy(&maxoff, &offbits, sizeof maxoff);
+    inner = maxoff < inner_thresh ? kSvdMaxInnerSweeps : 1;  // see svd.cuh kSvdMaxInnerSweeps
   }
   if (sweeps_out) *sweeps_out = sweeps;
   if (!converged) return set_err(HEFF_ENOCONV, "heff_svd_split: Jacobi did not converge in %d sweeps", kSvdMaxSweeps);

@@ -23,10 +23,29 @@ from paper_2007_14822_b200 import heff  # noqa: E402
 SIZES = {"c1": 16, "c2": 256, "c3": 1024, "c4": 4096}
 
 
+_DMRG_CACHE = {}
+
+
+def dmrg_psi(m: int, dev):
+    """Centre two-site wavefunction of a DMRG run (Heisenberg chain, maxdim m, cutoff 0) whose
+    bond reaches m: the realistic input of the split (tools/dmrg_gpu.py)."""
+    if m not in _DMRG_CACHE:
+        from heffgen import mpo
+        from tools.dmrg_gpu import dmrg
+        N = 2 * (max(1, (m - 1).bit_length()) + 2)
+        cap = {}
+        sched = [min(m, 16 * 2 ** s) for s in range(max(2, (m // 16).bit_length() + 1))] + [m]
+        dmrg([mpo.heisenberg_chain_W()] * N, sched, cutoff=0.0, lanczos_iter=8, log=lambda *_: None, capture=cap)
+        _DMRG_CACHE[m] = cap["psi"]
+    return _DMRG_CACHE[m]
+
+
 def run(m: int, kind: str, reps: int, maxdim: int, direction: int):
     dev = torch.device("cuda:0")
     if kind == "random":
         psi = C.random_psi(1000 + m, (m, 2, 2, m), dev)
+    elif kind == "dmrg":
+        psi = dmrg_psi(m, dev)
     else:
         psi = torch.from_numpy(C.graded_matrix(2 * m, 2 * m, 7, 12.0)).to(dev).view(m, 2, 2, m)
     heff.svd_split(psi, maxdim=maxdim, direction=direction)      # warm-up (arena, module load)
@@ -42,12 +61,12 @@ def run(m: int, kind: str, reps: int, maxdim: int, direction: int):
         ts.append(a.elapsed_time(b))
         sweeps.append(r.sweeps)
     ts.sort()
-    M = 2 * m
+    M = psi.shape[0] * psi.shape[1]
     nblk = ((M + 15) // 16 + 1) // 2 * 2
     # per sweep: every round streams X once for the Gram (read) and once for the rotation
     # (read + write): 24 B per element, (nblk - 1) rounds
     bytes_per_sweep = 24.0 * M * (nblk * 16) * (nblk - 1)
-    return dict(m=m, M=M, kind=kind, dir=direction, maxdim=maxdim, ms=ts[len(ts) // 2], ms_min=ts[0],
+    return dict(m=m, M=M, shape=list(psi.shape), kind=kind, dir=direction, maxdim=maxdim, ms=ts[len(ts) // 2], ms_min=ts[0],
                 sweeps=sweeps[-1], n=r.n, trunc_err=r.trunc_err,
                 ms_per_sweep=ts[len(ts) // 2] / sweeps[-1],
                 stream_GBps=bytes_per_sweep * sweeps[-1] / (ts[len(ts) // 2] * 1e-3) / 1e9)

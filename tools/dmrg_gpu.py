@@ -64,7 +64,9 @@ def split(psi, maxdim, cutoff, direction):
     return r.C.reshape(a, d1, k).contiguous(), r.Q.reshape(k, d2, b).contiguous(), r.trunc_err
 
 
-def dmrg(Ws, maxdims, cutoff=1e-11, seed=0, lanczos_iter=40, init_dim=8, device="cuda", log=print):
+def dmrg(Ws, maxdims, cutoff=1e-11, seed=0, lanczos_iter=40, init_dim=8, device="cuda", log=print, capture=None):
+    """capture: optional dict; receives the converged two-site wavefunction of the centre
+    bond (bond N/2-1, last left-to-right half sweep) under key "psi"."""
     N = len(Ws)
     d = Ws[0].shape[1]
     k = Ws[0].shape[0]
@@ -92,6 +94,8 @@ def dmrg(Ws, maxdims, cutoff=1e-11, seed=0, lanczos_iter=40, init_dim=8, device=
                 with Heff(Ls[j], tW[j], tW[j + 1], Rs[j + 2]) as h:
                     r = h.lanczos_ground(psi, max_iter=lanczos_iter, tol=1e-12, converge=True)
                 energy = r.energy
+                if capture is not None and direction == "right" and j == N // 2 - 1 and sw == len(maxdims) - 1:
+                    capture["psi"] = psi.clone()
                 A, B, disc = split(psi, maxdim, cutoff, direction)
                 maxdisc = max(maxdisc, disc)
                 As[j], As[j + 1] = A, B
