@@ -19,6 +19,7 @@
 #include "gemm.cuh"
 #include "mpo.cuh"
 #include "svd.cuh"
+#include "lq.cuh"
 #include "tridiag.h"
 
 using namespace heff;
@@ -1782,6 +1783,7 @@ static std::vector<int2> svd_pair_schedule(int nblk) {
 }
 
 static constexpr int kSvdMaxSweeps = 80;
+static int g_lq_grid = 0;  // co-resident CTAs of lq_panel_kernel (cooperative launch)
 static constexpr double kSvdRankEps = 1e-12;   // reading R21
 static constexpr double kSvdNegligible = 1e-15; // columns below this fraction of ||Psi||_F are not rotated
 
@@ -1798,8 +1800,17 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   CKR(init_device_once());
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t R = dir == 0 ? M : N;          // rows of X
-  const int64_t ncols = dir == 0 ? N : M;      // columns of X (orthogonalised)
   const int64_t kmin = std::min(M, N);
+  const int64_t colsP = dir == 0 ? N : M;      // columns of the working matrix P (Psi or Psi^T)
+  // LQ preconditioning (lq.cuh): Jacobi on the k = min(M,N) columns of L instead of P
+  if (g_lq_grid == 0) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lq_panel_kernel, kLqThreads, 0));
+    g_lq_grid = std::max(1, per_sm) * g_num_sms;
+  }
+  const bool precond = getenv("HEFF_SVD_NO_PRECOND") == nullptr && kmin > kSvdPair &&
+                       (colsP + g_lq_grid - 1) / g_lq_grid <= kLqMaxCols;
+  const int64_t ncols = precond ? kmin : colsP;  // columns of X (orthogonalised)
   int64_t nblk = (ncols + kSvdB - 1) / kSvdB;
   if (nblk & 1) ++nblk;
   if (nblk < 2) nblk = 2;
@@ -1824,8 +1835,28 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   const size_t bUt = dir == 0 ? al(sizeof(double) * kmin * M) : 0;
   const size_t bQ = al(sizeof(double) * (size_t)npairs * kSvdPair * kSvdPair) + al(sizeof(int) * npairs);
   const size_t bSortPerm = al(sizeof(int) * nblk * kSvdB);
-  CKR(svd_reserve(2 * bX + bG + bNorm + bPairs + bStat + bRed + bPerm + bUt + bQ + bSortPerm));
+  const size_t bLq = precond ? al(sizeof(double) * R * colsP) + al(sizeof(double) * kLqNb * colsP) +
+                                   al(sizeof(double) * R * kLqNb) +
+                                   al(sizeof(double) * R * (dir == 1 ? std::max<int64_t>(kLqNb, colsP) : kLqNb)) +
+                                   al(sizeof(int) * R) + 2 * al(sizeof(double) * kLqNb * kLqNb) +
+                                   al(sizeof(double) * kLqNb) + al(sizeof(double) * 2 * g_lq_grid * 2 * kLqNb)
+                             : 0;
+  CKR(svd_reserve(2 * bX + bG + bNorm + bPairs + bStat + bRed + bPerm + bUt + bQ + bSortPerm + bLq));
   unsigned char* w = reinterpret_cast<unsigned char*>(t_svd_arena.buf);
+  double *d_P = nullptr, *d_Vt = nullptr, *d_W = nullptr, *d_Y = nullptr, *d_VtV = nullptr, *d_negT = nullptr,
+         *d_beta = nullptr, *d_part = nullptr;
+  int* d_rowperm = nullptr;  // X row r = output row d_rowperm[r] (preconditioned path)
+  if (precond) {
+    d_P = reinterpret_cast<double*>(w); w += al(sizeof(double) * R * colsP);
+    d_Vt = reinterpret_cast<double*>(w); w += al(sizeof(double) * kLqNb * colsP);
+    d_W = reinterpret_cast<double*>(w); w += al(sizeof(double) * R * kLqNb);
+    d_Y = reinterpret_cast<double*>(w); w += al(sizeof(double) * R * (dir == 1 ? std::max<int64_t>(kLqNb, colsP) : kLqNb));
+    d_rowperm = reinterpret_cast<int*>(w); w += al(sizeof(int) * R);
+    d_VtV = reinterpret_cast<double*>(w); w += al(sizeof(double) * kLqNb * kLqNb);
+    d_negT = reinterpret_cast<double*>(w); w += al(sizeof(double) * kLqNb * kLqNb);
+    d_beta = reinterpret_cast<double*>(w); w += al(sizeof(double) * kLqNb);
+    d_part = reinterpret_cast<double*>(w); w += al(sizeof(double) * 2 * g_lq_grid * 2 * kLqNb);
+  }
   double* Xb = reinterpret_cast<double*>(w); w += bX;
   double* Xb2 = reinterpret_cast<double*>(w); w += bX;
   double* d_Qg = reinterpret_cast<double*>(w); w += al(sizeof(double) * (size_t)npairs * kSvdPair * kSvdPair);
@@ -1848,7 +1879,62 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   // ||Psi||_F^2 (deterministic two-pass) and the packed working copy
   svd_sumsq_partial_kernel<<<red_blocks, 256, 0, s>>>(psi, M * N, d_red);
   svd_sum_kernel<<<1, 32, 0, s>>>(d_red, red_blocks, d_red + red_blocks);
-  if (dir == 0) {
+  if (precond) {
+    // P = Pi Psi (moving right) or Pi Psi^T (moving left), R x colsP, rows sorted by
+    // descending norm (static row pivoting of the LQ); P <- L by blocked Householder
+    const double* src = psi;
+    if (dir == 1) {
+      dim3 tg((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
+      transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(psi, d_Y, M, N);  // d_Y is R x colsP here
+      src = d_Y;
+    }
+    svd_rownorm2_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(src, R, colsP, d_W);
+    std::vector<double> rn(R);
+    CK(cudaMemcpyAsync(rn.data(), d_W, sizeof(double) * R, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<int> rp(R);
+    for (int64_t i = 0; i < R; ++i) rp[i] = (int)i;
+    std::stable_sort(rp.begin(), rp.end(), [&](int a, int b) { return rn[a] > rn[b]; });
+    CK(cudaMemcpyAsync(d_rowperm, rp.data(), sizeof(int) * R, cudaMemcpyHostToDevice, s));
+    svd_gather_rows_kernel<<<dim3((unsigned)std::min<int64_t>((colsP + 255) / 256, 64), (unsigned)R), 256, 0, s>>>(
+        src, d_P, R, colsP, d_rowperm);
+    CK(cudaGetLastError());
+    int nl = 0;
+    for (int64_t j = 0; j < kmin; j += kLqNb) {
+      const int nbp = (int)std::min<int64_t>(kLqNb, kmin - j);
+      const int64_t L = colsP - j;
+      int grid = (int)std::min<int64_t>(g_lq_grid, (L + 31) / 32);
+      int cw = (int)((L + grid - 1) / grid);
+      grid = (int)((L + cw - 1) / cw);
+      CK(cudaMemsetAsync(d_Vt, 0, sizeof(double) * kLqNb * colsP, s));
+      double* Pp = d_P;
+      int64_t ldp = colsP, jj = j, ldv = colsP;
+      void* args[] = {&Pp, &ldp, &jj, (void*)&nbp, (void*)&L, &cw, &d_Vt, &ldv, &d_beta, &d_part};
+      CK(cudaLaunchCooperativeKernel((const void*)lq_panel_kernel, dim3(grid), dim3(kLqThreads), args, 0, s));
+      GemmOp gv;  // V^T V = Vt Vt^T (K = L)
+      gv.M = nbp; gv.N = nbp; gv.K = L; gv.A = d_Vt + j; gv.lda = colsP; gv.B = d_Vt + j; gv.ldb = colsP;
+      gv.b_kmajor = true; gv.C = d_VtV; gv.ldc = nbp;
+      CKR(launch_gemm(gv, 0, s, &nl, &t_svd_splitws));
+      lq_build_t_kernel<<<1, 32, 0, s>>>(d_VtV, d_beta, nbp, d_negT);
+      const int64_t rT = R - j - nbp;
+      if (rT > 0) {
+        double* Pt = d_P + (j + nbp) * colsP + j;
+        GemmOp g1;  // W = P_t V = P_t Vt^T
+        g1.M = rT; g1.N = nbp; g1.K = L; g1.A = Pt; g1.lda = colsP; g1.B = d_Vt + j; g1.ldb = colsP;
+        g1.b_kmajor = true; g1.C = d_W; g1.ldc = nbp;
+        CKR(launch_gemm(g1, 0, s, &nl, &t_svd_splitws));
+        GemmOp g2;  // Y = W (-T)
+        g2.M = rT; g2.N = nbp; g2.K = nbp; g2.A = d_W; g2.lda = nbp; g2.B = d_negT; g2.ldb = nbp;
+        g2.b_kmajor = false; g2.C = d_Y; g2.ldc = nbp;
+        CKR(launch_gemm(g2, 0, s, &nl, &t_svd_splitws));
+        GemmOp g3;  // P_t += Y Vt
+        g3.M = rT; g3.N = L; g3.K = nbp; g3.A = d_Y; g3.lda = nbp; g3.B = d_Vt + j; g3.ldb = colsP;
+        g3.b_kmajor = false; g3.C = Pt; g3.ldc = colsP; g3.accumulate = 1;
+        CKR(launch_gemm(g3, 0, s, &nl, &t_svd_splitws));
+      }
+    }
+    lq_pack_lower_kernel<<<ew_grid(nblk * kSvdB * R), 256, 0, s>>>(d_P, colsP, Xb, R, kmin, nblk);
+  } else if (dir == 0) {
     svd_pack_kernel<<<ew_grid(nblk * kSvdB * R), 256, 0, s>>>(psi, Xb, R, ncols, nblk);
   } else {
     dim3 grid((unsigned)((R + 31) / 32), (unsigned)(nblk * kSvdB / 32));
@@ -1935,12 +2021,12 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   CK(cudaMemcpyAsync(S, sv.data(), sizeof(double) * kmin, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(d_perm, order.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(d_skept, sv.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
-  svd_sign_kernel<<<(unsigned)n, 256, 0, s>>>(Xb, R, d_perm, d_skept, d_scale);
+  svd_sign_kernel<<<(unsigned)n, 256, 0, s>>>(Xb, R, d_perm, d_skept, d_scale, d_rowperm);
   dim3 gg((unsigned)std::min<int64_t>((R + 255) / 256, 1024), (unsigned)n);
   int nl = 0;
   int r = HEFF_OK;
   if (dir == 0) {
-    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, d_Ut);   // U^T [n][M]
+    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, d_Ut, d_rowperm);   // U^T [n][M]
     dim3 tg((unsigned)((M + 31) / 32), (unsigned)((n + 31) / 32));
     transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(d_Ut, Qout, n, M);            // U [M][n]
     CK(cudaGetLastError());
@@ -1948,7 +2034,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     g.M = n; g.N = N; g.K = M; g.A = d_Ut; g.lda = M; g.B = psi; g.ldb = N; g.b_kmajor = false; g.C = Cout; g.ldc = N;
     r = launch_gemm(g, 0, s, &nl, &t_svd_splitws);
   } else {
-    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, Qout);   // V^T [n][N]
+    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, Qout, d_rowperm);   // V^T [n][N]
     CK(cudaGetLastError());
     GemmOp g;  // C[M][n] = Psi[M][N] . (V^T)^T
     g.M = M; g.N = n; g.K = N; g.A = psi; g.lda = N; g.B = Qout; g.ldb = N; g.b_kmajor = true; g.C = Cout; g.ldc = n;

@@ -1,0 +1,143 @@
+// lq.cuh -- Householder LQ factor (L only) of the split's working matrix: the Jacobi
+// preconditioner of heff_svd_split.
+//
+// P = L Q (Q orthonormal rows, never formed), so P and L share U and S: one-sided Jacobi
+// on the columns of L gives L W = U S directly.  L is the transposed R factor of P^T; its
+// columns are graded (|l_ii| roughly decreasing), which is the case where one-sided Jacobi
+// converges in few sweeps (the Drmac-Veselic preconditioning; unpreconditioned Jacobi
+// needs ~2-3x more sweeps on spectra decaying over many decades, e.g. DMRG wavefunctions).
+//
+// Blocked right-looking Householder, 32 reflectors per panel:
+//   lq_panel_kernel   factors the panel rows [j, j+nb) over columns [j, n) with a
+//                     cooperative grid: every CTA keeps a 32 x <=128 column slice of the
+//                     panel in shared memory; per reflector one grid barrier joins the
+//                     partial dot products <x_r, x_i> (fixed-order sums: deterministic).
+//   lq_build_t_kernel the 32 x 32 triangular factor of the compact WY form
+//                     H_1 ... H_nb = I - V T V^T from V V^T and the betas.
+//   trailing rows     P_t <- P_t (I - V T V^T) by three DMMA GEMMs (heff_api.cu).
+#pragma once
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace heff {
+
+constexpr int kLqNb = 32;        // reflectors per panel
+constexpr int kLqThreads = 256;
+constexpr int kLqMaxCols = 128;  // panel columns per CTA (at most)
+constexpr int kLqPitch = kLqMaxCols + 1;
+
+// P: working matrix (row pitch ldp).  Panel: local rows [0, nbp) = global rows j.., local
+// columns [0, L) = global columns j..  Vt: [nbp][ldv] (global column index), zero on entry.
+// part: [2][gridDim.x][2 * kLqNb] scratch.  beta: [nbp].
+__global__ void __launch_bounds__(kLqThreads) lq_panel_kernel(double* __restrict__ P, int64_t ldp, int64_t j,
+                                                             int nbp, int64_t L, int cw, double* __restrict__ Vt,
+                                                             int64_t ldv, double* __restrict__ beta,
+                                                             double* __restrict__ part) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double S[kLqNb][kLqPitch];
+  __shared__ double sh_g[kLqNb], sh_col[kLqNb];
+  const int tid = threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.x * cw;
+  const int64_t rem = L - c0;
+  const int ncol = rem <= 0 ? 0 : (rem < cw ? (int)rem : cw);
+  double* base = P + j * ldp + j;
+  for (int e = tid; e < kLqNb * kLqMaxCols; e += blockDim.x) {
+    const int r = e / kLqMaxCols, c = e % kLqMaxCols;
+    S[r][c] = (r < nbp && c < ncol) ? base[(int64_t)r * ldp + c0 + c] : 0.0;
+  }
+  __syncthreads();
+  const int nparts = gridDim.x;
+  for (int i = 0; i < nbp; ++i) {
+    double* pb = part + (int64_t)(i & 1) * nparts * (2 * kLqNb) + (int64_t)blockIdx.x * (2 * kLqNb);
+    // partial <x_r, x_i> over this slice's columns >= i
+    {
+      const int r = tid >> 3, l = tid & 7;
+      double acc = 0.0;
+      if (r >= i && r < nbp)
+        for (int c = l; c < ncol; c += 8)
+          if (c0 + c >= i) acc = fma(S[r][c], S[i][c], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      if (l == 0) pb[r] = acc;
+      if (tid < kLqNb && i >= c0 && i < c0 + ncol) pb[kLqNb + tid] = S[tid][i - c0];  // column i (owner)
+    }
+    grid.sync();
+    const int owner = (int)(i / cw);
+    if (tid < kLqNb) {
+      double g = 0.0;
+      const double* pp = part + (int64_t)(i & 1) * nparts * (2 * kLqNb);
+      for (int b = 0; b < nparts; ++b) g += pp[(int64_t)b * (2 * kLqNb) + tid];
+      sh_g[tid] = g;
+      sh_col[tid] = pp[(int64_t)owner * (2 * kLqNb) + kLqNb + tid];
+    }
+    __syncthreads();
+    const double norm2 = sh_g[i], x0 = sh_col[i];
+    double alpha = 0.0, v0 = 0.0, bt = 0.0;
+    if (norm2 > 0.0) {
+      alpha = -copysign(sqrt(norm2), x0);
+      v0 = x0 - alpha;
+      bt = 1.0 / (norm2 - alpha * x0);  // 2 / v^T v with v^T v = 2 (norm2 - alpha x0)
+    }
+    // rows r > i: x_r <- x_r - beta <x_r, v> v, <x_r, v> = <x_r, x_i> - alpha x_r[i]
+    for (int e = tid; e < kLqNb * kLqMaxCols; e += blockDim.x) {
+      const int r = e / kLqMaxCols, c = e % kLqMaxCols;
+      if (r <= i || r >= nbp || c >= ncol || c0 + c < i) continue;
+      const double w = sh_g[r] - alpha * sh_col[r];
+      const double vc = (c0 + c == i) ? v0 : S[i][c];
+      S[r][c] = fma(-bt * w, vc, S[r][c]);
+    }
+    __syncthreads();
+    for (int c = tid; c < ncol; c += blockDim.x) {  // row i: v into Vt, L entries into P
+      const int64_t gc = c0 + c;
+      if (gc < i) continue;
+      Vt[(int64_t)i * ldv + j + gc] = (gc == i) ? v0 : S[i][c];
+      S[i][c] = (gc == i) ? alpha : 0.0;
+    }
+    if (blockIdx.x == 0 && tid == 0) beta[i] = bt;
+    __syncthreads();
+  }
+  for (int e = tid; e < kLqNb * kLqMaxCols; e += blockDim.x) {
+    const int r = e / kLqMaxCols, c = e % kLqMaxCols;
+    if (r < nbp && c < ncol) base[(int64_t)r * ldp + c0 + c] = S[r][c];
+  }
+}
+
+// T (upper triangular, nbp x nbp, row-major, written NEGATED for the update GEMM):
+// T_ii = beta_i, T[0:i, i] = -beta_i T[0:i, 0:i] (V^T v_i)[0:i]   (forward, column-wise WY)
+__global__ void lq_build_t_kernel(const double* __restrict__ VtV, const double* __restrict__ beta, int nbp,
+                                  double* __restrict__ negT) {
+  __shared__ double T[kLqNb][kLqNb + 1];
+  const int l = threadIdx.x;  // 32 threads
+  for (int c = 0; c < kLqNb; ++c) T[l][c] = 0.0;
+  __syncwarp();
+  for (int i = 0; i < nbp; ++i) {
+    double s = 0.0;
+    if (l < i)
+      for (int p = l; p < i; ++p) s = fma(T[l][p], VtV[p * nbp + i], s);
+    __syncwarp();
+    if (l < i) T[l][i] = -beta[i] * s;
+    if (l == i) T[i][i] = beta[i];
+    __syncwarp();
+  }
+  for (int c = 0; c < nbp; ++c)
+    if (l < nbp) negT[l * nbp + c] = -T[l][c];
+}
+
+// X (block-column layout, as svd_pack_kernel) from the lower trapezoid of P (rows R, the
+// first k columns): X[r][c] = (c <= r && c < k) ? P[r][c] : 0
+__global__ void lq_pack_lower_kernel(const double* __restrict__ P, int64_t ldp, double* __restrict__ Xb, int64_t R,
+                                     int64_t k, int64_t nblk) {
+  const int64_t total = nblk * R * 16;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int jj = (int)(e & 15);
+    const int64_t rb = e >> 4;
+    const int64_t blk = rb / R, r = rb - blk * R;
+    const int64_t c = blk * 16 + jj;
+    Xb[e] = (c < k && c <= r) ? P[r * ldp + c] : 0.0;
+  }
+}
+
+}  // namespace heff

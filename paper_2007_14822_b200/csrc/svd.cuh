@@ -388,21 +388,24 @@ __global__ void svd_colnorm_kernel(const double* __restrict__ Xb, int64_t R, int
 }
 
 // scale[k] = sign / s_k, sign making the largest-|.| entry of column perm[k] positive (first on ties)
+// rowperm (nullable): X's row r is row rowperm[r] of the output factor (ties break on that index)
 __global__ void svd_sign_kernel(const double* __restrict__ Xb, int64_t R, const int* __restrict__ perm,
-                                const double* __restrict__ s, double* __restrict__ scale) {
+                                const double* __restrict__ s, double* __restrict__ scale, const int* __restrict__ rowperm) {
   __shared__ double sv[256];
-  __shared__ int64_t si[256];
+  __shared__ int64_t si[256], sx[256];
   const int k = blockIdx.x;
   const int c = perm[k];
   const double* col = Xb + (int64_t)(c >> 4) * R * kSvdB + (c & 15);
   double best = -1.0;
-  int64_t bi = 0;
+  int64_t bi = 0, bx = 0;  // output-row index (tie-break), X row
   for (int64_t r = threadIdx.x; r < R; r += blockDim.x) {
     const double a = fabs(col[r * kSvdB]);
-    if (a > best) { best = a; bi = r; }
+    const int64_t ri = rowperm ? rowperm[r] : r;
+    if (a > best || (a == best && ri < bi)) { best = a; bi = ri; bx = r; }
   }
   sv[threadIdx.x] = best;
   si[threadIdx.x] = bi;
+  sx[threadIdx.x] = bx;
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
     if ((int)threadIdx.x < w) {
@@ -411,22 +414,47 @@ __global__ void svd_sign_kernel(const double* __restrict__ Xb, int64_t R, const 
       if (o > sv[threadIdx.x] || (o == sv[threadIdx.x] && oi < si[threadIdx.x])) {
         sv[threadIdx.x] = o;
         si[threadIdx.x] = oi;
+        sx[threadIdx.x] = sx[threadIdx.x + w];
       }
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) scale[k] = (col[si[0] * kSvdB] < 0.0 ? -1.0 : 1.0) / s[k];
+  if (threadIdx.x == 0) scale[k] = (col[sx[0] * kSvdB] < 0.0 ? -1.0 : 1.0) / s[k];
 }
 
 // out[k][r] = X[r][perm k] * scale[k]   (k < n: grid.y; r < R)
 __global__ void svd_gather_t_kernel(const double* __restrict__ Xb, int64_t R, const int* __restrict__ perm,
-                                    const double* __restrict__ scale, double* __restrict__ out) {
+                                    const double* __restrict__ scale, double* __restrict__ out,
+                                    const int* __restrict__ rowperm) {
   const int k = blockIdx.y;
   const int c = perm[k];
   const double sc = scale[k];
   const double* col = Xb + (int64_t)(c >> 4) * R * kSvdB + (c & 15);
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x)
-    out[(int64_t)k * R + r] = col[r * kSvdB] * sc;
+    out[(int64_t)k * R + (rowperm ? rowperm[r] : r)] = col[r * kSvdB] * sc;
+}
+
+// row norms^2 of a row-major matrix (one warp per row)
+__global__ void svd_rownorm2_kernel(const double* __restrict__ A, int64_t rows, int64_t cols, double* __restrict__ out) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  double acc = 0.0;
+  for (int64_t c = lane; c < cols; c += 32) {
+    const double v = A[row * cols + c];
+    acc = fma(v, v, acc);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[row] = acc;
+}
+
+// dst row r = src row perm[r] (row-major, cols per row)
+__global__ void svd_gather_rows_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t rows,
+                                       int64_t cols, const int* __restrict__ perm) {
+  const int64_t row = blockIdx.y;
+  const double* sr = src + (int64_t)perm[row] * cols;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x)
+    dst[row * cols + c] = sr[c];
 }
 
 }  // namespace heff
