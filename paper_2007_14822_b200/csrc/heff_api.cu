@@ -1784,6 +1784,7 @@ static std::vector<int2> svd_pair_schedule(int nblk) {
 
 static constexpr int kSvdMaxSweeps = 80;
 static int g_lq_grid = 0;  // co-resident CTAs of lq_panel_kernel (cooperative launch)
+static int g_svd_gram_occ = 0, g_svd_rot_occ = 0;  // co-resident CTAs per SM
 static constexpr double kSvdRankEps = 1e-12;   // reading R21
 static constexpr double kSvdNegligible = 1e-15; // columns below this fraction of ||Psi||_F are not rotated
 
@@ -1815,18 +1816,25 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   if (nblk & 1) ++nblk;
   if (nblk < 2) nblk = 2;
   const int npairs = (int)(nblk / 2), rounds = (int)(nblk - 1);
-  // row splits: about 4 CTAs per SM for the Gram, 8 for the rotation
-  const int64_t rs1 = std::max<int64_t>(1, std::min<int64_t>((4 * g_num_sms + npairs - 1) / npairs, (R + 127) / 128));
-  const int rows1 = (int)(((R + rs1 - 1) / rs1 + 127) / 128 * 128);
-  const int rsplit = (int)((R + rows1 - 1) / rows1);
-  const int64_t rs2 = std::max<int64_t>(1, std::min<int64_t>((8 * g_num_sms + npairs - 1) / npairs, (R + 31) / 32));
-  const int rows2 = (int)(((R + rs2 - 1) / rs2 + 31) / 32 * 32);
-  const int rsplit2 = (int)((R + rows2 - 1) / rows2);
+  // balanced persistent grids (svd.cuh): one wave of co-resident CTAs, work split evenly
+  if (g_svd_gram_occ == 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_gram_occ, svd_gram_kernel, kSvdGramThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_rot_occ, svd_rotate_kernel, kSvdRotThreads, 0));
+    g_svd_gram_occ = std::max(1, g_svd_gram_occ);
+    g_svd_rot_occ = std::max(1, g_svd_rot_occ);
+  }
+  const int64_t gram_chunks = (R + 127) / 128;
+  const int gram_grid = (int)std::min<int64_t>((int64_t)g_svd_gram_occ * g_num_sms, npairs * gram_chunks);
+  int nslots = 1;  // CTAs touching one pair, at most
+  for (int p = 0; p < npairs; ++p)
+    nslots = std::max(nslots, svd_sk_owner((int64_t)p * gram_chunks + gram_chunks - 1, npairs * gram_chunks, gram_grid) -
+                                  svd_sk_owner((int64_t)p * gram_chunks, npairs * gram_chunks, gram_grid) + 1);
+  const int rot_grid = (int)std::min<int64_t>((int64_t)g_svd_rot_occ * g_num_sms, npairs * ((R + 31) / 32));
   const int red_blocks = 4 * g_num_sms;
 
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t bX = al(sizeof(double) * nblk * kSvdB * R);
-  const size_t bG = al(sizeof(double) * (size_t)npairs * rsplit * kSvdPair * kSvdPair);
+  const size_t bG = al(sizeof(double) * (size_t)npairs * nslots * kSvdPair * kSvdPair);
   const size_t bNorm = al(sizeof(double) * nblk * kSvdB);
   const size_t bPairs = al(sizeof(int2) * (size_t)rounds * npairs);
   const size_t bStat = al(sizeof(unsigned long long) * kSvdMaxSweeps + sizeof(int) * kSvdMaxSweeps);
@@ -1972,10 +1980,10 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     }
     for (int r = 0; r < rounds; ++r) {
       const int2* pr = d_pairs + (size_t)r * npairs;
-      svd_gram_kernel<<<dim3(npairs, rsplit), kSvdGramThreads, 0, s>>>(Xb, R, pr, rows1, Gp);
-      svd_pair_eig_kernel<<<npairs, kSvdEigThreads, 0, s>>>(Gp, rsplit, tol, negl, inner, d_Qg, d_flag,
-                                                           d_maxoff + sw, d_nrot + sw);
-      svd_rotate_kernel<<<dim3(npairs, rsplit2), kSvdRotThreads, 0, s>>>(Xb, R, pr, d_Qg, d_flag, rows2);
+      svd_gram_kernel<<<gram_grid, kSvdGramThreads, 0, s>>>(Xb, R, pr, npairs, nslots, Gp);
+      svd_pair_eig_kernel<<<npairs, kSvdEigThreads, 0, s>>>(Gp, nslots, gram_chunks, gram_grid, tol, negl, inner,
+                                                           d_Qg, d_flag, d_maxoff + sw, d_nrot + sw);
+      svd_rotate_kernel<<<rot_grid, kSvdRotThreads, 0, s>>>(Xb, R, pr, npairs, d_Qg, d_flag);
     }
     CK(cudaGetLastError());
     int nrot = 0;

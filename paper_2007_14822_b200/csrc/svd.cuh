@@ -99,65 +99,96 @@ __global__ void svd_sum_kernel(const double* __restrict__ part, int n, double* _
 }
 
 // ---------------------------------------------------------------- Gram partials
-// Gp[(p * gridDim.y + split)][32][32] = sum over rows of the split of Y[r]^T Y[r],
-// Y = [X_I | X_J].  Lane (g, t) of a warp loads row (t) columns 4g..4g+3 (32 B): tile i of
-// the DMMA A/B operands is column 4g + i, so tile (i, j) accumulates G[4m+i][4n+j].
-__global__ void __launch_bounds__(kSvdGramThreads) svd_gram_kernel(const double* __restrict__ Xb, int64_t R,
-                                                                   const int2* __restrict__ pairs, int rows_per_cta,
-                                                                   double* __restrict__ Gp) {
+// Balanced persistent schedule (stream-K style): the work is npairs x C chunks of 128 rows
+// (chunk = one pass of the 8 warps x 4 lanes-rows x 4 unrolled rows); CTA b owns the
+// contiguous iteration range [T b / G, T (b+1) / G), T = npairs C, G = gridDim.x, so there
+// is no wave-quantisation tail.  A pair split across CTAs gets one partial Gram per CTA in
+// slot (b - b0(pair)); the eigen kernel sums the slots in order (deterministic).
+__host__ __device__ __forceinline__ int64_t svd_sk_start(int64_t T, int64_t b, int64_t G) { return T * b / G; }
+__host__ __device__ __forceinline__ int svd_sk_owner(int64_t it, int64_t T, int64_t G) {
+  int64_t b = (it * G) / T;
+  while (b + 1 < G && svd_sk_start(T, b + 1, G) <= it) ++b;
+  while (b > 0 && svd_sk_start(T, b, G) > it) --b;
+  return (int)b;
+}
+
+// G[4m+i][4n+j] tile accumulation of one 128-row chunk; lane (g, t) holds row (t) columns 4g..4g+3
+__device__ __forceinline__ void svd_gram_load(const double* __restrict__ base, int64_t rb, int64_t r_end, int warp,
+                                              int t, double (&v)[4][4]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t r = rb + u * 32 + warp * 4 + t;
+    if (r < r_end) {
+      const double2* src = reinterpret_cast<const double2*>(base + r * kSvdB);
+      const double2 a = __ldg(src), b = __ldg(src + 1);
+      v[u][0] = a.x; v[u][1] = a.y; v[u][2] = b.x; v[u][3] = b.y;
+    } else {
+      v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSvdGramThreads, 2) svd_gram_kernel(const double* __restrict__ Xb, int64_t R,
+                                                                   const int2* __restrict__ pairs, int npairs,
+                                                                   int nslots, double* __restrict__ Gp) {
   __shared__ double red[kSvdGramThreads / 32][10 * 64];
-  const int p = blockIdx.x, split = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int2 pr = pairs[p];
-  const double* base = Xb + (int64_t)(g < 4 ? pr.x : pr.y) * R * kSvdB + (g & 3) * 4;
-  double acc[10][2];
+  const int64_t C = (R + 127) / 128;
+  const int64_t T = (int64_t)npairs * C, G = gridDim.x;
+  int64_t it = svd_sk_start(T, blockIdx.x, G);
+  const int64_t it_end = svd_sk_start(T, blockIdx.x + 1, G);
+  while (it < it_end) {
+    const int p = (int)(it / C);
+    const int64_t ch0 = it - (int64_t)p * C;
+    const int64_t ch1 = min(C, ch0 + (it_end - it));
+    const int2 pr = pairs[p];
+    const double* base = Xb + (int64_t)(g < 4 ? pr.x : pr.y) * R * kSvdB + (g & 3) * 4;
+    double acc[10][2];
 #pragma unroll
-  for (int i = 0; i < 10; ++i) acc[i][0] = acc[i][1] = 0.0;
-  const int64_t r_begin = (int64_t)split * rows_per_cta;
-  const int64_t r_end = min(R, r_begin + (int64_t)rows_per_cta);
-  for (int64_t rb = r_begin; rb < r_end; rb += 128) {
-    double v[4][4];
+    for (int i = 0; i < 10; ++i) acc[i][0] = acc[i][1] = 0.0;
+    double v[4][4], w[4][4];
+    svd_gram_load(base, ch0 * 128, R, warp, t, v);
+    for (int64_t ch = ch0; ch < ch1; ++ch) {
+      if (ch + 1 < ch1) svd_gram_load(base, (ch + 1) * 128, R, warp, t, w);  // prefetch
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t r = rb + u * 32 + warp * 4 + t;
-      if (r < r_end) {
-        const double2* src = reinterpret_cast<const double2*>(base + r * kSvdB);
-        const double2 a = __ldg(src), b = __ldg(src + 1);
-        v[u][0] = a.x; v[u][1] = a.y; v[u][2] = b.x; v[u][3] = b.y;
-      } else {
-        v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.0;
+      for (int u = 0; u < 4; ++u) {
+        int idx = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = i; j < 4; ++j, ++idx) dmma_8x8x4(acc[idx][0], acc[idx][1], v[u][i], v[u][j]);
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[u][q] = w[u][q];
     }
+    // partial of this pair -> slot (b - b0)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int idx = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = i; j < 4; ++j, ++idx) dmma_8x8x4(acc[idx][0], acc[idx][1], v[u][i], v[u][j]);
+    for (int i = 0; i < 10; ++i) {
+      red[warp][i * 64 + lane * 2] = acc[i][0];
+      red[warp][i * 64 + lane * 2 + 1] = acc[i][1];
     }
-  }
+    __syncthreads();
+    const int slot = (int)blockIdx.x - svd_sk_owner((int64_t)p * C, T, G);
+    double* out = Gp + ((int64_t)p * nslots + slot) * (kSvdPair * kSvdPair);
+    for (int e = threadIdx.x; e < 10 * 64; e += blockDim.x) {
+      double sum = 0.0;
 #pragma unroll
-  for (int i = 0; i < 10; ++i) {
-    red[warp][i * 64 + lane * 2] = acc[i][0];
-    red[warp][i * 64 + lane * 2 + 1] = acc[i][1];
-  }
-  __syncthreads();
-  double* out = Gp + ((int64_t)p * gridDim.y + split) * (kSvdPair * kSvdPair);
-  for (int e = threadIdx.x; e < 10 * 64; e += blockDim.x) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kSvdGramThreads / 32; ++w) s += red[w][e];
-    const int idx = e >> 6, l = (e >> 1) & 31, h = e & 1;
-    int i = 0, j = 0, k = idx;  // idx -> (i, j), i <= j, row-major over the upper triangle
-    for (i = 0; i < 4; ++i) {
-      if (k < 4 - i) { j = i + k; break; }
-      k -= 4 - i;
+      for (int ww = 0; ww < kSvdGramThreads / 32; ++ww) sum += red[ww][e];
+      const int idx = e >> 6, l = (e >> 1) & 31, h = e & 1;
+      int i = 0, j = 0, k = idx;  // idx -> (i, j), i <= j, row-major over the upper triangle
+      for (i = 0; i < 4; ++i) {
+        if (k < 4 - i) { j = i + k; break; }
+        k -= 4 - i;
+      }
+      const int gm = l >> 2, tn = l & 3;
+      const int row = 4 * gm + i, col = 4 * (2 * tn + h) + j;
+      out[row * kSvdPair + col] = sum;
+      if (i != j) out[col * kSvdPair + row] = sum;
     }
-    const int gm = l >> 2, tn = l & 3;
-    const int row = 4 * gm + i, col = 4 * (2 * tn + h) + j;
-    out[row * kSvdPair + col] = s;
-    if (i != j) out[col * kSvdPair + row] = s;
+    __syncthreads();
+    it += ch1 - ch0;
   }
 }
 
@@ -171,7 +202,8 @@ __global__ void __launch_bounds__(kSvdGramThreads) svd_gram_kernel(const double*
 // 2x2 values), and Q <- Q J by columns.  Output: Qg[p] (row-major 32x32), flag[p].
 constexpr int kSvdEigThreads = 256;
 
-__global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const double* __restrict__ Gp, int rsplit,
+__global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const double* __restrict__ Gp, int nslots,
+                                                                     int64_t C, int gram_grid,
                                                                      double tol, double negl, int inner_sweeps,
                                                                      double* __restrict__ Qg, int* __restrict__ flag,
                                                                      unsigned long long* __restrict__ stat_maxoff,
@@ -185,10 +217,12 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
   __shared__ double s_off[kSvdEigThreads / 32];
   const int p = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const double* gsrc = Gp + (int64_t)p * rsplit * (kSvdPair * kSvdPair);
+  const double* gsrc = Gp + (int64_t)p * nslots * (kSvdPair * kSvdPair);
+  const int64_t T = (int64_t)gridDim.x * C;
+  const int nsum = svd_sk_owner((int64_t)p * C + C - 1, T, gram_grid) - svd_sk_owner((int64_t)p * C, T, gram_grid) + 1;
   for (int e = tid; e < kSvdPair * kSvdPair; e += blockDim.x) {
     double v = 0.0;
-    for (int sp = 0; sp < rsplit; ++sp) v += gsrc[(int64_t)sp * (kSvdPair * kSvdPair) + e];
+    for (int sp = 0; sp < nsum; ++sp) v += gsrc[(int64_t)sp * (kSvdPair * kSvdPair) + e];
     const int r = e >> 5, c = e & 31;
     G[r][c] = v;
     Q[r][c] = (r == c) ? 1.0 : 0.0;
@@ -290,58 +324,74 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
 }
 
 // ---------------------------------------------------------------- rotation
-// Y <- Y Q on a row range of a rotated pair.  A = Y (row g, k-slice kk of lane t = column
-// 8t + kk), B = Q fragments held in registers, D tile n = output columns 8n + {2t, 2t+1}.
-__global__ void __launch_bounds__(kSvdRotThreads) svd_rotate_kernel(double* __restrict__ Xb, int64_t R,
-                                                                   const int2* __restrict__ pairs,
-                                                                   const double* __restrict__ Qg,
-                                                                   const int* __restrict__ flag, int rows_per_cta) {
-  const int p = blockIdx.x;
-  if (!flag[p]) return;
+// Y <- Y Q on the rotated pairs.  A = Y (row g, k-slice kk of lane t = column 8t + kk),
+// B = Q fragments held in registers, D tile n = output columns 8n + {2t, 2t+1}.
+// Balanced persistent schedule over npairs x C2 groups of 32 rows (4 warps x 8 rows), the
+// next group's rows prefetched into registers while the current one is on the DMMA pipe.
+__device__ __forceinline__ void svd_rot_load(const double* __restrict__ src, bool ok, double (&y)[8]) {
+  if (ok) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 v = s2[q];
+      y[2 * q] = v.x;
+      y[2 * q + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kSvdRotThreads, 4) svd_rotate_kernel(double* __restrict__ Xb, int64_t R,
+                                                                      const int2* __restrict__ pairs, int npairs,
+                                                                      const double* __restrict__ Qg,
+                                                                      const int* __restrict__ flag) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const double* q = Qg + (int64_t)p * (kSvdPair * kSvdPair);
-  double qf[8][4];
-#pragma unroll
-  for (int kk = 0; kk < 8; ++kk)
-#pragma unroll
-    for (int n = 0; n < 4; ++n) qf[kk][n] = __ldg(q + (8 * t + kk) * kSvdPair + 8 * n + g);
-  const int2 pr = pairs[p];
-  double* XI = Xb + (int64_t)pr.x * R * kSvdB;
-  double* XJ = Xb + (int64_t)pr.y * R * kSvdB;
-  const double* src_base = (t < 2 ? XI : XJ) + (t & 1) * 8;
-  const int64_t r_begin = (int64_t)blockIdx.y * rows_per_cta;
-  const int64_t r_end = min(R, r_begin + (int64_t)rows_per_cta);
-#pragma unroll 2
-  for (int64_t rb = r_begin + warp * 8; rb < r_end; rb += 8 * (kSvdRotThreads / 32)) {
-    const int64_t row = rb + g;
-    const bool ok = row < r_end;
-    double y[8];
-    if (ok) {
-      const double2* s2 = reinterpret_cast<const double2*>(src_base + row * kSvdB);
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const double2 v = s2[qq];
-        y[2 * qq] = v.x;
-        y[2 * qq + 1] = v.y;
-      }
-    } else {
-#pragma unroll
-      for (int qq = 0; qq < 8; ++qq) y[qq] = 0.0;
-    }
-    double acc[4][2];
-#pragma unroll
-    for (int n = 0; n < 4; ++n) acc[n][0] = acc[n][1] = 0.0;
+  const int64_t C2 = (R + 31) / 32;
+  const int64_t T = (int64_t)npairs * C2, G = gridDim.x;
+  int64_t it = svd_sk_start(T, blockIdx.x, G);
+  const int64_t it_end = svd_sk_start(T, blockIdx.x + 1, G);
+  while (it < it_end) {
+    const int p = (int)(it / C2);
+    const int64_t g0 = it - (int64_t)p * C2;
+    const int64_t g1 = min(C2, g0 + (it_end - it));
+    it += g1 - g0;
+    if (!flag[p]) continue;
+    const double* q = Qg + (int64_t)p * (kSvdPair * kSvdPair);
+    double qf[8][4];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
-      for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[n][0], acc[n][1], y[kk], qf[kk][n]);
-    if (ok) {
+      for (int n = 0; n < 4; ++n) qf[kk][n] = __ldg(q + (8 * t + kk) * kSvdPair + 8 * n + g);
+    const int2 pr = pairs[p];
+    double* XI = Xb + (int64_t)pr.x * R * kSvdB;
+    double* XJ = Xb + (int64_t)pr.y * R * kSvdB;
+    const double* src_base = (t < 2 ? XI : XJ) + (t & 1) * 8;
+    double y[8], yn[8];
+    int64_t row = g0 * 32 + warp * 8 + g;
+    svd_rot_load(src_base + row * kSvdB, row < R, y);
+    for (int64_t gi = g0; gi < g1; ++gi) {
+      const int64_t nrow = row + 32;
+      if (gi + 1 < g1) svd_rot_load(src_base + nrow * kSvdB, nrow < R, yn);  // prefetch
+      double acc[4][2];
 #pragma unroll
-      for (int n = 0; n < 4; ++n) {
-        double* dst = (n < 2 ? XI : XJ) + row * kSvdB + (((8 * n) & 15) + 2 * t);
-        *reinterpret_cast<double2*>(dst) = make_double2(acc[n][0], acc[n][1]);
+      for (int n = 0; n < 4; ++n) acc[n][0] = acc[n][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[n][0], acc[n][1], y[kk], qf[kk][n]);
+      if (row < R) {
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          double* dst = (n < 2 ? XI : XJ) + row * kSvdB + (((8 * n) & 15) + 2 * t);
+          *reinterpret_cast<double2*>(dst) = make_double2(acc[n][0], acc[n][1]);
+        }
       }
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) y[qq] = yn[qq];
+      row = nrow;
     }
   }
 }
