@@ -240,8 +240,8 @@ int heff_env_update_right(const heff_env_dims* dims, const double* R, const doub
  * discarded weight) and sweeps (Jacobi sweeps used; may be NULL) are HOST pointers.
  * trunc == NULL: cutoff 0, maxdim unlimited, mindim 1.  Errors: HEFF_EINVAL (bad sizes,
  * cutoff < 0, dir not 0/1), HEFF_EZERO (psi == 0), HEFF_ENOCONV (Jacobi sweep cap).
- * Workspace lives in a per-thread arena (about (2 max(M,N) + n) min(M,N)... doubles,
- * grown on demand, reused).  Synchronous on `stream`. */
+ * Workspace lives in a per-thread arena (about 4 M N + 2 n max(M, N) doubles, grown on
+ * demand and kept for later calls).  Synchronous on `stream`. */
 typedef struct {
   double cutoff;
   int64_t maxdim;
@@ -249,6 +249,11 @@ typedef struct {
 } heff_trunc;
 int heff_svd_split(int64_t M, int64_t N, const double* psi, const heff_trunc* trunc, int dir, double* Q, double* S,
                    double* C, int64_t* n_kept, double* trunc_err, int* sweeps, heff_stream stream);
+
+/* Host-only (no device work): the truncation rule heff_svd_split applies, on HOST values
+ * s[0..k) (descending, non-negative).  n_kept / trunc_err as in heff_svd_split.
+ * HEFF_EINVAL (not descending, negative, cutoff < 0), HEFF_EZERO (s[0] == 0). */
+int heff_truncate_spectrum(const double* s, int64_t k, const heff_trunc* trunc, int64_t* n_kept, double* trunc_err);
 
 #ifdef __cplusplus
 }

@@ -1788,6 +1788,41 @@ static int g_svd_gram_occ = 0, g_svd_rot_occ = 0;  // co-resident CTAs per SM
 static constexpr double kSvdRankEps = 1e-12;   // reading R21
 static constexpr double kSvdNegligible = 1e-15; // columns below this fraction of ||Psi||_F are not rotated
 
+// The truncation rule of the split (readings R20/R21) on descending singular values.
+static void truncate_rule(const double* sv, int64_t k, double cutoff, int64_t maxdim, int64_t mindim, int64_t* n_out,
+                          double* err_out) {
+  double total = 0.0;
+  for (int64_t i = k - 1; i >= 0; --i) total += sv[i] * sv[i];
+  int64_t rank = 0;
+  while (rank < k && sv[rank] > kSvdRankEps * sv[0]) ++rank;
+  int64_t n = k;
+  double disc = 0.0;
+  while (n > 1 && disc + sv[n - 1] * sv[n - 1] <= cutoff * total) {  // discard smallest while within cutoff
+    disc += sv[n - 1] * sv[n - 1];
+    --n;
+  }
+  n = std::min(n, rank);
+  n = std::max(n, std::min(std::max<int64_t>(1, mindim), rank));
+  if (maxdim > 0) n = std::min(n, maxdim);
+  double err = 0.0;
+  for (int64_t i = k - 1; i >= n; --i) err += sv[i] * sv[i];
+  *n_out = n;
+  *err_out = err / total;
+}
+
+extern "C" int heff_truncate_spectrum(const double* s, int64_t k, const heff_trunc* trunc, int64_t* n_kept,
+                                      double* trunc_err) {
+  if (!s || k < 1 || !n_kept || !trunc_err) return set_err(HEFF_EINVAL, "heff_truncate_spectrum: bad argument");
+  const double cutoff = trunc ? trunc->cutoff : 0.0;
+  if (!(cutoff >= 0.0)) return set_err(HEFF_EINVAL, "heff_truncate_spectrum: cutoff < 0");
+  for (int64_t i = 0; i < k; ++i)
+    if (!(s[i] >= 0.0) || (i > 0 && s[i] > s[i - 1]))
+      return set_err(HEFF_EINVAL, "heff_truncate_spectrum: values must be descending and non-negative");
+  if (!(s[0] > 0.0)) return set_err(HEFF_EZERO, "heff_truncate_spectrum: zero spectrum");
+  truncate_rule(s, k, cutoff, trunc ? trunc->maxdim : 0, trunc ? trunc->mindim : 1, n_kept, trunc_err);
+  return HEFF_OK;
+}
+
 extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const heff_trunc* trunc, int dir, double* Qout,
                               double* S, double* Cout, int64_t* n_kept, double* trunc_err, int* sweeps_out,
                               heff_stream stream) {
@@ -2012,20 +2047,9 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   double total = 0.0;
   for (int64_t i = kmin - 1; i >= 0; --i) total += sv[i] * sv[i];
   if (!(sv[0] > 0.0)) return set_err(HEFF_EZERO, "heff_svd_split: psi is zero");
-  int64_t rank = 0;
-  while (rank < kmin && sv[rank] > kSvdRankEps * sv[0]) ++rank;
-  int64_t n = kmin;
-  double disc = 0.0;
-  while (n > 1 && disc + sv[n - 1] * sv[n - 1] <= cutoff * total) {
-    disc += sv[n - 1] * sv[n - 1];
-    --n;
-  }
-  n = std::min(n, rank);
-  n = std::max(n, std::min(mindim, rank));
-  if (maxdim > 0) n = std::min(n, maxdim);
+  int64_t n = 0;
   double err = 0.0;
-  for (int64_t i = kmin - 1; i >= n; --i) err += sv[i] * sv[i];
-  err /= total;
+  truncate_rule(sv.data(), kmin, cutoff, maxdim, mindim, &n, &err);
   CK(cudaMemcpyAsync(S, sv.data(), sizeof(double) * kmin, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(d_perm, order.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(d_skept, sv.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));

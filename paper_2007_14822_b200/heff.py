@@ -93,7 +93,9 @@ def lib() -> ctypes.CDLL:
         L.heff_env_update_right.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         L.heff_svd_split.argtypes = [i64, i64, vp, ctypes.POINTER(_Trunc), ip, vp, vp, vp, ctypes.POINTER(i64),
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ip), vp]
-        for f in ("heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
+        L.heff_truncate_spectrum.argtypes = [vp, i64, ctypes.POINTER(_Trunc), ctypes.POINTER(i64),
+                                             ctypes.POINTER(ctypes.c_double)]
+        for f in ("heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
                   "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z"):
@@ -106,7 +108,7 @@ EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "h
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
             "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z",
-            "heff_svd_split")
+            "heff_svd_split", "heff_truncate_spectrum")
 
 
 def _check(rc: int):
@@ -237,6 +239,17 @@ def svd_split(psi: torch.Tensor, cutoff: float = 0.0, maxdim: int = 0, mindim: i
     else:
         Qv, Cv = Q[: k * N].view(k, N), C[: M * k].view(M, k)
     return SplitResult(Qv, S, Cv, k, err.value, sw.value)
+
+
+def truncate_spectrum(s, cutoff: float = 0.0, maxdim: int = 0, mindim: int = 1) -> tuple[int, float]:
+    """libheff's host-side truncation rule (heff_truncate_spectrum) on descending values."""
+    import numpy as np
+    a = np.ascontiguousarray(np.asarray(s, dtype=np.float64))
+    n = ctypes.c_int64(0)
+    err = ctypes.c_double(0.0)
+    _check(lib().heff_truncate_spectrum(a.ctypes.data, a.size, ctypes.byref(_Trunc(float(cutoff), int(maxdim), int(mindim))),
+                                        ctypes.byref(n), ctypes.byref(err)))
+    return n.value, err.value
 
 
 def nccl_unique_id() -> bytes:

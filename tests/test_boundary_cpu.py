@@ -84,3 +84,33 @@ def test_library_tridiagonal_ql_vs_oracle_bisection_and_numpy(oracle_lib):
     # split matrix (a zero off-diagonal) and a 1x1
     th, y = heff.tridiag_lowest([2.0, -1.0, 3.0], [0.0, 0.5])
     assert abs(th - np.linalg.eigvalsh(np.diag([2.0, -1.0, 3.0]) + np.diag([0.0, 0.5], 1) + np.diag([0.0, 0.5], -1))[0]) < 1e-15
+
+
+def test_host_truncation_rule_matches_oracle_and_brute_force():
+    """heff_truncate_spectrum (the rule heff_svd_split applies on the host, readings R20/R21)
+    against the oracle's rule and SPEC.md's brute-force cut scan, host-only."""
+    import numpy as np
+    from oracle import split as osplit
+    from paper_2007_14822_b200 import heff
+    from tests.test_oracle_split import _brute_kept
+    assert heff.truncate_spectrum([1.0, 0, 0, 0]) == (1, 0.0)
+    n, e = heff.truncate_spectrum(np.array([1.0, 1, 1, 1]) / 2, maxdim=2)
+    assert n == 2 and abs(e - 0.5) < 1e-15
+    rng = np.random.default_rng(12)
+    for trial in range(400):
+        k = int(rng.integers(1, 50))
+        s = np.sort(np.exp(rng.uniform(-35, 0, k)))[::-1]
+        if rng.random() < 0.2 and k > 1:
+            s[rng.integers(1, k):] = 0.0
+        cutoff = float(10 ** rng.uniform(-16, -1)) if rng.random() < 0.9 else 0.0
+        maxdim, mindim = int(rng.integers(0, k + 3)), int(rng.integers(1, k + 2))
+        got = heff.truncate_spectrum(s, cutoff, maxdim, mindim)
+        ref = osplit.truncate_spectrum(s, cutoff, maxdim, mindim)
+        assert got[0] == ref[0] == _brute_kept(s, cutoff, maxdim, mindim), (trial, got, ref)
+        assert abs(got[1] - ref[1]) <= 1e-14 * max(1.0, ref[1])
+    with pytest.raises(heff.HeffError):
+        heff.truncate_spectrum([1.0, 2.0])
+    with pytest.raises(heff.HeffError):
+        heff.truncate_spectrum([1.0], cutoff=-1.0)
+    with pytest.raises(heff.HeffZeroVector):
+        heff.truncate_spectrum([0.0, 0.0])
