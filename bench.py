@@ -165,6 +165,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--sharded", action="store_true",
                     help="use the b'-sharded NCCL plan even at N=1 (exercises the multi-GPU code path)")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="sharded plans: GEMM_A reads the ranks' Krylov shards through NCCL symmetric-window "
+                         "(NVLink) pointers instead of ncclAllGather + relayout (NEXT-5)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -176,7 +179,7 @@ def main():
     from heffgen import configs as C
     from paper_2007_14822_b200 import Heff
     from paper_2007_14822_b200 import dist as hdist
-    from paper_2007_14822_b200.heff import OPT_PROFILE, OPT_TOTAL_LAUNCHES, nccl_unique_id
+    from paper_2007_14822_b200.heff import OPT_FUSED_GATHER, OPT_PROFILE, OPT_TOTAL_LAUNCHES, nccl_unique_id
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -207,6 +210,8 @@ def main():
         uid = hdist.broadcast_uid(nccl_unique_id() if rank == 0 else None, device=dev)
         Rg = x.R[lo:hi].contiguous()
         plan = Heff(x.L, x.W1, x.W2, Rg, dist=dict(nranks=world, rank=rank, b_lo=lo, b_hi=hi, uid=uid))
+        if args.fused_gather:
+            plan.set_option(OPT_FUSED_GATHER, 1)
         psi0 = x.psi[..., lo:hi].contiguous()
         order = "B (R-first) on b'-shards"
     else:
@@ -303,7 +308,9 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_name(args.config, dims), **dims, "order": order,
-                           "parallelism": f"b'-shard x{world} (NCCL)" if sharded else "single GPU",
+                           "parallelism": (f"b'-shard x{world} (" + ("gather-fused GEMM_A on NCCL symmetric-window "
+                                           "peer pointers" if args.fused_gather else "NCCL all-gather") + ")")
+                           if sharded else "single GPU",
                            "flops_per_matvec": flops, "l2": "inputs larger than L2 (psi 0.54 GB, L and R 2.7 GB each)",
                            "step": "one Lanczos iteration (matvec + CGS2 + norm + host tridiagonal)"},
                 "tflops": value * flops / 1e12, "frac_fp64_peak": value * flops / 1e12 / (FP64_PEAK_TFLOPS * world),

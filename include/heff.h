@@ -114,6 +114,13 @@ int heff_create_z(heff_plan* out, const heff_dims* dims, const double* L, const 
  * out must not alias psi.  Asynchronous on `stream`. */
 int heff_apply(heff_plan p, const double* psi, double* out, heff_stream stream);
 
+/* Gather-fused order-B matvec on a b'-sharded plan: psi is given
+ * as the P = mR / nb shards of the blocked layout psi_blocked[P][mL*d1*d2][nb] (what an
+ * all-gather of the shards produces) and GEMM_A reads every shard through its own TMA
+ * descriptor -- no re-layout.  out = this plan's shard [mL][d1][d2][nb].  Requires
+ * nb % 16 == 0, P <= 8, 16-byte alignment.  Asynchronous on `stream`. */
+int heff_apply_blocked(heff_plan p, const double* psi_blocked, double* out, heff_stream stream);
+
 /* Same as heff_apply with HOST psi / out (pageable or pinned); copies in and out on
  * `stream` and synchronises it.  The end-to-end entry point. */
 int heff_apply_host(heff_plan p, const double* psi_host, double* out_host, heff_stream stream);
@@ -202,6 +209,17 @@ typedef struct {
 } heff_qn;
 int heff_set_qn(heff_plan p, const heff_qn* qn);
 enum { HEFF_OPT_SPARSE_KBLOCKS = 6 }; /* get: scheduled (tile, 16-wide k-block) products per matvec */
+
+/* Gather-fused sharded Lanczos.  HEFF_OPT_FUSED_GATHER = 1 on a
+ * communicating b'-sharded plan (default: env HEFF_FUSED_GATHER, else 0): lanczos_ground
+ * keeps its Krylov basis in an NCCL symmetric-memory window (ncclMemAlloc +
+ * ncclCommWindowRegister, collective on the first call) and every matvec's GEMM_A reads the
+ * ranks' shards of v_j directly through their NVLink load/store pointers -- no ncclAllGather,
+ * no re-layout.  Ordering: after writing its shard of v_j a rank releases a flag in every
+ * rank's window; the matvec waits (acquire) for all flags (20 s bound -> HEFF_ENCCL).
+ * get returns option | 2 * (the last lanczos_ground used the fused path).  Requires
+ * nb % 16 == 0 and nranks <= 8; real, non-U(1) plans. */
+enum { HEFF_OPT_FUSED_GATHER = 7 };
 
 /* ---- Environment update --------------------------------------
  * After each local eigensolve a DMRG sweep moves the window one site and grows the

@@ -96,13 +96,23 @@ struct WorkRange {
   }
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR>
-__global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::kThreads, 1)
-    gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                         double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store,
-                         int dp_tiles, double* __restrict__ partial_ws, int accumulate,
-                         const int* __restrict__ tile_order, const int* __restrict__ kb_ptr,
-                         const int* __restrict__ kb_list) {
+// A operand split along K over up to kMaxShards tensor maps (NEXT-5 gather-fused GEMM_A):
+// k-block kb is read from map (16 kb) / ksh at column 16 kb - shard * ksh.  The maps may
+// address peer GPUs' memory (NCCL symmetric-window pointers over NVLink).
+constexpr int kMaxShards = 8;
+struct ShardedA {
+  CUtensorMap map[kMaxShards];
+  int nsh;
+  int ksh;
+};
+
+template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR, bool SHARDED_A>
+__device__ __forceinline__ void gemm_dmma_tma_body(const CUtensorMap* tmA, const ShardedA* sa, const CUtensorMap* tmB,
+                                                   double* __restrict__ C, int64_t ldc, int M, int N, int K,
+                                                   int group_m, int vec_store, int dp_tiles,
+                                                   double* __restrict__ partial_ws, int accumulate,
+                                                   const int* __restrict__ tile_order, const int* __restrict__ kb_ptr,
+                                                   const int* __restrict__ kb_list) {
   using Cfg = TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>;
   constexpr int MI = WM / 8, NJ = WN / 8;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -128,8 +138,12 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
     // ---------------- producer warpgroup: one lane drives the TMA ring ----------------
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::kProducerRegs));
     if (warp == Cfg::kConsumerWarps && lane == 0) {
-      tma_prefetch_desc(&tmA);
-      tma_prefetch_desc(&tmB);
+      if constexpr (SHARDED_A) {
+        for (int q = 0; q < sa->nsh; ++q) tma_prefetch_desc(&sa->map[q]);
+      } else {
+        tma_prefetch_desc(tmA);
+      }
+      tma_prefetch_desc(tmB);
       int stage = 0;
       uint32_t phase = 0;
       WorkRange wr(tiles, dp_tiles, ktiles, tile_order, kb_ptr);
@@ -143,13 +157,18 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
           unsigned char* sA = smem + stage * Cfg::kStageBytes;
           unsigned char* sB = sA + Cfg::kTileABytes;
           mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-          tma_load_2d(sA, &tmA, &full[stage], kb * kGemmBK, mb * BM);
+          if constexpr (SHARDED_A) {
+            const int k0 = kb * kGemmBK, sh = k0 / sa->ksh;
+            tma_load_2d(sA, &sa->map[sh], &full[stage], k0 - sh * sa->ksh, mb * BM);
+          } else {
+            tma_load_2d(sA, tmA, &full[stage], kb * kGemmBK, mb * BM);
+          }
           if constexpr (B_KMAJOR) {
-            tma_load_2d(sB, &tmB, &full[stage], kb * kGemmBK, nb * BN);
+            tma_load_2d(sB, tmB, &full[stage], kb * kGemmBK, nb * BN);
           } else {
 #pragma unroll
             for (int q = 0; q < BN / 16; ++q)
-              tma_load_2d(sB + q * 2048, &tmB, &full[stage], nb * BN + q * 16, kb * kGemmBK);
+              tma_load_2d(sB + q * 2048, tmB, &full[stage], nb * BN + q * 16, kb * kGemmBK);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -261,6 +280,28 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
     }
     if (tile >= dp_tiles) first_seg = false;
   }
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR>
+__global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::kThreads, 1)
+    gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store,
+                         int dp_tiles, double* __restrict__ partial_ws, int accumulate,
+                         const int* __restrict__ tile_order, const int* __restrict__ kb_ptr,
+                         const int* __restrict__ kb_list) {
+  gemm_dmma_tma_body<BM, BN, WM, WN, STAGES, B_KMAJOR, false>(&tmA, nullptr, &tmB, C, ldc, M, N, K, group_m, vec_store,
+                                                              dp_tiles, partial_ws, accumulate, tile_order, kb_ptr,
+                                                              kb_list);
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR>
+__global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::kThreads, 1)
+    gemm_dmma_tma_sharded_kernel(const __grid_constant__ ShardedA sa, const __grid_constant__ CUtensorMap tmB,
+                                 double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store,
+                                 int dp_tiles, double* __restrict__ partial_ws, int accumulate) {
+  gemm_dmma_tma_body<BM, BN, WM, WN, STAGES, B_KMAJOR, true>(nullptr, &sa, &tmB, C, ldc, M, N, K, group_m, vec_store,
+                                                             dp_tiles, partial_ws, accumulate, nullptr, nullptr,
+                                                             nullptr);
 }
 
 // Stream-K fixup: every stream-K tile whose k-range was split across CTAs is the sum, in

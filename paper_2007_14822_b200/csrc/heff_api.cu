@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -65,6 +66,11 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // symmetric memory windows (NCCL >= 2.27; optional: the gather-fused path needs them)
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*CommWindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+  ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
 };
 
 static NcclApi g_nccl;
@@ -83,6 +89,11 @@ static int nccl_load() {
   LD(GetUniqueId) LD(CommInitRank) LD(CommDestroy) LD(CommAbort) LD(AllReduce) LD(AllGather) LD(CommGetAsyncError)
   LD(GetErrorString)
 #undef LD
+  g_nccl.MemAlloc = reinterpret_cast<decltype(g_nccl.MemAlloc)>(dlsym(h, "ncclMemAlloc"));
+  g_nccl.MemFree = reinterpret_cast<decltype(g_nccl.MemFree)>(dlsym(h, "ncclMemFree"));
+  g_nccl.CommWindowRegister = reinterpret_cast<decltype(g_nccl.CommWindowRegister)>(dlsym(h, "ncclCommWindowRegister"));
+  g_nccl.CommWindowDeregister =
+      reinterpret_cast<decltype(g_nccl.CommWindowDeregister)>(dlsym(h, "ncclCommWindowDeregister"));
   g_nccl.loaded = true;
   return HEFF_OK;
 }
@@ -177,12 +188,14 @@ struct SplitWs {  // stream-K partial-tile workspace, grown on demand
   size_t bytes = 0;
 };
 
-static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitWs* ws) {
+// sa != nullptr: the A operand is K-sharded over sa->nsh tensor maps (gemm_dmma_tma_sharded_kernel;
+// g.A is ignored, the TMA path is required).
+static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitWs* ws, const ShardedA* sa = nullptr) {
   if (g.M == 0 || g.N == 0) return HEFF_OK;
-  const bool use_tma = (path == 2) || (path == 0 && tma_ok(g));
+  const bool use_tma = sa != nullptr || (path == 2) || (path == 0 && tma_ok(g));
   if (path == 2 && !tma_ok(g)) return set_err(HEFF_EUNSUPPORTED, "TMA GEMM path needs 16-byte rows/alignment");
   if (use_tma) {
-    if (g.mapA_ptr != g.A || g.mapA_rows != g.M) {
+    if (!sa && (g.mapA_ptr != g.A || g.mapA_rows != g.M)) {
       CKR(make_map(&g.mapA, g.A, g.M, g.K, g.lda, kGemmBK, kBM));
       g.mapA_ptr = g.A;
       g.mapA_rows = g.M;
@@ -228,7 +241,12 @@ static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitW
     }
     const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(g.C) & 15) == 0) ? 1 : 0;
     double* wsp = ws ? ws->ptr : nullptr;
-    if (g.b_kmajor) {
+    if (sa) {
+      if (!g.b_kmajor) return set_err(HEFF_EUNSUPPORTED, "sharded-A GEMM: NT only");
+      auto k = gemm_dmma_tma_sharded_kernel<kBM, kBN, kWM, kWN, kStages, true>;
+      k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(*sa, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
+                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate);
+    } else if (g.b_kmajor) {
       auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, true>;
       k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
                                                           kGroupM, vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order,
@@ -275,6 +293,8 @@ static int init_device_once() {
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNT::kSmemBytes));
   CK(cudaFuncSetAttribute(gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNN::kSmemBytes));
+  CK(cudaFuncSetAttribute(gemm_dmma_tma_sharded_kernel<kBM, kBN, kWM, kWN, kStages, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNT::kSmemBytes));
   CK(cudaFuncSetAttribute(mpo_orderA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   CK(cudaFuncSetAttribute(mpo_orderB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -334,6 +354,19 @@ struct heff_plan_s {
   int64_t qn_n = 0;
   double* dense_in = nullptr;               // zero outside the sector
   double* dense_out = nullptr;
+  // gather-fused sharded Lanczos (NEXT-5): the Krylov basis lives in an NCCL symmetric window;
+  // GEMM_A reads every rank's shard of v_j through its NVLink (LSA) pointer, ordered by
+  // per-rank flags (signal after v_j is written, wait before the matvec reads it)
+  int fused_gather = 0;                     // option HEFF_OPT_FUSED_GATHER
+  int fused_active = 0;                     // the last lanczos_ground used the fused path
+  ncclWindow_t win = nullptr;
+  void* win_buf = nullptr;
+  size_t win_bytes = 0;
+  int win_cap = 0;
+  int64_t win_ldv = 0, win_flag_off = 0;    // flags at byte offset win_flag_off
+  std::vector<char*> peer_base;             // LSA pointers of every rank's window (host copy)
+  uint64_t** d_peer_flags = nullptr;        // device array [P] of peer flag arrays
+  uint64_t epoch = 0;
   // e2e staging
   double *stage_in = nullptr, *stage_out = nullptr;
   // Lanczos
@@ -454,6 +487,9 @@ extern "C" int heff_destroy(heff_plan p) {
   free_csr(p->csrA);
   free_csr(p->csrB);
   for (auto& e : p->prof_ev) cudaEventDestroy(e);
+  if (p->win && p->comm && g_nccl.CommWindowDeregister) g_nccl.CommWindowDeregister(p->comm, p->win);
+  if (p->win_buf && g_nccl.MemFree) g_nccl.MemFree(p->win_buf);
+  cudaFree(p->d_peer_flags);
   if (p->comm && g_nccl.loaded) g_nccl.CommDestroy(p->comm);
   delete p;
   return HEFF_OK;
@@ -502,6 +538,7 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
       memcpy(id.internal, dist->nccl_uid, 128);
       ncclResult_t nr = g_nccl.CommInitRank(&p->comm, dist->nranks, id, dist->rank);
       if (nr != ncclSuccess) return fail(set_err(HEFF_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(nr)));
+      if (const char* e = getenv("HEFF_FUSED_GATHER")) p->fused_gather = atoi(e) ? 1 : 0;
     }
   }
   // W copies
@@ -707,6 +744,11 @@ extern "C" int heff_set_option(heff_plan p, int option, int64_t value) {
     case HEFF_OPT_TOTAL_LAUNCHES:
       p->total_launches = value;
       return HEFF_OK;
+    case HEFF_OPT_FUSED_GATHER:
+      if (value && !(p->sharded && p->comm))
+        return set_err(HEFF_EUNSUPPORTED, "fused gather: communicating b'-sharded plans only");
+      p->fused_gather = value ? 1 : 0;
+      return HEFF_OK;
     default:
       return set_err(HEFF_EINVAL, "unknown option %d", option);
   }
@@ -721,6 +763,7 @@ extern "C" int heff_get_option(heff_plan p, int option, int64_t* value) {
     case HEFF_OPT_PROFILE: *value = p->profile; return HEFF_OK;
     case HEFF_OPT_TOTAL_LAUNCHES: *value = p->total_launches; return HEFF_OK;
     case HEFF_OPT_SPARSE_KBLOCKS: *value = p->sp_kblocks; return HEFF_OK;
+    case HEFF_OPT_FUSED_GATHER: *value = p->fused_gather + 2 * p->fused_active; return HEFF_OK;
     default: return set_err(HEFF_EINVAL, "unknown option %d", option);
   }
 }
@@ -789,13 +832,33 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
   return HEFF_OK;
 }
 
-static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl, int accumulate) {
+// Gather-fused GEMM_A (NEXT-5): psi given as P shards [rows][nb] (row pitch nb) at
+// shards[0..P) -- local buffers, or peer GPUs' buffers through NCCL symmetric-window
+// pointers -- read directly by the GEMM's TMA producer: no all-gather copy, no relayout.
+static int build_sharded_a(heff_plan_s* p, const double* const* shards, int P, ShardedA* sa) {
+  const heff_dims& d = p->dims;
+  const int64_t rows = d.mL * d.d1 * d.d2;
+  if (P < 1 || P > kMaxShards) return set_err(HEFF_EUNSUPPORTED, "sharded GEMM_A: 1..%d shards", kMaxShards);
+  if (p->nb % kGemmBK != 0 || (int64_t)P * p->nb != d.mR)
+    return set_err(HEFF_EUNSUPPORTED, "sharded GEMM_A: shard width nb = %lld must be a multiple of %d and P nb = mR",
+                   (long long)p->nb, kGemmBK);
+  for (int q = 0; q < P; ++q) {
+    if (reinterpret_cast<uintptr_t>(shards[q]) & 15) return set_err(HEFF_EINVAL, "sharded GEMM_A: 16-byte alignment");
+    CKR(make_map(&sa->map[q], shards[q], rows, p->nb, p->nb, kGemmBK, kBM));
+  }
+  sa->nsh = P;
+  sa->ksh = (int)p->nb;
+  return HEFF_OK;
+}
+
+static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl, int accumulate,
+                        const ShardedA* sa = nullptr) {
   const heff_dims& d = p->dims;
   const int dd = (int)(d.d1 * d.d2);
   const size_t mpo_smem = sizeof(double) * dd * d.kR * kMpoCols;
   CKR(prof_mark(p, 0, s));
   p->gA.A = psi;
-  CKR(launch_gemm(p->gA, p->gemm_path, s, nl, &p->splitws));
+  CKR(launch_gemm(p->gA, p->gemm_path, s, nl, &p->splitws, sa));
   CKR(prof_mark(p, 1, s));
   dim3 grid((unsigned)((p->nb + kMpoCols - 1) / kMpoCols), (unsigned)d.mL);
   mpo_orderB_kernel<<<grid, kMpoThreads, mpo_smem, s>>>(p->V1, p->V3, d.mL, p->nb, dd, (int)d.kR, (int)d.kL,
@@ -962,6 +1025,24 @@ extern "C" int heff_set_penalty(heff_plan p, const double* phis, int nphi, doubl
   return HEFF_OK;
 }
 
+extern "C" int heff_apply_blocked(heff_plan p, const double* psi_blocked, double* out, heff_stream stream) {
+  if (!p || !psi_blocked || !out) return set_err(HEFF_EINVAL, "heff_apply_blocked: null argument");
+  if (!p->sharded || p->is_complex || !p->terms.empty() || p->nphi > 0)
+    return set_err(HEFF_EUNSUPPORTED, "heff_apply_blocked: b'-sharded real plans only");
+  const heff_dims& d = p->dims;
+  const int64_t rows = d.mL * d.d1 * d.d2;
+  const int P = (int)(d.mR / std::max<int64_t>(1, p->nb));
+  std::vector<const double*> sh(P);
+  for (int q = 0; q < P; ++q) sh[q] = psi_blocked + (int64_t)q * rows * p->nb;
+  ShardedA sa;
+  CKR(build_sharded_a(p, sh.data(), P, &sa));
+  int nl = 0;
+  CKR(apply_orderB(p, nullptr, out, reinterpret_cast<cudaStream_t>(stream), &nl, 0, &sa));
+  p->last_launches = nl;
+  p->total_launches += nl;
+  return HEFF_OK;
+}
+
 extern "C" int heff_apply(heff_plan p, const double* psi, double* out, heff_stream stream) {
   if (!p) return set_err(HEFF_EINVAL, "heff_apply: null plan");
   return apply_impl(p, psi, out, reinterpret_cast<cudaStream_t>(stream));
@@ -1104,6 +1185,89 @@ extern "C" int heff_relayout_blocked(const double* src, double* dst, int64_t row
   return HEFF_OK;
 }
 
+// ---- gather-fused sharded Lanczos (NEXT-5): NCCL symmetric window + peer flags ----------
+__global__ void window_peer_pointers_kernel(ncclWindow_t w, int P, char** out) {
+  const int q = threadIdx.x;
+  if (q < P) out[q] = static_cast<char*>(ncclGetPeerPointer(w, 0, q));
+}
+
+// rank `rank` announces "my basis slot for step value-1 is written": flags[rank] = value in
+// every rank's window (system-scope release after a system fence)
+__global__ void peer_signal_kernel(uint64_t* const* peer_flags, int rank, int P, unsigned long long value) {
+  __threadfence_system();
+  const int q = threadIdx.x;
+  if (q < P) {
+    uint64_t* f = peer_flags[q] + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(value) : "memory");
+  }
+}
+
+// wait until every rank's flag in this rank's window reached `value` (acquire); bounded
+// spin (~20 s by %globaltimer) so a missing peer turns into a reported error, not a hang
+__global__ void peer_wait_kernel(const uint64_t* flags, int P, unsigned long long value, int* timed_out) {
+  const int q = threadIdx.x;
+  if (q < P) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
+      if (v >= value) break;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) {
+        atomicExch(timed_out, 1);
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  __syncthreads();
+}
+
+static int release_window(heff_plan_s* p) {
+  if (p->win && g_nccl.CommWindowDeregister) g_nccl.CommWindowDeregister(p->comm, p->win);
+  if (p->win_buf && g_nccl.MemFree) g_nccl.MemFree(p->win_buf);
+  p->win = nullptr;
+  p->win_buf = nullptr;
+  p->win_cap = 0;
+  return HEFF_OK;
+}
+
+// Collective over the plan's ranks (every rank calls lanczos_ground with the same max_iter).
+static int ensure_window(heff_plan_s* p, int cap, int64_t ldv, cudaStream_t s) {
+  if (p->win && p->win_cap >= cap && p->win_ldv == ldv) return HEFF_OK;
+  if (!g_nccl.MemAlloc || !g_nccl.CommWindowRegister)
+    return set_err(HEFF_EUNSUPPORTED, "libnccl has no symmetric-memory windows (ncclCommWindowRegister)");
+  release_window(p);
+  const int P = p->nranks;
+  const size_t slots = sizeof(double) * (size_t)ldv * cap;
+  const size_t flag_off = (slots + 255) / 256 * 256;
+  const size_t bytes = (flag_off + 256 + 4095) / 4096 * 4096;
+  CKN(g_nccl.MemAlloc(&p->win_buf, bytes));
+  CK(cudaMemsetAsync(p->win_buf, 0, bytes, s));
+  CK(cudaStreamSynchronize(s));
+  CKN(g_nccl.CommWindowRegister(p->comm, p->win_buf, bytes, &p->win, NCCL_WIN_COLL_SYMMETRIC));
+  char** d_ptrs = nullptr;
+  CK(cudaMalloc(&d_ptrs, sizeof(char*) * P));
+  window_peer_pointers_kernel<<<1, 32, 0, s>>>(p->win, P, d_ptrs);
+  p->peer_base.assign(P, nullptr);
+  CK(cudaMemcpyAsync(p->peer_base.data(), d_ptrs, sizeof(char*) * P, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(d_ptrs);
+  std::vector<uint64_t*> pf(P);
+  for (int q = 0; q < P; ++q) pf[q] = reinterpret_cast<uint64_t*>(p->peer_base[q] + flag_off);
+  if (!p->d_peer_flags) CK(cudaMalloc(&p->d_peer_flags, sizeof(uint64_t*) * kMaxShards));
+  CK(cudaMemcpyAsync(p->d_peer_flags, pf.data(), sizeof(uint64_t*) * P, cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  p->win_bytes = bytes;
+  p->win_cap = cap;
+  p->win_ldv = ldv;
+  p->win_flag_off = (int64_t)flag_off;
+  p->epoch = 0;
+  return HEFF_OK;
+}
+
 extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts* o, double* energy, int* iters_done,
                               double* resid_est, heff_stream stream) {
   if (!p || !psi || !o || !energy) return set_err(HEFF_EINVAL, "lanczos_ground: null argument");
@@ -1123,17 +1287,25 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     CK(cudaMalloc(&p->dense_out, sizeof(double) * n_dense));
     CK(cudaMemsetAsync(p->dense_in, 0, sizeof(double) * n_dense, s));
   }
+  // gather-fused sharded path: the basis lives in an NCCL symmetric window
+  bool fgather = false;
+  if (p->comm && p->fused_gather && !cplx && !compact && p->nranks <= kMaxShards && p->nb % kGemmBK == 0) {
+    const int rw = ensure_window(p, cap, ldv, s);
+    if (rw != HEFF_OK) return rw;
+    fgather = true;
+  }
+  p->fused_active = fgather ? 1 : 0;
   // (re)allocate the Krylov basis and scratch
   if (p->basis_cap < cap || p->ldv != ldv) {
     cudaFree(p->basis); cudaFree(p->partial); cudaFree(p->scal);
     p->basis = nullptr; p->partial = nullptr; p->scal = nullptr;
     p->basis_cap = 0;
-    CK(cudaMalloc(&p->basis, sizeof(double) * ldv * cap));
+    CK(cudaMalloc(&p->basis, sizeof(double) * ldv * (fgather ? 1 : cap)));
     p->ldp = reduce_grid(nr);
     const size_t pcols = std::max<size_t>((size_t)p->ldp, (size_t)8 * g_num_sms);  // also the fused step's grid
     CK(cudaMalloc(&p->partial, sizeof(double) * (size_t)(2 * cap + 2 * kDotQ + 1) * pcols));
-    CK(cudaMalloc(&p->scal, sizeof(double) * 8 * (size_t)(cap + 1)));
-    p->basis_cap = cap;
+    CK(cudaMalloc(&p->scal, sizeof(double) * 9 * (size_t)(cap + 1)));  // + fused-gather timeout flag
+    p->basis_cap = fgather ? 0 : cap;  // a later non-fused call reallocates the full basis
     p->ldv = ldv;
   }
   if (!p->work || p->work_len < ldv) {
@@ -1142,7 +1314,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     CK(cudaMalloc(&p->work, sizeof(double) * ldv));
     p->work_len = ldv;
   }
-  if (p->sharded && p->comm && !p->full) {
+  if (p->sharded && p->comm && !p->full && !fgather) {
     const heff_dims& d = p->dims;
     CK(cudaMalloc(&p->full, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
     if (p->nranks > 1) CK(cudaMalloc(&p->gather, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
@@ -1153,8 +1325,32 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   double* beta = alpha + (cap + 1);
   double* invb = beta + (cap + 1);
   double* ydev = invb + (cap + 1);
-  double* V = p->basis;
+  double* V = fgather ? static_cast<double*>(p->win_buf) : p->basis;
   double* w = p->work;
+  int* d_timeout = reinterpret_cast<int*>(ydev + (cap + 1));  // scal has room: 8 (cap+1) doubles
+  auto fused_signal = [&](uint64_t value) -> int {
+    peer_signal_kernel<<<1, 32, 0, s>>>(p->d_peer_flags, p->rank, p->nranks, (unsigned long long)value);
+    ++p->total_launches;
+    CK(cudaGetLastError());
+    return HEFF_OK;
+  };
+  // matvec of the fused path: wait for every rank's slot, GEMM_A straight from their windows
+  auto fused_matvec = [&](int j) -> int {
+    const uint64_t* myflags = reinterpret_cast<const uint64_t*>(static_cast<char*>(p->win_buf) + p->win_flag_off);
+    peer_wait_kernel<<<1, 32, 0, s>>>(myflags, p->nranks, (unsigned long long)(p->epoch + j), d_timeout);
+    ++p->total_launches;
+    std::vector<const double*> sh(p->nranks);
+    for (int q = 0; q < p->nranks; ++q)  // own shard through the local mapping, peers through LSA pointers
+      sh[q] = reinterpret_cast<const double*>(q == p->rank ? static_cast<char*>(p->win_buf) : p->peer_base[q]) +
+              (int64_t)(j - 1) * ldv;
+    ShardedA sa;
+    CKR(build_sharded_a(p, sh.data(), p->nranks, &sa));
+    int nl = 0;
+    CKR(apply_orderB(p, nullptr, w, s, &nl, 0, &sa));
+    p->total_launches += nl;
+    return HEFF_OK;
+  };
+  if (fgather) CK(cudaMemsetAsync(d_timeout, 0, sizeof(int), s));
 
   // v1 = x0 / ||x0||  (copied into the aligned basis first)
   if (compact) {
@@ -1172,6 +1368,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   scale_kernel<<<ew_grid(nr), 256, 0, s>>>(V, invb + cap, V, nr);
   ++p->total_launches;
   CK(cudaGetLastError());
+  if (fgather) CKR(fused_signal(p->epoch + 1));
 
   std::vector<double> ha(cap), hb(cap);
   double theta = 0.0, ylast = 0.0, hnorm = 0.0;
@@ -1196,6 +1393,8 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       gather_kernel<<<ew_grid(n), 256, 0, s>>>(p->dense_out, p->qn_idx, n, w);
       p->total_launches += 2;
       CK(cudaGetLastError());
+    } else if (fgather) {
+      CKR(fused_matvec(j));
     } else {
       CKR(matvec_local(p, vj, w, s));
     }
@@ -1230,6 +1429,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     if (j < cap) {
       scale_kernel<<<ew_grid(nr), 256, 0, s>>>(w, invb + (j - 1), V + (int64_t)j * ldv, nr);
       ++p->total_launches;
+      if (fgather) CKR(fused_signal(p->epoch + j + 1));
     }
     CK(cudaGetLastError());
     return HEFF_OK;
@@ -1288,6 +1488,12 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   ++p->total_launches;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
+  if (fgather) {
+    p->epoch += (uint64_t)cap + 1;
+    int to = 0;
+    CK(cudaMemcpy(&to, d_timeout, sizeof(int), cudaMemcpyDeviceToHost));
+    if (to) return set_err(HEFF_ENCCL, "lanczos_ground: a peer never published its Krylov vector (20 s timeout)");
+  }
   *energy = theta;
   if (iters_done) *iters_done = j_done;
   if (resid_est) *resid_est = hb[j_done - 1] * std::fabs(y[j_done - 1]);

@@ -19,6 +19,7 @@ LIB_PATH = _PKG / "libheff.so"
 HEFF_OK, HEFF_EINVAL, HEFF_ENOMEM, HEFF_ECUDA, HEFF_ENCCL, HEFF_EZERO, HEFF_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 HEFF_ENOCONV = -7
 OPT_GEMM_PATH, OPT_LAST_KERNEL_COUNT, OPT_MPO_NNZ, OPT_PROFILE, OPT_TOTAL_LAUNCHES, OPT_SPARSE_KBLOCKS = 1, 2, 3, 4, 5, 6
+OPT_FUSED_GATHER = 7
 
 
 class HeffError(RuntimeError):
@@ -71,6 +72,7 @@ def lib() -> ctypes.CDLL:
         L.heff_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(_Dims), vp, vp, vp, vp, ctypes.POINTER(_Dist), vp]
         L.heff_apply.argtypes = [vp, vp, vp, vp]
         L.heff_apply_host.argtypes = [vp, vp, vp, vp]
+        L.heff_apply_blocked.argtypes = [vp, vp, vp, vp]
         L.lanczos_ground.argtypes = [vp, vp, ctypes.POINTER(_LanczosOpts), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ip), ctypes.POINTER(ctypes.c_double), vp]
         L.heff_destroy.argtypes = [vp]
@@ -95,7 +97,7 @@ def lib() -> ctypes.CDLL:
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ip), vp]
         L.heff_truncate_spectrum.argtypes = [vp, i64, ctypes.POINTER(_Trunc), ctypes.POINTER(i64),
                                              ctypes.POINTER(ctypes.c_double)]
-        for f in ("heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
+        for f in ("heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
                   "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z"):
@@ -108,7 +110,7 @@ EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "h
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
             "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z",
-            "heff_svd_split", "heff_truncate_spectrum")
+            "heff_svd_split", "heff_truncate_spectrum", "heff_apply_blocked")
 
 
 def _check(rc: int):
@@ -359,6 +361,16 @@ class Heff:
         if psi.numel() != n_in or out.numel() != n_in // self.dims["mR"] * self.nb:
             raise ValueError(f"psi must have {self.psi_shape} elements and out {self.out_shape}")
         _check(lib().heff_apply(self._h, psi.data_ptr(), out.data_ptr(), _stream(stream)))
+        return out
+
+    def apply_blocked(self, psi_blocked: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Gather-fused matvec of a b'-sharded plan (heff_apply_blocked): psi_blocked is the
+        blocked all-gather layout [P, mL*d1*d2, nb]; returns this plan's out shard."""
+        _dev(psi_blocked, "psi_blocked")
+        if out is None:
+            out = torch.empty(self.out_shape, dtype=torch.float64, device=psi_blocked.device)
+        _dev(out, "out")
+        _check(lib().heff_apply_blocked(self._h, psi_blocked.data_ptr(), out.data_ptr(), _stream(stream)))
         return out
 
     def apply_host(self, psi_host: torch.Tensor, out_host: torch.Tensor, stream=None) -> torch.Tensor:
