@@ -2128,6 +2128,12 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   // ||Psi||_F^2 (deterministic two-pass) and the packed working copy
   svd_sumsq_partial_kernel<<<red_blocks, 256, 0, s>>>(psi, M * N, d_red);
   svd_sum_kernel<<<1, 32, 0, s>>>(d_red, red_blocks, d_red + red_blocks);
+  // optional phase timing (HEFF_SVD_TIMING=1: LQ, Jacobi sweeps, extraction -> stderr)
+  const bool timing = getenv("HEFF_SVD_TIMING") != nullptr;
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (timing)
+    for (auto& e : tev) CK(cudaEventCreate(&e));
+  if (timing) CK(cudaEventRecord(tev[0], s));
   if (precond) {
     // P = Pi Psi (moving right) or Pi Psi^T (moving left), R x colsP, rows sorted by
     // descending norm (static row pivoting of the LQ); P <- L by blocked Householder
@@ -2198,6 +2204,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   const double tol = std::max(4.0 * eps * std::sqrt((double)R), 8.0 * eps);
   const double negl = kSvdNegligible * kSvdNegligible * fro2;
 
+  if (timing) CK(cudaEventRecord(tev[1], s));
   // Jacobi sweeps until a sweep rotates no pair
   int sweeps = 0;
   bool converged = false;
@@ -2241,6 +2248,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   if (sweeps_out) *sweeps_out = sweeps;
   if (!converged) return set_err(HEFF_ENOCONV, "heff_svd_split: Jacobi did not converge in %d sweeps", kSvdMaxSweeps);
 
+  if (timing) CK(cudaEventRecord(tev[2], s));
   // singular values = column norms; sort (descending, stable) and truncate on the host
   svd_colnorm_kernel<<<(unsigned)nblk, 256, 0, s>>>(Xb, R, ncols, d_norm);
   CK(cudaGetLastError());
@@ -2280,6 +2288,17 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   }
   CK(cudaStreamSynchronize(s));
   if (r != HEFF_OK) return r;
+  if (timing) {
+    CK(cudaEventRecord(tev[3], s));
+    CK(cudaEventSynchronize(tev[3]));
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, tev[0], tev[1]);
+    cudaEventElapsedTime(&b, tev[1], tev[2]);
+    cudaEventElapsedTime(&c, tev[2], tev[3]);
+    fprintf(stderr, "heff_svd_split %lldx%lld dir %d: precondition %.2f ms, %d sweeps %.2f ms (%.2f ms/sweep), "
+            "extract %.2f ms\n", (long long)M, (long long)N, dir, a, sweeps, b, b / std::max(1, sweeps), c);
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
   *n_kept = n;
   *trunc_err = err;
   return HEFF_OK;
