@@ -2209,7 +2209,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   int sweeps = 0;
   bool converged = false;
   const char* it_env = getenv("HEFF_SVD_INNER_THRESH");
-  const double inner_thresh = it_env ? atof(it_env) : 1e-2;
+  const double inner_thresh = it_env ? atof(it_env) : 0.0;  // default: one inner sweep throughout
   int inner = inner_thresh > 1.0 ? kSvdMaxInnerSweeps : 1;
   const bool sort_cols = getenv("HEFF_SVD_NO_SORT") == nullptr;
   std::vector<double> nrm(nblk * kSvdB);

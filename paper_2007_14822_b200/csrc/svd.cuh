@@ -36,11 +36,13 @@ constexpr int kSvdB = 16;              // columns per block
 constexpr int kSvdPair = 2 * kSvdB;    // columns per pair
 constexpr int kSvdGramThreads = 256;
 constexpr int kSvdRotThreads = 128;
-// Inner sweeps per pair step (host policy, heff_svd_split): far from convergence one inner
-// sweep is as good as a full diagonalisation of the 32 x 32 Gram (prototype: 12 / 25 outer
-// sweeps for Gaussian / graded inputs with 1, 2, 3 or 30 inner sweeps) and 8x shorter on
-// the critical path; near convergence (max relative off-diagonal of the previous sweep
-// < 1e-2) the full diagonalisation restores quadratic convergence.
+// Inner sweeps per pair step (host policy, heff_svd_split): one inner sweep of the 32 x 32
+// Gram is as good as its full diagonalisation for the outer convergence (prototype: 12 / 25
+// outer sweeps for Gaussian / graded inputs with 1, 2, 3 or 30 inner sweeps; on the GPU with
+// the LQ preconditioner: C2 / C3 DMRG states 18.0 / 28.8 ms with one inner sweep vs 20.8 /
+// 36.6 ms switching to full diagonalisation below an off-diagonal of 1e-2) and much shorter
+// on the critical path.  HEFF_SVD_INNER_THRESH=x switches to up to kSvdMaxInnerSweeps inner
+// sweeps once the previous outer sweep's max off-diagonal is below x.
 constexpr int kSvdMaxInnerSweeps = 12;
 
 // ---------------------------------------------------------------- packing
@@ -202,44 +204,106 @@ __global__ void __launch_bounds__(kSvdGramThreads, 2) svd_gram_kernel(const doub
 // 2x2 values), and Q <- Q J by columns.  Output: Qg[p] (row-major 32x32), flag[p].
 constexpr int kSvdEigThreads = 256;
 
+// FP64 rsqrt / reciprocal: MUFU approximation + two Newton steps (full precision for the
+// normal, positive arguments used here; any rounding in t only leaves a slightly larger
+// residual off-diagonal -- the rotation itself stays orthogonal because c, s come from t)
+__device__ __forceinline__ double svd_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double svd_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-x, y, 2.0);
+  y = y * fma(-x, y, 2.0);
+  return y;
+}
+
+struct SvdRot {
+  double c, s, na, nb;  // rotation and the exact rotated diagonal of the pair
+  int on;
+};
+
+// Jacobi rotation of the 2x2 block [[app, apq], [apq, aqq]]:
+// t = sign(th) om / (|th| + sqrt(th^2 + om^2)), th = aqq - app, om = 2 apq
+__device__ __forceinline__ SvdRot svd_make_rot(double app, double aqq, double apq, bool active, double tol) {
+  SvdRot r{1.0, 0.0, app, aqq, 0};
+  if (active && fabs(apq) > tol * sqrt(app * aqq)) {
+    const double th = aqq - app, om = 2.0 * apq;
+    const double h2 = fma(th, th, om * om);
+    const double den = fabs(th) + h2 * svd_rsqrt(h2);
+    const double tt = (th >= 0.0 ? om : -om) * svd_rcp(den);
+    const double c = svd_rsqrt(fma(tt, tt, 1.0));
+    r.c = c;
+    r.s = c * tt;
+    r.na = app - tt * apq;
+    r.nb = aqq + tt * apq;
+    r.on = 1;
+  }
+  return r;
+}
+
+// new 2x2 block (rows of pair k, columns of pair kk) of J^T G J from the old one
+__device__ __forceinline__ void svd_rot_block(double& x00, double& x01, double& x10, double& x11, const SvdRot& rk,
+                                              const SvdRot& rkk) {
+  if (rkk.on) {  // columns: [x.0 x.1] <- [x.0 x.1] [[c, s], [-s, c]]
+    const double y00 = rkk.c * x00 - rkk.s * x01, y01 = rkk.s * x00 + rkk.c * x01;
+    const double y10 = rkk.c * x10 - rkk.s * x11, y11 = rkk.s * x10 + rkk.c * x11;
+    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+  }
+  if (rk.on) {   // rows: [x0. ; x1.] <- [[c, -s], [s, c]] [x0. ; x1.]
+    const double y00 = rk.c * x00 - rk.s * x10, y10 = rk.s * x00 + rk.c * x10;
+    const double y01 = rk.c * x01 - rk.s * x11, y11 = rk.s * x01 + rk.c * x11;
+    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+  }
+}
+
 __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const double* __restrict__ Gp, int nslots,
                                                                      int64_t C, int gram_grid,
                                                                      double tol, double negl, int inner_sweeps,
                                                                      double* __restrict__ Qg, int* __restrict__ flag,
                                                                      unsigned long long* __restrict__ stat_maxoff,
                                                                      int* __restrict__ stat_nrot) {
-  __shared__ double G[kSvdPair][kSvdPair + 1];
+  __shared__ double Gs[2][kSvdPair][kSvdPair + 1];   // ping-pong: round rr reads Gs[rr&1], writes Gs[~]
   __shared__ double Q[kSvdPair][kSvdPair + 1];
-  __shared__ double s_c[16], s_s[16], s_na[16], s_nb[16];
-  __shared__ int s_do[16], s_neg[kSvdPair];
-  __shared__ unsigned char s_pa[31][16], s_pb[31][16];
-  __shared__ int s_any;
+  __shared__ SvdRot s_rot[2][16];
+  __shared__ int s_neg[kSvdPair];
+  __shared__ unsigned char s_pa[31][16], s_pb[31][16], s_kof[31][kSvdPair], s_hi[31][kSvdPair];
+  __shared__ int s_any[kSvdMaxInnerSweeps];          // did inner sweep i rotate anything
   __shared__ double s_off[kSvdEigThreads / 32];
   const int p = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double* gsrc = Gp + (int64_t)p * nslots * (kSvdPair * kSvdPair);
-  const int64_t T = (int64_t)gridDim.x * C;
+  const int64_t T = (int64_t)gridDim.x * C;  // gridDim.x = npairs
   const int nsum = svd_sk_owner((int64_t)p * C + C - 1, T, gram_grid) - svd_sk_owner((int64_t)p * C, T, gram_grid) + 1;
   for (int e = tid; e < kSvdPair * kSvdPair; e += blockDim.x) {
     double v = 0.0;
     for (int sp = 0; sp < nsum; ++sp) v += gsrc[(int64_t)sp * (kSvdPair * kSvdPair) + e];
     const int r = e >> 5, c = e & 31;
-    G[r][c] = v;
+    Gs[0][r][c] = v;
     Q[r][c] = (r == c) ? 1.0 : 0.0;
   }
   for (int e = tid; e < 31 * 16; e += blockDim.x) {  // round-robin (circle method) over 32 columns
     const int rr = e >> 4, k = e & 15;
     auto idx = [&](int i) { return i == 0 ? 0 : ((i - 1 + rr) % 31) + 1; };
-    s_pa[rr][k] = (unsigned char)idx(k);
-    s_pb[rr][k] = (unsigned char)idx(31 - k);
+    const int a = idx(k), b = idx(31 - k);
+    s_pa[rr][k] = (unsigned char)a;
+    s_pb[rr][k] = (unsigned char)b;
+    s_kof[rr][a] = s_kof[rr][b] = (unsigned char)k;   // which pair of round rr holds column a / b
+    s_hi[rr][a] = 0;
+    s_hi[rr][b] = 1;
   }
   __syncthreads();
-  if (tid < kSvdPair) s_neg[tid] = !(G[tid][tid] > negl);
+  if (tid < kSvdPair) s_neg[tid] = !(Gs[0][tid][tid] > negl);
   __syncthreads();
   double off = 0.0;
   for (int e = tid; e < kSvdPair * kSvdPair; e += blockDim.x) {
     const int r = e >> 5, c = e & 31;
-    if (r < c && !s_neg[r] && !s_neg[c]) off = fmax(off, fabs(G[r][c]) / sqrt(G[r][r] * G[c][c]));
+    if (r < c && !s_neg[r] && !s_neg[c]) off = fmax(off, fabs(Gs[0][r][c]) / sqrt(Gs[0][r][r] * Gs[0][c][c]));
   }
   for (int o = 16; o > 0; o >>= 1) off = fmax(off, __shfl_xor_sync(0xffffffffu, off, o));
   if (lane == 0) s_off[warp] = off;
@@ -254,70 +318,66 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
   }
   if (!rotate) return;
 
-  for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
-    if (tid == 0) s_any = 0;
-    __syncthreads();
-    for (int rr = 0; rr < 31; ++rr) {
-      if (tid < 16) {
-        const int a = s_pa[rr][tid], b = s_pb[rr][tid];
-        const double app = G[a][a], aqq = G[b][b], apq = G[a][b];
-        const bool d = !s_neg[a] && !s_neg[b] && fabs(apq) > tol * sqrt(app * aqq);
-        s_do[tid] = d;
-        if (d) {
-          // t = sign(z) / (|z| + sqrt(1 + z^2)), z = (aqq - app) / (2 apq), without forming z
-          const double th = aqq - app, om = 2.0 * apq;
-          const double tt = (th >= 0.0 ? om : -om) / (fabs(th) + sqrt(fma(th, th, om * om)));
-          const double c = rsqrt(fma(tt, tt, 1.0));
-          s_c[tid] = c;
-          s_s[tid] = c * tt;
-          s_na[tid] = app - tt * apq;   // exact rotated diagonal
-          s_nb[tid] = aqq + tt * apq;
-          s_any = 1;
-        }
+  // Cyclic two-sided Jacobi, one barrier per round: in round rr every thread writes its
+  // 2x2 block of the rotated G into the other buffer and updates Q, while threads 0..15
+  // already compute round rr+1's rotations from the OLD G and round rr's rotations.
+  if (tid < 16) {
+    const int a = s_pa[0][tid], b = s_pb[0][tid];
+    s_rot[0][tid] = svd_make_rot(Gs[0][a][a], Gs[0][b][b], Gs[0][a][b], !s_neg[a] && !s_neg[b], tol);
+  }
+  if (tid < kSvdMaxInnerSweeps) s_any[tid] = 0;
+  __syncthreads();
+  const int total_rounds = 31 * min(inner_sweeps, kSvdMaxInnerSweeps);
+  for (int it = 0; it < total_rounds; ++it) {
+    const int rr = it % 31, cur = it & 1, nxt = cur ^ 1;
+    const int sweep = it / 31;
+    double(*Go)[kSvdPair + 1] = Gs[cur];
+    double(*Gn)[kSvdPair + 1] = Gs[nxt];
+    {  // this thread's 2x2 block (pair k rows, pair kk columns)
+      const int k = tid >> 4, kk = tid & 15;
+      const int a = s_pa[rr][k], b = s_pb[rr][k], a2 = s_pa[rr][kk], b2 = s_pb[rr][kk];
+      const SvdRot rk = s_rot[cur][k], rkk = s_rot[cur][kk];
+      if (k == kk) {
+        Gn[a][a] = rk.na;
+        Gn[b][b] = rk.nb;
+        Gn[a][b] = Gn[b][a] = rk.on ? 0.0 : Go[a][b];
+      } else {
+        double x00 = Go[a][a2], x01 = Go[a][b2], x10 = Go[b][a2], x11 = Go[b][b2];
+        svd_rot_block(x00, x01, x10, x11, rk, rkk);
+        Gn[a][a2] = x00; Gn[a][b2] = x01; Gn[b][a2] = x10; Gn[b][b2] = x11;
       }
-      __syncthreads();
-      {  // G <- J^T G J: one 2x2 block (pair k rows, pair kk columns) per thread
-        const int k = tid >> 4, kk = tid & 15;
-        const bool dk = s_do[k], dkk = s_do[kk];
-        if (dk || dkk) {
-          const int a = s_pa[rr][k], b = s_pb[rr][k];
-          const int a2 = s_pa[rr][kk], b2 = s_pb[rr][kk];
-          if (k == kk) {
-            G[a][a] = s_na[k];
-            G[b][b] = s_nb[k];
-            G[a][b] = G[b][a] = 0.0;
-          } else {
-            double x00 = G[a][a2], x01 = G[a][b2], x10 = G[b][a2], x11 = G[b][b2];
-            if (dkk) {  // columns: [x.0 x.1] <- [x.0 x.1] [[c, s], [-s, c]]
-              const double c = s_c[kk], s = s_s[kk];
-              const double y00 = c * x00 - s * x01, y01 = s * x00 + c * x01;
-              const double y10 = c * x10 - s * x11, y11 = s * x10 + c * x11;
-              x00 = y00; x01 = y01; x10 = y10; x11 = y11;
-            }
-            if (dk) {   // rows: [x0. ; x1.] <- [[c, -s], [s, c]] [x0. ; x1.]
-              const double c = s_c[k], s = s_s[k];
-              const double y00 = c * x00 - s * x10, y10 = s * x00 + c * x10;
-              const double y01 = c * x01 - s * x11, y11 = s * x01 + c * x11;
-              x00 = y00; x01 = y01; x10 = y10; x11 = y11;
-            }
-            G[a][a2] = x00; G[a][b2] = x01; G[b][a2] = x10; G[b][b2] = x11;
-          }
-        }
-      }
-      for (int task = tid; task < 32 * 16; task += blockDim.x) {  // Q <- Q J
-        const int k = task & 15, r = task >> 4;
-        if (!s_do[k]) continue;
-        const int a = s_pa[rr][k], b = s_pb[rr][k];
-        const double c = s_c[k], s = s_s[k];
-        const double qa = Q[r][a], qb = Q[r][b];
-        Q[r][a] = c * qa - s * qb;
-        Q[r][b] = s * qa + c * qb;
-      }
-      __syncthreads();
+      if (tid < 16 && s_rot[cur][tid].on) s_any[sweep] = 1;
     }
-    const int any = s_any;
-    __syncthreads();  // every thread has read s_any before thread 0 resets it
-    if (!any) break;
+    for (int task = tid; task < 32 * 16; task += blockDim.x) {  // Q <- Q J (columns, in place)
+      const int k = task & 15, r = task >> 4;
+      const SvdRot rk = s_rot[cur][k];
+      if (!rk.on) continue;
+      const int a = s_pa[rr][k], b = s_pb[rr][k];
+      const double qa = Q[r][a], qb = Q[r][b];
+      Q[r][a] = rk.c * qa - rk.s * qb;
+      Q[r][b] = rk.s * qa + rk.c * qb;
+    }
+    if (tid < 16 && it + 1 < total_rounds) {  // round rr+1's rotation from the rotated entries
+      const int r1 = (rr + 1) % 31;
+      const int a = s_pa[r1][tid], b = s_pb[r1][tid];
+      auto rotated = [&](int x, int y) {  // (J^T G J)[x][y] of round rr from the old G
+        const int kx = s_kof[rr][x], ky = s_kof[rr][y];
+        const SvdRot rx = s_rot[cur][kx], ry = s_rot[cur][ky];
+        if (kx == ky) {
+          if (x == y) return s_hi[rr][x] ? rx.nb : rx.na;
+          return rx.on ? 0.0 : Go[x][y];
+        }
+        const int ax = s_pa[rr][kx], bx = s_pb[rr][kx], ay = s_pa[rr][ky], by = s_pb[rr][ky];
+        double x00 = Go[ax][ay], x01 = Go[ax][by], x10 = Go[bx][ay], x11 = Go[bx][by];
+        svd_rot_block(x00, x01, x10, x11, rx, ry);
+        const int hx = s_hi[rr][x], hy = s_hi[rr][y];
+        return hx ? (hy ? x11 : x10) : (hy ? x01 : x00);
+      };
+      const double app = rotated(a, a), aqq = rotated(b, b), apq = rotated(a, b);
+      s_rot[nxt][tid] = svd_make_rot(app, aqq, apq, !s_neg[a] && !s_neg[b], tol);
+    }
+    __syncthreads();
+    if (rr == 30 && !s_any[sweep]) break;  // end of an inner sweep that rotated nothing
   }
   double* q = Qg + (int64_t)p * (kSvdPair * kSvdPair);
   for (int e = tid; e < kSvdPair * kSvdPair; e += blockDim.x) q[e] = Q[e >> 5][e & 31];
