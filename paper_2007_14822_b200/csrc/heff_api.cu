@@ -367,8 +367,10 @@ struct heff_plan_s {
   std::vector<char*> peer_base;             // LSA pointers of every rank's window (host copy)
   uint64_t** d_peer_flags = nullptr;        // device array [P] of peer flag arrays
   uint64_t epoch = 0;
-  // e2e staging
+  // e2e staging; the overlapped host path's copy stream and chunk events
   double *stage_in = nullptr, *stage_out = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t e2e_ev[17] = {};                // 2 kE2eChunks + 1
   // Lanczos
   double* basis = nullptr;                  // [cap][ldv]
   int basis_cap = 0;
@@ -487,6 +489,9 @@ extern "C" int heff_destroy(heff_plan p) {
   free_csr(p->csrA);
   free_csr(p->csrB);
   for (auto& e : p->prof_ev) cudaEventDestroy(e);
+  for (auto& e : p->e2e_ev)
+    if (e) cudaEventDestroy(e);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->win && p->comm && g_nccl.CommWindowDeregister) g_nccl.CommWindowDeregister(p->comm, p->win);
   if (p->win_buf && g_nccl.MemFree) g_nccl.MemFree(p->win_buf);
   cudaFree(p->d_peer_flags);
@@ -1048,6 +1053,61 @@ extern "C" int heff_apply(heff_plan p, const double* psi, double* out, heff_stre
   return apply_impl(p, psi, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// End-to-end order-A matvec with the transfers overlapped: psi arrives in column chunks
+// (s1 s2 b) on a copy stream, GEMM1 runs per chunk as each lands; GEMM4 runs in row chunks
+// (a' s1' s2') and each finished block of out goes back while the next is computed.  Only
+// the first H2D chunk and the last D2H chunk are exposed.
+static constexpr int kE2eChunks = 8;
+static int apply_host_pipelined(heff_plan_s* p, const double* psi_host, double* out_host, cudaStream_t s) {
+  const heff_dims& d = p->dims;
+  const int64_t ncol = d.d1 * d.d2 * d.mR, nrow4 = d.mL * d.d1 * d.d2;
+  if (!p->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : p->e2e_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t c = p->copy_stream;
+  CK(cudaEventRecord(p->e2e_ev[2 * kE2eChunks], s));   // the copy stream starts after prior work on s
+  CK(cudaStreamWaitEvent(c, p->e2e_ev[2 * kE2eChunks], 0));
+  int nl = 0;
+  for (int k = 0; k < kE2eChunks; ++k) {
+    const int64_t c0 = ncol * k / kE2eChunks / 2 * 2, c1 = (k + 1 == kE2eChunks) ? ncol : ncol * (k + 1) / kE2eChunks / 2 * 2;
+    CK(cudaMemcpy2DAsync(p->stage_in + c0, sizeof(double) * ncol, psi_host + c0, sizeof(double) * ncol,
+                         sizeof(double) * (c1 - c0), d.mL, cudaMemcpyHostToDevice, c));
+    CK(cudaEventRecord(p->e2e_ev[k], c));
+    CK(cudaStreamWaitEvent(s, p->e2e_ev[k], 0));
+    p->g1.M = d.mL * d.kL;
+    p->g1.N = c1 - c0;
+    p->g1.A = p->L;
+    p->g1.B = p->stage_in + c0;
+    p->g1.C = p->T1 + c0;
+    CKR(launch_gemm(p->g1, p->gemm_path, s, &nl, &p->splitws));
+  }
+  p->g1.N = ncol;
+  const int64_t nin = d.kL * d.d1 * d.d2, nout = d.d1 * d.d2 * d.kR;
+  dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)d.mL);
+  mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(
+      p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr, p->csrA.d_col, p->csrA.d_val, p->mpo_live, 1, 0, 0);
+  CK(cudaGetLastError());
+  ++nl;
+  for (int k = 0; k < kE2eChunks; ++k) {
+    const int64_t r0 = nrow4 * k / kE2eChunks, r1 = nrow4 * (k + 1) / kE2eChunks;
+    p->g4.M = r1 - r0;
+    p->g4.A = p->T3 + r0 * d.kR * d.mR;
+    p->g4.C = p->stage_out + r0 * d.mR;
+    p->g4.accumulate = 0;
+    CKR(launch_gemm(p->g4, p->gemm_path, s, &nl, &p->splitws));
+    CK(cudaEventRecord(p->e2e_ev[kE2eChunks + k], s));
+    CK(cudaStreamWaitEvent(c, p->e2e_ev[kE2eChunks + k], 0));
+    CK(cudaMemcpyAsync(out_host + r0 * d.mR, p->stage_out + r0 * d.mR, sizeof(double) * (r1 - r0) * d.mR,
+                       cudaMemcpyDeviceToHost, c));
+  }
+  p->last_launches = nl;
+  p->total_launches += nl;
+  CK(cudaStreamSynchronize(c));
+  CK(cudaStreamSynchronize(s));
+  return HEFF_OK;
+}
+
 extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_host, heff_stream stream) {
   if (!p || !psi_host || !out_host) return set_err(HEFF_EINVAL, "heff_apply_host: null argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1059,6 +1119,10 @@ extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_
     CK(cudaMalloc(&p->stage_in, sizeof(double) * n_in));
     CK(cudaMalloc(&p->stage_out, sizeof(double) * n_out));
   }
+  const bool pipelined = !p->is_complex && !p->sharded && p->terms.empty() && p->nphi == 0 && p->sp1 == nullptr &&
+                         p->sp4 == nullptr && p->chunk_rows == d.mL && d.mL * d.d1 * d.d2 >= 8 * kE2eChunks &&
+                         getenv("HEFF_NO_E2E_PIPELINE") == nullptr;
+  if (pipelined) return apply_host_pipelined(p, psi_host, out_host, s);
   CK(cudaMemcpyAsync(p->stage_in, psi_host, sizeof(double) * n_in, cudaMemcpyHostToDevice, s));
   CKR(apply_impl(p, p->stage_in, p->stage_out, s));
   CK(cudaMemcpyAsync(out_host, p->stage_out, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));

@@ -138,16 +138,29 @@ def test_linearity_and_hermiticity_gpu(dev):
     assert abs(lhs - rhs) <= 1e-12 * torch.linalg.norm(phi) * torch.linalg.norm(Hpsi)
 
 
-def test_apply_host_e2e(dev, orc):
+@pytest.mark.parametrize("case", ["c2", "ragged_even", "tails"])
+def test_apply_host_e2e(dev, orc, case, monkeypatch):
+    """heff_apply_host: the overlapped path (column-chunked H2D + GEMM1, row-chunked GEMM4 +
+    D2H) and the plain copy-compute-copy path, pinned and pageable host buffers."""
     from paper_2007_14822_b200 import Heff
-    x = C.make("c2")
+    x = CASES[case]()
     L, W1, W2, R, psi = x.numpy()
     ref = orc.heff_apply(L, W1, W2, R, psi)
     xd = x.to(dev)
-    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
-        out = torch.empty(x.psi.shape, dtype=torch.float64).pin_memory()
-        h.apply_host(x.psi.contiguous(), out)
-    assert rel(out.numpy(), ref) <= MATVEC_TOL
+    outs = []
+    for pipelined in (True, False):
+        if not pipelined:
+            monkeypatch.setenv("HEFF_NO_E2E_PIPELINE", "1")
+        with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+            for pin in (True, False):
+                out = torch.empty(x.psi.shape, dtype=torch.float64)
+                if pin:
+                    out = out.pin_memory()
+                h.apply_host(x.psi.contiguous().pin_memory() if pin else x.psi.contiguous(), out)
+                assert rel(out.numpy(), ref) <= MATVEC_TOL, (pipelined, pin)
+                outs.append(out.numpy().copy())
+    # chunked GEMM4 schedules its stream-K splits per chunk: same values up to summation order
+    assert rel(outs[0], outs[2]) <= 1e-14
 
 
 # ------------------------------------------------------------------------ Lanczos
