@@ -38,3 +38,43 @@ def test_dmrg_cylinder_truncated_is_variational(dev):
     e0 = spla.eigsh(ed_ref.heisenberg(12, ed_ref.cylinder_bonds(2)), k=1, which="SA", tol=1e-14)[0][0]
     assert e >= e0 - 1e-10
     assert e - e0 < 5e-2 * abs(e0)
+
+
+def _mps_energy_and_norm(As, W):
+    """<psi|H|psi> and <psi|psi> of an MPS (site tensors [a, s, b]) with the chain MPO W
+    (boundary vectors of heffgen.mpo) by transfer-matrix contraction in numpy -- an evaluation
+    independent of libheff's Lanczos, environments and split."""
+    k = W.shape[0]
+    l, r = np.zeros(k), np.zeros(k)
+    l[k - 1] = 1.0   # start channel (reading R4)
+    r[0] = 1.0       # done channel
+    E = np.einsum("w,ab->awb", l, np.ones((1, 1)))          # [a', w, a]
+    N = np.ones((1, 1))
+    for A in As:
+        A = A.cpu().numpy()
+        E = np.einsum("xwy,xsa->wyas", E, A)                 # bra
+        E = np.einsum("wyas,wstv->yavt", E, W)               # W[w, s', s, w']: s' bra, s ket
+        E = np.einsum("yavt,ytb->avb", E, A)                 # ket
+        N = np.einsum("xy,xsa,ysb->ab", N, A, A)
+    return float(np.einsum("avb,v->", E, r)), float(N[0, 0])
+
+
+def test_dmrg_paper_appendix_a2_run(dev):
+    """The paper's own DMRG example (App. A.2): N = 100 Heisenberg chain,
+    random MPS of bond dimension 10, maxdim 10,20,100,100,200, cutoff 1e-11 -- every step on
+    libheff.  Checks: energies non-increasing sweep to sweep, E/N near the Bethe-ansatz bulk
+    value 1/4 - ln 2 (open-chain boundary cost pushes it up by ~1/N), and the returned energy
+    equals <psi|H|psi> of the returned MPS evaluated independently in numpy."""
+    from tools.dmrg_gpu import dmrg
+    W = mpo.heisenberg_chain_W()
+    energies = []
+    e, As = dmrg([W] * 100, [10, 20, 100, 100, 200], cutoff=1e-11, init_dim=10, seed=1,
+                 log=lambda msg: energies.append(float(msg.split("energy=")[1].split()[0])))
+    assert len(energies) == 5
+    assert all(b <= a + 1e-9 for a, b in zip(energies, energies[1:])), energies
+    assert -0.4432 < e / 100 < -0.4400, e
+    assert abs(energies[-1] - energies[-2]) < 1e-6
+    assert max(a.shape[2] for a in As[:-1]) <= 200
+    e_mps, nrm = _mps_energy_and_norm(As, W)
+    assert abs(nrm - 1.0) < 1e-10
+    assert abs(e_mps - e) < 1e-8 * abs(e), (e_mps, e)

@@ -118,7 +118,16 @@ def main():
     ap.add_argument("--sweeps", type=int, default=4)
     ap.add_argument("--model", default="chain", choices=["chain", "cylinder"])
     ap.add_argument("--lanczos", type=int, default=40)
+    ap.add_argument("--paper-a2", action="store_true",
+                    help="the paper's App. A.2 run (PAPER.md:1498-1517): N = 100 S=1/2 Heisenberg chain, random "
+                         "MPS of bond dimension 10, 5 sweeps with maxdim 10,20,100,100,200 and cutoff 1e-11")
     args = ap.parse_args()
+    if args.paper_a2:
+        t0 = time.perf_counter()
+        e, As = dmrg([mpo.heisenberg_chain_W()] * 100, [10, 20, 100, 100, 200], cutoff=1e-11, init_dim=10,
+                     lanczos_iter=args.lanczos)
+        print(f"G.S. energy = {e:.12f}  E0/N = {e / 100:.8f}  ({time.perf_counter() - t0:.1f} s)")
+        return
     if args.model == "chain":
         Ws = [mpo.heisenberg_chain_W()] * args.N
     else:
