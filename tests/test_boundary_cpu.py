@@ -114,3 +114,19 @@ def test_host_truncation_rule_matches_oracle_and_brute_force():
         heff.truncate_spectrum([1.0], cutoff=-1.0)
     with pytest.raises(heff.HeffZeroVector):
         heff.truncate_spectrum([0.0, 0.0])
+
+
+def _build_c_demo(out):
+    cmd = ["gcc", "-O2", "-I", str(ROOT / "include"), "-I", "/usr/local/cuda/include",
+           str(ROOT / "examples" / "heff_demo.c"), "-L", str(ROOT / "paper_2007_14822_b200"), "-lheff",
+           f"-Wl,-rpath,{ROOT / 'paper_2007_14822_b200'}", "-L", "/usr/local/cuda/lib64", "-lcudart", "-lm", "-o", str(out)]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
+def test_c_abi_demo_compiles_and_links(tmp_path):
+    """examples/heff_demo.c uses include/heff.h from plain C and links libheff.so -- the
+    boundary is a C ABI, not a Python one."""
+    import __graft_entry__ as g
+    g.build()
+    r = _build_c_demo(tmp_path / "heff_demo")
+    assert r.returncode == 0, r.stderr

@@ -282,3 +282,14 @@ def test_streamk_and_data_parallel_schedules(dev, orc, sk, monkeypatch):
         L, W1, W2, R, psi = x.numpy()
         ref = orc.heff_apply(L, W1, W2, R, psi)
         assert rel(gpu_apply(x, dev), ref) <= MATVEC_TOL
+
+
+def test_c_abi_demo_runs(dev, tmp_path):
+    """examples/heff_demo.c: lanczos_ground + heff_svd_split called from C give the N = 2
+    singlet (E0 = -3/4, Schmidt values 1/sqrt 2)."""
+    import subprocess
+    from tests.test_boundary_cpu import _build_c_demo
+    r = _build_c_demo(tmp_path / "heff_demo")
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(tmp_path / "heff_demo")], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
