@@ -2054,7 +2054,8 @@ static std::vector<int2> svd_pair_schedule(int nblk) {
 
 static constexpr int kSvdMaxSweeps = 80;
 static int g_lq_grid = 0;  // co-resident CTAs of lq_panel_kernel (cooperative launch)
-static int g_svd_gram_occ = 0, g_svd_rot_occ = 0;  // co-resident CTAs per SM
+static int g_svd_gram_occ = 0, g_svd_rot_occ = 0;    // co-resident CTAs per SM
+static int g_svd_tgram_occ = 0, g_svd_trot_occ = 0;  // (TMA-fed variants)
 static constexpr double kSvdRankEps = 1e-12;   // reading R21
 static constexpr double kSvdNegligible = 1e-15; // columns below this fraction of ||Psi||_F are not rotated
 
@@ -2127,14 +2128,27 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_rot_occ, svd_rotate_kernel, kSvdRotThreads, 0));
     g_svd_gram_occ = std::max(1, g_svd_gram_occ);
     g_svd_rot_occ = std::max(1, g_svd_rot_occ);
+    CK(cudaFuncSetAttribute(svd_rotate_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdTmaRotSmem));
+    CK(cudaFuncSetAttribute(svd_gram_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdTmaGramSmem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_tgram_occ, svd_gram_tma_kernel, (kSvdTmaGramWarps + 1) * 32,
+                                                     kSvdTmaGramSmem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_trot_occ, svd_rotate_tma_kernel, (kSvdTmaRotWarps + 1) * 32,
+                                                     kSvdTmaRotSmem));
+    g_svd_tgram_occ = std::max(1, g_svd_tgram_occ);
+    g_svd_trot_occ = std::max(1, g_svd_trot_occ);
   }
-  const int64_t gram_chunks = (R + 127) / 128;
-  const int gram_grid = (int)std::min<int64_t>((int64_t)g_svd_gram_occ * g_num_sms, npairs * gram_chunks);
+  // TMA-fed Gram / rotation (svd.cuh) unless disabled; tensor-map row coordinates are int32
+  const bool svd_tma = getenv("HEFF_SVD_NO_TMA") == nullptr && nblk * R < (1ll << 31);
+  const int64_t gram_chunks = (R + 127) / 128;  // 128-row chunks in both Gram kernels
+  const int gram_grid = (int)std::min<int64_t>((int64_t)(svd_tma ? g_svd_tgram_occ : g_svd_gram_occ) * g_num_sms,
+                                               npairs * gram_chunks);
   int nslots = 1;  // CTAs touching one pair, at most
   for (int p = 0; p < npairs; ++p)
     nslots = std::max(nslots, svd_sk_owner((int64_t)p * gram_chunks + gram_chunks - 1, npairs * gram_chunks, gram_grid) -
                                   svd_sk_owner((int64_t)p * gram_chunks, npairs * gram_chunks, gram_grid) + 1);
-  const int rot_grid = (int)std::min<int64_t>((int64_t)g_svd_rot_occ * g_num_sms, npairs * ((R + 31) / 32));
+  const int rot_grid = svd_tma ? (int)std::min<int64_t>((int64_t)g_svd_trot_occ * g_num_sms,
+                                                         npairs * ((R + kSvdTmaRotRows - 1) / kSvdTmaRotRows))
+                               : (int)std::min<int64_t>((int64_t)g_svd_rot_occ * g_num_sms, npairs * ((R + 31) / 32));
   const int red_blocks = 4 * g_num_sms;
 
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
@@ -2290,12 +2304,25 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
       svd_permute_kernel<<<ew_grid(nblk * kSvdB * R), 256, 0, s>>>(Xb, Xb2, R, ncols, nblk, d_sortperm);
       std::swap(Xb, Xb2);
     }
+    CUtensorMap xm_gram, xm_rot;  // Xb changes with the per-sweep column permutation
+    if (svd_tma) {
+      CKR(make_map(&xm_gram, Xb, nblk * R, kSvdB, kSvdB, kSvdB, kSvdTmaGramRows));
+      CKR(make_map(&xm_rot, Xb, nblk * R, kSvdB, kSvdB, kSvdB, kSvdTmaRotRows));
+    }
     for (int r = 0; r < rounds; ++r) {
       const int2* pr = d_pairs + (size_t)r * npairs;
-      svd_gram_kernel<<<gram_grid, kSvdGramThreads, 0, s>>>(Xb, R, pr, npairs, nslots, Gp);
+      if (svd_tma)
+        svd_gram_tma_kernel<<<gram_grid, (kSvdTmaGramWarps + 1) * 32, kSvdTmaGramSmem, s>>>(xm_gram, R, pr, npairs,
+                                                                                          nslots, Gp);
+      else
+        svd_gram_kernel<<<gram_grid, kSvdGramThreads, 0, s>>>(Xb, R, pr, npairs, nslots, Gp);
       svd_pair_eig_kernel<<<npairs, kSvdEigThreads, 0, s>>>(Gp, nslots, gram_chunks, gram_grid, tol, negl, inner,
                                                            d_Qg, d_flag, d_maxoff + sw, d_nrot + sw);
-      svd_rotate_kernel<<<rot_grid, kSvdRotThreads, 0, s>>>(Xb, R, pr, npairs, d_Qg, d_flag);
+      if (svd_tma)
+        svd_rotate_tma_kernel<<<rot_grid, (kSvdTmaRotWarps + 1) * 32, kSvdTmaRotSmem, s>>>(xm_rot, Xb, R, pr, npairs,
+                                                                                          d_Qg, d_flag);
+      else
+        svd_rotate_kernel<<<rot_grid, kSvdRotThreads, 0, s>>>(Xb, R, pr, npairs, d_Qg, d_flag);
     }
     CK(cudaGetLastError());
     int nrot = 0;
