@@ -109,3 +109,75 @@ def psi_matrix(psi: np.ndarray) -> np.ndarray:
     """psi[a, s1, s2, b] -> Psi[(a s1), (s2 b)] (row-major reshape; no data movement)."""
     mL, d1, d2, mR = psi.shape
     return np.ascontiguousarray(psi).reshape(mL * d1, d2 * mR)
+
+
+@dataclass
+class SplitQN:
+    Q: np.ndarray        # dir 0: U [M, n]; dir 1: V^T [n, N] -- new bond sector-sorted
+    S: np.ndarray        # all singular values of all sector blocks, descending, zero-padded to min(M, N)
+    Sk: np.ndarray       # kept singular values in new-bond order
+    qk: np.ndarray       # charge of each new-bond index (nondecreasing)
+    C: np.ndarray        # dir 0: S V^T [n, N]; dir 1: U S [M, n]
+    n: int
+    trunc_err: float
+
+
+def svd_split_qn(psi_mat: np.ndarray, qrow, qcol, cutoff: float = 0.0, maxdim: int = 0, mindim: int = 1,
+                 direction: int = 0) -> SplitQN:
+    """Two-site split of a charge-conserving Psi (U(1), Sec. 7): Psi[r][c]
+    is nonzero only if qrow[r] == qcol[c] (the charge carried by the centre bond), so Psi is
+    block diagonal over the charge sectors; factorizations of block-sparse ITensors treat
+    the nonzero blocks independently.  Every block gets its own
+    SVD (numpy/LAPACK, a library step); one truncation (reading R20/R21) runs over the union
+    of all blocks' singular values ("independent SVD per flux-sector block,
+    single global sorted truncation across sectors"); the new bond index is ordered by
+    charge, then by descending singular value within a charge (reading R24), and carries
+    the block's charge.  Gauge per vector as in svd_split (R22)."""
+    Psi = np.asarray(psi_mat, dtype=np.float64)
+    M, N = Psi.shape
+    qrow, qcol = np.asarray(qrow), np.asarray(qcol)
+    if qrow.shape != (M,) or qcol.shape != (N,):
+        raise ValueError("charge arrays must match Psi's shape")
+    allowed = qrow[:, None] == qcol[None, :]
+    if np.any(Psi[~allowed] != 0.0):
+        raise ValueError("Psi has entries outside its charge blocks")
+    sectors = sorted(set(qrow.tolist()) & set(qcol.tolist()))
+    cand = []        # (value, sector position, index in block)
+    blocks = {}
+    for si, c in enumerate(sectors):
+        rows, cols = np.nonzero(qrow == c)[0], np.nonzero(qcol == c)[0]
+        U, s, Vt = np.linalg.svd(Psi[np.ix_(rows, cols)], full_matrices=False)
+        blocks[c] = (rows, cols, U, s, Vt)
+        cand += [(float(v), si, j) for j, v in enumerate(s)]
+    if not cand:
+        raise ValueError("no charge sector is present in both rows and columns")
+    cand.sort(key=lambda e: (-e[0], e[1], e[2]))
+    S = np.zeros(min(M, N))
+    S[: len(cand)] = [e[0] for e in cand]
+    n, err = truncate_spectrum(S, cutoff, maxdim, mindim)
+    kept = sorted(cand[:n], key=lambda e: (e[1], -e[0], e[2]))    # new bond: charge, then value
+    Q = np.zeros((M, n)) if direction == 0 else np.zeros((n, N))
+    C = np.zeros((n, N)) if direction == 0 else np.zeros((M, n))
+    Sk, qk = np.zeros(n), np.zeros(n, dtype=int)
+    for k, (v, si, j) in enumerate(kept):
+        c = sectors[si]
+        rows, cols, U, s, Vt = blocks[c]
+        u, vt = U[:, j].copy(), Vt[j, :].copy()
+        vec = u if direction == 0 else vt
+        if vec[np.argmax(np.abs(vec))] < 0:                          # gauge (R22)
+            u, vt = -u, -vt
+        Sk[k], qk[k] = s[j], c
+        if direction == 0:
+            Q[rows, k] = u
+            C[k, cols] = s[j] * vt
+        else:
+            Q[k, cols] = vt
+            C[rows, k] = u * s[j]
+    return SplitQN(Q=Q, S=S, Sk=Sk, qk=qk, C=C, n=n, trunc_err=err)
+
+
+def qn_row_col_charges(qa, qs1, qs2, qb):
+    """Charges of Psi's rows (a s1) and columns (s2 b) for the U(1) convention of reading R18
+    (a bond carries the total charge to its left): qrow = q(a) + q(s1), qcol = q(b) - q(s2)."""
+    qa, qs1, qs2, qb = (np.asarray(v) for v in (qa, qs1, qs2, qb))
+    return (qa[:, None] + qs1[None, :]).reshape(-1), (qb[None, :] - qs2[:, None]).reshape(-1)

@@ -200,3 +200,66 @@ def test_directions_agree_and_gauge():
 def test_zero_matrix_is_an_error():
     with pytest.raises(ValueError):
         osplit.svd_split(np.zeros((4, 4)))
+
+
+# ---------------------------------------------------------------- U(1) block split (NEXT-2 x NEXT-3)
+def _qn_psi(N=10, seed=3):
+    """Sz = 0 ground state of the N-site chain as a two-site matrix with its charges."""
+    E, psi = _ed_ground(N)
+    h = N // 2
+    sz = lambda n: np.array([sum(1 if (i >> (n - 1 - b)) & 1 == 0 else -1 for b in range(n)) for i in range(2 ** n)])
+    qr, qc = sz(h), -sz(N - h)                               # q(left half) + q(right half) = 0
+    Psi = psi.reshape(2 ** h, 2 ** h) * (qr[:, None] == qc[None, :])   # drop eigsh's out-of-sector noise
+    return Psi / np.linalg.norm(Psi), qr, qc
+
+
+def test_qn_split_equals_dense_split():
+    """The block split of a charge-block-diagonal Psi has the dense split's spectrum, kept
+    count, truncation error and truncated approximation (a block-diagonal matrix's SVD is
+    the union of its blocks' SVDs)."""
+    Psi, qr, qc = _qn_psi()
+    for kw in (dict(), dict(maxdim=17), dict(cutoff=1e-6), dict(cutoff=1e-3, maxdim=30)):
+        for d in (0, 1):
+            a = osplit.svd_split_qn(Psi, qr, qc, direction=d, **kw)
+            b = osplit.svd_split(Psi, direction=d, **kw)
+            np.testing.assert_allclose(a.S, b.S, atol=1e-14)
+            assert a.n == b.n and a.trunc_err == pytest.approx(b.trunc_err, abs=1e-15)
+            ra = a.Q @ a.C if d == 0 else a.C @ a.Q
+            rb = b.Q @ b.C if d == 0 else b.C @ b.Q
+            s = b.S
+            if a.n == s.size or s[a.n - 1] - s[a.n] > 1e-8:
+                np.testing.assert_allclose(ra, rb, atol=1e-12)
+
+
+def test_qn_split_charge_conservation_and_order():
+    Psi, qr, qc = _qn_psi()
+    for d in (0, 1):
+        sp = osplit.svd_split_qn(Psi, qr, qc, maxdim=40, direction=d)
+        assert np.all(np.diff(sp.qk) >= 0)                       # sector-sorted new bond
+        for k in range(sp.n):
+            u = sp.Q[:, k] if d == 0 else sp.C[:, k]
+            v = sp.C[k, :] if d == 0 else sp.Q[k, :]
+            assert np.all(u[qr != sp.qk[k]] == 0.0) and np.all(v[qc != sp.qk[k]] == 0.0)
+        for c in set(sp.qk.tolist()):                            # descending inside a sector
+            assert np.all(np.diff(sp.Sk[sp.qk == c]) <= 0)
+        G = sp.Q.T @ sp.Q if d == 0 else sp.Q @ sp.Q.T
+        np.testing.assert_allclose(G, np.eye(sp.n), atol=1e-13)
+
+
+def test_qn_split_spin_flip_symmetry():
+    """The Sz = 0 ground state is spin-flip symmetric: the Schmidt values of the left half's
+    sectors Sz and -Sz coincide."""
+    Psi, qr, qc = _qn_psi()
+    sp = osplit.svd_split_qn(Psi, qr, qc)
+    for c in set(sp.qk.tolist()):
+        if c > 0:
+            np.testing.assert_allclose(np.sort(sp.Sk[sp.qk == c]), np.sort(sp.Sk[sp.qk == -c]), atol=1e-12)
+
+
+def test_qn_split_rejects_charge_violations():
+    Psi, qr, qc = _qn_psi()
+    bad = Psi.copy()
+    i, j = np.nonzero(qr[:, None] != qc[None, :])
+    bad[i[0], j[0]] = 1.0
+    with pytest.raises(ValueError):
+        osplit.svd_split_qn(bad, qr, qc)
