@@ -268,6 +268,19 @@ typedef struct {
 int heff_svd_split(int64_t M, int64_t N, const double* psi, const heff_trunc* trunc, int dir, double* Q, double* S,
                    double* C, int64_t* n_kept, double* trunc_err, int* sweeps, heff_stream stream);
 
+/* U(1) two-site split (NEXT-2 x NEXT-3, reading R24; block-sparse factorizations,
+ * P:L1076-1085): qrow[M] / qcol[N] are HOST charge arrays of Psi's rows (a s1) and columns
+ * (s2 b) -- for the R18 convention qrow = q(a) + q(s1), qcol = q(b) - q(s2).  Psi must vanish
+ * where qrow[r] != qcol[c] (HEFF_EINVAL otherwise).  Every charge block is split by the dense
+ * algorithm, one truncation (R20/R21) runs over the union of the blocks' values, and the new
+ * bond is ordered by charge (ascending) then by descending value.  Outputs as heff_svd_split
+ * plus Sk (DEVICE, n doubles: kept values in new-bond order) and qk (HOST, n ints: the new
+ * bond's charges); S holds all blocks' values, descending, zero-padded to min(M, N); sweeps =
+ * the most Jacobi sweeps any block needed.  Synchronous on `stream`. */
+int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const int* qrow, const int* qcol,
+                      const heff_trunc* trunc, int dir, double* Q, double* S, double* Sk, int* qk, double* C,
+                      int64_t* n_kept, double* trunc_err, int* sweeps, heff_stream stream);
+
 /* Host-only (no device work): the truncation rule heff_svd_split applies, on HOST values
  * s[0..k) (descending, non-negative).  n_kept / trunc_err as in heff_svd_split.
  * HEFF_EINVAL (not descending, negative, cutoff < 0), HEFF_EZERO (s[0] == 0). */

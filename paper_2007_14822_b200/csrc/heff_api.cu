@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -2392,5 +2393,167 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   }
   *n_kept = n;
   *trunc_err = err;
+  return HEFF_OK;
+}
+
+// --------------------------------------------------------------------------- U(1) split
+// NEXT-2 x NEXT-3 (reading R24): Psi is block diagonal over the centre-bond charge; every
+// block is split by heff_svd_split (dense Jacobi on the block), one truncation runs over the
+// union of the blocks' spectra, the new bond is ordered by (charge, descending value).
+struct SvdQnArena {
+  double* buf = nullptr;
+  size_t bytes = 0;
+};
+static thread_local SvdQnArena t_svdqn_arena;
+
+extern "C" int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const int* qrow, const int* qcol,
+                                 const heff_trunc* trunc, int dir, double* Qout, double* S, double* Sk, int* qk,
+                                 double* Cout, int64_t* n_kept, double* trunc_err, int* sweeps_out,
+                                 heff_stream stream) {
+  if (M < 1 || N < 1 || !psi || !qrow || !qcol || !Qout || !S || !Sk || !qk || !Cout || !n_kept || !trunc_err ||
+      (dir != 0 && dir != 1))
+    return set_err(HEFF_EINVAL, "heff_svd_split_qn: bad argument");
+  const double cutoff = trunc ? trunc->cutoff : 0.0;
+  const int64_t maxdim = trunc ? trunc->maxdim : 0;
+  const int64_t mindim = trunc ? std::max<int64_t>(1, trunc->mindim) : 1;
+  if (!(cutoff >= 0.0)) return set_err(HEFF_EINVAL, "heff_svd_split_qn: cutoff < 0");
+  CKR(init_device_once());
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // sectors: charges present on both sides, ascending
+  std::map<int, std::vector<int>> rows_of, cols_of;
+  for (int64_t r = 0; r < M; ++r) rows_of[qrow[r]].push_back((int)r);
+  for (int64_t c = 0; c < N; ++c) cols_of[qcol[c]].push_back((int)c);
+  std::vector<int> sectors;
+  for (auto& kv : rows_of)
+    if (cols_of.count(kv.first)) sectors.push_back(kv.first);
+  if (sectors.empty()) return set_err(HEFF_EZERO, "heff_svd_split_qn: no charge sector on both sides (psi = 0)");
+  const int ns = (int)sectors.size();
+  std::vector<int64_t> Mc(ns), Nc(ns), kc(ns), off_idx(ns), off_blk(ns), off_q(ns), off_c(ns), off_s(ns);
+  std::vector<int> idx_host;
+  int64_t tot_blk = 0, tot_q = 0, tot_c = 0, tot_s = 0;
+  for (int si = 0; si < ns; ++si) {
+    const auto& rw = rows_of[sectors[si]];
+    const auto& cl = cols_of[sectors[si]];
+    Mc[si] = (int64_t)rw.size();
+    Nc[si] = (int64_t)cl.size();
+    kc[si] = std::min(Mc[si], Nc[si]);
+    off_idx[si] = (int64_t)idx_host.size();
+    idx_host.insert(idx_host.end(), rw.begin(), rw.end());
+    idx_host.insert(idx_host.end(), cl.begin(), cl.end());
+    auto pad = [](int64_t x) { return (x + 31) / 32 * 32; };
+    off_blk[si] = tot_blk; tot_blk += pad(Mc[si] * Nc[si]);
+    off_q[si] = tot_q;     tot_q += pad(dir == 0 ? Mc[si] * kc[si] : kc[si] * Nc[si]);
+    off_c[si] = tot_c;     tot_c += pad(dir == 0 ? kc[si] * Nc[si] : Mc[si] * kc[si]);
+    off_s[si] = tot_s;     tot_s += pad(kc[si]);
+  }
+  const int64_t kmin = std::min(M, N);
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t need = al(sizeof(int) * idx_host.size()) + al(sizeof(int) * (M + N)) + al(sizeof(int)) +
+                      al(sizeof(double) * (tot_blk + tot_q + tot_c + tot_s)) + al(sizeof(int2) * kmin);
+  SvdQnArena& a = t_svdqn_arena;
+  if (a.bytes < need) {
+    cudaFree(a.buf);
+    a.buf = nullptr;
+    a.bytes = 0;
+    CK(cudaMalloc(&a.buf, need));
+    a.bytes = need;
+  }
+  unsigned char* w = reinterpret_cast<unsigned char*>(a.buf);
+  int* d_idx = reinterpret_cast<int*>(w); w += al(sizeof(int) * idx_host.size());
+  int* d_q = reinterpret_cast<int*>(w); w += al(sizeof(int) * (M + N));
+  int* d_flag = reinterpret_cast<int*>(w); w += al(sizeof(int));
+  double* d_blk = reinterpret_cast<double*>(w);
+  double* d_qc = d_blk + tot_blk;
+  double* d_cc = d_qc + tot_q;
+  double* d_sc = d_cc + tot_c;
+  w += al(sizeof(double) * (tot_blk + tot_q + tot_c + tot_s));
+  int2* d_jk = reinterpret_cast<int2*>(w);
+  CK(cudaMemcpyAsync(d_idx, idx_host.data(), sizeof(int) * idx_host.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_q, qrow, sizeof(int) * M, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_q + M, qcol, sizeof(int) * N, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
+  svd_qn_check_kernel<<<ew_grid(M * N), 256, 0, s>>>(psi, M, N, d_q, d_q + M, d_flag);
+  CK(cudaGetLastError());
+  int h_flag = 0;
+  CK(cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h_flag) return set_err(HEFF_EINVAL, "heff_svd_split_qn: psi has entries outside its charge blocks");
+  // one dense split per block (all values kept; numerical zeros per the block's own rank rule)
+  std::vector<int64_t> nc(ns, 0);
+  std::vector<double> sv_host(tot_s, 0.0);
+  int sweeps_max = 0;
+  for (int si = 0; si < ns; ++si) {
+    const int* d_rows = d_idx + off_idx[si];
+    const int* d_cols = d_rows + Mc[si];
+    svd_qn_gather_kernel<<<ew_grid(Mc[si] * Nc[si]), 256, 0, s>>>(psi, N, d_rows, d_cols, Mc[si], Nc[si],
+                                                                  d_blk + off_blk[si]);
+    CK(cudaGetLastError());
+    int64_t nk = 0;
+    double e = 0.0;
+    int swp = 0;
+    const int r = heff_svd_split(Mc[si], Nc[si], d_blk + off_blk[si], nullptr, dir, d_qc + off_q[si], d_sc + off_s[si],
+                                 d_cc + off_c[si], &nk, &e, &swp, stream);
+    if (r == HEFF_EZERO) continue;  // an all-zero block contributes nothing
+    if (r != HEFF_OK) return r;
+    nc[si] = nk;
+    sweeps_max = std::max(sweeps_max, swp);
+    CK(cudaMemcpyAsync(sv_host.data() + off_s[si], d_sc + off_s[si], sizeof(double) * kc[si], cudaMemcpyDeviceToHost,
+                       s));
+  }
+  CK(cudaStreamSynchronize(s));
+  struct Cand { double v; int si; int j; };
+  std::vector<Cand> cand;
+  for (int si = 0; si < ns; ++si)
+    if (nc[si] > 0)
+      for (int64_t j = 0; j < kc[si]; ++j) cand.push_back({sv_host[off_s[si] + j], si, (int)j});
+  if (cand.empty() || !(cand[0].v >= 0.0)) return set_err(HEFF_EZERO, "heff_svd_split_qn: psi is zero");
+  std::stable_sort(cand.begin(), cand.end(), [](const Cand& x, const Cand& y) {
+    if (x.v != y.v) return x.v > y.v;
+    if (x.si != y.si) return x.si < y.si;
+    return x.j < y.j;
+  });
+  std::vector<double> sall(kmin, 0.0);
+  for (size_t i = 0; i < cand.size() && (int64_t)i < kmin; ++i) sall[i] = cand[i].v;
+  if (!(sall[0] > 0.0)) return set_err(HEFF_EZERO, "heff_svd_split_qn: psi is zero");
+  int64_t n = 0;
+  double err = 0.0;
+  truncate_rule(sall.data(), kmin, cutoff, maxdim, mindim, &n, &err);
+  std::vector<Cand> kept(cand.begin(), cand.begin() + n);
+  std::stable_sort(kept.begin(), kept.end(), [](const Cand& x, const Cand& y) {
+    if (x.si != y.si) return x.si < y.si;
+    if (x.v != y.v) return x.v > y.v;
+    return x.j < y.j;
+  });
+  std::vector<double> sk(n);
+  std::vector<int2> jk(n);
+  for (int64_t k = 0; k < n; ++k) {
+    if (kept[k].j >= nc[kept[k].si]) return set_err(HEFF_ECUDA, "heff_svd_split_qn: kept a numerical zero");
+    sk[k] = kept[k].v;
+    qk[k] = sectors[kept[k].si];
+    jk[k] = make_int2(kept[k].j, (int)k);
+  }
+  CK(cudaMemcpyAsync(S, sall.data(), sizeof(double) * kmin, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(Sk, sk.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_jk, jk.data(), sizeof(int2) * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(Qout, 0, sizeof(double) * (dir == 0 ? M * n : n * N), s));
+  CK(cudaMemsetAsync(Cout, 0, sizeof(double) * (dir == 0 ? n * N : M * n), s));
+  int64_t k0 = 0;
+  for (int si = 0; si < ns && k0 < n; ++si) {
+    int64_t k1 = k0;
+    while (k1 < n && kept[k1].si == si) ++k1;
+    if (k1 > k0) {
+      const int* d_rows = d_idx + off_idx[si];
+      const int* d_cols = d_rows + Mc[si];
+      dim3 grid((unsigned)std::min<int64_t>((std::max(Mc[si], Nc[si]) + 255) / 256, 64), (unsigned)(k1 - k0));
+      svd_qn_scatter_kernel<<<grid, 256, 0, s>>>(d_qc + off_q[si], d_cc + off_c[si], d_jk + k0, d_rows, d_cols, Mc[si],
+                                                Nc[si], nc[si], dir, Qout, Cout, M, N, n);
+      CK(cudaGetLastError());
+    }
+    k0 = k1;
+  }
+  CK(cudaStreamSynchronize(s));
+  *n_kept = n;
+  *trunc_err = err;
+  if (sweeps_out) *sweeps_out = sweeps_max;
   return HEFF_OK;
 }

@@ -786,4 +786,43 @@ __global__ void __launch_bounds__((kSvdTmaGramWarps + 1) * 32) svd_gram_tma_kern
   }
 }
 
+// ---------------------------------------------------------------- U(1) block split helpers
+// flag = 1 if Psi has a nonzero entry outside its charge blocks (qrow[r] != qcol[c])
+__global__ void svd_qn_check_kernel(const double* __restrict__ psi, int64_t M, int64_t N, const int* __restrict__ qrow,
+                                    const int* __restrict__ qcol, int* __restrict__ flag) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < M * N; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / N, c = e - r * N;
+    if (qrow[r] != qcol[c] && psi[e] != 0.0) *flag = 1;
+  }
+}
+
+// out[i][l] = psi[rows[i]][cols[l]]  (one charge block, dense Mc x Nc)
+__global__ void svd_qn_gather_kernel(const double* __restrict__ psi, int64_t N, const int* __restrict__ rows,
+                                     const int* __restrict__ cols, int64_t Mc, int64_t Nc, double* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < Mc * Nc; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / Nc, l = e - i * Nc;
+    out[e] = psi[(int64_t)rows[i] * N + cols[l]];
+  }
+}
+
+// Scatter the kept vectors of one block into the full factors.  jk[q] = (j, k): block vector j
+// becomes new-bond index k.  dir 0: Q[rows[i]][k] = Qc[i][j] (pitch nc), C[k][cols[l]] = Cc[j][l];
+// dir 1: Q[k][cols[l]] = Qc[j][l], C[rows[i]][k] = Cc[i][j] (pitch nc).  grid.y = kept count.
+__global__ void svd_qn_scatter_kernel(const double* __restrict__ Qc, const double* __restrict__ Cc,
+                                      const int2* __restrict__ jk, const int* __restrict__ rows,
+                                      const int* __restrict__ cols, int64_t Mc, int64_t Nc, int64_t nc, int dir,
+                                      double* __restrict__ Q, double* __restrict__ C, int64_t M, int64_t N,
+                                      int64_t n) {
+  const int2 p = jk[blockIdx.y];
+  const int j = p.x, k = p.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Mc; i += (int64_t)gridDim.x * blockDim.x) {
+    if (dir == 0) Q[(int64_t)rows[i] * n + k] = Qc[i * nc + j];
+    else C[(int64_t)rows[i] * n + k] = Cc[i * nc + j];
+  }
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < Nc; l += (int64_t)gridDim.x * blockDim.x) {
+    if (dir == 0) C[(int64_t)k * N + cols[l]] = Cc[(int64_t)j * Nc + l];
+    else Q[(int64_t)k * N + cols[l]] = Qc[(int64_t)j * Nc + l];
+  }
+}
+
 }  // namespace heff

@@ -97,7 +97,9 @@ def lib() -> ctypes.CDLL:
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ip), vp]
         L.heff_truncate_spectrum.argtypes = [vp, i64, ctypes.POINTER(_Trunc), ctypes.POINTER(i64),
                                              ctypes.POINTER(ctypes.c_double)]
-        for f in ("heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
+        L.heff_svd_split_qn.argtypes = [i64, i64, vp, vp, vp, ctypes.POINTER(_Trunc), ip, vp, vp, vp, vp, vp,
+                                        ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ip), vp]
+        for f in ("heff_svd_split_qn", "heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
                   "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z"):
@@ -110,7 +112,7 @@ EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "h
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
             "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z",
-            "heff_svd_split", "heff_truncate_spectrum", "heff_apply_blocked")
+            "heff_svd_split", "heff_truncate_spectrum", "heff_apply_blocked", "heff_svd_split_qn")
 
 
 def _check(rc: int):
@@ -241,6 +243,55 @@ def svd_split(psi: torch.Tensor, cutoff: float = 0.0, maxdim: int = 0, mindim: i
     else:
         Qv, Cv = Q[: k * N].view(k, N), C[: M * k].view(M, k)
     return SplitResult(Qv, S, Cv, k, err.value, sw.value)
+
+
+@dataclass
+class SplitQNResult(SplitResult):
+    Sk: torch.Tensor = None   # kept values in new-bond order
+    qk: list = None           # charges of the new bond (nondecreasing)
+
+
+def psi_row_col_charges(qa, qs1, qs2, qb):
+    """Charges of Psi's rows (a s1) and columns (s2 b) in the convention of DESIGN.md R18 (a
+    bond carries the total charge to its left): q(a) + q(s1) and q(b) - q(s2)."""
+    qrow = [int(x) + int(y) for x in qa for y in qs1]
+    qcol = [int(b) - int(y) for y in qs2 for b in qb]
+    return qrow, qcol
+
+
+def svd_split_qn(psi: torch.Tensor, qrow, qcol, cutoff: float = 0.0, maxdim: int = 0, mindim: int = 1,
+                 direction: int = 0, stream=None) -> SplitQNResult:
+    """U(1) two-site split (heff_svd_split_qn): Psi's rows/columns carry charges qrow/qcol
+    (host int sequences); one dense split per charge block, one global truncation."""
+    _dev(psi, "psi")
+    if psi.dim() == 4:
+        mL, d1, d2, mR = psi.shape
+        M, N = mL * d1, d2 * mR
+    else:
+        M, N = psi.shape
+    qr = (ctypes.c_int * M)(*[int(v) for v in qrow])
+    qc = (ctypes.c_int * N)(*[int(v) for v in qcol])
+    if len(qrow) != M or len(qcol) != N:
+        raise ValueError("charge arrays must match Psi's shape")
+    kmax = min(M, N) if maxdim <= 0 else min(M, N, maxdim)
+    Q = torch.empty(max(1, M * kmax if direction == 0 else kmax * N), dtype=torch.float64, device=psi.device)
+    C = torch.empty(max(1, kmax * N if direction == 0 else M * kmax), dtype=torch.float64, device=psi.device)
+    S = torch.empty(min(M, N), dtype=torch.float64, device=psi.device)
+    Sk = torch.empty(max(1, kmax), dtype=torch.float64, device=psi.device)
+    qk = (ctypes.c_int * max(1, kmax))()
+    n = ctypes.c_int64(0)
+    err = ctypes.c_double(0.0)
+    sw = ctypes.c_int(0)
+    tr = _Trunc(float(cutoff), int(maxdim), int(mindim))
+    _check(lib().heff_svd_split_qn(M, N, psi.data_ptr(), qr, qc, ctypes.byref(tr), int(direction), Q.data_ptr(),
+                                   S.data_ptr(), Sk.data_ptr(), qk, C.data_ptr(), ctypes.byref(n), ctypes.byref(err),
+                                   ctypes.byref(sw), _stream(stream)))
+    k = n.value
+    if direction == 0:
+        Qv, Cv = Q[: M * k].view(M, k), C[: k * N].view(k, N)
+    else:
+        Qv, Cv = Q[: k * N].view(k, N), C[: M * k].view(M, k)
+    return SplitQNResult(Qv, S, Cv, k, err.value, sw.value, Sk[:k], list(qk)[:k])
 
 
 def truncate_spectrum(s, cutoff: float = 0.0, maxdim: int = 0, mindim: int = 1) -> tuple[int, float]:
