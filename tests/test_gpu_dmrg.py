@@ -78,3 +78,20 @@ def test_dmrg_paper_appendix_a2_run(dev):
     e_mps, nrm = _mps_energy_and_norm(As, W)
     assert abs(nrm - 1.0) < 1e-10
     assert abs(e_mps - e) < 1e-8 * abs(e), (e_mps, e)
+
+
+def test_dmrg_qn_matches_ed_and_dense(dev):
+    """U(1) sweeps (heff_set_qn matvec + Lanczos on the sector, heff_svd_split_qn) from the
+    Neel state reach the N = 12 chain's ED ground energy and the dense sweeps' energy."""
+    from heffgen import qn as hqn
+    from tools.dmrg_gpu import dmrg, dmrg_qn
+    N = 12
+    W = mpo.heisenberg_chain_W()
+    e_qn, As, bq = dmrg_qn([W] * N, [hqn.heisenberg_channel_charges()] * N, [16, 32, 64, 64], log=lambda *_: None)
+    e0 = spla.eigsh(ed_ref.heisenberg(N, ed_ref.chain_bonds(N)), k=1, which="SA", tol=1e-14)[0][0]
+    assert abs(e_qn - e0) <= 1e-9
+    for j, A in enumerate(As):                       # every site tensor conserves charge
+        qs = np.array([1, -1])
+        allowed = bq[j + 1][None, None, :] == bq[j][:, None, None] + qs[None, :, None]
+        assert np.all(A.cpu().numpy()[~allowed] == 0.0)
+    assert all(np.all(np.diff(q) >= 0) for q in bq)  # sector-sorted bonds

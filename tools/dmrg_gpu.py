@@ -111,6 +111,62 @@ def dmrg(Ws, maxdims, cutoff=1e-11, seed=0, lanczos_iter=40, init_dim=8, device=
     return energy, As
 
 
+def dmrg_qn(Ws, chan_q, maxdims, cutoff=1e-11, lanczos_iter=40, device="cuda", log=print):
+    """U(1) (Sz-conserving) two-site DMRG in the Sz = 0 sector (reading R18 conventions):
+    the start is the Neel product state; every bond declares its charges to the matvec
+    (heff_set_qn: block-sparse GEMM schedules, Lanczos on the sector's entries), splits with
+    heff_svd_split_qn (one SVD per centre-bond charge block) and records the new bond's
+    charges for the next plan.  chan_q[j]: MPO channel charges of the bond right of site j."""
+    from paper_2007_14822_b200.heff import psi_row_col_charges, svd_split_qn
+    N = len(Ws)
+    k = Ws[0].shape[0]
+    qs = np.array([1, -1])
+    tW = [torch.from_numpy(np.ascontiguousarray(W)).to(device) for W in Ws]
+    As, bq = [], [np.array([0])]
+    for j in range(N):                                   # Neel state: Up, Dn, Up, ...
+        A = torch.zeros((1, 2, 1), dtype=torch.float64, device=device)
+        A[0, j % 2, 0] = 1.0
+        As.append(A)
+        bq.append(bq[-1] + qs[j % 2])
+    chan = [np.zeros(k, dtype=int)] + [np.asarray(c) for c in chan_q]   # chan[j] = bond left of site j
+    Ls = [None] * (N + 1)
+    Rs = [None] * (N + 2)
+    Ls[0] = torch.zeros((1, k, 1), dtype=torch.float64, device=device)
+    Ls[0][0, k - 1, 0] = 1.0
+    Rs[N] = torch.zeros((1, k, 1), dtype=torch.float64, device=device)
+    Rs[N][0, 0, 0] = 1.0
+    for j in range(N - 1, 1, -1):
+        Rs[j] = env_update_right(Rs[j + 1], As[j], tW[j])
+    energy = None
+    for sw, maxdim in enumerate(maxdims):
+        t0 = time.perf_counter()
+        t_split = 0.0
+        for direction, bonds in (("right", range(N - 1)), ("left", range(N - 2, -1, -1))):
+            for j in bonds:
+                psi = two_site(As[j], As[j + 1]).contiguous()
+                with Heff(Ls[j], tW[j], tW[j + 1], Rs[j + 2]) as h:
+                    h.set_qn(dict(qa=bq[j], qb=bq[j + 2], qs1=qs, qs2=qs, cL=chan[j], cM=chan[j + 1], cR=chan[j + 2]))
+                    r = h.lanczos_ground(psi, max_iter=lanczos_iter, tol=1e-12, converge=True)
+                energy = r.energy
+                a, d1, d2, b = psi.shape
+                qrow, qcol = psi_row_col_charges(bq[j], qs, qs, bq[j + 2])
+                ts = time.perf_counter()
+                sp = svd_split_qn(psi, qrow, qcol, cutoff=cutoff, maxdim=maxdim,
+                                  direction=0 if direction == "right" else 1)
+                t_split += time.perf_counter() - ts
+                kk = sp.n
+                bq[j + 1] = np.asarray(sp.qk)
+                if direction == "right":
+                    As[j], As[j + 1] = sp.Q.reshape(a, d1, kk).contiguous(), sp.C.reshape(kk, d2, b).contiguous()
+                    Ls[j + 1] = env_update_left(Ls[j], As[j], tW[j])
+                else:
+                    As[j], As[j + 1] = sp.C.reshape(a, d1, kk).contiguous(), sp.Q.reshape(kk, d2, b).contiguous()
+                    Rs[j + 1] = env_update_right(Rs[j + 2], As[j + 1], tW[j + 1])
+        log(f"After sweep {sw + 1} energy={energy:.12f} maxlinkdim={max(a.shape[2] for a in As[:-1])} "
+            f"time={time.perf_counter() - t0:.2f} split {t_split:.2f} s")
+    return energy, As, bq
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--N", type=int, default=20)
@@ -118,6 +174,7 @@ def main():
     ap.add_argument("--sweeps", type=int, default=4)
     ap.add_argument("--model", default="chain", choices=["chain", "cylinder"])
     ap.add_argument("--lanczos", type=int, default=40)
+    ap.add_argument("--qn", action="store_true", help="U(1)-conserving sweeps in the Sz = 0 sector")
     ap.add_argument("--paper-a2", action="store_true",
                     help="the paper's App. A.2 run (PAPER.md:1498-1517): N = 100 S=1/2 Heisenberg chain, random "
                          "MPS of bond dimension 10, 5 sweeps with maxdim 10,20,100,100,200 and cutoff 1e-11")
@@ -133,6 +190,12 @@ def main():
     else:
         Ws = [mpo.cylinder_W(j) for j in range(args.N)]
     maxdims = [min(args.maxdim, 10 * 2 ** s) for s in range(args.sweeps)]
+    if args.qn:
+        from heffgen import qn as hqn
+        c = hqn.heisenberg_channel_charges() if args.model == "chain" else hqn.cylinder_channel_charges()
+        e, _, _ = dmrg_qn(Ws, [c] * args.N, maxdims, lanczos_iter=args.lanczos)
+        print(f"E0 = {e:.12f}  E0/N = {e / args.N:.8f}")
+        return
     e, _ = dmrg(Ws, maxdims, lanczos_iter=args.lanczos)
     print(f"E0 = {e:.12f}  E0/N = {e / args.N:.8f}")
 
