@@ -2230,7 +2230,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     for (int64_t i = 0; i < R; ++i) rp[i] = (int)i;
     std::stable_sort(rp.begin(), rp.end(), [&](int a, int b) { return rn[a] > rn[b]; });
     CK(cudaMemcpyAsync(d_rowperm, rp.data(), sizeof(int) * R, cudaMemcpyHostToDevice, s));
-    svd_gather_rows_kernel<<<dim3((unsigned)std::min<int64_t>((colsP + 255) / 256, 64), (unsigned)R), 256, 0, s>>>(
+    svd_gather_rows_kernel<<<dim3((unsigned)std::min<int64_t>((colsP + 255) / 256, 64), (unsigned)std::min<int64_t>(R, 65535)), 256, 0, s>>>(
         src, d_P, R, colsP, d_rowperm);
     CK(cudaGetLastError());
     int nl = 0;
@@ -2360,11 +2360,11 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   CK(cudaMemcpyAsync(d_perm, order.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(d_skept, sv.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
   svd_sign_kernel<<<(unsigned)n, 256, 0, s>>>(Xb, R, d_perm, d_skept, d_scale, d_rowperm);
-  dim3 gg((unsigned)std::min<int64_t>((R + 255) / 256, 1024), (unsigned)n);
+  dim3 gg((unsigned)std::min<int64_t>((R + 255) / 256, 1024), (unsigned)std::min<int64_t>(n, 65535));
   int nl = 0;
   int r = HEFF_OK;
   if (dir == 0) {
-    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, d_Ut, d_rowperm);   // U^T [n][M]
+    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, d_Ut, d_rowperm, n);   // U^T [n][M]
     dim3 tg((unsigned)((M + 31) / 32), (unsigned)((n + 31) / 32));
     transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(d_Ut, Qout, n, M);            // U [M][n]
     CK(cudaGetLastError());
@@ -2372,7 +2372,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     g.M = n; g.N = N; g.K = M; g.A = d_Ut; g.lda = M; g.B = psi; g.ldb = N; g.b_kmajor = false; g.C = Cout; g.ldc = N;
     r = launch_gemm(g, 0, s, &nl, &t_svd_splitws);
   } else {
-    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, Qout, d_rowperm);   // V^T [n][N]
+    svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, Qout, d_rowperm, n);   // V^T [n][N]
     CK(cudaGetLastError());
     GemmOp g;  // C[M][n] = Psi[M][N] . (V^T)^T
     g.M = M; g.N = n; g.K = N; g.A = psi; g.lda = N; g.B = Qout; g.ldb = N; g.b_kmajor = true; g.C = Cout; g.ldc = n;
@@ -2544,9 +2544,10 @@ extern "C" int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const 
     if (k1 > k0) {
       const int* d_rows = d_idx + off_idx[si];
       const int* d_cols = d_rows + Mc[si];
-      dim3 grid((unsigned)std::min<int64_t>((std::max(Mc[si], Nc[si]) + 255) / 256, 64), (unsigned)(k1 - k0));
+      dim3 grid((unsigned)std::min<int64_t>((std::max(Mc[si], Nc[si]) + 255) / 256, 64),
+                (unsigned)std::min<int64_t>(k1 - k0, 65535));
       svd_qn_scatter_kernel<<<grid, 256, 0, s>>>(d_qc + off_q[si], d_cc + off_c[si], d_jk + k0, d_rows, d_cols, Mc[si],
-                                                Nc[si], nc[si], dir, Qout, Cout, M, N, n);
+                                                Nc[si], nc[si], dir, Qout, Cout, M, N, n, (int)(k1 - k0));
       CK(cudaGetLastError());
     }
     k0 = k1;

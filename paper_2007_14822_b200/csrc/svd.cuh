@@ -536,13 +536,14 @@ __global__ void svd_sign_kernel(const double* __restrict__ Xb, int64_t R, const 
 // out[k][r] = X[r][perm k] * scale[k]   (k < n: grid.y; r < R)
 __global__ void svd_gather_t_kernel(const double* __restrict__ Xb, int64_t R, const int* __restrict__ perm,
                                     const double* __restrict__ scale, double* __restrict__ out,
-                                    const int* __restrict__ rowperm) {
-  const int k = blockIdx.y;
-  const int c = perm[k];
-  const double sc = scale[k];
-  const double* col = Xb + (int64_t)(c >> 4) * R * kSvdB + (c & 15);
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x)
-    out[(int64_t)k * R + (rowperm ? rowperm[r] : r)] = col[r * kSvdB] * sc;
+                                    const int* __restrict__ rowperm, int64_t n) {
+  for (int64_t k = blockIdx.y; k < n; k += gridDim.y) {
+    const int c = perm[k];
+    const double sc = scale[k];
+    const double* col = Xb + (int64_t)(c >> 4) * R * kSvdB + (c & 15);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x)
+      out[k * R + (rowperm ? rowperm[r] : r)] = col[r * kSvdB] * sc;
+  }
 }
 
 // row norms^2 of a row-major matrix (one warp per row)
@@ -562,10 +563,11 @@ __global__ void svd_rownorm2_kernel(const double* __restrict__ A, int64_t rows, 
 // dst row r = src row perm[r] (row-major, cols per row)
 __global__ void svd_gather_rows_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t rows,
                                        int64_t cols, const int* __restrict__ perm) {
-  const int64_t row = blockIdx.y;
-  const double* sr = src + (int64_t)perm[row] * cols;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x)
-    dst[row * cols + c] = sr[c];
+  for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+    const double* sr = src + (int64_t)perm[row] * cols;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x)
+      dst[row * cols + c] = sr[c];
+  }
 }
 
 
@@ -812,16 +814,18 @@ __global__ void svd_qn_scatter_kernel(const double* __restrict__ Qc, const doubl
                                       const int2* __restrict__ jk, const int* __restrict__ rows,
                                       const int* __restrict__ cols, int64_t Mc, int64_t Nc, int64_t nc, int dir,
                                       double* __restrict__ Q, double* __restrict__ C, int64_t M, int64_t N,
-                                      int64_t n) {
-  const int2 p = jk[blockIdx.y];
-  const int j = p.x, k = p.y;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Mc; i += (int64_t)gridDim.x * blockDim.x) {
-    if (dir == 0) Q[(int64_t)rows[i] * n + k] = Qc[i * nc + j];
-    else C[(int64_t)rows[i] * n + k] = Cc[i * nc + j];
-  }
-  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < Nc; l += (int64_t)gridDim.x * blockDim.x) {
-    if (dir == 0) C[(int64_t)k * N + cols[l]] = Cc[(int64_t)j * Nc + l];
-    else Q[(int64_t)k * N + cols[l]] = Qc[(int64_t)j * Nc + l];
+                                      int64_t n, int nkept) {
+  for (int q = blockIdx.y; q < nkept; q += gridDim.y) {
+    const int2 p = jk[q];
+    const int j = p.x, k = p.y;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Mc; i += (int64_t)gridDim.x * blockDim.x) {
+      if (dir == 0) Q[(int64_t)rows[i] * n + k] = Qc[i * nc + j];
+      else C[(int64_t)rows[i] * n + k] = Cc[i * nc + j];
+    }
+    for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < Nc; l += (int64_t)gridDim.x * blockDim.x) {
+      if (dir == 0) C[(int64_t)k * N + cols[l]] = Cc[(int64_t)j * Nc + l];
+      else Q[(int64_t)k * N + cols[l]] = Qc[(int64_t)j * Nc + l];
+    }
   }
 }
 
