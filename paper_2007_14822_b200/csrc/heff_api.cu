@@ -12,6 +12,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <map>
 #include <string>
 #include <vector>
@@ -120,14 +125,14 @@ typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint3
                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static PFN_encodeTiled_t get_encode() {
-  static PFN_encodeTiled_t fn = nullptr;
-  if (!fn) {
+  static const PFN_encodeTiled_t fn = [] {  // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
-  }
+      return reinterpret_cast<PFN_encodeTiled_t>(p);
+    return static_cast<PFN_encodeTiled_t>(nullptr);
+  }();
   return fn;
 }
 
@@ -279,9 +284,12 @@ static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitW
   return HEFF_OK;
 }
 
+static std::mutex g_init_mu;  // one-time initialisations may race from worker threads
 static int init_device_once() {
-  static bool done = false;
-  if (done) return HEFF_OK;
+  static std::atomic<bool> done{false};
+  if (done.load(std::memory_order_acquire)) return HEFF_OK;
+  std::lock_guard<std::mutex> lock(g_init_mu);
+  if (done.load(std::memory_order_acquire)) return HEFF_OK;
   int dev;
   CK(cudaGetDevice(&dev));
   int major = 0, minor = 0;
@@ -299,7 +307,7 @@ static int init_device_once() {
   CK(cudaFuncSetAttribute(mpo_orderA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   CK(cudaFuncSetAttribute(mpo_orderB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  done = true;
+  done.store(true, std::memory_order_release);
   return HEFF_OK;
 }
 
@@ -2095,6 +2103,31 @@ extern "C" int heff_truncate_spectrum(const double* s, int64_t k, const heff_tru
   return HEFF_OK;
 }
 
+// one-time occupancy queries / attributes of the split's kernels (thread-safe)
+static int svd_init_once() {
+  static std::atomic<bool> done{false};
+  if (done.load(std::memory_order_acquire)) return HEFF_OK;
+  std::lock_guard<std::mutex> lock(g_init_mu);
+  if (done.load(std::memory_order_acquire)) return HEFF_OK;
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lq_panel_kernel, kLqThreads, 0));
+  g_lq_grid = std::max(1, per_sm) * g_num_sms;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_gram_occ, svd_gram_kernel, kSvdGramThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_rot_occ, svd_rotate_kernel, kSvdRotThreads, 0));
+  g_svd_gram_occ = std::max(1, g_svd_gram_occ);
+  g_svd_rot_occ = std::max(1, g_svd_rot_occ);
+  CK(cudaFuncSetAttribute(svd_rotate_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdTmaRotSmem));
+  CK(cudaFuncSetAttribute(svd_gram_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdTmaGramSmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_tgram_occ, svd_gram_tma_kernel, (kSvdTmaGramWarps + 1) * 32,
+                                                   kSvdTmaGramSmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_trot_occ, svd_rotate_tma_kernel, (kSvdTmaRotWarps + 1) * 32,
+                                                   kSvdTmaRotSmem));
+  g_svd_tgram_occ = std::max(1, g_svd_tgram_occ);
+  g_svd_trot_occ = std::max(1, g_svd_trot_occ);
+  done.store(true, std::memory_order_release);
+  return HEFF_OK;
+}
+
 extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const heff_trunc* trunc, int dir, double* Qout,
                               double* S, double* Cout, int64_t* n_kept, double* trunc_err, int* sweeps_out,
                               heff_stream stream) {
@@ -2111,11 +2144,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   const int64_t kmin = std::min(M, N);
   const int64_t colsP = dir == 0 ? N : M;      // columns of the working matrix P (Psi or Psi^T)
   // LQ preconditioning (lq.cuh): Jacobi on the k = min(M,N) columns of L instead of P
-  if (g_lq_grid == 0) {
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lq_panel_kernel, kLqThreads, 0));
-    g_lq_grid = std::max(1, per_sm) * g_num_sms;
-  }
+  CKR(svd_init_once());
   const bool precond = getenv("HEFF_SVD_NO_PRECOND") == nullptr && kmin > kSvdPair &&
                        (colsP + g_lq_grid - 1) / g_lq_grid <= kLqMaxCols;
   const int64_t ncols = precond ? kmin : colsP;  // columns of X (orthogonalised)
@@ -2124,20 +2153,6 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   if (nblk < 2) nblk = 2;
   const int npairs = (int)(nblk / 2), rounds = (int)(nblk - 1);
   // balanced persistent grids (svd.cuh): one wave of co-resident CTAs, work split evenly
-  if (g_svd_gram_occ == 0) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_gram_occ, svd_gram_kernel, kSvdGramThreads, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_rot_occ, svd_rotate_kernel, kSvdRotThreads, 0));
-    g_svd_gram_occ = std::max(1, g_svd_gram_occ);
-    g_svd_rot_occ = std::max(1, g_svd_rot_occ);
-    CK(cudaFuncSetAttribute(svd_rotate_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdTmaRotSmem));
-    CK(cudaFuncSetAttribute(svd_gram_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSvdTmaGramSmem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_tgram_occ, svd_gram_tma_kernel, (kSvdTmaGramWarps + 1) * 32,
-                                                     kSvdTmaGramSmem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_trot_occ, svd_rotate_tma_kernel, (kSvdTmaRotWarps + 1) * 32,
-                                                     kSvdTmaRotSmem));
-    g_svd_tgram_occ = std::max(1, g_svd_tgram_occ);
-    g_svd_trot_occ = std::max(1, g_svd_trot_occ);
-  }
   // TMA-fed Gram / rotation (svd.cuh) unless disabled; tensor-map row coordinates are int32
   const bool svd_tma = getenv("HEFF_SVD_NO_TMA") == nullptr && nblk * R < (1ll << 31);
   const int64_t gram_chunks = (R + 127) / 128;  // 128-row chunks in both Gram kernels
@@ -2400,6 +2415,63 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
 // NEXT-2 x NEXT-3 (reading R24): Psi is block diagonal over the centre-bond charge; every
 // block is split by heff_svd_split (dense Jacobi on the block), one truncation runs over the
 // union of the blocks' spectra, the new bond is ordered by (charge, descending value).
+// Process-lifetime pool of host worker threads (never joined: a leaked singleton) for the
+// independent charge blocks of the U(1) split.  Each worker has its own CUDA stream and its
+// own thread-local split arenas, so several blocks are split on the GPU at once.
+static constexpr int kBlockWorkers = 4;
+class BlockPool {
+ public:
+  struct Batch {
+    std::mutex mu;
+    std::condition_variable cv;
+    int remaining = 0;
+  };
+  static BlockPool& get() {
+    static BlockPool* pool = new BlockPool();
+    return *pool;
+  }
+  // run every task on the workers; returns when all have finished
+  void run(std::vector<std::function<void(cudaStream_t)>>& tasks) {
+    Batch b;
+    b.remaining = (int)tasks.size();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (auto& t : tasks) q_.push_back({&t, &b});
+    }
+    cv_.notify_all();
+    std::unique_lock<std::mutex> lk(b.mu);
+    b.cv.wait(lk, [&] { return b.remaining == 0; });
+  }
+
+ private:
+  struct Item {
+    std::function<void(cudaStream_t)>* fn;
+    Batch* batch;
+  };
+  BlockPool() {
+    for (int i = 0; i < kBlockWorkers; ++i) std::thread([this] { loop(); }).detach();
+  }
+  void loop() {
+    cudaStream_t ws = nullptr;
+    for (;;) {
+      Item it;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return !q_.empty(); });
+        it = q_.front();
+        q_.erase(q_.begin());
+      }
+      if (!ws) cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking);
+      (*it.fn)(ws);
+      std::lock_guard<std::mutex> lk(it.batch->mu);
+      if (--it.batch->remaining == 0) it.batch->cv.notify_all();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::vector<Item> q_;
+};
+
 struct SvdQnArena {
   double* buf = nullptr;
   size_t bytes = 0;
@@ -2478,29 +2550,47 @@ extern "C" int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const 
   CK(cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (h_flag) return set_err(HEFF_EINVAL, "heff_svd_split_qn: psi has entries outside its charge blocks");
-  // one dense split per block (all values kept; numerical zeros per the block's own rank rule)
+  // one dense split per block (all values kept; numerical zeros per the block's own rank rule),
+  // the blocks spread over the worker pool's streams, largest first
   std::vector<int64_t> nc(ns, 0);
   std::vector<double> sv_host(tot_s, 0.0);
-  int sweeps_max = 0;
-  for (int si = 0; si < ns; ++si) {
+  std::vector<int> rc(ns, HEFF_OK), swp(ns, 0);
+  std::vector<std::string> msg(ns);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  auto block_task = [&](int si, cudaStream_t ws) {
+    cudaSetDevice(dev);
     const int* d_rows = d_idx + off_idx[si];
     const int* d_cols = d_rows + Mc[si];
-    svd_qn_gather_kernel<<<ew_grid(Mc[si] * Nc[si]), 256, 0, s>>>(psi, N, d_rows, d_cols, Mc[si], Nc[si],
-                                                                  d_blk + off_blk[si]);
-    CK(cudaGetLastError());
+    svd_qn_gather_kernel<<<ew_grid(Mc[si] * Nc[si]), 256, 0, ws>>>(psi, N, d_rows, d_cols, Mc[si], Nc[si],
+                                                                   d_blk + off_blk[si]);
     int64_t nk = 0;
     double e = 0.0;
-    int swp = 0;
-    const int r = heff_svd_split(Mc[si], Nc[si], d_blk + off_blk[si], nullptr, dir, d_qc + off_q[si], d_sc + off_s[si],
-                                 d_cc + off_c[si], &nk, &e, &swp, stream);
-    if (r == HEFF_EZERO) continue;  // an all-zero block contributes nothing
-    if (r != HEFF_OK) return r;
-    nc[si] = nk;
-    sweeps_max = std::max(sweeps_max, swp);
-    CK(cudaMemcpyAsync(sv_host.data() + off_s[si], d_sc + off_s[si], sizeof(double) * kc[si], cudaMemcpyDeviceToHost,
-                       s));
+    int r = heff_svd_split(Mc[si], Nc[si], d_blk + off_blk[si], nullptr, dir, d_qc + off_q[si], d_sc + off_s[si],
+                           d_cc + off_c[si], &nk, &e, &swp[si], ws);
+    if (r == HEFF_OK) {
+      nc[si] = nk;
+      if (cudaMemcpyAsync(sv_host.data() + off_s[si], d_sc + off_s[si], sizeof(double) * kc[si],
+                          cudaMemcpyDeviceToHost, ws) != cudaSuccess || cudaStreamSynchronize(ws) != cudaSuccess)
+        r = set_err(HEFF_ECUDA, "heff_svd_split_qn: block copy failed");
+    }
+    if (r == HEFF_EZERO) r = HEFF_OK;  // an all-zero block contributes nothing
+    rc[si] = r;
+    if (r != HEFF_OK) msg[si] = heff_last_error();
+  };
+  std::vector<int> order(ns);
+  for (int si = 0; si < ns; ++si) order[si] = si;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return Mc[x] * Nc[x] > Mc[y] * Nc[y]; });
+  if (ns > 1 && getenv("HEFF_SVD_QN_SERIAL") == nullptr) {
+    std::vector<std::function<void(cudaStream_t)>> tasks;
+    for (int si : order) tasks.push_back([&, si](cudaStream_t ws) { block_task(si, ws); });
+    BlockPool::get().run(tasks);
+  } else {
+    for (int si : order) block_task(si, s);
   }
-  CK(cudaStreamSynchronize(s));
+  for (int si = 0; si < ns; ++si)
+    if (rc[si] != HEFF_OK) return set_err(rc[si], "%s", msg[si].c_str());
+  const int sweeps_max = *std::max_element(swp.begin(), swp.end());
   struct Cand { double v; int si; int j; };
   std::vector<Cand> cand;
   for (int si = 0; si < ns; ++si)
