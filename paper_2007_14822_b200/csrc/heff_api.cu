@@ -2305,6 +2305,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   const char* it_env = getenv("HEFF_SVD_INNER_THRESH");
   const double inner_thresh = it_env ? atof(it_env) : 0.0;  // default: one inner sweep throughout
   int inner = inner_thresh > 1.0 ? kSvdMaxInnerSweeps : 1;
+  if (const char* f = getenv("HEFF_SVD_INNER_FORCE")) inner = atoi(f);
   const bool sort_cols = getenv("HEFF_SVD_NO_SORT") == nullptr;
   std::vector<double> nrm(nblk * kSvdB);
   std::vector<int> order(nblk * kSvdB);
@@ -2351,6 +2352,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     double maxoff;
     memcpy(&maxoff, &offbits, sizeof maxoff);
     inner = maxoff < inner_thresh ? kSvdMaxInnerSweeps : 1;  // see svd.cuh kSvdMaxInnerSweeps
+    if (const char* f = getenv("HEFF_SVD_INNER_FORCE")) inner = atoi(f);  // profiling knob
   }
   if (sweeps_out) *sweeps_out = sweeps;
   if (!converged) return set_err(HEFF_ENOCONV, "heff_svd_split: Jacobi did not converge in %d sweeps", kSvdMaxSweeps);

@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kSvdGramThreads, 2) svd_gram_kernel(const doub
 // 2x2 block (pair k rows, pair k' columns) of G <- J^T G J depends only on its old values,
 // so a thread updates a whole block at once (the diagonal blocks get the exact rotated
 // 2x2 values), and Q <- Q J by columns.  Output: Qg[p] (row-major 32x32), flag[p].
-constexpr int kSvdEigThreads = 256;
+constexpr int kSvdEigThreads = 288;  // 8 warps of 2x2-block updates + 1 warp for the next round's rotations
 
 // FP64 rsqrt / reciprocal: MUFU approximation + two Newton steps (full precision for the
 // normal, positive arguments used here; any rounding in t only leaves a slightly larger
@@ -233,7 +233,7 @@ struct SvdRot {
 // t = sign(th) om / (|th| + sqrt(th^2 + om^2)), th = aqq - app, om = 2 apq
 __device__ __forceinline__ SvdRot svd_make_rot(double app, double aqq, double apq, bool active, double tol) {
   SvdRot r{1.0, 0.0, app, aqq, 0};
-  if (active && fabs(apq) > tol * sqrt(app * aqq)) {
+  if (active && apq * apq > (tol * tol) * (app * aqq)) {  // |apq| > tol sqrt(app aqq), no sqrt
     const double th = aqq - app, om = 2.0 * apq;
     const double h2 = fma(th, th, om * om);
     const double den = fabs(th) + h2 * svd_rsqrt(h2);
@@ -271,9 +271,12 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
                                                                      int* __restrict__ stat_nrot) {
   __shared__ double Gs[2][kSvdPair][kSvdPair + 1];   // ping-pong: round rr reads Gs[rr&1], writes Gs[~]
   __shared__ double Q[kSvdPair][kSvdPair + 1];
-  __shared__ SvdRot s_rot[2][16];
+  __shared__ double2 s_cs[2][16], s_nn[2][16];       // (c, s) and the rotated diagonal per pair
+  __shared__ int s_on[2][16];
   __shared__ int s_neg[kSvdPair];
   __shared__ unsigned char s_pa[31][16], s_pb[31][16], s_kof[31][kSvdPair], s_hi[31][kSvdPair];
+  __shared__ uint32_t s_pk1[31][16], s_pk2[31][16];   // per (round, pair of the next round): index chains
+  __shared__ unsigned char s_pk3[31][16];
   __shared__ int s_any[kSvdMaxInnerSweeps];          // did inner sweep i rotate anything
   __shared__ double s_off[kSvdEigThreads / 32];
   const int p = blockIdx.x;
@@ -299,6 +302,15 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
     s_hi[rr][b] = 1;
   }
   __syncthreads();
+  for (int e = tid; e < 31 * 16; e += blockDim.x) {  // the dependent index lookups of the rotation warp
+    const int rr = e >> 4, t = e & 15, r1 = (rr + 1) % 31;
+    const int a = s_pa[r1][t], b = s_pb[r1][t];
+    const int ka = s_kof[rr][a], kb = s_kof[rr][b];
+    s_pk1[rr][t] = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)ka << 16) | ((uint32_t)kb << 24);
+    s_pk2[rr][t] = (uint32_t)s_pa[rr][ka] | ((uint32_t)s_pb[rr][ka] << 8) | ((uint32_t)s_pa[rr][kb] << 16) |
+                   ((uint32_t)s_pb[rr][kb] << 24);
+    s_pk3[rr][t] = (unsigned char)(s_hi[rr][a] | (s_hi[rr][b] << 1));
+  }
   if (tid < kSvdPair) s_neg[tid] = !(Gs[0][tid][tid] > negl);
   __syncthreads();
   double off = 0.0;
@@ -322,9 +334,24 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
   // Cyclic two-sided Jacobi, one barrier per round: in round rr every thread writes its
   // 2x2 block of the rotated G into the other buffer and updates Q, while threads 0..15
   // already compute round rr+1's rotations from the OLD G and round rr's rotations.
+  // Rotations live as (c, s) pairs -- the identity (1, 0) for a skipped pair, so the block
+  // update is branch-free -- plus the exact rotated diagonal (na, nb) and an on flag.
+  auto put_rot = [&](int buf, int k, const SvdRot& r) {
+    s_cs[buf][k] = make_double2(r.c, r.s);
+    s_nn[buf][k] = make_double2(r.na, r.nb);
+    s_on[buf][k] = r.on;
+  };
+  auto rot2 = [](double& x00, double& x01, double& x10, double& x11, double2 rk, double2 rkk) {
+    const double y00 = rkk.x * x00 - rkk.y * x01, y01 = rkk.y * x00 + rkk.x * x01;   // columns (pair kk)
+    const double y10 = rkk.x * x10 - rkk.y * x11, y11 = rkk.y * x10 + rkk.x * x11;
+    x00 = rk.x * y00 - rk.y * y10;                                                  // rows (pair k)
+    x10 = rk.y * y00 + rk.x * y10;
+    x01 = rk.x * y01 - rk.y * y11;
+    x11 = rk.y * y01 + rk.x * y11;
+  };
   if (tid < 16) {
     const int a = s_pa[0][tid], b = s_pb[0][tid];
-    s_rot[0][tid] = svd_make_rot(Gs[0][a][a], Gs[0][b][b], Gs[0][a][b], !s_neg[a] && !s_neg[b], tol);
+    put_rot(0, tid, svd_make_rot(Gs[0][a][a], Gs[0][b][b], Gs[0][a][b], !s_neg[a] && !s_neg[b], tol));
   }
   if (tid < kSvdMaxInnerSweeps) s_any[tid] = 0;
   __syncthreads();
@@ -334,48 +361,46 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
     const int sweep = it / 31;
     double(*Go)[kSvdPair + 1] = Gs[cur];
     double(*Gn)[kSvdPair + 1] = Gs[nxt];
-    {  // this thread's 2x2 block (pair k rows, pair kk columns)
+    if (tid < 256) {  // this thread's 2x2 block (pair k rows, pair kk columns)
       const int k = tid >> 4, kk = tid & 15;
       const int a = s_pa[rr][k], b = s_pb[rr][k], a2 = s_pa[rr][kk], b2 = s_pb[rr][kk];
-      const SvdRot rk = s_rot[cur][k], rkk = s_rot[cur][kk];
       if (k == kk) {
-        Gn[a][a] = rk.na;
-        Gn[b][b] = rk.nb;
-        Gn[a][b] = Gn[b][a] = rk.on ? 0.0 : Go[a][b];
+        const double2 nn = s_nn[cur][k];
+        Gn[a][a] = nn.x;
+        Gn[b][b] = nn.y;
+        Gn[a][b] = Gn[b][a] = s_on[cur][k] ? 0.0 : Go[a][b];
       } else {
         double x00 = Go[a][a2], x01 = Go[a][b2], x10 = Go[b][a2], x11 = Go[b][b2];
-        svd_rot_block(x00, x01, x10, x11, rk, rkk);
+        rot2(x00, x01, x10, x11, s_cs[cur][k], s_cs[cur][kk]);
         Gn[a][a2] = x00; Gn[a][b2] = x01; Gn[b][a2] = x10; Gn[b][b2] = x11;
       }
-      if (tid < 16 && s_rot[cur][tid].on) s_any[sweep] = 1;
+      if (tid < 16 && s_on[cur][tid]) s_any[sweep] = 1;
     }
-    for (int task = tid; task < 32 * 16; task += blockDim.x) {  // Q <- Q J (columns, in place)
+    for (int task = tid; task < 32 * 16; task += 256) {  // Q <- Q J (columns, in place)
+      if (tid >= 256) break;
       const int k = task & 15, r = task >> 4;
-      const SvdRot rk = s_rot[cur][k];
-      if (!rk.on) continue;
+      if (!s_on[cur][k]) continue;
+      const double2 rk = s_cs[cur][k];
       const int a = s_pa[rr][k], b = s_pb[rr][k];
       const double qa = Q[r][a], qb = Q[r][b];
-      Q[r][a] = rk.c * qa - rk.s * qb;
-      Q[r][b] = rk.s * qa + rk.c * qb;
+      Q[r][a] = rk.x * qa - rk.y * qb;
+      Q[r][b] = rk.y * qa + rk.x * qb;
     }
-    if (tid < 16 && it + 1 < total_rounds) {  // round rr+1's rotation from the rotated entries
-      const int r1 = (rr + 1) % 31;
-      const int a = s_pa[r1][tid], b = s_pb[r1][tid];
-      auto rotated = [&](int x, int y) {  // (J^T G J)[x][y] of round rr from the old G
-        const int kx = s_kof[rr][x], ky = s_kof[rr][y];
-        const SvdRot rx = s_rot[cur][kx], ry = s_rot[cur][ky];
-        if (kx == ky) {
-          if (x == y) return s_hi[rr][x] ? rx.nb : rx.na;
-          return rx.on ? 0.0 : Go[x][y];
-        }
-        const int ax = s_pa[rr][kx], bx = s_pb[rr][kx], ay = s_pa[rr][ky], by = s_pb[rr][ky];
-        double x00 = Go[ax][ay], x01 = Go[ax][by], x10 = Go[bx][ay], x11 = Go[bx][by];
-        svd_rot_block(x00, x01, x10, x11, rx, ry);
-        const int hx = s_hi[rr][x], hy = s_hi[rr][y];
-        return hx ? (hy ? x11 : x10) : (hy ? x01 : x00);
-      };
-      const double app = rotated(a, a), aqq = rotated(b, b), apq = rotated(a, b);
-      s_rot[nxt][tid] = svd_make_rot(app, aqq, apq, !s_neg[a] && !s_neg[b], tol);
+    const int pl = tid - 256;  // the rotation warp: round rr+1's rotations from the rotated entries
+    if (pl >= 0 && pl < 16 && it + 1 < total_rounds) {
+      const uint32_t p1 = s_pk1[rr][pl], p2 = s_pk2[rr][pl];
+      const int hh = s_pk3[rr][pl];
+      const int a = p1 & 255, b = (p1 >> 8) & 255, ka = (p1 >> 16) & 255, kb = p1 >> 24;
+      const int ax = p2 & 255, bx = (p2 >> 8) & 255, ay = (p2 >> 16) & 255, by = p2 >> 24;
+      const int hx = hh & 1, hy = hh >> 1;
+      const double2 nna = s_nn[cur][ka], nnb = s_nn[cur][kb];
+      const double app = hx ? nna.y : nna.x;                   // rotated diagonals: exact values
+      const double aqq = hy ? nnb.y : nnb.x;
+      // rotated off-diagonal (a, b): a and b sit in different pairs of round rr
+      double x00 = Go[ax][ay], x01 = Go[ax][by], x10 = Go[bx][ay], x11 = Go[bx][by];
+      rot2(x00, x01, x10, x11, s_cs[cur][ka], s_cs[cur][kb]);
+      const double apq = hx ? (hy ? x11 : x10) : (hy ? x01 : x00);
+      put_rot(nxt, pl, svd_make_rot(app, aqq, apq, !s_neg[a] && !s_neg[b], tol));
     }
     __syncthreads();
     if (rr == 30 && !s_any[sweep]) break;  // end of an inner sweep that rotated nothing
