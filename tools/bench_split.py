@@ -10,6 +10,7 @@ from __future__ import annotations
 import argparse
 import json
 import sys
+import time
 from pathlib import Path
 
 import torch
@@ -72,8 +73,27 @@ def run(m: int, kind: str, reps: int, maxdim: int, direction: int):
                 stream_GBps=bytes_per_sweep * sweeps[-1] / (ts[len(ts) // 2] * 1e-3) / 1e9)
 
 
+def oracle_time(m: int, kind: str, maxdim: int, direction: int):
+    """The CPU oracle (oracle/split.py: LAPACK SVD + the truncation rule) on the same Psi,
+    all host cores -- the reported baseline beside the GPU number."""
+    import os
+    from oracle import split as osplit
+    dev = torch.device("cuda:0")
+    if kind == "random":
+        Psi = C.random_psi(1000 + m, (m, 2, 2, m)).numpy().reshape(2 * m, 2 * m)
+    elif kind == "dmrg":
+        Psi = dmrg_psi(m, dev).cpu().numpy()
+        Psi = Psi.reshape(Psi.shape[0] * Psi.shape[1], -1)
+    else:
+        Psi = C.graded_matrix(2 * m, 2 * m, 7, 12.0)
+    t0 = time.perf_counter()
+    osplit.svd_split(Psi, maxdim=maxdim, direction=direction)
+    return time.perf_counter() - t0, os.cpu_count()
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--oracle", action="store_true", help="also time the CPU oracle (C4 takes minutes)")
     ap.add_argument("--configs", default="c1,c2,c3,c4")
     ap.add_argument("--kinds", default="random,graded")
     ap.add_argument("--reps", type=int, default=3)
@@ -85,6 +105,9 @@ def main():
         for kind in a.kinds.split(","):
             for d in (0, 1):
                 row = dict(config=c, **run(m, kind, a.reps if m < 4096 else max(1, a.reps - 1), m, d))
+                if a.oracle and d == 0:
+                    t, cores = oracle_time(m, kind, m, d)
+                    row.update(oracle_s=t, oracle_cores=cores, gpu_speedup=t / (row["ms"] * 1e-3))
                 print(json.dumps(row), flush=True)
                 rows.append(row)
     if a.out:
