@@ -293,3 +293,30 @@ def test_c_abi_demo_runs(dev, tmp_path):
     assert r.returncode == 0, r.stderr
     out = subprocess.run([str(tmp_path / "heff_demo")], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
+
+
+def test_lanczos_c4_bench_config_properties(dev, orc):
+    """The bench workload (C4, m = 4096) is too large for the oracle's Lanczos; check what holds
+    at any size: alpha_1 = <v1|H|v1> against the oracle's matvec on sampled rows, the Ritz value
+    equals the Rayleigh quotient of the returned vector, and the residual ||H x - theta x||
+    equals libheff's estimate beta_j |y_j[last]| (exact arithmetic identity)."""
+    from paper_2007_14822_b200 import Heff
+    x = C.make("c4", device=dev)
+    psi0 = x.psi / torch.linalg.norm(x.psi)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        v = psi0.clone()
+        r = h.lanczos_ground(v, max_iter=4)
+        hx = h.apply(v)
+        hv1 = h.apply(psi0)
+        torch.cuda.synchronize()
+    theta_rq = float(torch.vdot(v.reshape(-1), hx.reshape(-1)))
+    assert abs(theta_rq - r.energy) <= 1e-9 * abs(r.energy)
+    res = float(torch.linalg.norm(hx - r.energy * v))
+    assert abs(res - r.resid) <= 1e-6 * max(res, 1e-12) + 1e-10
+    # alpha_1 vs the oracle on sampled output rows a' (each row is independent in order A)
+    L, W1, W2, R = (t.cpu().numpy() for t in (x.L, x.W1, x.W2, x.R))
+    p0 = psi0.cpu().numpy()
+    for a in (0, 1777, 4095):
+        ref = orc.heff_apply(L, W1, W2, R, p0, rows=(a, a + 1))[0]
+        assert rel(hv1[a].cpu().numpy(), ref) <= MATVEC_TOL
+    assert abs(float(torch.vdot(psi0.reshape(-1), hv1.reshape(-1))) - r.alpha[0]) <= 1e-10 * abs(r.alpha[0])
