@@ -666,19 +666,23 @@ __global__ void __launch_bounds__((kSvdTmaRotWarps + 1) * 32) svd_rotate_tma_ker
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
-      for (int n = 0; n < 4; ++n) qf[kk][n] = __ldg(q + (8 * t + kk) * kSvdPair + 8 * n + g);
+      for (int n = 0; n < 4; ++n)  // k-slice kk of lane t = Y column 4t + kk (I) or 16 + 4t + kk - 4 (J)
+        qf[kk][n] = __ldg(q + (kk < 4 ? 4 * t + kk : 12 + 4 * t + kk) * kSvdPair + 8 * n + g);
     const int2 pr = pairs[p];
     double* XI = Xb + (int64_t)pr.x * R * kSvdB;
     double* XJ = Xb + (int64_t)pr.y * R * kSvdB;
     for (int64_t ch = g0; ch < g1; ++ch) {
       mbar_wait(&full[stage], phase);
-      const uint32_t buf = sbase + stage * kStageBytes + (t < 2 ? 0 : kStageBytes / 2);
+      // every quarter-warp reads one buffer at 8 distinct swizzled chunks: conflict-free
+      const uint32_t bufI = sbase + stage * kStageBytes, bufJ = bufI + kStageBytes / 2;
       double y[2][8];
 #pragma unroll
       for (int grp = 0; grp < 2; ++grp) {
         const int rl = warp * 16 + grp * 8 + g;
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) lds128(y[grp][2 * qq], y[grp][2 * qq + 1], svd_swz(buf, rl, (t & 1) * 4 + qq));
+        lds128(y[grp][0], y[grp][1], svd_swz(bufI, rl, 2 * t));
+        lds128(y[grp][2], y[grp][3], svd_swz(bufI, rl, 2 * t + 1));
+        lds128(y[grp][4], y[grp][5], svd_swz(bufJ, rl, 2 * t));
+        lds128(y[grp][6], y[grp][7], svd_swz(bufJ, rl, 2 * t + 1));
       }
       fence_proxy_async();
       __syncwarp();
@@ -766,7 +770,9 @@ __global__ void __launch_bounds__((kSvdTmaGramWarps + 1) * 32) svd_gram_tma_kern
       double v[4][4];
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
-        const int rl = warp * 16 + ks * 4 + t;
+        // the 4 rows of k-step ks: 8-row group ks/2, rows {0,1,4,5} + 2 (ks&1) of it, so the
+        // swizzled chunks 2g', 2g'+1 of a quarter-warp land in 8 distinct bank groups
+        const int rl = warp * 16 + (ks >> 1) * 8 + 2 * (ks & 1) + (t & 1) + 4 * (t >> 1);
         const bool ok = ch * kSvdTmaGramRows + rl < R;
         double a, b, c, d;
         lds128(a, b, svd_swz(buf, rl, 2 * (g & 3)));
