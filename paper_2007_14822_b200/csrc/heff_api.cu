@@ -2219,8 +2219,21 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   const std::vector<int2> sched = svd_pair_schedule((int)nblk);
   CK(cudaMemcpyAsync(d_pairs, sched.data(), sizeof(int2) * sched.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(d_maxoff, 0, bStat, s));
-  // ||Psi||_F^2 (deterministic two-pass) and the packed working copy
-  svd_sumsq_partial_kernel<<<red_blocks, 256, 0, s>>>(psi, M * N, d_red);
+  // Scale invariance: the working copy is scaled by a power of two (exact) that brings
+  // max |Psi| into [1, 2), so no Gram product under- or overflows; S is scaled back.
+  svd_maxabs_partial_kernel<<<red_blocks, 256, 0, s>>>(psi, M * N, d_red);
+  std::vector<double> hmax(red_blocks);
+  CK(cudaMemcpyAsync(hmax.data(), d_red, sizeof(double) * red_blocks, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  double maxabs = 0.0;
+  for (double v : hmax) {
+    if (!std::isfinite(v)) return set_err(HEFF_EINVAL, "heff_svd_split: psi has a non-finite entry");
+    maxabs = std::max(maxabs, v);
+  }
+  if (!(maxabs > 0.0)) return set_err(HEFF_EZERO, "heff_svd_split: psi is zero");
+  const double pscale = std::ldexp(1.0, -std::ilogb(maxabs));
+  // ||scale Psi||_F^2 (deterministic two-pass) and the packed working copy
+  svd_sumsq_partial_kernel<<<red_blocks, 256, 0, s>>>(psi, M * N, pscale, d_red);
   svd_sum_kernel<<<1, 32, 0, s>>>(d_red, red_blocks, d_red + red_blocks);
   // optional phase timing (HEFF_SVD_TIMING=1: LQ, Jacobi sweeps, extraction -> stderr)
   const bool timing = getenv("HEFF_SVD_TIMING") != nullptr;
@@ -2246,7 +2259,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     std::stable_sort(rp.begin(), rp.end(), [&](int a, int b) { return rn[a] > rn[b]; });
     CK(cudaMemcpyAsync(d_rowperm, rp.data(), sizeof(int) * R, cudaMemcpyHostToDevice, s));
     svd_gather_rows_kernel<<<dim3((unsigned)std::min<int64_t>((colsP + 255) / 256, 64), (unsigned)std::min<int64_t>(R, 65535)), 256, 0, s>>>(
-        src, d_P, R, colsP, d_rowperm);
+        src, d_P, R, colsP, d_rowperm, pscale);
     CK(cudaGetLastError());
     int nl = 0;
     for (int64_t j = 0; j < kmin; j += kLqNb) {
@@ -2284,10 +2297,10 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     }
     lq_pack_lower_kernel<<<ew_grid(nblk * kSvdB * R), 256, 0, s>>>(d_P, colsP, Xb, R, kmin, nblk);
   } else if (dir == 0) {
-    svd_pack_kernel<<<ew_grid(nblk * kSvdB * R), 256, 0, s>>>(psi, Xb, R, ncols, nblk);
+    svd_pack_kernel<<<ew_grid(nblk * kSvdB * R), 256, 0, s>>>(psi, Xb, R, ncols, nblk, pscale);
   } else {
     dim3 grid((unsigned)((R + 31) / 32), (unsigned)(nblk * kSvdB / 32));
-    svd_pack_t_kernel<<<grid, dim3(32, 8), 0, s>>>(psi, Xb, R, ncols);
+    svd_pack_t_kernel<<<grid, dim3(32, 8), 0, s>>>(psi, Xb, R, ncols, pscale);
   }
   CK(cudaGetLastError());
   double fro2 = 0.0;
@@ -2373,7 +2386,9 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   int64_t n = 0;
   double err = 0.0;
   truncate_rule(sv.data(), kmin, cutoff, maxdim, mindim, &n, &err);
-  CK(cudaMemcpyAsync(S, sv.data(), sizeof(double) * kmin, cudaMemcpyHostToDevice, s));
+  std::vector<double> sv_out(kmin);  // back to Psi's scale
+  for (int64_t i = 0; i < kmin; ++i) sv_out[i] = sv[i] / pscale;
+  CK(cudaMemcpyAsync(S, sv_out.data(), sizeof(double) * kmin, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(d_perm, order.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(d_skept, sv.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
   svd_sign_kernel<<<(unsigned)n, 256, 0, s>>>(Xb, R, d_perm, d_skept, d_scale, d_rowperm);

@@ -49,25 +49,26 @@ constexpr int kSvdMaxInnerSweeps = 12;
 // ---------------------------------------------------------------- packing
 // Moving right: X = Psi [R][ncols] -> Xb (zero beyond ncols).
 __global__ void svd_pack_kernel(const double* __restrict__ psi, double* __restrict__ Xb, int64_t R, int64_t ncols,
-                                int64_t nblk) {
+                                int64_t nblk, double scale) {
   const int64_t total = nblk * R * kSvdB;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int j = (int)(e & (kSvdB - 1));
     const int64_t rb = e >> 4;
     const int64_t blk = rb / R, r = rb - blk * R;
     const int64_t c = blk * kSvdB + j;
-    Xb[e] = c < ncols ? psi[r * ncols + c] : 0.0;
+    Xb[e] = c < ncols ? scale * psi[r * ncols + c] : 0.0;
   }
 }
 
 // Moving left: X = Psi^T, Psi is [ncols][R] -> Xb[blk][r][16] = Psi[blk*16+j][r]; 32x32 tiles.
-__global__ void svd_pack_t_kernel(const double* __restrict__ psi, double* __restrict__ Xb, int64_t R, int64_t ncols) {
+__global__ void svd_pack_t_kernel(const double* __restrict__ psi, double* __restrict__ Xb, int64_t R, int64_t ncols,
+                                  double scale) {
   __shared__ double tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
   for (int k = ty; k < 32; k += 8) {
     const int64_t c = c0 + k, r = r0 + tx;
-    tile[k][tx] = (c < ncols && r < R) ? psi[c * R + r] : 0.0;
+    tile[k][tx] = (c < ncols && r < R) ? scale * psi[c * R + r] : 0.0;
   }
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
@@ -76,12 +77,34 @@ __global__ void svd_pack_t_kernel(const double* __restrict__ psi, double* __rest
   }
 }
 
-// ---------------------------------------------------------------- sum of squares (deterministic)
-__global__ void svd_sumsq_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
+// ---------------------------------------------------------------- max |x| and sum of squares (deterministic)
+// part[blockIdx.x] = max |x| over the block's grid-stride range (NaN propagates)
+__global__ void svd_maxabs_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
+  __shared__ double red[256];
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = fabs(x[i]);
+    m = (v > m || v != v) ? v : m;
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      const double o = red[threadIdx.x + w];
+      if (o > red[threadIdx.x] || o != o) red[threadIdx.x] = o;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// sum of (scale x)^2 -- scale is a power of two that brings max |x| into [1, 2)
+__global__ void svd_sumsq_partial_kernel(const double* __restrict__ x, int64_t n, double scale,
+                                         double* __restrict__ part) {
   __shared__ double red[256];
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = x[i];
+    const double v = scale * x[i];
     s = fma(v, v, s);
   }
   red[threadIdx.x] = s;
@@ -587,11 +610,11 @@ __global__ void svd_rownorm2_kernel(const double* __restrict__ A, int64_t rows, 
 
 // dst row r = src row perm[r] (row-major, cols per row)
 __global__ void svd_gather_rows_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t rows,
-                                       int64_t cols, const int* __restrict__ perm) {
+                                       int64_t cols, const int* __restrict__ perm, double scale) {
   for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
     const double* sr = src + (int64_t)perm[row] * cols;
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x)
-      dst[row * cols + c] = sr[c];
+      dst[row * cols + c] = scale * sr[c];
   }
 }
 

@@ -150,3 +150,46 @@ def test_split_c4_size_properties():
     assert resid2 == pytest.approx(got.trunc_err * tot, rel=1e-8)
     # sum_i s_i^2 = ||Psi||_F^2: n values each within 1e-12 ||Psi||_F (R23) -> 2 sqrt(n) 1e-12
     assert tot == pytest.approx(torch.linalg.norm(Psi).item() ** 2, rel=2e-12 * (2 * m) ** 0.5)
+
+
+@pytest.mark.parametrize("direction", [0, 1])
+def test_split_identity_and_orthogonal_inputs(direction):
+    """Psi = I (all singular values 1, already orthogonal columns) and a random orthogonal
+    Psi: every s_i = 1, U.C reconstructs Psi; truncating to 10 keeps error 1 - 10/n."""
+    heff = _gpu()
+    n = 96
+    for Psi in (np.eye(n), np.linalg.qr(_rand((n, n), 8))[0]):
+        got = heff.svd_split(torch.from_numpy(Psi).to(DEV), direction=direction)
+        np.testing.assert_allclose(got.S.cpu().numpy(), np.ones(n), atol=1e-13)
+        Q, Cc = got.Q.cpu().numpy(), got.C.cpu().numpy()
+        np.testing.assert_allclose(Q @ Cc if direction == 0 else Cc @ Q, Psi, atol=1e-13)
+        t = heff.svd_split(torch.from_numpy(Psi).to(DEV), maxdim=10, direction=direction)
+        assert t.n == 10 and t.trunc_err == pytest.approx(1 - 10 / n, rel=1e-12)
+
+
+@pytest.mark.parametrize("direction", [0, 1])
+def test_split_rank_deficient(direction):
+    """rank-3 Psi (64 x 80): three singular values, the rest numerical zeros never kept (R21)."""
+    rng = np.random.default_rng(12)
+    Psi = rng.standard_normal((64, 3)) @ rng.standard_normal((3, 80))
+    got, ref = _compare(Psi, direction=direction)
+    assert got.n == 3
+
+
+@pytest.mark.parametrize("scale", [1e-150, 1e150])
+def test_split_scale_invariance(scale):
+    """The Jacobi tolerances are relative: Psi * 1e-150 and Psi * 1e150 give the scaled spectrum
+    and the same singular vectors (no underflow/overflow in the Gram products)."""
+    heff = _gpu()
+    Psi = _graded(80, 64, 3, decades=6.0)
+    a = heff.svd_split(torch.from_numpy(Psi).to(DEV), maxdim=20)
+    b = heff.svd_split(torch.from_numpy(Psi * scale).to(DEV), maxdim=20)
+    np.testing.assert_allclose(b.S.cpu().numpy() / scale, a.S.cpu().numpy(), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(b.Q.cpu().numpy(), a.Q.cpu().numpy(), atol=1e-10)
+    assert a.n == b.n
+
+
+@pytest.mark.parametrize("shape", [(1, 300), (300, 1), (2, 700), (700, 3)])
+@pytest.mark.parametrize("direction", [0, 1])
+def test_split_extreme_aspect(shape, direction):
+    _compare(_rand(shape, 41 + shape[0]), direction=direction)
