@@ -2124,6 +2124,8 @@ static int svd_init_once() {
                                                    kSvdTmaRotSmem));
   g_svd_tgram_occ = std::max(1, g_svd_tgram_occ);
   g_svd_trot_occ = std::max(1, g_svd_trot_occ);
+  CK(cudaFuncSetAttribute(svd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(sizeof(double) * ((size_t)kSvdSmallMax * kSvdSmallMax + 3 * kSvdSmallMax))));
   done.store(true, std::memory_order_release);
   return HEFF_OK;
 }
@@ -2143,8 +2145,29 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   const int64_t R = dir == 0 ? M : N;          // rows of X
   const int64_t kmin = std::min(M, N);
   const int64_t colsP = dir == 0 ? N : M;      // columns of the working matrix P (Psi or Psi^T)
-  // LQ preconditioning (lq.cuh): Jacobi on the k = min(M,N) columns of L instead of P
   CKR(svd_init_once());
+  if (R <= kSvdSmallDispatch && colsP <= kSvdSmallDispatch && getenv("HEFF_SVD_NO_SMALL") == nullptr) {
+    // small matrix: the whole split in one CTA (svd_small_kernel)
+    static thread_local double* d_info = nullptr;
+    if (!d_info) CK(cudaMalloc(&d_info, 4 * sizeof(double)));
+    const int64_t ncp = colsP + (colsP & 1);
+    const size_t smem = sizeof(double) * ((size_t)ncp * R + 3 * kSvdSmallMax);
+    svd_small_kernel<<<1, kSvdSmallThreads, smem, s>>>(psi, (int)M, (int)N, dir, cutoff, maxdim, mindim, Qout, S, Cout,
+                                                       d_info);
+    CK(cudaGetLastError());
+    double info[4];
+    CK(cudaMemcpyAsync(info, d_info, sizeof info, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (info[3] == 1.0) return set_err(HEFF_EZERO, "heff_svd_split: psi is zero");
+    if (info[3] == 2.0) return set_err(HEFF_EINVAL, "heff_svd_split: psi has a non-finite entry");
+    if (info[3] == 3.0) return set_err(HEFF_ENOCONV, "heff_svd_split: Jacobi did not converge in %d sweeps",
+                                       kSvdSmallMaxSweeps);
+    *n_kept = (int64_t)info[0];
+    *trunc_err = info[1];
+    if (sweeps_out) *sweeps_out = (int)info[2];
+    return HEFF_OK;
+  }
+  // LQ preconditioning (lq.cuh): Jacobi on the k = min(M,N) columns of L instead of P
   const bool precond = getenv("HEFF_SVD_NO_PRECOND") == nullptr && kmin > kSvdPair &&
                        (colsP + g_lq_grid - 1) / g_lq_grid <= kLqMaxCols;
   const int64_t ncols = precond ? kmin : colsP;  // columns of X (orthogonalised)

@@ -883,4 +883,221 @@ __global__ void svd_qn_scatter_kernel(const double* __restrict__ Qc, const doubl
   }
 }
 
+// ---------------------------------------------------------------- small-matrix split (one CTA)
+// For X of at most kSvdSmallMax rows and columns (DMRG bonds m <= 64 at d = 2) the whole
+// split runs in ONE kernel with X resident in shared memory: scalar cyclic one-sided Jacobi
+// (circle ordering, 8 warps, one warp per column pair, lanes over rows, warp-shuffle dot
+// products), column norms, a rank sort, the truncation rule, the gauge and both factors --
+// no host round trips, no per-round launches.  Same arithmetic contract as the large path:
+// relative convergence test tol = 4 eps sqrt(R), power-of-two pre-scaling, readings R20-R22.
+constexpr int kSvdSmallMax = 128;      // shared-memory capacity of svd_small_kernel
+constexpr int kSvdSmallDispatch = 96;  // heff_svd_split uses it up to here (block path faster above: 128^2 3.5 vs 4.1 ms)
+constexpr int kSvdSmallThreads = 1024;
+constexpr int kSvdSmallMaxSweeps = 80;
+
+__device__ __forceinline__ double svd_warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// info: [0] n_kept, [1] trunc_err, [2] sweeps, [3] status (0 ok, 1 zero, 2 non-finite, 3 no convergence)
+__global__ void __launch_bounds__(kSvdSmallThreads) svd_small_kernel(const double* __restrict__ psi, int M, int N,
+                                                                    int dir, double cutoff, int64_t maxdim,
+                                                                    int64_t mindim, double* __restrict__ Qout,
+                                                                    double* __restrict__ S, double* __restrict__ Cout,
+                                                                    double* __restrict__ info) {
+  extern __shared__ double sm[];
+  const int R = dir == 0 ? M : N, nc0 = dir == 0 ? N : M;
+  const int nc = nc0 + (nc0 & 1);                 // even column count (zero pad)
+  const int kmin = M < N ? M : N;
+  double* X = sm;                                  // [nc][R] column-major: column c at X + c R
+  double* nrm = X + (int64_t)nc * R;              // [nc]
+  double* scl = nrm + kSvdSmallMax;               // [nc] 1/s with the gauge sign
+  int* perm = reinterpret_cast<int*>(scl + kSvdSmallMax);   // [nc] sorted position -> column
+  __shared__ double s_tol, s_negl, s_err, s_wmax[kSvdSmallThreads / 32];
+  __shared__ int s_any, s_n, s_sweeps;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = kSvdSmallThreads / 32;
+  // max |psi| -> exact power-of-two scale (NaN propagates)
+  double m = 0.0;
+  for (int e = tid; e < M * N; e += blockDim.x) {
+    const double v = fabs(psi[e]);
+    m = (v > m || v != v) ? v : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double w = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (w > m || w != w) ? w : m;
+  }
+  if (lane == 0) s_wmax[warp] = m;
+  __syncthreads();
+  double mxv = s_wmax[0];
+  for (int w = 1; w < nwarps; ++w) mxv = (s_wmax[w] > mxv || s_wmax[w] != s_wmax[w]) ? s_wmax[w] : mxv;
+  const double mx = mxv;
+  if (!(mx < INFINITY)) {                           // NaN or inf
+    if (tid == 0) info[3] = 2.0;
+    return;
+  }
+  if (!(mx > 0.0)) {
+    if (tid == 0) info[3] = 1.0;
+    return;
+  }
+  const double sc = ldexp(1.0, -ilogb(mx));
+  for (int e = tid; e < nc * R; e += blockDim.x) {
+    const int c = e / R, r = e - c * R;
+    double v = 0.0;
+    if (c < nc0) v = dir == 0 ? psi[(int64_t)r * N + c] : psi[(int64_t)c * N + r];
+    X[e] = sc * v;
+  }
+  __syncthreads();
+  {  // ||X||_F^2: strided partials, warp sums, fixed-order total
+    double f = 0.0;
+    for (int e = tid; e < nc * R; e += blockDim.x) f = fma(X[e], X[e], f);
+    f = svd_warp_sum(f);
+    if (lane == 0) s_wmax[warp] = f;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double f = 0.0;
+    for (int w = 0; w < nwarps; ++w) f += s_wmax[w];
+    s_negl = 1e-30 * f;                                          // (1e-15 ||X||_F)^2
+    s_tol = fmax(4.0 * 1.1102230246251565e-16 * sqrt((double)R), 8.0 * 1.1102230246251565e-16);
+  }
+  __syncthreads();
+  const double tol = s_tol, negl = s_negl;
+  int sweep = 0;
+  for (; sweep < kSvdSmallMaxSweeps; ++sweep) {
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    for (int rr = 0; rr < nc - 1; ++rr) {
+      for (int k = warp; k < nc / 2; k += nwarps) {
+        auto idx = [&](int i) {  // circle ordering without an integer division
+          if (i == 0) return 0;
+          int v = i - 1 + rr;
+          if (v >= nc - 1) v -= nc - 1;
+          return v + 1;
+        };
+        const int a = idx(k), b = idx(nc - 1 - k);
+        double* xa = X + (int64_t)a * R;
+        double* xb = X + (int64_t)b * R;
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+        for (int r = lane; r < R; r += 32) {
+          const double u = xa[r], v = xb[r];
+          app = fma(u, u, app);
+          aqq = fma(v, v, aqq);
+          apq = fma(u, v, apq);
+        }
+        app = svd_warp_sum(app);
+        aqq = svd_warp_sum(aqq);
+        apq = svd_warp_sum(apq);
+        if (app > negl && aqq > negl && apq * apq > (tol * tol) * (app * aqq)) {
+          const double th = aqq - app, om = 2.0 * apq;
+          const double h2 = fma(th, th, om * om);
+          const double tt = (th >= 0.0 ? om : -om) * svd_rcp(fabs(th) + h2 * svd_rsqrt(h2));
+          const double cs = svd_rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
+          for (int r = lane; r < R; r += 32) {
+            const double u = xa[r], v = xb[r];
+            xa[r] = cs * u - sn * v;
+            xb[r] = sn * u + cs * v;
+          }
+          if (lane == 0) s_any = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!s_any) break;
+    __syncthreads();
+  }
+  if (tid == 0) s_sweeps = sweep + 1;
+  if (sweep == kSvdSmallMaxSweeps) {
+    if (tid == 0) { info[3] = 3.0; info[2] = kSvdSmallMaxSweeps; }
+    return;
+  }
+  // column norms, rank sort (descending, ties by column index)
+  for (int c = warp; c < nc; c += nwarps) {
+    double f = 0.0;
+    for (int r = lane; r < R; r += 32) f = fma(X[(int64_t)c * R + r], X[(int64_t)c * R + r], f);
+    f = svd_warp_sum(f);
+    if (lane == 0) nrm[c] = sqrt(f);
+  }
+  __syncthreads();
+  for (int c = tid; c < nc; c += blockDim.x) {
+    int rank = 0;
+    for (int c2 = 0; c2 < nc; ++c2) rank += (nrm[c2] > nrm[c]) || (nrm[c2] == nrm[c] && c2 < c);
+    perm[rank] = c;
+  }
+  __syncthreads();
+  if (tid == 0) {  // truncation rule (R20/R21) on the kmin largest values
+    double total = 0.0;
+    for (int i = kmin - 1; i >= 0; --i) total += nrm[perm[i]] * nrm[perm[i]];
+    const double s1 = nrm[perm[0]];
+    int64_t rank = 0;
+    while (rank < kmin && nrm[perm[rank]] > 1e-12 * s1) ++rank;
+    int64_t n = kmin;
+    double disc = 0.0;
+    while (n > 1 && disc + nrm[perm[n - 1]] * nrm[perm[n - 1]] <= cutoff * total) {
+      disc += nrm[perm[n - 1]] * nrm[perm[n - 1]];
+      --n;
+    }
+    n = n < rank ? n : rank;
+    const int64_t md = mindim < rank ? mindim : rank;
+    n = n > md ? n : md;
+    if (maxdim > 0 && n > maxdim) n = maxdim;
+    double err = 0.0;
+    for (int64_t i = kmin - 1; i >= n; --i) err += nrm[perm[i]] * nrm[perm[i]];
+    s_n = (int)n;
+    s_err = total > 0.0 ? err / total : 0.0;
+  }
+  __syncthreads();
+  const int n = s_n;
+  for (int i = tid; i < kmin; i += blockDim.x) S[i] = nrm[perm[i]] / sc;
+  // gauge: largest |entry| of each kept vector positive (first such row on ties); 1/s scale
+  for (int k = warp; k < n; k += nwarps) {
+    const double* x = X + (int64_t)perm[k] * R;
+    double best = -1.0;
+    int bi = 0;
+    for (int r = lane; r < R; r += 32) {
+      const double v = fabs(x[r]);
+      if (v > best) { best = v; bi = r; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) scl[k] = (x[bi] < 0.0 ? -1.0 : 1.0) / nrm[perm[k]];
+  }
+  __syncthreads();
+  // factors: the orthonormal one from X, the centre by one small product with Psi
+  if (dir == 0) {
+    for (int e = tid; e < M * n; e += blockDim.x) {        // U [M][n]
+      const int r = e / n, k = e - r * n;
+      Qout[e] = X[(int64_t)perm[k] * R + r] * scl[k];
+    }
+    for (int e = tid; e < n * N; e += blockDim.x) {        // C = U^T Psi [n][N]
+      const int k = e / N, j = e - k * N;
+      const double* u = X + (int64_t)perm[k] * R;
+      double acc = 0.0;
+      for (int r = 0; r < M; ++r) acc = fma(u[r], psi[(int64_t)r * N + j], acc);
+      Cout[e] = acc * scl[k];
+    }
+  } else {
+    for (int e = tid; e < n * N; e += blockDim.x) {        // V^T [n][N]
+      const int k = e / N, j = e - k * N;
+      Qout[e] = X[(int64_t)perm[k] * R + j] * scl[k];
+    }
+    for (int e = tid; e < M * n; e += blockDim.x) {        // C = Psi V [M][n]
+      const int i = e / n, k = e - i * n;
+      const double* v = X + (int64_t)perm[k] * R;
+      double acc = 0.0;
+      for (int j = 0; j < N; ++j) acc = fma(psi[(int64_t)i * N + j], v[j], acc);
+      Cout[e] = acc * scl[k];
+    }
+  }
+  if (tid == 0) {
+    info[0] = n;
+    info[1] = s_err;
+    info[2] = s_sweeps;
+    info[3] = 0.0;
+  }
+}
+
 }  // namespace heff

@@ -64,21 +64,38 @@ def _compare(Psi, cutoff=0.0, maxdim=0, mindim=1, direction=0, vectors=True):
     return got, ref
 
 
+PATHS = ["auto", "block"]   # auto: one-CTA kernel for sides <= 96; block: HEFF_SVD_NO_SMALL forces the block path
+
+
+def _path(monkeypatch, path):
+    if path == "block":
+        monkeypatch.setenv("HEFF_SVD_NO_SMALL", "1")
+    else:
+        monkeypatch.delenv("HEFF_SVD_NO_SMALL", raising=False)
+
+
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("direction", [0, 1])
-@pytest.mark.parametrize("shape", [(32, 32), (37, 23), (23, 37), (1, 5), (5, 1), (3, 3), (100, 300), (130, 64)])
-def test_split_small_shapes(shape, direction):
+@pytest.mark.parametrize("shape", [(32, 32), (37, 23), (23, 37), (1, 5), (5, 1), (3, 3), (96, 96), (100, 300),
+                                   (130, 64)])
+def test_split_small_shapes(shape, direction, path, monkeypatch):
+    _path(monkeypatch, path)
     _compare(_rand(shape, 17 + sum(shape)), direction=direction)
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("direction", [0, 1])
 @pytest.mark.parametrize("trunc", [dict(cutoff=1e-8), dict(maxdim=10), dict(cutoff=1e-6, maxdim=40),
                                    dict(cutoff=1e-3, mindim=30), dict(cutoff=0.5)])
-def test_split_truncation(trunc, direction):
+def test_split_truncation(trunc, direction, path, monkeypatch):
+    _path(monkeypatch, path)
     _compare(_graded(96, 80, 5, decades=10.0), direction=direction, **trunc)
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("direction", [0, 1])
-def test_split_c1_ground_state_degenerate_spectrum(direction):
+def test_split_c1_ground_state_degenerate_spectrum(direction, path, monkeypatch):
+    _path(monkeypatch, path)
     """C1's converged two-site ground state: SU(2) multiplets, so compare the spectrum and
     the truncated approximation (cut between multiplets) -- not the vectors."""
     from oracle import oracle
@@ -114,8 +131,14 @@ def test_split_deterministic():
     assert torch.equal(a.Q, b.Q) and torch.equal(a.C, b.C) and torch.equal(a.S, b.S)
 
 
-def test_split_errors():
+@pytest.mark.parametrize("path", PATHS)
+def test_split_errors(path, monkeypatch):
+    _path(monkeypatch, path)
     heff = _gpu()
+    bad = torch.ones((8, 8), dtype=torch.float64, device=DEV)
+    bad[3, 4] = float("nan")
+    with pytest.raises(heff.HeffError):
+        heff.svd_split(bad)
     with pytest.raises(heff.HeffZeroVector):
         heff.svd_split(torch.zeros((8, 8), dtype=torch.float64, device=DEV))
     with pytest.raises(heff.HeffError):
