@@ -281,6 +281,11 @@ int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const int* qrow, 
                       const heff_trunc* trunc, int dir, double* Q, double* S, double* Sk, int* qk, double* C,
                       int64_t* n_kept, double* trunc_err, int* sweeps, heff_stream stream);
 
+/* Frees the on-demand workspaces that heff_env_update_*, heff_gemm, heff_svd_split and
+ * heff_svd_split_qn keep per host thread (and those of the U(1) split's worker threads);
+ * they are re-allocated by the next call.  Synchronises the device. */
+int heff_release_caches(void);
+
 /* Host-only (no device work): the truncation rule heff_svd_split applies, on HOST values
  * s[0..k) (descending, non-negative).  n_kept / trunc_err as in heff_svd_split.
  * HEFF_EINVAL (not descending, negative, cutoff < 0), HEFF_EZERO (s[0] == 0). */

@@ -2034,6 +2034,7 @@ struct SvdArena {
 };
 static thread_local SvdArena t_svd_arena;
 static thread_local SplitWs t_svd_splitws;
+static thread_local double* t_small_info = nullptr;  // svd_small_kernel's 4-double read-back
 
 static int svd_reserve(size_t bytes) {
   SvdArena& a = t_svd_arena;
@@ -2148,7 +2149,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   CKR(svd_init_once());
   if (R <= kSvdSmallDispatch && colsP <= kSvdSmallDispatch && getenv("HEFF_SVD_NO_SMALL") == nullptr) {
     // small matrix: the whole split in one CTA (svd_small_kernel)
-    static thread_local double* d_info = nullptr;
+    double*& d_info = t_small_info;
     if (!d_info) CK(cudaMalloc(&d_info, 4 * sizeof(double)));
     const int64_t ncp = colsP + (colsP & 1);
     const size_t smem = sizeof(double) * ((size_t)ncp * R + 3 * kSvdSmallMax);
@@ -2510,6 +2511,25 @@ class BlockPool {
   std::mutex mu_;
   std::condition_variable cv_;
   std::vector<Item> q_;
+
+ public:
+  // one task on EVERY worker (thread-local cleanup): tasks park on a barrier until all
+  // workers hold one, so no worker takes two
+  void run_each_worker(std::vector<std::function<void(cudaStream_t)>>& tasks) {
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    const int W = (int)tasks.size();
+    std::vector<std::function<void(cudaStream_t)>> wrapped;
+    for (auto& t : tasks)
+      wrapped.push_back([&, t](cudaStream_t ws) {
+        t(ws);
+        std::unique_lock<std::mutex> lk(m);
+        if (++arrived == W) cv.notify_all();
+        cv.wait(lk, [&] { return arrived >= W; });
+      });
+    run(wrapped);
+  }
 };
 
 struct SvdQnArena {
@@ -2686,5 +2706,35 @@ extern "C" int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const 
   *n_kept = n;
   *trunc_err = err;
   if (sweeps_out) *sweeps_out = sweeps_max;
+  return HEFF_OK;
+}
+
+// --------------------------------------------------------------------------- cache release
+// Frees the calling thread's on-demand workspaces (environment update, GEMM primitive,
+// split and U(1) split arenas) and those of the U(1) split's worker threads.
+static void release_thread_caches() {
+  auto freews = [](SplitWs& w) { cudaFree(w.ptr); w.ptr = nullptr; w.bytes = 0; };
+  freews(t_env_splitws);
+  freews(t_gemm_ws);
+  freews(t_svd_splitws);
+  cudaFree(t_env_arena.buf); cudaFree(t_env_arena.rowptr); cudaFree(t_env_arena.col); cudaFree(t_env_arena.val);
+  t_env_arena = EnvArena();
+  cudaFree(t_svd_arena.buf);
+  t_svd_arena = SvdArena();
+  cudaFree(t_svdqn_arena.buf);
+  t_svdqn_arena = SvdQnArena();
+  cudaFree(t_small_info);
+  t_small_info = nullptr;
+}
+
+extern "C" int heff_release_caches(void) {
+  release_thread_caches();
+  std::vector<std::function<void(cudaStream_t)>> tasks;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  for (int i = 0; i < kBlockWorkers; ++i)
+    tasks.push_back([dev](cudaStream_t) { cudaSetDevice(dev); release_thread_caches(); });
+  BlockPool::get().run_each_worker(tasks);
+  CK(cudaDeviceSynchronize());
   return HEFF_OK;
 }

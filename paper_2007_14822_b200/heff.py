@@ -99,7 +99,8 @@ def lib() -> ctypes.CDLL:
                                              ctypes.POINTER(ctypes.c_double)]
         L.heff_svd_split_qn.argtypes = [i64, i64, vp, vp, vp, ctypes.POINTER(_Trunc), ip, vp, vp, vp, vp, vp,
                                         ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ip), vp]
-        for f in ("heff_svd_split_qn", "heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
+        L.heff_release_caches.argtypes = []
+        for f in ("heff_release_caches", "heff_svd_split_qn", "heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
                   "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z"):
@@ -112,7 +113,8 @@ EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "h
             "heff_workspace_bytes", "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
             "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z",
-            "heff_svd_split", "heff_truncate_spectrum", "heff_apply_blocked", "heff_svd_split_qn")
+            "heff_svd_split", "heff_truncate_spectrum", "heff_apply_blocked", "heff_svd_split_qn",
+            "heff_release_caches")
 
 
 def _check(rc: int):
@@ -292,6 +294,11 @@ def svd_split_qn(psi: torch.Tensor, qrow, qcol, cutoff: float = 0.0, maxdim: int
     else:
         Qv, Cv = Q[: k * N].view(k, N), C[: M * k].view(M, k)
     return SplitQNResult(Qv, S, Cv, k, err.value, sw.value, Sk[:k], list(qk)[:k])
+
+
+def release_caches():
+    """Free libheff's per-thread split / environment / GEMM workspaces (heff_release_caches)."""
+    _check(lib().heff_release_caches())
 
 
 def truncate_spectrum(s, cutoff: float = 0.0, maxdim: int = 0, mindim: int = 1) -> tuple[int, float]:

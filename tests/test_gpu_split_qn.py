@@ -68,3 +68,19 @@ def test_qn_split_rejects_out_of_sector_entries():
     bad[i[0], j[0]] = 1e-3
     with pytest.raises(heff.HeffError):
         heff.svd_split_qn(torch.from_numpy(bad).to(DEV), qr, qc)
+
+
+def test_release_caches_frees_workspaces_and_splits_still_work():
+    heff = _heff()
+    name, Psi, qr, qc, z = CASES[1]
+    P = torch.from_numpy(Psi).to(DEV)
+    a = heff.svd_split_qn(P, qr, qc, maxdim=40)
+    big = torch.from_numpy(np.random.default_rng(1).standard_normal((1024, 1024))).to(DEV)
+    heff.svd_split(big, maxdim=100)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    heff.release_caches()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free1 > free0                                   # arenas returned to the device
+    b = heff.svd_split_qn(P, qr, qc, maxdim=40)            # and re-grown on demand
+    assert torch.equal(a.S, b.S) and a.qk == b.qk
