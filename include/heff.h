@@ -241,6 +241,25 @@ int heff_env_update_left(const heff_env_dims* dims, const double* L, const doubl
 int heff_env_update_right(const heff_env_dims* dims, const double* R, const double* B, const double* W, double* Rout,
                           heff_stream stream);
 
+/* U(1) environment updates (NEXT-1 x NEXT-3): the same contraction with conserved charges
+ * declared (reading R18) so both GEMMs skip the k-blocks that vanish by symmetry.  HOST int
+ * arrays: q_in = charges of the incoming environment's bond (mi: x for left, y for right),
+ * q_out = charges of the site tensor's new bond (mo: a for left, b for right), qs (d),
+ * cl (kl) / cr (kr) = MPO channel charges of W's left / right bond.  The tensors must vanish
+ * where the charges forbid (undefined result otherwise); bonds should be sector-sorted for
+ * the schedule to pay off (the plain dense schedule is used when it does not). */
+typedef struct {
+  const int* q_in;
+  const int* q_out;
+  const int* qs;
+  const int* cl;
+  const int* cr;
+} heff_env_qn;
+int heff_env_update_left_qn(const heff_env_dims* dims, const double* L, const double* A, const double* W, double* Lout,
+                            const heff_env_qn* qn, heff_stream stream);
+int heff_env_update_right_qn(const heff_env_dims* dims, const double* R, const double* B, const double* W,
+                             double* Rout, const heff_env_qn* qn, heff_stream stream);
+
 /* ---- Two-site split ---------------------------------------------
  * After each local eigensolve a sweep splits the two-site wavefunction with a truncated SVD
  * (Sec. 5: "U,S,V = svd(W,(j,i);cutoff=1E-8,maxdim=10)"; Sec. 6.2,

@@ -1638,8 +1638,36 @@ static int env_common_check(const heff_env_dims* d, const void* a, const void* b
   return init_device_once();
 }
 
-extern "C" int heff_env_update_left(const heff_env_dims* dims, const double* L, const double* A, const double* W,
-                                    double* Lout, heff_stream stream) {
+static int build_sparse_schedule(int64_t M, int64_t N, const std::vector<int>& rowv, const std::vector<int>& colv,
+                                 const std::vector<std::vector<int>>& kvals, int** d_out, int64_t* total_kb,
+                                 const int** order, const int** ptr, const int** list, int64_t* makespan);
+static bool sparse_worth_it(int64_t M, int64_t N, int64_t K, int64_t makespan);
+
+// U(1) schedules of the environment GEMMs (heff_env_update_*_qn); per-thread device buffers
+static thread_local int* t_env_sp1 = nullptr;
+static thread_local int* t_env_sp3 = nullptr;
+
+// block-sparse schedule for one environment GEMM if charges are given and it pays off
+static int env_schedule(GemmOp& g, const std::vector<int>& rowv, const std::vector<int>& colv,
+                        const std::vector<std::vector<int>>& kvals, int** buf) {
+  int64_t tot = 0, span = 0;
+  CKR(build_sparse_schedule(g.M, g.N, rowv, colv, kvals, buf, &tot, &g.sp_order, &g.sp_ptr, &g.sp_list, &span));
+  if (!sparse_worth_it(g.M, g.N, g.K, span)) g.sp_order = g.sp_ptr = g.sp_list = nullptr;
+  return HEFF_OK;
+}
+
+static std::vector<std::vector<int>> kblock_values(int64_t K, const std::function<int(int64_t)>& val) {
+  std::vector<std::vector<int>> kv((K + kGemmBK - 1) / kGemmBK);
+  for (int64_t k = 0; k < K; ++k) {
+    auto& v = kv[k / kGemmBK];
+    const int x = val(k);
+    if (std::find(v.begin(), v.end(), x) == v.end()) v.push_back(x);
+  }
+  return kv;
+}
+
+static int env_left_impl(const heff_env_dims* dims, const double* L, const double* A, const double* W, double* Lout,
+                         const heff_env_qn* qn, heff_stream stream) {
   CKR(env_common_check(dims, L, A, W, Lout));
   const heff_env_dims d = *dims;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1675,6 +1703,24 @@ extern "C" int heff_env_update_left(const heff_env_dims* dims, const double* L, 
   GemmOp g1;  // X[(x' w), (s a)] = L[(x' w), x] . A[x, (s a)]
   g1.M = d.mi * d.kl; g1.N = d.d * d.mo; g1.K = d.mi;
   g1.A = L; g1.lda = d.mi; g1.B = A; g1.ldb = d.d * d.mo; g1.b_kmajor = false; g1.C = X; g1.ldc = d.d * d.mo;
+  GemmOp g3;  // Lout[a', (w' a)] = At[a', (x' s')] . Y[(x' s')][(w' a)]
+  g3.M = d.mo; g3.N = d.kr * d.mo; g3.K = d.mi * d.d;
+  g3.A = At; g3.lda = d.mi * d.d; g3.B = Y; g3.ldb = d.kr * d.mo; g3.b_kmajor = false; g3.C = Lout;
+  g3.ldc = d.kr * d.mo;
+  if (qn) {  // U(1): contracted x needs q(x') - c(w) (rows) = q(a) - q(s) (columns); then q(x') + q(s')
+    std::vector<int> rowv(g1.M), colv(g1.N), rowv3(g3.M), colv3(g3.N);
+    for (int64_t x = 0; x < d.mi; ++x)
+      for (int64_t w = 0; w < d.kl; ++w) rowv[x * d.kl + w] = qn->q_in[x] - qn->cl[w];
+    for (int64_t sg = 0; sg < d.d; ++sg)
+      for (int64_t a = 0; a < d.mo; ++a) colv[sg * d.mo + a] = qn->q_out[a] - qn->qs[sg];
+    CKR(env_schedule(g1, rowv, colv, kblock_values(g1.K, [&](int64_t k) { return qn->q_in[k]; }), &t_env_sp1));
+    for (int64_t a = 0; a < d.mo; ++a) rowv3[a] = qn->q_out[a];
+    for (int64_t wp = 0; wp < d.kr; ++wp)
+      for (int64_t a = 0; a < d.mo; ++a) colv3[wp * d.mo + a] = qn->q_out[a] + qn->cr[wp];
+    CKR(env_schedule(g3, rowv3, colv3,
+                     kblock_values(g3.K, [&](int64_t k) { return qn->q_in[k / d.d] + qn->qs[k % d.d]; }),
+                     &t_env_sp3));
+  }
   r = launch_gemm(g1, 0, s, &nl, &t_env_splitws);
   if (!r) {
     const int nin = (int)(d.kl * d.d), nout = (int)(d.d * d.kr);
@@ -1685,19 +1731,25 @@ extern "C" int heff_env_update_left(const heff_env_dims* dims, const double* L, 
     transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, At, d.mi * d.d, d.mo);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_left: launch failed");
   }
-  if (!r) {
-    GemmOp g3;  // Lout[a', (w' a)] = At[a', (x' s')] . Y[(x' s'), (w' a)]
-    g3.M = d.mo; g3.N = d.kr * d.mo; g3.K = d.mi * d.d;
-    g3.A = At; g3.lda = d.mi * d.d; g3.B = Y; g3.ldb = d.kr * d.mo; g3.b_kmajor = false; g3.C = Lout;
-    g3.ldc = d.kr * d.mo;
-    r = launch_gemm(g3, 0, s, &nl, &t_env_splitws);
-  }
+  if (!r) r = launch_gemm(g3, 0, s, &nl, &t_env_splitws);
   cleanup();
   return r;
 }
 
-extern "C" int heff_env_update_right(const heff_env_dims* dims, const double* R, const double* B, const double* W,
-                                     double* Rout, heff_stream stream) {
+extern "C" int heff_env_update_left(const heff_env_dims* dims, const double* L, const double* A, const double* W,
+                                    double* Lout, heff_stream stream) {
+  return env_left_impl(dims, L, A, W, Lout, nullptr, stream);
+}
+
+extern "C" int heff_env_update_left_qn(const heff_env_dims* dims, const double* L, const double* A, const double* W,
+                                       double* Lout, const heff_env_qn* qn, heff_stream stream) {
+  if (!qn || !qn->q_in || !qn->q_out || !qn->qs || !qn->cl || !qn->cr)
+    return set_err(HEFF_EINVAL, "heff_env_update_left_qn: null charge array");
+  return env_left_impl(dims, L, A, W, Lout, qn, stream);
+}
+
+static int env_right_impl(const heff_env_dims* dims, const double* R, const double* B, const double* W, double* Rout,
+                          const heff_env_qn* qn, heff_stream stream) {
   CKR(env_common_check(dims, R, B, W, Rout));
   const heff_env_dims d = *dims;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1732,6 +1784,23 @@ extern "C" int heff_env_update_right(const heff_env_dims* dims, const double* R,
   GemmOp g1;  // X[(b' s'), (w' y)] = B[(b' s'), y'] . R[y', (w' y)]
   g1.M = d.mo * d.d; g1.N = d.kr * d.mi; g1.K = d.mi;
   g1.A = B; g1.lda = d.mi; g1.B = R; g1.ldb = d.kr * d.mi; g1.b_kmajor = false; g1.C = X; g1.ldc = d.kr * d.mi;
+  GemmOp g3;  // Rout[(b' w), b] = Y[(b' w), (s y)] . B[b, (s y)]^T
+  g3.M = d.mo * d.kl; g3.N = d.mo; g3.K = d.d * d.mi;
+  g3.A = Y; g3.lda = d.d * d.mi; g3.B = B; g3.ldb = d.d * d.mi; g3.b_kmajor = true; g3.C = Rout; g3.ldc = d.mo;
+  if (qn) {  // U(1): contracted y' = q(b') + q(s') (rows) = q(y) + c(w') (columns); then q(y) - q(s)
+    std::vector<int> rowv(g1.M), colv(g1.N), rowv3(g3.M), colv3(g3.N);
+    for (int64_t b = 0; b < d.mo; ++b)
+      for (int64_t sg = 0; sg < d.d; ++sg) rowv[b * d.d + sg] = qn->q_out[b] + qn->qs[sg];
+    for (int64_t wp = 0; wp < d.kr; ++wp)
+      for (int64_t y = 0; y < d.mi; ++y) colv[wp * d.mi + y] = qn->q_in[y] + qn->cr[wp];
+    CKR(env_schedule(g1, rowv, colv, kblock_values(g1.K, [&](int64_t k) { return qn->q_in[k]; }), &t_env_sp1));
+    for (int64_t b = 0; b < d.mo; ++b)
+      for (int64_t w = 0; w < d.kl; ++w) rowv3[b * d.kl + w] = qn->q_out[b] - qn->cl[w];
+    for (int64_t b = 0; b < d.mo; ++b) colv3[b] = qn->q_out[b];
+    CKR(env_schedule(g3, rowv3, colv3,
+                     kblock_values(g3.K, [&](int64_t k) { return qn->q_in[k % d.mi] - qn->qs[k / d.mi]; }),
+                     &t_env_sp3));
+  }
   r = launch_gemm(g1, 0, s, &nl, &t_env_splitws);
   if (!r) {
     const int nin = (int)(d.d * d.kr), nout = (int)(d.kl * d.d);
@@ -1740,14 +1809,21 @@ extern "C" int heff_env_update_right(const heff_env_dims* dims, const double* R,
                                                                                  csr.d_col, csr.d_val, nullptr, 1, 0, 0);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_right: launch failed");
   }
-  if (!r) {
-    GemmOp g3;  // Rout[(b' w), b] = Y[(b' w), (s y)] . B[b, (s y)]^T
-    g3.M = d.mo * d.kl; g3.N = d.mo; g3.K = d.d * d.mi;
-    g3.A = Y; g3.lda = d.d * d.mi; g3.B = B; g3.ldb = d.d * d.mi; g3.b_kmajor = true; g3.C = Rout; g3.ldc = d.mo;
-    r = launch_gemm(g3, 0, s, &nl, &t_env_splitws);
-  }
+  if (!r) r = launch_gemm(g3, 0, s, &nl, &t_env_splitws);
   cleanup();
   return r;
+}
+
+extern "C" int heff_env_update_right(const heff_env_dims* dims, const double* R, const double* B, const double* W,
+                                     double* Rout, heff_stream stream) {
+  return env_right_impl(dims, R, B, W, Rout, nullptr, stream);
+}
+
+extern "C" int heff_env_update_right_qn(const heff_env_dims* dims, const double* R, const double* B, const double* W,
+                                        double* Rout, const heff_env_qn* qn, heff_stream stream) {
+  if (!qn || !qn->q_in || !qn->q_out || !qn->qs || !qn->cl || !qn->cr)
+    return set_err(HEFF_EINVAL, "heff_env_update_right_qn: null charge array");
+  return env_right_impl(dims, R, B, W, Rout, qn, stream);
 }
 
 // Host-only: the tridiagonal eigen-solve lanczos_ground uses (implicit QL, tridiag.h).

@@ -45,6 +45,10 @@ class _EnvDims(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("mi", "d", "mo", "kl", "kr")]
 
 
+class _EnvQN(ctypes.Structure):
+    _fields_ = [(n, ctypes.POINTER(ctypes.c_int)) for n in ("q_in", "q_out", "qs", "cl", "cr")]
+
+
 class _QN(ctypes.Structure):
     _fields_ = [(n, ctypes.POINTER(ctypes.c_int)) for n in ("qa", "qb", "qs1", "qs2", "cL", "cM", "cR")]
 
@@ -93,6 +97,8 @@ def lib() -> ctypes.CDLL:
         L.heff_gemm.argtypes = [i64, i64, i64, vp, i64, vp, i64, ip, vp, i64, ip, ip, vp]
         L.heff_env_update_left.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
         L.heff_env_update_right.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
+        L.heff_env_update_left_qn.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, ctypes.POINTER(_EnvQN), vp]
+        L.heff_env_update_right_qn.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, ctypes.POINTER(_EnvQN), vp]
         L.heff_svd_split.argtypes = [i64, i64, vp, ctypes.POINTER(_Trunc), ip, vp, vp, vp, ctypes.POINTER(i64),
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ip), vp]
         L.heff_truncate_spectrum.argtypes = [vp, i64, ctypes.POINTER(_Trunc), ctypes.POINTER(i64),
@@ -100,7 +106,7 @@ def lib() -> ctypes.CDLL:
         L.heff_svd_split_qn.argtypes = [i64, i64, vp, vp, vp, ctypes.POINTER(_Trunc), ip, vp, vp, vp, vp, vp,
                                         ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ip), vp]
         L.heff_release_caches.argtypes = []
-        for f in ("heff_release_caches", "heff_svd_split_qn", "heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
+        for f in ("heff_env_update_left_qn", "heff_env_update_right_qn", "heff_release_caches", "heff_svd_split_qn", "heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
                   "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z"):
@@ -114,7 +120,7 @@ EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "h
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
             "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z",
             "heff_svd_split", "heff_truncate_spectrum", "heff_apply_blocked", "heff_svd_split_qn",
-            "heff_release_caches")
+            "heff_release_caches", "heff_env_update_left_qn", "heff_env_update_right_qn")
 
 
 def _check(rc: int):
@@ -177,8 +183,15 @@ def tridiag_lowest(alpha, beta):
     return th.value, y
 
 
-def env_update_left(L: torch.Tensor, A: torch.Tensor, W: torch.Tensor, stream=None) -> torch.Tensor:
-    """Lout[a',w',a] = sum A[x',s',a'] L[x',w,x] W[w,s',s,w'] A[x,s,a] (heff_env_update_left)."""
+def _env_qn(qn):
+    import numpy as np
+    arrs = [np.ascontiguousarray(qn[k], dtype=np.int32) for k in ("q_in", "q_out", "qs", "cl", "cr")]
+    return arrs, _EnvQN(*[a.ctypes.data_as(ctypes.POINTER(ctypes.c_int)) for a in arrs])
+
+
+def env_update_left(L: torch.Tensor, A: torch.Tensor, W: torch.Tensor, stream=None, qn: dict | None = None) -> torch.Tensor:
+    """Lout[a',w',a] = sum A[x',s',a'] L[x',w,x] W[w,s',s,w'] A[x,s,a] (heff_env_update_left);
+    qn = dict(q_in, q_out, qs, cl, cr) selects the U(1) schedule (heff_env_update_left_qn)."""
     for t, n in ((L, "L"), (A, "A"), (W, "W")):
         _dev(t, n)
     mi, kl, _ = L.shape
@@ -187,13 +200,19 @@ def env_update_left(L: torch.Tensor, A: torch.Tensor, W: torch.Tensor, stream=No
     if tuple(L.shape) != (mi, kl, mi) or tuple(A.shape) != (mi, d, mo) or tuple(W.shape) != (kl, d, d, kr):
         raise ValueError("expected L[mi,kl,mi], A[mi,d,mo], W[kl,d,d,kr]")
     out = torch.empty((mo, kr, mo), dtype=torch.float64, device=L.device)
+    if qn is not None:
+        keep, q = _env_qn(qn)
+        _check(lib().heff_env_update_left_qn(ctypes.byref(_EnvDims(mi, d, mo, kl, kr)), L.data_ptr(), A.data_ptr(),
+                                             W.data_ptr(), out.data_ptr(), ctypes.byref(q), _stream(stream)))
+        return out
     _check(lib().heff_env_update_left(ctypes.byref(_EnvDims(mi, d, mo, kl, kr)), L.data_ptr(), A.data_ptr(),
                                       W.data_ptr(), out.data_ptr(), _stream(stream)))
     return out
 
 
-def env_update_right(R: torch.Tensor, B: torch.Tensor, W: torch.Tensor, stream=None) -> torch.Tensor:
-    """Rout[b',w,b] = sum B[b',s',y'] R[y',w',y] W[w,s',s,w'] B[b,s,y] (heff_env_update_right)."""
+def env_update_right(R: torch.Tensor, B: torch.Tensor, W: torch.Tensor, stream=None, qn: dict | None = None) -> torch.Tensor:
+    """Rout[b',w,b] = sum B[b',s',y'] R[y',w',y] W[w,s',s,w'] B[b,s,y] (heff_env_update_right);
+    qn = dict(q_in, q_out, qs, cl, cr) selects the U(1) schedule (heff_env_update_right_qn)."""
     for t, n in ((R, "R"), (B, "B"), (W, "W")):
         _dev(t, n)
     mi, kr, _ = R.shape
@@ -202,6 +221,11 @@ def env_update_right(R: torch.Tensor, B: torch.Tensor, W: torch.Tensor, stream=N
     if tuple(R.shape) != (mi, kr, mi) or tuple(B.shape) != (mo, d, mi) or tuple(W.shape) != (kl, d, d, kr):
         raise ValueError("expected R[mi,kr,mi], B[mo,d,mi], W[kl,d,d,kr]")
     out = torch.empty((mo, kl, mo), dtype=torch.float64, device=R.device)
+    if qn is not None:
+        keep, q = _env_qn(qn)
+        _check(lib().heff_env_update_right_qn(ctypes.byref(_EnvDims(mi, d, mo, kl, kr)), R.data_ptr(), B.data_ptr(),
+                                              W.data_ptr(), out.data_ptr(), ctypes.byref(q), _stream(stream)))
+        return out
     _check(lib().heff_env_update_right(ctypes.byref(_EnvDims(mi, d, mo, kl, kr)), R.data_ptr(), B.data_ptr(),
                                        W.data_ptr(), out.data_ptr(), _stream(stream)))
     return out

@@ -115,8 +115,9 @@ def dmrg_qn(Ws, chan_q, maxdims, cutoff=1e-11, lanczos_iter=40, device="cuda", l
     """U(1) (Sz-conserving) two-site DMRG in the Sz = 0 sector (reading R18 conventions):
     the start is the Neel product state; every bond declares its charges to the matvec
     (heff_set_qn: block-sparse GEMM schedules, Lanczos on the sector's entries), splits with
-    heff_svd_split_qn (one SVD per centre-bond charge block) and records the new bond's
-    charges for the next plan.  chan_q[j]: MPO channel charges of the bond right of site j."""
+    heff_svd_split_qn (one SVD per centre-bond charge block), records the new bond's charges
+    and grows the environments with heff_env_update_*_qn (block-sparse GEMM schedules).
+    chan_q[j]: MPO channel charges of the bond right of site j."""
     from paper_2007_14822_b200.heff import psi_row_col_charges, svd_split_qn
     N = len(Ws)
     k = Ws[0].shape[0]
@@ -135,8 +136,11 @@ def dmrg_qn(Ws, chan_q, maxdims, cutoff=1e-11, lanczos_iter=40, device="cuda", l
     Ls[0][0, k - 1, 0] = 1.0
     Rs[N] = torch.zeros((1, k, 1), dtype=torch.float64, device=device)
     Rs[N][0, 0, 0] = 1.0
+    def env_qn(j):  # charges of the site-j environment updates (heff_env_update_*_qn)
+        return dict(qs=qs, cl=chan[j], cr=chan[j + 1])
+
     for j in range(N - 1, 1, -1):
-        Rs[j] = env_update_right(Rs[j + 1], As[j], tW[j])
+        Rs[j] = env_update_right(Rs[j + 1], As[j], tW[j], qn=dict(q_in=bq[j + 1], q_out=bq[j], **env_qn(j)))
     energy = None
     for sw, maxdim in enumerate(maxdims):
         t0 = time.perf_counter()
@@ -158,10 +162,11 @@ def dmrg_qn(Ws, chan_q, maxdims, cutoff=1e-11, lanczos_iter=40, device="cuda", l
                 bq[j + 1] = np.asarray(sp.qk)
                 if direction == "right":
                     As[j], As[j + 1] = sp.Q.reshape(a, d1, kk).contiguous(), sp.C.reshape(kk, d2, b).contiguous()
-                    Ls[j + 1] = env_update_left(Ls[j], As[j], tW[j])
+                    Ls[j + 1] = env_update_left(Ls[j], As[j], tW[j], qn=dict(q_in=bq[j], q_out=bq[j + 1], **env_qn(j)))
                 else:
                     As[j], As[j + 1] = sp.C.reshape(a, d1, kk).contiguous(), sp.Q.reshape(kk, d2, b).contiguous()
-                    Rs[j + 1] = env_update_right(Rs[j + 2], As[j + 1], tW[j + 1])
+                    Rs[j + 1] = env_update_right(Rs[j + 2], As[j + 1], tW[j + 1],
+                                                 qn=dict(q_in=bq[j + 2], q_out=bq[j + 1], **env_qn(j + 1)))
         log(f"After sweep {sw + 1} energy={energy:.12f} maxlinkdim={max(a.shape[2] for a in As[:-1])} "
             f"time={time.perf_counter() - t0:.2f} split {t_split:.2f} s")
     return energy, As, bq
