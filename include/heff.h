@@ -159,6 +159,11 @@ size_t heff_workspace_bytes(const heff_dims* dims, const heff_dist* dist);
  * that gather shards themselves.  Asynchronous on `stream`. */
 int heff_relayout_blocked(const double* src, double* dst, int64_t rows, int64_t nb, int P, heff_stream stream);
 
+/* The Lanczos reduction kernels as a primitive (for kernel-level tests): *result (HOST) =
+ * sum_i x[i] y[i] over n DEVICE doubles, with the same deterministic two-pass reduction
+ * (per-block partials, fixed-order second pass) lanczos_ground uses.  Synchronous. */
+int heff_dot(int64_t n, const double* x, const double* y, double* result, heff_stream stream);
+
 /* Writes a fresh 128-byte ncclUniqueId (rank 0 calls this, then broadcasts it). */
 int heff_nccl_unique_id(unsigned char uid[128]);
 

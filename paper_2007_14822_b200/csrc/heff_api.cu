@@ -1246,6 +1246,25 @@ static int matvec_local(heff_plan_s* p, const double* v, double* w, cudaStream_t
   return apply_impl(p, p->full, w, s);
 }
 
+// The Lanczos reduction kernels as a primitive (kernel-level tests at adversarial lengths):
+// *result = x . y over n doubles through multidot_partial_kernel + reduce_partial_kernel.
+extern "C" int heff_dot(int64_t n, const double* x, const double* y, double* result, heff_stream stream) {
+  if (n < 0 || (n > 0 && (!x || !y)) || !result) return set_err(HEFF_EINVAL, "heff_dot: bad argument");
+  CKR(init_device_once());
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int G = reduce_grid(n);
+  double* buf = nullptr;
+  CK(cudaMalloc(&buf, sizeof(double) * (G + 1)));
+  multidot_partial_kernel<<<G, kRedThreads, 0, s>>>(x, 0, 1, y, n, buf, G);
+  reduce_partial_kernel<<<1, kRedThreads, 0, s>>>(buf, G, G, buf + G, 0, nullptr);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(result, buf + G, sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(buf);
+  if (e != cudaSuccess) return set_err(HEFF_ECUDA, "heff_dot: %s", cudaGetErrorString(e));
+  return HEFF_OK;
+}
+
 extern "C" int heff_relayout_blocked(const double* src, double* dst, int64_t rows, int64_t nb, int P,
                                      heff_stream stream) {
   if (!src || !dst || rows < 0 || nb < 0 || P < 1) return set_err(HEFF_EINVAL, "heff_relayout_blocked: bad argument");

@@ -106,7 +106,8 @@ def lib() -> ctypes.CDLL:
         L.heff_svd_split_qn.argtypes = [i64, i64, vp, vp, vp, ctypes.POINTER(_Trunc), ip, vp, vp, vp, vp, vp,
                                         ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ip), vp]
         L.heff_release_caches.argtypes = []
-        for f in ("heff_env_update_left_qn", "heff_env_update_right_qn", "heff_release_caches", "heff_svd_split_qn", "heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
+        L.heff_dot.argtypes = [i64, vp, vp, ctypes.POINTER(ctypes.c_double), vp]
+        for f in ("heff_dot", "heff_env_update_left_qn", "heff_env_update_right_qn", "heff_release_caches", "heff_svd_split_qn", "heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
                   "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z"):
@@ -120,7 +121,7 @@ EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "h
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
             "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z",
             "heff_svd_split", "heff_truncate_spectrum", "heff_apply_blocked", "heff_svd_split_qn",
-            "heff_release_caches", "heff_env_update_left_qn", "heff_env_update_right_qn")
+            "heff_release_caches", "heff_env_update_left_qn", "heff_env_update_right_qn", "heff_dot")
 
 
 def _check(rc: int):
@@ -318,6 +319,17 @@ def svd_split_qn(psi: torch.Tensor, qrow, qcol, cutoff: float = 0.0, maxdim: int
     else:
         Qv, Cv = Q[: k * N].view(k, N), C[: M * k].view(M, k)
     return SplitQNResult(Qv, S, Cv, k, err.value, sw.value, Sk[:k], list(qk)[:k])
+
+
+def dot(x: torch.Tensor, y: torch.Tensor, stream=None) -> float:
+    """x . y through libheff's Lanczos reduction kernels (heff_dot)."""
+    _dev(x, "x")
+    _dev(y, "y")
+    if x.numel() != y.numel():
+        raise ValueError("x and y must have the same length")
+    r = ctypes.c_double(0.0)
+    _check(lib().heff_dot(x.numel(), x.data_ptr(), y.data_ptr(), ctypes.byref(r), _stream(stream)))
+    return r.value
 
 
 def release_caches():
