@@ -154,10 +154,17 @@ static int make_map(CUtensorMap* map, const double* base, int64_t rows, int64_t 
 }
 
 // ----------------------------------------------------------------------------- GEMM launch
-// Tile configuration of the TMA path.
+// Tile configurations of the TMA path.  The 128x128 tile
+// (8 consumer warps of 64x32) runs every GEMM with at least one full wave of tiles; the
+// 64x64 tile (4 consumer warps of 32x32, 8-deep ring) runs dense GEMMs whose 128x128 tile
+// count is below one wave (C2-size matvecs, small environment / split GEMMs), where the
+// stream-K partial tiles -- and so the fixup traffic -- are 4x smaller.
 constexpr int kBM = 128, kBN = 128, kWM = 64, kWN = 32, kStages = 5, kGroupM = 16;
+constexpr int kBMs = 64, kBNs = 64, kWMs = 32, kWNs = 32, kStagesS = 8;
 using CfgNN = TmaGemmCfg<kBM, kBN, kWM, kWN, kStages, false>;
 using CfgNT = TmaGemmCfg<kBM, kBN, kWM, kWN, kStages, true>;
+using CfgNNs = TmaGemmCfg<kBMs, kBNs, kWMs, kWNs, kStagesS, false>;
+using CfgNTs = TmaGemmCfg<kBMs, kBNs, kWMs, kWNs, kStagesS, true>;
 
 struct GemmOp {
   int64_t M = 0, N = 0, K = 0;
@@ -173,11 +180,12 @@ struct GemmOp {
   const int* sp_order = nullptr;
   const int* sp_ptr = nullptr;
   const int* sp_list = nullptr;
-  // cached TMA maps (rebuilt when A/B pointers change)
+  // cached TMA maps (rebuilt when A/B pointers or the tile box change)
   CUtensorMap mapA, mapB;
   const double* mapA_ptr = nullptr;
   const double* mapB_ptr = nullptr;
   int64_t mapA_rows = -1, mapB_rows = -1;
+  int mapA_box = 0, mapB_box = 0;
 };
 
 static int g_num_sms = 0;
@@ -194,6 +202,96 @@ struct SplitWs {  // stream-K partial-tile workspace, grown on demand
   size_t bytes = 0;
 };
 
+// One dense/sparse TMA GEMM with tile BM x BN: maps, hybrid data-parallel + stream-K
+// schedule, kernel and (if any tile's k-range was split) the fixup.
+template <int BM, int BN, int WM, int WN, int ST>
+static int launch_tma(GemmOp& g, cudaStream_t s, int* nlaunch, SplitWs* ws, const ShardedA* sa) {
+  using NN = TmaGemmCfg<BM, BN, WM, WN, ST, false>;
+  using NT = TmaGemmCfg<BM, BN, WM, WN, ST, true>;
+  if (!sa && (g.mapA_ptr != g.A || g.mapA_rows != g.M || g.mapA_box != BM)) {
+    CKR(make_map(&g.mapA, g.A, g.M, g.K, g.lda, kGemmBK, BM));
+    g.mapA_ptr = g.A;
+    g.mapA_rows = g.M;
+    g.mapA_box = BM;
+  }
+  if (g.mapB_ptr != g.B || g.mapB_rows != g.N || g.mapB_box != BN) {
+    if (g.b_kmajor)
+      CKR(make_map(&g.mapB, g.B, g.N, g.K, g.ldb, kGemmBK, BN));
+    else
+      CKR(make_map(&g.mapB, g.B, g.K, g.N, g.ldb, 16, kGemmBK));
+    g.mapB_ptr = g.B;
+    g.mapB_rows = g.N;
+    g.mapB_box = BN;
+  }
+  const int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int64_t ktiles = (g.K + kGemmBK - 1) / kGemmBK;
+  // Hybrid schedule: whole tiles round-robin for all but the last one-to-two waves, whose
+  // (tile, k-block) iterations are balanced across the SMs by stream-K.
+  int grid = (int)std::min<int64_t>(tiles, g_num_sms);
+  int64_t dp_tiles = tiles;
+  const int64_t waves = (tiles + g_num_sms - 1) / g_num_sms;
+  const double eff = (double)tiles / (double)(waves * g_num_sms);
+  const bool sparse = g.sp_list != nullptr;
+  if (!sparse && ws && eff < 0.995 && getenv("HEFF_NO_STREAMK") == nullptr) {
+    dp_tiles = (tiles >= 2 * (int64_t)g_num_sms) ? (tiles / g_num_sms - 1) * g_num_sms : 0;
+    const int64_t sk_iters = (tiles - dp_tiles) * ktiles;
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>(g_num_sms, sk_iters / 4));  // >= 4 k-blocks per CTA
+    // every split tile must have <= kFixupMaxParts contributing CTAs
+    while (grid > 1 && ktiles / std::max<int64_t>(1, sk_iters / grid) + 2 > kFixupMaxParts) grid /= 2;
+    if (dp_tiles > 0) grid = g_num_sms;
+    const size_t need = sizeof(double) * 2 * (size_t)grid * BM * BN;
+    if (ws->bytes < need) {
+      cudaFree(ws->ptr);
+      ws->ptr = nullptr;
+      ws->bytes = 0;
+      if (cudaMalloc(&ws->ptr, need) != cudaSuccess) {
+        cudaGetLastError();
+        dp_tiles = tiles;  // no room for partial tiles: plain persistent schedule
+        grid = (int)std::min<int64_t>(tiles, g_num_sms);
+      } else {
+        ws->bytes = need;
+      }
+    }
+  }
+  const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(g.C) & 15) == 0) ? 1 : 0;
+  double* wsp = ws ? ws->ptr : nullptr;
+  if (sa) {
+    if (!g.b_kmajor) return set_err(HEFF_EUNSUPPORTED, "sharded-A GEMM: NT only");
+    auto k = gemm_dmma_tma_sharded_kernel<BM, BN, WM, WN, ST, true>;
+    k<<<grid, NT::kThreads, NT::kSmemBytes, s>>>(*sa, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K, kGroupM, vec,
+                                                 (int)dp_tiles, wsp, g.accumulate);
+  } else if (g.b_kmajor) {
+    auto k = gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, true>;
+    k<<<grid, NT::kThreads, NT::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K, kGroupM,
+                                                 vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order, g.sp_ptr,
+                                                 g.sp_list);
+  } else {
+    auto k = gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, false>;
+    k<<<grid, NN::kThreads, NN::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K, kGroupM,
+                                                 vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order, g.sp_ptr,
+                                                 g.sp_list);
+  }
+  if (dp_tiles < tiles) {
+    CK(cudaGetLastError());
+    if (nlaunch) ++*nlaunch;
+    streamk_fixup_kernel<BM, BN><<<(unsigned)((tiles - dp_tiles) * kFixupSplit), 256, 0, s>>>(
+        wsp, g.C, g.ldc, (int)g.M, (int)g.N, (int)ktiles, kGroupM, grid, (int)dp_tiles, g.accumulate);
+  }
+  return HEFF_OK;
+}
+
+// Tile choice: 64x64 for dense GEMMs with fewer 128x128 tiles than SMs (HEFF_GEMM_TILE=128 /
+// =64 forces one).  Block-sparse schedules and the sharded-A GEMM are built on 128x128 tiles.
+static bool use_small_tile(const GemmOp& g, const ShardedA* sa) {
+  if (sa || g.sp_list) return false;
+  const char* e = getenv("HEFF_GEMM_TILE");
+  const int force = e ? atoi(e) : 0;
+  if (force == 64) return true;
+  if (force == 128) return false;
+  const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + kBN - 1) / kBN);
+  return tiles < g_num_sms;
+}
+
 // sa != nullptr: the A operand is K-sharded over sa->nsh tensor maps (gemm_dmma_tma_sharded_kernel;
 // g.A is ignored, the TMA path is required).
 static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitWs* ws, const ShardedA* sa = nullptr) {
@@ -201,74 +299,10 @@ static int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitW
   const bool use_tma = sa != nullptr || (path == 2) || (path == 0 && tma_ok(g));
   if (path == 2 && !tma_ok(g)) return set_err(HEFF_EUNSUPPORTED, "TMA GEMM path needs 16-byte rows/alignment");
   if (use_tma) {
-    if (!sa && (g.mapA_ptr != g.A || g.mapA_rows != g.M)) {
-      CKR(make_map(&g.mapA, g.A, g.M, g.K, g.lda, kGemmBK, kBM));
-      g.mapA_ptr = g.A;
-      g.mapA_rows = g.M;
-    }
-    if (g.mapB_ptr != g.B || g.mapB_rows != g.N) {
-      if (g.b_kmajor)
-        CKR(make_map(&g.mapB, g.B, g.N, g.K, g.ldb, kGemmBK, kBN));
-      else
-        CKR(make_map(&g.mapB, g.B, g.K, g.N, g.ldb, 16, kGemmBK));
-      g.mapB_ptr = g.B;
-      g.mapB_rows = g.N;
-    }
-    const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + kBN - 1) / kBN);
-    const int64_t ktiles = (g.K + kGemmBK - 1) / kGemmBK;
-    // Hybrid schedule: whole tiles round-robin for all but the last one-to-two waves, whose
-    // (tile, k-block) iterations are balanced across the SMs by stream-K.
-    int grid = (int)std::min<int64_t>(tiles, g_num_sms);
-    int64_t dp_tiles = tiles;
-    const int64_t waves = (tiles + g_num_sms - 1) / g_num_sms;
-    const double eff = (double)tiles / (double)(waves * g_num_sms);
-    const bool sparse = g.sp_list != nullptr;
-    if (sparse) grid = (int)std::min<int64_t>(tiles, g_num_sms);
-    if (!sparse && ws && eff < 0.995 && getenv("HEFF_NO_STREAMK") == nullptr) {
-      dp_tiles = (tiles >= 2 * (int64_t)g_num_sms) ? (tiles / g_num_sms - 1) * g_num_sms : 0;
-      const int64_t sk_iters = (tiles - dp_tiles) * ktiles;
-      grid = (int)std::max<int64_t>(1, std::min<int64_t>(g_num_sms, sk_iters / 4));  // >= 4 k-blocks per CTA
-      // every split tile must have <= kFixupMaxParts contributing CTAs
-      while (grid > 1 && ktiles / std::max<int64_t>(1, sk_iters / grid) + 2 > kFixupMaxParts) grid /= 2;
-      if (dp_tiles > 0) grid = g_num_sms;
-      const size_t need = sizeof(double) * 2 * (size_t)grid * kBM * kBN;
-      if (ws->bytes < need) {
-        cudaFree(ws->ptr);
-        ws->ptr = nullptr;
-        ws->bytes = 0;
-        if (cudaMalloc(&ws->ptr, need) != cudaSuccess) {
-          cudaGetLastError();
-          dp_tiles = tiles;  // no room for partial tiles: plain persistent schedule
-          grid = (int)std::min<int64_t>(tiles, g_num_sms);
-        } else {
-          ws->bytes = need;
-        }
-      }
-    }
-    const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(g.C) & 15) == 0) ? 1 : 0;
-    double* wsp = ws ? ws->ptr : nullptr;
-    if (sa) {
-      if (!g.b_kmajor) return set_err(HEFF_EUNSUPPORTED, "sharded-A GEMM: NT only");
-      auto k = gemm_dmma_tma_sharded_kernel<kBM, kBN, kWM, kWN, kStages, true>;
-      k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(*sa, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate);
-    } else if (g.b_kmajor) {
-      auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, true>;
-      k<<<grid, CfgNT::kThreads, CfgNT::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order,
-                                                          g.sp_ptr, g.sp_list);
-    } else {
-      auto k = gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>;
-      k<<<grid, CfgNN::kThreads, CfgNN::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K,
-                                                          kGroupM, vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order,
-                                                          g.sp_ptr, g.sp_list);
-    }
-    if (dp_tiles < tiles) {
-      CK(cudaGetLastError());
-      if (nlaunch) ++*nlaunch;
-      streamk_fixup_kernel<kBM, kBN><<<(unsigned)((tiles - dp_tiles) * kFixupSplit), 256, 0, s>>>(
-          wsp, g.C, g.ldc, (int)g.M, (int)g.N, (int)ktiles, kGroupM, grid, (int)dp_tiles, g.accumulate);
-    }
+    if (use_small_tile(g, sa))
+      CKR((launch_tma<kBMs, kBNs, kWMs, kWNs, kStagesS>(g, s, nlaunch, ws, sa)));
+    else
+      CKR((launch_tma<kBM, kBN, kWM, kWN, kStages>(g, s, nlaunch, ws, sa)));
   } else {
     dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64));
     if (grid.y > 65535) return set_err(HEFF_EUNSUPPORTED, "plain GEMM path: M too large");
@@ -304,6 +338,12 @@ static int init_device_once() {
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNN::kSmemBytes));
   CK(cudaFuncSetAttribute(gemm_dmma_tma_sharded_kernel<kBM, kBN, kWM, kWN, kStages, true>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNT::kSmemBytes));
+  CK(cudaFuncSetAttribute(gemm_dmma_tma_kernel<kBMs, kBNs, kWMs, kWNs, kStagesS, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNTs::kSmemBytes));
+  CK(cudaFuncSetAttribute(gemm_dmma_tma_kernel<kBMs, kBNs, kWMs, kWNs, kStagesS, false>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNNs::kSmemBytes));
+  CK(cudaFuncSetAttribute(gemm_dmma_tma_sharded_kernel<kBMs, kBNs, kWMs, kWNs, kStagesS, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNTs::kSmemBytes));
   CK(cudaFuncSetAttribute(mpo_orderA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   CK(cudaFuncSetAttribute(mpo_orderB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));

@@ -21,8 +21,12 @@ def dev():
 
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("bk", [False, True])
-def test_gemm_vs_torch(dev, shape, bk):
+@pytest.mark.parametrize("tile", [None, "64", "128"])
+def test_gemm_vs_torch(dev, shape, bk, tile, monkeypatch):
+    """tile: the automatic choice, or the 64x64 / 128x128 TMA tile forced (HEFF_GEMM_TILE)."""
     from paper_2007_14822_b200.heff import gemm
+    if tile:
+        monkeypatch.setenv("HEFF_GEMM_TILE", tile)
     M, N, K = shape
     g = torch.Generator(device=dev).manual_seed(M * 7 + N * 3 + K)
     A = torch.randn(M, K, dtype=torch.float64, device=dev, generator=g)
@@ -43,8 +47,10 @@ def test_gemm_vs_torch(dev, shape, bk):
 
 
 @pytest.mark.parametrize("sk", ["1", None])
-def test_gemm_streamk_toggle_identical_results_tolerance(dev, sk, monkeypatch):
+@pytest.mark.parametrize("tile", ["64", "128"])
+def test_gemm_streamk_toggle_identical_results_tolerance(dev, sk, tile, monkeypatch):
     from paper_2007_14822_b200.heff import gemm
+    monkeypatch.setenv("HEFF_GEMM_TILE", tile)
     if sk:
         monkeypatch.setenv("HEFF_NO_STREAMK", sk)
     g = torch.Generator(device=dev).manual_seed(1)
