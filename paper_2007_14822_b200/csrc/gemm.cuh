@@ -65,12 +65,12 @@ struct WorkRange {
   // k-blocks kb_list[kb_ptr[t] .. kb_ptr[t+1])
   const int* order;
   const int* kb_ptr;
-  __device__ WorkRange(int tiles, int dp_tiles_, int ktiles_, const int* order_, const int* kb_ptr_)
+  __device__ WorkRange(int cta, int tiles, int dp_tiles_, int ktiles_, const int* order_, const int* kb_ptr_)
       : dp_tiles(dp_tiles_), ktiles(ktiles_), order(order_), kb_ptr(kb_ptr_) {
     const int64_t total = (int64_t)(tiles - dp_tiles_) * ktiles_;
-    it = total * blockIdx.x / gridDim.x;
-    it_end = total * (blockIdx.x + 1) / gridDim.x;
-    tile = blockIdx.x;
+    it = total * cta / gridDim.x;
+    it_end = total * (cta + 1) / gridDim.x;
+    tile = cta;
   }
   // next (tile, [i0, i1)) segment; i indexes k-blocks (dense) or kb_list (sparse)
   __device__ bool next(int& t, int& i0, int& i1) {
@@ -96,6 +96,41 @@ struct WorkRange {
   }
 };
 
+// In-kernel stream-K fixup (replaces streamk_fixup_kernel when `sk` is non-null).  Every
+// split tile is reduced by its HIGHEST contributing CTA after that CTA's own work: it waits
+// (release/acquire flags, one per partial slot, tagged with the launch epoch) for the lower
+// contributors' partial tiles, sums all slots in CTA order -- the fixup kernel's order, so
+// results are bitwise identical -- and stores the tile.  CTA indices are tickets taken from
+// a global counter at CTA start (not blockIdx), so every CTA a reducer waits for has already
+// started: waits cannot deadlock whatever order the hardware dispatches CTAs in, or
+// whatever else shares the GPU.  A wait that exceeds ~10 s traps (a reported launch error,
+// never a hang).
+struct StreamKSync {
+  unsigned int* counter;  // ticket counter: 0 between launches (the last ticket holder resets it)
+  int* flags;             // [2 * gridDim.x] slot flags
+  int epoch;              // this launch's flag value (> 0, increasing)
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void consumers_bar(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// CTA owning stream-K iteration `it` when `total` iterations are cut into G equal ranges
+__host__ __device__ __forceinline__ int sk_cta_of(int64_t it, int64_t total, int G) {
+  int64_t b = (it * G) / total;
+  while (b + 1 < G && total * (b + 1) / G <= it) ++b;
+  while (b > 0 && total * b / G > it) --b;
+  return (int)b;
+}
+
 // A operand split along K over up to kMaxShards tensor maps (NEXT-5 gather-fused GEMM_A):
 // k-block kb is read from map (16 kb) / ksh at column 16 kb - shard * ksh.  The maps may
 // address peer GPUs' memory (NCCL symmetric-window pointers over NVLink).
@@ -112,7 +147,7 @@ __device__ __forceinline__ void gemm_dmma_tma_body(const CUtensorMap* tmA, const
                                                    int group_m, int vec_store, int dp_tiles,
                                                    double* __restrict__ partial_ws, int accumulate,
                                                    const int* __restrict__ tile_order, const int* __restrict__ kb_ptr,
-                                                   const int* __restrict__ kb_list) {
+                                                   const int* __restrict__ kb_list, const StreamKSync* sk) {
   using Cfg = TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>;
   constexpr int MI = WM / 8, NJ = WN / 8;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -125,14 +160,22 @@ __device__ __forceinline__ void gemm_dmma_tma_body(const CUtensorMap* tmA, const
   const int tiles = num_m * num_n;
   const int ktiles = (K + kGemmBK - 1) / kGemmBK;
 
+  __shared__ int s_cta;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::kConsumerWarps);
     }
     fence_barrier_init();
+    int c = (int)blockIdx.x;
+    if (sk) {
+      c = (int)atomicAdd(sk->counter, 1u);
+      if (c == (int)gridDim.x - 1) atomicExch(sk->counter, 0u);  // every CTA holds its ticket
+    }
+    s_cta = c;
   }
   __syncthreads();
+  const int cta = s_cta;
 
   if (warp >= Cfg::kConsumerWarps) {
     // ---------------- producer warpgroup: one lane drives the TMA ring ----------------
@@ -146,7 +189,7 @@ __device__ __forceinline__ void gemm_dmma_tma_body(const CUtensorMap* tmA, const
       tma_prefetch_desc(tmB);
       int stage = 0;
       uint32_t phase = 0;
-      WorkRange wr(tiles, dp_tiles, ktiles, tile_order, kb_ptr);
+      WorkRange wr(cta, tiles, dp_tiles, ktiles, tile_order, kb_ptr);
       int tile, i0, i1;
       while (wr.next(tile, i0, i1)) {
         int mb, nb;
@@ -189,7 +232,7 @@ __device__ __forceinline__ void gemm_dmma_tma_body(const CUtensorMap* tmA, const
 
   int stage = 0;
   uint32_t phase = 0;
-  WorkRange wr(tiles, dp_tiles, ktiles, tile_order, kb_ptr);
+  WorkRange wr(cta, tiles, dp_tiles, ktiles, tile_order, kb_ptr);
   int tile, kb0, kb1;
   bool first_seg = true;  // first stream-K segment of this CTA
   while (wr.next(tile, kb0, kb1)) {
@@ -269,7 +312,8 @@ __device__ __forceinline__ void gemm_dmma_tma_body(const CUtensorMap* tmA, const
       }
     } else {
       // stream-K partial tile -> workspace slot (full BM x BN, row-major)
-      double* ws = partial_ws + ((int64_t)blockIdx.x * 2 + (first_seg ? 0 : 1)) * (BM * BN);
+      const int slot = cta * 2 + (first_seg ? 0 : 1);
+      double* ws = partial_ws + (int64_t)slot * (BM * BN);
       first_seg = false;
 #pragma unroll
       for (int i = 0; i < MI; ++i)
@@ -277,8 +321,85 @@ __device__ __forceinline__ void gemm_dmma_tma_body(const CUtensorMap* tmA, const
         for (int j = 0; j < NJ; ++j)
           *reinterpret_cast<double2*>(ws + (wm0 + 8 * i + g) * BN + wn0 + 8 * j + 2 * t) =
               make_double2(acc[i][j][0], acc[i][j][1]);
+      if (sk) {  // publish the slot: every writer fences, then one release store
+        __threadfence();
+        consumers_bar(Cfg::kConsumerWarps * 32);
+        if (threadIdx.x == 0) st_release_gpu(sk->flags + slot, sk->epoch);
+      }
     }
     if (tile >= dp_tiles) first_seg = false;
+  }
+
+  if (sk && !kb_list && dp_tiles < tiles) {
+    // Reduce the split tile that holds this CTA's first stream-K iteration, if this CTA also
+    // holds its last iteration (= the highest contributor) and the tile began in a lower CTA.
+    const int64_t total = (int64_t)(tiles - dp_tiles) * ktiles;
+    const int G = gridDim.x;
+    const int64_t it0 = total * cta / G, it1 = total * (cta + 1) / G;
+    if (it0 < it1 && it0 % ktiles != 0) {
+      const int local = (int)(it0 / ktiles);
+      if ((int64_t)(local + 1) * ktiles <= it1) {
+        const int b0 = sk_cta_of((int64_t)local * ktiles, total, G);
+        const int nthr = Cfg::kConsumerWarps * 32;
+        if (threadIdx.x == 0) {
+          long long t_start;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+          for (int b = b0; b < cta; ++b) {
+            const int slot_b = 2 * b + ((int)((total * b / G) / ktiles) == local ? 0 : 1);
+            while (ld_acquire_gpu(sk->flags + slot_b) != sk->epoch) {
+              __nanosleep(64);
+              long long t_now;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+              if (t_now - t_start > 10000000000ll) __trap();
+            }
+          }
+        }
+        consumers_bar(nthr);
+        int mb, nb;
+        tile_coords(dp_tiles + local, num_m, num_n, group_m, mb, nb);
+        // each thread owns kPer double2 of the tile, taken kChunk at a time: for one chunk it
+        // loads the slots in CTA order, kChunk independent L2 loads in flight per slot
+        constexpr int kPer = BM * BN / (2 * Cfg::kConsumerWarps * 32);
+        constexpr int kChunk = kPer < 16 ? kPer : 16;
+        static_assert(kPer % kChunk == 0, "chunking");
+#pragma unroll 1
+        for (int i0 = 0; i0 < kPer; i0 += kChunk) {
+          double2 a[kChunk];
+#pragma unroll
+          for (int i = 0; i < kChunk; ++i) a[i] = make_double2(0.0, 0.0);
+          for (int b = b0; b <= cta; ++b) {
+            const int slot_b = 2 * b + ((int)((total * b / G) / ktiles) == local ? 0 : 1);
+            const double2* src = reinterpret_cast<const double2*>(partial_ws + (int64_t)slot_b * (BM * BN));
+#pragma unroll
+            for (int i = 0; i < kChunk; ++i) {
+              const double2 v = __ldcg(src + threadIdx.x + (i0 + i) * nthr);
+              a[i].x += v.x;
+              a[i].y += v.y;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < kChunk; ++i) {
+            const int e = 2 * (threadIdx.x + (i0 + i) * nthr);
+            const int r = e / BN, c = e - r * BN;  // c even
+            const int row = mb * BM + r, col = nb * BN + c;
+            if (row >= M || col >= N) continue;
+            double* cp = C + (int64_t)row * ldc + col;
+            if (vec_store && col + 1 < N) {
+              double2 v = a[i];
+              if (accumulate) {
+                const double2 o = *reinterpret_cast<const double2*>(cp);
+                v.x += o.x;
+                v.y += o.y;
+              }
+              *reinterpret_cast<double2*>(cp) = v;
+            } else {
+              cp[0] = accumulate ? cp[0] + a[i].x : a[i].x;
+              if (col + 1 < N) cp[1] = accumulate ? cp[1] + a[i].y : a[i].y;
+            }
+          }
+        }
+      }
+    }
   }
 }
 
@@ -288,20 +409,21 @@ __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::
                          double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store,
                          int dp_tiles, double* __restrict__ partial_ws, int accumulate,
                          const int* __restrict__ tile_order, const int* __restrict__ kb_ptr,
-                         const int* __restrict__ kb_list) {
+                         const int* __restrict__ kb_list, const __grid_constant__ StreamKSync sk, int use_sk) {
   gemm_dmma_tma_body<BM, BN, WM, WN, STAGES, B_KMAJOR, false>(&tmA, nullptr, &tmB, C, ldc, M, N, K, group_m, vec_store,
                                                               dp_tiles, partial_ws, accumulate, tile_order, kb_ptr,
-                                                              kb_list);
+                                                              kb_list, use_sk ? &sk : nullptr);
 }
 
 template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR>
 __global__ void __launch_bounds__(TmaGemmCfg<BM, BN, WM, WN, STAGES, B_KMAJOR>::kThreads, 1)
     gemm_dmma_tma_sharded_kernel(const __grid_constant__ ShardedA sa, const __grid_constant__ CUtensorMap tmB,
                                  double* __restrict__ C, int64_t ldc, int M, int N, int K, int group_m, int vec_store,
-                                 int dp_tiles, double* __restrict__ partial_ws, int accumulate) {
+                                 int dp_tiles, double* __restrict__ partial_ws, int accumulate,
+                                 const __grid_constant__ StreamKSync sk, int use_sk) {
   gemm_dmma_tma_body<BM, BN, WM, WN, STAGES, B_KMAJOR, true>(nullptr, &sa, &tmB, C, ldc, M, N, K, group_m, vec_store,
                                                              dp_tiles, partial_ws, accumulate, nullptr, nullptr,
-                                                             nullptr);
+                                                             nullptr, use_sk ? &sk : nullptr);
 }
 
 // Stream-K fixup: every stream-K tile whose k-range was split across CTAs is the sum, in
@@ -324,12 +446,7 @@ __global__ void __launch_bounds__(256) streamk_fixup_kernel(const double* __rest
   if (threadIdx.x == 0) {
     const int64_t total = (int64_t)(num_m * num_n - dp_tiles) * ktiles;
     // CTA b owns stream-K iterations [total*b/grid, total*(b+1)/grid)
-    auto cta_of = [&](int64_t it) {
-      int64_t b = (it * grid) / total;
-      while (b + 1 < grid && total * (b + 1) / grid <= it) ++b;
-      while (b > 0 && total * b / grid > it) --b;
-      return (int)b;
-    };
+    auto cta_of = [&](int64_t it) { return sk_cta_of(it, total, grid); };
     const int64_t it_first = (int64_t)local * ktiles;
     const int b0 = cta_of(it_first), b1 = cta_of(it_first + ktiles - 1);
     int n = 0;

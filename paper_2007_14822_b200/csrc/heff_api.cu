@@ -160,7 +160,7 @@ static int make_map(CUtensorMap* map, const double* base, int64_t rows, int64_t 
 // count is below one wave (C2-size matvecs, small environment / split GEMMs), where the
 // stream-K partial tiles -- and so the fixup traffic -- are 4x smaller.
 constexpr int kBM = 128, kBN = 128, kWM = 64, kWN = 32, kStages = 5, kGroupM = 16;
-constexpr int kBMs = 64, kBNs = 64, kWMs = 32, kWNs = 32, kStagesS = 8;
+constexpr int kBMs = 64, kBNs = 64, kWMs = 32, kWNs = 16, kStagesS = 8;
 using CfgNN = TmaGemmCfg<kBM, kBN, kWM, kWN, kStages, false>;
 using CfgNT = TmaGemmCfg<kBM, kBN, kWM, kWN, kStages, true>;
 using CfgNNs = TmaGemmCfg<kBMs, kBNs, kWMs, kWNs, kStagesS, false>;
@@ -200,7 +200,14 @@ static bool tma_ok(const GemmOp& g) {
 struct SplitWs {  // stream-K partial-tile workspace, grown on demand
   double* ptr = nullptr;
   size_t bytes = 0;
+  // in-kernel fixup state (StreamKSync): [0] ticket counter, then int flags[2 * kSkMaxGrid]
+  void* sync = nullptr;
+  int epoch = 0;
 };
+constexpr int kSkMaxGrid = 1024;
+
+// HEFF_SK_FIXUP_KERNEL=1: sum split tiles in the separate streamk_fixup_kernel instead of in-kernel
+static bool sk_inkernel() { return getenv("HEFF_SK_FIXUP_KERNEL") == nullptr; }
 
 // One dense/sparse TMA GEMM with tile BM x BN: maps, hybrid data-parallel + stream-K
 // schedule, kernel and (if any tile's k-range was split) the fixup.
@@ -255,23 +262,37 @@ static int launch_tma(GemmOp& g, cudaStream_t s, int* nlaunch, SplitWs* ws, cons
   }
   const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(g.C) & 15) == 0) ? 1 : 0;
   double* wsp = ws ? ws->ptr : nullptr;
+  StreamKSync sk{};
+  int use_sk = 0;
+  if (dp_tiles < tiles && grid <= kSkMaxGrid && sk_inkernel()) {
+    if (!ws->sync) {
+      const size_t sb = 16 + sizeof(int) * 2 * kSkMaxGrid;
+      if (cudaMalloc(&ws->sync, sb) != cudaSuccess) return set_err(HEFF_ENOMEM, "stream-K sync buffer");
+      CK(cudaMemsetAsync(ws->sync, 0, sb, s));
+      ws->epoch = 0;
+    }
+    sk.counter = static_cast<unsigned int*>(ws->sync);
+    sk.flags = reinterpret_cast<int*>(static_cast<char*>(ws->sync) + 16);
+    sk.epoch = ++ws->epoch;
+    use_sk = 1;
+  }
   if (sa) {
     if (!g.b_kmajor) return set_err(HEFF_EUNSUPPORTED, "sharded-A GEMM: NT only");
     auto k = gemm_dmma_tma_sharded_kernel<BM, BN, WM, WN, ST, true>;
     k<<<grid, NT::kThreads, NT::kSmemBytes, s>>>(*sa, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K, kGroupM, vec,
-                                                 (int)dp_tiles, wsp, g.accumulate);
+                                                 (int)dp_tiles, wsp, g.accumulate, sk, use_sk);
   } else if (g.b_kmajor) {
     auto k = gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, true>;
     k<<<grid, NT::kThreads, NT::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K, kGroupM,
                                                  vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order, g.sp_ptr,
-                                                 g.sp_list);
+                                                 g.sp_list, sk, use_sk);
   } else {
     auto k = gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, false>;
     k<<<grid, NN::kThreads, NN::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K, kGroupM,
                                                  vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order, g.sp_ptr,
-                                                 g.sp_list);
+                                                 g.sp_list, sk, use_sk);
   }
-  if (dp_tiles < tiles) {
+  if (dp_tiles < tiles && !use_sk) {
     CK(cudaGetLastError());
     if (nlaunch) ++*nlaunch;
     streamk_fixup_kernel<BM, BN><<<(unsigned)((tiles - dp_tiles) * kFixupSplit), 256, 0, s>>>(
@@ -344,7 +365,8 @@ static int init_device_once() {
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNNs::kSmemBytes));
   CK(cudaFuncSetAttribute(gemm_dmma_tma_sharded_kernel<kBMs, kBNs, kWMs, kWNs, kStagesS, true>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNTs::kSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_orderA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(mpo_orderA_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(mpo_orderA_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   CK(cudaFuncSetAttribute(mpo_orderB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   done.store(true, std::memory_order_release);
@@ -533,6 +555,7 @@ extern "C" int heff_destroy(heff_plan p) {
   cudaFree(p->basis); cudaFree(p->work); cudaFree(p->full); cudaFree(p->gather);
   cudaFree(p->partial); cudaFree(p->scal);
   cudaFree(p->splitws.ptr);
+  cudaFree(p->splitws.sync);
   cudaFree(p->phis); cudaFree(p->pen_scratch);
   cudaFree(p->sp1); cudaFree(p->sp4);
   free_csr(p->csrA);
@@ -871,7 +894,7 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     CKR(launch_gemm(p->g1, p->gemm_path, s, nl, &p->splitws));
     CKR(prof_mark(p, 1, s));
     dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
-    mpo_orderA_kernel<<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
+    mpo_orderA_kernel<1><<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
                                                        p->csrA.d_col, p->csrA.d_val, p->mpo_live, 1, 0, 0);
     CK(cudaGetLastError());
     ++*nl;
@@ -956,7 +979,7 @@ static int apply_orderA_z(heff_plan_s* p, const double* psi, double* out, cudaSt
     }
     CKR(prof_mark(p, 1, s));
     dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
-    mpo_orderA_kernel<<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
+    mpo_orderA_kernel<2><<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
                                                        p->csrA.d_col, p->csrA.d_val, nullptr, 2, p->t1_plane,
                                                        p->t3_plane);
     CK(cudaGetLastError());
@@ -1134,7 +1157,7 @@ static int apply_host_pipelined(heff_plan_s* p, const double* psi_host, double* 
   p->g1.N = ncol;
   const int64_t nin = d.kL * d.d1 * d.d2, nout = d.d1 * d.d2 * d.kR;
   dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)d.mL);
-  mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(
+  mpo_orderA_kernel<1><<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(
       p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr, p->csrA.d_col, p->csrA.d_val, p->mpo_live, 1, 0, 0);
   CK(cudaGetLastError());
   ++nl;
@@ -1784,7 +1807,7 @@ static int env_left_impl(const heff_env_dims* dims, const double* L, const doubl
   if (!r) {
     const int nin = (int)(d.kl * d.d), nout = (int)(d.d * d.kr);
     dim3 grid((unsigned)((d.mo + kMpoCols - 1) / kMpoCols), (unsigned)d.mi);
-    mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mo, nin, nout, csr.d_rowptr,
+    mpo_orderA_kernel<1><<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mo, nin, nout, csr.d_rowptr,
                                                                                  csr.d_col, csr.d_val, nullptr, 1, 0, 0);
     dim3 tg((unsigned)((d.mo + 31) / 32), (unsigned)((d.mi * d.d + 31) / 32));
     transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, At, d.mi * d.d, d.mo);
@@ -1864,7 +1887,7 @@ static int env_right_impl(const heff_env_dims* dims, const double* R, const doub
   if (!r) {
     const int nin = (int)(d.d * d.kr), nout = (int)(d.kl * d.d);
     dim3 grid((unsigned)((d.mi + kMpoCols - 1) / kMpoCols), (unsigned)d.mo);
-    mpo_orderA_kernel<<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mi, nin, nout, csr.d_rowptr,
+    mpo_orderA_kernel<1><<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mi, nin, nout, csr.d_rowptr,
                                                                                  csr.d_col, csr.d_val, nullptr, 1, 0, 0);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_right: launch failed");
   }
@@ -2848,7 +2871,11 @@ extern "C" int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const 
 // Frees the calling thread's on-demand workspaces (environment update, GEMM primitive,
 // split and U(1) split arenas) and those of the U(1) split's worker threads.
 static void release_thread_caches() {
-  auto freews = [](SplitWs& w) { cudaFree(w.ptr); w.ptr = nullptr; w.bytes = 0; };
+  auto freews = [](SplitWs& w) {
+    cudaFree(w.ptr);
+    cudaFree(w.sync);
+    w = SplitWs();
+  };
   freews(t_env_splitws);
   freews(t_gemm_ws);
   freews(t_svd_splitws);

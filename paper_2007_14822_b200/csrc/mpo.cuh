@@ -27,6 +27,7 @@ constexpr int kMpoMaxRows = 200;  // k d1 d2 rows staged in shared memory (<= 20
 // Block (b-tile, a'): the nin x width input tile arrives by nin 1-D bulk async copies
 // (one thread issues them, one mbarrier counts the bytes), so the whole tile is in flight
 // at once; odd row pitches fall back to plain coalesced loads.
+template <int PLANES>
 __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* __restrict__ T1, double* __restrict__ T3,
                                                               int64_t mR, int nin, int nout,
                                                               const int* __restrict__ rowptr,
@@ -34,7 +35,7 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
                                                               const double* __restrict__ val,
                                                               const unsigned char* __restrict__ live,
                                                               int planes, int64_t in_plane, int64_t out_plane) {
-  // planes == 2 (complex plans): rows [0, nin/2) come from the real plane of T1 and
+  // PLANES == 2 (complex plans; `planes` must equal PLANES): rows [0, nin/2) come from the real plane of T1 and
   // [nin/2, nin) from the imaginary plane (in_plane doubles further); likewise for T3.
   // The CSR then holds the real 2x2 blocks [[Re, -Im], [Im, Re]] of the complex MPO.
   extern __shared__ __align__(16) double s_in[];  // [nin][kMpoCols]
@@ -43,12 +44,15 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
   // U(1) plans: blocks whose input and output are zero by symmetry are skipped (their T3
   // entries were zeroed once by heff_set_qn)
   if (live && !live[ap * gridDim.x + blockIdx.x]) return;
-  const int nin_p = nin / planes, nout_p = nout / planes;
+  const int nin_p = nin / PLANES, nout_p = nout / PLANES;
   const int64_t b0 = (int64_t)blockIdx.x * kMpoCols;
   const int width = (int)min((int64_t)kMpoCols, mR - b0);
+  const double* in0 = T1 + ap * nin_p * mR + b0;  // row r of plane pl: in0 + pl in_plane + r' mR
+  double* out0 = T3 + ap * nout_p * mR + b0;
   auto in_row = [&](int r) {
-    const int pl = r / nin_p;
-    return T1 + pl * in_plane + (ap * nin_p + (r - pl * nin_p)) * mR + b0;
+    if (PLANES == 1) return in0 + (int64_t)r * mR;
+    const int pl = r >= nin_p;
+    return in0 + pl * in_plane + (int64_t)(r - pl * nin_p) * mR;
   };
   const bool bulk = ((mR & 1) == 0) && ((width & 1) == 0);
   if (bulk) {
@@ -75,8 +79,12 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
     double acc = 0.0;
     const int e1 = __ldg(rowptr + o + 1);
     for (int e = __ldg(rowptr + o); e < e1; ++e) acc = fma(__ldg(val + e), s_in[__ldg(col + e) * kMpoCols + t], acc);
-    const int pl = o / nout_p;
-    __stcs(T3 + pl * out_plane + (ap * nout_p + (o - pl * nout_p)) * mR + b0 + t, acc);
+    if (PLANES == 1) {
+      __stcs(out0 + (int64_t)o * mR + t, acc);
+    } else {
+      const int pl = o >= nout_p;
+      __stcs(out0 + pl * out_plane + (int64_t)(o - pl * nout_p) * mR + t, acc);
+    }
   }
 }
 

@@ -62,3 +62,59 @@ def test_gemm_streamk_toggle_identical_results_tolerance(dev, sk, tile, monkeypa
         torch.cuda.synchronize()
         assert all(torch.equal(outs[0], o) for o in outs[1:])
         assert (outs[0] - ref).abs().max().item() <= 1e-12 * ref.abs().max().item()
+
+
+STREAMK_SHAPES = [(1280, 1024, 256), (1024, 256, 1280), (640, 512, 128), (300, 900, 2000), (20, 4096, 4096),
+                  (5120, 4096, 1024), (129, 130, 1700)]
+
+
+@pytest.mark.parametrize("tile", ["64", "128"])
+def test_streamk_inkernel_fixup_bitwise_equals_fixup_kernel(dev, tile, monkeypatch):
+    """The in-kernel stream-K reduction (highest contributor waits on release/acquire flags)
+    sums the partial tiles in the fixup kernel's order: bitwise the same C, also in
+    accumulate mode and across repeated launches (epoch-tagged flags, ticket reset)."""
+    from paper_2007_14822_b200.heff import gemm
+    monkeypatch.setenv("HEFF_GEMM_TILE", tile)
+    g = torch.Generator(device=dev).manual_seed(11)
+    for (M, N, K) in STREAMK_SHAPES:
+        for bk in (False, True):
+            A = torch.randn(M, K, dtype=torch.float64, device=dev, generator=g)
+            B = torch.randn((N, K) if bk else (K, N), dtype=torch.float64, device=dev, generator=g)
+            C0 = torch.randn(M, N, dtype=torch.float64, device=dev, generator=g)
+            monkeypatch.delenv("HEFF_SK_FIXUP_KERNEL", raising=False)
+            ink = [gemm(A, B, bk) for _ in range(3)]
+            inka = gemm(A, B, bk, C=C0.clone(), accumulate=True)
+            monkeypatch.setenv("HEFF_SK_FIXUP_KERNEL", "1")
+            ref = gemm(A, B, bk)
+            refa = gemm(A, B, bk, C=C0.clone(), accumulate=True)
+            torch.cuda.synchronize()
+            assert all(torch.equal(ref, x) for x in ink), (M, N, K, bk)
+            assert torch.equal(refa, inka), (M, N, K, bk)
+            exact = A @ (B.T if bk else B)
+            assert (ref - exact).abs().max().item() <= 1e-12 * exact.abs().max().item()
+
+
+def test_streamk_concurrent_streams_no_deadlock(dev):
+    """Stream-K GEMMs from two host threads on two streams share the SMs; reducers only wait
+    on CTAs that hold earlier tickets, so this finishes (a wait past ~10 s would trap)."""
+    import threading
+    from paper_2007_14822_b200.heff import gemm
+    g = torch.Generator(device=dev).manual_seed(5)
+    A = torch.randn(1024, 1280, dtype=torch.float64, device=dev, generator=g)
+    B = torch.randn(256, 1280, dtype=torch.float64, device=dev, generator=g)
+    ref = A @ B.T
+    errs = []
+
+    def work():
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            outs = [gemm(A, B, True) for _ in range(50)]
+        s.synchronize()
+        errs.append(max((o - ref).abs().max().item() for o in outs))
+
+    ts = [threading.Thread(target=work) for _ in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    assert len(errs) == 2 and max(errs) <= 1e-12 * ref.abs().max().item()
