@@ -104,6 +104,29 @@ def test_matvec_parity_c4_full_size_sampled_rows(dev, orc):
     assert np.isfinite(e_a)
 
 
+def test_matvec_parity_c5_full_size_sampled_rows(dev, orc):
+    """C5 (Hubbard, m = 8192, d = 4, k = 6: psi 8.6 GB, L and R 3.2 GB each) at full size on
+    one GPU; the oracle computes sampled output rows a' one by one."""
+    from paper_2007_14822_b200 import Heff
+    free, _ = torch.cuda.mem_get_info()
+    if free < 100 * 2**30:
+        pytest.skip("C5 needs ~100 GB of device memory")
+    x = C.make("c5", device=dev)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        out = h.apply(x.psi)
+        torch.cuda.synchronize()
+    mL = x.dims["mL"]
+    rows = sorted({0, mL - 1} | set(np.random.default_rng(7).integers(1, mL - 1, 2).tolist()))
+    outc = out[rows].cpu().numpy()
+    del out
+    L, W1, W2, R, psi = x.numpy()
+    del x
+    torch.cuda.empty_cache()
+    for i, a in enumerate(rows):
+        ref = orc.heff_apply(L, W1, W2, R, psi, rows=(a, a + 1))[0]
+        assert rel(outc[i], ref) <= MATVEC_TOL, (a, rel(outc[i], ref))
+
+
 def test_orderB_virtual_shards(dev, orc):
     from paper_2007_14822_b200 import Heff
     for x, P in ((C.make("c2"), 2), (C.make("c2"), 4), (C.make("c4", m=64), 8),
