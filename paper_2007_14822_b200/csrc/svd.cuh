@@ -226,6 +226,9 @@ __global__ void __launch_bounds__(kSvdGramThreads, 2) svd_gram_kernel(const doub
 // 2x2 block (pair k rows, pair k' columns) of G <- J^T G J depends only on its old values,
 // so a thread updates a whole block at once (the diagonal blocks get the exact rotated
 // 2x2 values), and Q <- Q J by columns.  Output: Qg[p] (row-major 32x32), flag[p].
+#ifdef HEFF_EIG_INSTR
+__device__ long long g_eig_instr[4];
+#endif
 constexpr int kSvdEigThreads = 288;  // 8 warps of 2x2-block updates + 1 warp for the next round's rotations
 
 // FP64 rsqrt / reciprocal: MUFU approximation + two Newton steps (full precision for the
@@ -286,20 +289,37 @@ __device__ __forceinline__ void svd_rot_block(double& x00, double& x01, double& 
   }
 }
 
+// Position layout: G and Q are stored by POSITION, and pair k of every round is positions
+// (k, 31-k).  After a round the column at position i moves to svd_np(i) (0 stays, 1 -> 31,
+// i -> i-1): the circle method of round-robin ordering with the data moving instead of the
+// index tables, so every thread's shared-memory addresses are fixed for the whole kernel.
+// After 31 rounds every column is back at its own position.  (Same rotations, in the same
+// order and arithmetic, as the index-table form: results are bitwise unchanged.)
+__device__ __forceinline__ double svd_lds(uint32_t a) {
+  double x;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a) : "memory");
+  return x;
+}
+__device__ __forceinline__ void svd_lds2(double& x, double& y, uint32_t a) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void svd_sts(uint32_t a, double x) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(x) : "memory");
+}
+__device__ __forceinline__ int svd_np(int i) { return i == 0 ? 0 : (i == 1 ? 31 : i - 1); }
+__device__ __forceinline__ int svd_np_inv(int i) { return i == 0 ? 0 : (i == 31 ? 1 : i + 1); }
+
 __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const double* __restrict__ Gp, int nslots,
                                                                      int64_t C, int gram_grid,
                                                                      double tol, double negl, int inner_sweeps,
                                                                      double* __restrict__ Qg, int* __restrict__ flag,
                                                                      unsigned long long* __restrict__ stat_maxoff,
                                                                      int* __restrict__ stat_nrot) {
-  __shared__ double Gs[2][kSvdPair][kSvdPair + 1];   // ping-pong: round rr reads Gs[rr&1], writes Gs[~]
-  __shared__ double Q[kSvdPair][kSvdPair + 1];
+  __shared__ double Gs[2][kSvdPair][kSvdPair + 1];   // ping-pong by round, position order
+  __shared__ double Qs[2][kSvdPair][kSvdPair + 1];   // Q[row][position], ping-pong by round
   __shared__ double2 s_cs[2][16], s_nn[2][16];       // (c, s) and the rotated diagonal per pair
   __shared__ int s_on[2][16];
-  __shared__ int s_neg[kSvdPair];
-  __shared__ unsigned char s_pa[31][16], s_pb[31][16], s_kof[31][kSvdPair], s_hi[31][kSvdPair];
-  __shared__ uint32_t s_pk1[31][16], s_pk2[31][16];   // per (round, pair of the next round): index chains
-  __shared__ unsigned char s_pk3[31][16];
+  __shared__ int s_neg[kSvdPair];                    // by column
   __shared__ int s_any[kSvdMaxInnerSweeps];          // did inner sweep i rotate anything
   __shared__ double s_off[kSvdEigThreads / 32];
   const int p = blockIdx.x;
@@ -312,28 +332,9 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
     for (int sp = 0; sp < nsum; ++sp) v += gsrc[(int64_t)sp * (kSvdPair * kSvdPair) + e];
     const int r = e >> 5, c = e & 31;
     Gs[0][r][c] = v;
-    Q[r][c] = (r == c) ? 1.0 : 0.0;
-  }
-  for (int e = tid; e < 31 * 16; e += blockDim.x) {  // round-robin (circle method) over 32 columns
-    const int rr = e >> 4, k = e & 15;
-    auto idx = [&](int i) { return i == 0 ? 0 : ((i - 1 + rr) % 31) + 1; };
-    const int a = idx(k), b = idx(31 - k);
-    s_pa[rr][k] = (unsigned char)a;
-    s_pb[rr][k] = (unsigned char)b;
-    s_kof[rr][a] = s_kof[rr][b] = (unsigned char)k;   // which pair of round rr holds column a / b
-    s_hi[rr][a] = 0;
-    s_hi[rr][b] = 1;
+    Qs[0][r][c] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
-  for (int e = tid; e < 31 * 16; e += blockDim.x) {  // the dependent index lookups of the rotation warp
-    const int rr = e >> 4, t = e & 15, r1 = (rr + 1) % 31;
-    const int a = s_pa[r1][t], b = s_pb[r1][t];
-    const int ka = s_kof[rr][a], kb = s_kof[rr][b];
-    s_pk1[rr][t] = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)ka << 16) | ((uint32_t)kb << 24);
-    s_pk2[rr][t] = (uint32_t)s_pa[rr][ka] | ((uint32_t)s_pb[rr][ka] << 8) | ((uint32_t)s_pa[rr][kb] << 16) |
-                   ((uint32_t)s_pb[rr][kb] << 24);
-    s_pk3[rr][t] = (unsigned char)(s_hi[rr][a] | (s_hi[rr][b] << 1));
-  }
   if (tid < kSvdPair) s_neg[tid] = !(Gs[0][tid][tid] > negl);
   __syncthreads();
   double off = 0.0;
@@ -355,10 +356,11 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
   if (!rotate) return;
 
   // Cyclic two-sided Jacobi, one barrier per round: in round rr every thread writes its
-  // 2x2 block of the rotated G into the other buffer and updates Q, while threads 0..15
-  // already compute round rr+1's rotations from the OLD G and round rr's rotations.
-  // Rotations live as (c, s) pairs -- the identity (1, 0) for a skipped pair, so the block
-  // update is branch-free -- plus the exact rotated diagonal (na, nb) and an on flag.
+  // 2x2 block of the rotated G (and two rotated Q entries per row pair) into the other
+  // buffers at the columns' next positions, while the rotation warp already computes round
+  // rr+1's rotations from the OLD G and round rr's rotations.  Rotations live as (c, s)
+  // pairs -- the identity (1, 0) for a skipped pair, so the updates are branch-free -- plus
+  // the exact rotated diagonal (na, nb) and an on flag.
   auto put_rot = [&](int buf, int k, const SvdRot& r) {
     s_cs[buf][k] = make_double2(r.c, r.s);
     s_nn[buf][k] = make_double2(r.na, r.nb);
@@ -372,64 +374,113 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
     x01 = rk.x * y01 - rk.y * y11;
     x11 = rk.y * y01 + rk.x * y11;
   };
-  if (tid < 16) {
-    const int a = s_pa[0][tid], b = s_pb[0][tid];
-    put_rot(0, tid, svd_make_rot(Gs[0][a][a], Gs[0][b][b], Gs[0][a][b], !s_neg[a] && !s_neg[b], tol));
-  }
+  if (tid < 16)  // round 0: the column at position i is column i
+    put_rot(0, tid, svd_make_rot(Gs[0][tid][tid], Gs[0][31 - tid][31 - tid], Gs[0][tid][31 - tid],
+                                 !s_neg[tid] && !s_neg[31 - tid], tol));
   if (tid < kSvdMaxInnerSweeps) s_any[tid] = 0;
   __syncthreads();
+  // update threads (tid < 256): G block (pair k rows, pair kk columns); Q rows k and k + 16 at pair kk
+  const int k = (tid >> 4) & 15, kk = tid & 15;
+  const int ra = k, rb = 31 - k, ca = kk, cb = 31 - kk;
+  const int nra = svd_np(ra), nrb = svd_np(rb), nca = svd_np(ca), ncb = svd_np(cb);
+  // rotation lane pl (tid 256..271): next round's pair pl = positions (pl, 31-pl), whose
+  // columns sit this round at positions pa, pb, in pairs kA, kB (second element if hA / hB)
+  const int pl = tid - 256;
+  const int pa = svd_np_inv(pl & 15), pb = svd_np_inv(31 - (pl & 15));
+  const int kA = min(pa, 31 - pa), kB = min(pb, 31 - pb);
+  const bool hA = pa > 15, hB = pb > 15;
+  // every shared-memory address below is a fixed byte offset from the round's buffer base
+  constexpr uint32_t kBuf = kSvdPair * (kSvdPair + 1) * 8;
+  auto soff = [](int r, int c) { return (uint32_t)((r * (kSvdPair + 1) + c) * 8); };
+  const uint32_t sG = smem_u32(&Gs[0][0][0]), sQ = smem_u32(&Qs[0][0][0]);
+  const uint32_t sCS = smem_u32(&s_cs[0][0]), sNN = smem_u32(&s_nn[0][0]);
+  const uint32_t o_aa = soff(ra, ca), o_ab = soff(ra, cb), o_ba = soff(rb, ca), o_bb = soff(rb, cb);
+  const uint32_t w_aa = soff(nra, nca), w_ab = soff(nra, ncb), w_ba = soff(nrb, nca), w_bb = soff(nrb, ncb);
+  const uint32_t d_ab = soff(ra, rb), dw_aa = soff(nra, nra), dw_bb = soff(nrb, nrb), dw_ab = soff(nra, nrb),
+                 dw_ba = soff(nrb, nra);
+  const uint32_t q0a = soff(k, ca), q0b = soff(k, cb), q1a = soff(k + 16, ca), q1b = soff(k + 16, cb);
+  const uint32_t qw0a = soff(k, nca), qw0b = soff(k, ncb), qw1a = soff(k + 16, nca), qw1b = soff(k + 16, ncb);
+  const uint32_t x_00 = soff(kA, kB), x_01 = soff(kA, 31 - kB), x_10 = soff(31 - kA, kB), x_11 = soff(31 - kA, 31 - kB);
   const int total_rounds = 31 * min(inner_sweeps, kSvdMaxInnerSweeps);
+  int cur = 0;
+#ifdef HEFF_EIG_INSTR  // tools/eigbench: cycles per round (update thread 0, rotation lane 0, whole round)
+  long long ins_t0 = clock64(), ins_upd = 0, ins_rot = 0, ins_round = 0;
+#endif
   for (int it = 0; it < total_rounds; ++it) {
-    const int rr = it % 31, cur = it & 1, nxt = cur ^ 1;
+#ifdef HEFF_EIG_INSTR
+    const long long ins_tb = clock64();
+#endif
+    const int rr = it % 31, nxt = cur ^ 1;
     const int sweep = it / 31;
-    double(*Go)[kSvdPair + 1] = Gs[cur];
-    double(*Gn)[kSvdPair + 1] = Gs[nxt];
-    if (tid < 256) {  // this thread's 2x2 block (pair k rows, pair kk columns)
-      const int k = tid >> 4, kk = tid & 15;
-      const int a = s_pa[rr][k], b = s_pb[rr][k], a2 = s_pa[rr][kk], b2 = s_pb[rr][kk];
+    const uint32_t go = sG + cur * kBuf, gn = sG + nxt * kBuf, qo = sQ + cur * kBuf, qn = sQ + nxt * kBuf;
+    const uint32_t cs = sCS + cur * 256, nnb_ = sNN + cur * 256;
+    if (tid < 256) {
+      double qx, qy;  // rotation of pair kk
+      svd_lds2(qx, qy, cs + kk * 16);
       if (k == kk) {
-        const double2 nn = s_nn[cur][k];
-        Gn[a][a] = nn.x;
-        Gn[b][b] = nn.y;
-        Gn[a][b] = Gn[b][a] = s_on[cur][k] ? 0.0 : Go[a][b];
+        double nx, ny;
+        svd_lds2(nx, ny, nnb_ + k * 16);
+        const double o = s_on[cur][k] ? 0.0 : svd_lds(go + d_ab);
+        svd_sts(gn + dw_aa, nx);
+        svd_sts(gn + dw_bb, ny);
+        svd_sts(gn + dw_ab, o);
+        svd_sts(gn + dw_ba, o);
       } else {
-        double x00 = Go[a][a2], x01 = Go[a][b2], x10 = Go[b][a2], x11 = Go[b][b2];
-        rot2(x00, x01, x10, x11, s_cs[cur][k], s_cs[cur][kk]);
-        Gn[a][a2] = x00; Gn[a][b2] = x01; Gn[b][a2] = x10; Gn[b][b2] = x11;
+        double x00 = svd_lds(go + o_aa), x01 = svd_lds(go + o_ab), x10 = svd_lds(go + o_ba), x11 = svd_lds(go + o_bb);
+        double kx, ky;
+        svd_lds2(kx, ky, cs + k * 16);
+        rot2(x00, x01, x10, x11, make_double2(kx, ky), make_double2(qx, qy));
+        svd_sts(gn + w_aa, x00);
+        svd_sts(gn + w_ab, x01);
+        svd_sts(gn + w_ba, x10);
+        svd_sts(gn + w_bb, x11);
+      }
+      {  // Q <- Q J: columns of pair kk, rows k and k + 16
+        const double a0 = svd_lds(qo + q0a), b0 = svd_lds(qo + q0b), a1 = svd_lds(qo + q1a), b1 = svd_lds(qo + q1b);
+        svd_sts(qn + qw0a, qx * a0 - qy * b0);
+        svd_sts(qn + qw0b, qy * a0 + qx * b0);
+        svd_sts(qn + qw1a, qx * a1 - qy * b1);
+        svd_sts(qn + qw1b, qy * a1 + qx * b1);
       }
       if (tid < 16 && s_on[cur][tid]) s_any[sweep] = 1;
-    }
-    for (int task = tid; task < 32 * 16; task += 256) {  // Q <- Q J (columns, in place)
-      if (tid >= 256) break;
-      const int k = task & 15, r = task >> 4;
-      if (!s_on[cur][k]) continue;
-      const double2 rk = s_cs[cur][k];
-      const int a = s_pa[rr][k], b = s_pb[rr][k];
-      const double qa = Q[r][a], qb = Q[r][b];
-      Q[r][a] = rk.x * qa - rk.y * qb;
-      Q[r][b] = rk.y * qa + rk.x * qb;
-    }
-    const int pl = tid - 256;  // the rotation warp: round rr+1's rotations from the rotated entries
-    if (pl >= 0 && pl < 16 && it + 1 < total_rounds) {
-      const uint32_t p1 = s_pk1[rr][pl], p2 = s_pk2[rr][pl];
-      const int hh = s_pk3[rr][pl];
-      const int a = p1 & 255, b = (p1 >> 8) & 255, ka = (p1 >> 16) & 255, kb = p1 >> 24;
-      const int ax = p2 & 255, bx = (p2 >> 8) & 255, ay = (p2 >> 16) & 255, by = p2 >> 24;
-      const int hx = hh & 1, hy = hh >> 1;
-      const double2 nna = s_nn[cur][ka], nnb = s_nn[cur][kb];
-      const double app = hx ? nna.y : nna.x;                   // rotated diagonals: exact values
-      const double aqq = hy ? nnb.y : nnb.x;
-      // rotated off-diagonal (a, b): a and b sit in different pairs of round rr
-      double x00 = Go[ax][ay], x01 = Go[ax][by], x10 = Go[bx][ay], x11 = Go[bx][by];
-      rot2(x00, x01, x10, x11, s_cs[cur][ka], s_cs[cur][kb]);
-      const double apq = hx ? (hy ? x11 : x10) : (hy ? x01 : x00);
-      put_rot(nxt, pl, svd_make_rot(app, aqq, apq, !s_neg[a] && !s_neg[b], tol));
+#ifdef HEFF_EIG_INSTR
+      if (tid == 0) ins_upd += clock64() - ins_tb;
+#endif
+    } else if (pl < 16 && it + 1 < total_rounds) {
+      double nax, nay, nbx, nby, ckx, cky, ckkx, ckky;
+      svd_lds2(nax, nay, nnb_ + kA * 16);
+      svd_lds2(nbx, nby, nnb_ + kB * 16);
+      svd_lds2(ckx, cky, cs + kA * 16);
+      svd_lds2(ckkx, ckky, cs + kB * 16);
+      const double app = hA ? nay : nax;                       // rotated diagonals: exact values
+      const double aqq = hB ? nby : nbx;
+      // rotated off-diagonal: the two columns sit in different pairs of round rr
+      double x00 = svd_lds(go + x_00), x01 = svd_lds(go + x_01), x10 = svd_lds(go + x_10), x11 = svd_lds(go + x_11);
+      rot2(x00, x01, x10, x11, make_double2(ckx, cky), make_double2(ckkx, ckky));
+      const double apq = hA ? (hB ? x11 : x10) : (hB ? x01 : x00);
+      // the columns at positions pl, 31-pl in round rr+1 (circle method)
+      const int r1 = rr + 1 == 31 ? 0 : rr + 1;
+      int ca1 = pl - 1 + r1, cb1 = 30 - pl + r1;
+      ca1 = pl == 0 ? 0 : (ca1 >= 31 ? ca1 - 31 : ca1) + 1;
+      cb1 = (cb1 >= 31 ? cb1 - 31 : cb1) + 1;
+      put_rot(nxt, pl, svd_make_rot(app, aqq, apq, !s_neg[ca1] && !s_neg[cb1], tol));
+#ifdef HEFF_EIG_INSTR
+      if (pl == 0) ins_rot += clock64() - ins_tb;
+#endif
     }
     __syncthreads();
+#ifdef HEFF_EIG_INSTR
+    ins_round += clock64() - ins_tb;
+#endif
+    cur = nxt;
     if (rr == 30 && !s_any[sweep]) break;  // end of an inner sweep that rotated nothing
   }
   double* q = Qg + (int64_t)p * (kSvdPair * kSvdPair);
-  for (int e = tid; e < kSvdPair * kSvdPair; e += blockDim.x) q[e] = Q[e >> 5][e & 31];
+  for (int e = tid; e < kSvdPair * kSvdPair; e += blockDim.x) q[e] = Qs[cur][e >> 5][e & 31];
+#ifdef HEFF_EIG_INSTR
+  if (p == 0 && tid == 0) { g_eig_instr[0] = ins_upd; g_eig_instr[2] = ins_round; g_eig_instr[3] = clock64() - ins_t0; }
+  if (p == 0 && tid == 256) g_eig_instr[1] = ins_rot;
+#endif
 }
 
 // ---------------------------------------------------------------- rotation
