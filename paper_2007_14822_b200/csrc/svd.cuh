@@ -255,18 +255,23 @@ struct SvdRot {
   int on;
 };
 
-// Jacobi rotation of the 2x2 block [[app, apq], [apq, aqq]]:
-// t = sign(th) om / (|th| + sqrt(th^2 + om^2)), th = aqq - app, om = 2 apq
+// Jacobi rotation of the 2x2 block [[app, apq], [apq, aqq]]: with th = aqq - app,
+// om = 2 apq, r = sqrt(th^2 + om^2) and x = |th| / r (= |cos 2phi|),
+//   c = sqrt((1 + x) / 2),  s = sign(th) om / (2 r c),  t = s / c = sign(th) om / (|th| + r)
+// (the same rotation as t = sign(th) om / (|th| + r), c = 1 / sqrt(1 + t^2), with two
+// dependent reciprocal square roots on the critical path instead of three transcendental
+// steps; c is in [1/sqrt 2, 1], so the half-angle form is well conditioned).
 __device__ __forceinline__ SvdRot svd_make_rot(double app, double aqq, double apq, bool active, double tol) {
   SvdRot r{1.0, 0.0, app, aqq, 0};
   if (active && apq * apq > (tol * tol) * (app * aqq)) {  // |apq| > tol sqrt(app aqq), no sqrt
     const double th = aqq - app, om = 2.0 * apq;
-    const double h2 = fma(th, th, om * om);
-    const double den = fabs(th) + h2 * svd_rsqrt(h2);
-    const double tt = (th >= 0.0 ? om : -om) * svd_rcp(den);
-    const double c = svd_rsqrt(fma(tt, tt, 1.0));
-    r.c = c;
-    r.s = c * tt;
+    const double ir = svd_rsqrt(fma(th, th, om * om));      // 1 / r
+    const double y = fma(0.5 * fabs(th), ir, 0.5);          // c^2 = (1 + x) / 2
+    const double ry = svd_rsqrt(y);                          // 1 / c
+    const double so = (th >= 0.0 ? om : -om) * (0.5 * ir);   // sign(th) om / (2 r)
+    const double tt = so * (ry * ry);                        // t = s / c
+    r.c = y * ry;
+    r.s = so * ry;
     r.na = app - tt * apq;
     r.nb = aqq + tt * apq;
     r.on = 1;
