@@ -84,6 +84,8 @@ typedef struct {
 /* Lanczos options (readings R11-R14).
  *   mode 0 (fixed): exactly max_iter matvecs unless an invariant subspace is hit;
  *   mode 1 (converge): stop when beta_j |y_j[last]| <= tol * hnorm_j, or at max_iter.
+ *     Vectors of <= 2^20 doubles run up to 3 steps past that point before the host sees the
+ *     scalars (HEFF_LANCZOS_BATCH=1 disables); the result is that of the stopping step.
  * alpha_out, beta_out, theta_out: optional HOST arrays of >= max_iter doubles receiving
  * the tridiagonal T_j and the lowest Ritz value after every step. */
 typedef struct {

@@ -1613,13 +1613,27 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       if (host_check(j)) break;
     }
   } else {
-    for (int j = 1; j <= cap; ++j) {
-      CKR(step(j));
-      CK(cudaMemcpyAsync(&ha[j - 1], alpha + (j - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(&hb[j - 1], beta + (j - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+    // Converge mode.  Small vectors (<= 2^20 doubles, steps of ~0.1 ms) enqueue `batch`
+    // steps per host round trip and test them in order: the stopping step j_done, T_j and
+    // the Ritz vector are exactly those of a per-step check (the extra steps' vectors and
+    // scalars are never read); only the read-back latency is amortised.
+    int batch = nr <= (int64_t(1) << 20) ? 4 : 1;
+    if (const char* e = getenv("HEFF_LANCZOS_BATCH")) batch = std::max(1, atoi(e));
+    bool stop = false;
+    for (int j = 1; j <= cap && !stop;) {
+      const int j1 = std::min(cap, j + batch - 1);
+      for (int jj = j; jj <= j1; ++jj) CKR(step(jj));
+      CK(cudaMemcpyAsync(&ha[j - 1], alpha + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(&hb[j - 1], beta + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      j_done = j;
-      if (host_check(j)) break;
+      for (int jj = j; jj <= j1; ++jj) {
+        j_done = jj;
+        if (host_check(jj)) {
+          stop = true;
+          break;
+        }
+      }
+      j = j1 + 1;
     }
   }
   if (o->alpha_out) memcpy(o->alpha_out, ha.data(), sizeof(double) * j_done);

@@ -196,6 +196,22 @@ def gpu_lanczos(x, dev, max_iter, tol=0.0, converge=False):
         return r, v.cpu().numpy()
 
 
+@pytest.mark.parametrize("name,tol", [("c1", 1e-10), ("c2", 1e-10), ("two_site", 1e-12), ("ragged_odd", 1e-9)])
+def test_lanczos_converge_batched_checks_are_exact(dev, name, tol, monkeypatch):
+    """Converge mode on small vectors runs up to 3 steps ahead of the host's residual test;
+    the stopping step, T_j, energy and Ritz vector must be bitwise those of per-step checks
+    (including an early invariant-subspace stop: the two-site singlet problem)."""
+    x = CASES[name]()
+    monkeypatch.setenv("HEFF_LANCZOS_BATCH", "1")
+    r1, v1 = gpu_lanczos(x, dev, 60, tol=tol, converge=True)
+    for b in ("4", "7"):
+        monkeypatch.setenv("HEFF_LANCZOS_BATCH", b)
+        rb, vb = gpu_lanczos(x, dev, 60, tol=tol, converge=True)
+        assert rb.iters == r1.iters and rb.energy == r1.energy, (b, rb.iters, r1.iters)
+        assert rb.alpha == r1.alpha and rb.beta == r1.beta and rb.thetas == r1.thetas
+        assert np.array_equal(vb, v1)
+
+
 @pytest.mark.parametrize("name,steps", [("c1", 20), ("c1_n8", 20), ("c3", 6)])
 def test_lanczos_fixed_steps_parity(dev, orc, name, steps):
     x = C.make(name)
