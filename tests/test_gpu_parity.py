@@ -267,6 +267,29 @@ def test_lanczos_zero_vector_and_errors(dev):
         Heff(bad, x.W1, x.W2, x.R)
 
 
+def test_c_abi_rejects_degenerate_dims(dev):
+    """heff_create through the C ABI: any zero or negative extent is HEFF_EINVAL with a
+    message, null tensors too; nothing is allocated or launched."""
+    import ctypes
+    from paper_2007_14822_b200 import heff
+    x = C.make("c1").to(dev)
+    good = [16, 2, 2, 16, 5, 5, 5]
+    for i in range(7):
+        for bad in (0, -3):
+            dims = list(good)
+            dims[i] = bad
+            d = heff._Dims(*dims)
+            plan = ctypes.c_void_p()
+            rc = heff.lib().heff_create(ctypes.byref(plan), ctypes.byref(d), x.L.data_ptr(), x.W1.data_ptr(), x.W2.data_ptr(),
+                                        x.R.data_ptr(), None, None)
+            assert rc == -1, (i, bad, rc)                  # HEFF_EINVAL
+            assert heff.lib().heff_last_error()
+    d = heff._Dims(*good)
+    plan = ctypes.c_void_p()
+    assert heff.lib().heff_create(ctypes.byref(plan), ctypes.byref(d), None, x.W1.data_ptr(), x.W2.data_ptr(),
+                                  x.R.data_ptr(), None, None) == -1
+
+
 def test_lanczos_nccl_single_rank(dev, orc):
     """The communicating (order B + NCCL) Lanczos path with one rank on one GPU."""
     from paper_2007_14822_b200 import Heff, nccl_unique_id
