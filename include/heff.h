@@ -228,6 +228,12 @@ enum { HEFF_OPT_SPARSE_KBLOCKS = 6 }; /* get: scheduled (tile, 16-wide k-block) 
  * nb % 16 == 0 and nranks <= 8; real, non-U(1) plans. */
 enum { HEFF_OPT_FUSED_GATHER = 7 };
 
+/* HEFF_OPT_LANCZOS_RESERVE = n (set only): allocate lanczos_ground's Krylov workspace for
+ * n iterations now (synchronous), so later calls with max_iter <= n allocate nothing --
+ * keeps cudaMalloc/cudaFree out of timed or latency-critical calls.  Collective for
+ * gather-fused sharded plans (the symmetric window is registered on every rank). */
+enum { HEFF_OPT_LANCZOS_RESERVE = 8 };
+
 /* ---- Environment update --------------------------------------
  * After each local eigensolve a DMRG sweep moves the window one site and grows the
  * environment by that site (Sec. 6.2; SPEC ProjMPO):

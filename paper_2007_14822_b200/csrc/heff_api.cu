@@ -807,6 +807,12 @@ extern "C" int heff_create_z(heff_plan* out, const heff_dims* dims, const double
   return HEFF_OK;
 }
 
+struct LanczosLayout {  // see lanczos_workspace
+  bool compact, cplx, fgather;
+  int64_t n_dense, n, nr, ldv;
+};
+static int lanczos_workspace(heff_plan_s* p, int cap, cudaStream_t s, LanczosLayout* out);
+
 extern "C" int heff_set_option(heff_plan p, int option, int64_t value) {
   if (!p) return set_err(HEFF_EINVAL, "null plan");
   switch (option) {
@@ -826,6 +832,14 @@ extern "C" int heff_set_option(heff_plan p, int option, int64_t value) {
         return set_err(HEFF_EUNSUPPORTED, "fused gather: communicating b'-sharded plans only");
       p->fused_gather = value ? 1 : 0;
       return HEFF_OK;
+    case HEFF_OPT_LANCZOS_RESERVE: {
+      if (value < 1 || value > 100000) return set_err(HEFF_EINVAL, "lanczos reserve: 1 <= iterations <= 100000");
+      LanczosLayout lay;
+      const int r = lanczos_workspace(p, (int)value, nullptr, &lay);
+      if (r != HEFF_OK) return r;
+      CK(cudaDeviceSynchronize());
+      return HEFF_OK;
+    }
     default:
       return set_err(HEFF_EINVAL, "unknown option %d", option);
   }
@@ -1423,13 +1437,10 @@ static int ensure_window(heff_plan_s* p, int cap, int64_t ldv, cudaStream_t s) {
   return HEFF_OK;
 }
 
-extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts* o, double* energy, int* iters_done,
-                              double* resid_est, heff_stream stream) {
-  if (!p || !psi || !o || !energy) return set_err(HEFF_EINVAL, "lanczos_ground: null argument");
-  if (o->max_iter < 1 || o->max_iter > 100000) return set_err(HEFF_EINVAL, "lanczos_ground: max_iter out of range");
-  if (o->mode != 0 && o->mode != 1) return set_err(HEFF_EINVAL, "lanczos_ground: mode must be 0 or 1");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int cap = o->max_iter;
+// Krylov workspace of lanczos_ground for `cap` iterations: the basis (or the NCCL window of
+// the gather-fused path), scalars, work vector, U(1) scatter buffers and the sharded gather
+// buffers; allocated on first need and grown, never inside a call that fits.
+static int lanczos_workspace(heff_plan_s* p, int cap, cudaStream_t s, LanczosLayout* out) {
   // U(1) plans iterate on the sector's entries only (gather/scatter around each matvec)
   const bool compact = p->qn_idx != nullptr && !p->sharded && p->terms.empty();
   const int64_t n_dense = vec_len(p);
@@ -1474,6 +1485,21 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     CK(cudaMalloc(&p->full, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
     if (p->nranks > 1) CK(cudaMalloc(&p->gather, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
   }
+  *out = LanczosLayout{compact, cplx, fgather, n_dense, n, nr, ldv};
+  return HEFF_OK;
+}
+
+extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts* o, double* energy, int* iters_done,
+                              double* resid_est, heff_stream stream) {
+  if (!p || !psi || !o || !energy) return set_err(HEFF_EINVAL, "lanczos_ground: null argument");
+  if (o->max_iter < 1 || o->max_iter > 100000) return set_err(HEFF_EINVAL, "lanczos_ground: max_iter out of range");
+  if (o->mode != 0 && o->mode != 1) return set_err(HEFF_EINVAL, "lanczos_ground: mode must be 0 or 1");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int cap = o->max_iter;
+  LanczosLayout lay;
+  CKR(lanczos_workspace(p, cap, s, &lay));
+  const bool compact = lay.compact, cplx = lay.cplx, fgather = lay.fgather;
+  const int64_t n_dense = lay.n_dense, n = lay.n, nr = lay.nr, ldv = lay.ldv;
   double* c1 = p->scal;                              // 2 (cap+1): room for complex coefficients
   double* c2 = c1 + 2 * (cap + 1);
   double* alpha = c2 + 2 * (cap + 1);

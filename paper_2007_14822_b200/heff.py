@@ -19,6 +19,7 @@ LIB_PATH = _PKG / "libheff.so"
 HEFF_OK, HEFF_EINVAL, HEFF_ENOMEM, HEFF_ECUDA, HEFF_ENCCL, HEFF_EZERO, HEFF_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 HEFF_ENOCONV = -7
 OPT_GEMM_PATH, OPT_LAST_KERNEL_COUNT, OPT_MPO_NNZ, OPT_PROFILE, OPT_TOTAL_LAUNCHES, OPT_SPARSE_KBLOCKS = 1, 2, 3, 4, 5, 6
+OPT_LANCZOS_RESERVE = 8
 OPT_FUSED_GATHER = 7
 
 

@@ -267,6 +267,23 @@ def test_lanczos_zero_vector_and_errors(dev):
         Heff(bad, x.W1, x.W2, x.R)
 
 
+def test_lanczos_reserve_option(dev):
+    """HEFF_OPT_LANCZOS_RESERVE pre-allocates the Krylov workspace; results are unchanged
+    and out-of-range values are rejected."""
+    from paper_2007_14822_b200 import Heff, HeffError
+    from paper_2007_14822_b200.heff import OPT_LANCZOS_RESERVE
+    x = C.make("c2").to(dev)
+    r0, v0 = gpu_lanczos(C.make("c2"), dev, 12)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        h.set_option(OPT_LANCZOS_RESERVE, 20)
+        v = x.psi.clone()
+        r = h.lanczos_ground(v, max_iter=12)
+        assert r.energy == r0.energy and np.array_equal(v.cpu().numpy(), v0)
+        for bad in (0, -1, 10**6):
+            with pytest.raises(HeffError):
+                h.set_option(OPT_LANCZOS_RESERVE, bad)
+
+
 def test_c_abi_rejects_degenerate_dims(dev):
     """heff_create through the C ABI: any zero or negative extent is HEFF_EINVAL with a
     message, null tensors too; nothing is allocated or launched."""
