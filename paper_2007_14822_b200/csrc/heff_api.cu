@@ -893,6 +893,19 @@ extern "C" int heff_last_timings(heff_plan p, float* g1, float* mpo, float* g4, 
   return HEFF_OK;
 }
 
+// Order-A MPO step on real data (one (a', 128-column) tile per block, two resident blocks
+// per SM at C4: a persistent double-buffered variant with one block per SM measured 1.8x
+// slower at C4 and was dropped).
+static int launch_mpo_A(const double* T1, double* T3, int64_t mR, int64_t rows, int nin, int nout, const Csr& csr,
+                        const unsigned char* live, cudaStream_t s) {
+  if (rows <= 0 || mR <= 0) return HEFF_OK;
+  dim3 grid((unsigned)((mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
+  mpo_orderA_kernel<1><<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(
+      T1, T3, mR, nin, nout, csr.d_rowptr, csr.d_col, csr.d_val, live, 1, 0, 0);
+  CK(cudaGetLastError());
+  return HEFF_OK;
+}
+
 // --------------------------------------------------------------------------- the matvec
 static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl, int accumulate) {
   const heff_dims& d = p->dims;
@@ -907,10 +920,7 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     p->g1.C = p->T1;
     CKR(launch_gemm(p->g1, p->gemm_path, s, nl, &p->splitws));
     CKR(prof_mark(p, 1, s));
-    dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
-    mpo_orderA_kernel<1><<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
-                                                       p->csrA.d_col, p->csrA.d_val, p->mpo_live, 1, 0, 0);
-    CK(cudaGetLastError());
+    CKR(launch_mpo_A(p->T1, p->T3, d.mR, rows, (int)nin, (int)nout, p->csrA, p->mpo_live, s));
     ++*nl;
     CKR(prof_mark(p, 2, s));
     p->g4.M = rows * d.d1 * d.d2;
@@ -1170,10 +1180,7 @@ static int apply_host_pipelined(heff_plan_s* p, const double* psi_host, double* 
   }
   p->g1.N = ncol;
   const int64_t nin = d.kL * d.d1 * d.d2, nout = d.d1 * d.d2 * d.kR;
-  dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)d.mL);
-  mpo_orderA_kernel<1><<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(
-      p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr, p->csrA.d_col, p->csrA.d_val, p->mpo_live, 1, 0, 0);
-  CK(cudaGetLastError());
+  CKR(launch_mpo_A(p->T1, p->T3, d.mR, d.mL, (int)nin, (int)nout, p->csrA, p->mpo_live, s));
   ++nl;
   for (int k = 0; k < kE2eChunks; ++k) {
     const int64_t r0 = nrow4 * k / kE2eChunks, r1 = nrow4 * (k + 1) / kE2eChunks;
@@ -1846,9 +1853,7 @@ static int env_left_impl(const heff_env_dims* dims, const double* L, const doubl
   r = launch_gemm(g1, 0, s, &nl, &t_env_splitws);
   if (!r) {
     const int nin = (int)(d.kl * d.d), nout = (int)(d.d * d.kr);
-    dim3 grid((unsigned)((d.mo + kMpoCols - 1) / kMpoCols), (unsigned)d.mi);
-    mpo_orderA_kernel<1><<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mo, nin, nout, csr.d_rowptr,
-                                                                                 csr.d_col, csr.d_val, nullptr, 1, 0, 0);
+    r = launch_mpo_A(X, Y, d.mo, d.mi, nin, nout, csr, nullptr, s);
     dim3 tg((unsigned)((d.mo + 31) / 32), (unsigned)((d.mi * d.d + 31) / 32));
     transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, At, d.mi * d.d, d.mo);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_left: launch failed");
@@ -1926,9 +1931,7 @@ static int env_right_impl(const heff_env_dims* dims, const double* R, const doub
   r = launch_gemm(g1, 0, s, &nl, &t_env_splitws);
   if (!r) {
     const int nin = (int)(d.d * d.kr), nout = (int)(d.kl * d.d);
-    dim3 grid((unsigned)((d.mi + kMpoCols - 1) / kMpoCols), (unsigned)d.mo);
-    mpo_orderA_kernel<1><<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(X, Y, d.mi, nin, nout, csr.d_rowptr,
-                                                                                 csr.d_col, csr.d_val, nullptr, 1, 0, 0);
+    r = launch_mpo_A(X, Y, d.mi, d.mo, nin, nout, csr, nullptr, s);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_right: launch failed");
   }
   if (!r) r = launch_gemm(g3, 0, s, &nl, &t_env_splitws);
