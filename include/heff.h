@@ -38,7 +38,10 @@
  * thread-local message for the last failure.  There is no CPU fallback: a missing or
  * failing device is an error.
  *
- * Concurrency: one plan per host thread at a time.
+ * Concurrency: one plan per host thread at a time, and a plan's calls on one stream at a
+ * time (its GEMMs share one stream-K partial-tile workspace and one CTA ticket counter);
+ * different plans, and the free functions on different host threads, may run
+ * concurrently on different streams.
  */
 #ifndef HEFF_H
 #define HEFF_H
