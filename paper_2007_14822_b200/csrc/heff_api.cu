@@ -206,6 +206,17 @@ struct SplitWs {  // stream-K partial-tile workspace, grown on demand
 };
 constexpr int kSkMaxGrid = 1024;
 
+// Per-thread, per-stream workspaces for the free functions (heff_gemm, environment
+// updates): GEMMs enqueued by one thread on two streams may run concurrently and must not
+// share partial slots or the CTA ticket counter.
+using StreamWs = std::vector<std::pair<cudaStream_t, SplitWs>>;
+static SplitWs* ws_for(StreamWs& v, cudaStream_t s) {
+  for (auto& e : v)
+    if (e.first == s) return &e.second;
+  v.emplace_back(s, SplitWs());
+  return &v.back().second;
+}
+
 // HEFF_SK_FIXUP_KERNEL=1: sum split tiles in the separate streamk_fixup_kernel instead of in-kernel
 static bool sk_inkernel() { return getenv("HEFF_SK_FIXUP_KERNEL") == nullptr; }
 
@@ -1708,7 +1719,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
 //   left:  X = L.A (NN GEMM) -> Y = W.X (MPO kernel, single-site CSR) -> Lout = A^T.Y (NN GEMM
 //          on an explicitly transposed A)
 //   right: X = B.R (NN GEMM) -> Y = W.X (MPO kernel) -> Rout = Y.B^T (NT GEMM)
-static thread_local SplitWs t_env_splitws;
+static thread_local StreamWs t_env_splitws;
 
 // Per-thread workspace of the environment updates, grown on demand and kept (no
 // cudaMalloc/cudaFree per call; each call synchronises its stream before returning).
@@ -1850,7 +1861,7 @@ static int env_left_impl(const heff_env_dims* dims, const double* L, const doubl
                      kblock_values(g3.K, [&](int64_t k) { return qn->q_in[k / d.d] + qn->qs[k % d.d]; }),
                      &t_env_sp3));
   }
-  r = launch_gemm(g1, 0, s, &nl, &t_env_splitws);
+  r = launch_gemm(g1, 0, s, &nl, ws_for(t_env_splitws, s));
   if (!r) {
     const int nin = (int)(d.kl * d.d), nout = (int)(d.d * d.kr);
     r = launch_mpo_A(X, Y, d.mo, d.mi, nin, nout, csr, nullptr, s);
@@ -1858,7 +1869,7 @@ static int env_left_impl(const heff_env_dims* dims, const double* L, const doubl
     transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, At, d.mi * d.d, d.mo);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_left: launch failed");
   }
-  if (!r) r = launch_gemm(g3, 0, s, &nl, &t_env_splitws);
+  if (!r) r = launch_gemm(g3, 0, s, &nl, ws_for(t_env_splitws, s));
   cleanup();
   return r;
 }
@@ -1928,13 +1939,13 @@ static int env_right_impl(const heff_env_dims* dims, const double* R, const doub
                      kblock_values(g3.K, [&](int64_t k) { return qn->q_in[k % d.mi] - qn->qs[k / d.mi]; }),
                      &t_env_sp3));
   }
-  r = launch_gemm(g1, 0, s, &nl, &t_env_splitws);
+  r = launch_gemm(g1, 0, s, &nl, ws_for(t_env_splitws, s));
   if (!r) {
     const int nin = (int)(d.d * d.kr), nout = (int)(d.kl * d.d);
     r = launch_mpo_A(X, Y, d.mi, d.mo, nin, nout, csr, nullptr, s);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_right: launch failed");
   }
-  if (!r) r = launch_gemm(g3, 0, s, &nl, &t_env_splitws);
+  if (!r) r = launch_gemm(g3, 0, s, &nl, ws_for(t_env_splitws, s));
   cleanup();
   return r;
 }
@@ -1963,7 +1974,7 @@ extern "C" int heff_tridiag_lowest(int j, const double* alpha, const double* bet
 
 // The FP64 GEMM primitive of the hot path, exposed for kernel-level tests and reuse:
 // C[M][N] (+)= A[M][K] . op(B), op(B) = B[K][N] (b_kmajor = 0) or B[N][K]^T (b_kmajor = 1).
-static thread_local SplitWs t_gemm_ws;
+static thread_local StreamWs t_gemm_ws;
 extern "C" int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
                          int b_kmajor, double* C, int64_t ldc, int accumulate, int path, heff_stream stream) {
   if (M < 0 || N < 0 || K < 0 || !A || !B || !C || path < 0 || path > 2)
@@ -1973,13 +1984,16 @@ extern "C" int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64
   g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.b_kmajor = b_kmajor != 0;
   g.C = C; g.ldc = ldc; g.accumulate = accumulate ? 1 : 0;
   int nl = 0;
-  return launch_gemm(g, path, reinterpret_cast<cudaStream_t>(stream), &nl, &t_gemm_ws);
+  const cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  return launch_gemm(g, path, cs, &nl, ws_for(t_gemm_ws, cs));
 }
 
-// debug: copy the calling thread's heff_gemm stream-K workspace (partial tiles) to dst
+// debug: copy the calling thread's heff_gemm stream-K workspace (partial tiles of its
+// first stream) to dst
 extern "C" int heff_debug_gemm_ws(double* dst, size_t bytes) {
-  if (!t_gemm_ws.ptr) return set_err(HEFF_EINVAL, "no workspace");
-  CK(cudaMemcpy(dst, t_gemm_ws.ptr, std::min(bytes, t_gemm_ws.bytes), cudaMemcpyDeviceToDevice));
+  if (t_gemm_ws.empty() || !t_gemm_ws[0].second.ptr) return set_err(HEFF_EINVAL, "no workspace");
+  const SplitWs& w = t_gemm_ws[0].second;
+  CK(cudaMemcpy(dst, w.ptr, std::min(bytes, w.bytes), cudaMemcpyDeviceToDevice));
   return HEFF_OK;
 }
 
@@ -2919,8 +2933,10 @@ static void release_thread_caches() {
     cudaFree(w.sync);
     w = SplitWs();
   };
-  freews(t_env_splitws);
-  freews(t_gemm_ws);
+  for (auto& e : t_env_splitws) freews(e.second);
+  t_env_splitws.clear();
+  for (auto& e : t_gemm_ws) freews(e.second);
+  t_gemm_ws.clear();
   freews(t_svd_splitws);
   cudaFree(t_env_arena.buf); cudaFree(t_env_arena.rowptr); cudaFree(t_env_arena.col); cudaFree(t_env_arena.val);
   t_env_arena = EnvArena();

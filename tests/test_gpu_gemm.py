@@ -118,3 +118,28 @@ def test_streamk_concurrent_streams_no_deadlock(dev):
     for t in ts:
         t.join(timeout=120)
     assert len(errs) == 2 and max(errs) <= 1e-12 * ref.abs().max().item()
+
+
+def test_streamk_one_thread_two_streams(dev):
+    """One host thread enqueues stream-K GEMMs on two streams without synchronising: each
+    stream gets its own partial-tile workspace and ticket counter, so the concurrently
+    running kernels neither mix partial tiles nor wait on each other's CTAs."""
+    from paper_2007_14822_b200.heff import gemm
+    g = torch.Generator(device=dev).manual_seed(9)
+    A = torch.randn(1024, 1280, dtype=torch.float64, device=dev, generator=g)
+    B = torch.randn(256, 1280, dtype=torch.float64, device=dev, generator=g)
+    A2 = torch.randn(1280, 256, dtype=torch.float64, device=dev, generator=g)
+    B2 = torch.randn(256, 1024, dtype=torch.float64, device=dev, generator=g)
+    ref1, ref2 = A @ B.T, A2 @ B2
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    torch.cuda.synchronize()
+    for _ in range(30):
+        with torch.cuda.stream(s1):          # C allocated, zeroed and written on s1
+            outs.append((1, gemm(A, B, True)))
+        with torch.cuda.stream(s2):
+            outs.append((2, gemm(A2, B2, False)))
+    torch.cuda.synchronize()
+    for k, o in outs:
+        ref = ref1 if k == 1 else ref2
+        assert (o - ref).abs().max().item() <= 1e-12 * ref.abs().max().item()
