@@ -151,6 +151,8 @@ int heff_create_sum(heff_plan* out, const heff_plan* terms, int nterms);
  * penalty.  Not supported on b'-sharded plans (HEFF_EUNSUPPORTED). */
 int heff_set_penalty(heff_plan p, const double* phis, int nphi, double weight, heff_stream stream);
 
+/* Destroys a plan (synchronises the device; workspace blocks go to the cache described at
+ * heff_release_caches). */
 int heff_destroy(heff_plan p);
 
 /* Thread-local message describing the last failure on this thread ("" if none). */
@@ -317,8 +319,12 @@ int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const int* qrow, 
                       int64_t* n_kept, double* trunc_err, int* sweeps, heff_stream stream);
 
 /* Frees the on-demand workspaces that heff_env_update_*, heff_gemm, heff_svd_split and
- * heff_svd_split_qn keep per host thread (and those of the U(1) split's worker threads);
- * they are re-allocated by the next call.  Synchronises the device. */
+ * heff_svd_split_qn keep per host thread (and those of the U(1) split's worker threads),
+ * and the workspace cache of destroyed plans on the current device (heff_destroy returns
+ * a plan's intermediates, Krylov basis and staging buffers to a process-wide cache -- blocks
+ * up to 4 GB, 16 GB in total -- that the next heff_create / lanczos_ground reuses: a DMRG
+ * sweep builds one plan per bond); they are re-allocated by the next call.  Synchronises
+ * the device. */
 int heff_release_caches(void);
 
 /* Host-only (no device work): the truncation rule heff_svd_split applies, on HOST values

@@ -16,6 +16,7 @@
 #include <condition_variable>
 #include <functional>
 #include <mutex>
+#include <unordered_map>
 #include <thread>
 #include <map>
 #include <string>
@@ -552,6 +553,105 @@ extern "C" size_t heff_workspace_bytes(const heff_dims* d, const heff_dist* dist
   return sizeof(double) * (size_t)(d->mL * (d->kL + d->kR) * d->d1 * d->d2 * d->mR);
 }
 
+// ----------------------------------------------------------------------- workspace cache
+// Plan workspaces (intermediates, Krylov basis, staging and scatter buffers) are taken
+// from and returned to a process-wide cache of device blocks: a DMRG sweep creates and
+// destroys one plan per bond, and cudaMalloc/cudaFree of ~GB buffers (cudaFree also
+// synchronises the device) cost 5-8 ms per bond at m = 256-1024 against 1-40 ms of
+// Lanczos.  A request takes the smallest cached block of the same device with
+// bytes <= size <= 2 bytes + 64 MB; heff_destroy synchronises the device and returns its
+// blocks (blocks up to 4 GB, 16 GB in total, are kept; others are freed); heff_release_caches
+// frees them all.
+// An allocation that fails frees the cache and retries.
+struct WsBlock {
+  void* p;
+  size_t bytes;
+  int dev;
+};
+static std::mutex g_ws_mu;
+static std::vector<WsBlock> g_ws_free;                      // cached, idle
+static std::unordered_map<void*, WsBlock> g_ws_live;        // handed out
+static size_t g_ws_cached = 0;
+constexpr size_t kWsCacheMax = size_t(16) << 30;   // idle bytes kept, all devices
+constexpr size_t kWsBlockMax = size_t(4) << 30;    // larger blocks are freed, not cached
+
+static void ws_cache_trim(int dev) {  // caller holds g_ws_mu
+  for (size_t i = 0; i < g_ws_free.size();) {
+    if (dev < 0 || g_ws_free[i].dev == dev) {
+      cudaFree(g_ws_free[i].p);
+      g_ws_cached -= g_ws_free[i].bytes;
+      g_ws_free[i] = g_ws_free.back();
+      g_ws_free.pop_back();
+    } else {
+      ++i;
+    }
+  }
+}
+
+template <typename T>
+static cudaError_t ws_malloc(T** out, size_t bytes) {
+  *out = nullptr;
+  if (bytes == 0) bytes = 256;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  int best = -1;
+  for (int i = 0; i < (int)g_ws_free.size(); ++i) {
+    const WsBlock& b = g_ws_free[i];
+    if (b.dev == dev && b.bytes >= bytes && b.bytes <= 2 * bytes + (size_t(64) << 20) &&
+        (best < 0 || b.bytes < g_ws_free[best].bytes))
+      best = i;
+  }
+  if (best >= 0) {
+    const WsBlock b = g_ws_free[best];
+    g_ws_free[best] = g_ws_free.back();
+    g_ws_free.pop_back();
+    g_ws_cached -= b.bytes;
+    g_ws_live[b.p] = b;
+    *out = static_cast<T*>(b.p);
+    return cudaSuccess;
+  }
+  void* ptr = nullptr;
+  cudaError_t e = cudaMalloc(&ptr, bytes);
+  if (e == cudaErrorMemoryAllocation && !g_ws_free.empty()) {
+    cudaGetLastError();
+    ws_cache_trim(dev);
+    e = cudaMalloc(&ptr, bytes);
+  }
+  if (e != cudaSuccess) return e;
+  g_ws_live[ptr] = WsBlock{ptr, bytes, dev};
+  *out = static_cast<T*>(ptr);
+  return cudaSuccess;
+}
+
+// Return a block to the cache.  The caller guarantees no pending device work uses it.
+static void ws_release(void* ptr) {
+  if (!ptr) return;
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  auto it = g_ws_live.find(ptr);
+  if (it == g_ws_live.end()) {  // not a cache block
+    cudaFree(ptr);
+    return;
+  }
+  const WsBlock b = it->second;
+  g_ws_live.erase(it);
+  if (b.bytes <= kWsBlockMax && g_ws_cached + b.bytes <= kWsCacheMax) {
+    g_ws_free.push_back(b);
+    g_ws_cached += b.bytes;
+  } else {
+    cudaFree(b.p);
+  }
+}
+
+// Bytes held idle by the cache on `dev` (counted as available by the workspace budget).
+static size_t ws_cached_bytes(int dev) {
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  size_t t = 0;
+  for (const auto& b : g_ws_free)
+    if (b.dev == dev) t += b.bytes;
+  return t;
+}
+
 static void free_csr(Csr& c) {
   cudaFree(c.d_rowptr);
   cudaFree(c.d_col);
@@ -561,10 +661,14 @@ static void free_csr(Csr& c) {
 
 extern "C" int heff_destroy(heff_plan p) {
   if (!p) return HEFF_OK;
-  cudaFree(p->T1); cudaFree(p->T3); cudaFree(p->V1); cudaFree(p->V3);
-  cudaFree(p->stage_in); cudaFree(p->stage_out);
-  cudaFree(p->basis); cudaFree(p->work); cudaFree(p->full); cudaFree(p->gather);
-  cudaFree(p->partial); cudaFree(p->scal);
+  cudaDeviceSynchronize();  // no kernel of this plan may still use a block handed back to the cache
+  for (void* b : {(void*)p->T1, (void*)p->T3, (void*)p->V1, (void*)p->V3, (void*)p->stage_in, (void*)p->stage_out,
+                  (void*)p->basis, (void*)p->work, (void*)p->full, (void*)p->gather, (void*)p->partial,
+                  (void*)p->scal, (void*)p->Lp, (void*)p->Rp, (void*)p->zin, (void*)p->zout, (void*)p->dense_in,
+                  (void*)p->dense_out})
+    ws_release(b);
+  cudaFree(p->mpo_live);
+  cudaFree(p->qn_idx);
   cudaFree(p->splitws.ptr);
   cudaFree(p->splitws.sync);
   cudaFree(p->phis); cudaFree(p->pen_scratch);
@@ -645,6 +749,11 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
     const int64_t per_row = (d.kL + d.kR) * d.d1 * d.d2 * d.mR * 8;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return fail(set_err(HEFF_ECUDA, "cudaMemGetInfo failed"));
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      free_b += ws_cached_bytes(dev);  // idle cached blocks are available to this plan
+    }
     int64_t budget = (int64_t)(0.45 * (double)free_b);
     if (const char* e = getenv("HEFF_WORKSPACE_MB")) budget = std::atoll(e) * (1ll << 20);
     int64_t rows = std::max<int64_t>(1, std::min<int64_t>(d.mL, budget / per_row));
@@ -652,8 +761,8 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
     const int64_t nchunks = (d.mL + rows - 1) / rows;
     rows = (d.mL + nchunks - 1) / nchunks;
     p->chunk_rows = rows;
-    if (cudaMalloc(&p->T1, sizeof(double) * rows * d.kL * d.d1 * d.d2 * d.mR) != cudaSuccess ||
-        cudaMalloc(&p->T3, sizeof(double) * rows * d.d1 * d.d2 * d.kR * d.mR) != cudaSuccess)
+    if (ws_malloc(&p->T1, sizeof(double) * rows * d.kL * d.d1 * d.d2 * d.mR) != cudaSuccess ||
+        ws_malloc(&p->T3, sizeof(double) * rows * d.d1 * d.d2 * d.kR * d.mR) != cudaSuccess)
       return fail(set_err(HEFF_ENOMEM, "heff_create: cannot allocate T1/T3 workspace (%lld a' rows)", (long long)rows));
     // GEMM1: T1[(a' w), (s1 s2 b)] = L[(a' w), a] . psi[a, (s1 s2 b)]   (NN)
     p->g1.N = d.d1 * d.d2 * d.mR;
@@ -672,8 +781,8 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
     p->g4.ldc = d.mR;
   } else {
     const int64_t nb = p->nb;
-    if (cudaMalloc(&p->V1, sizeof(double) * d.mL * d.d1 * d.d2 * nb * d.kR) != cudaSuccess ||
-        cudaMalloc(&p->V3, sizeof(double) * d.kL * d.mL * d.d1 * d.d2 * nb) != cudaSuccess)
+    if (ws_malloc(&p->V1, sizeof(double) * d.mL * d.d1 * d.d2 * nb * d.kR) != cudaSuccess ||
+        ws_malloc(&p->V3, sizeof(double) * d.kL * d.mL * d.d1 * d.d2 * nb) != cudaSuccess)
       return fail(set_err(HEFF_ENOMEM, "heff_create: cannot allocate V1/V3 workspace"));
     // GEMM_A: V1[(a s1 s2), (b' w2)] = psi[(a s1 s2), b] . R_g[(b' w2), b]^T   (NT)
     p->gA.M = d.mL * d.d1 * d.d2;
@@ -781,10 +890,10 @@ extern "C" int heff_create_z(heff_plan* out, const heff_dims* dims, const double
   int r = build_mpo_csr_complex(p, W1z, W2z);
   if (r) return fail(r);
   const int64_t nL = d.mL * d.kL * d.mL, nR = d.mR * d.kR * d.mR, n = d.mL * d.d1 * d.d2 * d.mR;
-  if (cudaMalloc(&p->Lp, sizeof(double) * 3 * nL) != cudaSuccess ||
-      cudaMalloc(&p->Rp, sizeof(double) * 3 * nR) != cudaSuccess ||
-      cudaMalloc(&p->zin, sizeof(double) * 2 * n) != cudaSuccess ||
-      cudaMalloc(&p->zout, sizeof(double) * 2 * n) != cudaSuccess)
+  if (ws_malloc(&p->Lp, sizeof(double) * 3 * nL) != cudaSuccess ||
+      ws_malloc(&p->Rp, sizeof(double) * 3 * nR) != cudaSuccess ||
+      ws_malloc(&p->zin, sizeof(double) * 2 * n) != cudaSuccess ||
+      ws_malloc(&p->zout, sizeof(double) * 2 * n) != cudaSuccess)
     return fail(set_err(HEFF_ENOMEM, "heff_create_z: cannot allocate planar copies"));
   deinterleave_kernel<<<ew_grid(2 * nL), 256, 0, s>>>(L, p->Lp, p->Lp + nL, nL);
   negate_kernel<<<ew_grid(2 * nL), 256, 0, s>>>(p->Lp + nL, p->Lp + 2 * nL, nL);
@@ -803,8 +912,8 @@ extern "C" int heff_create_z(heff_plan* out, const heff_dims* dims, const double
   p->chunk_rows = rows;
   p->t1_plane = rows * d.kL * d.d1 * d.d2 * d.mR;
   p->t3_plane = rows * d.d1 * d.d2 * d.kR * d.mR;
-  if (cudaMalloc(&p->T1, sizeof(double) * 2 * p->t1_plane) != cudaSuccess ||
-      cudaMalloc(&p->T3, sizeof(double) * 2 * p->t3_plane) != cudaSuccess)
+  if (ws_malloc(&p->T1, sizeof(double) * 2 * p->t1_plane) != cudaSuccess ||
+      ws_malloc(&p->T3, sizeof(double) * 2 * p->t3_plane) != cudaSuccess)
     return fail(set_err(HEFF_ENOMEM, "heff_create_z: cannot allocate T1/T3 workspace"));
   for (int k = 0; k < 4; ++k) {
     GemmOp& g1 = p->gz1[k];
@@ -1220,8 +1329,8 @@ extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_
   const int64_t n_in = zf * d.mL * d.d1 * d.d2 * d.mR;
   const int64_t n_out = zf * vec_len(p);
   if (!p->stage_in) {
-    CK(cudaMalloc(&p->stage_in, sizeof(double) * n_in));
-    CK(cudaMalloc(&p->stage_out, sizeof(double) * n_out));
+    CK(ws_malloc(&p->stage_in, sizeof(double) * n_in));
+    CK(ws_malloc(&p->stage_out, sizeof(double) * n_out));
   }
   const bool pipelined = !p->is_complex && !p->sharded && p->terms.empty() && p->nphi == 0 && p->sp1 == nullptr &&
                          p->sp4 == nullptr && p->chunk_rows == d.mL && d.mL * d.d1 * d.d2 >= 8 * kE2eChunks &&
@@ -1467,8 +1576,8 @@ static int lanczos_workspace(heff_plan_s* p, int cap, cudaStream_t s, LanczosLay
   const int64_t nr = cplx ? 2 * n : n;               // doubles per vector
   const int64_t ldv = (nr + 31) / 32 * 32;
   if (compact && !p->dense_in) {
-    CK(cudaMalloc(&p->dense_in, sizeof(double) * n_dense));
-    CK(cudaMalloc(&p->dense_out, sizeof(double) * n_dense));
+    CK(ws_malloc(&p->dense_in, sizeof(double) * n_dense));
+    CK(ws_malloc(&p->dense_out, sizeof(double) * n_dense));
     CK(cudaMemsetAsync(p->dense_in, 0, sizeof(double) * n_dense, s));
   }
   // gather-fused sharded path: the basis lives in an NCCL symmetric window
@@ -1481,27 +1590,29 @@ static int lanczos_workspace(heff_plan_s* p, int cap, cudaStream_t s, LanczosLay
   p->fused_active = fgather ? 1 : 0;
   // (re)allocate the Krylov basis and scratch
   if (p->basis_cap < cap || p->ldv != ldv) {
-    cudaFree(p->basis); cudaFree(p->partial); cudaFree(p->scal);
+    CK(cudaStreamSynchronize(s));  // the old blocks go back to the cache idle
+    ws_release(p->basis); ws_release(p->partial); ws_release(p->scal);
     p->basis = nullptr; p->partial = nullptr; p->scal = nullptr;
     p->basis_cap = 0;
-    CK(cudaMalloc(&p->basis, sizeof(double) * ldv * (fgather ? 1 : cap)));
+    CK(ws_malloc(&p->basis, sizeof(double) * ldv * (fgather ? 1 : cap)));
     p->ldp = reduce_grid(nr);
     const size_t pcols = std::max<size_t>((size_t)p->ldp, (size_t)8 * g_num_sms);  // also the fused step's grid
-    CK(cudaMalloc(&p->partial, sizeof(double) * (size_t)(2 * cap + 2 * kDotQ + 1) * pcols));
-    CK(cudaMalloc(&p->scal, sizeof(double) * 9 * (size_t)(cap + 1)));  // + fused-gather timeout flag
+    CK(ws_malloc(&p->partial, sizeof(double) * (size_t)(2 * cap + 2 * kDotQ + 1) * pcols));
+    CK(ws_malloc(&p->scal, sizeof(double) * 9 * (size_t)(cap + 1)));  // + fused-gather timeout flag
     p->basis_cap = fgather ? 0 : cap;  // a later non-fused call reallocates the full basis
     p->ldv = ldv;
   }
   if (!p->work || p->work_len < ldv) {
-    cudaFree(p->work);
+    CK(cudaStreamSynchronize(s));
+    ws_release(p->work);
     p->work = nullptr;
-    CK(cudaMalloc(&p->work, sizeof(double) * ldv));
+    CK(ws_malloc(&p->work, sizeof(double) * ldv));
     p->work_len = ldv;
   }
   if (p->sharded && p->comm && !p->full && !fgather) {
     const heff_dims& d = p->dims;
-    CK(cudaMalloc(&p->full, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
-    if (p->nranks > 1) CK(cudaMalloc(&p->gather, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
+    CK(ws_malloc(&p->full, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
+    if (p->nranks > 1) CK(ws_malloc(&p->gather, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
   }
   *out = LanczosLayout{compact, cplx, fgather, n_dense, n, nr, ldv};
   return HEFF_OK;
@@ -2096,7 +2207,8 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
   if (!p) return set_err(HEFF_EINVAL, "heff_set_qn: null plan");
   if (!qn) {  // back to dense
     cudaFree(p->sp1); cudaFree(p->sp4); cudaFree(p->mpo_live);
-    cudaFree(p->qn_idx); cudaFree(p->dense_in); cudaFree(p->dense_out);
+    cudaDeviceSynchronize();
+    cudaFree(p->qn_idx); ws_release(p->dense_in); ws_release(p->dense_out);
     p->sp1 = p->sp4 = nullptr;
     p->mpo_live = nullptr;
     p->qn_idx = nullptr;
@@ -2212,9 +2324,10 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
             const int64_t base = ((a * d.d1 + s1) * d.d2 + s2) * d.mR;
             for (const int* b = lo; b < hi; ++b) idx.push_back((int)(base + (b - qn->qb)));
           }
+      cudaDeviceSynchronize();
       cudaFree(p->qn_idx);
-      cudaFree(p->dense_in);
-      cudaFree(p->dense_out);
+      ws_release(p->dense_in);
+      ws_release(p->dense_out);
       p->qn_idx = nullptr;
       p->dense_in = p->dense_out = nullptr;
       p->qn_n = (int64_t)idx.size();
@@ -2957,5 +3070,9 @@ extern "C" int heff_release_caches(void) {
     tasks.push_back([dev](cudaStream_t) { cudaSetDevice(dev); release_thread_caches(); });
   BlockPool::get().run_each_worker(tasks);
   CK(cudaDeviceSynchronize());
+  {  // the plan workspace cache (blocks of destroyed plans) on this device
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    ws_cache_trim(dev);
+  }
   return HEFF_OK;
 }

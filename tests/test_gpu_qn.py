@@ -113,3 +113,44 @@ def test_qn_lanczos_fixed_steps_parity(dev, orc, case):
     vc = v.cpu().numpy()
     assert np.abs(vc[~z.mask()]).max() == 0.0
     assert abs(abs(np.vdot(vc, o.x)) - 1.0) < 1e-8
+
+
+def test_plan_lifecycle_returns_device_memory(dev):
+    """Creating and destroying U(1), complex and plain plans (with Lanczos runs, which add
+    the Krylov basis and the sector scatter buffers) leaves no device memory behind once
+    heff_release_caches has emptied the workspace cache; before that, the cache reuses the
+    destroyed plans' blocks instead of growing."""
+    from heffgen import configs as C
+    from paper_2007_14822_b200 import Heff
+    from paper_2007_14822_b200.heff import release_caches
+    z = CASES["chain_m256"]()
+    xd = z.x.to(dev)
+    xc = C.make("c2", device=dev)
+    Lz = torch.complex(xc.L, 0.1 * xc.L).contiguous()
+    W1z = torch.complex(xc.W1, torch.zeros_like(xc.W1)).contiguous()
+    W2z = torch.complex(xc.W2, torch.zeros_like(xc.W2)).contiguous()
+    Rz = torch.complex(xc.R, 0.1 * xc.R).contiguous()
+
+    def cycle():
+        with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+            h.set_qn(z.qn_dict())
+            h.lanczos_ground(xd.psi.clone(), max_iter=6)
+        with Heff(Lz, W1z, W2z, Rz) as hz:
+            hz.apply(torch.complex(xc.psi, xc.psi).contiguous())
+        with Heff(xc.L, xc.W1, xc.W2, xc.R) as h:
+            h.lanczos_ground(xc.psi.clone(), max_iter=6)
+        torch.cuda.synchronize()
+
+    cycle()
+    release_caches()
+    torch.cuda.empty_cache()
+    free0 = torch.cuda.mem_get_info()[0]
+    cycle()
+    free_cached = torch.cuda.mem_get_info()[0]
+    for _ in range(5):
+        cycle()
+    torch.cuda.empty_cache()
+    assert torch.cuda.mem_get_info()[0] >= free_cached - (64 << 20)   # blocks reused, not re-allocated
+    release_caches()
+    torch.cuda.empty_cache()
+    assert torch.cuda.mem_get_info()[0] >= free0 - (16 << 20)          # nothing leaked
