@@ -66,12 +66,17 @@ __global__ void __launch_bounds__(kLqThreads) lq_panel_kernel(double* __restrict
     }
     grid.sync();
     const int owner = (int)(i / cw);
-    if (tid < kLqNb) {
-      double g = 0.0;
+    {  // sum the CTAs' partials: 8 lanes per row r, CTA b on lane b % 8, then a fixed-order
+       // shuffle tree (deterministic; 8 independent load streams instead of one)
+      const int r = tid >> 3, l = tid & 7;
       const double* pp = part + (int64_t)(i & 1) * nparts * (2 * kLqNb);
-      for (int b = 0; b < nparts; ++b) g += pp[(int64_t)b * (2 * kLqNb) + tid];
-      sh_g[tid] = g;
-      sh_col[tid] = pp[(int64_t)owner * (2 * kLqNb) + kLqNb + tid];
+      double g = 0.0;
+      for (int b = l; b < nparts; b += 8) g += __ldcg(pp + (int64_t)b * (2 * kLqNb) + r);
+      g += __shfl_xor_sync(0xffffffffu, g, 4);
+      g += __shfl_xor_sync(0xffffffffu, g, 2);
+      g += __shfl_xor_sync(0xffffffffu, g, 1);
+      if (l == 0) sh_g[r] = g;
+      if (tid < kLqNb) sh_col[tid] = __ldcg(pp + (int64_t)owner * (2 * kLqNb) + kLqNb + tid);
     }
     __syncthreads();
     const double norm2 = sh_g[i], x0 = sh_col[i];
@@ -110,13 +115,17 @@ __global__ void __launch_bounds__(kLqThreads) lq_panel_kernel(double* __restrict
 __global__ void lq_build_t_kernel(const double* __restrict__ VtV, const double* __restrict__ beta, int nbp,
                                   double* __restrict__ negT) {
   __shared__ double T[kLqNb][kLqNb + 1];
+  __shared__ double G[kLqNb][kLqNb + 1];  // V^T V staged once (the recurrence reads it by column)
   const int l = threadIdx.x;  // 32 threads
-  for (int c = 0; c < kLqNb; ++c) T[l][c] = 0.0;
+  for (int c = 0; c < kLqNb; ++c) {
+    T[l][c] = 0.0;
+    G[c][l] = (c < nbp && l < nbp) ? VtV[c * nbp + l] : 0.0;
+  }
   __syncwarp();
   for (int i = 0; i < nbp; ++i) {
     double s = 0.0;
     if (l < i)
-      for (int p = l; p < i; ++p) s = fma(T[l][p], VtV[p * nbp + i], s);
+      for (int p = l; p < i; ++p) s = fma(T[l][p], G[p][i], s);
     __syncwarp();
     if (l < i) T[l][i] = -beta[i] * s;
     if (l == i) T[i][i] = beta[i];
