@@ -167,6 +167,11 @@ __device__ __forceinline__ void gemm_dmma_tma_body(const CUtensorMap* tmA, const
       mbar_init(&empty[s], Cfg::kConsumerWarps);
     }
     fence_barrier_init();
+  }
+  // launched with programmatic dependent launch: the prologue above overlaps the previous
+  // kernel's tail; operands, C and the stream-K ticket counter are touched only after it
+  pdl_wait();
+  if (threadIdx.x == 0) {
     int c = (int)blockIdx.x;
     if (sk) {
       c = (int)atomicAdd(sk->counter, 1u);
@@ -439,6 +444,7 @@ __global__ void __launch_bounds__(256) streamk_fixup_kernel(const double* __rest
                                                             int grid, int dp_tiles, int accumulate) {
   __shared__ int s_slot[kFixupMaxParts];
   __shared__ int s_n;
+  pdl_wait();
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
   const int local = blockIdx.x / kFixupSplit;  // stream-K tile index
   const int part = blockIdx.x % kFixupSplit;    // this block's 1/kFixupSplit of the tile

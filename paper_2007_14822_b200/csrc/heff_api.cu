@@ -190,6 +190,26 @@ struct GemmOp {
 };
 
 static int g_num_sms = 0;
+
+// Launch with programmatic dependent launch allowed (the kernel calls pdl_wait before it
+// touches memory the previous kernel in the stream writes or reads): the next kernel's
+// launch and prologue overlap this one's tail.  HEFF_NO_PDL=1 launches normally.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  static const bool off = getenv("HEFF_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 static int ew_grid(int64_t n);
 
 static bool tma_ok(const GemmOp& g) {
@@ -288,27 +308,25 @@ static int launch_tma(GemmOp& g, cudaStream_t s, int* nlaunch, SplitWs* ws, cons
     sk.epoch = ++ws->epoch;
     use_sk = 1;
   }
+  const int M32 = (int)g.M, N32 = (int)g.N, K32 = (int)g.K, dp32 = (int)dp_tiles;
   if (sa) {
     if (!g.b_kmajor) return set_err(HEFF_EUNSUPPORTED, "sharded-A GEMM: NT only");
-    auto k = gemm_dmma_tma_sharded_kernel<BM, BN, WM, WN, ST, true>;
-    k<<<grid, NT::kThreads, NT::kSmemBytes, s>>>(*sa, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K, kGroupM, vec,
-                                                 (int)dp_tiles, wsp, g.accumulate, sk, use_sk);
+    CK(launch_pdl(gemm_dmma_tma_sharded_kernel<BM, BN, WM, WN, ST, true>, dim3(grid), dim3(NT::kThreads),
+                  NT::kSmemBytes, s, *sa, g.mapB, g.C, g.ldc, M32, N32, K32, kGroupM, vec, dp32, wsp, g.accumulate, sk,
+                  use_sk));
   } else if (g.b_kmajor) {
-    auto k = gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, true>;
-    k<<<grid, NT::kThreads, NT::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K, kGroupM,
-                                                 vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order, g.sp_ptr,
-                                                 g.sp_list, sk, use_sk);
+    CK(launch_pdl(gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, true>, dim3(grid), dim3(NT::kThreads), NT::kSmemBytes, s,
+                  g.mapA, g.mapB, g.C, g.ldc, M32, N32, K32, kGroupM, vec, dp32, wsp, g.accumulate, g.sp_order,
+                  g.sp_ptr, g.sp_list, sk, use_sk));
   } else {
-    auto k = gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, false>;
-    k<<<grid, NN::kThreads, NN::kSmemBytes, s>>>(g.mapA, g.mapB, g.C, g.ldc, (int)g.M, (int)g.N, (int)g.K, kGroupM,
-                                                 vec, (int)dp_tiles, wsp, g.accumulate, g.sp_order, g.sp_ptr,
-                                                 g.sp_list, sk, use_sk);
+    CK(launch_pdl(gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, false>, dim3(grid), dim3(NN::kThreads), NN::kSmemBytes, s,
+                  g.mapA, g.mapB, g.C, g.ldc, M32, N32, K32, kGroupM, vec, dp32, wsp, g.accumulate, g.sp_order,
+                  g.sp_ptr, g.sp_list, sk, use_sk));
   }
   if (dp_tiles < tiles && !use_sk) {
-    CK(cudaGetLastError());
     if (nlaunch) ++*nlaunch;
-    streamk_fixup_kernel<BM, BN><<<(unsigned)((tiles - dp_tiles) * kFixupSplit), 256, 0, s>>>(
-        wsp, g.C, g.ldc, (int)g.M, (int)g.N, (int)ktiles, kGroupM, grid, (int)dp_tiles, g.accumulate);
+    CK(launch_pdl(streamk_fixup_kernel<BM, BN>, dim3((unsigned)((tiles - dp_tiles) * kFixupSplit)), dim3(256), 0, s,
+                  (const double*)wsp, g.C, g.ldc, M32, N32, (int)ktiles, kGroupM, grid, dp32, g.accumulate));
   }
   return HEFF_OK;
 }
@@ -1020,9 +1038,9 @@ static int launch_mpo_A(const double* T1, double* T3, int64_t mR, int64_t rows, 
                         const unsigned char* live, cudaStream_t s) {
   if (rows <= 0 || mR <= 0) return HEFF_OK;
   dim3 grid((unsigned)((mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
-  mpo_orderA_kernel<1><<<grid, kMpoThreads, sizeof(double) * nin * kMpoCols, s>>>(
-      T1, T3, mR, nin, nout, csr.d_rowptr, csr.d_col, csr.d_val, live, 1, 0, 0);
-  CK(cudaGetLastError());
+  CK(launch_pdl(mpo_orderA_kernel<1>, grid, dim3(kMpoThreads), sizeof(double) * nin * kMpoCols, s, T1, T3, mR, nin,
+                nout, (const int*)csr.d_rowptr, (const int*)csr.d_col, (const double*)csr.d_val, live, 1, (int64_t)0,
+                (int64_t)0));
   return HEFF_OK;
 }
 
@@ -2694,15 +2712,15 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     for (int r = 0; r < rounds; ++r) {
       const int2* pr = d_pairs + (size_t)r * npairs;
       if (svd_tma)
-        svd_gram_tma_kernel<<<gram_grid, (kSvdTmaGramWarps + 1) * 32, kSvdTmaGramSmem, s>>>(xm_gram, R, pr, npairs,
-                                                                                          nslots, Gp);
+        CK(launch_pdl(svd_gram_tma_kernel, dim3(gram_grid), dim3((kSvdTmaGramWarps + 1) * 32), kSvdTmaGramSmem, s,
+                      xm_gram, R, pr, npairs, nslots, Gp));
       else
         svd_gram_kernel<<<gram_grid, kSvdGramThreads, 0, s>>>(Xb, R, pr, npairs, nslots, Gp);
-      svd_pair_eig_kernel<<<npairs, kSvdEigThreads, 0, s>>>(Gp, nslots, gram_chunks, gram_grid, tol, negl, inner,
-                                                           d_Qg, d_flag, d_maxoff + sw, d_nrot + sw);
+      CK(launch_pdl(svd_pair_eig_kernel, dim3(npairs), dim3(kSvdEigThreads), 0, s, (const double*)Gp, nslots,
+                    (int64_t)gram_chunks, gram_grid, tol, negl, inner, d_Qg, d_flag, d_maxoff + sw, d_nrot + sw));
       if (svd_tma)
-        svd_rotate_tma_kernel<<<rot_grid, (kSvdTmaRotWarps + 1) * 32, kSvdTmaRotSmem, s>>>(xm_rot, Xb, R, pr, npairs,
-                                                                                          d_Qg, d_flag);
+        CK(launch_pdl(svd_rotate_tma_kernel, dim3(rot_grid), dim3((kSvdTmaRotWarps + 1) * 32), kSvdTmaRotSmem, s,
+                      xm_rot, Xb, R, pr, npairs, (const double*)d_Qg, (const int*)d_flag));
       else
         svd_rotate_kernel<<<rot_grid, kSvdRotThreads, 0, s>>>(Xb, R, pr, npairs, d_Qg, d_flag);
     }

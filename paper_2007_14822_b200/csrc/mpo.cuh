@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
   // The CSR then holds the real 2x2 blocks [[Re, -Im], [Im, Re]] of the complex MPO.
   extern __shared__ __align__(16) double s_in[];  // [nin][kMpoCols]
   __shared__ uint64_t bar;
+  pdl_wait();  // T1 from the GEMM before (programmatic dependent launch)
   const int64_t ap = blockIdx.y;
   // U(1) plans: blocks whose input and output are zero by symmetry are skipped (their T3
   // entries were zeroed once by heff_set_qn)

@@ -73,6 +73,12 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
+// Programmatic dependent launch (kernels launched with the programmatic-stream-serialization
+// attribute): wait until the previous grid in the stream has completed and its memory is
+// visible / allow the next grid to be scheduled (it still waits in its own pdl_wait).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void lds128(double& x, double& y, uint32_t addr) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
 }

@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(kSvdEigThreads) svd_pair_eig_kernel(const doub
   __shared__ double s_off[kSvdEigThreads / 32];
   const int p = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_wait();                 // the Gram partials of this round
   const double* gsrc = Gp + (int64_t)p * nslots * (kSvdPair * kSvdPair);
   const int64_t T = (int64_t)gridDim.x * C;  // gridDim.x = npairs
   const int nsum = svd_sk_owner((int64_t)p * C + C - 1, T, gram_grid) - svd_sk_owner((int64_t)p * C, T, gram_grid) + 1;
@@ -707,6 +708,7 @@ __global__ void __launch_bounds__((kSvdTmaRotWarps + 1) * 32) svd_rotate_tma_ker
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();                 // Q and flags of this round's eigen-solve
   const int64_t C2 = (R + kSvdTmaRotRows - 1) / kSvdTmaRotRows;
   const int64_t T = (int64_t)npairs * C2, G = gridDim.x;
   const int64_t it_begin = svd_sk_start(T, blockIdx.x, G), it_end = svd_sk_start(T, blockIdx.x + 1, G);
@@ -807,6 +809,7 @@ __global__ void __launch_bounds__((kSvdTmaGramWarps + 1) * 32) svd_gram_tma_kern
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();                 // Xb of the previous round's rotation; Gp free again
   const int64_t C = (R + kSvdTmaGramRows - 1) / kSvdTmaGramRows;
   const int64_t T = (int64_t)npairs * C, G = gridDim.x;
   const int64_t it_begin = svd_sk_start(T, blockIdx.x, G), it_end = svd_sk_start(T, blockIdx.x + 1, G);
