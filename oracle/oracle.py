@@ -215,6 +215,31 @@ def env_right(R, B, W) -> np.ndarray:
     return out
 
 
+def env_left_rows(L, A, W, rows) -> np.ndarray:
+    """Rows a' of env_left, one at a time (sampled checks at full size): the same sum as
+    env_left, Lout[a',w',a] = sum A[x',s',a'] L[x',w,x] W[w,s',s,w'] A[x,s,a], contracted
+    bra first for a fixed a' (numpy tensor contractions as library steps)."""
+    L, A, W = map(_c, (L, A, W))
+    out = []
+    for ap in rows:
+        Y = np.einsum("ys,ywx->swx", A[:, :, ap], L)      # sum_x' A[x',s',a'] L[x',w,x]
+        Z = np.einsum("wstv,swx->tvx", W, Y)              # sum_{w,s'} W[w,s',s,w'] Y[s',w,x]
+        out.append(np.einsum("tvx,xta->va", Z, A))        # sum_{x,s} Z[s,w',x] A[x,s,a]
+    return np.stack(out)
+
+
+def env_right_rows(R, B, W, rows) -> np.ndarray:
+    """Rows b' of env_right, one at a time: Rout[b',w,b] = sum B[b',s',y'] R[y',w',y]
+    W[w,s',s,w'] B[b,s,y], contracted bra first for a fixed b'."""
+    R, B, W = map(_c, (R, B, W))
+    out = []
+    for bp in rows:
+        Y = np.einsum("sy,yvz->svz", B[bp], R)            # sum_y' B[b',s',y'] R[y',w',y]
+        Z = np.einsum("wstv,svz->wtz", W, Y)              # sum_{s',w'} W[w,s',s,w'] Y[s',w',y]
+        out.append(np.einsum("wtz,btz->wb", Z, B))        # sum_{s,y} Z[w,s,y] B[b,s,y]
+    return np.stack(out)
+
+
 def tridiag_lowest(alpha, beta):
     alpha = _c(alpha)
     j = alpha.size

@@ -70,3 +70,32 @@ def test_gpu_grown_environment_block_ED(dev):
     ev = np.linalg.eigvalsh(0.5 * (Lc[:, 0, :] + Lc[:, 0, :].T))
     np.testing.assert_allclose(ev, np.linalg.eigvalsh(ed_ref.heisenberg(n, ed_ref.chain_bonds(n)).toarray()),
                                atol=1e-12)
+
+
+def test_env_update_c4_size_sampled_rows(dev, orc):
+    """Environment updates at the C4 size (bond 4096 -> 4096, d = 2, the cylinder's k = 20
+    MPO; L and the result 2.7 GB each) in the DMRG sweep's launch configuration; the oracle
+    computes sampled output rows one by one."""
+    from paper_2007_14822_b200 import env_update_left, env_update_right
+    m, d = 4096, 2
+    W = mpo.cylinder_W(17)
+    k = W.shape[0]
+    g = torch.Generator(device=dev).manual_seed(44)
+    L = torch.randn((m, k, m), dtype=torch.float64, device=dev, generator=g)
+    A = torch.randn((m, d, m), dtype=torch.float64, device=dev, generator=g)
+    Wt = torch.from_numpy(W).to(dev)
+    rows = [0, 1, 2047, m - 1]
+    gl = env_update_left(L, A, Wt)[rows].cpu().numpy()
+    Lh, Ah = L.cpu().numpy(), A.cpu().numpy()
+    del L
+    torch.cuda.empty_cache()
+    ref = orc.env_left_rows(Lh, Ah, W, rows)
+    for i in range(len(rows)):
+        assert rel(gl[i], ref[i]) <= 1e-12, (rows[i], rel(gl[i], ref[i]))
+    del Lh
+    R = torch.randn((m, k, m), dtype=torch.float64, device=dev, generator=g)
+    B = A.reshape(m, d, m)                       # any [b, s, y] tensor
+    gr = env_update_right(R, B, Wt)[rows].cpu().numpy()
+    ref = orc.env_right_rows(R.cpu().numpy(), Ah, W, rows)
+    for i in range(len(rows)):
+        assert rel(gr[i], ref[i]) <= 1e-12, (rows[i], rel(gr[i], ref[i]))

@@ -88,3 +88,19 @@ def test_env_ragged_brute_force(oracle_lib):
     R, B = rng.standard_normal((mi, kr, mi)), rng.standard_normal((mo, d, mi))
     ref = np.einsum("apx,xvy,wpsv,bsy->awb", B, R, W, B, optimize=False)
     np.testing.assert_allclose(oracle_lib.env_right(R, B, W), ref, rtol=1e-13, atol=1e-13)
+
+
+def test_env_row_oracle_matches_full_update():
+    """The row-at-a-time environment oracle (used for sampled checks at full size) against
+    the full C update on random and ragged shapes, every row."""
+    from oracle import oracle as orc
+    orc.build()
+    rng = np.random.default_rng(5)
+    for (mi, d, mo, kl, kr) in ((7, 2, 9, 5, 5), (16, 3, 11, 4, 6), (1, 2, 2, 5, 5)):
+        L, A = rng.standard_normal((mi, kl, mi)), rng.standard_normal((mi, d, mo))
+        R, B = rng.standard_normal((mi, kr, mi)), rng.standard_normal((mo, d, mi))
+        W = rng.standard_normal((kl, d, d, kr))
+        full_l, full_r = orc.env_left(L, A, W), orc.env_right(R, B, W)
+        rows = list(range(mo))
+        np.testing.assert_allclose(orc.env_left_rows(L, A, W, rows), full_l, rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(orc.env_right_rows(R, B, W, rows), full_r, rtol=1e-13, atol=1e-13)
