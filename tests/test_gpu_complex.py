@@ -97,3 +97,25 @@ def test_complex_apply_host_and_guards(dev, orc):
             h.set_penalty(torch.zeros((1,) + tuple(x.psi.shape), dtype=torch.complex128, device=dev), 1.0)
         with pytest.raises(TypeError):
             h.apply(xd.psi.real.contiguous())
+
+
+def test_complex_c4_size_sampled_rows(dev, orc):
+    """A complex problem of the C4 size (6x6 cylinder MPO, m = 4096, random complex
+    environments) in the launch configuration of tools/sweep_complex.py; the complex oracle
+    computes sampled output rows a' one by one."""
+    from heffgen import mpo
+    from paper_2007_14822_b200 import Heff
+    cyl = [mpo.cylinder_W(j).astype(complex) for j in range(36)]
+    x = C.model_inputs_complex(cyl, 17, 4096, seed=6, device=dev)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        out = h.apply(x.psi)
+        torch.cuda.synchronize()
+    rows = [0, 2047, 4095]
+    outc = out[rows].cpu().numpy()
+    del out
+    L, W1, W2, R, psi = x.numpy()
+    del x
+    torch.cuda.empty_cache()
+    for i, a in enumerate(rows):
+        ref = orc.heff_apply_z(L, W1, W2, R, psi, rows=(a, a + 1))[0]
+        assert rel(outc[i], ref) <= 1e-12, (a, rel(outc[i], ref))
