@@ -154,3 +154,23 @@ def test_plan_lifecycle_returns_device_memory(dev):
     release_caches()
     torch.cuda.empty_cache()
     assert torch.cuda.mem_get_info()[0] >= free0 - (16 << 20)          # nothing leaked
+
+
+def test_qn_c4qn_full_size_sampled_rows(dev, orc):
+    """C4-QN (6x6 cylinder, m = 4096, Sz = 0 sector; the configuration of tools/sweep_qn.py)
+    on the block-sparse schedules, against the dense oracle on sampled output rows."""
+    from paper_2007_14822_b200 import Heff
+    z = qn.cylinder_qn(6, 17, 4096, seed=2004, device=dev)
+    xd = z.x
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        h.set_qn(z.qn_dict())
+        out = h.apply(xd.psi)
+        torch.cuda.synchronize()
+    rows = [0, 1000, 2048, 4095]
+    outc = out[rows].cpu().numpy()
+    del out
+    L, W1, W2, R, psi = xd.numpy()
+    for i, a in enumerate(rows):
+        ref = orc.heff_apply(L, W1, W2, R, psi, rows=(a, a + 1))[0]
+        nrm = max(np.linalg.norm(ref), 1e-300)
+        assert np.linalg.norm(outc[i] - ref) / nrm <= 1e-12, a
