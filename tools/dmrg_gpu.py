@@ -11,6 +11,7 @@ sequences them.
 from __future__ import annotations
 
 import argparse
+import os
 import sys
 import time
 from pathlib import Path
@@ -45,6 +46,25 @@ def two_site(A, B):
 
 
 SPLIT_STATS = {"calls": 0, "sweeps": 0, "max_sweeps": 0, "ms": 0.0}
+
+# DMRG_PHASES=1: per-sweep wall time of each step of a bond update (synchronising after each)
+PHASES: dict = {}
+_PHASES_ON = os.environ.get("DMRG_PHASES") == "1"
+
+
+def _phase_clock():
+    if _PHASES_ON:
+        torch.cuda.synchronize()
+    return time.perf_counter()
+
+
+def _phase(name, t0):
+    if not _PHASES_ON:
+        return t0
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    PHASES[name] = PHASES.get(name, 0.0) + (t - t0)
+    return t
 
 
 def split(psi, maxdim, cutoff, direction):
@@ -90,19 +110,29 @@ def dmrg(Ws, maxdims, cutoff=1e-11, seed=0, lanczos_iter=40, init_dim=8, device=
         # left-to-right then right-to-left half sweeps
         for direction, bonds in (("right", range(N - 1)), ("left", range(N - 2, -1, -1))):
             for j in bonds:
+                tp = _phase_clock()
                 psi = two_site(As[j], As[j + 1]).contiguous()
+                tp = _phase("two_site", tp)
                 with Heff(Ls[j], tW[j], tW[j + 1], Rs[j + 2]) as h:
+                    tp = _phase("create", tp)
                     r = h.lanczos_ground(psi, max_iter=lanczos_iter, tol=1e-12, converge=True)
+                    tp = _phase("lanczos", tp)
+                tp = _phase("destroy", tp)
                 energy = r.energy
                 if capture is not None and direction == "right" and j == N // 2 - 1 and sw == len(maxdims) - 1:
                     capture["psi"] = psi.clone()
                 A, B, disc = split(psi, maxdim, cutoff, direction)
+                tp = _phase("split", tp)
                 maxdisc = max(maxdisc, disc)
                 As[j], As[j + 1] = A, B
                 if direction == "right":
                     Ls[j + 1] = env_update_left(Ls[j], As[j], tW[j])
                 else:
                     Rs[j + 1] = env_update_right(Rs[j + 2], As[j + 1], tW[j + 1])
+                _phase("env", tp)
+        if PHASES:
+            log("  phases (s): " + ", ".join(f"{k} {v:.2f}" for k, v in PHASES.items()))
+            PHASES.clear()
         log(f"After sweep {sw + 1} energy={energy:.12f} maxlinkdim={max(a.shape[2] for a in As[:-1])} "
             f"maxtrunc={maxdisc:.2e} time={time.perf_counter() - t0:.2f} split: {SPLIT_STATS['calls']} calls, "
             f"{SPLIT_STATS['sweeps'] / max(1, SPLIT_STATS['calls']):.1f} Jacobi sweeps avg "
