@@ -309,24 +309,29 @@ static int launch_tma(GemmOp& g, cudaStream_t s, int* nlaunch, SplitWs* ws, cons
     use_sk = 1;
   }
   const int M32 = (int)g.M, N32 = (int)g.N, K32 = (int)g.K, dp32 = (int)dp_tiles;
+  // tile raster: GROUP_M consecutive M-tiles per column sweep (block-sparse schedules are
+  // built for kGroupM; HEFF_GEMM_GROUP_M overrides it for dense GEMMs, a tuning knob)
+  int gm = kGroupM;
+  if (!sparse)
+    if (const char* e = getenv("HEFF_GEMM_GROUP_M")) gm = std::max(1, atoi(e));
   if (sa) {
     if (!g.b_kmajor) return set_err(HEFF_EUNSUPPORTED, "sharded-A GEMM: NT only");
     CK(launch_pdl(gemm_dmma_tma_sharded_kernel<BM, BN, WM, WN, ST, true>, dim3(grid), dim3(NT::kThreads),
-                  NT::kSmemBytes, s, *sa, g.mapB, g.C, g.ldc, M32, N32, K32, kGroupM, vec, dp32, wsp, g.accumulate, sk,
+                  NT::kSmemBytes, s, *sa, g.mapB, g.C, g.ldc, M32, N32, K32, gm, vec, dp32, wsp, g.accumulate, sk,
                   use_sk));
   } else if (g.b_kmajor) {
     CK(launch_pdl(gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, true>, dim3(grid), dim3(NT::kThreads), NT::kSmemBytes, s,
-                  g.mapA, g.mapB, g.C, g.ldc, M32, N32, K32, kGroupM, vec, dp32, wsp, g.accumulate, g.sp_order,
+                  g.mapA, g.mapB, g.C, g.ldc, M32, N32, K32, gm, vec, dp32, wsp, g.accumulate, g.sp_order,
                   g.sp_ptr, g.sp_list, sk, use_sk));
   } else {
     CK(launch_pdl(gemm_dmma_tma_kernel<BM, BN, WM, WN, ST, false>, dim3(grid), dim3(NN::kThreads), NN::kSmemBytes, s,
-                  g.mapA, g.mapB, g.C, g.ldc, M32, N32, K32, kGroupM, vec, dp32, wsp, g.accumulate, g.sp_order,
+                  g.mapA, g.mapB, g.C, g.ldc, M32, N32, K32, gm, vec, dp32, wsp, g.accumulate, g.sp_order,
                   g.sp_ptr, g.sp_list, sk, use_sk));
   }
   if (dp_tiles < tiles && !use_sk) {
     if (nlaunch) ++*nlaunch;
     CK(launch_pdl(streamk_fixup_kernel<BM, BN>, dim3((unsigned)((tiles - dp_tiles) * kFixupSplit)), dim3(256), 0, s,
-                  (const double*)wsp, g.C, g.ldc, M32, N32, (int)ktiles, kGroupM, grid, dp32, g.accumulate));
+                  (const double*)wsp, g.C, g.ldc, M32, N32, (int)ktiles, gm, grid, dp32, g.accumulate));
   }
   return HEFF_OK;
 }
