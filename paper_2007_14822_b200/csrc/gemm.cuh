@@ -7,7 +7,9 @@
 // The Blackwell parts are the memory pipeline: TMA (cp.async.bulk.tensor) with the
 // 128-byte swizzle fills a STAGES-deep shared-memory ring guarded by mbarriers, one
 // producer warp drives it, and 8 consumer warps run DMMA from ld.shared fragments.
-// Persistent: grid = #SMs, static round-robin over output tiles in GROUP_M raster.
+// Persistent: grid = #SMs, static round-robin over output tiles in GROUP_M raster, plus a
+// stream-K tail; launched with programmatic dependent launch (pdl_wait after the prologue).
+// Tiles: 128x128 (8 consumer warps of 64x32) and 64x64 (8 of 32x16) for sub-wave GEMMs.
 //
 // k-permutation: inside each 16-wide k block, DMMA k-slice kk (0..3) lane t (0..3) uses
 // k = 2t + (kk & 1) + 8 (kk >> 1), identically for A and B.  k is summed, so any
@@ -55,8 +57,9 @@ struct TmaGemmCfg {
 // tiles of the GROUP_M raster and share L2.  The remaining tiles' (tile, k-block)
 // iterations are cut into G equal contiguous ranges, one per CTA, so the last wave is
 // balanced to the k-block.  A tile whose k-range is split between CTAs is written as
-// partial tiles (slot 2b for CTA b's first stream-K tile, 2b+1 for its last) and summed by
-// streamk_fixup_kernel in CTA order (deterministic).  dp_tiles == tiles: plain persistent.
+// partial tiles (slot 2b for CTA b's first stream-K tile, 2b+1 for its last) and summed in
+// CTA order (deterministic) -- inside the kernel by the tile's highest contributor
+// (StreamKSync below), or by streamk_fixup_kernel.  dp_tiles == tiles: plain persistent.
 struct WorkRange {
   int64_t it, it_end;  // stream-K iteration range (iterations counted from dp_tiles*ktiles)
   int tile;            // data-parallel cursor
