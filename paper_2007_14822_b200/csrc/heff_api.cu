@@ -2640,7 +2640,10 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     for (int64_t j = 0; j < kmin; j += kLqNb) {
       const int nbp = (int)std::min<int64_t>(kLqNb, kmin - j);
       const int64_t L = colsP - j;
-      int grid = (int)std::min<int64_t>(g_lq_grid, (L + 31) / 32);
+      // few wide CTAs: a reflector's work per CTA is tiny (32 rows x <= 128 columns), the
+      // grid barrier per reflector is the cost and grows with the CTA count
+      const int64_t want = getenv("HEFF_LQ_NARROW") ? (L + 31) / 32 : (L + kLqMaxCols - 1) / kLqMaxCols;
+      int grid = (int)std::min<int64_t>(g_lq_grid, want);
       int cw = (int)((L + grid - 1) / grid);
       grid = (int)((L + cw - 1) / cw);
       CK(cudaMemsetAsync(d_Vt, 0, sizeof(double) * kLqNb * colsP, s));
