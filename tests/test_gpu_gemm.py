@@ -143,3 +143,25 @@ def test_streamk_one_thread_two_streams(dev):
     for k, o in outs:
         ref = ref1 if k == 1 else ref2
         assert (o - ref).abs().max().item() <= 1e-12 * ref.abs().max().item()
+
+
+def test_pdl_on_off_bitwise(dev, tmp_path):
+    """Programmatic dependent launch changes only when kernels start, never the arithmetic:
+    GEMM, Lanczos and split outputs are bitwise the same with HEFF_NO_PDL=1 (separate
+    processes: the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    import numpy as np
+    probe = os.path.join(os.path.dirname(__file__), "pdl_probe.py")
+    files = []
+    for off in ("", "1"):
+        env = dict(os.environ)
+        env.pop("HEFF_NO_PDL", None)
+        if off:
+            env["HEFF_NO_PDL"] = off
+        f = str(tmp_path / f"out{off or '0'}.npz")
+        subprocess.run([sys.executable, probe, f], check=True, env=env, timeout=600)
+        files.append(np.load(f))
+    for k in files[0].files:
+        assert np.array_equal(files[0][k], files[1][k]), k
