@@ -62,9 +62,11 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
       fence_barrier_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      mbar_arrive_expect_tx(&bar, (uint32_t)(nin * width * 8));
-      for (int r = 0; r < nin; ++r) bulk_load(s_in + r * kMpoCols, in_row(r), (uint32_t)(width * 8), &bar);
+    if (threadIdx.x < 32) {  // warp 0: lane 0 arms the barrier, the 32 lanes issue the row copies
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(nin * width * 8));
+      __syncwarp();
+      for (int r = threadIdx.x; r < nin; r += 32)
+        bulk_load(s_in + r * kMpoCols, in_row(r), (uint32_t)(width * 8), &bar);
     }
     mbar_wait(&bar, 0);
   } else {
@@ -73,6 +75,26 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
       if (c < width) s_in[e] = __ldcs(in_row(r) + c);
     }
     __syncthreads();
+  }
+  if (PLANES == 1 && bulk) {
+    // two adjacent columns per thread (width and the row pitch are even): 16-byte shared
+    // loads and streaming stores, the CSR entries read once per column pair; 8 threads per
+    // column pair step through the output rows.  Same fma order per element.
+    constexpr int kPairs = kMpoCols / 2, kStep = kMpoThreads / kPairs;
+    const int c2 = 2 * (threadIdx.x % kPairs);
+    if (c2 >= width) return;
+    for (int o = threadIdx.x / kPairs; o < nout; o += kStep) {
+      double2 acc = make_double2(0.0, 0.0);
+      const int e1 = __ldg(rowptr + o + 1);
+      for (int e = __ldg(rowptr + o); e < e1; ++e) {
+        const double v = __ldg(val + e);
+        const double2 xin = *reinterpret_cast<const double2*>(s_in + __ldg(col + e) * kMpoCols + c2);
+        acc.x = fma(v, xin.x, acc.x);
+        acc.y = fma(v, xin.y, acc.y);
+      }
+      __stcs(reinterpret_cast<double2*>(out0 + (int64_t)o * mR + c2), acc);
+    }
+    return;
   }
   const int t = threadIdx.x % kMpoCols;
   if (t >= width) return;
