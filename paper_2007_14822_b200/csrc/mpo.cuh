@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
     }
     __syncthreads();
   }
-  if (PLANES == 1 && bulk) {
+  if (bulk && (PLANES == 1 || (out_plane & 1) == 0)) {
     // two adjacent columns per thread (width and the row pitch are even): 16-byte shared
     // loads and streaming stores, the CSR entries read once per column pair; 8 threads per
     // column pair step through the output rows.  Same fma order per element.
@@ -92,7 +92,12 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
         acc.x = fma(v, xin.x, acc.x);
         acc.y = fma(v, xin.y, acc.y);
       }
-      __stcs(reinterpret_cast<double2*>(out0 + (int64_t)o * mR + c2), acc);
+      if (PLANES == 1) {
+        __stcs(reinterpret_cast<double2*>(out0 + (int64_t)o * mR + c2), acc);
+      } else {
+        const int pl = o >= nout_p;
+        __stcs(reinterpret_cast<double2*>(out0 + pl * out_plane + (int64_t)(o - pl * nout_p) * mR + c2), acc);
+      }
     }
     return;
   }
