@@ -29,7 +29,23 @@ __global__ void __launch_bounds__(kRedThreads) multidot_partial_kernel(const dou
   for (int q = 0; q < kDotQ; ++q) acc[q] = 0.0;
   const bool vec = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(V) | (uintptr_t)(ldv * 8)) & 15) == 0;
   const int64_t stride = (int64_t)gridDim.x * kRedThreads * 2;
-  for (int64_t i = ((int64_t)blockIdx.x * kRedThreads + threadIdx.x) * 2; i < n; i += stride) {
+  int64_t i = ((int64_t)blockIdx.x * kRedThreads + threadIdx.x) * 2;
+  if (vec)  // two grid-stride steps per trip (their loads in flight together), same order
+    for (; i + stride + 1 < n; i += 2 * stride) {
+      const double2 x0 = __ldg(reinterpret_cast<const double2*>(w + i));
+      const double2 x1 = __ldg(reinterpret_cast<const double2*>(w + i + stride));
+#pragma unroll
+      for (int q = 0; q < kDotQ; ++q)
+        if (q < nq) {
+          const double2 v0 = __ldcs(reinterpret_cast<const double2*>(V + q * ldv + i));
+          const double2 v1 = __ldcs(reinterpret_cast<const double2*>(V + q * ldv + i + stride));
+          acc[q] = fma(v0.x, x0.x, acc[q]);
+          acc[q] = fma(v0.y, x0.y, acc[q]);
+          acc[q] = fma(v1.x, x1.x, acc[q]);
+          acc[q] = fma(v1.y, x1.y, acc[q]);
+        }
+    }
+  for (; i < n; i += stride) {
     if (vec && i + 1 < n) {
       const double2 x = __ldg(reinterpret_cast<const double2*>(w + i));
 #pragma unroll
