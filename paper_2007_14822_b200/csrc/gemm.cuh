@@ -64,8 +64,8 @@ struct WorkRange {
   int64_t it, it_end;  // stream-K iteration range (iterations counted from dp_tiles*ktiles)
   int tile;            // data-parallel cursor
   int dp_tiles, ktiles;
-  // block-sparse mode (kb_list != null): tiles taken whole in `order`, each over the
-  // k-blocks kb_list[kb_ptr[t] .. kb_ptr[t+1])
+  // block-sparse mode (kb_list != null): tiles taken whole in `order` (CTA b: entries b,
+  // b+G, ...; -1 = padding), each over the k-blocks kb_list[kb_ptr[t] .. kb_ptr[t+1])
   const int* order;
   const int* kb_ptr;
   __device__ WorkRange(int cta, int tiles, int dp_tiles_, int ktiles_, const int* order_, const int* kb_ptr_)
@@ -77,8 +77,10 @@ struct WorkRange {
   }
   // next (tile, [i0, i1)) segment; i indexes k-blocks (dense) or kb_list (sparse)
   __device__ bool next(int& t, int& i0, int& i1) {
-    if (tile < dp_tiles) {
+    while (tile < dp_tiles) {
       t = order ? __ldg(order + tile) : tile;
+      tile += gridDim.x;
+      if (t < 0) continue;  // padding of a per-CTA (LPT) block-sparse schedule
       if (kb_ptr) {
         i0 = __ldg(kb_ptr + t);
         i1 = __ldg(kb_ptr + t + 1);
@@ -86,7 +88,6 @@ struct WorkRange {
         i0 = 0;
         i1 = ktiles;
       }
-      tile += gridDim.x;
       return true;
     }
     if (it >= it_end) return false;

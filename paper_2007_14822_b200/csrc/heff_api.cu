@@ -19,6 +19,7 @@
 #include <unordered_map>
 #include <thread>
 #include <map>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -211,6 +212,7 @@ static int launch_tma(GemmOp& g, cudaStream_t s, int* nlaunch, SplitWs* ws, cons
   const int64_t waves = (tiles + g_num_sms - 1) / g_num_sms;
   const double eff = (double)tiles / (double)(waves * g_num_sms);
   const bool sparse = g.sp_list != nullptr;
+  if (sparse && g.sp_len > 0) dp_tiles = g.sp_len;
   if (!sparse && ws && eff < 0.995 && getenv("HEFF_NO_STREAMK") == nullptr) {
     dp_tiles = (tiles >= 2 * (int64_t)g_num_sms) ? (tiles / g_num_sms - 1) * g_num_sms : 0;
     const int64_t sk_iters = (tiles - dp_tiles) * ktiles;
@@ -1852,7 +1854,8 @@ static int env_common_check(const heff_env_dims* d, const void* a, const void* b
 
 static int build_sparse_schedule(int64_t M, int64_t N, const std::vector<int>& rowv, const std::vector<int>& colv,
                                  const std::vector<std::vector<int>>& kvals, int** d_out, int64_t* total_kb,
-                                 const int** order, const int** ptr, const int** list, int64_t* makespan);
+                                 const int** order, const int** ptr, const int** list, int64_t* makespan,
+                                 int* order_len);
 static bool sparse_worth_it(int64_t M, int64_t N, int64_t K, int64_t makespan);
 
 // U(1) schedules of the environment GEMMs (heff_env_update_*_qn); per-thread device buffers
@@ -1863,8 +1866,9 @@ static thread_local int* t_env_sp3 = nullptr;
 static int env_schedule(GemmOp& g, const std::vector<int>& rowv, const std::vector<int>& colv,
                         const std::vector<std::vector<int>>& kvals, int** buf) {
   int64_t tot = 0, span = 0;
-  CKR(build_sparse_schedule(g.M, g.N, rowv, colv, kvals, buf, &tot, &g.sp_order, &g.sp_ptr, &g.sp_list, &span));
-  if (!sparse_worth_it(g.M, g.N, g.K, span)) g.sp_order = g.sp_ptr = g.sp_list = nullptr;
+  CKR(build_sparse_schedule(g.M, g.N, rowv, colv, kvals, buf, &tot, &g.sp_order, &g.sp_ptr, &g.sp_list, &span,
+                            &g.sp_len));
+  if (!sparse_worth_it(g.M, g.N, g.K, span)) { g.sp_order = g.sp_ptr = g.sp_list = nullptr; g.sp_len = 0; }
   return HEFF_OK;
 }
 
@@ -2089,7 +2093,8 @@ static std::vector<std::vector<int>> kblocks_by_value(const std::vector<int>& kv
 // kvals[kb]: the charges present in k-block kb.  Returns order | ptr | list in one buffer.
 static int build_sparse_schedule(int64_t M, int64_t N, const std::vector<int>& rowv, const std::vector<int>& colv,
                                  const std::vector<std::vector<int>>& kvals, int** d_out, int64_t* total_kb,
-                                 const int** order, const int** ptr, const int** list, int64_t* makespan) {
+                                 const int** order, const int** ptr, const int** list, int64_t* makespan,
+                                 int* order_len) {
   const int num_m = (int)((M + kBM - 1) / kBM), num_n = (int)((N + kBN - 1) / kBN);
   const int tiles = num_m * num_n;
   int vmin = INT32_MAX, vmax = INT32_MIN;
@@ -2122,17 +2127,48 @@ static int build_sparse_schedule(int64_t M, int64_t N, const std::vector<int>& r
     lists[t] = kb;
     tot += (int64_t)kb.size();
   }
-  std::vector<int> ord(tiles);
-  for (int t = 0; t < tiles; ++t) ord[t] = t;
-  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return lists[a].size() > lists[b].size(); });
-  {  // k-blocks of the busiest CTA under the kernel's round-robin over `ord` (+ per-tile overhead ~2 k-blocks)
-    const int G = std::min<int>(tiles, g_num_sms);
-    std::vector<int64_t> load(G, 0);
-    for (int i = 0; i < tiles; ++i) load[i % G] += (int64_t)lists[ord[i]].size() + 2;
-    *makespan = *std::max_element(load.begin(), load.end());
+  std::vector<int> byw(tiles);
+  for (int t = 0; t < tiles; ++t) byw[t] = t;
+  std::stable_sort(byw.begin(), byw.end(), [&](int a, int b) { return lists[a].size() > lists[b].size(); });
+  // LPT: tiles in descending work (k-blocks + ~2 of per-tile overhead) each to the least
+  // loaded of the G CTAs (ties: lowest index); the kernel walks CTA b's list as entries
+  // b, b+G, ... of `ord`, padded with -1 to the longest list
+  const int G = std::min<int>(tiles, g_num_sms);
+  std::vector<std::vector<int>> per(G);
+  if (getenv("HEFF_QN_ROUND_ROBIN")) {  // the plain round-robin over `byw` (comparison knob)
+    int64_t span = 0;
+    for (int b = 0; b < G; ++b) {
+      int64_t l = 0;
+      for (int i = b; i < tiles; i += G) {
+        per[b].push_back(byw[i]);
+        l += (int64_t)lists[byw[i]].size() + 2;
+      }
+      span = std::max(span, l);
+    }
+    *makespan = span;
+  } else {
+    using Load = std::pair<int64_t, int>;
+    std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+    for (int b = 0; b < G; ++b) heap.push({0, b});
+    int64_t span = 0;
+    for (int t : byw) {
+      Load l = heap.top();
+      heap.pop();
+      per[l.second].push_back(t);
+      l.first += (int64_t)lists[t].size() + 2;
+      span = std::max(span, l.first);
+      heap.push(l);
+    }
+    *makespan = span;
   }
+  size_t cmax = 0;
+  for (auto& v : per) cmax = std::max(cmax, v.size());
+  std::vector<int> ord((size_t)G * cmax, -1);
+  for (int b = 0; b < G; ++b)
+    for (size_t i = 0; i < per[b].size(); ++i) ord[i * G + b] = per[b][i];
+  *order_len = (int)ord.size();
   std::vector<int> buf;
-  buf.reserve((size_t)tiles * 2 + 1 + (size_t)tot);
+  buf.reserve(ord.size() + (size_t)tiles + 1 + (size_t)tot);
   buf.insert(buf.end(), ord.begin(), ord.end());
   int64_t acc = 0;
   for (int t = 0; t < tiles; ++t) { buf.push_back((int)acc); acc += (int64_t)lists[t].size(); }
@@ -2144,8 +2180,8 @@ static int build_sparse_schedule(int64_t M, int64_t N, const std::vector<int>& r
   CK(cudaMalloc(d_out, sizeof(int) * buf.size()));
   CK(cudaMemcpy(*d_out, buf.data(), sizeof(int) * buf.size(), cudaMemcpyHostToDevice));
   *order = *d_out;
-  *ptr = *d_out + tiles;
-  *list = *d_out + 2 * tiles + 1;
+  *ptr = *d_out + ord.size();
+  *list = *d_out + ord.size() + tiles + 1;
   *total_kb = tot;
   return HEFF_OK;
 }
@@ -2175,8 +2211,8 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
     p->qn_idx = nullptr;
     p->dense_in = p->dense_out = nullptr;
     p->qn_n = 0;
-    p->g1.sp_order = p->g1.sp_ptr = p->g1.sp_list = nullptr;
-    p->g4.sp_order = p->g4.sp_ptr = p->g4.sp_list = nullptr;
+    p->g1.sp_order = p->g1.sp_ptr = p->g1.sp_list = nullptr; p->g1.sp_len = 0;
+    p->g4.sp_order = p->g4.sp_ptr = p->g4.sp_list = nullptr; p->g4.sp_len = 0;
     p->sp_kblocks = 0;
     return HEFF_OK;
   }
@@ -2206,10 +2242,10 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
     }
     int64_t tot = 0, span = 0;
     CKR(build_sparse_schedule(M, N, rowv, colv, kvals, &p->sp1, &tot, &p->g1.sp_order, &p->g1.sp_ptr, &p->g1.sp_list,
-                              &span));
+                              &span, &p->g1.sp_len));
     p->sp_kblocks = tot;
     if (!sparse_worth_it(M, N, K, span)) {  // dense (stream-K) schedule is faster here
-      p->g1.sp_order = p->g1.sp_ptr = p->g1.sp_list = nullptr;
+      p->g1.sp_order = p->g1.sp_ptr = p->g1.sp_list = nullptr; p->g1.sp_len = 0;
       p->sp_kblocks = dense_kblock_tiles(M, N, K);
     }
   }
@@ -2230,9 +2266,9 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
       }
     int64_t tot = 0, span = 0;
     CKR(build_sparse_schedule(M, N, rowv, colv, kvals, &p->sp4, &tot, &p->g4.sp_order, &p->g4.sp_ptr, &p->g4.sp_list,
-                              &span));
+                              &span, &p->g4.sp_len));
     if (!sparse_worth_it(M, N, K, span)) {
-      p->g4.sp_order = p->g4.sp_ptr = p->g4.sp_list = nullptr;
+      p->g4.sp_order = p->g4.sp_ptr = p->g4.sp_list = nullptr; p->g4.sp_len = 0;
       tot = dense_kblock_tiles(M, N, K);
     }
     p->sp_kblocks += tot;

@@ -53,6 +53,7 @@ struct GemmOp {
   const int* sp_order = nullptr;
   const int* sp_ptr = nullptr;
   const int* sp_list = nullptr;
+  int sp_len = 0;  // length of sp_order (per-CTA LPT lists interleaved, -1 padded); 0: #tiles
   // cached TMA maps (rebuilt when A/B pointers or the tile box change)
   CUtensorMap mapA, mapB;
   const double* mapA_ptr = nullptr;
