@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
@@ -389,6 +390,14 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     converged = nrot == 0;
     double maxoff;
     memcpy(&maxoff, &offbits, sizeof maxoff);
+    if (timing) {
+      static thread_local std::chrono::steady_clock::time_point t_prev;
+      const auto t_now = std::chrono::steady_clock::now();
+      if (sw > 0)
+        fprintf(stderr, "  sweep %d: %d of %lld pair steps rotated, max off-diagonal %.2e, %.2f ms\n", sw, nrot,
+                (long long)npairs * rounds, maxoff, std::chrono::duration<double, std::milli>(t_now - t_prev).count());
+      t_prev = t_now;
+    }
     inner = maxoff < inner_thresh ? kSvdMaxInnerSweeps : 1;  // see svd.cuh kSvdMaxInnerSweeps
     if (const char* f = getenv("HEFF_SVD_INNER_FORCE")) inner = atoi(f);  // profiling knob
   }
