@@ -115,6 +115,8 @@ def run_reference(args):
     if rank != 0:
         return 0
     oracle.build()
+    # all host cores (torchrun exports OMP_NUM_THREADS=1 to its ranks; only rank 0 works here)
+    oracle.set_threads(os.cpu_count() or 1)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     x = C.make(args.config, device=dev).to("cpu")
     L, W1, W2, R, psi = x.numpy()
