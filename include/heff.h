@@ -151,8 +151,10 @@ int heff_create_sum(heff_plan* out, const heff_plan* terms, int nterms);
  * penalty.  Not supported on b'-sharded plans (HEFF_EUNSUPPORTED). */
 int heff_set_penalty(heff_plan p, const double* phis, int nphi, double weight, heff_stream stream);
 
-/* Destroys a plan (synchronises the device; workspace blocks go to the cache described at
- * heff_release_caches). */
+/* Destroys a plan: waits for the plan's last enqueued operation (a completion event
+ * recorded by heff_apply / heff_apply_blocked / heff_set_penalty; the whole device if the
+ * plan never ran), then returns its workspace blocks to the cache described at
+ * heff_release_caches. */
 int heff_destroy(heff_plan p);
 
 /* Thread-local message describing the last failure on this thread ("" if none). */

@@ -419,6 +419,7 @@ struct heff_plan_s {
   double *stage_in = nullptr, *stage_out = nullptr;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t e2e_ev[17] = {};                // 2 kE2eChunks + 1
+  cudaEvent_t done_ev = nullptr;              // recorded after each enqueued plan operation
   // Lanczos
   double* basis = nullptr;                  // [cap][ldv]
   int basis_cap = 0;
@@ -624,9 +625,21 @@ static void free_csr(Csr& c) {
   c = Csr{};
 }
 
+// Record the plan's completion event on `s` after an enqueued operation (heff_destroy
+// waits for it before handing the plan's blocks back to the workspace cache).
+static int mark_done(heff_plan_s* p, cudaStream_t s) {
+  if (!p->done_ev) CK(cudaEventCreateWithFlags(&p->done_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(p->done_ev, s));
+  return HEFF_OK;
+}
+
 extern "C" int heff_destroy(heff_plan p) {
   if (!p) return HEFF_OK;
-  cudaDeviceSynchronize();  // no kernel of this plan may still use a block handed back to the cache
+  // no kernel of this plan may still use a block handed back to the cache: wait for the
+  // plan's last operation (plans are used on one stream at a time), not the whole device
+  if (p->done_ev) cudaEventSynchronize(p->done_ev);
+  else cudaDeviceSynchronize();
+  if (p->copy_stream) cudaStreamSynchronize(p->copy_stream);
   for (void* b : {(void*)p->T1, (void*)p->T3, (void*)p->V1, (void*)p->V3, (void*)p->stage_in, (void*)p->stage_out,
                   (void*)p->basis, (void*)p->work, (void*)p->full, (void*)p->gather, (void*)p->partial,
                   (void*)p->scal, (void*)p->Lp, (void*)p->Rp, (void*)p->zin, (void*)p->zout, (void*)p->dense_in,
@@ -644,6 +657,7 @@ extern "C" int heff_destroy(heff_plan p) {
   for (auto& e : p->e2e_ev)
     if (e) cudaEventDestroy(e);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->done_ev) cudaEventDestroy(p->done_ev);
   if (p->win && p->comm && g_nccl.CommWindowDeregister) g_nccl.CommWindowDeregister(p->comm, p->win);
   if (p->win_buf && g_nccl.MemFree) g_nccl.MemFree(p->win_buf);
   cudaFree(p->d_peer_flags);
@@ -1207,7 +1221,7 @@ extern "C" int heff_set_penalty(heff_plan p, const double* phis, int nphi, doubl
                        cudaMemcpyDeviceToDevice, s));
   p->nphi = nphi;
   p->pen_weight = weight;
-  return HEFF_OK;
+  return mark_done(p, s);
 }
 
 extern "C" int heff_apply_blocked(heff_plan p, const double* psi_blocked, double* out, heff_stream stream) {
@@ -1225,12 +1239,16 @@ extern "C" int heff_apply_blocked(heff_plan p, const double* psi_blocked, double
   CKR(apply_orderB(p, nullptr, out, reinterpret_cast<cudaStream_t>(stream), &nl, 0, &sa));
   p->last_launches = nl;
   p->total_launches += nl;
-  return HEFF_OK;
+  return mark_done(p, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int heff_apply(heff_plan p, const double* psi, double* out, heff_stream stream) {
   if (!p) return set_err(HEFF_EINVAL, "heff_apply: null plan");
-  return apply_impl(p, psi, out, reinterpret_cast<cudaStream_t>(stream));
+  const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CKR(apply_impl(p, psi, out, s));
+  CKR(mark_done(p, s));
+  for (heff_plan_s* t : p->terms) CKR(mark_done(t, s));  // a composite's terms ran on s too
+  return HEFF_OK;
 }
 
 // End-to-end order-A matvec with the transfers overlapped: psi arrives in column chunks
