@@ -344,6 +344,7 @@ int init_device_once() {
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNTs::kSmemBytes));
   CK(cudaFuncSetAttribute(mpo_orderA_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   CK(cudaFuncSetAttribute(mpo_orderA_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(heff_small_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallMvMaxSmem));
   CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   CK(cudaFuncSetAttribute(mpo_orderB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   done.store(true, std::memory_order_release);
@@ -1006,9 +1007,36 @@ static int launch_mpo_A(const double* T1, double* T3, int64_t mR, int64_t rows, 
 }
 
 // --------------------------------------------------------------------------- the matvec
+// shared memory of heff_small_matvec_kernel for these dims (0 if it does not apply)
+static size_t small_matvec_smem(const heff_plan_s* p) {
+  const heff_dims& d = p->dims;
+  const int64_t dd = d.d1 * d.d2;
+  const int64_t n = d.mL * dd * d.mR + d.mR * d.kR * d.mR + d.kL * d.mL + (d.kL * dd + dd * d.kR) * d.mR;
+  const size_t bytes = sizeof(double) * (size_t)n;
+  // FMAs per CTA (one output row a'): the L.psi row and the .R^T row; above ~48k the
+  // 256-thread CTA loses to the DMMA path (measured: chain m <= 32 and cylinder m = 16 win,
+  // cylinder m = 24 at 92k loses 41 vs 32 us)
+  const int64_t work = d.kL * dd * d.mR * d.mL + dd * d.mR * d.kR * d.mR;
+  return (bytes <= (size_t)kSmallMvMaxSmem && work <= 48 * 1024) ? bytes : 0;
+}
+
 static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStream_t s, int* nl, int accumulate) {
   const heff_dims& d = p->dims;
   const int64_t nin = d.kL * d.d1 * d.d2, nout = d.d1 * d.d2 * d.kR;
+  // small bonds: the whole matvec in one launch (not with kernel profiling, which times the
+  // GEMM / MPO steps separately; HEFF_NO_SMALL_MATVEC=1 disables)
+  if (!p->profile && p->sp1 == nullptr && p->sp4 == nullptr && p->gemm_path == 0 && p->chunk_rows == d.mL) {
+    static const bool off = getenv("HEFF_NO_SMALL_MATVEC") != nullptr;
+    const size_t smem = off ? 0 : small_matvec_smem(p);
+    if (smem > 0) {
+      CK(launch_pdl(heff_small_matvec_kernel, dim3((unsigned)d.mL), dim3(kSmallMvThreads), smem, s, p->L, psi, p->R,
+                    out, (int)d.mL, (int)(d.d1 * d.d2), (int)d.mR, (int)d.kL, (int)d.kR,
+                    (const int*)p->csrA.d_rowptr, (const int*)p->csrA.d_col, (const double*)p->csrA.d_val,
+                    accumulate));
+      ++*nl;
+      return HEFF_OK;
+    }
+  }
   for (int64_t a0 = 0; a0 < d.mL; a0 += p->chunk_rows) {
     const int64_t rows = std::min(p->chunk_rows, d.mL - a0);
     CKR(prof_mark(p, 0, s));

@@ -116,6 +116,59 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_orderA_kernel(const double* _
   }
 }
 
+// Small bonds (the whole order-A matvec in one launch, m up to ~48): one CTA per output row
+// a' stages psi, R and L[a'] in shared memory and runs the three steps of (D) for that row --
+// T1[(w s1 s2)][b] = sum_a L[a',w,a] psi[a,(s1 s2),b], the two-site MPO through the CSR,
+// out[a',(s1' s2'),b'] = sum_{w2,b} T3[(s1' s2' w2)][b] R[b',w2,b] -- with plain FP64 FMAs.
+// At these sizes the DMMA GEMM path is launch- and latency-bound (three launches of a few
+// tiles each).  accumulate: out += instead of =.
+constexpr int kSmallMvThreads = 256;
+constexpr int kSmallMvMaxSmem = 200 * 1024;  // larger bonds: the GEMM path wins (measured)
+__global__ void __launch_bounds__(kSmallMvThreads) heff_small_matvec_kernel(
+    const double* __restrict__ L, const double* __restrict__ psi, const double* __restrict__ R,
+    double* __restrict__ out, int mL, int dd, int mR, int kL, int kR, const int* __restrict__ rowptr,
+    const int* __restrict__ col, const double* __restrict__ val, int accumulate) {
+  extern __shared__ __align__(16) double sm[];
+  const int nin = kL * dd, nout = dd * kR;
+  double* s_psi = sm;                                // [mL][dd][mR]
+  double* s_R = s_psi + (size_t)mL * dd * mR;        // [mR][kR][mR]
+  double* s_L = s_R + (size_t)mR * kR * mR;          // [kL][mL]  (row a')
+  double* s_T1 = s_L + (size_t)kL * mL;              // [nin][mR]
+  double* s_T3 = s_T1 + (size_t)nin * mR;            // [nout][mR]
+  pdl_wait();
+  const int ap = blockIdx.x, tid = threadIdx.x;
+  for (int e = tid; e < mL * dd * mR; e += kSmallMvThreads) s_psi[e] = psi[e];
+  for (int e = tid; e < mR * kR * mR; e += kSmallMvThreads) s_R[e] = R[e];
+  for (int e = tid; e < kL * mL; e += kSmallMvThreads) s_L[e] = L[(size_t)ap * kL * mL + e];
+  __syncthreads();
+  for (int e = tid; e < nin * mR; e += kSmallMvThreads) {  // T1 row (w, s) at column b
+    const int r = e / mR, b = e - r * mR, w = r / dd, sp = r - w * dd;
+    double acc = 0.0;
+    for (int a = 0; a < mL; ++a) acc = fma(s_L[w * mL + a], s_psi[((size_t)a * dd + sp) * mR + b], acc);
+    s_T1[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < nout * mR; e += kSmallMvThreads) {  // the two-site MPO
+    const int o = e / mR, b = e - o * mR;
+    double acc = 0.0;
+    const int e1 = __ldg(rowptr + o + 1);
+    for (int q = __ldg(rowptr + o); q < e1; ++q) acc = fma(__ldg(val + q), s_T1[__ldg(col + q) * mR + b], acc);
+    s_T3[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < dd * mR; e += kSmallMvThreads) {  // out[a', s', b']
+    const int sp = e / mR, bp = e - sp * mR;
+    double acc = 0.0;
+    for (int w2 = 0; w2 < kR; ++w2) {
+      const double* t3 = s_T3 + (size_t)(sp * kR + w2) * mR;
+      const double* r = s_R + ((size_t)bp * kR + w2) * mR;
+      for (int b = 0; b < mR; ++b) acc = fma(t3[b], r[b], acc);
+    }
+    double* o = out + ((size_t)ap * dd + sp) * mR + bp;
+    *o = accumulate ? *o + acc : acc;
+  }
+}
+
 // Order B on a b'-shard of width nb.  V1: [mL][d1 d2][nb][kR]; V3: [kL][mL][d1 d2][nb].
 // CSR rows o = (w,s1',s2') (nout = kL d1 d2).  The host stores each CSR column already as
 // its shared-memory offset (s*kMpoCols + 0)*kR + w2 for input (s = (s1,s2), w2), so the
