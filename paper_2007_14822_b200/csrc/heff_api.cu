@@ -526,9 +526,9 @@ extern "C" size_t heff_workspace_bytes(const heff_dims* d, const heff_dist* dist
 // destroys one plan per bond, and cudaMalloc/cudaFree of ~GB buffers (cudaFree also
 // synchronises the device) cost 5-8 ms per bond at m = 256-1024 against 1-40 ms of
 // Lanczos.  A request takes the smallest cached block of the same device with
-// bytes <= size <= 2 bytes + 64 MB; heff_destroy synchronises the device and returns its
-// blocks (blocks up to 4 GB, 16 GB in total, are kept; others are freed); heff_release_caches
-// frees them all.
+// bytes <= size <= 2 bytes + 64 MB; heff_destroy waits for the plan's last operation and
+// returns its blocks (blocks up to 4 GB are kept, 16 GB in total, the least recently
+// released evicted first); heff_release_caches frees them all.
 // An allocation that fails frees the cache and retries.
 struct WsBlock {
   void* p;
@@ -571,8 +571,7 @@ static cudaError_t ws_malloc(T** out, size_t bytes) {
   }
   if (best >= 0) {
     const WsBlock b = g_ws_free[best];
-    g_ws_free[best] = g_ws_free.back();
-    g_ws_free.pop_back();
+    g_ws_free.erase(g_ws_free.begin() + best);  // keeps the release order (oldest first)
     g_ws_cached -= b.bytes;
     g_ws_live[b.p] = b;
     *out = static_cast<T*>(b.p);
@@ -602,11 +601,16 @@ static void ws_release(void* ptr) {
   }
   const WsBlock b = it->second;
   g_ws_live.erase(it);
-  if (b.bytes <= kWsBlockMax && g_ws_cached + b.bytes <= kWsCacheMax) {
-    g_ws_free.push_back(b);
-    g_ws_cached += b.bytes;
-  } else {
+  if (b.bytes > kWsBlockMax) {
     cudaFree(b.p);
+    return;
+  }
+  g_ws_free.push_back(b);
+  g_ws_cached += b.bytes;
+  while (g_ws_cached > kWsCacheMax) {  // evict the least recently released blocks
+    cudaFree(g_ws_free.front().p);
+    g_ws_cached -= g_ws_free.front().bytes;
+    g_ws_free.erase(g_ws_free.begin());
   }
 }
 
