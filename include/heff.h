@@ -176,7 +176,9 @@ int heff_dot(int64_t n, const double* x, const double* y, double* result, heff_s
 /* Writes a fresh 128-byte ncclUniqueId (rank 0 calls this, then broadcasts it). */
 int heff_nccl_unique_id(unsigned char uid[128]);
 
-/* Tuning / test knobs.  HEFF_OPT_GEMM_PATH: 0 auto, 1 plain-load DMMA GEMM, 2 TMA DMMA GEMM.
+/* Tuning / test knobs.  HEFF_OPT_GEMM_PATH: 0 auto (small bonds: the fused one-launch
+ * matvec kernel; otherwise the TMA DMMA GEMM where the operands allow it), 1 plain-load DMMA
+ * GEMM, 2 TMA DMMA GEMM.
  * HEFF_OPT_LAST_KERNEL_COUNT (get only): kernels launched by the last heff_apply. */
 enum { HEFF_OPT_GEMM_PATH = 1, HEFF_OPT_LAST_KERNEL_COUNT = 2, HEFF_OPT_MPO_NNZ = 3 };
 int heff_set_option(heff_plan p, int option, int64_t value);
