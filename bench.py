@@ -99,13 +99,26 @@ def cpu_baseline(x, budget_s: float = 12.0) -> dict:
         el = time.perf_counter() - t0
         if el >= budget_s or rows_done >= mL:
             break
-    return {"value": rows_done / mL / el, "unit": "matvec/s", "cores": cores, "kind": "oracle",
+    return {"value": rows_done / mL / el, "unit": "matvec/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{rows_done} of {mL} output rows a' (order A, independent per a'), {el:.1f} s; "
                       f"value = rows/s / mL", "seconds": el}
 
 
+def bench_config(cfg: str, dims: dict, flops: float) -> dict:
+    """The workload description both arms print (identical dicts: same metric, same config)."""
+    return {"workload": workload_name(cfg, dims), **dims, "flops_per_matvec": flops,
+            "step": "one Lanczos iteration (one H_eff.psi matvec + CGS2 + norm + host tridiagonal)",
+            "l2": "inputs larger than L2 (psi 0.54 GB, L and R 2.7 GB each)" if cfg == "c4" else "see DESIGN.md 7"}
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle timed on bounded samples of the same workload."""
+    """--impl reference: the CPU oracle timed on bounded samples of the same workload.
+
+    Each step computes a bounded sample of one matvec -- `cores` output rows a' (order A
+    rows are independent), one per host thread -- and its measured wall time is the line's
+    ms_per_step; value (matvec/s) = (rows / mL) / that time.  The whole-matvec time this
+    implies is reported separately (ms_per_matvec_extrapolated), checked against one whole
+    oracle matvec in profiles/r02_oracle_timings.json."""
     import numpy as np  # noqa: F401
     import torch
     from heffgen import configs as C
@@ -133,16 +146,51 @@ def run_reference(args):
     frac = rows / mL
     value = args.steps * frac / el
     flops = C.flops_per_matvec(x.dims)
+    sample = f"each step = {rows} of {mL} output rows a' of one matvec (order A oracle, one row per thread)"
     line = {"metric": METRIC, "value": value, "unit": "matvec/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3 / frac,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "ms_per_matvec_extrapolated": el / args.steps * 1e3 / frac,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.config, x.dims), **x.dims, "parallelism": "cpu_oracle"},
+            "config": bench_config(args.config, x.dims, flops), "layout": "CPU oracle (oracle/heff_oracle.c, OpenMP)",
             "tflops": value * flops / 1e12,
-            "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle",
-                             "sample": f"each step = {rows} of {mL} output rows a' of one matvec (order A oracle)"},
+            "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_model() -> str | None:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """--gpus N without a torchrun environment: re-launch this command as N ranks (one per
+    GPU) under torch.distributed.run and return its exit code.  Fewer than N visible GPUs is
+    an error (never a 1-GPU number labelled as N)."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} but only {have} CUDA device(s) are visible", file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    print("bench.py: spawning " + " ".join(cmd[1:6]) + f" ... ({n} ranks)", file=sys.stderr, flush=True)
+    return subprocess.run(cmd).returncode
 
 
 def load_ncu_traffic(kernel_key: str):
@@ -173,6 +221,11 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus < 1:
+        print("bench.py: --gpus must be >= 1", file=sys.stderr)
+        return 2
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus)
 
     import numpy as np
     import torch
@@ -188,7 +241,9 @@ def main():
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
     if world != args.gpus:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE", file=sys.stderr)
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}: refusing to report a mismatched n_gpus",
+              file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     sharded = world > 1 or args.sharded
@@ -312,12 +367,11 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload_name(args.config, dims), **dims, "order": order,
+                "config": bench_config(args.config, dims, flops),
+                "layout": {"order": order,
                            "parallelism": (f"b'-shard x{world} (" + ("gather-fused GEMM_A on NCCL symmetric-window "
                                            "peer pointers" if args.fused_gather else "NCCL all-gather") + ")")
-                           if sharded else "single GPU",
-                           "flops_per_matvec": flops, "l2": "inputs larger than L2 (psi 0.54 GB, L and R 2.7 GB each)",
-                           "step": "one Lanczos iteration (matvec + CGS2 + norm + host tridiagonal)"},
+                           if sharded else "single GPU"},
                 "tflops": value * flops / 1e12, "frac_fp64_peak": value * flops / 1e12 / (FP64_PEAK_TFLOPS * world),
                 "lanczos": {"energy": res.energy, "iters": res.iters},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}

@@ -243,6 +243,19 @@ enum { HEFF_OPT_FUSED_GATHER = 7 };
  * gather-fused sharded plans (the symmetric window is registered on every rank). */
 enum { HEFF_OPT_LANCZOS_RESERVE = 8 };
 
+/* Communicating plans (dist with a uid).
+ * HEFF_OPT_FORCE_ALLGATHER = 1: lanczos_ground runs the P > 1 exchange (ncclAllGather of
+ *   the shard into the blocked buffer + the re-layout kernel) even on a 1-rank
+ *   communicator, where it otherwise copies the shard (default: env HEFF_FORCE_ALLGATHER).
+ * Failure detection: every host wait of lanczos_ground on a communicating plan
+ *   polls the stream, ncclCommGetAsyncError and a no-progress timeout (env
+ *   HEFF_NCCL_TIMEOUT_S, default 300 s without a Lanczos step completing); a gather-fused
+ *   peer wait that times out (20 s) counts as an error too.  On error the plan calls
+ *   ncclCommAbort -- so the peers' collectives fail instead of hanging -- and returns
+ *   HEFF_ENCCL; the plan is then unusable (every later call returns HEFF_ENCCL; destroy it).
+ * HEFF_OPT_COMM_STATE (get only): 1 live communicator, 0 none, -1 aborted. */
+enum { HEFF_OPT_FORCE_ALLGATHER = 9, HEFF_OPT_COMM_STATE = 10 };
+
 /* ---- Environment update --------------------------------------
  * After each local eigensolve a DMRG sweep moves the window one site and grows the
  * environment by that site (Sec. 6.2; SPEC ProjMPO):

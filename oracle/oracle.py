@@ -134,6 +134,18 @@ def heff_apply_B(L, W1, W2, R, psi, cols: tuple[int, int] | None = None) -> np.n
     return out
 
 
+def heff_apply_B_cols(L, W1, W2, R, psi, cols) -> np.ndarray:
+    """Order B on an arbitrary list of output columns b' (sampled full-size parity): output
+    column b' depends on R only through its row R[b', :, :], so the listed rows are moved to
+    the front of an otherwise unread R' and ref_heff_apply_B runs on b' in [0, len(cols)).
+    Returns [mL, d1, d2, len(cols)].  (Row selection only; the arithmetic is ref_heff_apply_B.)"""
+    L, W1, W2, R, psi = map(_c, (L, W1, W2, R, psi))
+    cols = [int(c) for c in cols]
+    Rp = np.empty_like(R)                 # rows >= len(cols) are never read
+    Rp[: len(cols)] = R[cols]
+    return heff_apply_B(L, W1, W2, Rp, psi, cols=(0, len(cols)))
+
+
 def _cz(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.complex128)
 

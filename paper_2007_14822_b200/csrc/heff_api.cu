@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -171,11 +172,13 @@ static bool tma_ok(const GemmOp& g) {
 // Per-thread, per-stream workspaces for the free functions (heff_gemm, environment
 // updates): GEMMs enqueued by one thread on two streams may run concurrently and must not
 // share partial slots or the CTA ticket counter.
-using StreamWs = std::vector<std::pair<cudaStream_t, SplitWs>>;
+// Keyed by (device, stream): the legacy default stream (0) has the same handle on every device.
+using StreamWs = std::vector<std::pair<std::pair<int, cudaStream_t>, SplitWs>>;
 static SplitWs* ws_for(StreamWs& v, cudaStream_t s) {
+  const std::pair<int, cudaStream_t> key(cur_device(), s);
   for (auto& e : v)
-    if (e.first == s) return &e.second;
-  v.emplace_back(s, SplitWs());
+    if (e.first == key) return &e.second;
+  v.emplace_back(key, SplitWs());
   return &v.back().second;
 }
 
@@ -317,19 +320,33 @@ int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitWs* ws, 
 }
 
 static std::mutex g_init_mu;  // one-time initialisations may race from worker threads
+static std::atomic<uint64_t> g_dev_inited{0};  // bit d: device d initialised
+
+int cur_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  return std::min(std::max(dev, 0), kMaxDevices - 1);
+}
+
 int init_device_once() {
-  static std::atomic<bool> done{false};
-  if (done.load(std::memory_order_acquire)) return HEFF_OK;
-  std::lock_guard<std::mutex> lock(g_init_mu);
-  if (done.load(std::memory_order_acquire)) return HEFF_OK;
   int dev;
   CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return set_err(HEFF_EUNSUPPORTED, "device ordinal %d >= %d", dev, kMaxDevices);
+  const uint64_t bit = uint64_t(1) << dev;
+  if (g_dev_inited.load(std::memory_order_acquire) & bit) return HEFF_OK;
+  std::lock_guard<std::mutex> lock(g_init_mu);
+  if (g_dev_inited.load(std::memory_order_acquire) & bit) return HEFF_OK;
   int major = 0, minor = 0;
   CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
   CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
   if (major != 10 || minor != 0)
     return set_err(HEFF_EUNSUPPORTED, "libheff is built for sm_100a (B200); device is sm_%d%d", major, minor);
-  CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // grids are sized from one SM count: every device of a process must agree (all B200s do)
+  if (g_num_sms != 0 && g_num_sms != sms)
+    return set_err(HEFF_EUNSUPPORTED, "device %d has %d SMs, an earlier device %d", dev, sms, g_num_sms);
+  g_num_sms = sms;
   CK(cudaFuncSetAttribute(gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, true>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNT::kSmemBytes));
   CK(cudaFuncSetAttribute(gemm_dmma_tma_kernel<kBM, kBN, kWM, kWN, kStages, false>,
@@ -347,7 +364,7 @@ int init_device_once() {
   CK(cudaFuncSetAttribute(heff_small_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallMvMaxSmem));
   CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   CK(cudaFuncSetAttribute(mpo_orderB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  done.store(true, std::memory_order_release);
+  g_dev_inited.fetch_or(bit, std::memory_order_release);
   return HEFF_OK;
 }
 
@@ -416,6 +433,13 @@ struct heff_plan_s {
   std::vector<char*> peer_base;             // LSA pointers of every rank's window (host copy)
   uint64_t** d_peer_flags = nullptr;        // device array [P] of peer flag arrays
   uint64_t epoch = 0;
+  // failure handling of communicating plans: waits poll ncclCommGetAsyncError and a
+  // no-progress timeout; on error the communicator is aborted and the plan is unusable
+  int comm_dead = 0;
+  std::string comm_err;
+  int force_allgather = 0;                  // option HEFF_OPT_FORCE_ALLGATHER (1 rank: run the P>1 branch)
+  std::vector<cudaEvent_t> step_ev;         // recorded after each Lanczos step (progress of a wait)
+  int step_ev_used = 0;
   // e2e staging; the overlapped host path's copy stream and chunk events
   double *stage_in = nullptr, *stage_out = nullptr;
   cudaStream_t copy_stream = nullptr;
@@ -642,8 +666,14 @@ extern "C" int heff_destroy(heff_plan p) {
   if (!p) return HEFF_OK;
   // no kernel of this plan may still use a block handed back to the cache: wait for the
   // plan's last operation (plans are used on one stream at a time), not the whole device
-  if (p->done_ev) cudaEventSynchronize(p->done_ev);
-  else cudaDeviceSynchronize();
+  if (p->comm_dead) {
+    // work stuck behind an aborted collective completes (or fails) after ncclCommAbort
+    if (p->done_ev) cudaEventSynchronize(p->done_ev);
+  } else if (p->done_ev) {
+    cudaEventSynchronize(p->done_ev);
+  } else {
+    cudaDeviceSynchronize();
+  }
   if (p->copy_stream) cudaStreamSynchronize(p->copy_stream);
   for (void* b : {(void*)p->T1, (void*)p->T3, (void*)p->V1, (void*)p->V3, (void*)p->stage_in, (void*)p->stage_out,
                   (void*)p->basis, (void*)p->work, (void*)p->full, (void*)p->gather, (void*)p->partial,
@@ -663,6 +693,10 @@ extern "C" int heff_destroy(heff_plan p) {
     if (e) cudaEventDestroy(e);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->done_ev) cudaEventDestroy(p->done_ev);
+  for (auto& e : p->step_ev) cudaEventDestroy(e);
+  // an aborted communicator (comm == nullptr, comm_dead) is gone with its window handles:
+  // only the local allocation is freed (deregistration is collective and would wait for
+  // the dead peers)
   if (p->win && p->comm && g_nccl.CommWindowDeregister) g_nccl.CommWindowDeregister(p->comm, p->win);
   if (p->win_buf && g_nccl.MemFree) g_nccl.MemFree(p->win_buf);
   cudaFree(p->d_peer_flags);
@@ -715,6 +749,7 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
       ncclResult_t nr = g_nccl.CommInitRank(&p->comm, dist->nranks, id, dist->rank);
       if (nr != ncclSuccess) return fail(set_err(HEFF_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(nr)));
       if (const char* e = getenv("HEFF_FUSED_GATHER")) p->fused_gather = atoi(e) ? 1 : 0;
+      if (const char* e = getenv("HEFF_FORCE_ALLGATHER")) p->force_allgather = atoi(e) ? 1 : 0;
     }
   }
   // W copies
@@ -936,6 +971,11 @@ extern "C" int heff_set_option(heff_plan p, int option, int64_t value) {
         return set_err(HEFF_EUNSUPPORTED, "fused gather: communicating b'-sharded plans only");
       p->fused_gather = value ? 1 : 0;
       return HEFF_OK;
+    case HEFF_OPT_FORCE_ALLGATHER:
+      if (value && !(p->sharded && p->comm))
+        return set_err(HEFF_EUNSUPPORTED, "force all-gather: communicating b'-sharded plans only");
+      p->force_allgather = value ? 1 : 0;
+      return HEFF_OK;
     case HEFF_OPT_LANCZOS_RESERVE: {
       if (value < 1 || value > 100000) return set_err(HEFF_EINVAL, "lanczos reserve: 1 <= iterations <= 100000");
       LanczosLayout lay;
@@ -959,6 +999,8 @@ extern "C" int heff_get_option(heff_plan p, int option, int64_t* value) {
     case HEFF_OPT_TOTAL_LAUNCHES: *value = p->total_launches; return HEFF_OK;
     case HEFF_OPT_SPARSE_KBLOCKS: *value = p->sp_kblocks; return HEFF_OK;
     case HEFF_OPT_FUSED_GATHER: *value = p->fused_gather + 2 * p->fused_active; return HEFF_OK;
+    case HEFF_OPT_FORCE_ALLGATHER: *value = p->force_allgather; return HEFF_OK;
+    case HEFF_OPT_COMM_STATE: *value = p->comm ? 1 : (p->comm_dead ? -1 : 0); return HEFF_OK;
     default: return set_err(HEFF_EINVAL, "unknown option %d", option);
   }
 }
@@ -1445,6 +1487,78 @@ static int norm2(heff_plan_s* p, const double* w, int64_t n, double* nrm, double
   return HEFF_OK;
 }
 
+// ---- failure detection of communicating plans (SURVEY.md 5 "Failure detection") -----------
+// ncclCommAbort the plan's communicator after an error or timeout: the peers' pending and
+// future collectives on it fail instead of hanging; the plan stays unusable.
+static int comm_abort(heff_plan_s* p, const char* fmt, ...) {
+  char buf[384];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (p->comm && g_nccl.CommAbort) g_nccl.CommAbort(p->comm);
+  p->comm = nullptr;
+  p->comm_dead = 1;
+  p->win = nullptr;  // the window died with the communicator
+  p->comm_err = buf;
+  return set_err(HEFF_ENCCL, "%s (communicator aborted; destroy the plan)", buf);
+}
+
+static double nccl_timeout_s() {
+  static const double t = [] {
+    const char* e = getenv("HEFF_NCCL_TIMEOUT_S");
+    const double v = e ? atof(e) : 300.0;
+    return v > 0 ? v : 300.0;
+  }();
+  return t;
+}
+
+// Record "Lanczos step done" on s (progress marker for comm_wait).
+static int mark_step(heff_plan_s* p, cudaStream_t s) {
+  if (!p->comm) return HEFF_OK;
+  if (p->step_ev_used == (int)p->step_ev.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->step_ev.push_back(e);
+  }
+  CK(cudaEventRecord(p->step_ev[p->step_ev_used++], s));
+  return HEFF_OK;
+}
+
+// Wait for stream s.  Plans without a communicator: cudaStreamSynchronize.  With one: poll
+// the stream, ncclCommGetAsyncError (aborting on an error) and progress -- a step marker
+// completing resets the clock; no progress for HEFF_NCCL_TIMEOUT_S aborts the communicator.
+static int comm_wait(heff_plan_s* p, cudaStream_t s) {
+  if (!p->comm) {
+    if (p->comm_dead) return set_err(HEFF_ENCCL, "plan's communicator was aborted: %s", p->comm_err.c_str());
+    CK(cudaStreamSynchronize(s));
+    return HEFF_OK;
+  }
+  using clk = std::chrono::steady_clock;
+  auto t_prog = clk::now();
+  int seen = 0;
+  unsigned spin = 0;
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return comm_abort(p, "stream failed: %s", cudaGetErrorString(q));
+    ncclResult_t ar = ncclSuccess;
+    if (g_nccl.CommGetAsyncError(p->comm, &ar) != ncclSuccess ||
+        (ar != ncclSuccess && ar != ncclInProgress))
+      return comm_abort(p, "NCCL asynchronous error: %s", g_nccl.GetErrorString(ar));
+    while (seen < p->step_ev_used && cudaEventQuery(p->step_ev[seen]) == cudaSuccess) {
+      ++seen;
+      t_prog = clk::now();
+    }
+    const double idle = std::chrono::duration<double>(clk::now() - t_prog).count();
+    if (idle > nccl_timeout_s())
+      return comm_abort(p, "no progress for %.0f s (a peer is gone or stuck; HEFF_NCCL_TIMEOUT_S)", idle);
+    if (++spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  p->step_ev_used = 0;
+  return HEFF_OK;
+}
+
 // full-psi input for the matvec: all-gather the shard (communicating plans) or use v as is
 static int matvec_local(heff_plan_s* p, const double* v, double* w, cudaStream_t s) {
   if (!p->sharded) return apply_impl(p, v, w, s);
@@ -1452,7 +1566,7 @@ static int matvec_local(heff_plan_s* p, const double* v, double* w, cudaStream_t
   const heff_dims& d = p->dims;
   const int64_t rows = d.mL * d.d1 * d.d2;
   const int64_t nloc = rows * p->nb;
-  if (p->nranks == 1) {
+  if (p->nranks == 1 && !p->force_allgather) {
     CK(cudaMemcpyAsync(p->full, v, sizeof(double) * nloc, cudaMemcpyDeviceToDevice, s));
   } else {
     CKN(g_nccl.AllGather(v, p->gather, nloc, ncclFloat64, p->comm, s));
@@ -1515,7 +1629,7 @@ __global__ void peer_signal_kernel(uint64_t* const* peer_flags, int rank, int P,
 // spin (~20 s by %globaltimer) so a missing peer turns into a reported error, not a hang
 __global__ void peer_wait_kernel(const uint64_t* flags, int P, unsigned long long value, int* timed_out) {
   const int q = threadIdx.x;
-  if (q < P) {
+  if (q < P && *(volatile int*)timed_out == 0) {  // after one timeout the later waits fall through
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
@@ -1622,10 +1736,14 @@ static int lanczos_workspace(heff_plan_s* p, int cap, cudaStream_t s, LanczosLay
     CK(ws_malloc(&p->work, sizeof(double) * ldv));
     p->work_len = ldv;
   }
+  if (p->sharded && p->comm && !fgather && p->full && !p->gather && (p->nranks > 1 || p->force_allgather)) {
+    const heff_dims& d = p->dims;
+    CK(ws_malloc(&p->gather, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
+  }
   if (p->sharded && p->comm && !p->full && !fgather) {
     const heff_dims& d = p->dims;
     CK(ws_malloc(&p->full, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
-    if (p->nranks > 1) CK(ws_malloc(&p->gather, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
+    if (p->nranks > 1 || p->force_allgather) CK(ws_malloc(&p->gather, sizeof(double) * d.mL * d.d1 * d.d2 * d.mR));
   }
   *out = LanczosLayout{compact, cplx, fgather, n_dense, n, nr, ldv};
   return HEFF_OK;
@@ -1636,8 +1754,10 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   if (!p || !psi || !o || !energy) return set_err(HEFF_EINVAL, "lanczos_ground: null argument");
   if (o->max_iter < 1 || o->max_iter > 100000) return set_err(HEFF_EINVAL, "lanczos_ground: max_iter out of range");
   if (o->mode != 0 && o->mode != 1) return set_err(HEFF_EINVAL, "lanczos_ground: mode must be 0 or 1");
+  if (p->comm_dead) return set_err(HEFF_ENCCL, "plan's communicator was aborted: %s", p->comm_err.c_str());
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int cap = o->max_iter;
+  p->step_ev_used = 0;
   LanczosLayout lay;
   CKR(lanczos_workspace(p, cap, s, &lay));
   const bool compact = lay.compact, cplx = lay.cplx, fgather = lay.fgather;
@@ -1686,7 +1806,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   CKR(norm2(p, V, nr, beta + cap, invb + cap, s));
   double h_nrm = 0.0;
   CK(cudaMemcpyAsync(&h_nrm, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CKR(comm_wait(p, s));
   if (!(h_nrm > 0.0)) return set_err(HEFF_EZERO, "lanczos_ground: zero start vector");
   scale_kernel<<<ew_grid(nr), 256, 0, s>>>(V, invb + cap, V, nr);
   ++p->total_launches;
@@ -1772,10 +1892,13 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
 
   if (o->mode == 0) {
     // fixed steps: enqueue everything, read the scalars once, truncate at a breakdown
-    for (int j = 1; j <= cap; ++j) CKR(step(j));
+    for (int j = 1; j <= cap; ++j) {
+      CKR(step(j));
+      CKR(mark_step(p, s));
+    }
     CK(cudaMemcpyAsync(ha.data(), alpha, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hb.data(), beta, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CKR(comm_wait(p, s));
     for (int j = 1; j <= cap; ++j) {
       j_done = j;
       if (host_check(j)) break;
@@ -1790,10 +1913,13 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     bool stop = false;
     for (int j = 1; j <= cap && !stop;) {
       const int j1 = std::min(cap, j + batch - 1);
-      for (int jj = j; jj <= j1; ++jj) CKR(step(jj));
+      for (int jj = j; jj <= j1; ++jj) {
+        CKR(step(jj));
+        CKR(mark_step(p, s));
+      }
       CK(cudaMemcpyAsync(&ha[j - 1], alpha + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(&hb[j - 1], beta + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+      CKR(comm_wait(p, s));
       for (int jj = j; jj <= j1; ++jj) {
         j_done = jj;
         if (host_check(jj)) {
@@ -1824,12 +1950,14 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   }
   ++p->total_launches;
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(s));
+  CKR(comm_wait(p, s));
   if (fgather) {
     p->epoch += (uint64_t)cap + 1;
     int to = 0;
     CK(cudaMemcpy(&to, d_timeout, sizeof(int), cudaMemcpyDeviceToHost));
-    if (to) return set_err(HEFF_ENCCL, "lanczos_ground: a peer never published its Krylov vector (20 s timeout)");
+    // a rank that timed out cannot resynchronise its flag epoch with peers that went on:
+    // abort, so every rank's next collective fails instead of reading stale slots
+    if (to) return comm_abort(p, "lanczos_ground: a peer never published its Krylov vector (20 s timeout)");
   }
   *energy = theta;
   if (iters_done) *iters_done = j_done;
@@ -1855,10 +1983,10 @@ struct EnvArena {
   double* val = nullptr;
   size_t csr_cap = 0;
 };
-static thread_local EnvArena t_env_arena;
+static thread_local PerDev<EnvArena> t_env_arena;
 
 static int env_reserve(size_t doubles) {
-  EnvArena& a = t_env_arena;
+  EnvArena& a = t_env_arena();
   if (a.bytes >= doubles * sizeof(double)) return HEFF_OK;
   cudaFree(a.buf);
   a.buf = nullptr;
@@ -1870,7 +1998,7 @@ static int env_reserve(size_t doubles) {
 
 static int upload_csr(Csr& c, const std::vector<int>& rp, const std::vector<int>& cl, const std::vector<double>& vl,
                       cudaStream_t s) {
-  EnvArena& a = t_env_arena;
+  EnvArena& a = t_env_arena();
   const size_t need = std::max(rp.size(), std::max<size_t>(1, vl.size()));
   if (a.csr_cap < need) {
     cudaFree(a.rowptr); cudaFree(a.col); cudaFree(a.val);
@@ -1909,8 +2037,8 @@ static int build_sparse_schedule(int64_t M, int64_t N, const std::vector<int>& r
 static bool sparse_worth_it(int64_t M, int64_t N, int64_t K, int64_t makespan);
 
 // U(1) schedules of the environment GEMMs (heff_env_update_*_qn); per-thread device buffers
-static thread_local int* t_env_sp1 = nullptr;
-static thread_local int* t_env_sp3 = nullptr;
+static thread_local PerDev<int*> t_env_sp1 = {};
+static thread_local PerDev<int*> t_env_sp3 = {};
 
 // block-sparse schedule for one environment GEMM if charges are given and it pays off
 static int env_schedule(GemmOp& g, const std::vector<int>& rowv, const std::vector<int>& colv,
@@ -1960,7 +2088,7 @@ static int env_left_impl(const heff_env_dims* dims, const double* L, const doubl
   const int64_t nX = pad(d.mi * d.kl * d.d * d.mo), nY = pad(d.mi * d.d * d.kr * d.mo), nA = pad(d.mi * d.d * d.mo);
   CKR(env_reserve((size_t)(nX + nY + nA)));
   CKR(upload_csr(csr, rp, cl, vl, s));
-  double* X = t_env_arena.buf;
+  double* X = t_env_arena().buf;
   double* Y = X + nX;
   double* At = Y + nY;
   auto cleanup = [&]() { cudaStreamSynchronize(s); };
@@ -1979,13 +2107,13 @@ static int env_left_impl(const heff_env_dims* dims, const double* L, const doubl
       for (int64_t w = 0; w < d.kl; ++w) rowv[x * d.kl + w] = qn->q_in[x] - qn->cl[w];
     for (int64_t sg = 0; sg < d.d; ++sg)
       for (int64_t a = 0; a < d.mo; ++a) colv[sg * d.mo + a] = qn->q_out[a] - qn->qs[sg];
-    CKR(env_schedule(g1, rowv, colv, kblock_values(g1.K, [&](int64_t k) { return qn->q_in[k]; }), &t_env_sp1));
+    CKR(env_schedule(g1, rowv, colv, kblock_values(g1.K, [&](int64_t k) { return qn->q_in[k]; }), &t_env_sp1()));
     for (int64_t a = 0; a < d.mo; ++a) rowv3[a] = qn->q_out[a];
     for (int64_t wp = 0; wp < d.kr; ++wp)
       for (int64_t a = 0; a < d.mo; ++a) colv3[wp * d.mo + a] = qn->q_out[a] + qn->cr[wp];
     CKR(env_schedule(g3, rowv3, colv3,
                      kblock_values(g3.K, [&](int64_t k) { return qn->q_in[k / d.d] + qn->qs[k % d.d]; }),
-                     &t_env_sp3));
+                     &t_env_sp3()));
   }
   r = launch_gemm(g1, 0, s, &nl, ws_for(t_env_splitws, s));
   if (!r) {
@@ -2040,7 +2168,7 @@ static int env_right_impl(const heff_env_dims* dims, const double* R, const doub
   const int64_t nX = pad(d.mo * d.d * d.kr * d.mi), nY = pad(d.mo * d.kl * d.d * d.mi);
   CKR(env_reserve((size_t)(nX + nY)));
   CKR(upload_csr(csr, rp, cl, vl, s));
-  double* X = t_env_arena.buf;
+  double* X = t_env_arena().buf;
   double* Y = X + nX;
   auto cleanup = [&]() { cudaStreamSynchronize(s); };
   int r = HEFF_OK;
@@ -2057,13 +2185,13 @@ static int env_right_impl(const heff_env_dims* dims, const double* R, const doub
       for (int64_t sg = 0; sg < d.d; ++sg) rowv[b * d.d + sg] = qn->q_out[b] + qn->qs[sg];
     for (int64_t wp = 0; wp < d.kr; ++wp)
       for (int64_t y = 0; y < d.mi; ++y) colv[wp * d.mi + y] = qn->q_in[y] + qn->cr[wp];
-    CKR(env_schedule(g1, rowv, colv, kblock_values(g1.K, [&](int64_t k) { return qn->q_in[k]; }), &t_env_sp1));
+    CKR(env_schedule(g1, rowv, colv, kblock_values(g1.K, [&](int64_t k) { return qn->q_in[k]; }), &t_env_sp1()));
     for (int64_t b = 0; b < d.mo; ++b)
       for (int64_t w = 0; w < d.kl; ++w) rowv3[b * d.kl + w] = qn->q_out[b] - qn->cl[w];
     for (int64_t b = 0; b < d.mo; ++b) colv3[b] = qn->q_out[b];
     CKR(env_schedule(g3, rowv3, colv3,
                      kblock_values(g3.K, [&](int64_t k) { return qn->q_in[k % d.mi] - qn->qs[k / d.mi]; }),
-                     &t_env_sp3));
+                     &t_env_sp3()));
   }
   r = launch_gemm(g1, 0, s, &nl, ws_for(t_env_splitws, s));
   if (!r) {
@@ -2420,8 +2548,10 @@ void release_thread_caches() {
   t_env_splitws.clear();
   for (auto& e : t_gemm_ws) freews(e.second);
   t_gemm_ws.clear();
-  cudaFree(t_env_arena.buf); cudaFree(t_env_arena.rowptr); cudaFree(t_env_arena.col); cudaFree(t_env_arena.val);
-  t_env_arena = EnvArena();
+  t_env_arena.each([](EnvArena& a) {
+    cudaFree(a.buf); cudaFree(a.rowptr); cudaFree(a.col); cudaFree(a.val);
+    a = EnvArena();
+  });
   split_release_thread_caches();
 }
 

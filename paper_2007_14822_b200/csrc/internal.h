@@ -32,7 +32,25 @@ int set_err(int code, const char* fmt, ...);
   } while (0)
 
 extern int g_num_sms;
+// One-time per-DEVICE initialisation (sm_100 check, SM count, >48 KB shared-memory
+// attributes -- function attributes belong to a device context).  Every entry point calls
+// it for the calling thread's current device; cheap after the first call per device.
 int init_device_once();
+constexpr int kMaxDevices = 64;
+int cur_device();  // cudaGetDevice(), clamped to [0, kMaxDevices)
+
+// Per-thread, per-device state (workspace arenas): one T per device, selected by the
+// calling thread's current device, so a thread that switches devices (torchrun ranks after
+// set_device, the U(1) split's workers) never uses another device's buffers.
+template <typename T>
+struct PerDev {
+  T v[kMaxDevices];
+  T& operator()() { return v[cur_device()]; }
+  template <typename F>
+  void each(F&& f) {
+    for (int d = 0; d < kMaxDevices; ++d) f(v[d]);
+  }
+};
 int ew_grid(int64_t n);
 // 2-D row-major fp64 tensor map: `rows` x `cols`, row pitch `ld`; box {box_cols, box_rows};
 // 128-byte swizzle; OOB reads return zero

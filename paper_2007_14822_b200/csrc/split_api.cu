@@ -31,12 +31,13 @@ struct SvdArena {
   double* buf = nullptr;
   size_t bytes = 0;
 };
-static thread_local SvdArena t_svd_arena;
-static thread_local SplitWs t_svd_splitws;
-static thread_local double* t_small_info = nullptr;  // svd_small_kernel's 4-double read-back
+// per thread and per device (PerDev, internal.h)
+static thread_local PerDev<SvdArena> t_svd_arena;
+static thread_local PerDev<SplitWs> t_svd_splitws;
+static thread_local PerDev<double*> t_small_info = {};  // svd_small_kernel's 4-double read-back
 
 static int svd_reserve(size_t bytes) {
-  SvdArena& a = t_svd_arena;
+  SvdArena& a = t_svd_arena();
   if (a.bytes >= bytes) return HEFF_OK;
   cudaFree(a.buf);
   a.buf = nullptr;
@@ -106,10 +107,11 @@ extern "C" int heff_truncate_spectrum(const double* s, int64_t k, const heff_tru
 
 // one-time occupancy queries / attributes of the split's kernels (thread-safe)
 static int svd_init_once() {
-  static std::atomic<bool> done{false};
-  if (done.load(std::memory_order_acquire)) return HEFF_OK;
+  static std::atomic<uint64_t> done{0};  // bit d: device d (attributes are per device context)
+  const uint64_t bit = uint64_t(1) << cur_device();
+  if (done.load(std::memory_order_acquire) & bit) return HEFF_OK;
   std::lock_guard<std::mutex> lock(g_svd_init_mu);
-  if (done.load(std::memory_order_acquire)) return HEFF_OK;
+  if (done.load(std::memory_order_acquire) & bit) return HEFF_OK;
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lq_panel_kernel, kLqThreads, 0));
   g_lq_grid = std::max(1, per_sm) * g_num_sms;
@@ -127,7 +129,7 @@ static int svd_init_once() {
   g_svd_trot_occ = std::max(1, g_svd_trot_occ);
   CK(cudaFuncSetAttribute(svd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(sizeof(double) * ((size_t)kSvdSmallMax * kSvdSmallMax + 3 * kSvdSmallMax))));
-  done.store(true, std::memory_order_release);
+  done.fetch_or(bit, std::memory_order_release);
   return HEFF_OK;
 }
 
@@ -149,7 +151,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   CKR(svd_init_once());
   if (R <= kSvdSmallDispatch && colsP <= kSvdSmallDispatch && getenv("HEFF_SVD_NO_SMALL") == nullptr) {
     // small matrix: the whole split in one CTA (svd_small_kernel)
-    double*& d_info = t_small_info;
+    double*& d_info = t_small_info();
     if (!d_info) CK(cudaMalloc(&d_info, 4 * sizeof(double)));
     const int64_t ncp = colsP + (colsP & 1);
     const size_t smem = sizeof(double) * ((size_t)ncp * R + 3 * kSvdSmallMax);
@@ -209,7 +211,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
                                    al(sizeof(double) * kLqNb) + al(sizeof(double) * 2 * g_lq_grid * 2 * kLqNb)
                              : 0;
   CKR(svd_reserve(2 * bX + bG + bNorm + bPairs + bStat + bRed + bPerm + bUt + bQ + bSortPerm + bLq));
-  unsigned char* w = reinterpret_cast<unsigned char*>(t_svd_arena.buf);
+  unsigned char* w = reinterpret_cast<unsigned char*>(t_svd_arena().buf);
   double *d_P = nullptr, *d_Vt = nullptr, *d_W = nullptr, *d_Y = nullptr, *d_VtV = nullptr, *d_negT = nullptr,
          *d_beta = nullptr, *d_part = nullptr;
   int* d_rowperm = nullptr;  // X row r = output row d_rowperm[r] (preconditioned path)
@@ -302,7 +304,7 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
       GemmOp gv;  // V^T V = Vt Vt^T (K = L)
       gv.M = nbp; gv.N = nbp; gv.K = L; gv.A = d_Vt + j; gv.lda = colsP; gv.B = d_Vt + j; gv.ldb = colsP;
       gv.b_kmajor = true; gv.C = d_VtV; gv.ldc = nbp;
-      CKR(launch_gemm(gv, 0, s, &nl, &t_svd_splitws));
+      CKR(launch_gemm(gv, 0, s, &nl, &t_svd_splitws()));
       lq_build_t_kernel<<<1, 32, 0, s>>>(d_VtV, d_beta, nbp, d_negT);
       const int64_t rT = R - j - nbp;
       if (rT > 0) {
@@ -310,15 +312,15 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
         GemmOp g1;  // W = P_t V = P_t Vt^T
         g1.M = rT; g1.N = nbp; g1.K = L; g1.A = Pt; g1.lda = colsP; g1.B = d_Vt + j; g1.ldb = colsP;
         g1.b_kmajor = true; g1.C = d_W; g1.ldc = nbp;
-        CKR(launch_gemm(g1, 0, s, &nl, &t_svd_splitws));
+        CKR(launch_gemm(g1, 0, s, &nl, &t_svd_splitws()));
         GemmOp g2;  // Y = W (-T)
         g2.M = rT; g2.N = nbp; g2.K = nbp; g2.A = d_W; g2.lda = nbp; g2.B = d_negT; g2.ldb = nbp;
         g2.b_kmajor = false; g2.C = d_Y; g2.ldc = nbp;
-        CKR(launch_gemm(g2, 0, s, &nl, &t_svd_splitws));
+        CKR(launch_gemm(g2, 0, s, &nl, &t_svd_splitws()));
         GemmOp g3;  // P_t += Y Vt
         g3.M = rT; g3.N = L; g3.K = nbp; g3.A = d_Y; g3.lda = nbp; g3.B = d_Vt + j; g3.ldb = colsP;
         g3.b_kmajor = false; g3.C = Pt; g3.ldc = colsP; g3.accumulate = 1;
-        CKR(launch_gemm(g3, 0, s, &nl, &t_svd_splitws));
+        CKR(launch_gemm(g3, 0, s, &nl, &t_svd_splitws()));
       }
     }
     lq_pack_lower_kernel<<<ew_grid(nblk * kSvdB * R), 256, 0, s>>>(d_P, colsP, Xb, R, kmin, nblk);
@@ -434,13 +436,13 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     CKR(launch_transpose(d_Ut, Qout, n, M, s));                               // U [M][n]
     GemmOp g;  // C[n][N] = U^T[n][M] . Psi[M][N]
     g.M = n; g.N = N; g.K = M; g.A = d_Ut; g.lda = M; g.B = psi; g.ldb = N; g.b_kmajor = false; g.C = Cout; g.ldc = N;
-    r = launch_gemm(g, 0, s, &nl, &t_svd_splitws);
+    r = launch_gemm(g, 0, s, &nl, &t_svd_splitws());
   } else {
     svd_gather_t_kernel<<<gg, 256, 0, s>>>(Xb, R, d_perm, d_scale, Qout, d_rowperm, n);   // V^T [n][N]
     CK(cudaGetLastError());
     GemmOp g;  // C[M][n] = Psi[M][N] . (V^T)^T
     g.M = M; g.N = n; g.K = N; g.A = psi; g.lda = N; g.B = Qout; g.ldb = N; g.b_kmajor = true; g.C = Cout; g.ldc = n;
-    r = launch_gemm(g, 0, s, &nl, &t_svd_splitws);
+    r = launch_gemm(g, 0, s, &nl, &t_svd_splitws());
   }
   CK(cudaStreamSynchronize(s));
   if (r != HEFF_OK) return r;
@@ -480,12 +482,15 @@ class BlockPool {
     return *pool;
   }
   // run every task on the workers; returns when all have finished
+  // (on the calling thread's current device: each worker switches to it and uses its own
+  // stream of that device)
   void run(std::vector<std::function<void(cudaStream_t)>>& tasks) {
     Batch b;
     b.remaining = (int)tasks.size();
+    const int dev = cur_device();
     {
       std::lock_guard<std::mutex> lk(mu_);
-      for (auto& t : tasks) q_.push_back({&t, &b});
+      for (auto& t : tasks) q_.push_back({&t, &b, dev});
     }
     cv_.notify_all();
     std::unique_lock<std::mutex> lk(b.mu);
@@ -496,12 +501,13 @@ class BlockPool {
   struct Item {
     std::function<void(cudaStream_t)>* fn;
     Batch* batch;
+    int dev;
   };
   BlockPool() {
     for (int i = 0; i < kBlockWorkers; ++i) std::thread([this] { loop(); }).detach();
   }
   void loop() {
-    cudaStream_t ws = nullptr;
+    std::vector<cudaStream_t> ws(kMaxDevices, nullptr);  // this worker's stream on each device
     for (;;) {
       Item it;
       {
@@ -510,8 +516,9 @@ class BlockPool {
         it = q_.front();
         q_.erase(q_.begin());
       }
-      if (!ws) cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking);
-      (*it.fn)(ws);
+      cudaSetDevice(it.dev);
+      if (!ws[it.dev]) cudaStreamCreateWithFlags(&ws[it.dev], cudaStreamNonBlocking);
+      (*it.fn)(ws[it.dev]);
       std::lock_guard<std::mutex> lk(it.batch->mu);
       if (--it.batch->remaining == 0) it.batch->cv.notify_all();
     }
@@ -544,7 +551,7 @@ struct SvdQnArena {
   double* buf = nullptr;
   size_t bytes = 0;
 };
-static thread_local SvdQnArena t_svdqn_arena;
+static thread_local PerDev<SvdQnArena> t_svdqn_arena;
 
 extern "C" int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const int* qrow, const int* qcol,
                                  const heff_trunc* trunc, int dir, double* Qout, double* S, double* Sk, int* qk,
@@ -590,7 +597,7 @@ extern "C" int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const 
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t need = al(sizeof(int) * idx_host.size()) + al(sizeof(int) * (M + N)) + al(sizeof(int)) +
                       al(sizeof(double) * (tot_blk + tot_q + tot_c + tot_s)) + al(sizeof(int2) * kmin);
-  SvdQnArena& a = t_svdqn_arena;
+  SvdQnArena& a = t_svdqn_arena();
   if (a.bytes < need) {
     cudaFree(a.buf);
     a.buf = nullptr;
@@ -720,15 +727,23 @@ extern "C" int heff_svd_split_qn(int64_t M, int64_t N, const double* psi, const 
 
 // --------------------------------------------------------------------------- cache release
 void split_release_thread_caches() {
-  cudaFree(t_svd_splitws.ptr);
-  cudaFree(t_svd_splitws.sync);
-  t_svd_splitws = SplitWs();
-  cudaFree(t_svd_arena.buf);
-  t_svd_arena = SvdArena();
-  cudaFree(t_svdqn_arena.buf);
-  t_svdqn_arena = SvdQnArena();
-  cudaFree(t_small_info);
-  t_small_info = nullptr;
+  t_svd_splitws.each([](SplitWs& w) {
+    cudaFree(w.ptr);
+    cudaFree(w.sync);
+    w = SplitWs();
+  });
+  t_svd_arena.each([](SvdArena& a) {
+    cudaFree(a.buf);
+    a = SvdArena();
+  });
+  t_svdqn_arena.each([](SvdQnArena& a) {
+    cudaFree(a.buf);
+    a = SvdQnArena();
+  });
+  t_small_info.each([](double*& p) {
+    cudaFree(p);
+    p = nullptr;
+  });
 }
 
 int split_release_worker_caches(int dev) {

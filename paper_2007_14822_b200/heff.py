@@ -21,6 +21,7 @@ HEFF_ENOCONV = -7
 OPT_GEMM_PATH, OPT_LAST_KERNEL_COUNT, OPT_MPO_NNZ, OPT_PROFILE, OPT_TOTAL_LAUNCHES, OPT_SPARSE_KBLOCKS = 1, 2, 3, 4, 5, 6
 OPT_LANCZOS_RESERVE = 8
 OPT_FUSED_GATHER = 7
+OPT_FORCE_ALLGATHER, OPT_COMM_STATE = 9, 10
 
 
 class HeffError(RuntimeError):
@@ -442,6 +443,14 @@ class Heff:
         return (d["mL"], d["d1"], d["d2"], d["mR"])
 
     @property
+    def lanczos_len(self) -> int:
+        """Entries of lanczos_ground's vector: the shard on communicating sharded plans, else
+        the full psi (complex plans: complex entries)."""
+        d = self.dims
+        comm = self.dist is not None and self.dist.get("uid") is not None
+        return d["mL"] * d["d1"] * d["d2"] * (self.nb if comm else d["mR"])
+
+    @property
     def out_shape(self):
         d = self.dims
         return (d["mL"], d["d1"], d["d2"], self.nb)
@@ -462,9 +471,15 @@ class Heff:
         """Gather-fused matvec of a b'-sharded plan (heff_apply_blocked): psi_blocked is the
         blocked all-gather layout [P, mL*d1*d2, nb]; returns this plan's out shard."""
         _dev(psi_blocked, "psi_blocked")
+        d = self.dims
+        if psi_blocked.numel() != d["mL"] * d["d1"] * d["d2"] * d["mR"]:
+            raise ValueError(f"psi_blocked must hold P * mL*d1*d2 * nb = {d['mL'] * d['d1'] * d['d2'] * d['mR']} "
+                             f"doubles, got {psi_blocked.numel()}")
         if out is None:
             out = torch.empty(self.out_shape, dtype=torch.float64, device=psi_blocked.device)
         _dev(out, "out")
+        if out.numel() != d["mL"] * d["d1"] * d["d2"] * self.nb:
+            raise ValueError(f"out must have {self.out_shape} elements")
         _check(lib().heff_apply_blocked(self._h, psi_blocked.data_ptr(), out.data_ptr(), _stream(stream)))
         return out
 
@@ -474,13 +489,20 @@ class Heff:
         dt = torch.complex128 if getattr(self, "cplx", False) else torch.float64
         assert psi_host.dtype == dt and out_host.dtype == dt
         assert psi_host.is_contiguous() and out_host.is_contiguous()
+        d = self.dims
+        if psi_host.numel() != d["mL"] * d["d1"] * d["d2"] * d["mR"] or \
+                out_host.numel() != d["mL"] * d["d1"] * d["d2"] * self.nb:
+            raise ValueError(f"psi_host must have {self.psi_shape} elements and out_host {self.out_shape}")
         _check(lib().heff_apply_host(self._h, psi_host.data_ptr(), out_host.data_ptr(), _stream(stream)))
         return out_host
 
     def lanczos_ground(self, psi: torch.Tensor, max_iter: int, tol: float = 0.0, converge: bool = False,
                        stream=None) -> LanczosResult:
-        """psi: start vector (overwritten with the normalised Ritz vector)."""
+        """psi: start vector (overwritten with the normalised Ritz vector): the full vector
+        [mL, d1, d2, mR], or this rank's shard [mL, d1, d2, nb] on a communicating sharded plan."""
         _dev(psi, "psi", getattr(self, "cplx", False))
+        if psi.numel() != self.lanczos_len:
+            raise ValueError(f"psi must have {self.lanczos_len} entries for this plan, got {psi.numel()}")
         a = (ctypes.c_double * max_iter)()
         b = (ctypes.c_double * max_iter)()
         th = (ctypes.c_double * max_iter)()

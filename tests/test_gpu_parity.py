@@ -399,3 +399,54 @@ def test_lanczos_c4_bench_config_properties(dev, orc):
         ref = orc.heff_apply(L, W1, W2, R, p0, rows=(a, a + 1))[0]
         assert rel(hv1[a].cpu().numpy(), ref) <= MATVEC_TOL
     assert abs(float(torch.vdot(psi0.reshape(-1), hv1.reshape(-1))) - r.alpha[0]) <= 1e-10 * abs(r.alpha[0])
+
+
+def test_lanczos_nccl_single_rank_forced_allgather(dev, orc):
+    """HEFF_OPT_FORCE_ALLGATHER runs the P > 1 exchange (ncclAllGather into the blocked buffer +
+    the re-layout kernel) on a 1-rank communicator: same energy and Ritz vector as the oracle,
+    bitwise the same as the copy shortcut (both are exact copies at P = 1)."""
+    from paper_2007_14822_b200 import Heff, nccl_unique_id
+    from paper_2007_14822_b200.heff import OPT_COMM_STATE, OPT_FORCE_ALLGATHER
+    x = C.make("c2")
+    L, W1, W2, R, psi = x.numpy()
+    o = orc.lanczos_heff(L, W1, W2, R, psi, max_iter=12)
+    xd = x.to(dev)
+    with Heff(xd.L, xd.W1, xd.W2, xd.R, dist=dict(nranks=1, rank=0, b_lo=0, b_hi=R.shape[0],
+                                                   uid=nccl_unique_id())) as h:
+        assert h.get_option(OPT_COMM_STATE) == 1
+        v0 = xd.psi.clone()
+        r0 = h.lanczos_ground(v0, max_iter=12)
+        h.set_option(OPT_FORCE_ALLGATHER, 1)
+        assert h.get_option(OPT_FORCE_ALLGATHER) == 1
+        v1 = xd.psi.clone()
+        r1 = h.lanczos_ground(v1, max_iter=12)
+    assert abs(r1.energy - o.energy) <= ENERGY_TOL * max(1.0, abs(o.energy))
+    assert r1.energy == r0.energy and torch.equal(v0, v1)
+    assert abs(abs(float(np.dot(v1.cpu().numpy().reshape(-1), o.x.reshape(-1)))) - 1.0) <= 1e-10
+
+
+def test_force_allgather_needs_a_communicator(dev):
+    from paper_2007_14822_b200 import Heff
+    from paper_2007_14822_b200.heff import OPT_COMM_STATE, OPT_FORCE_ALLGATHER, HeffError
+    x = C.make("c1", device=dev)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        assert h.get_option(OPT_COMM_STATE) == 0
+        with pytest.raises(HeffError):
+            h.set_option(OPT_FORCE_ALLGATHER, 1)
+
+
+def test_binding_rejects_wrong_vector_sizes(dev):
+    """The binding checks psi's length against the plan (full vector, or the shard of a
+    communicating plan) before any pointer crosses the C ABI."""
+    from paper_2007_14822_b200 import Heff, nccl_unique_id
+    x = C.make("c2", device=dev)
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        with pytest.raises(ValueError):
+            h.lanczos_ground(x.psi[:, :, :, :128].contiguous(), max_iter=2)
+        with pytest.raises(ValueError):
+            h.apply(x.psi[:128].contiguous())
+    Rg = x.R[:128].contiguous()
+    with Heff(x.L, x.W1, x.W2, Rg, dist=dict(nranks=2, rank=0, b_lo=0, b_hi=128)) as h:   # virtual shard
+        with pytest.raises(ValueError):
+            h.apply_blocked(x.psi[:, :, :, :128].contiguous())
+        h.apply_blocked(x.psi.reshape(-1).clone())

@@ -68,11 +68,24 @@ def main():
         row = dict(config=a.config, P=P, nb=nb)
         for g in sorted({0, P - 1}):
             Rg = x.R[g * nb:(g + 1) * nb].contiguous()
+            torch.cuda.synchronize()
+            free0, _ = torch.cuda.mem_get_info()
             with Heff(x.L, x.W1, x.W2, Rg, dist=dict(nranks=P, rank=g, b_lo=g * nb, b_hi=(g + 1) * nb)) as h:
+                torch.cuda.synchronize()
+                row["plan_workspace_gb_measured"] = (free0 - torch.cuda.mem_get_info()[0]) / 2**30
                 o = torch.empty(h.out_shape, dtype=torch.float64, device=dev)
                 t = timed(lambda: h.apply_blocked(blocked, o), a.reps)
             row[f"rank{g}_ms"] = t
             del Rg
+        # per-rank device memory of a communicating rank (analytic, bytes): full L, W1/W2, its R
+        # rows, V1 + V3 (order-B intermediates), the gathered full psi + the blocked all-gather
+        # buffer, a 20-vector Krylov basis of shards and the work vector
+        shard = rows * nb
+        mem = {"L": d["mL"] * d["kL"] * d["mL"], "R_shard": nb * d["kR"] * mR,
+               "V1": rows * nb * d["kR"], "V3": d["kL"] * rows * nb, "psi_full": rows * mR,
+               "allgather_buffer": rows * mR if P > 1 else 0, "krylov_basis_20": 20 * shard, "work": shard}
+        row["per_rank_memory_gb"] = {k: v * 8 / 2**30 for k, v in mem.items()}
+        row["per_rank_memory_gb"]["total"] = sum(mem.values()) * 8 / 2**30
         t_rank = max(row[f"rank{g}_ms"] for g in sorted({0, P - 1}))
         if P == 1:
             t1 = t_rank
