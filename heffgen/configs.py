@@ -179,6 +179,11 @@ CONFIGS = {
     "c4": dict(model="cylinder", Lx=6, window=17, m=4096, seed=1004),
     # C5: Hubbard U=4 t=1 chain
     "c5": dict(model="hubbard", m=8192, seed=1005),
+    # beyond BASELINE.json: Hubbard U=4 t=1 on a width-6 cylinder (d = 4, k = 26; reading R26),
+    # 4 x 6 sites snaked into 24, window (11,12) -- the k d1 d2 = 416 MPO of the quasi-2D
+    # Hubbard studies; a parity / throughput case of the MPO kernel's
+    # narrow column tiles
+    "hcyl6": dict(model="hubbard_cylinder", Lx=4, window=11, m=256, seed=1006),
 }
 
 
@@ -196,6 +201,10 @@ def make(name: str, device="cpu", m: int | None = None) -> HeffInputs:
         N = c["Lx"] * mpo.CYL_WIDTH
         Ws = [mpo.cylinder_W(j) for j in range(N)]
         return model_inputs(Ws, c["window"], mm, c["seed"], device, dict(model="cylinder", config=name))
+    if c["model"] == "hubbard_cylinder":
+        N = c["Lx"] * mpo.CYL_WIDTH
+        Ws = [mpo.hubbard_cylinder_W(j) for j in range(N)]
+        return model_inputs(Ws, c["window"], mm, c["seed"], device, dict(model="hubbard_cylinder", config=name))
     if c["model"] == "hubbard":
         ns = n_side_for(mm, 4)
         return model_inputs([mpo.hubbard_W()] * (2 * ns + 2), ns, mm, c["seed"], device,

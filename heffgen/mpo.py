@@ -151,6 +151,36 @@ def hubbard_W(t: float = 1.0, U: float = 4.0) -> np.ndarray:
     return W
 
 
+def hubbard_cylinder_W(j: int, width: int = CYL_WIDTH, t: float = 1.0, U: float = 4.0) -> np.ndarray:
+    """Per-site W at snake site j of the Hubbard model on a width-`width` cylinder (periodic in
+    y, open in x, snake i = x*width + y; hopping -t on the J1 bonds of cylinder_bond, on-site
+    U n_up n_dn).  Jordan-Wigner as in hubbard_W: c+_i c_j (i < j) = (C^T F)_i F..F (C)_j and
+    its h.c. (F C)_i F..F (C^T)_j, so channels passing a site carry the string F.
+
+    Channels: done = 0, (op, t) = 1 + op*width + (t-1) for the four openers
+    op = (C_up^T F, F C_up, C_dn^T F, F C_dn) and t = 1..width sites since the opener,
+    start = 4*width + 1: k = 4*width + 2 (26 at width 6).  d = 4.  The quasi-2D Hubbard
+    workload of the paper's applications; reading R26."""
+    k = 4 * width + 2
+    start, done = k - 1, 0
+    opens = (CUP.T @ FJW, FJW @ CUP, CDN.T @ FJW, FJW @ CDN)
+    closes = (CUP, CUP.T, CDN, CDN.T)
+    W = np.zeros((k, 4, 4, k))
+    W[start, :, :, start] = I4
+    W[done, :, :, done] = I4
+    W[start, :, :, done] = U * NUPDN
+    for op in range(4):
+        W[start, :, :, 1 + op * width] = opens[op]
+        for tt in range(1, width + 1):
+            ch = 1 + op * width + (tt - 1)
+            if tt < width:
+                W[ch, :, :, ch + 1] = FJW
+            J = cylinder_bond(j - tt, j, width) if j - tt >= 0 else 0.0
+            if J != 0.0:
+                W[ch, :, :, done] = -t * J * closes[op]
+    return W
+
+
 def boundary_vectors(k: int) -> tuple[np.ndarray, np.ndarray]:
     """(left, right) MPO boundary vectors: left selects start = k-1, right selects done = 0."""
     l = np.zeros(k); l[k - 1] = 1.0

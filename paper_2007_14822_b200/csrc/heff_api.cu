@@ -359,22 +359,80 @@ int init_device_once() {
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNNs::kSmemBytes));
   CK(cudaFuncSetAttribute(gemm_dmma_tma_sharded_kernel<kBMs, kBNs, kWMs, kWNs, kStagesS, true>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNTs::kSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_orderA_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  CK(cudaFuncSetAttribute(mpo_orderA_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
   CK(cudaFuncSetAttribute(heff_small_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallMvMaxSmem));
   CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-  CK(cudaFuncSetAttribute(mpo_orderB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   g_dev_inited.fetch_or(bit, std::memory_order_release);
   return HEFF_OK;
 }
 
 // ----------------------------------------------------------------------------- plan
 struct Csr {
-  int nrows = 0, nnz = 0;
+  int nrows = 0, nnz = -1;  // nnz: -1 until read back from d_nnz (heff_get_option)
   int* d_rowptr = nullptr;
   int* d_col = nullptr;
   double* d_val = nullptr;
+  int* d_nnz = nullptr;
+  bool owned = true;        // false: arena buffers (environment updates)
 };
+
+// CSR of the two-site (or, kCsrSingle, one-site) MPO built on the device from the device
+// tensors W1/W2 by mpo_csr_build_kernel -- no host copy, no stream synchronisation.
+static void csr_shape(int mode, int64_t kL, int64_t kR, int64_t d1, int64_t d2, int64_t* nrows, int64_t* nslots) {
+  const int64_t nin = kL * d1 * d2, nout = d1 * d2 * kR;
+  switch (mode) {
+    case kCsrOrderA: *nrows = nout; *nslots = nin; break;
+    case kCsrOrderB: *nrows = nin; *nslots = nout; break;
+    case kCsrComplexA: *nrows = 2 * nout; *nslots = 2 * nin; break;
+    case kCsrSingle: *nrows = d1 * kR; *nslots = kL * d1; break;
+    default: *nrows = kL * d1; *nslots = d1 * kR; break;
+  }
+}
+
+static int build_csr_dev(Csr& c, int mode, const double* W1, const double* W2, int64_t kL, int64_t kM, int64_t kR,
+                         int64_t d1, int64_t d2, cudaStream_t s) {
+  int64_t nrows = 0, nslots = 0;
+  csr_shape(mode, kL, kR, d1, d2, &nrows, &nslots);
+  if (nrows * nslots > INT32_MAX) return set_err(HEFF_EUNSUPPORTED, "MPO CSR: %lld entries", (long long)(nrows * nslots));
+  if (c.owned) {
+    CK(cudaMalloc(&c.d_rowptr, sizeof(int) * (nrows + 2)));  // + the nnz slot
+    CK(cudaMalloc(&c.d_col, sizeof(int) * std::max<int64_t>(1, nrows * nslots)));
+    CK(cudaMalloc(&c.d_val, sizeof(double) * std::max<int64_t>(1, nrows * nslots)));
+    c.d_nnz = c.d_rowptr + nrows + 1;
+  }
+  c.nrows = (int)nrows;
+  c.nnz = -1;
+  mpo_csr_build_kernel<<<1, kCsrThreads, 0, s>>>(W1, W2, (int)kL, (int)kM, (int)kR, (int)d1, (int)d2, mode, c.d_rowptr,
+                                                 c.d_col, c.d_val, c.d_nnz);
+  CK(cudaGetLastError());
+  return HEFF_OK;
+}
+
+static int csr_nnz(Csr& c) {  // synchronous read-back (heff_get_option only)
+  if (c.nnz < 0 && c.d_nnz) {
+    int v = 0;
+    if (cudaMemcpy(&v, c.d_nnz, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    c.nnz = v;
+  }
+  return c.nnz;
+}
+
+// W must be a device (or managed) pointer: checked without touching the stream.
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
 
 struct heff_plan_s {
   heff_dims dims{};
@@ -396,7 +454,8 @@ struct heff_plan_s {
   double* pen_scratch = nullptr;            // partials [nphi][pen_G] + coefficients [nphi]
   int pen_G = 0;
   const double *L = nullptr, *R = nullptr;  // borrowed
-  std::vector<double> W1h, W2h;             // host copies
+  int tcA = 128, tcB = 128;                 // MPO kernels' column-tile widths (mpo_tile_cols)
+  double* Rperm = nullptr;                  // order B: R's shard with rows reordered (w2, b'), plan-owned
   bool sharded = false;                     // order B on a b'-shard
   int nranks = 1, rank = 0;
   int64_t b_lo = 0, b_hi = 0, nb = 0;
@@ -445,6 +504,8 @@ struct heff_plan_s {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t e2e_ev[17] = {};                // 2 kE2eChunks + 1
   cudaEvent_t done_ev = nullptr;              // recorded after each enqueued plan operation
+  cudaEvent_t setup_ev = nullptr;             // end of the device-side set-up heff_create enqueued
+  std::vector<cudaStream_t> setup_streams;    // streams already ordered after setup_ev
   // Lanczos
   double* basis = nullptr;                  // [cap][ldv]
   int basis_cap = 0;
@@ -465,71 +526,6 @@ struct heff_plan_s {
   size_t prof_used = 0;
 };
 
-static int build_csr(Csr& c, const std::vector<int>& rowptr, const std::vector<int>& col, const std::vector<double>& val) {
-  c.nrows = (int)rowptr.size() - 1;
-  c.nnz = (int)val.size();
-  CK(cudaMalloc(&c.d_rowptr, sizeof(int) * rowptr.size()));
-  CK(cudaMalloc(&c.d_col, sizeof(int) * std::max<size_t>(1, col.size())));
-  CK(cudaMalloc(&c.d_val, sizeof(double) * std::max<size_t>(1, val.size())));
-  CK(cudaMemcpy(c.d_rowptr, rowptr.data(), sizeof(int) * rowptr.size(), cudaMemcpyHostToDevice));
-  if (!col.empty()) {
-    CK(cudaMemcpy(c.d_col, col.data(), sizeof(int) * col.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c.d_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
-  }
-  return HEFF_OK;
-}
-
-// Two-site MPO Wc[w,s1',s1,s2',s2,w2] = sum_w1 W1[w,s1',s1,w1] W2[w1,s2',s2,w2], as CSR
-// in the (out-row, in-col) order each kernel wants.  Exact zeros are dropped.
-static int build_mpo_csr(heff_plan_s* p) {
-  const int64_t kL = p->dims.kL, kM = p->dims.kM, kR = p->dims.kR, d1 = p->dims.d1, d2 = p->dims.d2;
-  auto W1 = [&](int64_t w, int64_t s1p, int64_t s1, int64_t w1) { return p->W1h[((w * d1 + s1p) * d1 + s1) * kM + w1]; };
-  auto W2 = [&](int64_t w1, int64_t s2p, int64_t s2, int64_t w2) { return p->W2h[((w1 * d2 + s2p) * d2 + s2) * kR + w2]; };
-  auto Wc = [&](int64_t w, int64_t s1p, int64_t s1, int64_t s2p, int64_t s2, int64_t w2) {
-    double acc = 0.0;
-    for (int64_t w1 = 0; w1 < kM; ++w1) acc += W1(w, s1p, s1, w1) * W2(w1, s2p, s2, w2);
-    return acc;
-  };
-  std::vector<int> rp, cl;
-  std::vector<double> vl;
-  // order A: rows (s1',s2',w2), cols (w,s1,s2)
-  rp.push_back(0);
-  for (int64_t s1p = 0; s1p < d1; ++s1p)
-    for (int64_t s2p = 0; s2p < d2; ++s2p)
-      for (int64_t w2 = 0; w2 < kR; ++w2) {
-        for (int64_t w = 0; w < kL; ++w)
-          for (int64_t s1 = 0; s1 < d1; ++s1)
-            for (int64_t s2 = 0; s2 < d2; ++s2) {
-              const double v = Wc(w, s1p, s1, s2p, s2, w2);
-              if (v != 0.0) {
-                cl.push_back((int)((w * d1 + s1) * d2 + s2));
-                vl.push_back(v);
-              }
-            }
-        rp.push_back((int)vl.size());
-      }
-  CKR(build_csr(p->csrA, rp, cl, vl));
-  rp.clear(); cl.clear(); vl.clear();
-  // order B: rows (w,s1',s2'), cols (s1,s2,w2)
-  rp.push_back(0);
-  for (int64_t w = 0; w < kL; ++w)
-    for (int64_t s1p = 0; s1p < d1; ++s1p)
-      for (int64_t s2p = 0; s2p < d2; ++s2p) {
-        for (int64_t s1 = 0; s1 < d1; ++s1)
-          for (int64_t s2 = 0; s2 < d2; ++s2)
-            for (int64_t w2 = 0; w2 < kR; ++w2) {
-              const double v = Wc(w, s1p, s1, s2p, s2, w2);
-              if (v != 0.0) {
-                cl.push_back((int)((s1 * d2 + s2) * kMpoCols * kR + w2));  // shared-memory offset, see mpo.cuh
-                vl.push_back(v);
-              }
-            }
-        rp.push_back((int)vl.size());
-      }
-  CKR(build_csr(p->csrB, rp, cl, vl));
-  return HEFF_OK;
-}
-
 static int64_t vec_len(const heff_plan_s* p) {  // local vector length
   const heff_dims& d = p->dims;
   return d.mL * d.d1 * d.d2 * (p->sharded ? p->nb : d.mR);
@@ -539,7 +535,9 @@ extern "C" size_t heff_workspace_bytes(const heff_dims* d, const heff_dist* dist
   if (!d) return 0;
   if (dist) {
     const int64_t nb = dist->b_hi - dist->b_lo;
-    return sizeof(double) * (size_t)(d->mL * d->d1 * d->d2 * nb * d->kR + d->kL * d->mL * d->d1 * d->d2 * nb);
+    // V1 + V3 + the (w2, b')-ordered copy of R's shard
+    return sizeof(double) * (size_t)(d->mL * d->d1 * d->d2 * nb * d->kR + d->kL * d->mL * d->d1 * d->d2 * nb +
+                                     nb * d->kR * d->mR);
   }
   return sizeof(double) * (size_t)(d->mL * (d->kL + d->kR) * d->d1 * d->d2 * d->mR);
 }
@@ -648,14 +646,26 @@ static size_t ws_cached_bytes(int dev) {
 }
 
 static void free_csr(Csr& c) {
-  cudaFree(c.d_rowptr);
-  cudaFree(c.d_col);
-  cudaFree(c.d_val);
+  if (c.owned) {
+    cudaFree(c.d_rowptr);
+    cudaFree(c.d_col);
+    cudaFree(c.d_val);
+  }
   c = Csr{};
 }
 
 // Record the plan's completion event on `s` after an enqueued operation (heff_destroy
 // waits for it before handing the plan's blocks back to the workspace cache).
+// Order stream s after the plan's device-side set-up (once per stream).
+static int after_setup(heff_plan_s* p, cudaStream_t s) {
+  if (!p->setup_ev) return HEFF_OK;
+  for (cudaStream_t x : p->setup_streams)
+    if (x == s) return HEFF_OK;
+  CK(cudaStreamWaitEvent(s, p->setup_ev, 0));
+  p->setup_streams.push_back(s);
+  return HEFF_OK;
+}
+
 static int mark_done(heff_plan_s* p, cudaStream_t s) {
   if (!p->done_ev) CK(cudaEventCreateWithFlags(&p->done_ev, cudaEventDisableTiming));
   CK(cudaEventRecord(p->done_ev, s));
@@ -677,7 +687,7 @@ extern "C" int heff_destroy(heff_plan p) {
   if (p->copy_stream) cudaStreamSynchronize(p->copy_stream);
   for (void* b : {(void*)p->T1, (void*)p->T3, (void*)p->V1, (void*)p->V3, (void*)p->stage_in, (void*)p->stage_out,
                   (void*)p->basis, (void*)p->work, (void*)p->full, (void*)p->gather, (void*)p->partial,
-                  (void*)p->scal, (void*)p->Lp, (void*)p->Rp, (void*)p->zin, (void*)p->zout, (void*)p->dense_in,
+                  (void*)p->scal, (void*)p->Lp, (void*)p->Rp, (void*)p->Rperm, (void*)p->zin, (void*)p->zout, (void*)p->dense_in,
                   (void*)p->dense_out})
     ws_release(b);
   cudaFree(p->mpo_live);
@@ -693,6 +703,10 @@ extern "C" int heff_destroy(heff_plan p) {
     if (e) cudaEventDestroy(e);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->done_ev) cudaEventDestroy(p->done_ev);
+  if (p->setup_ev) {
+    cudaEventSynchronize(p->setup_ev);
+    cudaEventDestroy(p->setup_ev);
+  }
   for (auto& e : p->step_ev) cudaEventDestroy(e);
   // an aborted communicator (comm == nullptr, comm_dead) is gone with its window handles:
   // only the local allocation is freed (deregistration is collective and would wait for
@@ -718,6 +732,8 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
   for (const void* ptr : {(const void*)L, (const void*)W1, (const void*)W2, (const void*)R})
     if (reinterpret_cast<uintptr_t>(ptr) & 7) return set_err(HEFF_EINVAL, "heff_create: pointers must be 8-byte aligned");
   CKR(init_device_once());
+  if (!is_device_ptr(W1) || !is_device_ptr(W2))
+    return set_err(HEFF_EINVAL, "heff_create: W1/W2 are not device pointers");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
 
   heff_plan_s* p = new heff_plan_s();
@@ -752,16 +768,15 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
       if (const char* e = getenv("HEFF_FORCE_ALLGATHER")) p->force_allgather = atoi(e) ? 1 : 0;
     }
   }
-  // W copies
-  p->W1h.resize(d.kL * d.d1 * d.d1 * d.kM);
-  p->W2h.resize(d.kM * d.d2 * d.d2 * d.kR);
-  if (cudaMemcpyAsync(p->W1h.data(), W1, sizeof(double) * p->W1h.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaMemcpyAsync(p->W2h.data(), W2, sizeof(double) * p->W2h.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess)
-    return fail(set_err(HEFF_EINVAL, "heff_create: W1/W2 are not readable device pointers (%s)",
-                        cudaGetErrorString(cudaGetLastError())));
-  int r = build_mpo_csr(p);
+  // the two-site MPO as CSR, built on the device on `s` (S0; no host copy or sync)
+  p->tcA = mpo_tile_cols(d.kL * d.d1 * d.d2);
+  p->tcB = mpo_tile_cols(d.d1 * d.d2 * d.kR);
+  int r = build_csr_dev(p->csrA, kCsrOrderA, W1, W2, d.kL, d.kM, d.kR, d.d1, d.d2, s);
   if (r) return fail(r);
+  if (p->sharded) {
+    r = build_csr_dev(p->csrB, kCsrOrderB, W1, W2, d.kL, d.kM, d.kR, d.d1, d.d2, s);
+    if (r) return fail(r);
+  }
 
   if (!p->sharded) {
     // order A, chunked over a' so that T1 + T3 fit the workspace budget
@@ -801,14 +816,18 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
   } else {
     const int64_t nb = p->nb;
     if (ws_malloc(&p->V1, sizeof(double) * d.mL * d.d1 * d.d2 * nb * d.kR) != cudaSuccess ||
-        ws_malloc(&p->V3, sizeof(double) * d.kL * d.mL * d.d1 * d.d2 * nb) != cudaSuccess)
+        ws_malloc(&p->V3, sizeof(double) * d.kL * d.mL * d.d1 * d.d2 * nb) != cudaSuccess ||
+        ws_malloc(&p->Rperm, sizeof(double) * nb * d.kR * d.mR) != cudaSuccess)
       return fail(set_err(HEFF_ENOMEM, "heff_create: cannot allocate V1/V3 workspace"));
-    // GEMM_A: V1[(a s1 s2), (b' w2)] = psi[(a s1 s2), b] . R_g[(b' w2), b]^T   (NT)
+    // R's shard with rows (w2, b') (a plan-owned copy; R stays borrowed and unmodified)
+    permute_r_shard_kernel<<<(unsigned)(nb * d.kR), 256, 0, s>>>(R, p->Rperm, nb, (int)d.kR, d.mR);
+    if (cudaGetLastError() != cudaSuccess) return fail(set_err(HEFF_ECUDA, "heff_create: R permutation launch failed"));
+    // GEMM_A: V1[(a s1 s2), (w2 b')] = psi[(a s1 s2), b] . Rperm[(w2 b'), b]^T   (NT)
     p->gA.M = d.mL * d.d1 * d.d2;
     p->gA.N = nb * d.kR;
     p->gA.K = d.mR;
     p->gA.lda = d.mR;
-    p->gA.B = R;
+    p->gA.B = p->Rperm;
     p->gA.ldb = d.mR;
     p->gA.b_kmajor = true;
     p->gA.C = p->V1;
@@ -824,6 +843,11 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
     p->gD.b_kmajor = false;
     p->gD.ldc = d.d1 * d.d2 * nb;
   }
+  // the CSR / R permutation kernels ran on s: later calls on other streams wait for them
+  if (cudaEventCreateWithFlags(&p->setup_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(p->setup_ev, s) != cudaSuccess)
+    return fail(set_err(HEFF_ECUDA, "heff_create: event record failed"));
+  p->setup_streams.push_back(s);
   *out = p;
   return HEFF_OK;
 }
@@ -834,51 +858,6 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
 // imaginary planes of L and R turn the subtraction into an accumulating GEMM) and the two
 // MPO steps run as one real MPO kernel on stacked [re; im] rows with the 2x2 blocks
 // [[Re, -Im], [Im, Re]] of the complex two-site MPO.
-static int build_mpo_csr_complex(heff_plan_s* p, const std::vector<double>& W1z, const std::vector<double>& W2z) {
-  const int64_t kL = p->dims.kL, kM = p->dims.kM, kR = p->dims.kR, d1 = p->dims.d1, d2 = p->dims.d2;
-  auto W1 = [&](int64_t w, int64_t s1p, int64_t s1, int64_t w1, int c) {
-    return W1z[2 * (((w * d1 + s1p) * d1 + s1) * kM + w1) + c];
-  };
-  auto W2 = [&](int64_t w1, int64_t s2p, int64_t s2, int64_t w2, int c) {
-    return W2z[2 * (((w1 * d2 + s2p) * d2 + s2) * kR + w2) + c];
-  };
-  const int64_t nin = kL * d1 * d2, nout = d1 * d2 * kR;
-  std::vector<std::vector<std::pair<int, double>>> rows(2 * nout);
-  for (int64_t s1p = 0; s1p < d1; ++s1p)
-    for (int64_t s2p = 0; s2p < d2; ++s2p)
-      for (int64_t w2 = 0; w2 < kR; ++w2)
-        for (int64_t w = 0; w < kL; ++w)
-          for (int64_t s1 = 0; s1 < d1; ++s1)
-            for (int64_t s2 = 0; s2 < d2; ++s2) {
-              double re = 0.0, im = 0.0;
-              for (int64_t w1 = 0; w1 < kM; ++w1) {
-                const double ar = W1(w, s1p, s1, w1, 0), ai = W1(w, s1p, s1, w1, 1);
-                const double br = W2(w1, s2p, s2, w2, 0), bi = W2(w1, s2p, s2, w2, 1);
-                re += ar * br - ai * bi;
-                im += ar * bi + ai * br;
-              }
-              const int o = (int)((s1p * d2 + s2p) * kR + w2), c = (int)((w * d1 + s1) * d2 + s2);
-              if (re != 0.0) {
-                rows[o].push_back({c, re});                          // Re out <- Re in
-                rows[nout + o].push_back({(int)nin + c, re});        // Im out <- Im in
-              }
-              if (im != 0.0) {
-                rows[o].push_back({(int)nin + c, -im});              // Re out <- -Im * Im in
-                rows[nout + o].push_back({c, im});                   // Im out <- Im * Re in
-              }
-            }
-  std::vector<int> rp{0}, cl;
-  std::vector<double> vl;
-  for (auto& r : rows) {
-    for (auto& e : r) {
-      cl.push_back(e.first);
-      vl.push_back(e.second);
-    }
-    rp.push_back((int)vl.size());
-  }
-  return build_csr(p->csrA, rp, cl, vl);
-}
-
 extern "C" int heff_create_z(heff_plan* out, const heff_dims* dims, const double* L, const double* W1,
                              const double* W2, const double* R, const heff_dist* dist, heff_stream stream) {
   if (!out || !dims || !L || !W1 || !W2 || !R) return set_err(HEFF_EINVAL, "heff_create_z: null argument");
@@ -901,12 +880,9 @@ extern "C" int heff_create_z(heff_plan* out, const heff_dims* dims, const double
     heff_destroy(p);
     return code;
   };
-  std::vector<double> W1z(2 * d.kL * d.d1 * d.d1 * d.kM), W2z(2 * d.kM * d.d2 * d.d2 * d.kR);
-  if (cudaMemcpyAsync(W1z.data(), W1, sizeof(double) * W1z.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaMemcpyAsync(W2z.data(), W2, sizeof(double) * W2z.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess)
-    return fail(set_err(HEFF_EINVAL, "heff_create_z: W1/W2 are not readable device pointers"));
-  int r = build_mpo_csr_complex(p, W1z, W2z);
+  if (!is_device_ptr(W1) || !is_device_ptr(W2)) return fail(set_err(HEFF_EINVAL, "heff_create_z: W1/W2 are not device pointers"));
+  p->tcA = mpo_tile_cols(2 * d.kL * d.d1 * d.d2);
+  int r = build_csr_dev(p->csrA, kCsrComplexA, W1, W2, d.kL, d.kM, d.kR, d.d1, d.d2, s);
   if (r) return fail(r);
   const int64_t nL = d.mL * d.kL * d.mL, nR = d.mR * d.kR * d.mR, n = d.mL * d.d1 * d.d2 * d.mR;
   if (ws_malloc(&p->Lp, sizeof(double) * 3 * nL) != cudaSuccess ||
@@ -942,6 +918,10 @@ extern "C" int heff_create_z(heff_plan* out, const heff_dims* dims, const double
   }
   p->L = p->Lp;
   p->R = p->Rp;
+  if (cudaEventCreateWithFlags(&p->setup_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(p->setup_ev, s) != cudaSuccess)
+    return fail(set_err(HEFF_ECUDA, "heff_create_z: event record failed"));
+  p->setup_streams.push_back(s);
   *out = p;
   return HEFF_OK;
 }
@@ -994,7 +974,7 @@ extern "C" int heff_get_option(heff_plan p, int option, int64_t* value) {
   switch (option) {
     case HEFF_OPT_GEMM_PATH: *value = p->gemm_path; return HEFF_OK;
     case HEFF_OPT_LAST_KERNEL_COUNT: *value = p->last_launches; return HEFF_OK;
-    case HEFF_OPT_MPO_NNZ: *value = p->sharded ? p->csrB.nnz : p->csrA.nnz; return HEFF_OK;
+    case HEFF_OPT_MPO_NNZ: *value = csr_nnz(p->sharded ? p->csrB : p->csrA); return HEFF_OK;
     case HEFF_OPT_PROFILE: *value = p->profile; return HEFF_OK;
     case HEFF_OPT_TOTAL_LAUNCHES: *value = p->total_launches; return HEFF_OK;
     case HEFF_OPT_SPARSE_KBLOCKS: *value = p->sp_kblocks; return HEFF_OK;
@@ -1039,17 +1019,47 @@ extern "C" int heff_last_timings(heff_plan p, float* g1, float* mpo, float* g4, 
   return HEFF_OK;
 }
 
-// Order-A MPO step on real data (one (a', 128-column) tile per block, two resident blocks
-// per SM at C4: a persistent double-buffered variant with one block per SM measured 1.8x
-// slower at C4 and was dropped).
-static int launch_mpo_A(const double* T1, double* T3, int64_t mR, int64_t rows, int nin, int nout, const Csr& csr,
-                        const unsigned char* live, cudaStream_t s) {
-  if (rows <= 0 || mR <= 0) return HEFF_OK;
-  dim3 grid((unsigned)((mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
-  CK(launch_pdl(mpo_orderA_kernel<1>, grid, dim3(kMpoThreads), sizeof(double) * nin * kMpoCols, s, T1, T3, mR, nin,
-                nout, (const int*)csr.d_rowptr, (const int*)csr.d_col, (const double*)csr.d_val, live, 1, (int64_t)0,
-                (int64_t)0));
+// One MPO application (mpo_apply_kernel; column tile `tc` from mpo_tile_cols): `nblk`
+// blocks along y (a' for order A / environments, a for order B).
+template <int PL>
+static int launch_mpo(const MpoIO& io, int tc, int64_t nblk, const Csr& csr, const unsigned char* live, cudaStream_t s) {
+  if (nblk <= 0 || io.ncol <= 0) return HEFF_OK;
+  if (nblk > 65535) return set_err(HEFF_EUNSUPPORTED, "MPO kernel: %lld blocks along y", (long long)nblk);
+  dim3 grid((unsigned)((io.ncol + tc - 1) / tc), (unsigned)nblk);
+  const size_t smem = sizeof(double) * (size_t)io.nin * tc;
+  const int* rp = csr.d_rowptr;
+  const int* cl = csr.d_col;
+  const double* vl = csr.d_val;
+  switch (tc) {
+    case 128: CK(launch_pdl(mpo_apply_kernel<PL, 128>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
+    case 64: CK(launch_pdl(mpo_apply_kernel<PL, 64>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
+    case 32: CK(launch_pdl(mpo_apply_kernel<PL, 32>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
+    case 16: CK(launch_pdl(mpo_apply_kernel<PL, 16>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
+    default: return set_err(HEFF_EUNSUPPORTED, "MPO kernel: %d input rows exceed the shared-memory tile", io.nin);
+  }
   return HEFF_OK;
+}
+
+// Order A (and the environment updates): `rows` blocks of nin rows (w,s1,s2) x ncol columns
+// -> nout rows (s1',s2',w2), both with row pitch ncol.
+static MpoIO mpo_io_A(const double* in, double* out, int64_t ncol, int nin, int nout) {
+  MpoIO io{};
+  io.in = in;
+  io.out = out;
+  io.ncol = ncol;
+  io.nin = nin;
+  io.nout = nout;
+  io.in_blk = (int64_t)nin * ncol;
+  io.in_row = ncol;
+  io.out_blk = (int64_t)nout * ncol;
+  io.out_row = ncol;
+  io.out_grp = nout;
+  return io;
+}
+
+static int launch_mpo_A(const double* T1, double* T3, int64_t mR, int64_t rows, int nin, int nout, const Csr& csr,
+                        const unsigned char* live, int tc, cudaStream_t s) {
+  return launch_mpo<1>(mpo_io_A(T1, T3, mR, nin, nout), tc, rows, csr, live, s);
 }
 
 // --------------------------------------------------------------------------- the matvec
@@ -1092,7 +1102,7 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     p->g1.C = p->T1;
     CKR(launch_gemm(p->g1, p->gemm_path, s, nl, &p->splitws));
     CKR(prof_mark(p, 1, s));
-    CKR(launch_mpo_A(p->T1, p->T3, d.mR, rows, (int)nin, (int)nout, p->csrA, p->mpo_live, s));
+    CKR(launch_mpo_A(p->T1, p->T3, d.mR, rows, (int)nin, (int)nout, p->csrA, p->mpo_live, p->tcA, s));
     ++*nl;
     CKR(prof_mark(p, 2, s));
     p->g4.M = rows * d.d1 * d.d2;
@@ -1128,15 +1138,25 @@ static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStre
                         const ShardedA* sa = nullptr) {
   const heff_dims& d = p->dims;
   const int dd = (int)(d.d1 * d.d2);
-  const size_t mpo_smem = sizeof(double) * dd * d.kR * kMpoCols;
   CKR(prof_mark(p, 0, s));
   p->gA.A = psi;
   CKR(launch_gemm(p->gA, p->gemm_path, s, nl, &p->splitws, sa));
   CKR(prof_mark(p, 1, s));
-  dim3 grid((unsigned)((p->nb + kMpoCols - 1) / kMpoCols), (unsigned)d.mL);
-  mpo_orderB_kernel<<<grid, kMpoThreads, mpo_smem, s>>>(p->V1, p->V3, d.mL, p->nb, dd, (int)d.kR, (int)d.kL,
-                                                     p->csrB.d_rowptr, p->csrB.d_col, p->csrB.d_val);
-  CK(cudaGetLastError());
+  {  // V1[a][(s1 s2 w2)][b'] -> V3[w][a][(s1' s2')][b']
+    MpoIO io{};
+    io.in = p->V1;
+    io.out = p->V3;
+    io.ncol = p->nb;
+    io.nin = dd * (int)d.kR;
+    io.nout = (int)d.kL * dd;
+    io.in_blk = (int64_t)dd * d.kR * p->nb;
+    io.in_row = p->nb;
+    io.out_blk = (int64_t)dd * p->nb;
+    io.out_row = p->nb;
+    io.out_grp = dd;
+    io.out_grp_stride = d.mL * dd * p->nb;
+    CKR(launch_mpo<1>(io, p->tcB, d.mL, p->csrB, nullptr, s));
+  }
   ++*nl;
   CKR(prof_mark(p, 2, s));
   p->gD.C = out;
@@ -1154,7 +1174,6 @@ static int apply_orderA_z(heff_plan_s* p, const double* psi, double* out, cudaSt
   deinterleave_kernel<<<ew_grid(2 * n), 256, 0, s>>>(psi, p->zin, p->zin + n, n);
   ++*nl;
   const int64_t nin = 2 * d.kL * d.d1 * d.d2, nout = 2 * d.d1 * d.d2 * d.kR;
-  const size_t mpo_smem = sizeof(double) * nin * kMpoCols;
   for (int64_t a0 = 0; a0 < d.mL; a0 += p->chunk_rows) {
     const int64_t rows = std::min(p->chunk_rows, d.mL - a0);
     CKR(prof_mark(p, 0, s));
@@ -1174,11 +1193,15 @@ static int apply_orderA_z(heff_plan_s* p, const double* psi, double* out, cudaSt
       CKR(launch_gemm(g, p->gemm_path, s, nl, &p->splitws));
     }
     CKR(prof_mark(p, 1, s));
-    dim3 grid((unsigned)((d.mR + kMpoCols - 1) / kMpoCols), (unsigned)rows);
-    mpo_orderA_kernel<2><<<grid, kMpoThreads, mpo_smem, s>>>(p->T1, p->T3, d.mR, (int)nin, (int)nout, p->csrA.d_rowptr,
-                                                       p->csrA.d_col, p->csrA.d_val, nullptr, 2, p->t1_plane,
-                                                       p->t3_plane);
-    CK(cudaGetLastError());
+    {  // stacked [re; im] planes of T1 -> T3
+      MpoIO io = mpo_io_A(p->T1, p->T3, d.mR, (int)nin, (int)nout);
+      io.in_blk = nin / 2 * d.mR;
+      io.in_plane = p->t1_plane;
+      io.out_blk = nout / 2 * d.mR;
+      io.out_plane = p->t3_plane;
+      io.out_grp = (int)(nout / 2);
+      CKR(launch_mpo<2>(io, p->tcA, rows, p->csrA, nullptr, s));
+    }
     ++*nl;
     CKR(prof_mark(p, 2, s));
     const double *T3re = p->T3, *T3im = p->T3 + p->t3_plane;
@@ -1233,6 +1256,7 @@ static int apply_impl(heff_plan_s* p, const double* psi, double* out, cudaStream
   if (psi == out) return set_err(HEFF_EINVAL, "heff_apply: out must not alias psi");
   if ((reinterpret_cast<uintptr_t>(psi) | reinterpret_cast<uintptr_t>(out)) & 7)
     return set_err(HEFF_EINVAL, "heff_apply: psi/out must be 8-byte aligned");
+  CKR(after_setup(p, s));
   int nl = 0;
   int r = HEFF_OK;
   if (!p->terms.empty()) {
@@ -1310,6 +1334,7 @@ extern "C" int heff_apply_blocked(heff_plan p, const double* psi_blocked, double
   ShardedA sa;
   CKR(build_sharded_a(p, sh.data(), P, &sa));
   int nl = 0;
+  CKR(after_setup(p, reinterpret_cast<cudaStream_t>(stream)));
   CKR(apply_orderB(p, nullptr, out, reinterpret_cast<cudaStream_t>(stream), &nl, 0, &sa));
   p->last_launches = nl;
   p->total_launches += nl;
@@ -1356,7 +1381,7 @@ static int apply_host_pipelined(heff_plan_s* p, const double* psi_host, double* 
   }
   p->g1.N = ncol;
   const int64_t nin = d.kL * d.d1 * d.d2, nout = d.d1 * d.d2 * d.kR;
-  CKR(launch_mpo_A(p->T1, p->T3, d.mR, d.mL, (int)nin, (int)nout, p->csrA, p->mpo_live, s));
+  CKR(launch_mpo_A(p->T1, p->T3, d.mR, d.mL, (int)nin, (int)nout, p->csrA, p->mpo_live, p->tcA, s));
   ++nl;
   for (int k = 0; k < kE2eChunks; ++k) {
     const int64_t r0 = nrow4 * k / kE2eChunks, r1 = nrow4 * (k + 1) / kE2eChunks;
@@ -1388,6 +1413,7 @@ extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_
     CK(ws_malloc(&p->stage_in, sizeof(double) * n_in));
     CK(ws_malloc(&p->stage_out, sizeof(double) * n_out));
   }
+  CKR(after_setup(p, s));
   const bool pipelined = !p->is_complex && !p->sharded && p->terms.empty() && p->nphi == 0 && p->sp1 == nullptr &&
                          p->sp4 == nullptr && p->chunk_rows == d.mL && d.mL * d.d1 * d.d2 >= 8 * kE2eChunks &&
                          getenv("HEFF_NO_E2E_PIPELINE") == nullptr;
@@ -1758,6 +1784,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int cap = o->max_iter;
   p->step_ev_used = 0;
+  CKR(after_setup(p, s));
   LanczosLayout lay;
   CKR(lanczos_workspace(p, cap, s, &lay));
   const bool compact = lay.compact, cplx = lay.cplx, fgather = lay.fgather;
@@ -1996,29 +2023,28 @@ static int env_reserve(size_t doubles) {
   return HEFF_OK;
 }
 
-static int upload_csr(Csr& c, const std::vector<int>& rp, const std::vector<int>& cl, const std::vector<double>& vl,
-                      cudaStream_t s) {
+// The environment update's one-site MPO as CSR, built on the device into this thread's
+// arena (mode kCsrSingle: left update, kCsrSingleR: right update).
+static int env_csr(Csr& c, int mode, const double* W, int64_t kl, int64_t d, int64_t kr, cudaStream_t s) {
   EnvArena& a = t_env_arena();
-  const size_t need = std::max(rp.size(), std::max<size_t>(1, vl.size()));
+  int64_t nrows = 0, nslots = 0;
+  csr_shape(mode, kl, kr, d, d, &nrows, &nslots);
+  const size_t need = (size_t)std::max<int64_t>(nrows + 2, nrows * nslots);
   if (a.csr_cap < need) {
     cudaFree(a.rowptr); cudaFree(a.col); cudaFree(a.val);
+    a.rowptr = nullptr; a.col = nullptr; a.val = nullptr;
     a.csr_cap = 0;
     CK(cudaMalloc(&a.rowptr, sizeof(int) * need));
     CK(cudaMalloc(&a.col, sizeof(int) * need));
     CK(cudaMalloc(&a.val, sizeof(double) * need));
     a.csr_cap = need;
   }
-  CK(cudaMemcpyAsync(a.rowptr, rp.data(), sizeof(int) * rp.size(), cudaMemcpyHostToDevice, s));
-  if (!vl.empty()) {
-    CK(cudaMemcpyAsync(a.col, cl.data(), sizeof(int) * cl.size(), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(a.val, vl.data(), sizeof(double) * vl.size(), cudaMemcpyHostToDevice, s));
-  }
+  c.owned = false;
   c.d_rowptr = a.rowptr;
   c.d_col = a.col;
   c.d_val = a.val;
-  c.nrows = (int)rp.size() - 1;
-  c.nnz = (int)vl.size();
-  return HEFF_OK;
+  c.d_nnz = a.rowptr + nrows + 1;
+  return build_csr_dev(c, mode, W, nullptr, kl, 1, kr, d, d, s);
 }
 
 static int env_common_check(const heff_env_dims* d, const void* a, const void* b, const void* w, const void* o) {
@@ -2065,29 +2091,12 @@ static int env_left_impl(const heff_env_dims* dims, const double* L, const doubl
   CKR(env_common_check(dims, L, A, W, Lout));
   const heff_env_dims d = *dims;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  std::vector<double> Wh(d.kl * d.d * d.d * d.kr);
-  CK(cudaMemcpyAsync(Wh.data(), W, sizeof(double) * Wh.size(), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  // CSR: rows (s',w'), cols (w,s)
-  std::vector<int> rp{0}, cl;
-  std::vector<double> vl;
-  for (int64_t sp = 0; sp < d.d; ++sp)
-    for (int64_t wp = 0; wp < d.kr; ++wp) {
-      for (int64_t w = 0; w < d.kl; ++w)
-        for (int64_t ss = 0; ss < d.d; ++ss) {
-          const double v = Wh[((w * d.d + sp) * d.d + ss) * d.kr + wp];
-          if (v != 0.0) {
-            cl.push_back((int)(w * d.d + ss));
-            vl.push_back(v);
-          }
-        }
-      rp.push_back((int)vl.size());
-    }
-  Csr csr;
+  if (!is_device_ptr(W)) return set_err(HEFF_EINVAL, "heff_env_update_left: W is not a device pointer");
+  Csr csr;  // rows (s',w'), cols (w,s), built on the device
   auto pad = [](int64_t x) { return (x + 31) / 32 * 32; };  // keep every sub-buffer 256-byte aligned
   const int64_t nX = pad(d.mi * d.kl * d.d * d.mo), nY = pad(d.mi * d.d * d.kr * d.mo), nA = pad(d.mi * d.d * d.mo);
   CKR(env_reserve((size_t)(nX + nY + nA)));
-  CKR(upload_csr(csr, rp, cl, vl, s));
+  CKR(env_csr(csr, kCsrSingle, W, d.kl, d.d, d.kr, s));
   double* X = t_env_arena().buf;
   double* Y = X + nX;
   double* At = Y + nY;
@@ -2118,7 +2127,7 @@ static int env_left_impl(const heff_env_dims* dims, const double* L, const doubl
   r = launch_gemm(g1, 0, s, &nl, ws_for(t_env_splitws, s));
   if (!r) {
     const int nin = (int)(d.kl * d.d), nout = (int)(d.d * d.kr);
-    r = launch_mpo_A(X, Y, d.mo, d.mi, nin, nout, csr, nullptr, s);
+    r = launch_mpo_A(X, Y, d.mo, d.mi, nin, nout, csr, nullptr, mpo_tile_cols(nin), s);
     dim3 tg((unsigned)((d.mo + 31) / 32), (unsigned)((d.mi * d.d + 31) / 32));
     transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, At, d.mi * d.d, d.mo);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_left: launch failed");
@@ -2145,29 +2154,12 @@ static int env_right_impl(const heff_env_dims* dims, const double* R, const doub
   CKR(env_common_check(dims, R, B, W, Rout));
   const heff_env_dims d = *dims;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  std::vector<double> Wh(d.kl * d.d * d.d * d.kr);
-  CK(cudaMemcpyAsync(Wh.data(), W, sizeof(double) * Wh.size(), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  // CSR: rows (w,s), cols (s',w')
-  std::vector<int> rp{0}, cl;
-  std::vector<double> vl;
-  for (int64_t w = 0; w < d.kl; ++w)
-    for (int64_t ss = 0; ss < d.d; ++ss) {
-      for (int64_t sp = 0; sp < d.d; ++sp)
-        for (int64_t wp = 0; wp < d.kr; ++wp) {
-          const double v = Wh[((w * d.d + sp) * d.d + ss) * d.kr + wp];
-          if (v != 0.0) {
-            cl.push_back((int)(sp * d.kr + wp));
-            vl.push_back(v);
-          }
-        }
-      rp.push_back((int)vl.size());
-    }
-  Csr csr;
+  if (!is_device_ptr(W)) return set_err(HEFF_EINVAL, "heff_env_update_right: W is not a device pointer");
+  Csr csr;  // rows (w,s), cols (s',w'), built on the device
   auto pad = [](int64_t x) { return (x + 31) / 32 * 32; };
   const int64_t nX = pad(d.mo * d.d * d.kr * d.mi), nY = pad(d.mo * d.kl * d.d * d.mi);
   CKR(env_reserve((size_t)(nX + nY)));
-  CKR(upload_csr(csr, rp, cl, vl, s));
+  CKR(env_csr(csr, kCsrSingleR, W, d.kl, d.d, d.kr, s));
   double* X = t_env_arena().buf;
   double* Y = X + nX;
   auto cleanup = [&]() { cudaStreamSynchronize(s); };
@@ -2196,7 +2188,7 @@ static int env_right_impl(const heff_env_dims* dims, const double* R, const doub
   r = launch_gemm(g1, 0, s, &nl, ws_for(t_env_splitws, s));
   if (!r) {
     const int nin = (int)(d.d * d.kr), nout = (int)(d.kl * d.d);
-    r = launch_mpo_A(X, Y, d.mi, d.mo, nin, nout, csr, nullptr, s);
+    r = launch_mpo_A(X, Y, d.mi, d.mo, nin, nout, csr, nullptr, mpo_tile_cols(nin), s);
     if (cudaGetLastError() != cudaSuccess) r = set_err(HEFF_ECUDA, "heff_env_update_right: launch failed");
   }
   if (!r) r = launch_gemm(g3, 0, s, &nl, ws_for(t_env_splitws, s));
@@ -2451,10 +2443,11 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
     }
     p->sp_kblocks += tot;
   }
-  // MPO blocks (a', 128-column b tile): live iff some (w,s1,s2) input or (s1',s2',w2) output
+  // MPO blocks (a', tcA-column b tile): live iff some (w,s1,s2) input or (s1',s2',w2) output
   // entry of the block is allowed; the rest are skipped and their T3 entries stay zero.
   {
-    const int nbt = (int)((d.mR + kMpoCols - 1) / kMpoCols);
+    const int tc = p->tcA;  // the MPO kernel's column tile
+    const int nbt = (int)((d.mR + tc - 1) / tc);
     std::vector<unsigned char> live((size_t)d.mL * nbt, 0);
     std::vector<int> in_off, out_off;  // charge offsets: q(b) must equal qa[a'] + off
     for (int64_t w = 0; w < d.kL; ++w)
@@ -2468,7 +2461,7 @@ extern "C" int heff_set_qn(heff_plan p, const heff_qn* qn) {
     std::sort(offs.begin(), offs.end());
     offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
     for (int t = 0; t < nbt; ++t) {
-      const int64_t b0 = (int64_t)t * kMpoCols, b1 = std::min<int64_t>(d.mR, b0 + kMpoCols);
+      const int64_t b0 = (int64_t)t * tc, b1 = std::min<int64_t>(d.mR, b0 + tc);
       std::vector<int> tq(qn->qb + b0, qn->qb + b1);
       tq.erase(std::unique(tq.begin(), tq.end()), tq.end());  // qb sorted
       for (int64_t ap = 0; ap < d.mL; ++ap) {

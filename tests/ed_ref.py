@@ -45,9 +45,12 @@ def cylinder_bonds(Lx, Ly=6):
     return [(min(i, j), max(i, j), J) for i, j, J in b]
 
 
-def hubbard(N: int, t=1.0, U=4.0) -> sp.csr_matrix:
-    """Open Hubbard chain on 2N fermionic modes p = 2i + sigma (up=0, dn=1), Jordan-Wigner
-    strings over all modes q < p.  Mode basis |n> with n=1 occupied; a = [[0,1],[0,0]]."""
+def hubbard(N: int, t=1.0, U=4.0, bonds=None) -> sp.csr_matrix:
+    """Hubbard model on 2N fermionic modes p = 2i + sigma (up=0, dn=1), Jordan-Wigner
+    strings over all modes q < p.  Mode basis |n> with n=1 occupied; a = [[0,1],[0,0]].
+    bonds: hopping pairs (i, j, J) (default: the open chain, J = 1); hopping -t J."""
+    if bonds is None:
+        bonds = chain_bonds(N)
     M = 2 * N
     a = sp.csr_matrix(np.array([[0.0, 1.0], [0.0, 0.0]]))
     Z = sp.csr_matrix(np.diag([1.0, -1.0]))
@@ -62,11 +65,11 @@ def hubbard(N: int, t=1.0, U=4.0) -> sp.csr_matrix:
 
     cs = [c(p) for p in range(M)]
     H = sp.csr_matrix((2 ** M, 2 ** M))
-    for i in range(N - 1):
+    for i, j, J in bonds:
         for s in range(2):
-            p, q = 2 * i + s, 2 * (i + 1) + s
+            p, q = 2 * i + s, 2 * j + s
             hop = cs[p].T @ cs[q]
-            H = H - t * (hop + hop.T)
+            H = H - t * J * (hop + hop.T)
     for i in range(N):
         H = H + U * (cs[2 * i].T @ cs[2 * i]) @ (cs[2 * i + 1].T @ cs[2 * i + 1])
     return H.tocsr()

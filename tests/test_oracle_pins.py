@@ -62,6 +62,35 @@ def test_p11_hubbard_mpo_vs_jordan_wigner():
     np.testing.assert_allclose(Hm, Hj[np.ix_(p, p)], atol=1e-13)
 
 
+def _jw_perm(N):
+    """Site basis permutation: the JW mode basis orders a site (n_up n_dn) = (00, 01, 10, 11),
+    the MPO's is (0, up, dn, updn)."""
+    p = np.arange(4 ** N).reshape((4,) * N)
+    for ax in range(N):
+        p = np.take(p, np.array([0, 2, 1, 3]), axis=ax)
+    return p.reshape(-1)
+
+
+@pytest.mark.parametrize("width,Lx", [(3, 2), (4, 2), (6, 1)])
+def test_p11_hubbard_cylinder_mpo_vs_jordan_wigner(width, Lx):
+    """The d = 4, k = 4 width + 2 Hubbard-cylinder MPO (k = 26 at width 6) against the
+    Jordan-Wigner Hamiltonian of the same cylinder built from fermionic mode operators
+    (column, y-wrap and x hoppings; (6, 1) is the k = 26 generator on one ring)."""
+    N = width * Lx
+    Ws = [mpo.hubbard_cylinder_W(j, width) for j in range(N)]
+    k = Ws[0].shape[0]
+    assert k == 4 * width + 2 and Ws[0].shape[1] == 4
+    l, r = mpo.boundary_vectors(k)
+    H = ed_ref.hubbard(N, bonds=ed_ref.cylinder_bonds(Lx, width))
+    p = _jw_perm(N)
+    rng = np.random.default_rng(width)
+    for _ in range(2):
+        x = rng.standard_normal(4 ** N)
+        xj = np.zeros_like(x)
+        xj[p] = x
+        np.testing.assert_allclose(ed_ref.mpo_apply(Ws, l, r, x), (H @ xj)[p], atol=1e-12)
+
+
 # ---------------------------------------------------------------- P1: N=2, trivial boundary
 def test_p1_two_site_trivial_boundary_is_dense_H(oracle_lib):
     x = C.trivial_two_site()
@@ -133,6 +162,21 @@ def test_p2_hubbard_ed(oracle_lib):
     res = oracle_lib.lanczos_heff(L, W1, W2, R, psi, max_iter=300, tol=1e-10, converge=True)
     e0 = np.linalg.eigvalsh(ed_ref.hubbard(4).toarray())[0]
     assert abs(res.energy - e0) <= 1e-10
+
+
+def test_p2_hubbard_cylinder_ed(oracle_lib):
+    """Full-rank environments of the 2 x 3 Hubbard cylinder (d = 4, k = 14; window (2,3):
+    mL = mR = 16, dim 4096 = 4^6): the oracle's converged Lanczos equals the ground energy of
+    the Jordan-Wigner Hamiltonian."""
+    width, Lx = 3, 2
+    N = width * Lx
+    Ws = [mpo.hubbard_cylinder_W(j, width) for j in range(N)]
+    x = C.model_inputs(Ws, 2, 16, seed=13)
+    L, W1, W2, R, psi = x.numpy()
+    assert L.shape[0] * 16 * R.shape[0] == 4 ** N
+    res = oracle_lib.lanczos_heff(L, W1, W2, R, psi, max_iter=400, tol=1e-10, converge=True)
+    e0 = spla.eigsh(ed_ref.hubbard(N, bonds=ed_ref.cylinder_bonds(Lx, width)), k=1, which="SA", tol=1e-14)[0][0]
+    assert abs(res.energy - e0) <= 1e-10, (res.energy, e0)
 
 
 # ---------------------------------------------------------------- P3, P4, P5, P6, P9
