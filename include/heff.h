@@ -28,8 +28,10 @@
  * lengths) enables the TMA-fed GEMM path, otherwise a plain-load path runs.
  *
  * Ownership: L, W1, W2 and R are BORROWED -- they must stay allocated and unmodified
- * for the plan's lifetime (W1/W2 are also copied at create).  The plan owns its
- * workspace (intermediates, Lanczos basis, gather buffer) and its NCCL communicator.
+ * for the plan's lifetime (W1/W2 are read once, at create, into the plan's device-side
+ * two-site MPO; a sharded plan also keeps a row-reordered copy of its R shard).  The plan
+ * owns its workspace (intermediates, Lanczos basis, gather buffer) and its NCCL
+ * communicator.
  *
  * Streams: `heff_stream` is a cudaStream_t (NULL = legacy default stream).  heff_apply
  * is stream-ordered and returns before completion.  lanczos_ground blocks until done.
@@ -100,8 +102,13 @@ typedef struct {
   double* theta_out;
 } heff_lanczos_opts;
 
-/* Create a plan: validates dims, copies W1/W2, allocates workspace, and (dist with a
- * uid) joins the NCCL communicator (collective over all ranks). */
+/* Create a plan: validates dims, allocates workspace, builds the two-site MPO
+ * Wc = sum_w1 W1 W2 as a CSR list ON THE DEVICE (no host copy, no synchronisation: the
+ * set-up kernels are enqueued on `stream`, and every later call on another stream is
+ * ordered after them by an event), and (dist with a uid) joins the NCCL communicator
+ * (collective over all ranks).  Limits: kL d1 d2 <= 1600 and d1 d2 kR <= 1600 (the MPO
+ * kernel's shared-memory tile narrows from 128 to 16 columns as k d^2 grows; HEFF_EUNSUPPORTED
+ * beyond).  W1/W2 must be device pointers (HEFF_EINVAL otherwise). */
 int heff_create(heff_plan* out, const heff_dims* dims, const double* L, const double* W1, const double* W2,
                 const double* R, const heff_dist* dist, heff_stream stream);
 

@@ -1,0 +1,353 @@
+// gemm_small.cuh -- the order-A matvec for small bonds (m ~ 64..512): the regime where the
+// general persistent GEMM spends as much time in tile ramp-up, epilogues and stream-K
+// fix-ups as in DMMA (C2, m = 256: 35 us per GEMM for 18 us of DMMA work; ncu: the DMMA
+// pipe busy for exactly the algorithmic cycles, the rest idle).  Two kernels replace the
+// three launches GEMM1 -> MPO -> GEMM4:
+//
+//  gemm1_mpo_fused_kernel: GEMM1 on "fat" tiles whose rows are TA whole a' groups of L
+//    (rows (a', w), BM = TA kL = 80) and whose columns are TB b values for every (s1 s2)
+//    (BN = d1 d2 TB = 128, four 16-column TMA boxes per (s1 s2) block of psi); the finished
+//    accumulator tile -- every (w, s1, s2) of T1 for TA a' and TB b -- is staged in shared
+//    memory and the two-site MPO (CSR) is applied there, so T1 never reaches memory and
+//    the MPO kernel launch disappears: T3[a'][(s1' s2' w2)][b] is written directly.
+//
+//  gemm_cluster_splitk_kernel: GEMM4 (and any GEMM with fewer 64x64 tiles than SMs / 2)
+//    with each output tile's K range split over the CS CTAs of a thread-block cluster; the
+//    ranks > 0 push their partial accumulators into rank 0's shared memory through DSMEM
+//    (st.shared::cluster + a cluster-scope mbarrier), rank 0 sums them in rank order
+//    (deterministic) and stores the tile -- no partial-tile round trip through L2, no
+//    ticket / flag protocol, one wave.
+//
+// Both use the DMMA main loop of gemm.cuh (TMA ring, mbarriers, one producer lane,
+// 8 consumer warps, the same k-permutation and swizzled fragment loads).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "gemm.cuh"
+#include "ptx.cuh"
+
+namespace heff {
+
+// ---- DMMA over one stage (the k-block held in shared memory) -------------------------
+// acc[MI][NJ][2] += A_stage(rows wm0..wm0+WM) . B_stage(cols wn0..wn0+WN) for one 16-wide k
+// block; B N-major (box layout of psi's 16x16 TMA boxes, box index n >> 4) or K-major.
+template <int MI, int NJ, bool B_KMAJOR>
+__device__ __forceinline__ void dmma_stage(double (&acc)[MI][NJ][2], uint32_t sA, uint32_t sB, uint32_t offA0,
+                                           uint32_t offB0, int wn0, int g, int t) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double a[MI][2], b[NJ][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) lds128(a[i][0], a[i][1], sA + ((offA0 + i * 1024) ^ (h * 64)));
+    if constexpr (B_KMAJOR) {
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) lds128(b[j][0], b[j][1], sB + ((offB0 + j * 1024) ^ (h * 64)));
+    } else {
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int n = wn0 + 8 * j + g;
+        const int ni = n & 15;
+        const uint32_t box = sB + (n >> 4) * 2048;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int k = 2 * t + q + 8 * h;
+          b[j][q] = lds64(box + k * 128 + ((((ni >> 1) ^ (k & 7))) << 4) + ((ni & 1) << 3));
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][q], b[j][q]);
+  }
+}
+
+// ---- GEMM1 + two-site MPO, fused ---------------------------------------------------------
+constexpr int kFusedBM = 80, kFusedBN = 128, kFusedWM = 40, kFusedWN = 32, kFusedStages = 5;
+constexpr int kFusedConsumerWarps = (kFusedBM / kFusedWM) * (kFusedBN / kFusedWN);  // 8
+constexpr int kFusedThreads = (kFusedConsumerWarps + 4) * 32;
+constexpr int kFusedStageBytes = kFusedBM * 128 + kFusedBN * 128;
+constexpr int kFusedEpiPitch = kFusedBN + 4;  // doubles per staged row: conflict-free double2 stores
+constexpr int kFusedSmemBytes =
+    kFusedStages * kFusedStageBytes + kFusedBM * kFusedEpiPitch * 8 + 2 * kFusedStages * 8 + 1024;
+
+// Tile (ta, tb): T1 rows (a', w) for a' in [ta TA, ta TA + TA) = L rows [ta BM, ta BM + BM)
+// (TA kL == BM), columns (s, b) for s < dd, b in [tb TB, tb TB + TB) (dd TB == BN).
+// csr: the order-A two-site MPO, rows o = (s1', s2', w2) (nout = dd kR), columns (w, s1, s2).
+__global__ void __launch_bounds__(kFusedThreads, 1)
+    gemm1_mpo_fused_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmPsi,
+                           double* __restrict__ T3, int mL, int mR, int kL, int dd, int TA, int TB, int nout,
+                           const int* __restrict__ rowptr, const int* __restrict__ col,
+                           const double* __restrict__ val) {
+  constexpr int MI = kFusedWM / 8, NJ = kFusedWN / 8, ST = kFusedStages;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* epi = reinterpret_cast<double*>(smem + ST * kFusedStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kFusedBM * kFusedEpiPitch);
+  uint64_t* empty = full + ST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ta_n = mL / TA, tb_n = mR / TB;
+  const int tiles = ta_n * tb_n;
+  const int ktiles = (mL + kGemmBK - 1) / kGemmBK;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kFusedConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  pdl_wait();  // L, psi and T3 only after the previous kernel in the stream
+  __syncthreads();
+
+  if (warp >= kFusedConsumerWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(40));
+    if (warp == kFusedConsumerWarps && lane == 0) {
+      tma_prefetch_desc(&tmL);
+      tma_prefetch_desc(&tmPsi);
+      int stage = 0;
+      uint32_t phase = 0;
+      const int bps = TB / 16;  // 16-column boxes per (s1 s2) block
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int ta = tile / tb_n, tb = tile - ta * tb_n;
+        for (int kb = 0; kb < ktiles; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          unsigned char* sA = smem + stage * kFusedStageBytes;
+          unsigned char* sB = sA + kFusedBM * 128;
+          mbar_arrive_expect_tx(&full[stage], kFusedStageBytes);
+          tma_load_2d(sA, &tmL, &full[stage], kb * kGemmBK, ta * kFusedBM);
+#pragma unroll 1
+          for (int q = 0; q < kFusedBN / 16; ++q) {
+            const int s = q / bps, c = q - s * bps;
+            tma_load_2d(sB + q * 2048, &tmPsi, &full[stage], s * mR + tb * TB + c * 16, kb * kGemmBK);
+          }
+          if (++stage == ST) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(232));
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp / (kFusedBN / kFusedWN)) * kFusedWM;
+  const int wn0 = (warp % (kFusedBN / kFusedWN)) * kFusedWN;
+  const uint32_t smem_base = smem_u32(smem);
+  const uint32_t offA0 = (wm0 + g) * 128 + ((t ^ g) << 4);
+  constexpr int kCons = kFusedConsumerWarps * 32;
+  const int ctid = threadIdx.x;  // consumers are threads [0, kCons)
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int ta = tile / tb_n, tb = tile - ta * tb_n;
+    double acc[MI][NJ][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kb = 0; kb < ktiles; ++kb) {
+      mbar_wait(&full[stage], phase);
+      const uint32_t sA = smem_base + stage * kFusedStageBytes;
+      dmma_stage<MI, NJ, false>(acc, sA, sA + kFusedBM * 128, offA0, 0, wn0, g, t);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == ST) { stage = 0; phase ^= 1; }
+    }
+    // the T1 tile -> shared memory (the previous tile's MPO reads are finished)
+    consumers_bar(kCons);
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        *reinterpret_cast<double2*>(epi + (wm0 + 8 * i + g) * kFusedEpiPitch + wn0 + 8 * j + 2 * t) =
+            make_double2(acc[i][j][0], acc[i][j][1]);
+    consumers_bar(kCons);
+    // two-site MPO: T3[a'][o][b] = sum_c Wc[o][c] T1[a'][c][b], c = (w, s), b-pairs per thread
+    const int pairs = TB / 2, rows_out = TA * nout;
+    const int bp = ctid % pairs;
+    for (int ro = ctid / pairs; ro < rows_out; ro += kCons / pairs) {
+      const int al = ro / nout, o = ro - al * nout;
+      const double* src = epi + al * kL * kFusedEpiPitch + 2 * bp;
+      double2 a2 = make_double2(0.0, 0.0);
+      const int e1 = __ldg(rowptr + o + 1);
+      for (int e = __ldg(rowptr + o); e < e1; ++e) {
+        const int c = __ldg(col + e);
+        const int w = c / dd, s = c - w * dd;
+        const double v = __ldg(val + e);
+        const double2 x = *reinterpret_cast<const double2*>(src + w * kFusedEpiPitch + s * TB);
+        a2.x = fma(v, x.x, a2.x);
+        a2.y = fma(v, x.y, a2.y);
+      }
+      const int64_t ap = (int64_t)ta * TA + al;
+      *reinterpret_cast<double2*>(T3 + (ap * nout + o) * mR + (int64_t)tb * TB + 2 * bp) = a2;
+    }
+  }
+}
+
+// ---- GEMM with cluster split-K ------------------------------------------------------------
+// One output tile per cluster of CS CTAs; rank r runs k-blocks [kt r / CS, kt (r+1) / CS).
+// Shared memory: the TMA ring, then (rank 0) CS - 1 partial slots [i][j][thread] of double2.
+template <int BM, int BN, int WM, int WN, int STAGES, int CS>
+struct ClusterGemmCfg {
+  static constexpr int kConsumerWarps = (BM / WM) * (BN / WN);
+  static constexpr int kThreads = (kConsumerWarps + 4) * 32;
+  static constexpr int kStageBytes = BM * 128 + BN * 128;
+  static constexpr int kSlotBytes = BM * BN * 8;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + (CS - 1) * kSlotBytes + (2 * STAGES + 1) * 8 + 1024;
+  static_assert(kConsumerWarps == 8, "8 consumer warps");
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR, int CS>
+__global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kThreads, 1)
+    gemm_cluster_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                               double* __restrict__ C, int64_t ldc, int M, int N, int K, int vec_store,
+                               int accumulate) {
+  using Cfg = ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>;
+  constexpr int MI = WM / 8, NJ = WN / 8;
+  constexpr int kCons = Cfg::kConsumerWarps * 32;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double2* slots = reinterpret_cast<double2*>(smem + STAGES * Cfg::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes + (CS - 1) * Cfg::kSlotBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* red = empty + STAGES;  // rank 0: the partial slots are full
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int tile = blockIdx.x / CS;
+  const int num_n = (N + BN - 1) / BN;
+  const int mb = tile / num_n, nb = tile - mb * num_n;
+  const int ktiles = (K + kGemmBK - 1) / kGemmBK;
+  const int kb0 = (int)((int64_t)ktiles * rank / CS), kb1 = (int)((int64_t)ktiles * (rank + 1) / CS);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::kConsumerWarps);
+    }
+    mbar_init(red, (CS - 1) * kCons);
+    fence_barrier_init();
+  }
+  cluster_sync_all();  // rank 0's reduction barrier exists before any peer arrives on it
+  pdl_wait();
+
+  if (warp >= Cfg::kConsumerWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(40));
+    if (warp == Cfg::kConsumerWarps && lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char* sA = smem + stage * Cfg::kStageBytes;
+        unsigned char* sB = sA + BM * 128;
+        mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+        tma_load_2d(sA, &tmA, &full[stage], kb * kGemmBK, mb * BM);
+        if constexpr (B_KMAJOR) {
+          tma_load_2d(sB, &tmB, &full[stage], kb * kGemmBK, nb * BN);
+        } else {
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) tma_load_2d(sB + q * 2048, &tmB, &full[stage], nb * BN + q * 16, kb * kGemmBK);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    return;
+  }
+
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(232));
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp / (BN / WN)) * WM;
+  const int wn0 = (warp % (BN / WN)) * WN;
+  const uint32_t smem_base = smem_u32(smem);
+  const uint32_t offA0 = (wm0 + g) * 128 + ((t ^ g) << 4);
+  const uint32_t offB0 = (wn0 + g) * 128 + ((t ^ g) << 4);
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int kb = kb0; kb < kb1; ++kb) {
+    mbar_wait(&full[stage], phase);
+    const uint32_t sA = smem_base + stage * Cfg::kStageBytes;
+    dmma_stage<MI, NJ, B_KMAJOR>(acc, sA, sA + BM * 128, offA0, offB0, wn0, g, t);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+  }
+  const int ctid = threadIdx.x;
+  if (rank != 0) {
+    // push the partial into rank 0's slot (rank - 1), then arrive on rank 0's barrier
+    const uint32_t dst = mapa_shared(smem_u32(slots + (size_t)(rank - 1) * (BM * BN / 2)), 0);
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const uint32_t a = dst + (uint32_t)(((i * NJ + j) * kCons + ctid) * 16);
+        asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(acc[i][j][0]), "d"(acc[i][j][1])
+                     : "memory");
+      }
+    const uint32_t rb = mapa_shared(smem_u32(red), 0);
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+    return;
+  }
+  // rank 0: wait for the CS - 1 partials, sum in rank order, store
+  {
+    const uint32_t rb = smem_u32(red);
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], 0;\n"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(rb)
+        : "memory");
+  }
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int row = mb * BM + wm0 + 8 * i + g;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+#pragma unroll
+      for (int r = 0; r < CS - 1; ++r) {
+        const double2 p = slots[(size_t)r * (BM * BN / 2) + (i * NJ + j) * kCons + ctid];
+        v.x += p.x;
+        v.y += p.y;
+      }
+      if (row >= M) continue;
+      double* crow = C + (int64_t)row * ldc;
+      const int colj = nb * BN + wn0 + 8 * j + 2 * t;
+      if (vec_store && colj + 1 < N) {
+        if (accumulate) {
+          const double2 o = *reinterpret_cast<const double2*>(crow + colj);
+          v.x += o.x;
+          v.y += o.y;
+        }
+        *reinterpret_cast<double2*>(crow + colj) = v;
+      } else {
+        if (colj < N) crow[colj] = v.x + (accumulate ? crow[colj] : 0.0);
+        if (colj + 1 < N) crow[colj + 1] = v.y + (accumulate ? crow[colj + 1] : 0.0);
+      }
+    }
+  }
+}
+
+}  // namespace heff

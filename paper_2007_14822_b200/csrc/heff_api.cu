@@ -27,6 +27,7 @@
 #include "../../include/heff.h"
 #include "blas1.cuh"
 #include "gemm.cuh"
+#include "gemm_small.cuh"
 #include "mpo.cuh"
 #include "tridiag.h"
 #include "internal.h"
@@ -154,6 +155,10 @@ using CfgNN = TmaGemmCfg<kBM, kBN, kWM, kWN, kStages, false>;
 using CfgNT = TmaGemmCfg<kBM, kBN, kWM, kWN, kStages, true>;
 using CfgNNs = TmaGemmCfg<kBMs, kBNs, kWMs, kWNs, kStagesS, false>;
 using CfgNTs = TmaGemmCfg<kBMs, kBNs, kWMs, kWNs, kStagesS, true>;
+// cluster split-K (gemm_small.cuh): 64x64 tiles, 6-stage ring, CS = 2 or 4 CTAs per tile
+constexpr int kClStages = 6;
+using CfgCl2 = ClusterGemmCfg<64, 64, 32, 16, kClStages, 2>;
+using CfgCl4 = ClusterGemmCfg<64, 64, 32, 16, kClStages, 4>;
 
 
 
@@ -295,11 +300,76 @@ static bool use_small_tile(const GemmOp& g, const ShardedA* sa) {
 
 // sa != nullptr: the A operand is K-sharded over sa->nsh tensor maps (gemm_dmma_tma_sharded_kernel;
 // g.A is ignored, the TMA path is required).
+// Cluster split-K for dense GEMMs with few 64x64 tiles (gemm_small.cuh): CS CTAs of a cluster
+// share one tile's K range and reduce through DSMEM.  Chosen when tiles x CS fills at least
+// 60% of the SMs in one wave with >= 4 k-blocks per rank (else the stream-K schedule, which
+// spreads a handful of tiles over every SM, is better).  HEFF_NO_CLUSTER_SPLITK=1 disables.
+static int cluster_splitk_size(const GemmOp& g, const ShardedA* sa) {
+  if (sa || g.sp_list || getenv("HEFF_NO_CLUSTER_SPLITK") != nullptr) return 0;
+  if (const char* e = getenv("HEFF_GEMM_TILE"))
+    if (atoi(e) == 128) return 0;
+  const int64_t tiles = ((g.M + 63) / 64) * ((g.N + 63) / 64);
+  const int64_t ktiles = (g.K + kGemmBK - 1) / kGemmBK;
+  for (int cs : {4, 2})
+    if (tiles * cs <= g_num_sms && tiles * cs * 10 >= 6 * (int64_t)g_num_sms && ktiles >= 4 * cs) return cs;
+  return 0;
+}
+
+template <int CS>
+static int launch_cluster_splitk(GemmOp& g, cudaStream_t s) {
+  using Cfg = ClusterGemmCfg<64, 64, 32, 16, kClStages, CS>;
+  if (g.mapA_ptr != g.A || g.mapA_rows != g.M || g.mapA_box != 64) {
+    CKR(make_map(&g.mapA, g.A, g.M, g.K, g.lda, kGemmBK, 64));
+    g.mapA_ptr = g.A;
+    g.mapA_rows = g.M;
+    g.mapA_box = 64;
+  }
+  if (g.mapB_ptr != g.B || g.mapB_rows != g.N || g.mapB_box != 64) {
+    if (g.b_kmajor)
+      CKR(make_map(&g.mapB, g.B, g.N, g.K, g.ldb, kGemmBK, 64));
+    else
+      CKR(make_map(&g.mapB, g.B, g.K, g.N, g.ldb, 16, kGemmBK));
+    g.mapB_ptr = g.B;
+    g.mapB_rows = g.N;
+    g.mapB_box = 64;
+  }
+  const int64_t tiles = ((g.M + 63) / 64) * ((g.N + 63) / 64);
+  const int vec = ((g.ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(g.C) & 15) == 0) ? 1 : 0;
+  static const bool pdl_off = getenv("HEFF_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(tiles * CS));
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_off ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const int M32 = (int)g.M, N32 = (int)g.N, K32 = (int)g.K;
+  if (g.b_kmajor)
+    CK(cudaLaunchKernelEx(&cfg, gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, CS>, g.mapA, g.mapB, g.C,
+                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate));
+  else
+    CK(cudaLaunchKernelEx(&cfg, gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, false, CS>, g.mapA, g.mapB, g.C,
+                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate));
+  return HEFF_OK;
+}
+
 int launch_gemm(GemmOp& g, int path, cudaStream_t s, int* nlaunch, SplitWs* ws, const ShardedA* sa) {
   if (g.M == 0 || g.N == 0) return HEFF_OK;
   const bool use_tma = sa != nullptr || (path == 2) || (path == 0 && tma_ok(g));
   if (path == 2 && !tma_ok(g)) return set_err(HEFF_EUNSUPPORTED, "TMA GEMM path needs 16-byte rows/alignment");
-  if (use_tma) {
+  const int cs = use_tma ? cluster_splitk_size(g, sa) : 0;
+  if (cs == 4) {
+    CKR(launch_cluster_splitk<4>(g, s));
+  } else if (cs == 2) {
+    CKR(launch_cluster_splitk<2>(g, s));
+  } else if (use_tma) {
     if (use_small_tile(g, sa))
       CKR((launch_tma<kBMs, kBNs, kWMs, kWNs, kStagesS>(g, s, nlaunch, ws, sa)));
     else
@@ -368,6 +438,15 @@ int init_device_once() {
   CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
   CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
   CK(cudaFuncSetAttribute(heff_small_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallMvMaxSmem));
+  CK(cudaFuncSetAttribute(gemm1_mpo_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemBytes));
+  CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, false, 2>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgCl2::kSmemBytes));
+  CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, 2>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgCl2::kSmemBytes));
+  CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, false, 4>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgCl4::kSmemBytes));
+  CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, 4>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, CfgCl4::kSmemBytes));
   CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   g_dev_inited.fetch_or(bit, std::memory_order_release);
   return HEFF_OK;
@@ -464,6 +543,11 @@ struct heff_plan_s {
   int64_t chunk_rows = 0;                   // a' rows per chunk
   double *T1 = nullptr, *T3 = nullptr;
   GemmOp g1, g4;                            // per-chunk ops (A/C pointers advanced per chunk)
+  // small bonds: GEMM1 + MPO fused (gemm1_mpo_fused_kernel), fat tiles of TA a' x TB b
+  int fusedTA = 0, fusedTB = 0;             // 0: not eligible
+  CUtensorMap fmapL, fmapPsi;
+  const double* fpsi_ptr = nullptr;
+  bool fmapL_ok = false;
   // order B workspace
   double *V1 = nullptr, *V3 = nullptr;
   GemmOp gA, gD;
@@ -813,6 +897,26 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
     p->g4.ldb = d.kR * d.mR;
     p->g4.b_kmajor = true;
     p->g4.ldc = d.mR;
+    // GEMM1 + MPO fused on fat tiles (gemm_small.cuh): rows = whole a' groups (TA kL = 80),
+    // columns = TB b for each (s1 s2) (d1 d2 TB = 128); used when the tiles make 0.5..1 wave
+    {
+      const int64_t dd = d.d1 * d.d2;
+      const bool shape_ok = (kFusedBM % d.kL == 0) && (kFusedBN % dd == 0) && (kFusedBN / dd) % 16 == 0 &&
+                            rows == d.mL && (d.mL % 2 == 0) &&
+                            (reinterpret_cast<uintptr_t>(L) & 15) == 0;
+      if (shape_ok) {
+        const int64_t TA = kFusedBM / d.kL, TB = kFusedBN / dd;
+        if (d.mL % TA == 0 && d.mR % TB == 0) {
+          const int64_t tiles = (d.mL / TA) * (d.mR / TB);
+          bool use = tiles <= g_num_sms && 2 * tiles >= g_num_sms;
+          if (const char* e = getenv("HEFF_FUSED_MATVEC")) use = atoi(e) != 0;
+          if (use) {
+            p->fusedTA = (int)TA;
+            p->fusedTB = (int)TB;
+          }
+        }
+      }
+    }
   } else {
     const int64_t nb = p->nb;
     if (ws_malloc(&p->V1, sizeof(double) * d.mL * d.d1 * d.d2 * nb * d.kR) != cudaSuccess ||
@@ -1092,6 +1196,35 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
       ++*nl;
       return HEFF_OK;
     }
+  }
+  if (p->fusedTA > 0 && p->sp1 == nullptr && p->sp4 == nullptr && p->gemm_path == 0 &&
+      (reinterpret_cast<uintptr_t>(psi) & 15) == 0) {
+    // GEMM1 + two-site MPO in one kernel (T1 never written), then GEMM4
+    const int64_t dd = d.d1 * d.d2;
+    if (!p->fmapL_ok) {
+      CKR(make_map(&p->fmapL, p->L, d.mL * d.kL, d.mL, d.mL, kGemmBK, kFusedBM));
+      p->fmapL_ok = true;
+    }
+    if (p->fpsi_ptr != psi) {
+      CKR(make_map(&p->fmapPsi, psi, d.mL, dd * d.mR, dd * d.mR, 16, kGemmBK));
+      p->fpsi_ptr = psi;
+    }
+    const int tiles = (int)((d.mL / p->fusedTA) * (d.mR / p->fusedTB));
+    CKR(prof_mark(p, 0, s));
+    CK(launch_pdl(gemm1_mpo_fused_kernel, dim3((unsigned)std::min(tiles, g_num_sms)), dim3(kFusedThreads),
+                  kFusedSmemBytes, s, p->fmapL, p->fmapPsi, p->T3, (int)d.mL, (int)d.mR, (int)d.kL, (int)dd,
+                  p->fusedTA, p->fusedTB, (int)(dd * d.kR), (const int*)p->csrA.d_rowptr, (const int*)p->csrA.d_col,
+                  (const double*)p->csrA.d_val));
+    ++*nl;
+    CKR(prof_mark(p, 1, s));
+    CKR(prof_mark(p, 2, s));
+    p->g4.M = d.mL * dd;
+    p->g4.A = p->T3;
+    p->g4.C = out;
+    p->g4.accumulate = accumulate;
+    CKR(launch_gemm(p->g4, p->gemm_path, s, nl, &p->splitws));
+    CKR(prof_mark(p, 3, s));
+    return HEFF_OK;
   }
   for (int64_t a0 = 0; a0 < d.mL; a0 += p->chunk_rows) {
     const int64_t rows = std::min(p->chunk_rows, d.mL - a0);

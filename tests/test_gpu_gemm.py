@@ -165,3 +165,35 @@ def test_pdl_on_off_bitwise(dev, tmp_path):
         files.append(np.load(f))
     for k in files[0].files:
         assert np.array_equal(files[0][k], files[1][k]), k
+
+
+# shapes whose 64x64 tile count x CS fills 60..100% of the SMs in one wave: the cluster
+# split-K kernel (CS = 2 or 4 CTAs per tile, DSMEM reduction) runs them
+CLUSTER_SHAPES = [(1024, 256, 1280), (512, 256, 2048), (1000, 250, 1100), (448, 320, 999), (200, 1200, 600)]
+
+
+@pytest.mark.parametrize("shape", CLUSTER_SHAPES)
+@pytest.mark.parametrize("bk", [False, True])
+def test_gemm_cluster_splitk(dev, shape, bk, monkeypatch):
+    """Cluster split-K against torch.matmul, bitwise run-to-run, with accumulate; and against
+    the stream-K schedule (HEFF_NO_CLUSTER_SPLITK) within rounding."""
+    from paper_2007_14822_b200.heff import gemm
+    M, N, K = shape
+    if (K if bk else N) % 2 or K % 2:
+        pytest.skip("TMA path needs even row pitches")
+    g = torch.Generator(device=dev).manual_seed(M + N + K)
+    A = torch.randn(M, K, dtype=torch.float64, device=dev, generator=g)
+    B = torch.randn((N, K) if bk else (K, N), dtype=torch.float64, device=dev, generator=g)
+    ref = A @ (B.T if bk else B)
+    tol = 1e-13 * max(1.0, K ** 0.5) * ref.abs().max().item()
+    C1 = gemm(A, B, bk)
+    C2 = gemm(A, B, bk)
+    C0 = torch.randn(M, N, dtype=torch.float64, device=dev, generator=g)
+    C3 = gemm(A, B, bk, C=C0.clone(), accumulate=True)
+    monkeypatch.setenv("HEFF_NO_CLUSTER_SPLITK", "1")
+    Csk = gemm(A, B, bk)
+    torch.cuda.synchronize()
+    assert (C1 - ref).abs().max().item() <= tol
+    assert torch.equal(C1, C2), "cluster split-K not bitwise reproducible"
+    assert (C3 - (C0 + ref)).abs().max().item() <= tol + 1e-15 * C0.abs().max().item()
+    assert (C1 - Csk).abs().max().item() <= tol

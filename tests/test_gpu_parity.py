@@ -450,3 +450,30 @@ def test_binding_rejects_wrong_vector_sizes(dev):
         with pytest.raises(ValueError):
             h.apply_blocked(x.psi[:, :, :, :128].contiguous())
         h.apply_blocked(x.psi.reshape(-1).clone())
+
+
+@pytest.mark.parametrize("case,env", [("c2", None), ("c2", "0"), ("cyl128", None), ("uneven", "1"),
+                                      ("c2_m240", None)])
+def test_fused_gemm1_mpo_matvec(dev, orc, case, env, monkeypatch):
+    """Small bonds: GEMM1 + the two-site MPO fused on fat tiles (T1 never written), GEMM4 by
+    cluster split-K -- the default at C2 (m = 256) and the k = 20 cylinder at m = 128; forced
+    (HEFF_FUSED_MATVEC=1) on a sub-half-wave mL != mR shape; off (=0) for comparison; m = 240
+    (mR not a multiple of the 32-wide b tile) falls back.  Parity with the oracle in all."""
+    from paper_2007_14822_b200 import Heff
+    if env is not None:
+        monkeypatch.setenv("HEFF_FUSED_MATVEC", env)
+    x = {"c2": lambda: C.make("c2"), "cyl128": lambda: C.make("c4", m=128),
+         "uneven": lambda: C.model_inputs([C.mpo.heisenberg_chain_W()] * 20, 6, 192, seed=77),
+         "c2_m240": lambda: C.make("c2", m=240)}[case]()
+    L, W1, W2, R, psi = x.numpy()
+    ref = orc.heff_apply(L, W1, W2, R, psi)
+    xd = x.to(dev)
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        out = h.apply(xd.psi)
+        out2 = h.apply(xd.psi)
+        torch.cuda.synchronize()
+        nl = h.get_option(2)
+    assert rel(out.cpu().numpy(), ref) <= MATVEC_TOL
+    assert torch.equal(out, out2)
+    if case in ("c2", "cyl128", "uneven") and env != "0":
+        assert nl == 2, nl                 # fused GEMM1+MPO, GEMM4
