@@ -177,13 +177,34 @@ def free_port() -> int:
         return sk.getsockname()[1]
 
 
-def spawn_ranks(n: int) -> int:
+def dry_run(args) -> int:
+    """--dry-run: the rank plumbing alone (gloo on CPU): every rank joins, the ranks are summed."""
+    import torch
+    import torch.distributed as dist
+    world = env_int("WORLD_SIZE", 1)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+        return 2
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([float(env_int("RANK", 0))])
+        dist.all_reduce(t)
+        dist.destroy_process_group()
+        total = int(t.item())
+    else:
+        total = 0
+    if env_int("RANK", 0) == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "rank_sum": total}), flush=True)
+    return 0
+
+
+def spawn_ranks(n: int, check_devices: bool = True) -> int:
     """--gpus N without a torchrun environment: re-launch this command as N ranks (one per
     GPU) under torch.distributed.run and return its exit code.  Fewer than N visible GPUs is
     an error (never a 1-GPU number labelled as N)."""
     import torch
     have = torch.cuda.device_count()
-    if have < n:
+    if check_devices and have < n:
         print(f"bench.py: --gpus {n} but only {have} CUDA device(s) are visible", file=sys.stderr)
         return 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
@@ -215,6 +236,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--sharded", action="store_true",
                     help="use the b'-sharded NCCL plan even at N=1 (exercises the multi-GPU code path)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check only: spawn the N ranks (gloo, no GPU work), all-reduce their ranks and "
+                         "print one JSON line from rank 0")
     ap.add_argument("--fused-gather", action="store_true",
                     help="sharded plans: GEMM_A reads the ranks' Krylov shards through NCCL symmetric-window "
                          "(NVLink) pointers instead of ncclAllGather + relayout (NEXT-5)")
@@ -225,7 +249,9 @@ def main():
         print("bench.py: --gpus must be >= 1", file=sys.stderr)
         return 2
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
-        return spawn_ranks(args.gpus)
+        return spawn_ranks(args.gpus, check_devices=not args.dry_run)
+    if args.dry_run:
+        return dry_run(args)
 
     import numpy as np
     import torch

@@ -80,7 +80,8 @@ constexpr int kFusedSmemBytes =
 // csr: the order-A two-site MPO, rows o = (s1', s2', w2) (nout = dd kR), columns (w, s1, s2).
 __global__ void __launch_bounds__(kFusedThreads, 1)
     gemm1_mpo_fused_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmPsi,
-                           double* __restrict__ T3, int mL, int mR, int kL, int dd, int TA, int TB, int nout,
+                           double* __restrict__ T3, int mL, int mR, int kL, int dd, int log2dd, int TA, int TB,
+                           int nout,
                            const int* __restrict__ rowptr, const int* __restrict__ col,
                            const double* __restrict__ val) {
   constexpr int MI = kFusedWM / 8, NJ = kFusedWN / 8, ST = kFusedStages;
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const uint32_t offA0 = (wm0 + g) * 128 + ((t ^ g) << 4);
   constexpr int kCons = kFusedConsumerWarps * 32;
   const int ctid = threadIdx.x;  // consumers are threads [0, kCons)
+  const uint32_t epi_s = smem_u32(epi);
   int stage = 0;
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -163,27 +165,32 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
-        *reinterpret_cast<double2*>(epi + (wm0 + 8 * i + g) * kFusedEpiPitch + wn0 + 8 * j + 2 * t) =
-            make_double2(acc[i][j][0], acc[i][j][1]);
+        sts128(epi_s + (uint32_t)(((wm0 + 8 * i + g) * kFusedEpiPitch + wn0 + 8 * j + 2 * t) * 8), acc[i][j][0],
+               acc[i][j][1]);
     consumers_bar(kCons);
-    // two-site MPO: T3[a'][o][b] = sum_c Wc[o][c] T1[a'][c][b], c = (w, s), b-pairs per thread
-    const int pairs = TB / 2, rows_out = TA * nout;
-    const int bp = ctid % pairs;
-    for (int ro = ctid / pairs; ro < rows_out; ro += kCons / pairs) {
-      const int al = ro / nout, o = ro - al * nout;
-      const double* src = epi + al * kL * kFusedEpiPitch + 2 * bp;
-      double2 a2 = make_double2(0.0, 0.0);
+    // two-site MPO: T3[a'][o][b] = sum_c Wc[o][c] T1[a'][c][b], c = (w, s); one b-pair per
+    // thread, output rows (a', o) walked with an incremental (a', o) (no integer division)
+    const int pairs = TB >> 1, step = kCons / pairs;
+    const int bp = ctid & (pairs - 1);
+    int al = 0, o = ctid / pairs;
+    while (o >= nout) { o -= nout; ++al; }
+    const uint32_t col_s = epi_s + (uint32_t)(2 * bp * 8);
+    double* t3 = T3 + ((int64_t)ta * TA * nout) * mR + (int64_t)tb * TB + 2 * bp;
+    while (al < TA) {
+      const uint32_t src = col_s + (uint32_t)(al * kL * kFusedEpiPitch * 8);
+      double ax = 0.0, ay = 0.0;
       const int e1 = __ldg(rowptr + o + 1);
       for (int e = __ldg(rowptr + o); e < e1; ++e) {
         const int c = __ldg(col + e);
-        const int w = c / dd, s = c - w * dd;
         const double v = __ldg(val + e);
-        const double2 x = *reinterpret_cast<const double2*>(src + w * kFusedEpiPitch + s * TB);
-        a2.x = fma(v, x.x, a2.x);
-        a2.y = fma(v, x.y, a2.y);
+        double x, y;  // T1 row (a', w = c >> log2dd), column block s = c & (dd - 1)
+        lds128(x, y, src + (uint32_t)((((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB) * 8));
+        ax = fma(v, x, ax);
+        ay = fma(v, y, ay);
       }
-      const int64_t ap = (int64_t)ta * TA + al;
-      *reinterpret_cast<double2*>(T3 + (ap * nout + o) * mR + (int64_t)tb * TB + 2 * bp) = a2;
+      *reinterpret_cast<double2*>(t3 + ((int64_t)al * nout + o) * mR) = make_double2(ax, ay);
+      o += step;
+      while (o >= nout) { o -= nout; ++al; }
     }
   }
 }

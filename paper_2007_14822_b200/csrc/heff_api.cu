@@ -901,7 +901,7 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
     // columns = TB b for each (s1 s2) (d1 d2 TB = 128); used when the tiles make 0.5..1 wave
     {
       const int64_t dd = d.d1 * d.d2;
-      const bool shape_ok = (kFusedBM % d.kL == 0) && (kFusedBN % dd == 0) && (kFusedBN / dd) % 16 == 0 &&
+      const bool shape_ok = (kFusedBM % d.kL == 0) && (dd & (dd - 1)) == 0 && (kFusedBN / dd) % 16 == 0 &&
                             rows == d.mL && (d.mL % 2 == 0) &&
                             (reinterpret_cast<uintptr_t>(L) & 15) == 0;
       if (shape_ok) {
@@ -1213,7 +1213,7 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     CKR(prof_mark(p, 0, s));
     CK(launch_pdl(gemm1_mpo_fused_kernel, dim3((unsigned)std::min(tiles, g_num_sms)), dim3(kFusedThreads),
                   kFusedSmemBytes, s, p->fmapL, p->fmapPsi, p->T3, (int)d.mL, (int)d.mR, (int)d.kL, (int)dd,
-                  p->fusedTA, p->fusedTB, (int)(dd * d.kR), (const int*)p->csrA.d_rowptr, (const int*)p->csrA.d_col,
+                  __builtin_ctz((unsigned)dd), p->fusedTA, p->fusedTB, (int)(dd * d.kR), (const int*)p->csrA.d_rowptr, (const int*)p->csrA.d_col,
                   (const double*)p->csrA.d_val));
     ++*nl;
     CKR(prof_mark(p, 1, s));

@@ -83,6 +83,10 @@ __device__ __forceinline__ void lds128(double& x, double& y, uint32_t addr) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
 }
 
+__device__ __forceinline__ void sts128(uint32_t addr, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
+
 __device__ __forceinline__ double lds64(uint32_t addr) {
   double x;
   asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(x) : "r"(addr));

@@ -326,7 +326,7 @@ def test_kernel_launch_count(dev):
     x = C.make("c2", device=dev)
     with Heff(x.L, x.W1, x.W2, x.R) as h:
         h.apply(x.psi)
-        assert h.get_option(2) >= 3      # GEMM1, fused MPO, GEMM4 (+ split-K reductions)
+        assert h.get_option(2) >= 2      # GEMM1 (+ the MPO when fused), the MPO kernel otherwise, GEMM4
 
 
 def test_relayout_kernel(dev):

@@ -26,7 +26,16 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns
          "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "second": 1.0, "nsecond": 1e-9}
 
 
-def kernel_key(name: str) -> str:
+def kernel_key(name: str, order: str = "A") -> str:
+    if "gemm1_mpo_fused" in name:
+        return "gemm1_mpo_fused_A"
+    if "gemm_cluster_splitk" in name:
+        return "gemm_cluster_splitk"
+    if "mpo_apply_kernel" in name:
+        return f"mpo_{order}"
+    if "gemm_dmma_tma_kernel" in name and order == "B":
+        kmajor = re.search(r"gemm_dmma_tma_kernel<[^>]*,\s*(\d)\s*>", name)
+        return "gemm_first_B" if (kmajor and kmajor.group(1) == "1") else "gemm_last_B"
     if "gemm_dmma_tma_kernel" in name:
         # template args <BM, BN, WM, WN, STAGES, B_KMAJOR>: order A's first GEMM is NN, its last is NT
         kmajor = re.search(r"gemm_dmma_tma_kernel<[^>]*,\s*(\d)\s*>", name)
@@ -80,6 +89,9 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--json", default=str(ROOT / "profiles" / "ncu_summary.json"))
+    ap.add_argument("--order", default="A", choices=["A", "B"], help="matvec order the capture ran (kernel keys)")
+    ap.add_argument("--commit", default=None, help="git commit the captured build was made from")
+    ap.add_argument("--build", default=None, help="libheff.so source hash of the captured build")
     args = ap.parse_args()
     md = [f"# ncu summary {args.tag}\n"]
     js = json.loads(Path(args.json).read_text()) if Path(args.json).exists() else {}
@@ -102,9 +114,10 @@ def main():
             rb = d.get("dram__bytes_read.sum", (None,))[0]
             wb = d.get("dram__bytes_write.sum", (None,))[0]
             if rb is not None and wb is not None and rb == rb and wb == wb:
-                key = kernel_key(d["kernel"])
+                key = kernel_key(d["kernel"], args.order)
                 js[key] = {"dram_bytes_per_launch": rb + wb, "kernel": d["kernel"][:120], "tag": args.tag,
-                           "duration_s": d.get("gpu__time_duration.sum", (None,))[0]}
+                           "duration_s": d.get("gpu__time_duration.sum", (None,))[0],
+                           "commit": args.commit, "build": args.build}
             md.append("")
     out = ROOT / "profiles" / f"{args.tag}_ncu.md"
     out.write_text("\n".join(md) + "\n")
