@@ -249,10 +249,13 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
-// partial[q][b] <- block b's sum over its chunk of V[q][i] w[i], q < j (8 vectors per pass)
+// partial[q][b] <- block b's sum over its chunk of V[q][i] w[i], q < j (8 vectors per pass).
+// Every warp reduces its kDotQ accumulators by shuffles; one barrier per group of 8; the
+// first nq threads add the kStepThreads/32 warp sums in warp order (deterministic).
 __device__ __forceinline__ void chunk_dots(const double* __restrict__ V, int64_t ldv, int j,
                                            const double* __restrict__ w, int64_t lo, int64_t hi,
-                                           double* __restrict__ partial, double* red) {
+                                           double* __restrict__ partial, double (*red)[kStepThreads / 32]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int q0 = 0; q0 < j; q0 += kDotQ) {
     const int nq = min(kDotQ, j - q0);
     double acc[kDotQ];
@@ -267,9 +270,29 @@ __device__ __forceinline__ void chunk_dots(const double* __restrict__ V, int64_t
 #pragma unroll
     for (int q = 0; q < kDotQ; ++q)
       if (q < nq) {
-        const double s = block_sum(acc[q], red);
-        if (threadIdx.x == 0) partial[(q0 + q) * gridDim.x + blockIdx.x] = s;
+        const double v = warp_sum(acc[q]);
+        if (lane == 0) red[q][warp] = v;
       }
+    __syncthreads();
+    if (threadIdx.x < nq) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < kStepThreads / 32; ++k) t += red[threadIdx.x][k];
+      partial[(q0 + threadIdx.x) * gridDim.x + blockIdx.x] = t;
+    }
+    __syncthreads();  // red is reused by the next group
+  }
+}
+
+// Grid-wide sums s[q] = sum_b pp[q][b], q < j, computed identically in every block: warp
+// (q mod warps) adds b = lane, lane + 32, ... then a shuffle tree (fixed order).
+__device__ __forceinline__ void grid_sums(const double* __restrict__ pp, int j, int G, double* s_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = warp; q < j; q += kStepThreads / 32) {
+    double t = 0.0;
+    for (int b = lane; b < G; b += 32) t += __ldcg(pp + (int64_t)q * G + b);
+    t = warp_sum(t);
+    if (lane == 0) s_out[q] = t;
   }
 }
 
@@ -282,7 +305,7 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
                                                                   double* __restrict__ vnext) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double s_c[];  // [j]
-  __shared__ double red[kStepThreads / 32];
+  __shared__ double red[kDotQ][kStepThreads / 32];
   const int G = gridDim.x;
   const int64_t chunk = ((n + G - 1) / G + 1) / 2 * 2;
   const int64_t lo = min(n, (int64_t)blockIdx.x * chunk), hi = min(n, lo + chunk);
@@ -294,13 +317,10 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
     double* cc = pass ? c2 : c1;
     chunk_dots(V, ldv, j, w, lo, hi, pp, red);
     grid.sync();
-    for (int q = threadIdx.x; q < j; q += kStepThreads) {  // same fixed-order sum in every block
-      double s = 0.0;
-      for (int b = 0; b < G; ++b) s += pp[q * G + b];
-      s_c[q] = s;
-      if (blockIdx.x == 0) cc[q] = s;
-    }
+    grid_sums(pp, j, G, s_c);  // the same fixed-order sums in every block
     __syncthreads();
+    if (blockIdx.x == 0)
+      for (int q = threadIdx.x; q < j; q += kStepThreads) cc[q] = s_c[q];
     for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) {
       double x = w[i];
       for (int q = 0; q < j; ++q) x = fma(-s_c[q], V[q * ldv + i], x);
@@ -309,11 +329,12 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
   }
   double acc = 0.0;
   for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) acc = fma(w[i], w[i], acc);
-  const double s = block_sum(acc, red);
+  const double s = block_sum(acc, red[0]);
   if (threadIdx.x == 0) p3[blockIdx.x] = s;
   grid.sync();
-  double nrm2 = 0.0;
-  for (int b = 0; b < G; ++b) nrm2 += p3[b];  // every thread, same order
+  grid_sums(p3, 1, G, s_c);  // fixed order, every block
+  __syncthreads();
+  const double nrm2 = s_c[0];
   const double bt = sqrt(nrm2);
   const double ib = bt > 0.0 ? 1.0 / bt : 0.0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -67,13 +67,15 @@ __device__ __forceinline__ void dmma_stage(double (&acc)[MI][NJ][2], uint32_t sA
 }
 
 // ---- GEMM1 + two-site MPO, fused ---------------------------------------------------------
-constexpr int kFusedBM = 80, kFusedBN = 128, kFusedWM = 40, kFusedWN = 32, kFusedStages = 5;
+constexpr int kFusedBM = 80, kFusedBN = 128, kFusedWM = 40, kFusedWN = 32, kFusedStages = 4;
+constexpr int kFusedCsrMaxRows = 256, kFusedCsrMaxNnz = 1024;  // CSR staged in shared memory up to these
 constexpr int kFusedConsumerWarps = (kFusedBM / kFusedWM) * (kFusedBN / kFusedWN);  // 8
 constexpr int kFusedThreads = (kFusedConsumerWarps + 4) * 32;
 constexpr int kFusedStageBytes = kFusedBM * 128 + kFusedBN * 128;
 constexpr int kFusedEpiPitch = kFusedBN + 4;  // doubles per staged row: conflict-free double2 stores
-constexpr int kFusedSmemBytes =
-    kFusedStages * kFusedStageBytes + kFusedBM * kFusedEpiPitch * 8 + 2 * kFusedStages * 8 + 1024;
+constexpr int kFusedCsrBytes = (kFusedCsrMaxRows + 1) * 4 + kFusedCsrMaxNnz * 12 + 16;
+constexpr int kFusedSmemBytes = kFusedStages * kFusedStageBytes + kFusedBM * kFusedEpiPitch * 8 + kFusedCsrBytes +
+                                2 * kFusedStages * 8 + 1024;
 
 // Tile (ta, tb): T1 rows (a', w) for a' in [ta TA, ta TA + TA) = L rows [ta BM, ta BM + BM)
 // (TA kL == BM), columns (s, b) for s < dd, b in [tb TB, tb TB + TB) (dd TB == BN).
@@ -88,7 +90,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   double* epi = reinterpret_cast<double*>(smem + ST * kFusedStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kFusedBM * kFusedEpiPitch);
+  double* s_val = epi + kFusedBM * kFusedEpiPitch;                       // [nnz] CSR values
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(s_val + kFusedCsrMaxNnz);  // [nnz] byte offsets into a T1 row block
+  int* s_rp = reinterpret_cast<int*>(s_off + kFusedCsrMaxNnz);            // [nout + 1]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * kFusedStageBytes + kFusedBM * kFusedEpiPitch * 8 +
+                                               ((kFusedCsrBytes + 15) & ~15));
   uint64_t* empty = full + ST;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ta_n = mL / TA, tb_n = mR / TB;
@@ -101,7 +107,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     fence_barrier_init();
   }
-  pdl_wait();  // L, psi and T3 only after the previous kernel in the stream
+  pdl_wait();  // L, psi, T3 and the CSR only after the previous kernel in the stream
+  // the CSR (built by a kernel at plan creation) into shared memory, each
+  // entry's column c = (w, s) turned into its byte offset in the staged T1 tile
+  const int nnz = __ldg(rowptr + nout);
+  const bool csr_smem = nout <= kFusedCsrMaxRows && nnz <= kFusedCsrMaxNnz;
+  if (csr_smem) {
+    for (int r = threadIdx.x; r <= nout; r += blockDim.x) s_rp[r] = __ldg(rowptr + r);
+    for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
+      const int c = __ldg(col + e);
+      s_off[e] = (uint32_t)((((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB) * 8);
+      s_val[e] = __ldg(val + e);
+    }
+  }
   __syncthreads();
 
   if (warp >= kFusedConsumerWarps) {
@@ -141,6 +159,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   constexpr int kCons = kFusedConsumerWarps * 32;
   const int ctid = threadIdx.x;  // consumers are threads [0, kCons)
   const uint32_t epi_s = smem_u32(epi);
+  const uint32_t val_s = smem_u32(s_val), off_s = smem_u32(s_off), rp_s = smem_u32(s_rp);
   int stage = 0;
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -179,14 +198,25 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     while (al < TA) {
       const uint32_t src = col_s + (uint32_t)(al * kL * kFusedEpiPitch * 8);
       double ax = 0.0, ay = 0.0;
-      const int e1 = __ldg(rowptr + o + 1);
-      for (int e = __ldg(rowptr + o); e < e1; ++e) {
-        const int c = __ldg(col + e);
-        const double v = __ldg(val + e);
-        double x, y;  // T1 row (a', w = c >> log2dd), column block s = c & (dd - 1)
-        lds128(x, y, src + (uint32_t)((((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB) * 8));
-        ax = fma(v, x, ax);
-        ay = fma(v, y, ay);
+      if (csr_smem) {
+        const int e1 = (int)lds32(rp_s + 4 * (o + 1));
+        for (int e = (int)lds32(rp_s + 4 * o); e < e1; ++e) {
+          double x, y;
+          lds128(x, y, src + lds32(off_s + 4 * e));
+          const double v = lds64(val_s + 8 * e);
+          ax = fma(v, x, ax);
+          ay = fma(v, y, ay);
+        }
+      } else {
+        const int e1 = __ldg(rowptr + o + 1);
+        for (int e = __ldg(rowptr + o); e < e1; ++e) {
+          const int c = __ldg(col + e);
+          const double v = __ldg(val + e);
+          double x, y;  // T1 row (a', w = c >> log2dd), column block s = c & (dd - 1)
+          lds128(x, y, src + (uint32_t)((((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB) * 8));
+          ax = fma(v, x, ax);
+          ay = fma(v, y, ay);
+        }
       }
       *reinterpret_cast<double2*>(t3 + ((int64_t)al * nout + o) * mR) = make_double2(ax, ay);
       o += step;

@@ -48,9 +48,10 @@ def main():
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     res = []
-    for name in args.configs.split(","):
+    for spec in args.configs.split(","):
+        name, _, mm = spec.partition(":")   # "c4:128" = preset c4 at bond cap m = 128
         t0 = time.perf_counter()
-        x = C.make(name, device=dev)
+        x = C.make(name, device=dev, m=int(mm) if mm else None)
         gen_s = time.perf_counter() - t0
         d = x.dims
         flops = C.flops_per_matvec(d)
@@ -73,7 +74,7 @@ def main():
             lz = (time.perf_counter() - t0) / steps * 1e3
         g1f = 2.0 * d["mL"] * d["kL"] * d["mL"] * d["d1"] * d["d2"] * d["mR"]
         g4f = C.gemm_flops_per_matvec(d) - g1f
-        row = {"config": name, **d, "gen_s": round(gen_s, 2), "matvec_ms": ms, "matvecs_per_s": 1e3 / ms,
+        row = {"config": spec, **d, "gen_s": round(gen_s, 2), "matvec_ms": ms, "matvecs_per_s": 1e3 / ms,
                "tflops": flops / ms / 1e9, "frac_peak": flops / ms / 1e9 / PEAK,
                "gemm_first_ms": g1, "mpo_ms": mpo, "gemm_last_ms": g4,
                "gemm_first_tflops": g1f / g1 / 1e9 if g1 else None, "gemm_last_tflops": g4f / g4 / 1e9 if g4 else None,
