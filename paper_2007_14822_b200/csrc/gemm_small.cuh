@@ -107,7 +107,21 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     fence_barrier_init();
   }
-  pdl_wait();  // L, psi, T3 and the CSR only after the previous kernel in the stream
+  __syncthreads();
+  const bool producer = warp == kFusedConsumerWarps && lane == 0;
+  // L (plan input, never written by the previous kernel) for the first stages is requested
+  // before the dependency wait, so it is in flight while the previous kernel drains
+  const int npre = (int)blockIdx.x < tiles ? min(ST, ktiles) : 0;
+  if (producer) {
+    tma_prefetch_desc(&tmL);
+    tma_prefetch_desc(&tmPsi);
+    const int ta0 = (int)blockIdx.x / tb_n;
+    for (int kb = 0; kb < npre; ++kb) {
+      mbar_arrive_expect_tx(&full[kb], kFusedStageBytes);
+      tma_load_2d(smem + kb * kFusedStageBytes, &tmL, &full[kb], kb * kGemmBK, ta0 * kFusedBM);
+    }
+  }
+  pdl_wait();  // psi, T3 and the CSR only after the previous kernel in the stream
   // the CSR (built by a kernel at plan creation) into shared memory, each
   // entry's column c = (w, s) turned into its byte offset in the staged T1 tile
   const int nnz = __ldg(rowptr + nout);
@@ -124,20 +138,22 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 
   if (warp >= kFusedConsumerWarps) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(40));
-    if (warp == kFusedConsumerWarps && lane == 0) {
-      tma_prefetch_desc(&tmL);
-      tma_prefetch_desc(&tmPsi);
+    if (producer) {
       int stage = 0;
       uint32_t phase = 0;
       const int bps = TB / 16;  // 16-column boxes per (s1 s2) block
+      bool first = true;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int ta = tile / tb_n, tb = tile - ta * tb_n;
         for (int kb = 0; kb < ktiles; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          const bool pre = first && kb < npre;  // L already requested before the wait
+          if (!pre) mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* sA = smem + stage * kFusedStageBytes;
           unsigned char* sB = sA + kFusedBM * 128;
-          mbar_arrive_expect_tx(&full[stage], kFusedStageBytes);
-          tma_load_2d(sA, &tmL, &full[stage], kb * kGemmBK, ta * kFusedBM);
+          if (!pre) {
+            mbar_arrive_expect_tx(&full[stage], kFusedStageBytes);
+            tma_load_2d(sA, &tmL, &full[stage], kb * kGemmBK, ta * kFusedBM);
+          }
 #pragma unroll 1
           for (int q = 0; q < kFusedBN / 16; ++q) {
             const int s = q / bps, c = q - s * bps;
@@ -145,6 +161,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           }
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
+        first = false;
       }
     }
     return;
@@ -178,6 +195,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == ST) { stage = 0; phase ^= 1; }
     }
+    // the next kernel (GEMM4) may be scheduled now: its CTAs take the idle SMs and request
+    // their R stages while this epilogue runs (they wait for T3 in griddepcontrol.wait)
+    if (tile + (int)gridDim.x >= tiles) pdl_launch_dependents();
     // the T1 tile -> shared memory (the previous tile's MPO reads are finished)
     consumers_bar(kCons);
 #pragma unroll
@@ -256,7 +276,7 @@ template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR, int CS>
 __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kThreads, 1)
     gemm_cluster_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                double* __restrict__ C, int64_t ldc, int M, int N, int K, int vec_store,
-                               int accumulate) {
+                               int accumulate, int b_static) {
   using Cfg = ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>;
   constexpr int MI = WM / 8, NJ = WN / 8;
   constexpr int kCons = Cfg::kConsumerWarps * 32;
@@ -282,27 +302,40 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
     fence_barrier_init();
   }
   cluster_sync_all();  // rank 0's reduction barrier exists before any peer arrives on it
-  pdl_wait();
+  // Only the producer waits for the previous kernel (griddepcontrol.wait): the consumers read
+  // nothing but TMA-filled stages, and C is written after those, i.e. after the wait.  With
+  // b_static (B is a plan input the previous kernel does not write, e.g. GEMM4's R) the B
+  // halves of the first stages are requested before the wait.
 
   if (warp >= Cfg::kConsumerWarps) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(40));
     if (warp == Cfg::kConsumerWarps && lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
+      auto load_b = [&](unsigned char* sB, uint64_t* bar, int kb) {
+        if constexpr (B_KMAJOR) {
+          tma_load_2d(sB, &tmB, bar, kb * kGemmBK, nb * BN);
+        } else {
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) tma_load_2d(sB + q * 2048, &tmB, bar, nb * BN + q * 16, kb * kGemmBK);
+        }
+      };
+      const int npre = b_static ? min(STAGES, kb1 - kb0) : 0;
+      for (int i = 0; i < npre; ++i) {
+        mbar_arrive_expect_tx(&full[i], Cfg::kStageBytes);
+        load_b(smem + i * Cfg::kStageBytes + BM * 128, &full[i], kb0 + i);
+      }
+      pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
+        const bool pre = kb - kb0 < npre;
+        if (!pre) mbar_wait(&empty[stage], phase ^ 1);
         unsigned char* sA = smem + stage * Cfg::kStageBytes;
         unsigned char* sB = sA + BM * 128;
-        mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+        if (!pre) mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
         tma_load_2d(sA, &tmA, &full[stage], kb * kGemmBK, mb * BM);
-        if constexpr (B_KMAJOR) {
-          tma_load_2d(sB, &tmB, &full[stage], kb * kGemmBK, nb * BN);
-        } else {
-#pragma unroll
-          for (int q = 0; q < BN / 16; ++q) tma_load_2d(sB + q * 2048, &tmB, &full[stage], nb * BN + q * 16, kb * kGemmBK);
-        }
+        if (!pre) load_b(sB, &full[stage], kb);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }

@@ -353,10 +353,10 @@ static int launch_cluster_splitk(GemmOp& g, cudaStream_t s) {
   const int M32 = (int)g.M, N32 = (int)g.N, K32 = (int)g.K;
   if (g.b_kmajor)
     CK(cudaLaunchKernelEx(&cfg, gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, CS>, g.mapA, g.mapB, g.C,
-                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate));
+                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate, g.b_static ? 1 : 0));
   else
     CK(cudaLaunchKernelEx(&cfg, gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, false, CS>, g.mapA, g.mapB, g.C,
-                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate));
+                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate, g.b_static ? 1 : 0));
   return HEFF_OK;
 }
 
@@ -896,6 +896,7 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
     p->g4.B = R;
     p->g4.ldb = d.kR * d.mR;
     p->g4.b_kmajor = true;
+    p->g4.b_static = true;  // R: a borrowed input no kernel of the matvec writes
     p->g4.ldc = d.mR;
     // GEMM1 + MPO fused on fat tiles (gemm_small.cuh): rows = whole a' groups (TA kL = 80),
     // columns = TB b for each (s1 s2) (d1 d2 TB = 128); used when the tiles make 0.5..1 wave

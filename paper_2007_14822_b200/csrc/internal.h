@@ -67,6 +67,7 @@ struct GemmOp {
   double* C = nullptr;
   int64_t ldc = 0;
   int accumulate = 0;  // C += A.B instead of C = A.B
+  bool b_static = false;  // B is never written by the kernel before this GEMM (it may be prefetched early)
   // block-sparse schedule (heff_set_qn): tile order + per-tile k-block lists, device arrays
   const int* sp_order = nullptr;
   const int* sp_ptr = nullptr;
