@@ -69,6 +69,7 @@ __device__ __forceinline__ void dmma_stage(double (&acc)[MI][NJ][2], uint32_t sA
 // ---- GEMM1 + two-site MPO, fused ---------------------------------------------------------
 constexpr int kFusedBM = 80, kFusedBN = 128, kFusedWM = 40, kFusedWN = 32, kFusedStages = 4;
 constexpr int kFusedCsrMaxRows = 256, kFusedCsrMaxNnz = 1024;  // CSR staged in shared memory up to these
+constexpr int kFusedEll = 4;  // ELL row width of the staged two-site MPO (rows with more: CSR form)
 constexpr int kFusedConsumerWarps = (kFusedBM / kFusedWM) * (kFusedBN / kFusedWN);  // 8
 constexpr int kFusedThreads = (kFusedConsumerWarps + 4) * 32;
 constexpr int kFusedStageBytes = kFusedBM * 128 + kFusedBN * 128;
@@ -124,9 +125,24 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   pdl_wait();  // psi, T3 and the CSR only after the previous kernel in the stream
   // the CSR (built by a kernel at plan creation) into shared memory, each
   // entry's column c = (w, s) turned into its byte offset in the staged T1 tile
+  // In ELL form (every row padded to kFusedEll entries of value 0 and offset 0) when no row
+  // has more: the epilogue's inner loop then has a fixed trip count and unrolls.
   const int nnz = __ldg(rowptr + nout);
-  const bool csr_smem = nout <= kFusedCsrMaxRows && nnz <= kFusedCsrMaxNnz;
-  if (csr_smem) {
+  int ell_ok = nout * kFusedEll <= kFusedCsrMaxNnz;
+  for (int r = threadIdx.x; r < nout; r += blockDim.x) ell_ok &= (__ldg(rowptr + r + 1) - __ldg(rowptr + r)) <= kFusedEll;
+  ell_ok = __syncthreads_and(ell_ok);
+  const bool csr_smem = !ell_ok && nout <= kFusedCsrMaxRows && nnz <= kFusedCsrMaxNnz;
+  if (ell_ok) {
+    for (int i = threadIdx.x; i < nout * kFusedEll; i += blockDim.x) {
+      const int r = i / kFusedEll, k = i - r * kFusedEll;
+      const int e = __ldg(rowptr + r) + k;
+      const bool live = e < __ldg(rowptr + r + 1);
+      const int c = live ? __ldg(col + e) : 0;
+      s_off[i] = (uint32_t)((((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB) * 8);
+      s_val[i] = live ? __ldg(val + e) : 0.0;
+    }
+    for (int r = threadIdx.x; r < nout; r += blockDim.x) s_rp[r] = __ldg(rowptr + r + 1) - __ldg(rowptr + r);
+  } else if (csr_smem) {
     for (int r = threadIdx.x; r <= nout; r += blockDim.x) s_rp[r] = __ldg(rowptr + r);
     for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
       const int c = __ldg(col + e);
@@ -215,6 +231,30 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     while (o >= nout) { o -= nout; ++al; }
     const uint32_t col_s = epi_s + (uint32_t)(2 * bp * 8);
     double* t3 = T3 + ((int64_t)ta * TA * nout) * mR + (int64_t)tb * TB + 2 * bp;
+    if (ell_ok) {
+      // fixed-length rows: independent iterations, loads of two rows in flight together
+#pragma unroll 2
+      for (; al < TA;) {
+        const uint32_t src = col_s + (uint32_t)(al * kL * kFusedEpiPitch * 8);
+        const int len = (int)lds32(rp_s + 4 * o);  // entries of row o (<= kFusedEll)
+        double ax = 0.0, ay = 0.0;
+#pragma unroll
+        for (int k = 0; k < kFusedEll; ++k) {
+          if (k < len) {  // predicated: padding is never read (no 0 * Inf)
+            const int i = o * kFusedEll + k;
+            double x, y;
+            lds128(x, y, src + lds32(off_s + 4 * i));
+            const double v = lds64(val_s + 8 * i);
+            ax = fma(v, x, ax);
+            ay = fma(v, y, ay);
+          }
+        }
+        *reinterpret_cast<double2*>(t3 + ((int64_t)al * nout + o) * mR) = make_double2(ax, ay);
+        o += step;
+        while (o >= nout) { o -= nout; ++al; }
+      }
+      continue;
+    }
     while (al < TA) {
       const uint32_t src = col_s + (uint32_t)(al * kL * kFusedEpiPitch * 8);
       double ax = 0.0, ay = 0.0;
