@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                            const double* __restrict__ val) {
   constexpr int MI = kFusedWM / 8, NJ = kFusedWN / 8, ST = kFusedStages;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base by pointer arithmetic on the __shared__ array (keeps the shared
+  // address space visible to the compiler: the epilogue's C++ loads/stores become LDS/STS)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* epi = reinterpret_cast<double*>(smem + ST * kFusedStageBytes);
   double* s_val = epi + kFusedBM * kFusedEpiPitch;                       // [nnz] CSR values
   uint32_t* s_off = reinterpret_cast<uint32_t*>(s_val + kFusedCsrMaxNnz);  // [nnz] byte offsets into a T1 row block
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int e = __ldg(rowptr + r) + k;
       const bool live = e < __ldg(rowptr + r + 1);
       const int c = live ? __ldg(col + e) : 0;
-      s_off[i] = (uint32_t)((((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB) * 8);
+      s_off[i] = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);  // doubles
       s_val[i] = live ? __ldg(val + e) : 0.0;
     }
     for (int r = threadIdx.x; r < nout; r += blockDim.x) s_rp[r] = __ldg(rowptr + r + 1) - __ldg(rowptr + r);
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     for (int r = threadIdx.x; r <= nout; r += blockDim.x) s_rp[r] = __ldg(rowptr + r);
     for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
       const int c = __ldg(col + e);
-      s_off[e] = (uint32_t)((((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB) * 8);
+      s_off[e] = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);  // doubles
       s_val[e] = __ldg(val + e);
     }
   }
@@ -191,8 +193,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const uint32_t offA0 = (wm0 + g) * 128 + ((t ^ g) << 4);
   constexpr int kCons = kFusedConsumerWarps * 32;
   const int ctid = threadIdx.x;  // consumers are threads [0, kCons)
-  const uint32_t epi_s = smem_u32(epi);
-  const uint32_t val_s = smem_u32(s_val), off_s = smem_u32(s_off), rp_s = smem_u32(s_rp);
   int stage = 0;
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
-        sts128(epi_s + (uint32_t)(((wm0 + 8 * i + g) * kFusedEpiPitch + wn0 + 8 * j + 2 * t) * 8), acc[i][j][0],
-               acc[i][j][1]);
+        *reinterpret_cast<double2*>(epi + (wm0 + 8 * i + g) * kFusedEpiPitch + wn0 + 8 * j + 2 * t) =
+            make_double2(acc[i][j][0], acc[i][j][1]);
     consumers_bar(kCons);
     // two-site MPO: T3[a'][o][b] = sum_c Wc[o][c] T1[a'][c][b], c = (w, s); one b-pair per
     // thread, output rows (a', o) walked with an incremental (a', o) (no integer division)
@@ -229,24 +229,23 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     const int bp = ctid & (pairs - 1);
     int al = 0, o = ctid / pairs;
     while (o >= nout) { o -= nout; ++al; }
-    const uint32_t col_s = epi_s + (uint32_t)(2 * bp * 8);
+    const double* col_p = epi + 2 * bp;
     double* t3 = T3 + ((int64_t)ta * TA * nout) * mR + (int64_t)tb * TB + 2 * bp;
     if (ell_ok) {
       // fixed-length rows: independent iterations, loads of two rows in flight together
 #pragma unroll 2
       for (; al < TA;) {
-        const uint32_t src = col_s + (uint32_t)(al * kL * kFusedEpiPitch * 8);
-        const int len = (int)lds32(rp_s + 4 * o);  // entries of row o (<= kFusedEll)
+        const double* src = col_p + al * kL * kFusedEpiPitch;
+        const int len = s_rp[o];  // entries of row o (<= kFusedEll)
         double ax = 0.0, ay = 0.0;
 #pragma unroll
         for (int k = 0; k < kFusedEll; ++k) {
           if (k < len) {  // predicated: padding is never read (no 0 * Inf)
             const int i = o * kFusedEll + k;
-            double x, y;
-            lds128(x, y, src + lds32(off_s + 4 * i));
-            const double v = lds64(val_s + 8 * i);
-            ax = fma(v, x, ax);
-            ay = fma(v, y, ay);
+            const double2 xy = *reinterpret_cast<const double2*>(src + s_off[i]);
+            const double v = s_val[i];
+            ax = fma(v, xy.x, ax);
+            ay = fma(v, xy.y, ay);
           }
         }
         *reinterpret_cast<double2*>(t3 + ((int64_t)al * nout + o) * mR) = make_double2(ax, ay);
@@ -256,26 +255,26 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       continue;
     }
     while (al < TA) {
-      const uint32_t src = col_s + (uint32_t)(al * kL * kFusedEpiPitch * 8);
+      const double* src = col_p + al * kL * kFusedEpiPitch;
       double ax = 0.0, ay = 0.0;
       if (csr_smem) {
-        const int e1 = (int)lds32(rp_s + 4 * (o + 1));
-        for (int e = (int)lds32(rp_s + 4 * o); e < e1; ++e) {
-          double x, y;
-          lds128(x, y, src + lds32(off_s + 4 * e));
-          const double v = lds64(val_s + 8 * e);
-          ax = fma(v, x, ax);
-          ay = fma(v, y, ay);
+        const int e1 = s_rp[o + 1];
+        for (int e = s_rp[o]; e < e1; ++e) {
+          const double2 xy = *reinterpret_cast<const double2*>(src + s_off[e]);
+          const double v = s_val[e];
+          ax = fma(v, xy.x, ax);
+          ay = fma(v, xy.y, ay);
         }
       } else {
         const int e1 = __ldg(rowptr + o + 1);
         for (int e = __ldg(rowptr + o); e < e1; ++e) {
           const int c = __ldg(col + e);
           const double v = __ldg(val + e);
-          double x, y;  // T1 row (a', w = c >> log2dd), column block s = c & (dd - 1)
-          lds128(x, y, src + (uint32_t)((((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB) * 8));
-          ax = fma(v, x, ax);
-          ay = fma(v, y, ay);
+          // T1 row (a', w = c >> log2dd), column block s = c & (dd - 1)
+          const double2 xy =
+              *reinterpret_cast<const double2*>(src + ((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
+          ax = fma(v, xy.x, ax);
+          ay = fma(v, xy.y, ay);
         }
       }
       *reinterpret_cast<double2*>(t3 + ((int64_t)al * nout + o) * mR) = make_double2(ax, ay);
