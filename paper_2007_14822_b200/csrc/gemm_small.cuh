@@ -86,8 +86,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                            double* __restrict__ T3, int mL, int mR, int kL, int dd, int log2dd, int TA, int TB,
                            int nout,
                            const int* __restrict__ rowptr, const int* __restrict__ col,
-                           const double* __restrict__ val) {
+                           const double* __restrict__ val, unsigned long long* __restrict__ dbg) {
+  // dbg (diagnostics, normally null): per CTA, %globaltimer at entry, after the dependency
+  // wait, after the last tile's main loop and at exit (thread 0)
   constexpr int MI = kFusedWM / 8, NJ = kFusedWN / 8, ST = kFusedStages;
+  auto stamp = [&](int k) {
+    if (dbg && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      dbg[blockIdx.x * 4 + k] = t;
+    }
+  };
+  stamp(0);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned base by pointer arithmetic on the __shared__ array (keeps the shared
   // address space visible to the compiler: the epilogue's C++ loads/stores become LDS/STS)
@@ -125,6 +135,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
   }
   pdl_wait();  // psi, T3 and the CSR only after the previous kernel in the stream
+  stamp(1);
   // the CSR (built by a kernel at plan creation) into shared memory, each
   // entry's column c = (w, s) turned into its byte offset in the staged T1 tile
   // In ELL form (every row padded to kFusedEll entries of value 0 and offset 0) when no row
@@ -213,7 +224,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     // the next kernel (GEMM4) may be scheduled now: its CTAs take the idle SMs and request
     // their R stages while this epilogue runs (they wait for T3 in griddepcontrol.wait)
-    if (tile + (int)gridDim.x >= tiles) pdl_launch_dependents();
+    if (tile + (int)gridDim.x >= tiles) {
+      pdl_launch_dependents();
+      stamp(2);
+    }
     // the T1 tile -> shared memory (the previous tile's MPO reads are finished)
     consumers_bar(kCons);
 #pragma unroll
@@ -282,6 +296,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       while (o >= nout) { o -= nout; ++al; }
     }
   }
+  stamp(3);
 }
 
 // ---- GEMM with cluster split-K ------------------------------------------------------------

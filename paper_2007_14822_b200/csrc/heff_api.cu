@@ -163,6 +163,8 @@ using CfgCl4 = ClusterGemmCfg<64, 64, 32, 16, kClStages, 4>;
 
 
 int g_num_sms = 0;
+// diagnostics of the fused small-bond kernel (heff_debug_fused_timestamps): per-CTA timers
+static unsigned long long* g_fused_dbg = nullptr;
 
 
 
@@ -1214,8 +1216,8 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     CKR(prof_mark(p, 0, s));
     CK(launch_pdl(gemm1_mpo_fused_kernel, dim3((unsigned)std::min(tiles, g_num_sms)), dim3(kFusedThreads),
                   kFusedSmemBytes, s, p->fmapL, p->fmapPsi, p->T3, (int)d.mL, (int)d.mR, (int)d.kL, (int)dd,
-                  __builtin_ctz((unsigned)dd), p->fusedTA, p->fusedTB, (int)(dd * d.kR), (const int*)p->csrA.d_rowptr, (const int*)p->csrA.d_col,
-                  (const double*)p->csrA.d_val));
+                  __builtin_ctz((unsigned)dd), p->fusedTA, p->fusedTB, (int)(dd * d.kR), (const int*)p->csrA.d_rowptr,
+                  (const int*)p->csrA.d_col, (const double*)p->csrA.d_val, g_fused_dbg));
     ++*nl;
     CKR(prof_mark(p, 1, s));
     CKR(prof_mark(p, 2, s));
@@ -2366,6 +2368,23 @@ extern "C" int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64
   int nl = 0;
   const cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   return launch_gemm(g, path, cs, &nl, ws_for(t_gemm_ws, cs));
+}
+
+// debug: enable (n > 0: a device buffer of 4 n timers) / read back the fused small-bond
+// kernel's per-CTA %globaltimer stamps (entry, after the dependency wait, after the main
+// loop, exit); host buffer `out` of 4 n values, n = 0 disables
+extern "C" int heff_debug_fused_timestamps(int n, unsigned long long* out) {
+  if (n <= 0) {
+    cudaFree(g_fused_dbg);
+    g_fused_dbg = nullptr;
+    return HEFF_OK;
+  }
+  if (!g_fused_dbg) {
+    CK(cudaMalloc(&g_fused_dbg, sizeof(unsigned long long) * 4 * (size_t)n));
+    CK(cudaMemset(g_fused_dbg, 0, sizeof(unsigned long long) * 4 * (size_t)n));
+  }
+  if (out) CK(cudaMemcpy(out, g_fused_dbg, sizeof(unsigned long long) * 4 * (size_t)n, cudaMemcpyDeviceToHost));
+  return HEFF_OK;
 }
 
 // debug: copy the calling thread's heff_gemm stream-K workspace (partial tiles of its
