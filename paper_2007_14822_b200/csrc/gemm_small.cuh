@@ -69,7 +69,8 @@ __device__ __forceinline__ void dmma_stage(double (&acc)[MI][NJ][2], uint32_t sA
 // ---- GEMM1 + two-site MPO, fused ---------------------------------------------------------
 constexpr int kFusedBM = 80, kFusedBN = 128, kFusedWM = 40, kFusedWN = 32, kFusedStages = 4;
 constexpr int kFusedCsrMaxRows = 256, kFusedCsrMaxNnz = 1024;  // CSR staged in shared memory up to these
-constexpr int kFusedEll = 4;  // ELL row width of the staged two-site MPO (rows with more: CSR form)
+constexpr int kFusedCache = 8;    // CSR entries of a row held in registers by the epilogue (longer rows: loop)
+constexpr int kFusedAlChunk = 4;  // a' per epilogue work unit
 constexpr int kFusedConsumerWarps = (kFusedBM / kFusedWM) * (kFusedBN / kFusedWN);  // 8
 constexpr int kFusedThreads = (kFusedConsumerWarps + 4) * 32;
 constexpr int kFusedStageBytes = kFusedBM * 128 + kFusedBN * 128;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                            double* __restrict__ T3, int mL, int mR, int kL, int dd, int log2dd, int TA, int TB,
                            int nout,
                            const int* __restrict__ rowptr, const int* __restrict__ col,
-                           const double* __restrict__ val, unsigned long long* __restrict__ dbg) {
+                           const double* __restrict__ val, unsigned long long* __restrict__ dbg, int dbg_mode) {
   // dbg (diagnostics, normally null): per CTA, %globaltimer at entry, after the dependency
   // wait, after the last tile's main loop and at exit (thread 0)
   constexpr int MI = kFusedWM / 8, NJ = kFusedWN / 8, ST = kFusedStages;
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     if (dbg && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      dbg[blockIdx.x * 4 + k] = t;
+      dbg[blockIdx.x * 8 + k] = t;
     }
   };
   stamp(0);
@@ -138,24 +139,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   stamp(1);
   // the CSR (built by a kernel at plan creation) into shared memory, each
   // entry's column c = (w, s) turned into its byte offset in the staged T1 tile
-  // In ELL form (every row padded to kFusedEll entries of value 0 and offset 0) when no row
-  // has more: the epilogue's inner loop then has a fixed trip count and unrolls.
   const int nnz = __ldg(rowptr + nout);
-  int ell_ok = nout * kFusedEll <= kFusedCsrMaxNnz;
-  for (int r = threadIdx.x; r < nout; r += blockDim.x) ell_ok &= (__ldg(rowptr + r + 1) - __ldg(rowptr + r)) <= kFusedEll;
-  ell_ok = __syncthreads_and(ell_ok);
-  const bool csr_smem = !ell_ok && nout <= kFusedCsrMaxRows && nnz <= kFusedCsrMaxNnz;
-  if (ell_ok) {
-    for (int i = threadIdx.x; i < nout * kFusedEll; i += blockDim.x) {
-      const int r = i / kFusedEll, k = i - r * kFusedEll;
-      const int e = __ldg(rowptr + r) + k;
-      const bool live = e < __ldg(rowptr + r + 1);
-      const int c = live ? __ldg(col + e) : 0;
-      s_off[i] = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);  // doubles
-      s_val[i] = live ? __ldg(val + e) : 0.0;
-    }
-    for (int r = threadIdx.x; r < nout; r += blockDim.x) s_rp[r] = __ldg(rowptr + r + 1) - __ldg(rowptr + r);
-  } else if (csr_smem) {
+  const bool csr_smem = nout <= kFusedCsrMaxRows && nnz <= kFusedCsrMaxNnz;
+  if (csr_smem) {
     for (int r = threadIdx.x; r <= nout; r += blockDim.x) s_rp[r] = __ldg(rowptr + r);
     for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
       const int c = __ldg(col + e);
@@ -237,63 +223,80 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         *reinterpret_cast<double2*>(epi + (wm0 + 8 * i + g) * kFusedEpiPitch + wn0 + 8 * j + 2 * t) =
             make_double2(acc[i][j][0], acc[i][j][1]);
     consumers_bar(kCons);
-    // two-site MPO: T3[a'][o][b] = sum_c Wc[o][c] T1[a'][c][b], c = (w, s); one b-pair per
-    // thread, output rows (a', o) walked with an incremental (a', o) (no integer division)
-    const int pairs = TB >> 1, step = kCons / pairs;
-    const int bp = ctid & (pairs - 1);
-    int al = 0, o = ctid / pairs;
-    while (o >= nout) { o -= nout; ++al; }
+    if (tile + (int)gridDim.x >= tiles) stamp(4);
+    if (dbg_mode & 2) continue;  // diagnostics: skip the MPO epilogue
+    // two-site MPO: T3[a'][o][b] = sum_c Wc[o][c] T1[a'][c][b], c = (w, s).  A thread owns one
+    // b-pair; work units are (row o, chunk of kFusedAlChunk a'), dealt round-robin to the
+    // kCons / pairs thread groups.  A unit reads its row's CSR entries once (registers, up to
+    // kFusedCache) and applies them to each a' of the chunk: independent iterations, so the
+    // shared loads of several a' are in flight together.
+    const int pairs = TB >> 1, G = kCons / pairs;
+    const int bp = ctid & (pairs - 1), grp = ctid / pairs;
     const double* col_p = epi + 2 * bp;
     double* t3 = T3 + ((int64_t)ta * TA * nout) * mR + (int64_t)tb * TB + 2 * bp;
-    if (ell_ok) {
-      // fixed-length rows: independent iterations, loads of two rows in flight together
-#pragma unroll 2
-      for (; al < TA;) {
-        const double* src = col_p + al * kL * kFusedEpiPitch;
-        const int len = s_rp[o];  // entries of row o (<= kFusedEll)
-        double ax = 0.0, ay = 0.0;
+    const int nq = (TA + kFusedAlChunk - 1) / kFusedAlChunk;
+    for (int u = grp; u < nout * nq; u += G) {
+      const int o = u / nq, al0 = (u - o * nq) * kFusedAlChunk, al1 = min(TA, al0 + kFusedAlChunk);
+      const int e0 = csr_smem ? s_rp[o] : __ldg(rowptr + o);
+      const int e1 = csr_smem ? s_rp[o + 1] : __ldg(rowptr + o + 1);
+      const int n = e1 - e0;
+      double* dst = t3 + (int64_t)o * mR;
+      if (n <= kFusedCache) {
+        uint32_t off[kFusedCache];
+        double v[kFusedCache];
 #pragma unroll
-        for (int k = 0; k < kFusedEll; ++k) {
-          if (k < len) {  // predicated: padding is never read (no 0 * Inf)
-            const int i = o * kFusedEll + k;
-            const double2 xy = *reinterpret_cast<const double2*>(src + s_off[i]);
-            const double v = s_val[i];
-            ax = fma(v, xy.x, ax);
-            ay = fma(v, xy.y, ay);
+        for (int k = 0; k < kFusedCache; ++k) {
+          off[k] = 0;
+          v[k] = 0.0;
+          if (k < n) {
+            if (csr_smem) {
+              off[k] = s_off[e0 + k];
+              v[k] = s_val[e0 + k];
+            } else {
+              const int c = __ldg(col + e0 + k);
+              off[k] = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
+              v[k] = __ldg(val + e0 + k);
+            }
           }
         }
-        *reinterpret_cast<double2*>(t3 + ((int64_t)al * nout + o) * mR) = make_double2(ax, ay);
-        o += step;
-        while (o >= nout) { o -= nout; ++al; }
-      }
-      continue;
-    }
-    while (al < TA) {
-      const double* src = col_p + al * kL * kFusedEpiPitch;
-      double ax = 0.0, ay = 0.0;
-      if (csr_smem) {
-        const int e1 = s_rp[o + 1];
-        for (int e = s_rp[o]; e < e1; ++e) {
-          const double2 xy = *reinterpret_cast<const double2*>(src + s_off[e]);
-          const double v = s_val[e];
-          ax = fma(v, xy.x, ax);
-          ay = fma(v, xy.y, ay);
+#pragma unroll
+        for (int al = al0; al < al0 + kFusedAlChunk; ++al) {
+          if (al < al1) {
+            const double* src = col_p + al * kL * kFusedEpiPitch;
+            double ax = 0.0, ay = 0.0;
+#pragma unroll
+            for (int k = 0; k < kFusedCache; ++k)
+              if (k < n) {
+                const double2 xy = *reinterpret_cast<const double2*>(src + off[k]);
+                ax = fma(v[k], xy.x, ax);
+                ay = fma(v[k], xy.y, ay);
+              }
+            if (!(dbg_mode & 1))
+              *reinterpret_cast<double2*>(dst + (int64_t)al * nout * mR) = make_double2(ax, ay);
+          }
         }
       } else {
-        const int e1 = __ldg(rowptr + o + 1);
-        for (int e = __ldg(rowptr + o); e < e1; ++e) {
-          const int c = __ldg(col + e);
-          const double v = __ldg(val + e);
-          // T1 row (a', w = c >> log2dd), column block s = c & (dd - 1)
-          const double2 xy =
-              *reinterpret_cast<const double2*>(src + ((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
-          ax = fma(v, xy.x, ax);
-          ay = fma(v, xy.y, ay);
+        for (int al = al0; al < al1; ++al) {
+          const double* src = col_p + al * kL * kFusedEpiPitch;
+          double ax = 0.0, ay = 0.0;
+          for (int e = e0; e < e1; ++e) {
+            uint32_t of;
+            double vv;
+            if (csr_smem) {
+              of = s_off[e];
+              vv = s_val[e];
+            } else {
+              const int c = __ldg(col + e);
+              of = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
+              vv = __ldg(val + e);
+            }
+            const double2 xy = *reinterpret_cast<const double2*>(src + of);
+            ax = fma(vv, xy.x, ax);
+            ay = fma(vv, xy.y, ay);
+          }
+          if (!(dbg_mode & 1)) *reinterpret_cast<double2*>(dst + (int64_t)al * nout * mR) = make_double2(ax, ay);
         }
       }
-      *reinterpret_cast<double2*>(t3 + ((int64_t)al * nout + o) * mR) = make_double2(ax, ay);
-      o += step;
-      while (o >= nout) { o -= nout; ++al; }
     }
   }
   stamp(3);

@@ -165,6 +165,7 @@ using CfgCl4 = ClusterGemmCfg<64, 64, 32, 16, kClStages, 4>;
 int g_num_sms = 0;
 // diagnostics of the fused small-bond kernel (heff_debug_fused_timestamps): per-CTA timers
 static unsigned long long* g_fused_dbg = nullptr;
+static int g_fused_dbg_mode = 0;  // 1: no T3 stores, 2: no MPO epilogue (timing experiments; wrong results)
 
 
 
@@ -1217,7 +1218,7 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
     CK(launch_pdl(gemm1_mpo_fused_kernel, dim3((unsigned)std::min(tiles, g_num_sms)), dim3(kFusedThreads),
                   kFusedSmemBytes, s, p->fmapL, p->fmapPsi, p->T3, (int)d.mL, (int)d.mR, (int)d.kL, (int)dd,
                   __builtin_ctz((unsigned)dd), p->fusedTA, p->fusedTB, (int)(dd * d.kR), (const int*)p->csrA.d_rowptr,
-                  (const int*)p->csrA.d_col, (const double*)p->csrA.d_val, g_fused_dbg));
+                  (const int*)p->csrA.d_col, (const double*)p->csrA.d_val, g_fused_dbg, g_fused_dbg_mode));
     ++*nl;
     CKR(prof_mark(p, 1, s));
     CKR(prof_mark(p, 2, s));
@@ -2374,16 +2375,18 @@ extern "C" int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64
 // kernel's per-CTA %globaltimer stamps (entry, after the dependency wait, after the main
 // loop, exit); host buffer `out` of 4 n values, n = 0 disables
 extern "C" int heff_debug_fused_timestamps(int n, unsigned long long* out) {
+  if (const char* e = getenv("HEFF_DEBUG_FUSED_MODE")) g_fused_dbg_mode = atoi(e);
   if (n <= 0) {
+    g_fused_dbg_mode = 0;
     cudaFree(g_fused_dbg);
     g_fused_dbg = nullptr;
     return HEFF_OK;
   }
   if (!g_fused_dbg) {
-    CK(cudaMalloc(&g_fused_dbg, sizeof(unsigned long long) * 4 * (size_t)n));
-    CK(cudaMemset(g_fused_dbg, 0, sizeof(unsigned long long) * 4 * (size_t)n));
+    CK(cudaMalloc(&g_fused_dbg, sizeof(unsigned long long) * 8 * (size_t)n));
+    CK(cudaMemset(g_fused_dbg, 0, sizeof(unsigned long long) * 8 * (size_t)n));
   }
-  if (out) CK(cudaMemcpy(out, g_fused_dbg, sizeof(unsigned long long) * 4 * (size_t)n, cudaMemcpyDeviceToHost));
+  if (out) CK(cudaMemcpy(out, g_fused_dbg, sizeof(unsigned long long) * 8 * (size_t)n, cudaMemcpyDeviceToHost));
   return HEFF_OK;
 }
 
