@@ -69,7 +69,6 @@ __device__ __forceinline__ void dmma_stage(double (&acc)[MI][NJ][2], uint32_t sA
 // ---- GEMM1 + two-site MPO, fused ---------------------------------------------------------
 constexpr int kFusedBM = 80, kFusedBN = 128, kFusedWM = 40, kFusedWN = 32, kFusedStages = 4;
 constexpr int kFusedCsrMaxRows = 256, kFusedCsrMaxNnz = 1024;  // CSR staged in shared memory up to these
-constexpr int kFusedCache = 8;    // CSR entries of a row held in registers by the epilogue (longer rows: loop)
 constexpr int kFusedAlChunk = 4;  // a' per epilogue work unit
 constexpr int kFusedConsumerWarps = (kFusedBM / kFusedWM) * (kFusedBN / kFusedWN);  // 8
 constexpr int kFusedThreads = (kFusedConsumerWarps + 4) * 32;
@@ -227,75 +226,42 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     if (dbg_mode & 2) continue;  // diagnostics: skip the MPO epilogue
     // two-site MPO: T3[a'][o][b] = sum_c Wc[o][c] T1[a'][c][b], c = (w, s).  A thread owns one
     // b-pair; work units are (row o, chunk of kFusedAlChunk a'), dealt round-robin to the
-    // kCons / pairs thread groups.  A unit reads its row's CSR entries once (registers, up to
-    // kFusedCache) and applies them to each a' of the chunk: independent iterations, so the
-    // shared loads of several a' are in flight together.
+    // kCons / pairs thread groups.  The loops are deliberately NOT unrolled: this code runs
+    // once per CTA, cold in the instruction cache, and fetching a large unrolled epilogue
+    // from L2 cost ~5 us per CTA (measured: the same time for every loop shape while the
+    // code was ~11 KB; tools/fused_timeline.py).
     const int pairs = TB >> 1, G = kCons / pairs;
     const int bp = ctid & (pairs - 1), grp = ctid / pairs;
     const double* col_p = epi + 2 * bp;
     double* t3 = T3 + ((int64_t)ta * TA * nout) * mR + (int64_t)tb * TB + 2 * bp;
     const int nq = (TA + kFusedAlChunk - 1) / kFusedAlChunk;
+#pragma unroll 1
     for (int u = grp; u < nout * nq; u += G) {
       const int o = u / nq, al0 = (u - o * nq) * kFusedAlChunk, al1 = min(TA, al0 + kFusedAlChunk);
       const int e0 = csr_smem ? s_rp[o] : __ldg(rowptr + o);
       const int e1 = csr_smem ? s_rp[o + 1] : __ldg(rowptr + o + 1);
-      const int n = e1 - e0;
       double* dst = t3 + (int64_t)o * mR;
-      if (n <= kFusedCache) {
-        uint32_t off[kFusedCache];
-        double v[kFusedCache];
-#pragma unroll
-        for (int k = 0; k < kFusedCache; ++k) {
-          off[k] = 0;
-          v[k] = 0.0;
-          if (k < n) {
-            if (csr_smem) {
-              off[k] = s_off[e0 + k];
-              v[k] = s_val[e0 + k];
-            } else {
-              const int c = __ldg(col + e0 + k);
-              off[k] = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
-              v[k] = __ldg(val + e0 + k);
-            }
+#pragma unroll 1
+      for (int al = al0; al < al1; ++al) {
+        const double* src = col_p + al * kL * kFusedEpiPitch;
+        double ax = 0.0, ay = 0.0;
+#pragma unroll 1
+        for (int e = e0; e < e1; ++e) {
+          uint32_t of;
+          double vv;
+          if (csr_smem) {
+            of = s_off[e];
+            vv = s_val[e];
+          } else {  // T1 row (a', w = c >> log2dd), column block s = c & (dd - 1)
+            const int c = __ldg(col + e);
+            of = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
+            vv = __ldg(val + e);
           }
+          const double2 xy = *reinterpret_cast<const double2*>(src + of);
+          ax = fma(vv, xy.x, ax);
+          ay = fma(vv, xy.y, ay);
         }
-#pragma unroll
-        for (int al = al0; al < al0 + kFusedAlChunk; ++al) {
-          if (al < al1) {
-            const double* src = col_p + al * kL * kFusedEpiPitch;
-            double ax = 0.0, ay = 0.0;
-#pragma unroll
-            for (int k = 0; k < kFusedCache; ++k)
-              if (k < n) {
-                const double2 xy = *reinterpret_cast<const double2*>(src + off[k]);
-                ax = fma(v[k], xy.x, ax);
-                ay = fma(v[k], xy.y, ay);
-              }
-            if (!(dbg_mode & 1))
-              *reinterpret_cast<double2*>(dst + (int64_t)al * nout * mR) = make_double2(ax, ay);
-          }
-        }
-      } else {
-        for (int al = al0; al < al1; ++al) {
-          const double* src = col_p + al * kL * kFusedEpiPitch;
-          double ax = 0.0, ay = 0.0;
-          for (int e = e0; e < e1; ++e) {
-            uint32_t of;
-            double vv;
-            if (csr_smem) {
-              of = s_off[e];
-              vv = s_val[e];
-            } else {
-              const int c = __ldg(col + e);
-              of = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
-              vv = __ldg(val + e);
-            }
-            const double2 xy = *reinterpret_cast<const double2*>(src + of);
-            ax = fma(vv, xy.x, ax);
-            ay = fma(vv, xy.y, ay);
-          }
-          if (!(dbg_mode & 1)) *reinterpret_cast<double2*>(dst + (int64_t)al * nout * mR) = make_double2(ax, ay);
-        }
+        if (!(dbg_mode & 1)) *reinterpret_cast<double2*>(dst + (int64_t)al * nout * mR) = make_double2(ax, ay);
       }
     }
   }
