@@ -241,28 +241,41 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int e0 = csr_smem ? s_rp[o] : __ldg(rowptr + o);
       const int e1 = csr_smem ? s_rp[o + 1] : __ldg(rowptr + o + 1);
       double* dst = t3 + (int64_t)o * mR;
+      if (u == grp && tile + (int)gridDim.x >= tiles) stamp(5);
+      // the chunk's a' are independent accumulators: per CSR entry one (offset, value) load,
+      // then kFusedAlChunk shared loads and FMA pairs in flight together
+      double ax[kFusedAlChunk], ay[kFusedAlChunk];
+#pragma unroll
+      for (int q = 0; q < kFusedAlChunk; ++q) ax[q] = ay[q] = 0.0;
+      const double* src0 = col_p + al0 * kL * kFusedEpiPitch;
+      const int rstride = kL * kFusedEpiPitch;
 #pragma unroll 1
-      for (int al = al0; al < al1; ++al) {
-        const double* src = col_p + al * kL * kFusedEpiPitch;
-        double ax = 0.0, ay = 0.0;
-#pragma unroll 1
-        for (int e = e0; e < e1; ++e) {
-          uint32_t of;
-          double vv;
-          if (csr_smem) {
-            of = s_off[e];
-            vv = s_val[e];
-          } else {  // T1 row (a', w = c >> log2dd), column block s = c & (dd - 1)
-            const int c = __ldg(col + e);
-            of = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
-            vv = __ldg(val + e);
-          }
-          const double2 xy = *reinterpret_cast<const double2*>(src + of);
-          ax = fma(vv, xy.x, ax);
-          ay = fma(vv, xy.y, ay);
+      for (int e = e0; e < e1; ++e) {
+        uint32_t of;
+        double vv;
+        if (csr_smem) {
+          of = s_off[e];
+          vv = s_val[e];
+        } else {  // T1 row (a', w = c >> log2dd), column block s = c & (dd - 1)
+          const int c = __ldg(col + e);
+          of = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
+          vv = __ldg(val + e);
         }
-        if (!(dbg_mode & 1)) *reinterpret_cast<double2*>(dst + (int64_t)al * nout * mR) = make_double2(ax, ay);
+#pragma unroll
+        for (int q = 0; q < kFusedAlChunk; ++q)
+          if (al0 + q < al1) {
+            const double2 xy = *reinterpret_cast<const double2*>(src0 + q * rstride + of);
+            ax[q] = fma(vv, xy.x, ax[q]);
+            ay[q] = fma(vv, xy.y, ay[q]);
+          }
       }
+      if (!(dbg_mode & 1)) {
+#pragma unroll
+        for (int q = 0; q < kFusedAlChunk; ++q)
+          if (al0 + q < al1)
+            *reinterpret_cast<double2*>(dst + (int64_t)(al0 + q) * nout * mR) = make_double2(ax[q], ay[q]);
+      }
+      if (u == grp && tile + (int)gridDim.x >= tiles) stamp(6);
     }
   }
   stamp(3);
@@ -299,7 +312,17 @@ template <int BM, int BN, int WM, int WN, int STAGES, bool B_KMAJOR, int CS>
 __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kThreads, 1)
     gemm_cluster_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                double* __restrict__ C, int64_t ldc, int M, int N, int K, int vec_store,
-                               int accumulate, int b_static) {
+                               int accumulate, int b_static, unsigned long long* __restrict__ dbg) {
+  // dbg (diagnostics, normally null): per CTA %globaltimer at entry, first stage ready, end of
+  // the main loop, after the partial push / reduction, exit (consumer thread 0)
+  auto stamp = [&](int kk) {
+    if (dbg && threadIdx.x == 0) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      dbg[blockIdx.x * 8 + kk] = tt;
+    }
+  };
+  stamp(0);
   using Cfg = ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>;
   constexpr int MI = WM / 8, NJ = WN / 8;
   constexpr int kCons = Cfg::kConsumerWarps * 32;
@@ -381,6 +404,7 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
   uint32_t phase = 0;
   for (int kb = kb0; kb < kb1; ++kb) {
     mbar_wait(&full[stage], phase);
+    if (kb == kb0) stamp(1);
     const uint32_t sA = smem_base + stage * Cfg::kStageBytes;
     dmma_stage<MI, NJ, B_KMAJOR>(acc, sA, sA + BM * 128, offA0, offB0, wn0, g, t);
     fence_proxy_async();
@@ -389,6 +413,7 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
     if (++stage == STAGES) { stage = 0; phase ^= 1; }
   }
   const int ctid = threadIdx.x;
+  stamp(2);
   if (rank != 0) {
     // push the partial into rank 0's slot (rank - 1), then arrive on rank 0's barrier
     const uint32_t dst = mapa_shared(smem_u32(slots + (size_t)(rank - 1) * (BM * BN / 2)), 0);
@@ -402,6 +427,7 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
       }
     const uint32_t rb = mapa_shared(smem_u32(red), 0);
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+    stamp(3);
     return;
   }
   // rank 0: wait for the CS - 1 partials, sum in rank order, store
@@ -413,6 +439,7 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
         "@!P1 bra WAIT_%=;\n}\n" ::"r"(rb)
         : "memory");
   }
+  stamp(3);
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     const int row = mb * BM + wm0 + 8 * i + g;
@@ -441,6 +468,7 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
       }
     }
   }
+  stamp(4);
 }
 
 }  // namespace heff

@@ -156,6 +156,7 @@ using CfgNT = TmaGemmCfg<kBM, kBN, kWM, kWN, kStages, true>;
 using CfgNNs = TmaGemmCfg<kBMs, kBNs, kWMs, kWNs, kStagesS, false>;
 using CfgNTs = TmaGemmCfg<kBMs, kBNs, kWMs, kWNs, kStagesS, true>;
 // cluster split-K (gemm_small.cuh): 64x64 tiles, 6-stage ring, CS = 2 or 4 CTAs per tile
+static unsigned long long* g_cluster_dbg = nullptr;  // diagnostics (heff_debug_fused_timestamps)
 constexpr int kClStages = 6;
 using CfgCl2 = ClusterGemmCfg<64, 64, 32, 16, kClStages, 2>;
 using CfgCl4 = ClusterGemmCfg<64, 64, 32, 16, kClStages, 4>;
@@ -356,10 +357,12 @@ static int launch_cluster_splitk(GemmOp& g, cudaStream_t s) {
   const int M32 = (int)g.M, N32 = (int)g.N, K32 = (int)g.K;
   if (g.b_kmajor)
     CK(cudaLaunchKernelEx(&cfg, gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, CS>, g.mapA, g.mapB, g.C,
-                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate, g.b_static ? 1 : 0));
+                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate, g.b_static ? 1 : 0,
+                          g_cluster_dbg));
   else
     CK(cudaLaunchKernelEx(&cfg, gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, false, CS>, g.mapA, g.mapB, g.C,
-                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate, g.b_static ? 1 : 0));
+                          (int64_t)g.ldc, M32, N32, K32, vec, g.accumulate, g.b_static ? 1 : 0,
+                          g_cluster_dbg));
   return HEFF_OK;
 }
 
@@ -2380,12 +2383,14 @@ extern "C" int heff_debug_fused_timestamps(int n, unsigned long long* out) {
     g_fused_dbg_mode = 0;
     cudaFree(g_fused_dbg);
     g_fused_dbg = nullptr;
+    g_cluster_dbg = nullptr;
     return HEFF_OK;
   }
   if (!g_fused_dbg) {
     CK(cudaMalloc(&g_fused_dbg, sizeof(unsigned long long) * 8 * (size_t)n));
     CK(cudaMemset(g_fused_dbg, 0, sizeof(unsigned long long) * 8 * (size_t)n));
   }
+  if (!g_cluster_dbg) g_cluster_dbg = g_fused_dbg + 8 * (size_t)(n / 2);  // second half: the cluster GEMM
   if (out) CK(cudaMemcpy(out, g_fused_dbg, sizeof(unsigned long long) * 8 * (size_t)n, cudaMemcpyDeviceToHost));
   return HEFF_OK;
 }
