@@ -5,6 +5,8 @@
 #include <cooperative_groups.h>
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace cg = cooperative_groups;
 
 namespace heff {
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
                                                                   double* __restrict__ vnext) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double s_c[];  // [j]
+  pdl_wait();  // w comes from the matvec kernel before (launched with programmatic serialization)
   __shared__ double red[kDotQ][kStepThreads / 32];
   const int G = gridDim.x;
   const int64_t chunk = ((n + G - 1) / G + 1) / 2 * 2;

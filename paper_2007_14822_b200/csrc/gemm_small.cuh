@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
   }
   const int ctid = threadIdx.x;
   stamp(2);
+  pdl_launch_dependents();  // the next kernel's launch overlaps this reduction and store
   if (rank != 0) {
     // push the partial into rank 0's slot (rank - 1), then arrive on rank 0's barrier
     const uint32_t dst = mapa_shared(smem_u32(slots + (size_t)(rank - 1) * (BM * BN / 2)), 0);

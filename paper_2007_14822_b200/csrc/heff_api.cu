@@ -2017,8 +2017,22 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       int64_t nn = n;
       double* wp = w;
       void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &alpha, &beta, &invb, &vnext};
-      CK(cudaLaunchCooperativeKernel((const void*)cgs2_step_kernel, dim3(step_grid), dim3(kStepThreads), args,
-                                     sizeof(double) * (size_t)j, s));
+      // cooperative (grid syncs) and, unless HEFF_NO_PDL, programmatic serialization: the
+      // launch overlaps the matvec's last kernel, the body starts after griddepcontrol.wait
+      static const bool pdl_off = getenv("HEFF_NO_PDL") != nullptr;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(step_grid);
+      cfg.blockDim = dim3(kStepThreads);
+      cfg.dynamicSmemBytes = sizeof(double) * (size_t)j;
+      cfg.stream = s;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = pdl_off ? 0 : 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      CK(cudaLaunchKernelExC(&cfg, (const void*)cgs2_step_kernel, args));
       ++p->total_launches;
       return HEFF_OK;
     }
