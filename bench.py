@@ -215,14 +215,17 @@ def spawn_ranks(n: int, check_devices: bool = True) -> int:
 
 
 def load_ncu_traffic(kernel_key: str):
+    """DRAM bytes per launch of the dominant kernel from one `ncu --set full` capture
+    (profiles/ncu_summary.json, written by tools/ncu_summarize.py) and where they come from."""
     f = ROOT / "profiles" / "ncu_summary.json"
     if not f.exists():
-        return None
+        return None, None
     try:
-        d = json.loads(f.read_text())
-        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+        e = json.loads(f.read_text()).get(kernel_key, {})
+        src = f"profiles/{e.get('tag')}_ncu.md (ncu --set full, build of commit {e.get('commit')})" if e else None
+        return e.get("dram_bytes_per_launch"), src
     except Exception:
-        return None
+        return None, None
 
 
 def main():
@@ -370,9 +373,10 @@ def main():
     achieved = dom[2] / (per_launch_ms / 1e3) / 1e12 if per_launch_ms > 0 else None
     kernel_names = {"gemm_first": "gemm_dmma_tma_kernel NT (psi.R_g^T)" if sharded else "gemm_dmma_tma_kernel NN (L.psi)",
                     "gemm_last": "gemm_dmma_tma_kernel NN (L.V3)" if sharded else "gemm_dmma_tma_kernel NT (T3.R^T)"}
+    traffic, traffic_src = load_ncu_traffic(dom[0] + ("_B" if sharded else "_A"))
     roofline = {"bound": "tensor", "kernel": kernel_names[dom[0]], "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
-                "traffic": load_ncu_traffic(dom[0] + ("_B" if sharded else "_A")),
+                "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": "derived FP64 DMMA peak 148 SM x 128 flop/clk x 1.965 GHz = 37.2 TF/s (no FP64 entry "
                                "in MEASURED_PEAKS.json); DMMA microbenchmark 37.16 TF/s sustained",
                 "per_launch_ms": per_launch_ms,
