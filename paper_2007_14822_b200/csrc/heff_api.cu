@@ -1670,13 +1670,10 @@ static int comm_abort(heff_plan_s* p, const char* fmt, ...) {
   return set_err(HEFF_ENCCL, "%s (communicator aborted; destroy the plan)", buf);
 }
 
-static double nccl_timeout_s() {
-  static const double t = [] {
-    const char* e = getenv("HEFF_NCCL_TIMEOUT_S");
-    const double v = e ? atof(e) : 300.0;
-    return v > 0 ? v : 300.0;
-  }();
-  return t;
+static double nccl_timeout_s() {  // read per wait (tests lower it at run time)
+  const char* e = getenv("HEFF_NCCL_TIMEOUT_S");
+  const double v = e ? atof(e) : 300.0;
+  return v > 0 ? v : 300.0;
 }
 
 // Record "Lanczos step done" on s (progress marker for comm_wait).
@@ -1992,7 +1989,13 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs2_step_kernel, kStepThreads,
                                                      sizeof(double) * (size_t)cap));
-    const int64_t want = std::max<int64_t>(1, (n + 4 * kStepThreads - 1) / (4 * kStepThreads));
+    // elements per thread (HEFF_STEP_EPT, default 2; round 1: 4): fewer = more blocks in
+    // flight (C1 41.6 -> 37.5 us, cylinder m = 128 91 -> 78-82 us per Lanczos step)
+    static const int ept = [] {
+      const char* e = getenv("HEFF_STEP_EPT");
+      return e ? std::max(1, atoi(e)) : 2;
+    }();
+    const int64_t want = std::max<int64_t>(1, (n + (int64_t)ept * kStepThreads - 1) / ((int64_t)ept * kStepThreads));
     step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * g_num_sms, want));
   }
   auto step = [&](int j) -> int {  // j = 1-based step: v_j = V[j-1]

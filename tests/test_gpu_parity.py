@@ -477,3 +477,29 @@ def test_fused_gemm1_mpo_matvec(dev, orc, case, env, monkeypatch):
     assert torch.equal(out, out2)
     if case in ("c2", "cyl128", "uneven") and env != "0":
         assert nl == 2, nl                 # fused GEMM1+MPO, GEMM4
+
+
+def test_comm_failure_detection_aborts(dev, monkeypatch):
+    """Failure detection of communicating plans: a stream that makes no
+    progress for HEFF_NCCL_TIMEOUT_S makes lanczos_ground abort the communicator
+    (ncclCommAbort) and return HEFF_ENCCL; the plan is then unusable (comm state -1, later
+    calls fail fast) and can be destroyed.  Simulated on one GPU by a ~3 s spin kernel queued
+    ahead of the solve on the same stream with a 1 s timeout."""
+    from paper_2007_14822_b200 import Heff, nccl_unique_id
+    from paper_2007_14822_b200.heff import OPT_COMM_STATE, HeffError
+    x = C.make("c1").to(dev)
+    h = Heff(x.L, x.W1, x.W2, x.R, dist=dict(nranks=1, rank=0, b_lo=0, b_hi=x.R.shape[0], uid=nccl_unique_id()))
+    try:
+        h.lanczos_ground(x.psi.clone(), max_iter=4)          # healthy first
+        assert h.get_option(OPT_COMM_STATE) == 1
+        monkeypatch.setenv("HEFF_NCCL_TIMEOUT_S", "1")
+        torch.cuda._sleep(int(3.0 * 2.0e9))                    # ~3 s of spinning at ~2 GHz
+        with pytest.raises(HeffError) as ei:
+            h.lanczos_ground(x.psi.clone(), max_iter=4)
+        assert ei.value.code == -4 and "aborted" in str(ei.value)
+        assert h.get_option(OPT_COMM_STATE) == -1
+        with pytest.raises(HeffError):
+            h.lanczos_ground(x.psi.clone(), max_iter=4)
+        torch.cuda.synchronize()
+    finally:
+        h.close()
