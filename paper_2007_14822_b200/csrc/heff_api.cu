@@ -588,6 +588,8 @@ struct heff_plan_s {
   std::string comm_err;
   int force_allgather = 0;                  // option HEFF_OPT_FORCE_ALLGATHER (1 rank: run the P>1 branch)
   std::vector<cudaEvent_t> step_ev;         // recorded after each Lanczos step (progress of a wait)
+  double* hpin = nullptr;                   // pinned host scalars of lanczos_ground: device->host
+  size_t hpin_n = 0;                        // copies stay asynchronous, so every wait is a poll
   int step_ev_used = 0;
   // e2e staging; the overlapped host path's copy stream and chunk events
   double *stage_in = nullptr, *stage_out = nullptr;
@@ -798,6 +800,7 @@ extern "C" int heff_destroy(heff_plan p) {
     cudaEventDestroy(p->setup_ev);
   }
   for (auto& e : p->step_ev) cudaEventDestroy(e);
+  if (p->hpin) cudaFreeHost(p->hpin);
   // an aborted communicator (comm == nullptr, comm_dead) is gone with its window handles:
   // only the local allocation is freed (deregistration is collective and would wait for
   // the dead peers)
@@ -1892,6 +1895,16 @@ static int lanczos_workspace(heff_plan_s* p, int cap, cudaStream_t s, LanczosLay
     p->basis_cap = fgather ? 0 : cap;  // a later non-fused call reallocates the full basis
     p->ldv = ldv;
   }
+  if (p->hpin_n < (size_t)(3 * cap + 4)) {  // alpha, beta, y, norm
+    if (p->hpin) {
+      CK(cudaStreamSynchronize(s));
+      cudaFreeHost(p->hpin);
+      p->hpin = nullptr;
+      p->hpin_n = 0;
+    }
+    CK(cudaMallocHost(&p->hpin, sizeof(double) * (size_t)(3 * cap + 4)));
+    p->hpin_n = (size_t)(3 * cap + 4);
+  }
   if (!p->work || p->work_len < ldv) {
     CK(cudaStreamSynchronize(s));
     ws_release(p->work);
@@ -1968,9 +1981,13 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     CK(cudaMemcpyAsync(V, psi, sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
   }
   CKR(norm2(p, V, nr, beta + cap, invb + cap, s));
-  double h_nrm = 0.0;
-  CK(cudaMemcpyAsync(&h_nrm, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
+  double* h_a = p->hpin;                 // pinned: the copies below never block the host,
+  double* h_b = h_a + cap;               // comm_wait polls (failure detection)
+  double* h_y = h_b + cap;
+  double* h_n = h_y + cap;
+  CK(cudaMemcpyAsync(h_n, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
   CKR(comm_wait(p, s));
+  const double h_nrm = *h_n;
   if (!(h_nrm > 0.0)) return set_err(HEFF_EZERO, "lanczos_ground: zero start vector");
   scale_kernel<<<ew_grid(nr), 256, 0, s>>>(V, invb + cap, V, nr);
   ++p->total_launches;
@@ -2080,9 +2097,11 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       CKR(step(j));
       CKR(mark_step(p, s));
     }
-    CK(cudaMemcpyAsync(ha.data(), alpha, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hb.data(), beta, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_a, alpha, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h_b, beta, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
     CKR(comm_wait(p, s));
+    memcpy(ha.data(), h_a, sizeof(double) * cap);
+    memcpy(hb.data(), h_b, sizeof(double) * cap);
     for (int j = 1; j <= cap; ++j) {
       j_done = j;
       if (host_check(j)) break;
@@ -2101,9 +2120,11 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
         CKR(step(jj));
         CKR(mark_step(p, s));
       }
-      CK(cudaMemcpyAsync(&ha[j - 1], alpha + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(&hb[j - 1], beta + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(h_a + (j - 1), alpha + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(h_b + (j - 1), beta + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
       CKR(comm_wait(p, s));
+      memcpy(&ha[j - 1], h_a + (j - 1), sizeof(double) * (j1 - j + 1));
+      memcpy(&hb[j - 1], h_b + (j - 1), sizeof(double) * (j1 - j + 1));
       for (int jj = j; jj <= j1; ++jj) {
         j_done = jj;
         if (host_check(jj)) {
@@ -2120,7 +2141,8 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   std::vector<double> y(j_done);
   if (!tridiag_lowest_vec(j_done, ha.data(), hb.data(), &theta, y.data()))
     return set_err(HEFF_ECUDA, "lanczos_ground: tridiagonal QL did not converge");
-  CK(cudaMemcpyAsync(ydev, y.data(), sizeof(double) * j_done, cudaMemcpyHostToDevice, s));
+  memcpy(h_y, y.data(), sizeof(double) * j_done);
+  CK(cudaMemcpyAsync(ydev, h_y, sizeof(double) * j_done, cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(w, 0, sizeof(double) * nr, s));
   CKR(multiaxpy(p, V, j_done, ydev, 1.0, w, nr, s));   // real y: also right for complex V
   CKR(norm2(p, w, nr, beta + cap, invb + cap, s));
@@ -2137,8 +2159,10 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   CKR(comm_wait(p, s));
   if (fgather) {
     p->epoch += (uint64_t)cap + 1;
+    CK(cudaMemcpyAsync(h_n, d_timeout, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));  // the stream already drained (comm_wait above)
     int to = 0;
-    CK(cudaMemcpy(&to, d_timeout, sizeof(int), cudaMemcpyDeviceToHost));
+    memcpy(&to, h_n, sizeof(int));
     // a rank that timed out cannot resynchronise its flag epoch with peers that went on:
     // abort, so every rank's next collective fails instead of reading stale slots
     if (to) return comm_abort(p, "lanczos_ground: a peer never published its Krylov vector (20 s timeout)");
