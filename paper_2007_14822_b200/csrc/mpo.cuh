@@ -78,14 +78,31 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_apply_kernel(MpoIO io, const 
     const int pl = r >= nin_p;
     return in0 + pl * io.in_plane + (int64_t)(r - pl * nin_p) * io.in_row;
   };
-  auto out_row = [&](int o) {
-    int pl = 0;
-    if (PLANES == 2) {
-      pl = o >= nout_p;
-      o -= pl * nout_p;
+  // output row address of row o: the rows a thread writes advance by a fixed step, so the
+  // (plane, group, row-in-group) position is tracked incrementally -- no integer division per
+  // row (an issue-bound kernel: a division per row cost 16% at C4)
+  struct RowPos {
+    int pl, q, g, rr;  // plane, row within the plane = g out_grp + rr
+  };
+  auto row_pos = [&](int o) {  // o: row over all planes
+    RowPos r;
+    r.pl = (PLANES == 2 && o >= nout_p) ? 1 : 0;
+    r.q = o - r.pl * nout_p;
+    r.g = r.q / io.out_grp;
+    r.rr = r.q - r.g * io.out_grp;
+    return r;
+  };
+  auto advance = [&](RowPos& r, int step) {
+    r.q += step;
+    r.rr += step;
+    while (r.rr >= io.out_grp) {
+      r.rr -= io.out_grp;
+      ++r.g;
     }
-    const int g = o / io.out_grp, rr = o - g * io.out_grp;
-    return out0 + pl * io.out_plane + g * io.out_grp_stride + (int64_t)rr * io.out_row;
+    if (PLANES == 2 && r.pl == 0 && r.q >= nout_p) r = row_pos(r.q);  // into the imaginary plane (once)
+  };
+  auto out_row = [&](const RowPos& r) {
+    return out0 + r.pl * io.out_plane + (int64_t)r.g * io.out_grp_stride + (int64_t)r.rr * io.out_row;
   };
   const bool even = ((io.in_row | io.in_blk | io.in_plane | width) & 1) == 0 &&
                     (reinterpret_cast<uintptr_t>(io.in) & 15) == 0;
@@ -117,7 +134,8 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_apply_kernel(MpoIO io, const 
     constexpr int kPairs = TC / 2, kStep = kMpoThreads / kPairs;
     const int c2 = 2 * (threadIdx.x % kPairs);
     if (c2 >= width) return;
-    for (int o = threadIdx.x / kPairs; o < nout; o += kStep) {
+    RowPos rp = row_pos(threadIdx.x / kPairs);
+    for (int o = threadIdx.x / kPairs; o < nout; o += kStep, advance(rp, kStep)) {
       double2 acc = make_double2(0.0, 0.0);
       const int e1 = __ldg(rowptr + o + 1);
       for (int e = __ldg(rowptr + o); e < e1; ++e) {
@@ -126,17 +144,18 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_apply_kernel(MpoIO io, const 
         acc.x = fma(v, xin.x, acc.x);
         acc.y = fma(v, xin.y, acc.y);
       }
-      __stcs(reinterpret_cast<double2*>(out_row(o) + c2), acc);
+      __stcs(reinterpret_cast<double2*>(out_row(rp) + c2), acc);
     }
     return;
   }
   const int t = threadIdx.x % TC;
   if (t >= width) return;
-  for (int o = threadIdx.x / TC; o < nout; o += kMpoThreads / TC) {
+  RowPos rp = row_pos(threadIdx.x / TC);
+  for (int o = threadIdx.x / TC; o < nout; o += kMpoThreads / TC, advance(rp, kMpoThreads / TC)) {
     double acc = 0.0;
     const int e1 = __ldg(rowptr + o + 1);
     for (int e = __ldg(rowptr + o); e < e1; ++e) acc = fma(__ldg(val + e), s_in[__ldg(col + e) * TC + t], acc);
-    __stcs(out_row(o) + t, acc);
+    __stcs(out_row(rp) + t, acc);
   }
 }
 
