@@ -435,14 +435,18 @@ int init_device_once() {
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNNs::kSmemBytes));
   CK(cudaFuncSetAttribute(gemm_dmma_tma_sharded_kernel<kBMs, kBNs, kWMs, kWNs, kStagesS, true>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgNTs::kSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
-  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<1, 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
+  CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
   CK(cudaFuncSetAttribute(heff_small_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallMvMaxSmem));
   CK(cudaFuncSetAttribute(gemm1_mpo_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemBytes));
   CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, false, 2>,
@@ -1135,7 +1139,7 @@ extern "C" int heff_last_timings(heff_plan p, float* g1, float* mpo, float* g4, 
 
 // One MPO application (mpo_apply_kernel; column tile `tc` from mpo_tile_cols): `nblk`
 // blocks along y (a' for order A / environments, a for order B).
-template <int PL>
+template <int PL, bool GR>
 static int launch_mpo(const MpoIO& io, int tc, int64_t nblk, const Csr& csr, const unsigned char* live, cudaStream_t s) {
   if (nblk <= 0 || io.ncol <= 0) return HEFF_OK;
   if (nblk > 65535) return set_err(HEFF_EUNSUPPORTED, "MPO kernel: %lld blocks along y", (long long)nblk);
@@ -1145,10 +1149,10 @@ static int launch_mpo(const MpoIO& io, int tc, int64_t nblk, const Csr& csr, con
   const int* cl = csr.d_col;
   const double* vl = csr.d_val;
   switch (tc) {
-    case 128: CK(launch_pdl(mpo_apply_kernel<PL, 128>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
-    case 64: CK(launch_pdl(mpo_apply_kernel<PL, 64>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
-    case 32: CK(launch_pdl(mpo_apply_kernel<PL, 32>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
-    case 16: CK(launch_pdl(mpo_apply_kernel<PL, 16>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
+    case 128: CK(launch_pdl(mpo_apply_kernel<PL, 128, GR>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
+    case 64: CK(launch_pdl(mpo_apply_kernel<PL, 64, GR>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
+    case 32: CK(launch_pdl(mpo_apply_kernel<PL, 32, GR>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
+    case 16: CK(launch_pdl(mpo_apply_kernel<PL, 16, GR>, grid, dim3(kMpoThreads), smem, s, io, rp, cl, vl, live)); break;
     default: return set_err(HEFF_EUNSUPPORTED, "MPO kernel: %d input rows exceed the shared-memory tile", io.nin);
   }
   return HEFF_OK;
@@ -1173,7 +1177,7 @@ static MpoIO mpo_io_A(const double* in, double* out, int64_t ncol, int nin, int 
 
 static int launch_mpo_A(const double* T1, double* T3, int64_t mR, int64_t rows, int nin, int nout, const Csr& csr,
                         const unsigned char* live, int tc, cudaStream_t s) {
-  return launch_mpo<1>(mpo_io_A(T1, T3, mR, nin, nout), tc, rows, csr, live, s);
+  return launch_mpo<1, false>(mpo_io_A(T1, T3, mR, nin, nout), tc, rows, csr, live, s);
 }
 
 // --------------------------------------------------------------------------- the matvec
@@ -1298,7 +1302,7 @@ static int apply_orderB(heff_plan_s* p, const double* psi, double* out, cudaStre
     io.out_row = p->nb;
     io.out_grp = dd;
     io.out_grp_stride = d.mL * dd * p->nb;
-    CKR(launch_mpo<1>(io, p->tcB, d.mL, p->csrB, nullptr, s));
+    CKR((launch_mpo<1, true>(io, p->tcB, d.mL, p->csrB, nullptr, s)));
   }
   ++*nl;
   CKR(prof_mark(p, 2, s));
@@ -1343,7 +1347,7 @@ static int apply_orderA_z(heff_plan_s* p, const double* psi, double* out, cudaSt
       io.out_blk = nout / 2 * d.mR;
       io.out_plane = p->t3_plane;
       io.out_grp = (int)(nout / 2);
-      CKR(launch_mpo<2>(io, p->tcA, rows, p->csrA, nullptr, s));
+      CKR((launch_mpo<2, false>(io, p->tcA, rows, p->csrA, nullptr, s)));
     }
     ++*nl;
     CKR(prof_mark(p, 2, s));

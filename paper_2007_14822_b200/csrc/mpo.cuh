@@ -53,7 +53,10 @@ struct MpoIO {
   int out_grp;
 };
 
-template <int PLANES, int TC>
+// GROUPED: output rows scattered in groups (order B); otherwise one row pitch (order A,
+// environments, complex planes) -- the kernel is issue-bound, so the common case carries no
+// per-row group bookkeeping.
+template <int PLANES, int TC, bool GROUPED>
 __global__ void __launch_bounds__(kMpoThreads) mpo_apply_kernel(MpoIO io, const int* __restrict__ rowptr,
                                                                  const int* __restrict__ col,
                                                                  const double* __restrict__ val,
@@ -88,20 +91,23 @@ __global__ void __launch_bounds__(kMpoThreads) mpo_apply_kernel(MpoIO io, const 
     RowPos r;
     r.pl = (PLANES == 2 && o >= nout_p) ? 1 : 0;
     r.q = o - r.pl * nout_p;
-    r.g = r.q / io.out_grp;
+    r.g = GROUPED ? r.q / io.out_grp : 0;
     r.rr = r.q - r.g * io.out_grp;
     return r;
   };
   auto advance = [&](RowPos& r, int step) {
     r.q += step;
-    r.rr += step;
-    while (r.rr >= io.out_grp) {
-      r.rr -= io.out_grp;
-      ++r.g;
+    if (GROUPED) {
+      r.rr += step;
+      while (r.rr >= io.out_grp) {
+        r.rr -= io.out_grp;
+        ++r.g;
+      }
     }
     if (PLANES == 2 && r.pl == 0 && r.q >= nout_p) r = row_pos(r.q);  // into the imaginary plane (once)
   };
   auto out_row = [&](const RowPos& r) {
+    if (!GROUPED) return out0 + r.pl * io.out_plane + (int64_t)r.q * io.out_row;
     return out0 + r.pl * io.out_plane + (int64_t)r.g * io.out_grp_stride + (int64_t)r.rr * io.out_row;
   };
   const bool even = ((io.in_row | io.in_blk | io.in_plane | width) & 1) == 0 &&
