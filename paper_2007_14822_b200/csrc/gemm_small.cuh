@@ -36,11 +36,13 @@ namespace heff {
 template <int MI, int NJ, bool B_KMAJOR>
 __device__ __forceinline__ void dmma_stage(double (&acc)[MI][NJ][2], uint32_t sA, uint32_t sB, uint32_t offA0,
                                            uint32_t offB0, int wn0, int g, int t) {
+  // Program order = issue order (the loads and DMMAs are asm volatile): the B fragments
+  // first, then each A fragment right before the k-slice-0 DMMAs that use it, so the first
+  // DMMA waits for one A load instead of all of them; the k-slice-1 DMMAs follow
+  // (every accumulator's two updates stay MI*NJ DMMAs apart).
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     double a[MI][2], b[NJ][2];
-#pragma unroll
-    for (int i = 0; i < MI; ++i) lds128(a[i][0], a[i][1], sA + ((offA0 + i * 1024) ^ (h * 64)));
     if constexpr (B_KMAJOR) {
 #pragma unroll
       for (int j = 0; j < NJ; ++j) lds128(b[j][0], b[j][1], sB + ((offB0 + j * 1024) ^ (h * 64)));
@@ -58,11 +60,15 @@ __device__ __forceinline__ void dmma_stage(double (&acc)[MI][NJ][2], uint32_t sA
       }
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+    for (int i = 0; i < MI; ++i) {
+      lds128(a[i][0], a[i][1], sA + ((offA0 + i * 1024) ^ (h * 64)));
 #pragma unroll
-      for (int i = 0; i < MI; ++i)
+      for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][0], b[j][0]);
+    }
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][q], b[j][q]);
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][1], b[j][1]);
   }
 }
 
