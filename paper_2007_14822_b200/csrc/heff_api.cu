@@ -308,6 +308,44 @@ static bool use_small_tile(const GemmOp& g, const ShardedA* sa) {
 // share one tile's K range and reduce through DSMEM.  Chosen when tiles x CS fills at least
 // 60% of the SMs in one wave with >= 4 k-blocks per rank (else the stream-K schedule, which
 // spreads a handful of tiles over every SM, is better).  HEFF_NO_CLUSTER_SPLITK=1 disables.
+// Co-resident clusters of CS CTAs (clusters live inside one GPC: at CS = 4 a B200 holds 32
+// of them, 128 of its 148 SMs, not 37); queried once per device and size.
+static int max_active_clusters(int cs) {
+  static std::mutex mu;
+  static int cache[kMaxDevices][5] = {};
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lock(mu);
+  int& c = cache[dev][cs];
+  if (c == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(cs * 64));
+    cfg.blockDim = dim3(cs == 4 ? CfgCl4::kThreads : CfgCl2::kThreads);
+    cfg.dynamicSmemBytes = cs == 4 ? CfgCl4::kSmemBytes : CfgCl2::kSmemBytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const cudaError_t e =
+        cs == 4 ? cudaOccupancyMaxActiveClusters(&n, gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, 4>, &cfg)
+                : cudaOccupancyMaxActiveClusters(&n, gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, 2>, &cfg);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = -1;  // unknown: never choose the cluster path
+    }
+    c = n;
+  }
+  return c;
+}
+
+// Cluster split-K for dense GEMMs with few 64x64 tiles (gemm_small.cuh): CS CTAs of a cluster
+// share one tile's K range and reduce through DSMEM.  Chosen when the tiles x CS CTAs run in
+// ONE wave of co-resident clusters filling >= 60% of the SMs, with >= 4 k-blocks per rank
+// (else the stream-K schedule, which spreads a handful of tiles over every SM, is better).
+// HEFF_NO_CLUSTER_SPLITK=1 disables.
 static int cluster_splitk_size(const GemmOp& g, const ShardedA* sa) {
   if (sa || g.sp_list || getenv("HEFF_NO_CLUSTER_SPLITK") != nullptr) return 0;
   if (const char* e = getenv("HEFF_GEMM_TILE"))
@@ -315,7 +353,9 @@ static int cluster_splitk_size(const GemmOp& g, const ShardedA* sa) {
   const int64_t tiles = ((g.M + 63) / 64) * ((g.N + 63) / 64);
   const int64_t ktiles = (g.K + kGemmBK - 1) / kGemmBK;
   for (int cs : {4, 2})
-    if (tiles * cs <= g_num_sms && tiles * cs * 10 >= 6 * (int64_t)g_num_sms && ktiles >= 4 * cs) return cs;
+    if (tiles * cs <= g_num_sms && tiles * cs * 10 >= 6 * (int64_t)g_num_sms && ktiles >= 4 * cs &&
+        tiles <= max_active_clusters(cs))
+      return cs;
   return 0;
 }
 
@@ -912,7 +952,7 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
     p->g4.b_static = true;  // R: a borrowed input no kernel of the matvec writes
     p->g4.ldc = d.mR;
     // GEMM1 + MPO fused on fat tiles (gemm_small.cuh): rows = whole a' groups (TA kL = 80),
-    // columns = TB b for each (s1 s2) (d1 d2 TB = 128); used when the tiles make 0.5..1 wave
+    // columns = TB b for each (s1 s2) (d1 d2 TB = 128); used when the tiles make 0.5..2 waves
     {
       const int64_t dd = d.d1 * d.d2;
       const bool shape_ok = (kFusedBM % d.kL == 0) && (dd & (dd - 1)) == 0 && (kFusedBN / dd) % 16 == 0 &&
@@ -922,7 +962,9 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
         const int64_t TA = kFusedBM / d.kL, TB = kFusedBN / dd;
         if (d.mL % TA == 0 && d.mR % TB == 0) {
           const int64_t tiles = (d.mL / TA) * (d.mR / TB);
-          bool use = tiles <= g_num_sms && 2 * tiles >= g_num_sms;
+          // 0.5 .. 2 waves of fat tiles (measured: C2 and the m = 128 cylinder 1 wave, chain
+          // m = 384 1.95 waves 183 -> 165 us; at 3.5 waves the general path is as fast)
+          bool use = tiles <= 2 * (int64_t)g_num_sms && 2 * tiles >= g_num_sms;
           if (const char* e = getenv("HEFF_FUSED_MATVEC")) use = atoi(e) != 0;
           if (use) {
             p->fusedTA = (int)TA;
