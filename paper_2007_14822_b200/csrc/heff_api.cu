@@ -952,7 +952,7 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
     p->g4.b_static = true;  // R: a borrowed input no kernel of the matvec writes
     p->g4.ldc = d.mR;
     // GEMM1 + MPO fused on fat tiles (gemm_small.cuh): rows = whole a' groups (TA kL = 80),
-    // columns = TB b for each (s1 s2) (d1 d2 TB = 128); used when the tiles make 0.5..2 waves
+    // columns = TB b for each (s1 s2) (d1 d2 TB = 128); used up to 2 waves of tiles
     {
       const int64_t dd = d.d1 * d.d2;
       const bool shape_ok = (kFusedBM % d.kL == 0) && (dd & (dd - 1)) == 0 && (kFusedBN / dd) % 16 == 0 &&
@@ -962,9 +962,10 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
         const int64_t TA = kFusedBM / d.kL, TB = kFusedBN / dd;
         if (d.mL % TA == 0 && d.mR % TB == 0) {
           const int64_t tiles = (d.mL / TA) * (d.mR / TB);
-          // 0.5 .. 2 waves of fat tiles (measured: C2 and the m = 128 cylinder 1 wave, chain
-          // m = 384 1.95 waves 183 -> 165 us; at 3.5 waves the general path is as fast)
-          bool use = tiles <= 2 * (int64_t)g_num_sms && 2 * tiles >= g_num_sms;
+          // up to 2 waves of fat tiles (measured: C2 and the m = 128 cylinder 1 wave, chain
+          // m = 384 1.95 waves 183 -> 165 us, sub-wave m = 64..192 equal or faster (cylinder
+          // m = 96 65 -> 54 us); at 3.5 waves the general path is as fast)
+          bool use = tiles <= 2 * (int64_t)g_num_sms;
           if (const char* e = getenv("HEFF_FUSED_MATVEC")) use = atoi(e) != 0;
           if (use) {
             p->fusedTA = (int)TA;
