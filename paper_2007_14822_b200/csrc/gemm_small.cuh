@@ -30,6 +30,16 @@
 
 namespace heff {
 
+// ---- fragment row order -----------------------------------------------------------------
+// A K-major operand row of the 128-byte-swizzled stage is read by lane (g, t) as 16-byte chunk
+// t (^ 4 for the second k-slice pair) of row g: physical chunk t ^ (row & 7).  LDS.128 is
+// served per quarter-warp (8 lanes = two rows g, g + 1); rows differing only in bit 0 put
+// their four chunks on the same banks -- a 2-way conflict on every fragment load (ncu: 8
+// wavefronts per LDS.128, ideal 4).  Fragment row g therefore reads tile row sg(g), which
+// puts the two rows of a quarter-warp four chunks apart (conflict-free); the accumulator
+// rows (and, for a K-major B, columns) follow the same permutation in the epilogue.
+__device__ __forceinline__ int sg(int g) { return (g >> 1) | ((g & 1) << 2); }
+
 // ---- DMMA over one stage (the k-block held in shared memory) -------------------------
 // acc[MI][NJ][2] += A_stage(rows wm0..wm0+WM) . B_stage(cols wn0..wn0+WN) for one 16-wide k
 // block; B N-major (box layout of psi's 16x16 TMA boxes, box index n >> 4) or K-major.
@@ -192,7 +202,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const int wm0 = (warp / (kFusedBN / kFusedWN)) * kFusedWM;
   const int wn0 = (warp % (kFusedBN / kFusedWN)) * kFusedWN;
   const uint32_t smem_base = smem_u32(smem);
-  const uint32_t offA0 = (wm0 + g) * 128 + ((t ^ g) << 4);
+  const int gs = sg(g);  // fragment row g reads tile row gs (conflict-free fragment loads)
+  const uint32_t offA0 = (wm0 + gs) * 128 + ((t ^ gs) << 4);
   constexpr int kCons = kFusedConsumerWarps * 32;
   const int ctid = threadIdx.x;  // consumers are threads [0, kCons)
   int stage = 0;
@@ -225,7 +236,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
-        *reinterpret_cast<double2*>(epi + (wm0 + 8 * i + g) * kFusedEpiPitch + wn0 + 8 * j + 2 * t) =
+        *reinterpret_cast<double2*>(epi + (wm0 + 8 * i + gs) * kFusedEpiPitch + wn0 + 8 * j + 2 * t) =
             make_double2(acc[i][j][0], acc[i][j][1]);
     consumers_bar(kCons);
     if (tile + (int)gridDim.x >= tiles) stamp(4);
@@ -399,8 +410,9 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
   const int wm0 = (warp / (BN / WN)) * WM;
   const int wn0 = (warp % (BN / WN)) * WN;
   const uint32_t smem_base = smem_u32(smem);
-  const uint32_t offA0 = (wm0 + g) * 128 + ((t ^ g) << 4);
-  const uint32_t offB0 = (wn0 + g) * 128 + ((t ^ g) << 4);
+  const int gs = sg(g);  // fragment rows of A (and K-major B) read tile rows gs
+  const uint32_t offA0 = (wm0 + gs) * 128 + ((t ^ gs) << 4);
+  const uint32_t offB0 = B_KMAJOR ? (wn0 + gs) * 128 + ((t ^ gs) << 4) : 0;
   double acc[MI][NJ][2];
 #pragma unroll
   for (int i = 0; i < MI; ++i)
@@ -449,7 +461,7 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
   stamp(3);
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
-    const int row = mb * BM + wm0 + 8 * i + g;
+    const int row = mb * BM + wm0 + 8 * i + gs;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
@@ -461,6 +473,13 @@ __global__ void __launch_bounds__(ClusterGemmCfg<BM, BN, WM, WN, STAGES, CS>::kT
       }
       if (row >= M) continue;
       double* crow = C + (int64_t)row * ldc;
+      if (B_KMAJOR) {
+        // fragment columns 2t, 2t + 1 are B rows sg(2t) = t and sg(2t + 1) = t + 4
+        const int c0 = nb * BN + wn0 + 8 * j + t, c1 = c0 + 4;
+        if (c0 < N) crow[c0] = v.x + (accumulate ? crow[c0] : 0.0);
+        if (c1 < N) crow[c1] = v.y + (accumulate ? crow[c1] : 0.0);
+        continue;
+      }
       const int colj = nb * BN + wn0 + 8 * j + 2 * t;
       if (vec_store && colj + 1 < N) {
         if (accumulate) {
