@@ -46,16 +46,17 @@ __device__ __forceinline__ int sg(int g) { return (g >> 1) | ((g & 1) << 2); }
 template <int MI, int NJ, bool B_KMAJOR>
 __device__ __forceinline__ void dmma_stage(double (&acc)[MI][NJ][2], uint32_t sA, uint32_t sB, uint32_t offA0,
                                            uint32_t offB0, int wn0, int g, int t) {
-  // Program order = issue order (the loads and DMMAs are asm volatile): the B fragments
-  // first, then each A fragment right before the k-slice-0 DMMAs that use it, so the first
-  // DMMA waits for one A load instead of all of them; the k-slice-1 DMMAs follow
-  // (every accumulator's two updates stay MI*NJ DMMAs apart).
+  // All fragments of the stage (both k-slice pairs) are requested before the first DMMA:
+  // the consumer warps of an SM reach each stage together, so fragments loaded per half
+  // would leave the DMMA pipe idle for a load latency twice per stage.  Program order =
+  // issue order (asm volatile): B, then A of half 0 interleaved with its k-slice-0 DMMAs,
+  // the rest of the loads, then the remaining DMMAs.
+  double a[2][MI][2], b[2][NJ][2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    double a[MI][2], b[NJ][2];
     if constexpr (B_KMAJOR) {
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) lds128(b[j][0], b[j][1], sB + ((offB0 + j * 1024) ^ (h * 64)));
+      for (int j = 0; j < NJ; ++j) lds128(b[h][j][0], b[h][j][1], sB + ((offB0 + j * 1024) ^ (h * 64)));
     } else {
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
@@ -65,21 +66,29 @@ __device__ __forceinline__ void dmma_stage(double (&acc)[MI][NJ][2], uint32_t sA
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int k = 2 * t + q + 8 * h;
-          b[j][q] = lds64(box + k * 128 + ((((ni >> 1) ^ (k & 7))) << 4) + ((ni & 1) << 3));
+          b[h][j][q] = lds64(box + k * 128 + ((((ni >> 1) ^ (k & 7))) << 4) + ((ni & 1) << 3));
         }
       }
     }
+  }
 #pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      lds128(a[i][0], a[i][1], sA + ((offA0 + i * 1024) ^ (h * 64)));
+  for (int i = 0; i < MI; ++i) {
+    lds128(a[0][i][0], a[0][i][1], sA + (offA0 + i * 1024));
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][0], b[j][0]);
-    }
+    for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[0][i][0], b[0][j][0]);
+  }
+#pragma unroll
+  for (int i = 0; i < MI; ++i) lds128(a[1][i][0], a[1][i][1], sA + ((offA0 + i * 1024) ^ 64));
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[0][i][1], b[0][j][1]);
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][1], b[j][1]);
-  }
+      for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[1][i][q], b[1][j][q]);
 }
 
 // ---- GEMM1 + two-site MPO, fused ---------------------------------------------------------
