@@ -305,7 +305,13 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
                                                                   double* __restrict__ alpha, double* __restrict__ beta,
                                                                   double* __restrict__ invb,
                                                                   double* __restrict__ vnext) {
+  // gridDim.x == 1 (vectors of a few thousand entries): launched as an ordinary kernel and
+  // the grid-wide barriers are block barriers (a cooperative launch costs ~10 us there)
   cg::grid_group grid = cg::this_grid();
+  auto gsync = [&] {
+    if (gridDim.x > 1) grid.sync();
+    else __syncthreads();
+  };
   extern __shared__ double s_c[];  // [j]
   pdl_wait();  // w comes from the matvec kernel before (launched with programmatic serialization)
   __shared__ double red[kDotQ][kStepThreads / 32];
@@ -319,7 +325,7 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
     double* pp = pass ? p2 : p1;
     double* cc = pass ? c2 : c1;
     chunk_dots(V, ldv, j, w, lo, hi, pp, red);
-    grid.sync();
+    gsync();
     grid_sums(pp, j, G, s_c);  // the same fixed-order sums in every block
     __syncthreads();
     if (blockIdx.x == 0)
@@ -334,7 +340,7 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
   for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) acc = fma(w[i], w[i], acc);
   const double s = block_sum(acc, red[0]);
   if (threadIdx.x == 0) p3[blockIdx.x] = s;
-  grid.sync();
+  gsync();
   grid_sums(p3, 1, G, s_c);  // fixed order, every block
   __syncthreads();
   const double nrm2 = s_c[0];

@@ -2094,7 +2094,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       cfg.stream = s;
       cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeCooperative;
-      at[0].val.cooperative = 1;
+      at[0].val.cooperative = step_grid > 1 ? 1 : 0;  // one block: an ordinary launch
       at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[1].val.programmaticStreamSerializationAllowed = pdl_off ? 0 : 1;
       cfg.attrs = at;
