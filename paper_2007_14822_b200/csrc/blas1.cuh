@@ -117,17 +117,10 @@ __global__ void __launch_bounds__(256) multiaxpy_kernel(const double* __restrict
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i < n; i += stride) {
     if (vec && i + 1 < n) {
       double2 x = *reinterpret_cast<double2*>(w + i);
-      for (int q0 = 0; q0 < nq; q0 += 8) {  // eight independent loads in flight, then the FMAs
-        double2 v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          v[k] = (q0 + k < nq) ? __ldcs(reinterpret_cast<const double2*>(V + (q0 + k) * ldv + i)) : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (q0 + k < nq) {
-            x.x = fma(sc[q0 + k], v[k].x, x.x);
-            x.y = fma(sc[q0 + k], v[k].y, x.y);
-          }
+      for (int q = 0; q < nq; ++q) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(V + q * ldv + i));
+        x.x = fma(sc[q], v.x, x.x);
+        x.y = fma(sc[q], v.y, x.y);
       }
       *reinterpret_cast<double2*>(w + i) = x;
     } else {
@@ -339,16 +332,7 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
       for (int q = threadIdx.x; q < j; q += kStepThreads) cc[q] = s_c[q];
     for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) {
       double x = w[i];
-      // eight basis entries requested before they are used (the loads are independent; a
-      // plain loop waits for each one in turn: ~20 us for a 1024-entry step at j = 20)
-      for (int q0 = 0; q0 < j; q0 += kDotQ) {
-        double v[kDotQ];
-#pragma unroll
-        for (int k = 0; k < kDotQ; ++k) v[k] = (q0 + k < j) ? V[(int64_t)(q0 + k) * ldv + i] : 0.0;
-#pragma unroll
-        for (int k = 0; k < kDotQ; ++k)
-          if (q0 + k < j) x = fma(-s_c[q0 + k], v[k], x);
-      }
+      for (int q = 0; q < j; ++q) x = fma(-s_c[q], V[q * ldv + i], x);
       w[i] = x;
     }
   }
