@@ -1592,6 +1592,63 @@ static int apply_host_pipelined(heff_plan_s* p, const double* psi_host, double* 
   return HEFF_OK;
 }
 
+// End-to-end order-B matvec of a b'-sharded plan with the host-to-device copy of the full psi
+// overlapped: psi's rows (a s1 s2) arrive in kE2eChunks row blocks on the copy stream and
+// GEMM_A runs per block as each lands (its rows are independent); the MPO step and GEMM_D run
+// once, then this rank's out shard (1/P of psi) goes back.
+static int apply_host_pipelined_B(heff_plan_s* p, const double* psi_host, double* out_host, cudaStream_t s) {
+  const heff_dims& d = p->dims;
+  const int64_t rows = d.mL * d.d1 * d.d2, ldv1 = p->nb * d.kR;
+  if (!p->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : p->e2e_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t c = p->copy_stream;
+  CK(cudaEventRecord(p->e2e_ev[2 * kE2eChunks], s));
+  CK(cudaStreamWaitEvent(c, p->e2e_ev[2 * kE2eChunks], 0));
+  int nl = 0;
+  const GemmOp saved = p->gA;
+  for (int k = 0; k < kE2eChunks; ++k) {
+    const int64_t r0 = rows * k / kE2eChunks, r1 = rows * (k + 1) / kE2eChunks;
+    CK(cudaMemcpyAsync(p->stage_in + r0 * d.mR, psi_host + r0 * d.mR, sizeof(double) * (r1 - r0) * d.mR,
+                       cudaMemcpyHostToDevice, c));
+    CK(cudaEventRecord(p->e2e_ev[k], c));
+    CK(cudaStreamWaitEvent(s, p->e2e_ev[k], 0));
+    p->gA.M = r1 - r0;
+    p->gA.A = p->stage_in + r0 * d.mR;
+    p->gA.C = p->V1 + r0 * ldv1;
+    CKR(launch_gemm(p->gA, p->gemm_path, s, &nl, &p->splitws));
+  }
+  p->gA = saved;
+  // MPO step and GEMM_D (apply_orderB without its GEMM_A)
+  {
+    const int dd = (int)(d.d1 * d.d2);
+    MpoIO io{};
+    io.in = p->V1;
+    io.out = p->V3;
+    io.ncol = p->nb;
+    io.nin = dd * (int)d.kR;
+    io.nout = (int)d.kL * dd;
+    io.in_blk = (int64_t)dd * d.kR * p->nb;
+    io.in_row = p->nb;
+    io.out_blk = (int64_t)dd * p->nb;
+    io.out_row = p->nb;
+    io.out_grp = dd;
+    io.out_grp_stride = d.mL * dd * p->nb;
+    CKR((launch_mpo<1, true>(io, p->tcB, d.mL, p->csrB, nullptr, s)));
+    ++nl;
+  }
+  p->gD.C = p->stage_out;
+  p->gD.accumulate = 0;
+  CKR(launch_gemm(p->gD, p->gemm_path, s, &nl, &p->splitws));
+  CK(cudaMemcpyAsync(out_host, p->stage_out, sizeof(double) * rows * p->nb, cudaMemcpyDeviceToHost, s));
+  p->last_launches = nl;
+  p->total_launches += nl;
+  CK(cudaStreamSynchronize(c));
+  CK(cudaStreamSynchronize(s));
+  return HEFF_OK;
+}
+
 extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_host, heff_stream stream) {
   if (!p || !psi_host || !out_host) return set_err(HEFF_EINVAL, "heff_apply_host: null argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1608,6 +1665,9 @@ extern "C" int heff_apply_host(heff_plan p, const double* psi_host, double* out_
                          p->sp4 == nullptr && p->chunk_rows == d.mL && d.mL * d.d1 * d.d2 >= 8 * kE2eChunks &&
                          getenv("HEFF_NO_E2E_PIPELINE") == nullptr;
   if (pipelined) return apply_host_pipelined(p, psi_host, out_host, s);
+  if (!p->is_complex && p->sharded && p->terms.empty() && p->nphi == 0 && d.mL * d.d1 * d.d2 >= 8 * kE2eChunks &&
+      getenv("HEFF_NO_E2E_PIPELINE") == nullptr)
+    return apply_host_pipelined_B(p, psi_host, out_host, s);
   CK(cudaMemcpyAsync(p->stage_in, psi_host, sizeof(double) * n_in, cudaMemcpyHostToDevice, s));
   CKR(apply_impl(p, p->stage_in, p->stage_out, s));
   CK(cudaMemcpyAsync(out_host, p->stage_out, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));

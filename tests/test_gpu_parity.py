@@ -503,3 +503,26 @@ def test_comm_failure_detection_aborts(dev, monkeypatch):
         torch.cuda.synchronize()
     finally:
         h.close()
+
+
+@pytest.mark.parametrize("P,g", [(2, 1), (4, 0), (8, 5)])
+def test_apply_host_sharded_pipelined(dev, orc, P, g):
+    """End-to-end matvec of a b'-shard (heff_apply_host: psi's row blocks copied in on a copy
+    stream while GEMM_A runs per block) against the order-B oracle on the shard's columns,
+    and bitwise against the device-resident heff_apply of the same plan."""
+    from paper_2007_14822_b200 import Heff
+    x = C.make("c2")
+    L, W1, W2, R, psi = x.numpy()
+    mR = R.shape[0]
+    nb = mR // P
+    ref = orc.heff_apply_B(L, W1, W2, R, psi, cols=(g * nb, (g + 1) * nb))
+    xd = x.to(dev)
+    Rg = xd.R[g * nb:(g + 1) * nb].contiguous()
+    with Heff(xd.L, xd.W1, xd.W2, Rg, dist=dict(nranks=P, rank=g, b_lo=g * nb, b_hi=(g + 1) * nb)) as h:
+        hin = x.psi.clone().pin_memory()
+        hout = torch.empty(h.out_shape, dtype=torch.float64).pin_memory()
+        h.apply_host(hin, hout)
+        dout = h.apply(xd.psi)
+        torch.cuda.synchronize()
+    assert rel(hout.numpy(), ref) <= MATVEC_TOL
+    assert torch.equal(hout, dout.cpu())
