@@ -508,8 +508,9 @@ def test_comm_failure_detection_aborts(dev, monkeypatch):
 @pytest.mark.parametrize("P,g", [(2, 1), (4, 0), (8, 5)])
 def test_apply_host_sharded_pipelined(dev, orc, P, g):
     """End-to-end matvec of a b'-shard (heff_apply_host: psi's row blocks copied in on a copy
-    stream while GEMM_A runs per block) against the order-B oracle on the shard's columns,
-    and bitwise against the device-resident heff_apply of the same plan."""
+    stream while GEMM_A runs per block) against the order-B oracle on the shard's columns and
+    against the device-resident heff_apply of the same plan (the row-blocked GEMM_A may split K
+    differently: rounding only)."""
     from paper_2007_14822_b200 import Heff
     x = C.make("c2")
     L, W1, W2, R, psi = x.numpy()
@@ -525,4 +526,4 @@ def test_apply_host_sharded_pipelined(dev, orc, P, g):
         dout = h.apply(xd.psi)
         torch.cuda.synchronize()
     assert rel(hout.numpy(), ref) <= MATVEC_TOL
-    assert torch.equal(hout, dout.cpu())
+    assert rel(hout.numpy(), dout.cpu().numpy()) <= 1e-14
