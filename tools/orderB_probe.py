@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--P", type=int, default=8)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--full", action="store_true",
+                    help="GEMM_A from the full psi (heff_apply: the NCCL all-gather path's kernels) instead of "
+                         "the blocked shards (heff_apply_blocked: the gather-fused path's)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     x = C.make(a.config, device=dev)
@@ -39,11 +42,12 @@ def main():
     res = dict(config=a.config, P=P, nb=nb)
     with Heff(x.L, x.W1, x.W2, Rg, dist=dict(nranks=P, rank=0, b_lo=0, b_hi=nb)) as h:
         out = torch.empty(h.out_shape, dtype=torch.float64, device=dev)
-        h.apply_blocked(blocked, out)
+        run = (lambda: h.apply(x.psi, out)) if a.full else (lambda: h.apply_blocked(blocked, out))
+        run()
         torch.cuda.synchronize()
         h.set_option(OPT_PROFILE, 1)
         for _ in range(a.reps):
-            h.apply_blocked(blocked, out)
+            run()
         g1, mpo, g4, n = h.last_timings()
         h.set_option(OPT_PROFILE, 0)
     # the order-B MPO kernel reads V1 and writes V3: (kR + kL) d1 d2 doubles per (a, b')
