@@ -232,35 +232,27 @@ __global__ void negate_kernel(const double* __restrict__ x, double* __restrict__
 // One fused CGS2 Lanczos step (single device, no communicator), cooperative launch.
 // Given w = H v_j and the basis V[0..j):
 //   c1 = V^T w ; w -= V c1 ; c2 = V^T w ; w -= V c2 ; alpha = c1[j-1] + c2[j-1] ;
-//   beta = ||w|| ; vnext = w / beta   (vnext may be null)
-// Each block owns one contiguous chunk of the vectors for all phases; the three
+//   beta = ||w|| ; vnext = w / beta   (vnext may be null; then w holds w'' on return,
+//   otherwise w holds w' and vnext the normalised w'')
+// Each block owns one contiguous chunk of the vectors for all phases; the two
 // grid-wide reductions are per-block partials + a grid sync + the same fixed-order sum in
 // every block (deterministic, no atomics).  Replaces ~16 launches per step with one.
-// partial: [2*jmax + 1][gridDim.x].
+// partial: [2*jmax + 1][gridDim.x] (the second pass uses rows jmax .. jmax + j).
 // ------------------------------------------------------------------------------------
 constexpr int kStepThreads = 512;
 
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int k = 0; k < kStepThreads / 32; ++k) t += red[k];
-  return t;
-}
-
-// partial[q][b] <- block b's sum over its chunk of V[q][i] w[i], q < j (8 vectors per pass).
-// Every warp reduces its kDotQ accumulators by shuffles; one barrier per group of 8; the
-// first nq threads add the kStepThreads/32 warp sums in warp order (deterministic).
-__device__ __forceinline__ void chunk_dots(const double* __restrict__ V, int64_t ldv, int j,
+// partial[q][b] <- block b's sum over its chunk of V[q][i] w[i], q < j (8 vectors per pass),
+// and with `wnorm` also partial[j][b] <- its sum of w[i]^2 (accumulated in the first group).
+// Every warp reduces its accumulators by shuffles; one barrier per group of 8; the first
+// threads add the kStepThreads/32 warp sums in warp order (deterministic).
+__device__ __forceinline__ void chunk_dots(const double* __restrict__ V, int64_t ldv, int j, bool wnorm,
                                            const double* __restrict__ w, int64_t lo, int64_t hi,
                                            double* __restrict__ partial, double (*red)[kStepThreads / 32]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int q0 = 0; q0 < j; q0 += kDotQ) {
     const int nq = min(kDotQ, j - q0);
-    double acc[kDotQ];
+    const bool nrm = wnorm && q0 == 0;
+    double acc[kDotQ], accw = 0.0;
 #pragma unroll
     for (int q = 0; q < kDotQ; ++q) acc[q] = 0.0;
     for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) {
@@ -268,6 +260,7 @@ __device__ __forceinline__ void chunk_dots(const double* __restrict__ V, int64_t
 #pragma unroll
       for (int q = 0; q < kDotQ; ++q)
         if (q < nq) acc[q] = fma(V[(q0 + q) * ldv + i], x, acc[q]);
+      accw = fma(x, x, accw);
     }
 #pragma unroll
     for (int q = 0; q < kDotQ; ++q)
@@ -275,12 +268,16 @@ __device__ __forceinline__ void chunk_dots(const double* __restrict__ V, int64_t
         const double v = warp_sum(acc[q]);
         if (lane == 0) red[q][warp] = v;
       }
+    if (nrm) {
+      accw = warp_sum(accw);
+      if (lane == 0) red[kDotQ][warp] = accw;
+    }
     __syncthreads();
-    if (threadIdx.x < nq) {
+    if (threadIdx.x < nq || (nrm && threadIdx.x == kDotQ)) {
       double t = 0.0;
 #pragma unroll
       for (int k = 0; k < kStepThreads / 32; ++k) t += red[threadIdx.x][k];
-      partial[(q0 + threadIdx.x) * gridDim.x + blockIdx.x] = t;
+      partial[(threadIdx.x < nq ? q0 + threadIdx.x : j) * gridDim.x + blockIdx.x] = t;
     }
     __syncthreads();  // red is reused by the next group
   }
@@ -312,47 +309,57 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
     if (gridDim.x > 1) grid.sync();
     else __syncthreads();
   };
-  extern __shared__ double s_c[];  // [j]
+  extern __shared__ double s_c[];  // [j + 1]
   pdl_wait();  // w comes from the matvec kernel before (launched with programmatic serialization)
-  __shared__ double red[kDotQ][kStepThreads / 32];
+  __shared__ double red[kDotQ + 1][kStepThreads / 32];
   const int G = gridDim.x;
   const int64_t chunk = ((n + G - 1) / G + 1) / 2 * 2;
   const int64_t lo = min(n, (int64_t)blockIdx.x * chunk), hi = min(n, lo + chunk);
   double* p1 = partial;
   double* p2 = partial + (int64_t)jmax * G;
-  double* p3 = partial + 2 * (int64_t)jmax * G;
+  // Two grid barriers: the second pass's reduction also carries ||w'||^2 (w' = w after the
+  // first update), and ||w''||^2 = ||w'||^2 - ||c2||^2 (V orthonormal: exact up to
+  // O(eps ||c2||^2), and c2 = O(eps ||w||) after the first pass), so the norm needs no third
+  // barrier and the last update writes v_{j+1} = w'' / beta directly.
+#pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
     double* pp = pass ? p2 : p1;
     double* cc = pass ? c2 : c1;
-    chunk_dots(V, ldv, j, w, lo, hi, pp, red);
+    chunk_dots(V, ldv, j, pass == 1, w, lo, hi, pp, red);
     gsync();
-    grid_sums(pp, j, G, s_c);  // the same fixed-order sums in every block
+    grid_sums(pp, j + pass, G, s_c);  // the same fixed-order sums in every block
     __syncthreads();
     if (blockIdx.x == 0)
       for (int q = threadIdx.x; q < j; q += kStepThreads) cc[q] = s_c[q];
-    for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) {
-      double x = w[i];
-      for (int q = 0; q < j; ++q) x = fma(-s_c[q], V[q * ldv + i], x);
-      w[i] = x;
+    double scale = 1.0;  // 1 / beta for the v_{j+1} store
+    if (pass) {
+      double nrm2 = s_c[j];
+      for (int q = 0; q < j; ++q) nrm2 = fma(-s_c[q], s_c[q], nrm2);
+      const double bt = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
+      const double ib = bt > 0.0 ? 1.0 / bt : 0.0;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        alpha[j - 1] = c1[j - 1] + s_c[j - 1];
+        beta[j - 1] = bt;
+        invb[j - 1] = ib;
+      }
+      if (vnext) scale = ib;
+    }
+    if (pass && vnext) {
+#pragma unroll 1
+      for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) {
+        double x = w[i];
+        for (int q = 0; q < j; ++q) x = fma(-s_c[q], V[q * ldv + i], x);
+        vnext[i] = x * scale;
+      }
+    } else {
+#pragma unroll 1
+      for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) {
+        double x = w[i];
+        for (int q = 0; q < j; ++q) x = fma(-s_c[q], V[q * ldv + i], x);
+        w[i] = x;
+      }
     }
   }
-  double acc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) acc = fma(w[i], w[i], acc);
-  const double s = block_sum(acc, red[0]);
-  if (threadIdx.x == 0) p3[blockIdx.x] = s;
-  gsync();
-  grid_sums(p3, 1, G, s_c);  // fixed order, every block
-  __syncthreads();
-  const double nrm2 = s_c[0];
-  const double bt = sqrt(nrm2);
-  const double ib = bt > 0.0 ? 1.0 / bt : 0.0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    alpha[j - 1] = c1[j - 1] + c2[j - 1];
-    beta[j - 1] = bt;
-    invb[j - 1] = ib;
-  }
-  if (vnext)
-    for (int64_t i = lo + threadIdx.x; i < hi; i += kStepThreads) vnext[i] = w[i] * ib;
 }
 
 }  // namespace heff

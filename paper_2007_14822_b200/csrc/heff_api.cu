@@ -2112,7 +2112,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   if (fused) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs2_step_kernel, kStepThreads,
-                                                     sizeof(double) * (size_t)cap));
+                                                     sizeof(double) * (size_t)(cap + 1)));
     // elements per thread (HEFF_STEP_EPT, default 2; round 1: 4): fewer = more blocks in
     // flight (C1 41.6 -> 37.5 us, cylinder m = 128 91 -> 78-82 us per Lanczos step)
     static const int ept = [] {
@@ -2150,7 +2150,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(step_grid);
       cfg.blockDim = dim3(kStepThreads);
-      cfg.dynamicSmemBytes = sizeof(double) * (size_t)j;
+      cfg.dynamicSmemBytes = sizeof(double) * (size_t)(j + 1);
       cfg.stream = s;
       cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeCooperative;
