@@ -71,7 +71,10 @@ struct NcclApi {
 
 static NcclApi g_nccl;
 
+static std::mutex g_nccl_mu;  // ranks of one process may create their plans concurrently
+
 static int nccl_load() {
+  std::lock_guard<std::mutex> lock(g_nccl_mu);
   if (g_nccl.loaded) return HEFF_OK;
   const char* env = getenv("HEFF_NCCL_PATH");
   void* h = nullptr;
