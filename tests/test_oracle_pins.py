@@ -296,3 +296,33 @@ def test_lanczos_fixed_steps_count(oracle_lib):
     r = oracle_lib.lanczos_heff(L, W1, W2, R, psi, max_iter=20)
     assert r.iters == 20
     assert np.all(np.diff(r.thetas) <= 1e-12)
+
+
+# ---------------------------------------------------------------- P12: closed form at full size
+@pytest.mark.parametrize("m,d,mR", [(4096, 2, 4096), (1024, 4, 768), (37, 3, 53)])
+def test_p12_closed_form_full_size(oracle_lib, m, d, mR):
+    """heffgen.closed.permuted_diagonal: (D) has a closed form at any size (weighted
+    permutations in the environments, one non-symmetric site operator per MPO); the oracle's
+    order A (sampled output rows a') and order B (sampled columns b') match it at the C4 size
+    (m = 4096, d = 2, psi 537 MB), at d = 4 and at ragged tiny dims -- a size-dependent
+    indexing or chunking mistake, a transposed environment (pi vs pi^-1) or a transposed site
+    operator would fail."""
+    from heffgen import closed
+    from tests import closed_form
+
+    x = closed.permuted_diagonal(m, d, seed=12 + m, mR=mR)
+    L, W1, W2, R, psi = x.numpy()
+    rows = sorted({0, 1, m // 2, m - 2, m - 1})
+    for a in rows:
+        got = oracle_lib.heff_apply(L, W1, W2, R, psi, rows=(a, a + 1))
+        ref = closed_form.expected_rows(x.meta, psi, [a])
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max(), a
+    cols = sorted({0, mR // 3, mR - 1})
+    for b in cols:
+        got = oracle_lib.heff_apply_B(L, W1, W2, R, psi, cols=(b, b + 1))
+        ref = closed_form.expected_cols(x.meta, psi, [b])
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max(), b
+    if m * d * d * mR <= 10 ** 6:  # tiny: the whole output, and the literal 7-fold sum
+        ref = closed_form.expected_rows(x.meta, psi, range(m))
+        assert np.abs(oracle_lib.heff_apply(L, W1, W2, R, psi) - ref).max() <= 1e-13 * np.abs(ref).max()
+        assert np.abs(oracle_lib.heff_direct(L, W1, W2, R, psi) - ref).max() <= 1e-13 * np.abs(ref).max()
