@@ -54,3 +54,27 @@ def test_closed_form_full_output_order_B_shards(dev, m, d, mR, P):
         with Heff(x.L, x.W1, x.W2, x.R[lo:hi].contiguous(), dist=dict(nranks=P, rank=g, b_lo=lo, b_hi=hi)) as h:
             out = h.apply(x.psi)
         assert _maxrel(out, ref[..., lo:hi].contiguous()) <= TOL, g
+
+
+@pytest.mark.parametrize("m,d,mR", [(4096, 2, 4096), (1024, 4, 768)])
+def test_closed_form_lanczos_full_size(dev, m, d, mR):
+    """lanczos_ground at full size against the closed-form ground state of the separable
+    member (heffgen.closed.separable): E0 = min eL + min eig O1 + min eig O2 + min eR and the
+    product ground state."""
+    from heffgen import closed
+    from paper_2007_14822_b200 import Heff
+
+    xc = closed.separable(m, d, seed=33 + m, mR=mR)
+    x = xc.to(dev)
+    mt = xc.meta
+    l1, u1 = np.linalg.eigh(mt["O1"])
+    l2, u2 = np.linalg.eigh(mt["O2"])
+    a0, b0 = int(np.argmin(mt["eL"])), int(np.argmin(mt["eR"]))
+    E0 = mt["eL"][a0] + l1[0] + l2[0] + mt["eR"][b0]
+    with Heff(x.L, x.W1, x.W2, x.R) as h:
+        v = x.psi.clone()
+        r = h.lanczos_ground(v, max_iter=300, tol=1e-12, converge=True)
+    assert abs(r.energy - E0) <= 1e-10 * max(1.0, abs(E0)), (r.energy, E0, r.iters)
+    x0 = np.einsum("i,j->ij", u1[:, 0], u2[:, 0])
+    ov = float(np.sum(v[a0, :, :, b0].cpu().numpy() * x0))
+    assert abs(abs(ov) - 1.0) <= 1e-9, ov

@@ -326,3 +326,16 @@ def test_p12_closed_form_full_size(oracle_lib, m, d, mR):
         ref = closed_form.expected_rows(x.meta, psi, range(m))
         assert np.abs(oracle_lib.heff_apply(L, W1, W2, R, psi) - ref).max() <= 1e-13 * np.abs(ref).max()
         assert np.abs(oracle_lib.heff_direct(L, W1, W2, R, psi) - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_p12_separable_lanczos_closed_form(oracle_lib):
+    """The oracle's Lanczos on the Hermitian member of the P12 family reaches the closed-form
+    ground energy min eL + min eig O1 + min eig O2 + min eR (no ED involved)."""
+    from heffgen import closed
+
+    x = closed.separable(96, 3, seed=7, mR=80)
+    L, W1, W2, R, psi = x.numpy()
+    mt = x.meta
+    E0 = mt["eL"].min() + np.linalg.eigvalsh(mt["O1"])[0] + np.linalg.eigvalsh(mt["O2"])[0] + mt["eR"].min()
+    o = oracle_lib.lanczos_heff(L, W1, W2, R, psi, max_iter=120)
+    assert abs(o.energy - E0) <= 1e-10 * abs(E0), (o.energy, E0)
