@@ -65,6 +65,7 @@ static std::vector<int2> svd_pair_schedule(int nblk) {
 static std::mutex g_svd_init_mu;  // svd_init_once may race from the U(1) split's workers
 static constexpr int kSvdMaxSweeps = 80;
 static int g_lq_grid = 0;  // co-resident CTAs of lq_panel_kernel (cooperative launch)
+static int g_lq_cl_max = 0;  // largest cluster of lq_panel_cluster_kernel that fits (0: none)
 static int g_svd_gram_occ = 0, g_svd_rot_occ = 0;    // co-resident CTAs per SM
 static int g_svd_tgram_occ = 0, g_svd_trot_occ = 0;  // (TMA-fed variants)
 static constexpr double kSvdRankEps = 1e-12;   // reading R21
@@ -115,6 +116,25 @@ static int svd_init_once() {
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lq_panel_kernel, kLqThreads, 0));
   g_lq_grid = std::max(1, per_sm) * g_num_sms;
+  CK(cudaFuncSetAttribute(lq_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          lq_cluster_smem(kLqClMaxCols)));
+  CK(cudaFuncSetAttribute(lq_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  for (int cs = kLqClMaxCtas; cs >= 2 && g_lq_cl_max == 0; cs /= 2) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kLqClThreads);
+    cfg.dynamicSmemBytes = lq_cluster_smem(kLqClMaxCols);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, lq_panel_cluster_kernel, &cfg) == cudaSuccess && ncl >= 1) g_lq_cl_max = cs;
+  }
+  (void)cudaGetLastError();
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_gram_occ, svd_gram_kernel, kSvdGramThreads, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_svd_rot_occ, svd_rotate_kernel, kSvdRotThreads, 0));
   g_svd_gram_occ = std::max(1, g_svd_gram_occ);
@@ -299,8 +319,29 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
       CK(cudaMemsetAsync(d_Vt, 0, sizeof(double) * kLqNb * colsP, s));
       double* Pp = d_P;
       int64_t ldp = colsP, jj = j, ldv = colsP;
-      void* args[] = {&Pp, &ldp, &jj, (void*)&nbp, (void*)&L, &cw, &d_Vt, &ldv, &d_beta, &d_part};
-      CK(cudaLaunchCooperativeKernel((const void*)lq_panel_kernel, dim3(grid), dim3(kLqThreads), args, 0, s));
+      if (g_lq_cl_max > 0 && L <= (int64_t)g_lq_cl_max * kLqClMaxCols && getenv("HEFF_LQ_GRID") == nullptr) {
+        // one cluster: a cluster barrier + DSMEM reads per reflector instead of a grid barrier
+        int cs = (int)std::max<int64_t>(1, std::min<int64_t>(g_lq_cl_max, (L + 255) / 256));
+        int ccw = (int)((L + cs - 1) / cs);
+        ccw = (ccw + 7) / 8 * 8;
+        cs = (int)((L + ccw - 1) / ccw);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kLqClThreads);
+        cfg.dynamicSmemBytes = lq_cluster_smem(ccw);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, lq_panel_cluster_kernel, Pp, ldp, jj, nbp, (int64_t)L, ccw, d_Vt, ldv, d_beta));
+      } else {
+        void* args[] = {&Pp, &ldp, &jj, (void*)&nbp, (void*)&L, &cw, &d_Vt, &ldv, &d_beta, &d_part};
+        CK(cudaLaunchCooperativeKernel((const void*)lq_panel_kernel, dim3(grid), dim3(kLqThreads), args, 0, s));
+      }
       GemmOp gv;  // V^T V = Vt Vt^T (K = L)
       gv.M = nbp; gv.N = nbp; gv.K = L; gv.A = d_Vt + j; gv.lda = colsP; gv.B = d_Vt + j; gv.ldb = colsP;
       gv.b_kmajor = true; gv.C = d_VtV; gv.ldc = nbp;
