@@ -307,6 +307,348 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   stamp(3);
 }
 
+// ---- the whole order-A matvec, one thread-block cluster per a' block (C2-size chains) -------
+// The fat tile (ta, tb) of gemm1_mpo_fused_kernel holds T3 for TA a' and TB b -- every
+// (s1' s2' w2) -- which is exactly the K-slice (w2, b in block tb) of GEMM4 for the 64 output
+// rows (a' s1' s2') of a' block ta.  So the CTA keeps its T3 tile in shared memory and
+// multiplies it by the matching slice of R right there:
+//     part_tb[(a' s1' s2')][b'] = sum_{w2, b in tb} T3[(a' s1' s2')][(w2 b)] R[b'][(w2 b)],
+// and out = sum_tb part_tb is a reduction over the CS = mR / TB CTAs of the a' block, which
+// form one thread-block cluster: each CTA parks its partial in its own shared memory, and
+// after a cluster barrier CTA rank r sums rows [64 r / CS, 64 (r+1) / CS) of the CS partials
+// in rank order through DSMEM (deterministic) and stores them.  One launch per matvec; T1
+// and T3 never leave the SM; no dependency between CTAs except the final reduction.
+// Per CTA: GEMM1 2 (TA kL) (d1 d2 TB) mL flops + GEMM4 2 (TA d1 d2) mR (kR TB) flops (equal
+// for mL = mR, kL = kR); at C2 (m = 256, 16 a' blocks x 8 b blocks) 128 CTAs in 16 clusters.
+// Shapes: TA d1 d2 == 64 (the chain's kL = 5, d = 2: TA = 16), kR TB <= 160, mR / TB <= 8.
+constexpr int kMvcM4 = 64;                 // GEMM4 rows per cluster: TA a' x (s1', s2')
+constexpr int kMvcNP = 128;                // GEMM4 columns (b') per pass (two passes at mR = 256)
+constexpr int kMvcSt1 = 4, kMvcSt4 = 2;    // GEMM1 ring (L + psi stages), GEMM4 ring (R stages)
+constexpr int kMvcRing1 = kMvcSt1 * kFusedStageBytes;  // GEMM1 ring, then the T1 tile, then partial 0
+constexpr int kMvcT3Bytes = 81920;         // T3 tile = GEMM4's A operand (64 rows x kR TB <= 160), then partial 1
+constexpr int kMvcRStage = kMvcNP * 128;   // 128 rows of R x 16 k
+constexpr int kMvcPartPitch = 136;         // doubles per partial row (conflict-free double2 stores)
+constexpr int kMvcCsrRows = 64, kMvcCsrNnz = 256;  // CSR staged in shared memory up to these (else read via L1)
+constexpr int kMvcCsrBytes = (kMvcCsrRows + 1) * 4 + kMvcCsrNnz * 12 + 16;
+constexpr int kMvcSmemBytes = kMvcRing1 + kMvcT3Bytes + kMvcSt4 * kMvcRStage + kMvcCsrBytes +
+                              2 * (kMvcSt1 + kMvcSt4) * 8 + 1024;
+static_assert(kMvcM4 * kMvcPartPitch * 8 <= kMvcT3Bytes && kFusedBM * kFusedEpiPitch * 8 <= kMvcRing1,
+              "T1 tile and partials fit the freed regions");
+static_assert(kMvcSmemBytes <= 232448, "shared memory");
+static_assert(kMvcRing1 % 1024 == 0 && kMvcT3Bytes % 1024 == 0 && kMvcRStage % 1024 == 0, "TMA stage alignment");
+
+// Cluster reduction of matvec_cluster_kernel: rank tb sums rows [tb RR, tb RR + RR), RR = 64 / CS, of
+// the CS partials (pass p's partial at the same shared offset `base` in every CTA of the
+// cluster) in rank order; all CS loads of a thread's pairs are in flight before the adds.
+template <int CS>
+__device__ __forceinline__ void mvc_reduce(uint32_t base, int tb, int p, double* __restrict__ out, int64_t row0,
+                                           int mR, int accumulate) {
+  constexpr int RR = kMvcM4 / CS;            // rows owned by this CTA
+  constexpr int NPAIR = RR * (kMvcNP / 2);   // (row, column pair) items of the pass
+  constexpr int NIT = (NPAIR + 255) / 256;   // per consumer thread
+  double vx[NIT][CS], vy[NIT][CS];
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int idx = threadIdx.x + 256 * it;
+    if (idx < NPAIR) {
+      const int row = tb * RR + idx / (kMvcNP / 2), pc = 2 * (idx % (kMvcNP / 2));
+      const uint32_t a = base + (uint32_t)((row * kMvcPartPitch + pc) * 8);
+#pragma unroll
+      for (int q = 0; q < CS; ++q)
+        asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];"
+                     : "=d"(vx[it][q]), "=d"(vy[it][q])
+                     : "r"(mapa_shared(a, (uint32_t)q))
+                     : "memory");
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int idx = threadIdx.x + 256 * it;
+    if (idx < NPAIR) {
+      const int row = tb * RR + idx / (kMvcNP / 2), pc = 2 * (idx % (kMvcNP / 2));
+      // stored pair at column 8j + 2t holds b' = 8j + t and 8j + t + 4
+      const int c0 = p * kMvcNP + (pc & ~7) + ((pc & 7) >> 1), c1 = c0 + 4;
+      double sx = vx[it][0], sy = vy[it][0];
+#pragma unroll
+      for (int q = 1; q < CS; ++q) {
+        sx += vx[it][q];
+        sy += vy[it][q];
+      }
+      double* orow = out + (row0 + row) * mR;
+      if (c0 < mR) orow[c0] = sx + (accumulate ? orow[c0] : 0.0);
+      if (c1 < mR) orow[c1] = sy + (accumulate ? orow[c1] : 0.0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFusedThreads, 1)
+    matvec_cluster_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmPsi,
+                          const __grid_constant__ CUtensorMap tmR, double* __restrict__ out, int mL, int mR, int kL,
+                          int kR, int dd, int log2dd, int TA, int TB, int nout, const int* __restrict__ rowptr,
+                          const int* __restrict__ col, const double* __restrict__ val, int accumulate,
+                          unsigned long long* __restrict__ dbg) {
+  // dbg (diagnostics, normally null): per CTA %globaltimer at entry, end of GEMM1, end of the
+  // MPO epilogue, end of GEMM4, end of the reduction (thread 0)
+  auto stamp = [&](int k) {
+    if (dbg && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      dbg[blockIdx.x * 8 + k] = t;
+    }
+  };
+  stamp(0);
+  constexpr int MI = kFusedWM / 8, NJ = kFusedWN / 8;  // GEMM1 warp tile 40 x 32
+  constexpr int MI4 = 4, NJ4 = 4;                      // GEMM4 warp tile 32 x 32 (2 x 4 warps)
+  constexpr int kCons = kFusedConsumerWarps * 32;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // 1024-byte aligned regions first (TMA destinations with the 128-byte swizzle)
+  unsigned char* region1 = smem;                                        // GEMM1 ring, then T1, then partial 0
+  double* epi = reinterpret_cast<double*>(region1);                     // the T1 tile (after the main loop)
+  unsigned char* t3 = smem + kMvcRing1;                                 // T3 tile, then partial 1
+  unsigned char* rring = t3 + kMvcT3Bytes;                              // R stages
+  double* s_val = reinterpret_cast<double*>(rring + kMvcSt4 * kMvcRStage);
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(s_val + kMvcCsrNnz);
+  int* s_rp = reinterpret_cast<int*>(s_off + kMvcCsrNnz);
+  uint64_t* full1 = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(s_val) + ((kMvcCsrBytes + 15) & ~15));
+  uint64_t* empty1 = full1 + kMvcSt1;
+  uint64_t* full4 = empty1 + kMvcSt1;
+  uint64_t* empty4 = full4 + kMvcSt4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t CS;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(CS));
+  const int tb = (int)cluster_ctarank();
+  const int ta = (int)blockIdx.x / (int)CS;
+  const int ktiles = (mL + kGemmBK - 1) / kGemmBK;
+  const int kb4n = kR * TB / kGemmBK;       // GEMM4 k-blocks per pass
+  const int npass = (mR + kMvcNP - 1) / kMvcNP;
+  const int n4 = npass * kb4n;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMvcSt1; ++s) {
+      mbar_init(&full1[s], 1);
+      mbar_init(&empty1[s], kFusedConsumerWarps);
+    }
+    for (int s = 0; s < kMvcSt4; ++s) {
+      mbar_init(&full4[s], 1);
+      mbar_init(&empty4[s], kFusedConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const bool producer = warp == kFusedConsumerWarps && lane == 0;
+  // L and R are plan inputs no kernel of the stream writes: the first stages of both are
+  // requested before the dependency wait
+  const int npre1 = min(kMvcSt1, ktiles), npre4 = min(kMvcSt4, n4);
+  auto load_r = [&](int it, int stage) {
+    const int p = it / kb4n, kb = it - p * kb4n;
+    const int bpw = TB / kGemmBK;  // k-blocks per w2
+    const int w2 = kb / bpw, c = kb - w2 * bpw;
+    tma_load_2d(rring + stage * kMvcRStage, &tmR, &full4[stage], w2 * mR + tb * TB + c * kGemmBK, p * kMvcNP);
+  };
+  if (producer) {
+    tma_prefetch_desc(&tmL);
+    tma_prefetch_desc(&tmPsi);
+    tma_prefetch_desc(&tmR);
+    for (int kb = 0; kb < npre1; ++kb) {
+      mbar_arrive_expect_tx(&full1[kb], kFusedStageBytes);
+      tma_load_2d(region1 + kb * kFusedStageBytes, &tmL, &full1[kb], kb * kGemmBK, ta * kFusedBM);
+    }
+    for (int it = 0; it < npre4; ++it) {
+      mbar_arrive_expect_tx(&full4[it], kMvcRStage);
+      load_r(it, it);
+    }
+  }
+  pdl_wait();  // psi (and out) only after the previous kernel in the stream
+  const int nnz = __ldg(rowptr + nout);
+  const bool csr_smem = nout <= kMvcCsrRows && nnz <= kMvcCsrNnz;
+  if (csr_smem) {
+    for (int r = threadIdx.x; r <= nout; r += blockDim.x) s_rp[r] = __ldg(rowptr + r);
+    for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
+      const int c = __ldg(col + e);
+      s_off[e] = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
+      s_val[e] = __ldg(val + e);
+    }
+  }
+  __syncthreads();
+
+  if (warp >= kFusedConsumerWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(40));
+    if (producer) {
+      // GEMM1 stages: L rows of a' block ta, psi columns (s, b in block tb) for every s
+      const int bps = TB / 16;  // 16-column boxes per (s1 s2) block
+      for (int kb = 0; kb < ktiles; ++kb) {
+        const int stage = kb % kMvcSt1;
+        unsigned char* sA = region1 + stage * kFusedStageBytes;
+        if (kb >= npre1) {
+          mbar_wait(&empty1[stage], ((kb / kMvcSt1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full1[stage], kFusedStageBytes);
+          tma_load_2d(sA, &tmL, &full1[stage], kb * kGemmBK, ta * kFusedBM);
+        }
+#pragma unroll 1
+        for (int q = 0; q < kFusedBN / 16; ++q) {
+          const int s = q / bps, c = q - s * bps;
+          tma_load_2d(sA + kFusedBM * 128 + q * 2048, &tmPsi, &full1[stage], s * mR + tb * TB + c * 16,
+                      kb * kGemmBK);
+        }
+      }
+      // GEMM4 stages: R rows b' of the pass, k = (w2, b in block tb)
+      for (int it = npre4; it < n4; ++it) {
+        const int stage = it % kMvcSt4;
+        mbar_wait(&empty4[stage], ((it / kMvcSt4) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full4[stage], kMvcRStage);
+        load_r(it, stage);
+      }
+    }
+    __syncwarp();
+    // the two cluster barriers of the reduction below (code after a setmaxnreg.dec runs
+    // with 40 registers, so the reduction itself stays in the consumer branch)
+    cluster_sync_all();
+    cluster_sync_all();
+    return;
+  }
+  {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(232));
+    const int g = lane >> 2, t = lane & 3;
+    const int gs = sg(g);
+    const int ctid = threadIdx.x;
+    const uint32_t smem_base = smem_u32(smem);
+    // ---- GEMM1: T1 tile [(a' w)][(s b)] = L[(a' w)][a] psi[a][(s b)]
+    {
+      const int wm0 = (warp / (kFusedBN / kFusedWN)) * kFusedWM;
+      const int wn0 = (warp % (kFusedBN / kFusedWN)) * kFusedWN;
+      const uint32_t offA0 = (wm0 + gs) * 128 + ((t ^ gs) << 4);
+      double acc[MI][NJ][2];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int kb = 0; kb < ktiles; ++kb) {
+        const int stage = kb % kMvcSt1;
+        mbar_wait(&full1[stage], (kb / kMvcSt1) & 1);
+        const uint32_t sA = smem_base + stage * kFusedStageBytes;
+        dmma_stage<MI, NJ, false>(acc, sA, sA + kFusedBM * 128, offA0, 0, wn0, g, t);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty1[stage]);
+      }
+      consumers_bar(kCons);  // every warp is done with the ring: the T1 tile goes there
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          *reinterpret_cast<double2*>(epi + (wm0 + 8 * i + gs) * kFusedEpiPitch + wn0 + 8 * j + 2 * t) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+    stamp(1);
+    consumers_bar(kCons);  // T1 staged
+    // ---- two-site MPO into the T3 tile, stored as GEMM4's A operand: row r = (a', s'),
+    // k = w2 TB + b (16-wide k-blocks of 64 rows x 128 bytes, 128-byte swizzle)
+    {
+      const int pairs = TB >> 1, G = kCons / pairs;
+      const int bp = ctid & (pairs - 1), grp = ctid / pairs;
+      const double* col_p = epi + 2 * bp;
+      const int nq = (TA + kFusedAlChunk - 1) / kFusedAlChunk;
+      const int rstride = kL * kFusedEpiPitch;
+#pragma unroll 1
+      for (int u = grp; u < nout * nq; u += G) {
+        const int o = u / nq, al0 = (u - o * nq) * kFusedAlChunk, al1 = min(TA, al0 + kFusedAlChunk);
+        const int e0 = csr_smem ? s_rp[o] : __ldg(rowptr + o);
+        const int e1 = csr_smem ? s_rp[o + 1] : __ldg(rowptr + o + 1);
+        double ax[kFusedAlChunk], ay[kFusedAlChunk];
+#pragma unroll
+        for (int q = 0; q < kFusedAlChunk; ++q) ax[q] = ay[q] = 0.0;
+        const double* src0 = col_p + al0 * rstride;
+#pragma unroll 1
+        for (int e = e0; e < e1; ++e) {
+          uint32_t of;
+          double vv;
+          if (csr_smem) {
+            of = s_off[e];
+            vv = s_val[e];
+          } else {
+            const int c = __ldg(col + e);
+            of = (uint32_t)(((c >> log2dd) * kFusedEpiPitch) + (c & (dd - 1)) * TB);
+            vv = __ldg(val + e);
+          }
+#pragma unroll
+          for (int q = 0; q < kFusedAlChunk; ++q)
+            if (al0 + q < al1) {
+              const double2 xy = *reinterpret_cast<const double2*>(src0 + q * rstride + of);
+              ax[q] = fma(vv, xy.x, ax[q]);
+              ay[q] = fma(vv, xy.y, ay[q]);
+            }
+        }
+        // o = (s', w2): s' = o / kR
+        const int sp = o / kR, w2 = o - sp * kR;
+        const int k = w2 * TB + 2 * bp;
+        const uint32_t kbase = smem_u32(t3) + (uint32_t)((k >> 4) * (kMvcM4 * 128));
+        const int ch = (k & 15) >> 1;
+#pragma unroll
+        for (int q = 0; q < kFusedAlChunk; ++q)
+          if (al0 + q < al1) {
+            const int r = (al0 + q) * dd + sp;
+            sts128(kbase + r * 128 + ((ch ^ (r & 7)) << 4), ax[q], ay[q]);
+          }
+      }
+    }
+    stamp(2);
+    consumers_bar(kCons);  // T3 complete
+    // ---- GEMM4 partial: part[(a' s')][b'] = T3[(a' s')][(w2 b)] R[b'][(w2 b)], two passes of 128 b'
+    {
+      const int wm4 = (warp / 4) * 32, wn4 = (warp % 4) * 32;
+      const uint32_t offA4 = (wm4 + gs) * 128 + ((t ^ gs) << 4);
+      const uint32_t offB4 = (wn4 + gs) * 128 + ((t ^ gs) << 4);
+      const uint32_t rbase = smem_u32(rring), t3base = smem_u32(t3);
+      int it = 0;
+      for (int p = 0; p < npass; ++p) {
+        double acc[MI4][NJ4][2];
+#pragma unroll
+        for (int i = 0; i < MI4; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kb = 0; kb < kb4n; ++kb, ++it) {
+          const int stage = it % kMvcSt4;
+          mbar_wait(&full4[stage], (it / kMvcSt4) & 1);
+          dmma_stage<MI4, NJ4, true>(acc, t3base + kb * (kMvcM4 * 128), rbase + stage * kMvcRStage, offA4, offB4,
+                                     wn4, g, t);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty4[stage]);
+        }
+        if (p == npass - 1) pdl_launch_dependents();
+        // partial of pass p -> shared memory (pass 0: the T1 staging area; pass 1: the T3 area,
+        // once every warp is done reading T3).  Fragment columns 2t, 2t+1 are b' = 8j + t and
+        // 8j + t + 4 (K-major B rows sg(2t), sg(2t+1)); stored as a pair at column 8j + 2t.
+        double* part = reinterpret_cast<double*>(p == 0 ? region1 : t3);
+        if (p == 1) consumers_bar(kCons);
+#pragma unroll
+        for (int i = 0; i < MI4; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ4; ++j)
+            *reinterpret_cast<double2*>(part + (wm4 + 8 * i + gs) * kMvcPartPitch + wn4 + 8 * j + 2 * t) =
+                make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    }
+    stamp(3);
+  }
+  // ---- cluster reduction: rank tb owns rows [64 tb / CS, 64 (tb+1) / CS) of the a' block (CS | 64)
+  cluster_sync_all();  // every CTA's partials are in its shared memory
+  {
+    const int64_t row0 = (int64_t)ta * kMvcM4;
+    for (int p = 0; p < npass; ++p) {
+      const uint32_t base = smem_u32(p == 0 ? region1 : t3);
+      switch (CS) {
+        case 1: mvc_reduce<1>(base, tb, p, out, row0, mR, accumulate); break;
+        case 2: mvc_reduce<2>(base, tb, p, out, row0, mR, accumulate); break;
+        case 4: mvc_reduce<4>(base, tb, p, out, row0, mR, accumulate); break;
+        default: mvc_reduce<8>(base, tb, p, out, row0, mR, accumulate); break;
+      }
+    }
+  }
+  stamp(4);
+  cluster_sync_all();  // no CTA leaves while a peer still reads its shared memory
+}
+
 // ---- GEMM with cluster split-K ------------------------------------------------------------
 // One output tile per cluster of CS CTAs; rank r runs k-blocks [kt r / CS, kt (r+1) / CS).
 // Shared memory: the TMA ring, then (rank 0) CS - 1 partial slots [i][j][thread] of double2.

@@ -344,6 +344,35 @@ static int max_active_clusters(int cs) {
   return c;
 }
 
+// Co-resident clusters of CS CTAs of matvec_cluster_kernel (one CTA per SM: its shared memory)
+static int max_active_mvc_clusters(int cs) {
+  static std::mutex mu;
+  static int cache[kMaxDevices][9] = {};
+  const int dev = cur_device();
+  std::lock_guard<std::mutex> lock(mu);
+  int& c = cache[dev][cs];
+  if (c == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(cs * 32));
+    cfg.blockDim = dim3(kFusedThreads);
+    cfg.dynamicSmemBytes = kMvcSmemBytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, matvec_cluster_kernel, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = -1;  // unknown: never choose the cluster matvec
+    }
+    c = n;
+  }
+  return c;
+}
+
 // Cluster split-K for dense GEMMs with few 64x64 tiles (gemm_small.cuh): CS CTAs of a cluster
 // share one tile's K range and reduce through DSMEM.  Chosen when the tiles x CS CTAs run in
 // ONE wave of co-resident clusters filling >= 60% of the SMs, with >= 4 k-blocks per rank
@@ -492,6 +521,7 @@ int init_device_once() {
   CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
   CK(cudaFuncSetAttribute(heff_small_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallMvMaxSmem));
   CK(cudaFuncSetAttribute(gemm1_mpo_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemBytes));
+  CK(cudaFuncSetAttribute(matvec_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMvcSmemBytes));
   CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, false, 2>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgCl2::kSmemBytes));
   CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, 2>,
@@ -601,6 +631,10 @@ struct heff_plan_s {
   CUtensorMap fmapL, fmapPsi;
   const double* fpsi_ptr = nullptr;
   bool fmapL_ok = false;
+  // C2-size chains: the whole matvec in one cluster launch (matvec_cluster_kernel); cluster
+  // size mR / fusedTB, 0 = not eligible
+  int mvc_cs = 0;
+  CUtensorMap fmapR;
   // order B workspace
   double *V1 = nullptr, *V3 = nullptr;
   GemmOp gA, gD;
@@ -974,6 +1008,28 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
             p->fusedTA = (int)TA;
             p->fusedTB = (int)TB;
           }
+          // one cluster per a' block (matvec_cluster_kernel): 64 GEMM4 rows per a' block, the
+          // T3 tile (kR TB columns) in shared memory, CS = mR / TB in {1, 2, 4, 8} CTAs per
+          // cluster, one wave of co-resident clusters.  Measured back to back (B200): chain
+          // m = 128 39.0 -> 31.9 us, m = 64 25.1 / 25.7 us (equal); C2 (16 clusters of 8) does not
+          // fit (15 co-resident) and keeps the two-kernel form
+          const int64_t cs = d.mR / TB;
+          bool mvc = TA * dd == kMvcM4 && d.kR * TB * kMvcM4 * 8 <= kMvcT3Bytes && (d.kR * TB) % kGemmBK == 0 &&
+                     (cs == 1 || cs == 2 || cs == 4 || cs == 8) && tiles <= g_num_sms && (d.kR * d.mR) % 2 == 0 &&
+                     (reinterpret_cast<uintptr_t>(R) & 15) == 0 && d.mR <= 2 * kMvcNP &&
+                     d.mL / TA <= max_active_mvc_clusters((int)cs);
+          if (const char* e = getenv("HEFF_CLUSTER_MATVEC")) mvc = mvc && atoi(e) != 0;
+          if (getenv("HEFF_DEBUG_MVC"))
+            fprintf(stderr, "cluster matvec: TA %lld TB %lld CS %lld a'-blocks %lld tiles %lld max clusters %d -> %d\n",
+                    (long long)TA, (long long)TB, (long long)cs, (long long)(d.mL / TA), (long long)tiles,
+                    (cs >= 1 && cs <= 8) ? max_active_mvc_clusters((int)cs) : -1, (int)mvc);
+          if (mvc) {
+            const int r = make_map(&p->fmapR, R, d.mR, d.kR * d.mR, d.kR * d.mR, kGemmBK, kMvcNP);
+            if (r) return fail(r);
+            p->fusedTA = (int)TA;
+            p->fusedTB = (int)TB;
+            p->mvc_cs = (int)cs;
+          }
         }
       }
     }
@@ -1270,6 +1326,34 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
       p->fpsi_ptr = psi;
     }
     const int tiles = (int)((d.mL / p->fusedTA) * (d.mR / p->fusedTB));
+    if (p->mvc_cs > 0) {
+      // the whole matvec: one cluster of mR / TB CTAs per a' block
+      static const bool pdl_off = getenv("HEFF_NO_PDL") != nullptr;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)tiles);
+      cfg.blockDim = dim3(kFusedThreads);
+      cfg.dynamicSmemBytes = kMvcSmemBytes;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)p->mvc_cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = pdl_off ? 0 : 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+      CKR(prof_mark(p, 0, s));
+      CK(cudaLaunchKernelEx(&cfg, matvec_cluster_kernel, p->fmapL, p->fmapPsi, p->fmapR, out, (int)d.mL, (int)d.mR,
+                            (int)d.kL, (int)d.kR, (int)dd, (int)__builtin_ctz((unsigned)dd), p->fusedTA, p->fusedTB,
+                            (int)(dd * d.kR), (const int*)p->csrA.d_rowptr, (const int*)p->csrA.d_col,
+                            (const double*)p->csrA.d_val, accumulate, g_fused_dbg));
+      ++*nl;
+      CKR(prof_mark(p, 1, s));
+      CKR(prof_mark(p, 2, s));
+      CKR(prof_mark(p, 3, s));
+      return HEFF_OK;
+    }
     CKR(prof_mark(p, 0, s));
     CK(launch_pdl(gemm1_mpo_fused_kernel, dim3((unsigned)std::min(tiles, g_num_sms)), dim3(kFusedThreads),
                   kFusedSmemBytes, s, p->fmapL, p->fmapPsi, p->T3, (int)d.mL, (int)d.mR, (int)d.kL, (int)dd,

@@ -462,6 +462,7 @@ def test_fused_gemm1_mpo_matvec(dev, orc, case, env, monkeypatch):
     from paper_2007_14822_b200 import Heff
     if env is not None:
         monkeypatch.setenv("HEFF_FUSED_MATVEC", env)
+    monkeypatch.setenv("HEFF_CLUSTER_MATVEC", "0")   # the two-kernel form (test_cluster_matvec: one launch)
     x = {"c2": lambda: C.make("c2"), "cyl128": lambda: C.make("c4", m=128),
          "uneven": lambda: C.model_inputs([C.mpo.heisenberg_chain_W()] * 20, 6, 192, seed=77),
          "c2_m240": lambda: C.make("c2", m=240)}[case]()
@@ -527,3 +528,63 @@ def test_apply_host_sharded_pipelined(dev, orc, P, g):
         torch.cuda.synchronize()
     assert rel(hout.numpy(), ref) <= MATVEC_TOL
     assert rel(hout.numpy(), dout.cpu().numpy()) <= 1e-14
+
+
+CLUSTER_CASES = {   # case: (inputs, runs as one cluster launch)
+    "chain_m128": (lambda: C.make("c2", m=128), True),            # clusters of 4, one 128-wide b' pass
+    "mL128_mR256": (lambda: C.random_dense(dict(mL=128, d1=2, d2=2, mR=256, kL=5, kM=4, kR=5), seed=42), True),
+    "m64": (lambda: C.random_dense(dict(mL=64, d1=2, d2=2, mR=64, kL=5, kM=2, kR=5), seed=43), True),
+    "mR32": (lambda: C.random_dense(dict(mL=96, d1=2, d2=2, mR=32, kL=5, kM=5, kR=5), seed=44), True),
+    # clusters of 6 (not a divisor of 64) and C2's 16 clusters of 8 (more than the 15 that are
+    # co-resident on a B200) fall back to the two-kernel form
+    "mR192": (lambda: C.random_dense(dict(mL=256, d1=2, d2=2, mR=192, kL=5, kM=3, kR=5), seed=41), False),
+    "c2": (lambda: C.make("c2"), False),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CLUSTER_CASES))
+def test_cluster_matvec(dev, orc, case, monkeypatch):
+    """Small chains: the whole order-A matvec in ONE launch (matvec_cluster_kernel: GEMM1 +
+    two-site MPO + the GEMM4 slice of each fat tile in shared memory, the GEMM4 split-K
+    reduced over the a' block's thread-block cluster through DSMEM).  Parity with the oracle,
+    bitwise run-to-run, and the kernel count; with HEFF_CLUSTER_MATVEC=0 the two-kernel form."""
+    from paper_2007_14822_b200 import Heff
+    make, single = CLUSTER_CASES[case]
+    x = make()
+    L, W1, W2, R, psi = x.numpy()
+    ref = orc.heff_apply(L, W1, W2, R, psi)
+    xd = x.to(dev)
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        out = h.apply(xd.psi)
+        out2 = h.apply(xd.psi)
+        torch.cuda.synchronize()
+        nl = h.get_option(2)
+    assert (nl == 1) == single, nl
+    assert rel(out.cpu().numpy(), ref) <= MATVEC_TOL
+    assert torch.equal(out, out2)
+    monkeypatch.setenv("HEFF_CLUSTER_MATVEC", "0")
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        out3 = h.apply(xd.psi)
+        torch.cuda.synchronize()
+        assert h.get_option(2) >= 2
+    assert rel(out3.cpu().numpy(), ref) <= MATVEC_TOL
+
+
+def test_cluster_matvec_accumulate_and_lanczos(dev, orc):
+    """The cluster matvec's accumulating epilogue (MPO sums: out += H_t psi) and a Lanczos
+    solve on it (chain, m = 128), against the oracle."""
+    from paper_2007_14822_b200 import Heff, HeffSum
+    x = C.make("c2", m=128)
+    L, W1, W2, R, psi = x.numpy()
+    xd = x.to(dev)
+    ref = orc.heff_apply(L, W1, W2, R, psi)
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h1, Heff(xd.L, xd.W1, xd.W2, xd.R) as h2:
+        hs = HeffSum([h1, h2])
+        out = hs.apply(xd.psi)
+        torch.cuda.synchronize()
+        assert rel(out.cpu().numpy(), 2 * ref) <= MATVEC_TOL
+        hs.close()
+        v = xd.psi.clone()
+        r = h1.lanczos_ground(v, max_iter=10)
+    o = orc.lanczos_heff(L, W1, W2, R, psi, max_iter=10)
+    assert abs(r.energy - o.energy) <= ENERGY_TOL * max(1.0, abs(o.energy))

@@ -51,6 +51,14 @@ def show(t, labels, steps, title):
         print(f"  [{lab:20s}] min {d[:, k].min():7.2f}  median {np.median(d[:, k]):7.2f}  max {d[:, k].max():7.2f}")
 
 
+if (allt[: n // 2, 5] == 0).all() and (allt[: n // 2, 4] > 0).any():
+    # matvec_cluster_kernel (one launch): entry, GEMM1 done, MPO done, GEMM4 done, reduction done
+    m = allt[: n // 2][:, [0, 1, 2, 3, 4]]
+    m = m[m[:, 0] > 0]
+    t0 = m[:, 0].min()
+    show(m, ("entry", "GEMM1 done", "MPO -> T3 done", "GEMM4 done", "reduction done"),
+         ("GEMM1 (incl. wait)", "MPO epilogue", "GEMM4 passes", "cluster reduction"), f"{name} matvec_cluster")
+    sys.exit(0)
 show(f, ("entry", "after pdl_wait", "after main loop", "after T1 staging", "1st unit CSR", "1st unit done", "exit"),
      ("wait", "main loop", "T1 -> smem", "to 1st unit", "1st unit", "other units"), f"{name} gemm1_mpo_fused")
 if len(g):
