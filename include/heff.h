@@ -211,6 +211,14 @@ int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, con
  * component positive (reading R14). */
 int heff_tridiag_lowest(int j, const double* alpha, const double* beta, double* theta, double* y);
 
+/* Host-only: the O(j) per-step check lanczos_ground runs after every step -- the lowest
+ * eigenvalue of T_j by Sturm-sequence bisection to machine precision and |y_j[last]| of its
+ * unit eigenvector by two steps of inverse iteration (tridiagonal LU with partial pivoting);
+ * *ylast's sign is arbitrary.  The stopping test beta_j |y_j[last]| <= tol ||T_j|| and
+ * theta_out use it; the returned energy and Ritz vector come from heff_tridiag_lowest.
+ * Errors: HEFF_EINVAL (j < 1 or a null pointer). */
+int heff_tridiag_lowest_check(int j, const double* alpha, const double* beta, double* theta, double* ylast);
+
 /* ---- U(1) block sparsity (Sec. 7) -----------------
  * Declares conserved charges so heff_apply skips the GEMM k-blocks that are zero by
  * symmetry.  Conventions (reading R18): a bond index carries the total charge to

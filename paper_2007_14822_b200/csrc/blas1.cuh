@@ -362,4 +362,116 @@ __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* _
   }
 }
 
+// ------------------------------------------------------------------------------------
+// The same CGS2 step for short vectors (one block; n up to a few thousand entries).  The
+// step is bound by dependent memory latency there (cgs2_step_kernel's one-block path:
+// ~22 us + ~1 us per basis vector at n = 1024, ncu profiles/r02_c1_cgs2_ncu.md), so it is
+// organised around few dependent waits: thread i owns entries i, i + 512, ...; the basis
+// entries of 16 vectors are requested together (one latency per 16 vectors); the 16 partial
+// dot products of a batch are reduced by warp shuffles, then across the 16 warps by one
+// shuffle tree per vector (one warp per vector of the batch) -- fixed order, deterministic.
+// Same outputs and formulas as cgs2_step_kernel (beta^2 = ||w'||^2 - ||c2||^2); the dot
+// products are summed in a different fixed order.
+// ------------------------------------------------------------------------------------
+constexpr int kSmallStepThreads = 512;
+constexpr int kSmallStepQ = 16;  // basis vectors per batch
+constexpr int kSmallStepE = 8;   // entries per thread held in registers (n <= 4096)
+
+__global__ void __launch_bounds__(kSmallStepThreads) cgs2_step_small_kernel(
+    const double* __restrict__ V, int64_t ldv, int j, double* __restrict__ w, int64_t n, double* __restrict__ c1,
+    double* __restrict__ c2, double* __restrict__ alpha, double* __restrict__ beta, double* __restrict__ invb,
+    double* __restrict__ vnext) {
+  extern __shared__ double s_c[];  // [j + 1]
+  __shared__ double red[kSmallStepQ][kSmallStepThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  pdl_wait();  // w comes from the matvec kernel before (launched with programmatic serialization)
+  double x[kSmallStepE];  // this thread's entries of w (then w')
+#pragma unroll
+  for (int e = 0; e < kSmallStepE; ++e) {
+    const int64_t i = tid + (int64_t)e * kSmallStepThreads;
+    x[e] = i < n ? w[i] : 0.0;
+  }
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    // s_c[q] = V_q . w (q < j); in the second pass also s_c[j] = ||w'||^2
+    const int nd = j + pass;
+#pragma unroll 1
+    for (int q0 = 0; q0 < nd; q0 += kSmallStepQ) {
+      double acc[kSmallStepQ];
+#pragma unroll
+      for (int k = 0; k < kSmallStepQ; ++k) acc[k] = 0.0;
+#pragma unroll
+      for (int e = 0; e < kSmallStepE; ++e) {
+        const int64_t i = tid + (int64_t)e * kSmallStepThreads;
+        if (i < n) {
+          double v[kSmallStepQ];
+#pragma unroll
+          for (int k = 0; k < kSmallStepQ; ++k)
+            v[k] = (q0 + k < j) ? V[(int64_t)(q0 + k) * ldv + i] : x[e];  // q = j: w' itself
+#pragma unroll
+          for (int k = 0; k < kSmallStepQ; ++k) acc[k] = fma(v[k], x[e], acc[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kSmallStepQ; ++k) {
+        const double t = warp_sum(acc[k]);
+        if (lane == 0) red[k][warp] = t;
+      }
+      __syncthreads();
+      if (warp < kSmallStepQ && q0 + warp < nd) {
+        constexpr int kW = kSmallStepThreads / 32;
+        const double t = warp_sum(lane < kW ? red[warp][lane] : 0.0);
+        if (lane == 0) s_c[q0 + warp] = t;
+      }
+      __syncthreads();
+    }
+    double* cc = pass ? c2 : c1;
+    for (int q = tid; q < j; q += kSmallStepThreads) cc[q] = s_c[q];
+    double scale = 1.0;
+    if (pass) {
+      double nrm2 = s_c[j];
+      for (int q = 0; q < j; ++q) nrm2 = fma(-s_c[q], s_c[q], nrm2);
+      const double bt = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
+      const double ib = bt > 0.0 ? 1.0 / bt : 0.0;
+      if (tid == 0) {
+        alpha[j - 1] = c1[j - 1] + s_c[j - 1];
+        beta[j - 1] = bt;
+        invb[j - 1] = ib;
+      }
+      if (vnext) scale = ib;
+    }
+    // x -= V s_c, basis entries of 16 vectors in flight at a time
+#pragma unroll 1
+    for (int q0 = 0; q0 < j; q0 += kSmallStepQ) {
+#pragma unroll
+      for (int e = 0; e < kSmallStepE; ++e) {
+        const int64_t i = tid + (int64_t)e * kSmallStepThreads;
+        if (i < n) {
+          double v[kSmallStepQ];
+#pragma unroll
+          for (int k = 0; k < kSmallStepQ; ++k) v[k] = (q0 + k < j) ? V[(int64_t)(q0 + k) * ldv + i] : 0.0;
+#pragma unroll
+          for (int k = 0; k < kSmallStepQ; ++k)
+            if (q0 + k < j) x[e] = fma(-s_c[q0 + k], v[k], x[e]);
+        }
+      }
+    }
+    if (pass == 0 || !vnext) {
+#pragma unroll
+      for (int e = 0; e < kSmallStepE; ++e) {
+        const int64_t i = tid + (int64_t)e * kSmallStepThreads;
+        if (i < n) w[i] = x[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < kSmallStepE; ++e) {
+        const int64_t i = tid + (int64_t)e * kSmallStepThreads;
+        if (i < n) vnext[i] = x[e] * scale;
+      }
+    }
+    __syncthreads();  // s_c is rewritten by the next pass
+  }
+}
+
 }  // namespace heff

@@ -2196,6 +2196,12 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   const bool fused = !cplx && (p->comm == nullptr) && (cap <= 4096) &&
                      (n <= (int64_t(1) << 21) || getenv("HEFF_FUSED_STEP")) && getenv("HEFF_NO_FUSED_STEP") == nullptr;
   int step_grid = 0;
+  // vectors up to this length take the one-block step kernel when the grid is one block
+  // (HEFF_SMALL_STEP_N overrides; 0 = never)
+  static const int64_t small_step_max = [] {
+    const char* e = getenv("HEFF_SMALL_STEP_N");
+    return std::min<int64_t>(e ? (int64_t)atoll(e) : (int64_t)2048, (int64_t)kSmallStepThreads * kSmallStepE);
+  }();
   if (fused) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs2_step_kernel, kStepThreads,
@@ -2230,10 +2236,17 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       double* vnext = (j < cap) ? V + (int64_t)j * ldv : nullptr;
       int64_t nn = n;
       double* wp = w;
+      static const bool pdl_off = getenv("HEFF_NO_PDL") != nullptr;
+      if (n <= small_step_max) {
+        // short vectors: the one-block latency-optimised step (cgs2_step_small_kernel)
+        CK(launch_pdl(cgs2_step_small_kernel, dim3(1), dim3(kSmallStepThreads), sizeof(double) * (size_t)(j + 1), s,
+                      Vc, ldv_, jj, wp, nn, c1, c2, alpha, beta, invb, vnext));
+        ++p->total_launches;
+        return HEFF_OK;
+      }
       void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &alpha, &beta, &invb, &vnext};
       // cooperative (grid syncs) and, unless HEFF_NO_PDL, programmatic serialization: the
       // launch overlaps the matvec's last kernel, the body starts after griddepcontrol.wait
-      static const bool pdl_off = getenv("HEFF_NO_PDL") != nullptr;
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(step_grid);
       cfg.blockDim = dim3(kStepThreads);
@@ -2273,12 +2286,14 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     return HEFF_OK;
   };
   // scalar bookkeeping on the host: returns true to stop after step j
+  // (hnorm: Gershgorin bound of T_j, updated with the rows the new step changes)
   auto host_check = [&](int j) -> bool {
-    for (int i = 0; i < j; ++i) {
+    for (int i = std::max(0, j - 2); i < j; ++i) {
       const double gsh = std::fabs(ha[i]) + (i > 0 ? hb[i - 1] : 0.0) + hb[i];
       hnorm = std::max(hnorm, gsh);
     }
-    tridiag_lowest_last(j, ha.data(), hb.data(), &theta, &ylast);
+    if (!tridiag_lowest_fast(j, ha.data(), hb.data(), &theta, &ylast))
+      tridiag_lowest_last(j, ha.data(), hb.data(), &theta, &ylast);  // (never seen; QL as the fallback)
     if (o->theta_out) o->theta_out[j - 1] = theta;
     if (hb[j - 1] <= 1e-12 * hnorm) return true;  // breakdown: invariant subspace
     if (o->mode == 1 && hb[j - 1] * std::fabs(ylast) <= o->tol * hnorm) return true;
@@ -2287,19 +2302,29 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
 
   if (o->mode == 0) {
     // fixed steps: enqueue everything, read the scalars once, truncate at a breakdown
+    static const bool timing = getenv("HEFF_LANCZOS_TIMING") != nullptr;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     for (int j = 1; j <= cap; ++j) {
       CKR(step(j));
       CKR(mark_step(p, s));
     }
+    const auto t1 = clk::now();
     CK(cudaMemcpyAsync(h_a, alpha, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(h_b, beta, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
     CKR(comm_wait(p, s));
+    const auto t2 = clk::now();
     memcpy(ha.data(), h_a, sizeof(double) * cap);
     memcpy(hb.data(), h_b, sizeof(double) * cap);
     for (int j = 1; j <= cap; ++j) {
       j_done = j;
       if (host_check(j)) break;
     }
+    if (timing)
+      fprintf(stderr, "lanczos_ground fixed %d steps: enqueue %.1f us, wait %.1f us, host checks %.1f us\n", cap,
+              std::chrono::duration<double, std::micro>(t1 - t0).count(),
+              std::chrono::duration<double, std::micro>(t2 - t1).count(),
+              std::chrono::duration<double, std::micro>(clk::now() - t2).count());
   } else {
     // Converge mode.  Small vectors (<= 2^20 doubles, steps of ~0.1 ms) enqueue `batch`
     // steps per host round trip and test them in order: the stopping step j_done, T_j and
@@ -2581,6 +2606,16 @@ extern "C" int heff_env_update_right_qn(const heff_env_dims* dims, const double*
   if (!qn || !qn->q_in || !qn->q_out || !qn->qs || !qn->cl || !qn->cr)
     return set_err(HEFF_EINVAL, "heff_env_update_right_qn: null charge array");
   return env_right_impl(dims, R, B, W, Rout, qn, stream);
+}
+
+// Host-only: lanczos_ground's per-step check (Sturm bisection + inverse iteration, tridiag.h).
+extern "C" int heff_tridiag_lowest_check(int j, const double* alpha, const double* beta, double* theta,
+                                         double* ylast) {
+  if (j < 1 || !alpha || !theta || !ylast || (j > 1 && !beta))
+    return set_err(HEFF_EINVAL, "heff_tridiag_lowest_check: bad argument");
+  if (!tridiag_lowest_fast(j, alpha, beta, theta, ylast))
+    return set_err(HEFF_ECUDA, "heff_tridiag_lowest_check: inverse iteration failed");
+  return HEFF_OK;
 }
 
 // Host-only: the tridiagonal eigen-solve lanczos_ground uses (implicit QL, tridiag.h).

@@ -95,6 +95,7 @@ def lib() -> ctypes.CDLL:
         L.heff_set_penalty.argtypes = [vp, vp, ip, ctypes.c_double, vp]
         dp = ctypes.POINTER(ctypes.c_double)
         L.heff_tridiag_lowest.argtypes = [ip, dp, dp, dp, dp]
+        L.heff_tridiag_lowest_check.argtypes = [ip, dp, dp, dp, dp]
         L.heff_set_qn.argtypes = [vp, ctypes.POINTER(_QN)]
         L.heff_gemm.argtypes = [i64, i64, i64, vp, i64, vp, i64, ip, vp, i64, ip, ip, vp]
         L.heff_env_update_left.argtypes = [ctypes.POINTER(_EnvDims), vp, vp, vp, vp, vp]
@@ -112,7 +113,8 @@ def lib() -> ctypes.CDLL:
         for f in ("heff_dot", "heff_env_update_left_qn", "heff_env_update_right_qn", "heff_release_caches", "heff_svd_split_qn", "heff_apply_blocked", "heff_truncate_spectrum", "heff_svd_split", "heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "heff_destroy",
                   "heff_nccl_unique_id", "heff_set_option", "heff_get_option", "heff_last_timings",
                   "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
-                  "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z"):
+                  "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z",
+                  "heff_tridiag_lowest_check"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -123,7 +125,8 @@ EXPORTED = ("heff_create", "heff_apply", "heff_apply_host", "lanczos_ground", "h
             "heff_relayout_blocked", "heff_create_sum", "heff_set_penalty", "heff_env_update_left",
             "heff_env_update_right", "heff_tridiag_lowest", "heff_gemm", "heff_set_qn", "heff_create_z",
             "heff_svd_split", "heff_truncate_spectrum", "heff_apply_blocked", "heff_svd_split_qn",
-            "heff_release_caches", "heff_env_update_left_qn", "heff_env_update_right_qn", "heff_dot")
+            "heff_release_caches", "heff_env_update_left_qn", "heff_env_update_right_qn", "heff_dot",
+            "heff_tridiag_lowest_check")
 
 
 def _check(rc: int):
@@ -184,6 +187,20 @@ def tridiag_lowest(alpha, beta):
     _check(lib().heff_tridiag_lowest(j, a.ctypes.data_as(dp), b.ctypes.data_as(dp), ctypes.byref(th),
                                      y.ctypes.data_as(dp)))
     return th.value, y
+
+
+def tridiag_lowest_check(alpha, beta):
+    """libheff's per-step Lanczos check (Sturm bisection + inverse iteration; no GPU needed):
+    (theta, |y_last|)."""
+    import numpy as np
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    j = a.size
+    b = np.ascontiguousarray(np.append(np.asarray(beta, dtype=np.float64)[: max(0, j - 1)], 0.0), dtype=np.float64)
+    th, yl = ctypes.c_double(), ctypes.c_double()
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(lib().heff_tridiag_lowest_check(j, a.ctypes.data_as(dp), b.ctypes.data_as(dp), ctypes.byref(th),
+                                           ctypes.byref(yl)))
+    return th.value, abs(yl.value)
 
 
 def _env_qn(qn):

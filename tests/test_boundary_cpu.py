@@ -86,6 +86,56 @@ def test_library_tridiagonal_ql_vs_oracle_bisection_and_numpy(oracle_lib):
     assert abs(th - np.linalg.eigvalsh(np.diag([2.0, -1.0, 3.0]) + np.diag([0.0, 0.5], 1) + np.diag([0.0, 0.5], -1))[0]) < 1e-15
 
 
+def test_library_tridiagonal_per_step_check_vs_numpy():
+    """lanczos_ground's O(j) per-step check (Sturm bisection + inverse iteration) against
+    numpy.linalg.eigh: the lowest eigenvalue to machine precision and |y[last]| of its unit
+    eigenvector -- random T, Lanczos-like T of a Heisenberg-chain Hamiltonian (clustered
+    low end), a split T (zero off-diagonal), 1x1 and 2x2 closed forms; no GPU needed."""
+    import numpy as np
+    from paper_2007_14822_b200 import heff
+    rng = np.random.default_rng(12)
+    cases = []
+    for j in (3, 5, 20, 64, 150):
+        cases.append((rng.standard_normal(j) * 3.0, np.abs(rng.standard_normal(j - 1))))
+    # T_j of a Lanczos run on a random symmetric matrix with a clustered low spectrum
+    n = 300
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.concatenate([[-5.0, -4.999, -4.99], np.linspace(-4, 4, n - 3)])
+    H = (Q * lam) @ Q.T
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    V, al, be = [v], [], []
+    for k in range(60):
+        w = H @ V[-1]
+        al.append(V[-1] @ w)
+        for _ in range(2):
+            w -= np.array(V).T @ (np.array(V) @ w)
+        be.append(np.linalg.norm(w))
+        V.append(w / be[-1])
+    for j in (10, 30, 60):
+        cases.append((np.array(al[:j]), np.array(be[:j - 1])))
+    for a, b in cases:
+        T = np.diag(a) + np.diag(b, 1) + np.diag(b, -1)
+        ev, U = np.linalg.eigh(T)
+        scale = max(1.0, np.abs(a).max() + 2 * b.max())
+        th, yl = heff.tridiag_lowest_check(a, b)
+        assert abs(th - ev[0]) <= 8e-16 * scale * 4, (len(a), th, ev[0])
+        if ev[1] - ev[0] > 1e-6 * scale:   # the eigenvector is well defined
+            assert abs(yl - abs(U[-1, 0])) <= 1e-9 * max(1.0, 1.0 / (ev[1] - ev[0])), (len(a), yl, U[-1, 0])
+    # closed forms: 1x1; 2x2 [[a, b], [b, c]]
+    th, yl = heff.tridiag_lowest_check([1.5], [])
+    assert th == 1.5 and yl == 1.0
+    a0, c0, b0 = 1.0, 3.0, 0.5
+    lo = 0.5 * (a0 + c0) - np.hypot(0.5 * (a0 - c0), b0)
+    th, yl = heff.tridiag_lowest_check([a0, c0], [b0])
+    y = np.array([b0, lo - a0])
+    assert abs(th - lo) <= 1e-15 * 4 and abs(yl - abs(y[1]) / np.linalg.norm(y)) <= 1e-12
+    # split matrix: the lowest eigenvalue sits in the first block, its last component is 0
+    th, yl = heff.tridiag_lowest_check([-2.0, 1.0, 3.0], [0.3, 0.0])
+    ev, U = np.linalg.eigh(np.diag([-2.0, 1.0, 3.0]) + np.diag([0.3, 0.0], 1) + np.diag([0.3, 0.0], -1))
+    assert abs(th - ev[0]) <= 1e-14 and yl <= 1e-12
+
+
 def test_host_truncation_rule_matches_oracle_and_brute_force():
     """heff_truncate_spectrum (the rule heff_svd_split applies on the host, readings R20/R21)
     against the oracle's rule and SPEC.md's brute-force cut scan, host-only."""
