@@ -2206,11 +2206,12 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs2_step_kernel, kStepThreads,
                                                      sizeof(double) * (size_t)(cap + 1)));
-    // elements per thread (HEFF_STEP_EPT, default 2; round 1: 4): fewer = more blocks in
-    // flight (C1 41.6 -> 37.5 us, cylinder m = 128 91 -> 78-82 us per Lanczos step)
+    // elements per thread (HEFF_STEP_EPT, default 1; round 1: 4, then 2): fewer = more blocks
+    // in flight (C1 41.6 -> 37.5 us, cylinder m = 128 91 -> 78-82 us per Lanczos step at 2;
+    // at 1: cylinder m = 64 71.2 -> 67.1 us, chain m = 128 57.8 -> 55.2 us, C2 87.3 / 88.4 us)
     static const int ept = [] {
       const char* e = getenv("HEFF_STEP_EPT");
-      return e ? std::max(1, atoi(e)) : 2;
+      return e ? std::max(1, atoi(e)) : 1;
     }();
     const int64_t want = std::max<int64_t>(1, (n + (int64_t)ept * kStepThreads - 1) / ((int64_t)ept * kStepThreads));
     step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * g_num_sms, want));
