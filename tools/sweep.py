@@ -1,5 +1,5 @@
-"""Per-config timing of libheff on one GPU: H_eff.psi matvec and Lanczos-step latency for
-C1..C4 (and C5 when it fits).  Writes one JSON object per config (stdout, and --out).
+"""Per-config timing of libheff on one GPU: H_eff.psi matvec (single launch, and back to back
+as lanczos_ground enqueues them) and Lanczos-step latency for C1..C4 (and C5 when it fits).  Writes one JSON object per config (stdout, and --out).
 
     python tools/sweep.py [--configs c1,c2,c3,c4] [--reps 20] [--out profiles/sweep.json]
 """
@@ -40,6 +40,22 @@ def time_matvec(h, psi, out, reps):
     return ts[len(ts) // 2]
 
 
+def time_matvec_b2b(h, psi, out, n):
+    """Back-to-back matvecs (the way lanczos_ground enqueues them: no host wait between
+    launches): device time of n consecutive applies / n."""
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        h.apply(psi, out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(n):
+        h.apply(psi, out)
+    e1.record(s)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / n
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c1,c2,c3,c4")
@@ -60,6 +76,8 @@ def main():
         with Heff(x.L, x.W1, x.W2, x.R) as h:
             out = torch.empty_like(x.psi)
             ms = time_matvec(h, x.psi, out, reps)
+            ms_b2b = time_matvec_b2b(h, x.psi, out, 3 if big else 200)
+            h_launches = h.get_option(2)
             h.set_option(OPT_PROFILE, 1)
             h.apply(x.psi, out)
             g1, mpo, g4, n = h.last_timings()
@@ -74,7 +92,9 @@ def main():
             lz = (time.perf_counter() - t0) / steps * 1e3
         g1f = 2.0 * d["mL"] * d["kL"] * d["mL"] * d["d1"] * d["d2"] * d["mR"]
         g4f = C.gemm_flops_per_matvec(d) - g1f
-        row = {"config": spec, **d, "gen_s": round(gen_s, 2), "matvec_ms": ms, "matvecs_per_s": 1e3 / ms,
+        row = {"config": spec, **d, "gen_s": round(gen_s, 2), "matvec_ms": ms, "matvec_b2b_ms": ms_b2b,
+               "tflops_b2b": flops / ms_b2b / 1e9, "frac_peak_b2b": flops / ms_b2b / 1e9 / PEAK,
+               "launches_per_matvec": h_launches, "matvecs_per_s": 1e3 / ms,
                "tflops": flops / ms / 1e9, "frac_peak": flops / ms / 1e9 / PEAK,
                "gemm_first_ms": g1, "mpo_ms": mpo, "gemm_last_ms": g4,
                "gemm_first_tflops": g1f / g1 / 1e9 if g1 else None, "gemm_last_tflops": g4f / g4 / 1e9 if g4 else None,
