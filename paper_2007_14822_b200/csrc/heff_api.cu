@@ -2216,6 +2216,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     const int64_t want = std::max<int64_t>(1, (n + (int64_t)ept * kStepThreads - 1) / ((int64_t)ept * kStepThreads));
     step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * g_num_sms, want));
   }
+  std::vector<cudaEvent_t>* phase_ev = nullptr;  // HEFF_LANCZOS_TIMING >= 2 (fixed mode)
   auto step = [&](int j) -> int {  // j = 1-based step: v_j = V[j-1]
     double* vj = V + (int64_t)(j - 1) * ldv;
     if (compact) {
@@ -2229,6 +2230,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     } else {
       CKR(matvec_local(p, vj, w, s));
     }
+    if (phase_ev) cudaEventRecord((*phase_ev)[2 * j - 1], s);
     if (fused) {
       const double* Vc = V;
       int64_t ldv_ = ldv;
@@ -2303,12 +2305,22 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
 
   if (o->mode == 0) {
     // fixed steps: enqueue everything, read the scalars once, truncate at a breakdown
-    static const bool timing = getenv("HEFF_LANCZOS_TIMING") != nullptr;
+    static const int timing = getenv("HEFF_LANCZOS_TIMING") ? atoi(getenv("HEFF_LANCZOS_TIMING")) : 0;
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
+    // timing >= 2: events between the steps' phases (serialises the launches: a breakdown,
+    // not the pipelined time)
+    std::vector<cudaEvent_t> tev;
+    if (timing >= 2) {
+      tev.resize(2 * (size_t)cap + 1);
+      for (auto& e : tev) cudaEventCreate(&e);
+      cudaEventRecord(tev[0], s);
+      phase_ev = &tev;
+    }
     for (int j = 1; j <= cap; ++j) {
       CKR(step(j));
       CKR(mark_step(p, s));
+      if (timing >= 2) cudaEventRecord(tev[2 * j], s);
     }
     const auto t1 = clk::now();
     CK(cudaMemcpyAsync(h_a, alpha, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
@@ -2320,6 +2332,20 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     for (int j = 1; j <= cap; ++j) {
       j_done = j;
       if (host_check(j)) break;
+    }
+    if (timing >= 2) {
+      double tm = 0, tc = 0;
+      for (int j = 1; j <= cap; ++j) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, tev[2 * j - 2], tev[2 * j - 1]);
+        cudaEventElapsedTime(&b, tev[2 * j - 1], tev[2 * j]);
+        tm += a;
+        tc += b;
+      }
+      fprintf(stderr, "lanczos_ground phases (serialised): matvec %.1f us, orthogonalisation %.1f us per step\n",
+              tm * 1e3 / cap, tc * 1e3 / cap);
+      for (auto& e : tev) cudaEventDestroy(e);
+      phase_ev = nullptr;
     }
     if (timing)
       fprintf(stderr, "lanczos_ground fixed %d steps: enqueue %.1f us, wait %.1f us, host checks %.1f us\n", cap,

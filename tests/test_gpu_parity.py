@@ -226,6 +226,26 @@ def test_lanczos_fixed_steps_parity(dev, orc, name, steps):
     assert abs(abs(np.vdot(v, o.x)) - 1.0) < 1e-8
 
 
+@pytest.mark.parametrize("variant", ["cooperative", "separate"])
+def test_lanczos_step_kernels_c2(dev, orc, variant, monkeypatch):
+    """The single-GPU CGS2 step forms on a mid-size vector (C2, n = 262 144), 24 fixed steps
+    against the oracle: the fused cooperative step (default) and the separate multi-dot /
+    multi-axpy kernels (HEFF_NO_FUSED_STEP); bitwise run to run."""
+    if variant == "separate":
+        monkeypatch.setenv("HEFF_NO_FUSED_STEP", "1")
+    x = C.make("c2")
+    L, W1, W2, R, psi = x.numpy()
+    o = orc.lanczos_heff(L, W1, W2, R, psi, max_iter=24)
+    r, v = gpu_lanczos(x, dev, 24)
+    assert r.iters == o.iters == 24
+    assert abs(r.energy - o.energy) <= ENERGY_TOL * max(1.0, abs(o.energy))
+    np.testing.assert_allclose(r.alpha, o.alpha, rtol=0, atol=1e-10)
+    np.testing.assert_allclose(r.beta, o.beta, rtol=0, atol=1e-10)
+    assert abs(abs(np.vdot(v, o.x)) - 1.0) < 1e-8
+    r2, v2 = gpu_lanczos(x, dev, 24)   # deterministic
+    assert r2.alpha == r.alpha and np.array_equal(v2, v)
+
+
 def test_lanczos_converge_c2(dev, orc):
     x = C.make("c2")
     L, W1, W2, R, psi = x.numpy()
