@@ -474,4 +474,99 @@ __global__ void __launch_bounds__(kSmallStepThreads) cgs2_step_small_kernel(
   }
 }
 
+// ------------------------------------------------------------------------------------
+// The CGS2 step with the basis resident in shared memory (n <= 2048, j <= 31, j n 8 bytes
+// <= kSmemStepMaxBytes: C1's whole Lanczos run).  The short-vector step is bound by
+// dependent memory latency (one-block kernels: ~0.75 us per basis vector and step, i.e.
+// ~4 round trips to L2 per vector -- measured with heff_debug_launch_probe), so here the
+// j basis vectors arrive by j bulk copies (TMA, one mbarrier) right after the dependency
+// wait -- one latency per step -- and both passes' dot products and updates read them from
+// shared memory.  Each partial dot product is reduced by a warp shuffle tree, then across the
+// 32 warps by warp q (one shuffle tree per vector, q <= 31): fixed order, deterministic.
+// Same outputs and formulas as cgs2_step_kernel.
+// ------------------------------------------------------------------------------------
+constexpr int kSmemStepThreads = 1024;
+constexpr int kSmemStepMaxJ = 31;
+constexpr int kSmemStepMaxBytes = 200 * 1024;
+
+__global__ void __launch_bounds__(kSmemStepThreads) cgs2_step_smem_kernel(
+    const double* __restrict__ V, int64_t ldv, int j, double* __restrict__ w, int64_t n, double* __restrict__ c1,
+    double* __restrict__ c2, double* __restrict__ alpha, double* __restrict__ beta, double* __restrict__ invb,
+    double* __restrict__ vnext) {
+  extern __shared__ __align__(16) double vs[];  // [j][np]
+  __shared__ double red[kSmemStepMaxJ + 1][32];
+  __shared__ double s_c[kSmemStepMaxJ + 1];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int np = (int)((n + 1) & ~int64_t(1));  // 16-byte rows (ldv >= np: the pitch is a multiple of 32)
+  constexpr int E = 2;                            // entries per thread (n <= 2048)
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();  // w (matvec) and v_{j-1} (previous step) come from the kernels before
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)(j * np * 8));
+    for (int q = 0; q < j; ++q) bulk_load(vs + (int64_t)q * np, V + (int64_t)q * ldv, (uint32_t)(np * 8), &bar);
+  }
+  double x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t i = tid + (int64_t)e * kSmemStepThreads;
+    x[e] = i < n ? w[i] : 0.0;
+  }
+  mbar_wait(&bar, 0);
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const int nd = j + pass;  // pass 1 also ||w'||^2 (q = j)
+#pragma unroll 4
+    for (int q = 0; q < nd; ++q) {
+      double t = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int64_t i = tid + (int64_t)e * kSmemStepThreads;
+        if (i < n) t = fma(q < j ? vs[(int64_t)q * np + i] : x[e], x[e], t);
+      }
+      t = warp_sum(t);
+      if (lane == 0) red[q][warp] = t;
+    }
+    __syncthreads();
+    if (warp < nd) {
+      const double t = warp_sum(red[warp][lane]);
+      if (lane == 0) s_c[warp] = t;
+    }
+    __syncthreads();
+    double* cc = pass ? c2 : c1;
+    if (tid < j) cc[tid] = s_c[tid];
+    double scale = 1.0;
+    if (pass) {
+      double nrm2 = s_c[j];
+      for (int q = 0; q < j; ++q) nrm2 = fma(-s_c[q], s_c[q], nrm2);
+      const double bt = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
+      const double ib = bt > 0.0 ? 1.0 / bt : 0.0;
+      if (tid == 0) {
+        alpha[j - 1] = c1[j - 1] + s_c[j - 1];
+        beta[j - 1] = bt;
+        invb[j - 1] = ib;
+      }
+      if (vnext) scale = ib;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t i = tid + (int64_t)e * kSmemStepThreads;
+      if (i < n) {
+        double xe = x[e];
+        for (int q = 0; q < j; ++q) xe = fma(-s_c[q], vs[(int64_t)q * np + i], xe);
+        x[e] = xe;
+        if (pass == 0 || !vnext)
+          w[i] = xe;
+        else
+          vnext[i] = xe * scale;
+      }
+    }
+    __syncthreads();  // s_c and red are rewritten by the next pass
+  }
+}
+
 }  // namespace heff

@@ -531,6 +531,7 @@ int init_device_once() {
   CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, 4>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgCl4::kSmemBytes));
   CK(cudaFuncSetAttribute(cgs2_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+  CK(cudaFuncSetAttribute(cgs2_step_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemStepMaxBytes));
   g_dev_inited.fetch_or(bit, std::memory_order_release);
   return HEFF_OK;
 }
@@ -2216,6 +2217,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     const int64_t want = std::max<int64_t>(1, (n + (int64_t)ept * kStepThreads - 1) / ((int64_t)ept * kStepThreads));
     step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * g_num_sms, want));
   }
+  static const bool no_smem_step = getenv("HEFF_NO_SMEM_STEP") != nullptr;
   std::vector<cudaEvent_t>* phase_ev = nullptr;  // HEFF_LANCZOS_TIMING >= 2 (fixed mode)
   auto step = [&](int j) -> int {  // j = 1-based step: v_j = V[j-1]
     double* vj = V + (int64_t)(j - 1) * ldv;
@@ -2240,6 +2242,15 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       int64_t nn = n;
       double* wp = w;
       static const bool pdl_off = getenv("HEFF_NO_PDL") != nullptr;
+      const int64_t np = (n + 1) & ~int64_t(1);
+      if (n <= 2 * kSmemStepThreads && j <= kSmemStepMaxJ && (int64_t)j * np * 8 <= kSmemStepMaxBytes &&
+          !no_smem_step) {
+        // short vectors, basis resident in shared memory (cgs2_step_smem_kernel)
+        CK(launch_pdl(cgs2_step_smem_kernel, dim3(1), dim3(kSmemStepThreads), (size_t)(j * np * 8), s, Vc, ldv_, jj, wp,
+                      nn, c1, c2, alpha, beta, invb, vnext));
+        ++p->total_launches;
+        return HEFF_OK;
+      }
       if (n <= small_step_max) {
         // short vectors: the one-block latency-optimised step (cgs2_step_small_kernel)
         CK(launch_pdl(cgs2_step_small_kernel, dim3(1), dim3(kSmallStepThreads), sizeof(double) * (size_t)(j + 1), s,
@@ -2674,6 +2685,68 @@ extern "C" int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64
 // debug: enable (n > 0: a device buffer of 4 n timers) / read back the fused small-bond
 // kernel's per-CTA %globaltimer stamps (entry, after the dependency wait, after the main
 // loop, exit); host buffer `out` of 4 n values, n = 0 disables
+// Diagnostics (not in heff.h): launch-cost probe for the small-vector Lanczos kernels.  which:
+// 0 empty kernel, 1 empty kernel with PDL + griddepcontrol.wait, 2 cgs2_step_small_kernel
+// (n, j) with PDL, 3 the same without PDL, 4 cgs2_step_kernel one block; `reps` launches back
+// to back, device time per launch in *us.  Scratch buffers are allocated and freed here.
+__global__ void probe_empty_kernel(int x) {
+  if (x == 12345) printf("x");
+}
+__global__ void probe_empty_pdl_kernel(int x) {
+  pdl_wait();
+  if (x == 12345) printf("x");
+}
+extern "C" int heff_debug_launch_probe(int which, int64_t n, int j, int reps, float* us) {
+  CKR(init_device_once());
+  double* buf = nullptr;
+  const int64_t ldv = (n + 31) / 32 * 32;
+  CK(cudaMalloc(&buf, sizeof(double) * (size_t)(ldv * (j + 2) + 64 * 1024)));
+  CK(cudaMemset(buf, 0, sizeof(double) * (size_t)(ldv * (j + 2) + 64 * 1024)));
+  double* V = buf;
+  double* w = buf + ldv * (j + 1);
+  double* sc = buf + ldv * (j + 2);
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto launch = [&]() -> cudaError_t {
+    switch (which) {
+      case 0: probe_empty_kernel<<<1, 32, 0, s>>>(0); return cudaGetLastError();
+      case 1: return launch_pdl(probe_empty_pdl_kernel, dim3(1), dim3(32), 0, s, 0);
+      case 2:
+        return launch_pdl(cgs2_step_small_kernel, dim3(1), dim3(kSmallStepThreads), sizeof(double) * (size_t)(j + 1), s,
+                          (const double*)V, ldv, j, w, n, sc, sc + 4096, sc + 8192, sc + 12288, sc + 16384,
+                          V + (int64_t)j * ldv);
+      case 3:
+        cgs2_step_small_kernel<<<1, kSmallStepThreads, sizeof(double) * (size_t)(j + 1), s>>>(
+            V, ldv, j, w, n, sc, sc + 4096, sc + 8192, sc + 12288, sc + 16384, V + (int64_t)j * ldv);
+        return cudaGetLastError();
+      case 5:
+        return launch_pdl(cgs2_step_smem_kernel, dim3(1), dim3(kSmemStepThreads), (size_t)(j * ((n + 1) & ~1ll) * 8), s,
+                          (const double*)V, ldv, j, w, n, sc, sc + 4096, sc + 8192, sc + 12288, sc + 16384,
+                          V + (int64_t)j * ldv);
+      default:
+        cgs2_step_kernel<<<1, kStepThreads, sizeof(double) * (size_t)(j + 1), s>>>(
+            V, ldv, j, w, n, sc + 20480, 4096, sc, sc + 4096, sc + 8192, sc + 12288, sc + 16384, V + (int64_t)j * ldv);
+        return cudaGetLastError();
+    }
+  };
+  for (int i = 0; i < 3; ++i) CK(launch());
+  cudaEventRecord(e0, s);
+  for (int i = 0; i < reps; ++i) CK(launch());
+  cudaEventRecord(e1, s);
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *us = ms * 1e3f / (float)reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(s);
+  cudaFree(buf);
+  return HEFF_OK;
+}
+
 extern "C" int heff_debug_fused_timestamps(int n, unsigned long long* out) {
   if (const char* e = getenv("HEFF_DEBUG_FUSED_MODE")) g_fused_dbg_mode = atoi(e);
   if (n <= 0) {
