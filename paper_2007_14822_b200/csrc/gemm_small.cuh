@@ -320,19 +320,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 // and T3 never leave the SM; no dependency between CTAs except the final reduction.
 // Per CTA: GEMM1 2 (TA kL) (d1 d2 TB) mL flops + GEMM4 2 (TA d1 d2) mR (kR TB) flops (equal
 // for mL = mR, kL = kR); at C2 (m = 256, 16 a' blocks x 8 b blocks) 128 CTAs in 16 clusters.
-// Shapes: TA d1 d2 == 64 (the chain's kL = 5, d = 2: TA = 16), kR TB <= 160, mR / TB <= 8.
-constexpr int kMvcM4 = 64;                 // GEMM4 rows per cluster: TA a' x (s1', s2')
+// Shapes: M4 = TA d1 d2 in {16, 32, 64} (chain kL = 5, d = 2: TA = 16, M4 = 64; the k = 20
+// cylinder: TA = 4, M4 = 16), M4 kR TB doubles <= 80 KB, CS = mR / TB in {1, 2, 4, 8}.
+constexpr int kMvcM4Max = 64;              // GEMM4 rows per cluster (M4 = TA d1 d2 in {16, 32, 64})
 constexpr int kMvcNP = 128;                // GEMM4 columns (b') per pass (two passes at mR = 256)
 constexpr int kMvcSt1 = 4, kMvcSt4 = 2;    // GEMM1 ring (L + psi stages), GEMM4 ring (R stages)
 constexpr int kMvcRing1 = kMvcSt1 * kFusedStageBytes;  // GEMM1 ring, then the T1 tile, then partial 0
 constexpr int kMvcT3Bytes = 81920;         // T3 tile = GEMM4's A operand (64 rows x kR TB <= 160), then partial 1
 constexpr int kMvcRStage = kMvcNP * 128;   // 128 rows of R x 16 k
 constexpr int kMvcPartPitch = 136;         // doubles per partial row (conflict-free double2 stores)
-constexpr int kMvcCsrRows = 64, kMvcCsrNnz = 256;  // CSR staged in shared memory up to these (else read via L1)
+constexpr int kMvcCsrRows = 128, kMvcCsrNnz = 256;  // CSR staged in shared memory up to these (else read via L1)
 constexpr int kMvcCsrBytes = (kMvcCsrRows + 1) * 4 + kMvcCsrNnz * 12 + 16;
 constexpr int kMvcSmemBytes = kMvcRing1 + kMvcT3Bytes + kMvcSt4 * kMvcRStage + kMvcCsrBytes +
                               2 * (kMvcSt1 + kMvcSt4) * 8 + 1024;
-static_assert(kMvcM4 * kMvcPartPitch * 8 <= kMvcT3Bytes && kFusedBM * kFusedEpiPitch * 8 <= kMvcRing1,
+static_assert(kMvcM4Max * kMvcPartPitch * 8 <= kMvcT3Bytes && kFusedBM * kFusedEpiPitch * 8 <= kMvcRing1,
               "T1 tile and partials fit the freed regions");
 static_assert(kMvcSmemBytes <= 232448, "shared memory");
 static_assert(kMvcRing1 % 1024 == 0 && kMvcT3Bytes % 1024 == 0 && kMvcRStage % 1024 == 0, "TMA stage alignment");
@@ -340,10 +341,10 @@ static_assert(kMvcRing1 % 1024 == 0 && kMvcT3Bytes % 1024 == 0 && kMvcRStage % 1
 // Cluster reduction of matvec_cluster_kernel: rank tb sums rows [tb RR, tb RR + RR), RR = 64 / CS, of
 // the CS partials (pass p's partial at the same shared offset `base` in every CTA of the
 // cluster) in rank order; all CS loads of a thread's pairs are in flight before the adds.
-template <int CS>
+template <int M4, int CS>
 __device__ __forceinline__ void mvc_reduce(uint32_t base, int tb, int p, double* __restrict__ out, int64_t row0,
                                            int mR, int accumulate) {
-  constexpr int RR = kMvcM4 / CS;            // rows owned by this CTA
+  constexpr int RR = M4 / CS;                // rows owned by this CTA
   constexpr int NPAIR = RR * (kMvcNP / 2);   // (row, column pair) items of the pass
   constexpr int NIT = (NPAIR + 255) / 256;   // per consumer thread
   double vx[NIT][CS], vy[NIT][CS];
@@ -381,6 +382,7 @@ __device__ __forceinline__ void mvc_reduce(uint32_t base, int tb, int p, double*
   }
 }
 
+template <int M4>
 __global__ void __launch_bounds__(kFusedThreads, 1)
     matvec_cluster_kernel(const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmPsi,
                           const __grid_constant__ CUtensorMap tmR, double* __restrict__ out, int mL, int mR, int kL,
@@ -398,7 +400,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   };
   stamp(0);
   constexpr int MI = kFusedWM / 8, NJ = kFusedWN / 8;  // GEMM1 warp tile 40 x 32
-  constexpr int MI4 = 4, NJ4 = 4;                      // GEMM4 warp tile 32 x 32 (2 x 4 warps)
+  // GEMM4 warp tiles: M4 = 64: 2 x 4 warps of 32 x 32; 32: 1 x 8 of 32 x 16; 16: 1 x 8 of 16 x 16
+  constexpr int WM4 = M4 >= 64 ? 32 : M4, WARPS_M4 = M4 / WM4, WN4 = 128 / (8 / WARPS_M4);
+  constexpr int MI4 = WM4 / 8, NJ4 = WN4 / 8;
+  static_assert(M4 == 16 || M4 == 32 || M4 == 64, "M4");
   constexpr int kCons = kFusedConsumerWarps * 32;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -581,7 +586,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         // o = (s', w2): s' = o / kR
         const int sp = o / kR, w2 = o - sp * kR;
         const int k = w2 * TB + 2 * bp;
-        const uint32_t kbase = smem_u32(t3) + (uint32_t)((k >> 4) * (kMvcM4 * 128));
+        const uint32_t kbase = smem_u32(t3) + (uint32_t)((k >> 4) * (M4 * 128));
         const int ch = (k & 15) >> 1;
 #pragma unroll
         for (int q = 0; q < kFusedAlChunk; ++q)
@@ -595,7 +600,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     consumers_bar(kCons);  // T3 complete
     // ---- GEMM4 partial: part[(a' s')][b'] = T3[(a' s')][(w2 b)] R[b'][(w2 b)], two passes of 128 b'
     {
-      const int wm4 = (warp / 4) * 32, wn4 = (warp % 4) * 32;
+      const int wm4 = (warp / (8 / WARPS_M4)) * WM4, wn4 = (warp % (8 / WARPS_M4)) * WN4;
       const uint32_t offA4 = (wm4 + gs) * 128 + ((t ^ gs) << 4);
       const uint32_t offB4 = (wn4 + gs) * 128 + ((t ^ gs) << 4);
       const uint32_t rbase = smem_u32(rring), t3base = smem_u32(t3);
@@ -609,7 +614,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         for (int kb = 0; kb < kb4n; ++kb, ++it) {
           const int stage = it % kMvcSt4;
           mbar_wait(&full4[stage], (it / kMvcSt4) & 1);
-          dmma_stage<MI4, NJ4, true>(acc, t3base + kb * (kMvcM4 * 128), rbase + stage * kMvcRStage, offA4, offB4,
+          dmma_stage<MI4, NJ4, true>(acc, t3base + kb * (M4 * 128), rbase + stage * kMvcRStage, offA4, offB4,
                                      wn4, g, t);
           fence_proxy_async();
           __syncwarp();
@@ -631,17 +636,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     stamp(3);
   }
-  // ---- cluster reduction: rank tb owns rows [64 tb / CS, 64 (tb+1) / CS) of the a' block (CS | 64)
+  // ---- cluster reduction: rank tb owns rows [M4 tb / CS, M4 (tb+1) / CS) of the a' block (CS | M4)
   cluster_sync_all();  // every CTA's partials are in its shared memory
   {
-    const int64_t row0 = (int64_t)ta * kMvcM4;
+    const int64_t row0 = (int64_t)ta * M4;
     for (int p = 0; p < npass; ++p) {
       const uint32_t base = smem_u32(p == 0 ? region1 : t3);
       switch (CS) {
-        case 1: mvc_reduce<1>(base, tb, p, out, row0, mR, accumulate); break;
-        case 2: mvc_reduce<2>(base, tb, p, out, row0, mR, accumulate); break;
-        case 4: mvc_reduce<4>(base, tb, p, out, row0, mR, accumulate); break;
-        default: mvc_reduce<8>(base, tb, p, out, row0, mR, accumulate); break;
+        case 1: mvc_reduce<M4, 1>(base, tb, p, out, row0, mR, accumulate); break;
+        case 2: mvc_reduce<M4, 2>(base, tb, p, out, row0, mR, accumulate); break;
+        case 4: mvc_reduce<M4, 4>(base, tb, p, out, row0, mR, accumulate); break;
+        default: mvc_reduce<M4, 8>(base, tb, p, out, row0, mR, accumulate); break;
       }
     }
   }

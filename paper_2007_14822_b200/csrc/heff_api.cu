@@ -364,7 +364,7 @@ static int max_active_mvc_clusters(int cs) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, matvec_cluster_kernel, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, matvec_cluster_kernel<64>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       n = -1;  // unknown: never choose the cluster matvec
     }
@@ -521,7 +521,9 @@ int init_device_once() {
   CK(cudaFuncSetAttribute(mpo_apply_kernel<2, 16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMpoSmemBytes));
   CK(cudaFuncSetAttribute(heff_small_matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallMvMaxSmem));
   CK(cudaFuncSetAttribute(gemm1_mpo_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemBytes));
-  CK(cudaFuncSetAttribute(matvec_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMvcSmemBytes));
+  CK(cudaFuncSetAttribute(matvec_cluster_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMvcSmemBytes));
+  CK(cudaFuncSetAttribute(matvec_cluster_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMvcSmemBytes));
+  CK(cudaFuncSetAttribute(matvec_cluster_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMvcSmemBytes));
   CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, false, 2>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, CfgCl2::kSmemBytes));
   CK(cudaFuncSetAttribute(gemm_cluster_splitk_kernel<64, 64, 32, 16, kClStages, true, 2>,
@@ -1015,8 +1017,10 @@ extern "C" int heff_create(heff_plan* out, const heff_dims* dims, const double* 
           // m = 128 39.0 -> 31.9 us, m = 64 25.1 / 25.7 us (equal); C2 (16 clusters of 8) does not
           // fit (15 co-resident) and keeps the two-kernel form
           const int64_t cs = d.mR / TB;
-          bool mvc = TA * dd == kMvcM4 && d.kR * TB * kMvcM4 * 8 <= kMvcT3Bytes && (d.kR * TB) % kGemmBK == 0 &&
-                     (cs == 1 || cs == 2 || cs == 4 || cs == 8) && tiles <= g_num_sms && (d.kR * d.mR) % 2 == 0 &&
+          const int64_t M4 = TA * dd;
+          bool mvc = (M4 == 16 || M4 == 32 || M4 == 64) && d.kR * TB * M4 * 8 <= kMvcT3Bytes &&
+                     (d.kR * TB) % kGemmBK == 0 && (cs == 1 || cs == 2 || cs == 4 || cs == 8) && cs <= M4 &&
+                     tiles <= g_num_sms && (d.kR * d.mR) % 2 == 0 &&
                      (reinterpret_cast<uintptr_t>(R) & 15) == 0 && d.mR <= 2 * kMvcNP &&
                      d.mL / TA <= max_active_mvc_clusters((int)cs);
           if (const char* e = getenv("HEFF_CLUSTER_MATVEC")) mvc = mvc && atoi(e) != 0;
@@ -1345,10 +1349,12 @@ static int apply_orderA(heff_plan_s* p, const double* psi, double* out, cudaStre
       cfg.attrs = attr;
       cfg.numAttrs = 2;
       CKR(prof_mark(p, 0, s));
-      CK(cudaLaunchKernelEx(&cfg, matvec_cluster_kernel, p->fmapL, p->fmapPsi, p->fmapR, out, (int)d.mL, (int)d.mR,
-                            (int)d.kL, (int)d.kR, (int)dd, (int)__builtin_ctz((unsigned)dd), p->fusedTA, p->fusedTB,
-                            (int)(dd * d.kR), (const int*)p->csrA.d_rowptr, (const int*)p->csrA.d_col,
-                            (const double*)p->csrA.d_val, accumulate, g_fused_dbg));
+      const int M4 = p->fusedTA * (int)dd;
+      auto kern = M4 == 64 ? matvec_cluster_kernel<64> : (M4 == 32 ? matvec_cluster_kernel<32> : matvec_cluster_kernel<16>);
+      CK(cudaLaunchKernelEx(&cfg, kern, p->fmapL, p->fmapPsi, p->fmapR, out, (int)d.mL, (int)d.mR, (int)d.kL, (int)d.kR,
+                            (int)dd, (int)__builtin_ctz((unsigned)dd), p->fusedTA, p->fusedTB, (int)(dd * d.kR),
+                            (const int*)p->csrA.d_rowptr, (const int*)p->csrA.d_col, (const double*)p->csrA.d_val,
+                            accumulate, g_fused_dbg));
       ++*nl;
       CKR(prof_mark(p, 1, s));
       CKR(prof_mark(p, 2, s));

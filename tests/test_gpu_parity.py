@@ -555,6 +555,10 @@ CLUSTER_CASES = {   # case: (inputs, runs as one cluster launch)
     "mL128_mR256": (lambda: C.random_dense(dict(mL=128, d1=2, d2=2, mR=256, kL=5, kM=4, kR=5), seed=42), True),
     "m64": (lambda: C.random_dense(dict(mL=64, d1=2, d2=2, mR=64, kL=5, kM=2, kR=5), seed=43), True),
     "mR32": (lambda: C.random_dense(dict(mL=96, d1=2, d2=2, mR=32, kL=5, kM=5, kR=5), seed=44), True),
+    # the k = 20 cylinder (TA = 4 a' per fat tile: 16 GEMM4 rows per cluster, 20 w2 x 32 b per
+    # CTA's K-slice): m = 64 clusters of 2, m = 128 32 clusters of 4
+    "cyl_m64": (lambda: C.make("c4", m=64), True),
+    "cyl_m128": (lambda: C.make("c4", m=128), True),
     # clusters of 6 (not a divisor of 64) and C2's 16 clusters of 8 (more than the 15 that are
     # co-resident on a B200) fall back to the two-kernel form
     "mR192": (lambda: C.random_dense(dict(mL=256, d1=2, d2=2, mR=192, kL=5, kM=3, kR=5), seed=41), False),
