@@ -2691,10 +2691,11 @@ extern "C" int heff_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64
 // debug: enable (n > 0: a device buffer of 4 n timers) / read back the fused small-bond
 // kernel's per-CTA %globaltimer stamps (entry, after the dependency wait, after the main
 // loop, exit); host buffer `out` of 4 n values, n = 0 disables
-// Diagnostics (not in heff.h): launch-cost probe for the small-vector Lanczos kernels.  which:
+// Diagnostics (not in heff.h): launch-cost probe for the Lanczos step kernels.  which:
 // 0 empty kernel, 1 empty kernel with PDL + griddepcontrol.wait, 2 cgs2_step_small_kernel
-// (n, j) with PDL, 3 the same without PDL, 4 cgs2_step_kernel one block; `reps` launches back
-// to back, device time per launch in *us.  Scratch buffers are allocated and freed here.
+// (n, j) with PDL, 3 the same without PDL, 4 cgs2_step_kernel one block, 5 cgs2_step_smem_kernel,
+// 6 cgs2_step_kernel cooperative on its lanczos_ground grid; `reps` launches back to back, device
+// time per launch in *us.  Scratch buffers are allocated and freed here.
 __global__ void probe_empty_kernel(int x) {
   if (x == 12345) printf("x");
 }
@@ -2706,8 +2707,9 @@ extern "C" int heff_debug_launch_probe(int which, int64_t n, int j, int reps, fl
   CKR(init_device_once());
   double* buf = nullptr;
   const int64_t ldv = (n + 31) / 32 * 32;
-  CK(cudaMalloc(&buf, sizeof(double) * (size_t)(ldv * (j + 2) + 64 * 1024)));
-  CK(cudaMemset(buf, 0, sizeof(double) * (size_t)(ldv * (j + 2) + 64 * 1024)));
+  const size_t extra = (size_t)64 * 1024 + (size_t)(2 * 4096 + 8) * 8 * 148;  // scalars + partials
+  CK(cudaMalloc(&buf, sizeof(double) * ((size_t)ldv * (j + 2) + extra)));
+  CK(cudaMemset(buf, 0, sizeof(double) * ((size_t)ldv * (j + 2) + extra)));
   double* V = buf;
   double* w = buf + ldv * (j + 1);
   double* sc = buf + ldv * (j + 2);
@@ -2732,6 +2734,33 @@ extern "C" int heff_debug_launch_probe(int which, int64_t n, int j, int reps, fl
         return launch_pdl(cgs2_step_smem_kernel, dim3(1), dim3(kSmemStepThreads), (size_t)(j * ((n + 1) & ~1ll) * 8), s,
                           (const double*)V, ldv, j, w, n, sc, sc + 4096, sc + 8192, sc + 12288, sc + 16384,
                           V + (int64_t)j * ldv);
+      case 6: {  // the cooperative multi-block step as lanczos_ground launches it (one element per thread)
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs2_step_kernel, kStepThreads,
+                                                      sizeof(double) * (size_t)(j + 1));
+        const int G = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * g_num_sms, (n + kStepThreads - 1) / kStepThreads));
+        const double* Vc = V;
+        int64_t ldv_ = ldv, nn = n;
+        int jj = j, jmax = 4096;
+        double* partial = sc + 20480;
+        double *c1 = sc, *c2 = sc + 4096, *al = sc + 8192, *be = sc + 12288, *ib = sc + 16384;
+        double* vn = V + (int64_t)j * ldv;
+        double* wp = w;
+        void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &al, &be, &ib, &vn};
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(kStepThreads);
+        cfg.dynamicSmemBytes = sizeof(double) * (size_t)(j + 1);
+        cfg.stream = s;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        return cudaLaunchKernelExC(&cfg, (const void*)cgs2_step_kernel, args);
+      }
       default:
         cgs2_step_kernel<<<1, kStepThreads, sizeof(double) * (size_t)(j + 1), s>>>(
             V, ldv, j, w, n, sc + 20480, 4096, sc, sc + 4096, sc + 8192, sc + 12288, sc + 16384, V + (int64_t)j * ldv);
