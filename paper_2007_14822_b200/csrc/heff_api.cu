@@ -167,6 +167,10 @@ using CfgCl4 = ClusterGemmCfg<64, 64, 32, 16, kClStages, 4>;
 
 
 int g_num_sms = 0;
+// the plan workspace cache (defined with the plan code below)
+template <typename T>
+static cudaError_t ws_malloc(T** out, size_t bytes);
+static void ws_release(void* ptr);
 // diagnostics of the fused small-bond kernel (heff_debug_fused_timestamps): per-CTA timers
 static unsigned long long* g_fused_dbg = nullptr;
 static int g_fused_dbg_mode = 0;  // 1: no T3 stores, 2: no MPO epilogue (timing experiments; wrong results)
@@ -237,10 +241,17 @@ static int launch_tma(GemmOp& g, cudaStream_t s, int* nlaunch, SplitWs* ws, cons
     if (dp_tiles > 0) grid = g_num_sms;
     const size_t need = sizeof(double) * 2 * (size_t)grid * BM * BN;
     if (ws->bytes < need) {
-      cudaFree(ws->ptr);
+      if (ws->cached) {
+        if (ws->ptr) {
+          CK(cudaStreamSynchronize(s));  // the old block is idle before it returns to the cache
+          ws_release(ws->ptr);
+        }
+      } else {
+        cudaFree(ws->ptr);
+      }
       ws->ptr = nullptr;
       ws->bytes = 0;
-      if (cudaMalloc(&ws->ptr, need) != cudaSuccess) {
+      if ((ws->cached ? ws_malloc(&ws->ptr, need) : cudaMalloc(&ws->ptr, need)) != cudaSuccess) {
         cudaGetLastError();
         dp_tiles = tiles;  // no room for partial tiles: plain persistent schedule
         grid = (int)std::min<int64_t>(tiles, g_num_sms);
@@ -256,8 +267,9 @@ static int launch_tma(GemmOp& g, cudaStream_t s, int* nlaunch, SplitWs* ws, cons
   if (dp_tiles < tiles && grid <= kSkMaxGrid && sk_inkernel()) {
     if (!ws->sync) {
       const size_t sb = 16 + sizeof(int) * 2 * kSkMaxGrid;
-      if (cudaMalloc(&ws->sync, sb) != cudaSuccess) return set_err(HEFF_ENOMEM, "stream-K sync buffer");
-      CK(cudaMemsetAsync(ws->sync, 0, sb, s));
+      if ((ws->cached ? ws_malloc(&ws->sync, sb) : cudaMalloc(&ws->sync, sb)) != cudaSuccess)
+        return set_err(HEFF_ENOMEM, "stream-K sync buffer");
+      CK(cudaMemsetAsync(ws->sync, 0, sb, s));  // (a reused block: stale flags must not match an epoch)
       ws->epoch = 0;
     }
     sk.counter = static_cast<unsigned int*>(ws->sync);
@@ -567,9 +579,10 @@ static int build_csr_dev(Csr& c, int mode, const double* W1, const double* W2, i
   csr_shape(mode, kL, kR, d1, d2, &nrows, &nslots);
   if (nrows * nslots > INT32_MAX) return set_err(HEFF_EUNSUPPORTED, "MPO CSR: %lld entries", (long long)(nrows * nslots));
   if (c.owned) {
-    CK(cudaMalloc(&c.d_rowptr, sizeof(int) * (nrows + 2)));  // + the nnz slot
-    CK(cudaMalloc(&c.d_col, sizeof(int) * std::max<int64_t>(1, nrows * nslots)));
-    CK(cudaMalloc(&c.d_val, sizeof(double) * std::max<int64_t>(1, nrows * nslots)));
+    // (workspace-cache blocks: one plan per DMRG bond reuses the previous plan's CSR blocks)
+    CK(ws_malloc(&c.d_rowptr, sizeof(int) * (nrows + 2)));  // + the nnz slot
+    CK(ws_malloc(&c.d_col, sizeof(int) * std::max<int64_t>(1, nrows * nslots)));
+    CK(ws_malloc(&c.d_val, sizeof(double) * std::max<int64_t>(1, nrows * nslots)));
     c.d_nnz = c.d_rowptr + nrows + 1;
   }
   c.nrows = (int)nrows;
@@ -642,7 +655,7 @@ struct heff_plan_s {
   double *V1 = nullptr, *V3 = nullptr;
   GemmOp gA, gD;
   Csr csrA, csrB;
-  SplitWs splitws;
+  SplitWs splitws{nullptr, 0, nullptr, 0, true};  // stream-K workspace from the plan workspace cache
   // U(1) block-sparse schedules of the two GEMMs (heff_set_qn); one device allocation each
   int* sp1 = nullptr;
   int* sp4 = nullptr;
@@ -763,7 +776,10 @@ static cudaError_t ws_malloc(T** out, size_t bytes) {
   int best = -1;
   for (int i = 0; i < (int)g_ws_free.size(); ++i) {
     const WsBlock& b = g_ws_free[i];
-    if (b.dev == dev && b.bytes >= bytes && b.bytes <= 2 * bytes + (size_t(64) << 20) &&
+    // best fit within 2x (+ 64 MB of slack for large blocks only: a small request must not
+    // take a previous plan's large T1/T3 block, which its successor then re-allocates)
+    const size_t slack = bytes >= (size_t(8) << 20) ? (size_t(64) << 20) : 0;
+    if (b.dev == dev && b.bytes >= bytes && b.bytes <= 2 * bytes + slack &&
         (best < 0 || b.bytes < g_ws_free[best].bytes))
       best = i;
   }
@@ -812,6 +828,47 @@ static void ws_release(void* ptr) {
   }
 }
 
+// Pinned host scalars of lanczos_ground (alpha, beta, y, norm): cudaMallocHost / cudaFreeHost
+// cost ~1 ms / ~0.4 ms, which made a freshly created plan's first Lanczos call and its
+// destruction dominate small bonds (one plan per DMRG bond).  A process-wide pool keeps the
+// released blocks (power-of-two sizes >= 4 KB) for the next plan; heff_release_caches frees it.
+static std::mutex g_pin_mu;
+static std::vector<std::pair<size_t, double*>> g_pin_free;
+static cudaError_t pin_alloc(double** out, size_t* bytes_out, size_t need) {
+  size_t b = 4096;
+  while (b < need) b <<= 1;
+  {
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    for (size_t i = 0; i < g_pin_free.size(); ++i)
+      if (g_pin_free[i].first == b) {
+        *out = g_pin_free[i].second;
+        *bytes_out = b;
+        g_pin_free.erase(g_pin_free.begin() + (long)i);
+        return cudaSuccess;
+      }
+  }
+  void* p = nullptr;
+  const cudaError_t e = cudaMallocHost(&p, b);
+  if (e != cudaSuccess) return e;
+  *out = static_cast<double*>(p);
+  *bytes_out = b;
+  return cudaSuccess;
+}
+static void pin_release(double* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  if (g_pin_free.size() < 64) {
+    g_pin_free.emplace_back(bytes, p);
+    return;
+  }
+  cudaFreeHost(p);
+}
+static void pin_trim() {
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  for (auto& e : g_pin_free) cudaFreeHost(e.second);
+  g_pin_free.clear();
+}
+
 // Bytes held idle by the cache on `dev` (counted as available by the workspace budget).
 static size_t ws_cached_bytes(int dev) {
   std::lock_guard<std::mutex> lock(g_ws_mu);
@@ -822,10 +879,10 @@ static size_t ws_cached_bytes(int dev) {
 }
 
 static void free_csr(Csr& c) {
-  if (c.owned) {
-    cudaFree(c.d_rowptr);
-    cudaFree(c.d_col);
-    cudaFree(c.d_val);
+  if (c.owned) {  // heff_destroy calls this after the plan's last operation completed
+    ws_release(c.d_rowptr);
+    ws_release(c.d_col);
+    ws_release(c.d_val);
   }
   c = Csr{};
 }
@@ -868,8 +925,8 @@ extern "C" int heff_destroy(heff_plan p) {
     ws_release(b);
   cudaFree(p->mpo_live);
   cudaFree(p->qn_idx);
-  cudaFree(p->splitws.ptr);
-  cudaFree(p->splitws.sync);
+  ws_release(p->splitws.ptr);  // cache blocks (splitws.cached): the next plan reuses them
+  ws_release(p->splitws.sync);
   cudaFree(p->phis); cudaFree(p->pen_scratch);
   cudaFree(p->sp1); cudaFree(p->sp4);
   free_csr(p->csrA);
@@ -884,7 +941,7 @@ extern "C" int heff_destroy(heff_plan p) {
     cudaEventDestroy(p->setup_ev);
   }
   for (auto& e : p->step_ev) cudaEventDestroy(e);
-  if (p->hpin) cudaFreeHost(p->hpin);
+  pin_release(p->hpin, p->hpin_n * sizeof(double));  // (the plan's stream work is complete here)
   // an aborted communicator (comm == nullptr, comm_dead) is gone with its window handles:
   // only the local allocation is freed (deregistration is collective and would wait for
   // the dead peers)
@@ -2099,12 +2156,13 @@ static int lanczos_workspace(heff_plan_s* p, int cap, cudaStream_t s, LanczosLay
   if (p->hpin_n < (size_t)(3 * cap + 4)) {  // alpha, beta, y, norm
     if (p->hpin) {
       CK(cudaStreamSynchronize(s));
-      cudaFreeHost(p->hpin);
+      pin_release(p->hpin, p->hpin_n * sizeof(double));
       p->hpin = nullptr;
       p->hpin_n = 0;
     }
-    CK(cudaMallocHost(&p->hpin, sizeof(double) * (size_t)(3 * cap + 4)));
-    p->hpin_n = (size_t)(3 * cap + 4);
+    size_t bytes = 0;
+    CK(pin_alloc(&p->hpin, &bytes, sizeof(double) * (size_t)(3 * cap + 4)));
+    p->hpin_n = bytes / sizeof(double);
   }
   if (!p->work || p->work_len < ldv) {
     CK(cudaStreamSynchronize(s));
@@ -3124,5 +3182,6 @@ extern "C" int heff_release_caches(void) {
     std::lock_guard<std::mutex> lock(g_ws_mu);
     ws_cache_trim(dev);
   }
+  pin_trim();
   return HEFF_OK;
 }

@@ -87,6 +87,8 @@ struct SplitWs {  // stream-K partial-tile workspace, grown on demand
   // in-kernel fixup state (StreamKSync): [0] ticket counter, then int flags[2 * kSkMaxGrid]
   void* sync = nullptr;
   int epoch = 0;
+  bool cached = false;  // blocks from the plan workspace cache (ws_malloc / ws_release): plans'
+                        // own stream-K workspaces, reused by the next plan of a DMRG sweep
 };
 constexpr int kSkMaxGrid = 1024;
 
