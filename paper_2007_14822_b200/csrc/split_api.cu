@@ -169,7 +169,9 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   const int64_t kmin = std::min(M, N);
   const int64_t colsP = dir == 0 ? N : M;      // columns of the working matrix P (Psi or Psi^T)
   CKR(svd_init_once());
-  if (R <= kSvdSmallDispatch && colsP <= kSvdSmallDispatch && getenv("HEFF_SVD_NO_SMALL") == nullptr) {
+  const char* sn = getenv("HEFF_SVD_SMALL_N");  // (read per call: tests switch it)
+  const int64_t small_n = sn ? std::min<int64_t>(std::max(0, atoi(sn)), kSvdSmallMax) : (int64_t)kSvdSmallDispatch;
+  if (R <= small_n && colsP <= small_n && getenv("HEFF_SVD_NO_SMALL") == nullptr) {
     // small matrix: the whole split in one CTA (svd_small_kernel)
     double*& d_info = t_small_info();
     if (!d_info) CK(cudaMalloc(&d_info, 4 * sizeof(double)));

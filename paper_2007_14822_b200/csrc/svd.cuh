@@ -950,7 +950,12 @@ __global__ void svd_qn_scatter_kernel(const double* __restrict__ Qc, const doubl
 // no host round trips, no per-round launches.  Same arithmetic contract as the large path:
 // relative convergence test tol = 4 eps sqrt(R), power-of-two pre-scaling, readings R20-R22.
 constexpr int kSvdSmallMax = 128;      // shared-memory capacity of svd_small_kernel
-constexpr int kSvdSmallDispatch = 96;  // heff_svd_split uses it up to here (block path faster above: 128^2 3.5 vs 4.1 ms)
+// heff_svd_split uses it up to here (HEFF_SVD_SMALL_N overrides, <= kSvdSmallMax).  Round 2
+// measured both paths on random and graded (DMRG-like, 12 decades) inputs: the one-CTA kernel
+// has no LQ preconditioner, so on graded spectra it needs 20-29 sweeps above 40 columns
+// (64^2: 2.17 vs 1.18 ms, 96^2: 5.98 vs 1.78 ms on the block path) while it still wins on
+// random ones up to 64; at 48^2 the two are equal on graded inputs (1.16 / 1.09 ms).
+constexpr int kSvdSmallDispatch = 48;
 constexpr int kSvdSmallThreads = 1024;
 constexpr int kSvdSmallMaxSweeps = 80;
 

@@ -64,7 +64,9 @@ def _compare(Psi, cutoff=0.0, maxdim=0, mindim=1, direction=0, vectors=True):
     return got, ref
 
 
-PATHS = ["auto", "block"]   # auto: one-CTA kernel for sides <= 96; block: HEFF_SVD_NO_SMALL forces the block path
+# auto: one-CTA kernel for sides <= 48; block: HEFF_SVD_NO_SMALL forces the block path;
+# small: HEFF_SVD_SMALL_N = 128 sends every side <= 128 to the one-CTA kernel (its full capacity)
+PATHS = ["auto", "block", "small"]
 
 
 def _path(monkeypatch, path):
@@ -72,6 +74,10 @@ def _path(monkeypatch, path):
         monkeypatch.setenv("HEFF_SVD_NO_SMALL", "1")
     else:
         monkeypatch.delenv("HEFF_SVD_NO_SMALL", raising=False)
+    if path == "small":
+        monkeypatch.setenv("HEFF_SVD_SMALL_N", "128")
+    else:
+        monkeypatch.delenv("HEFF_SVD_SMALL_N", raising=False)
 
 
 @pytest.mark.parametrize("path", PATHS)
