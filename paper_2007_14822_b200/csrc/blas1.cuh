@@ -287,7 +287,7 @@ __device__ __forceinline__ void chunk_dots(const double* __restrict__ V, int64_t
 // (q mod warps) adds b = lane, lane + 32, ... then a shuffle tree (fixed order).
 __device__ __forceinline__ void grid_sums(const double* __restrict__ pp, int j, int G, double* s_out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int q = warp; q < j; q += kStepThreads / 32) {
+  for (int q = warp; q < j; q += (int)(blockDim.x >> 5)) {
     double t = 0.0;
     for (int b = lane; b < G; b += 32) t += __ldcg(pp + (int64_t)q * G + b);
     t = warp_sum(t);
@@ -566,6 +566,122 @@ __global__ void __launch_bounds__(kSmemStepThreads) cgs2_step_smem_kernel(
       }
     }
     __syncthreads();  // s_c and red are rewritten by the next pass
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// The cooperative CGS2 step in three passes over the basis instead of four (j <= kStep3MaxJ):
+// pass A: c1 = V^T w;  pass B: w' = w - V c1 and, from the same basis entries held in
+// registers, c2 = V^T w' and ||w'||^2;  pass C: v_{j+1} = (w' - V c2) / beta.  At C2 size the
+// step streams the basis from HBM (~5-7 TB/s, profiles/r02_final_c2_lanczos20_ncu.md), so one
+// pass less is a quarter less traffic.  Same formulas and the same two grid barriers as
+// cgs2_step_kernel; per-block partial sums (warp shuffles, then the warps in order) and
+// fixed-order grid sums: deterministic.
+// ------------------------------------------------------------------------------------
+constexpr int kStep3MaxJ = 24;
+constexpr int kStep3Threads = 256;  // 1 block per SM: up to 255 registers for the basis entries
+
+// acc[0..j) per thread (+ slot j already in red when nq = j + 1) -> pp[q * G + blockIdx.x] = the
+// block's sum (warp shuffles, then the warps in order); a macro to keep acc in registers
+#define HEFF_STEP3_BLOCK_PARTIALS(acc, nq, red, pp, G)                      \
+  do {                                                                       \
+    const int warp_ = threadIdx.x >> 5, lane_ = threadIdx.x & 31;            \
+    _Pragma("unroll") for (int q_ = 0; q_ < kStep3MaxJ; ++q_) if (q_ < (nq) && q_ < j) { \
+      const double v_ = warp_sum(acc[q_]);                                   \
+      if (lane_ == 0) red[q_][warp_] = v_;                                   \
+    }                                                                        \
+    __syncthreads();                                                         \
+    if ((int)threadIdx.x < (nq)) {                                           \
+      double t_ = 0.0;                                                       \
+      _Pragma("unroll") for (int k_ = 0; k_ < kStep3Threads / 32; ++k_) t_ += red[threadIdx.x][k_]; \
+      (pp)[(int64_t)threadIdx.x * (G) + blockIdx.x] = t_;                    \
+    }                                                                        \
+  } while (0)
+
+__global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const double* __restrict__ V, int64_t ldv, int j,
+                                                                   double* __restrict__ w, int64_t n,
+                                                                   double* __restrict__ partial, int jmax,
+                                                                   double* __restrict__ c1, double* __restrict__ c2,
+                                                                   double* __restrict__ alpha, double* __restrict__ beta,
+                                                                   double* __restrict__ invb,
+                                                                   double* __restrict__ vnext) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double s_c[kStep3MaxJ + 1];
+  __shared__ double red[kStep3MaxJ + 1][kStep3Threads / 32];
+  pdl_wait();  // w comes from the matvec kernel before
+  const int G = gridDim.x;
+  const int64_t chunk = ((n + G - 1) / G + 1) / 2 * 2;
+  const int64_t lo = min(n, (int64_t)blockIdx.x * chunk), hi = min(n, lo + chunk);
+  double* p1 = partial;
+  double* p2 = partial + (int64_t)jmax * G;
+  double acc[kStep3MaxJ + 1];
+  // ---- pass A: c1 partials
+#pragma unroll
+  for (int q = 0; q <= kStep3MaxJ; ++q) acc[q] = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kStep3Threads) {
+    const double x = w[i];
+#pragma unroll
+    for (int q = 0; q < kStep3MaxJ; ++q)
+      if (q < j) acc[q] = fma(V[(int64_t)q * ldv + i], x, acc[q]);
+  }
+  HEFF_STEP3_BLOCK_PARTIALS(acc, j, red, p1, G);
+  grid.sync();
+  grid_sums(p1, j, G, s_c);
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int q = threadIdx.x; q < j; q += kStep3Threads) c1[q] = s_c[q];
+  // ---- pass B: w' = w - V c1; c2 partials and ||w'||^2 from the same basis entries
+#pragma unroll
+  for (int q = 0; q <= kStep3MaxJ; ++q) acc[q] = 0.0;
+  double nacc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kStep3Threads) {
+    double v[kStep3MaxJ];
+#pragma unroll
+    for (int q = 0; q < kStep3MaxJ; ++q) v[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
+    double x = w[i];
+#pragma unroll
+    for (int q = 0; q < kStep3MaxJ; ++q)
+      if (q < j) x = fma(-s_c[q], v[q], x);
+    w[i] = x;
+#pragma unroll
+    for (int q = 0; q < kStep3MaxJ; ++q)
+      if (q < j) acc[q] = fma(v[q], x, acc[q]);
+    nacc = fma(x, x, nacc);
+  }
+  __syncthreads();  // red is rewritten
+  {
+    // ||w'||^2 into slot j of red (a register array indexed by j would go to local memory)
+    const double v = warp_sum(nacc);
+    if ((threadIdx.x & 31) == 0) red[j][threadIdx.x >> 5] = v;
+  }
+  HEFF_STEP3_BLOCK_PARTIALS(acc, j + 1, red, p2, G);
+  grid.sync();
+  grid_sums(p2, j + 1, G, s_c);
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int q = threadIdx.x; q < j; q += kStep3Threads) c2[q] = s_c[q];
+  double nrm2 = s_c[j];
+  for (int q = 0; q < j; ++q) nrm2 = fma(-s_c[q], s_c[q], nrm2);
+  const double bt = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
+  const double ib = bt > 0.0 ? 1.0 / bt : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    alpha[j - 1] = c1[j - 1] + s_c[j - 1];
+    beta[j - 1] = bt;
+    invb[j - 1] = ib;
+  }
+  // ---- pass C: v_{j+1} = (w' - V c2) / beta   (or w = w'' without vnext)
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kStep3Threads) {
+    double v[kStep3MaxJ];
+#pragma unroll
+    for (int q = 0; q < kStep3MaxJ; ++q) v[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
+    double x = w[i];
+#pragma unroll
+    for (int q = 0; q < kStep3MaxJ; ++q)
+      if (q < j) x = fma(-s_c[q], v[q], x);
+    if (vnext)
+      vnext[i] = x * ib;
+    else
+      w[i] = x;
   }
 }
 

@@ -2260,7 +2260,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   // (launch-bound sizes only: above ~2M elements the separate vectorised kernels stream faster)
   const bool fused = !cplx && (p->comm == nullptr) && (cap <= 4096) &&
                      (n <= (int64_t(1) << 21) || getenv("HEFF_FUSED_STEP")) && getenv("HEFF_NO_FUSED_STEP") == nullptr;
-  int step_grid = 0;
+  int step_grid = 0, step3_grid = 0;
   // vectors up to this length take the one-block step kernel when the grid is one block
   // (HEFF_SMALL_STEP_N overrides; 0 = never)
   static const int64_t small_step_max = [] {
@@ -2280,6 +2280,10 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     }();
     const int64_t want = std::max<int64_t>(1, (n + (int64_t)ept * kStepThreads - 1) / ((int64_t)ept * kStepThreads));
     step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * g_num_sms, want));
+    int per_sm3 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, cgs2_step3_kernel, kStep3Threads, 0));
+    step3_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm3 * g_num_sms,
+                                                             (n + kStep3Threads - 1) / kStep3Threads));
   }
   static const bool no_smem_step = getenv("HEFF_NO_SMEM_STEP") != nullptr;
   std::vector<cudaEvent_t>* phase_ev = nullptr;  // HEFF_LANCZOS_TIMING >= 2 (fixed mode)
@@ -2322,6 +2326,8 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
         ++p->total_launches;
         return HEFF_OK;
       }
+      // j <= kStep3MaxJ: three passes over the basis (cgs2_step3_kernel), else four
+      const bool three = j <= kStep3MaxJ && step_grid > 1 && getenv("HEFF_NO_STEP3") == nullptr;
       void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &alpha, &beta, &invb, &vnext};
       // cooperative (grid syncs) and, unless HEFF_NO_PDL, programmatic serialization: the
       // launch overlaps the matvec's last kernel, the body starts after griddepcontrol.wait
@@ -2337,7 +2343,13 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       at[1].val.programmaticStreamSerializationAllowed = pdl_off ? 0 : 1;
       cfg.attrs = at;
       cfg.numAttrs = 2;
-      CK(cudaLaunchKernelExC(&cfg, (const void*)cgs2_step_kernel, args));
+      if (three) {
+        cfg.dynamicSmemBytes = 0;
+        cfg.gridDim = dim3(step3_grid);
+        cfg.blockDim = dim3(kStep3Threads);
+        at[0].val.cooperative = step3_grid > 1 ? 1 : 0;
+      }
+      CK(cudaLaunchKernelExC(&cfg, three ? (const void*)cgs2_step3_kernel : (const void*)cgs2_step_kernel, args));
       ++p->total_launches;
       return HEFF_OK;
     }
