@@ -393,12 +393,18 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   const bool sort_cols = getenv("HEFF_SVD_NO_SORT") == nullptr;
   std::vector<double> nrm(nblk * kSvdB);
   std::vector<int> order(nblk * kSvdB);
+  // The column norms of the current Xb are read back together with each sweep's convergence
+  // scalars (one host synchronisation per sweep instead of two); they order the next sweep's
+  // columns and, after the last sweep, are the singular values.
+  const bool do_sort = sort_cols && ncols > kSvdPair;
+  if (do_sort) {
+    svd_colnorm_kernel<<<(unsigned)nblk, 256, 0, s>>>(Xb, R, ncols, d_norm);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(nrm.data(), d_norm, sizeof(double) * ncols, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
   for (int sw = 0; sw < kSvdMaxSweeps && !converged; ++sw) {
-    if (sort_cols && ncols > kSvdPair) {  // descending-norm column order for this sweep
-      svd_colnorm_kernel<<<(unsigned)nblk, 256, 0, s>>>(Xb, R, ncols, d_norm);
-      CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(nrm.data(), d_norm, sizeof(double) * ncols, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+    if (do_sort) {  // descending-norm column order for this sweep (norms read back above)
       for (int64_t i = 0; i < ncols; ++i) order[i] = (int)i;
       std::stable_sort(order.begin(), order.begin() + ncols, [&](int a, int b) { return nrm[a] > nrm[b]; });
       CK(cudaMemcpyAsync(d_sortperm, order.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice, s));
@@ -428,8 +434,11 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
     CK(cudaGetLastError());
     int nrot = 0;
     unsigned long long offbits = 0;
+    svd_colnorm_kernel<<<(unsigned)nblk, 256, 0, s>>>(Xb, R, ncols, d_norm);
+    CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&nrot, d_nrot + sw, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&offbits, d_maxoff + sw, sizeof(offbits), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(nrm.data(), d_norm, sizeof(double) * ncols, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     sweeps = sw + 1;
     converged = nrot == 0;
@@ -450,11 +459,8 @@ extern "C" int heff_svd_split(int64_t M, int64_t N, const double* psi, const hef
   if (!converged) return set_err(HEFF_ENOCONV, "heff_svd_split: Jacobi did not converge in %d sweeps", kSvdMaxSweeps);
 
   if (timing) CK(cudaEventRecord(tev[2], s));
-  // singular values = column norms; sort (descending, stable) and truncate on the host
-  svd_colnorm_kernel<<<(unsigned)nblk, 256, 0, s>>>(Xb, R, ncols, d_norm);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(nrm.data(), d_norm, sizeof(double) * ncols, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  // singular values = column norms of the final Xb (read back with the last sweep's scalars);
+  // sort (descending, stable) and truncate on the host
   for (int64_t i = 0; i < ncols; ++i) order[i] = (int)i;
   std::stable_sort(order.begin(), order.begin() + ncols, [&](int a, int b) { return nrm[a] > nrm[b]; });
   std::vector<double> sv(kmin);
