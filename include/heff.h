@@ -141,7 +141,10 @@ int heff_apply_host(heff_plan p, const double* psi_host, double* out_host, heff_
  * psi: in = start vector, out = normalised Ritz vector (device; the local shard
  * [mL][d1][d2][nb] on a communicating sharded plan, else the full vector).
  * energy: lowest Ritz value; iters_done: matvecs performed; resid_est:
- * beta_j |y_j[last]|.  Synchronous.  HEFF_EZERO if psi == 0. */
+ * beta_j |y_j[last]|.  Synchronous.  HEFF_EZERO if psi == 0 (psi is then left unchanged;
+ * on plans without a communicator the test is made at the first scalar read-back, so the
+ * call costs one host round trip less).  opts->theta_out == NULL in fixed mode: only the
+ * breakdown test runs per step, and the last step's tridiagonal problem is solved once. */
 int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts* opts, double* energy, int* iters_done,
                    double* resid_est, heff_stream stream);
 

@@ -2244,10 +2244,17 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   double* h_b = h_a + cap;               // comm_wait polls (failure detection)
   double* h_y = h_b + cap;
   double* h_n = h_y + cap;
-  CK(cudaMemcpyAsync(h_n, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
-  CKR(comm_wait(p, s));
-  const double h_nrm = *h_n;
-  if (!(h_nrm > 0.0)) return set_err(HEFF_EZERO, "lanczos_ground: zero start vector");
+  // Without a communicator the zero-start-vector test waits for the first scalar read-back
+  // below (a zero x0 gives 1/||x0|| = 0 on the device, so the steps run on zeros and break
+  // down at once; psi is left untouched): one host round trip less per call.  With one, every
+  // rank must learn it before the first collective.
+  const bool defer_zero = p->comm == nullptr && getenv("HEFF_EAGER_ZERO_CHECK") == nullptr;
+  auto zero_start = [&]() { return set_err(HEFF_EZERO, "lanczos_ground: zero start vector"); };
+  if (!defer_zero) {
+    CK(cudaMemcpyAsync(h_n, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CKR(comm_wait(p, s));
+    if (!(*h_n > 0.0)) return zero_start();
+  }
   scale_kernel<<<ew_grid(nr), 256, 0, s>>>(V, invb + cap, V, nr);
   ++p->total_launches;
   CK(cudaGetLastError());
@@ -2377,11 +2384,15 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   };
   // scalar bookkeeping on the host: returns true to stop after step j
   // (hnorm: Gershgorin bound of T_j, updated with the rows the new step changes)
+  // (fixed mode without theta_out needs only the breakdown test per step: the Ritz pair of
+  // the last step is solved below anyway)
+  const bool need_theta = o->mode == 1 || o->theta_out != nullptr;
   auto host_check = [&](int j) -> bool {
     for (int i = std::max(0, j - 2); i < j; ++i) {
       const double gsh = std::fabs(ha[i]) + (i > 0 ? hb[i - 1] : 0.0) + hb[i];
       hnorm = std::max(hnorm, gsh);
     }
+    if (!need_theta) return hb[j - 1] <= 1e-12 * hnorm || j == cap;
     if (!tridiag_lowest_fast(j, ha.data(), hb.data(), &theta, &ylast))
       tridiag_lowest_last(j, ha.data(), hb.data(), &theta, &ylast);  // (never seen; QL as the fallback)
     if (o->theta_out) o->theta_out[j - 1] = theta;
@@ -2412,7 +2423,12 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     const auto t1 = clk::now();
     CK(cudaMemcpyAsync(h_a, alpha, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(h_b, beta, sizeof(double) * cap, cudaMemcpyDeviceToHost, s));
+    if (defer_zero) CK(cudaMemcpyAsync(h_n, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
     CKR(comm_wait(p, s));
+    if (defer_zero && !(*h_n > 0.0)) {
+      for (auto& e : tev) cudaEventDestroy(e);
+      return zero_start();
+    }
     const auto t2 = clk::now();
     memcpy(ha.data(), h_a, sizeof(double) * cap);
     memcpy(hb.data(), h_b, sizeof(double) * cap);
@@ -2455,7 +2471,9 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       }
       CK(cudaMemcpyAsync(h_a + (j - 1), alpha + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(h_b + (j - 1), beta + (j - 1), sizeof(double) * (j1 - j + 1), cudaMemcpyDeviceToHost, s));
+      if (defer_zero && j == 1) CK(cudaMemcpyAsync(h_n, beta + cap, sizeof(double), cudaMemcpyDeviceToHost, s));
       CKR(comm_wait(p, s));
+      if (defer_zero && j == 1 && !(*h_n > 0.0)) return zero_start();
       memcpy(&ha[j - 1], h_a + (j - 1), sizeof(double) * (j1 - j + 1));
       memcpy(&hb[j - 1], h_b + (j - 1), sizeof(double) * (j1 - j + 1));
       for (int jj = j; jj <= j1; ++jj) {

@@ -514,9 +514,11 @@ class Heff:
         return out_host
 
     def lanczos_ground(self, psi: torch.Tensor, max_iter: int, tol: float = 0.0, converge: bool = False,
-                       stream=None) -> LanczosResult:
+                       stream=None, thetas: bool = False) -> LanczosResult:
         """psi: start vector (overwritten with the normalised Ritz vector): the full vector
-        [mL, d1, d2, mR], or this rank's shard [mL, d1, d2, nb] on a communicating sharded plan."""
+        [mL, d1, d2, mR], or this rank's shard [mL, d1, d2, nb] on a communicating sharded plan.
+        thetas: also return the lowest Ritz value of every step (theta_out; a fixed-step run
+        without it solves only the last step's tridiagonal problem)."""
         _dev(psi, "psi", getattr(self, "cplx", False))
         if psi.numel() != self.lanczos_len:
             raise ValueError(f"psi must have {self.lanczos_len} entries for this plan, got {psi.numel()}")
@@ -524,12 +526,12 @@ class Heff:
         b = (ctypes.c_double * max_iter)()
         th = (ctypes.c_double * max_iter)()
         o = _LanczosOpts(max_iter, 1 if converge else 0, tol, ctypes.cast(a, ctypes.c_void_p),
-                         ctypes.cast(b, ctypes.c_void_p), ctypes.cast(th, ctypes.c_void_p))
+                         ctypes.cast(b, ctypes.c_void_p), ctypes.cast(th, ctypes.c_void_p) if thetas else None)
         e, it, r = ctypes.c_double(), ctypes.c_int(), ctypes.c_double()
         _check(lib().lanczos_ground(self._h, psi.data_ptr(), ctypes.byref(o), ctypes.byref(e), ctypes.byref(it),
                                     ctypes.byref(r), _stream(stream)))
         j = it.value
-        return LanczosResult(e.value, j, r.value, list(a[:j]), list(b[:j]), list(th[:j]))
+        return LanczosResult(e.value, j, r.value, list(a[:j]), list(b[:j]), list(th[:j]) if thetas else [])
 
     def set_option(self, opt: int, value: int):
         _check(lib().heff_set_option(self._h, opt, int(value)))

@@ -187,13 +187,28 @@ def test_apply_host_e2e(dev, orc, case, monkeypatch):
 
 
 # ------------------------------------------------------------------------ Lanczos
-def gpu_lanczos(x, dev, max_iter, tol=0.0, converge=False):
+def gpu_lanczos(x, dev, max_iter, tol=0.0, converge=False, thetas=True):
     from paper_2007_14822_b200 import Heff
     xd = x.to(dev)
     with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
         v = xd.psi.clone()
-        r = h.lanczos_ground(v, max_iter=max_iter, tol=tol, converge=converge)
+        r = h.lanczos_ground(v, max_iter=max_iter, tol=tol, converge=converge, thetas=thetas)
         return r, v.cpu().numpy()
+
+
+@pytest.mark.parametrize("name,steps", [("c1", 20), ("two_site", 6), ("c2", 8)])
+def test_lanczos_fixed_without_thetas_is_exact(dev, name, steps):
+    """A fixed-step run that does not ask for the per-step Ritz values checks only for
+    breakdown per step; the stopping step (incl. the singlet's early invariant-subspace stop),
+    T_j, energy, residual and Ritz vector must be bitwise those of the run that solves T_j
+    at every step."""
+    x = CASES[name]()
+    r1, v1 = gpu_lanczos(x, dev, steps, thetas=True)
+    r0, v0 = gpu_lanczos(x, dev, steps, thetas=False)
+    assert len(r1.thetas) == r1.iters and r0.thetas == []
+    assert (r0.iters, r0.energy, r0.resid) == (r1.iters, r1.energy, r1.resid)
+    assert r0.alpha == r1.alpha and r0.beta == r1.beta
+    assert np.array_equal(v0, v1)
 
 
 @pytest.mark.parametrize("name,tol", [("c1", 1e-10), ("c2", 1e-10), ("two_site", 1e-12), ("ragged_odd", 1e-9)])
@@ -278,6 +293,17 @@ def test_lanczos_zero_vector_and_errors(dev):
     with Heff(x.L, x.W1, x.W2, x.R) as h:
         with pytest.raises(HeffZeroVector):
             h.lanczos_ground(torch.zeros_like(x.psi), max_iter=5)
+        # converge mode, and a theta_out request: the same error, psi left untouched, and
+        # the plan still solves afterwards (the zero test waits for the first read-back)
+        z = torch.zeros_like(x.psi)
+        with pytest.raises(HeffZeroVector):
+            h.lanczos_ground(z, max_iter=30, tol=1e-10, converge=True)
+        assert int(torch.count_nonzero(z)) == 0
+        r0 = h.lanczos_ground(x.psi.clone(), max_iter=20)
+        with pytest.raises(HeffZeroVector):
+            h.lanczos_ground(torch.zeros_like(x.psi), max_iter=5, thetas=True)
+        r1 = h.lanczos_ground(x.psi.clone(), max_iter=20)
+        assert r1.energy == r0.energy
         with pytest.raises(HeffError):
             h.apply(x.psi, x.psi)                       # aliasing
         with pytest.raises(HeffError):
