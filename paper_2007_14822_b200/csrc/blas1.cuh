@@ -295,19 +295,46 @@ __device__ __forceinline__ void grid_sums(const double* __restrict__ pp, int j, 
   }
 }
 
+// Grid barrier of the CGS2 step kernels when they are launched as ordinary (not cooperative)
+// kernels: one counter in global memory whose low 31 bits are 0 between barriers; block 0
+// adds 2^31 - (G - 1), every other block 1, so the last arrival flips bit 31 and the low bits
+// return to 0 (the counter is reusable across barriers and launches without a reset).
+// Co-residency: the grid is at most the occupancy-limited resident grid, and its dependents
+// launch only after every block has started, so no block waits on one that cannot start.
+__device__ __forceinline__ void grid_barrier_flip(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+    __threadfence();
+    const unsigned int old = atomicAdd(bar, inc);
+    unsigned int cur;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+    } while (((old ^ cur) & 0x80000000u) == 0);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kStepThreads) cgs2_step_kernel(const double* __restrict__ V, int64_t ldv, int j,
                                                                   double* __restrict__ w, int64_t n,
                                                                   double* __restrict__ partial, int jmax,
                                                                   double* __restrict__ c1, double* __restrict__ c2,
                                                                   double* __restrict__ alpha, double* __restrict__ beta,
                                                                   double* __restrict__ invb,
-                                                                  double* __restrict__ vnext) {
+                                                                  double* __restrict__ vnext,
+                                                                  unsigned int* __restrict__ gbar) {
   // gridDim.x == 1 (vectors of a few thousand entries): launched as an ordinary kernel and
-  // the grid-wide barriers are block barriers (a cooperative launch costs ~10 us there)
+  // the grid-wide barriers are block barriers (a cooperative launch costs ~10 us there);
+  // gbar != null: an ordinary launch with grid_barrier_flip, else cooperative
   cg::grid_group grid = cg::this_grid();
   auto gsync = [&] {
-    if (gridDim.x > 1) grid.sync();
-    else __syncthreads();
+    if (gridDim.x > 1) {
+      if (gbar) grid_barrier_flip(gbar);
+      else grid.sync();
+    } else {
+      __syncthreads();
+    }
   };
   extern __shared__ double s_c[];  // [j + 1]
   pdl_wait();  // w comes from the matvec kernel before (launched with programmatic serialization)
@@ -604,8 +631,13 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
                                                                    double* __restrict__ c1, double* __restrict__ c2,
                                                                    double* __restrict__ alpha, double* __restrict__ beta,
                                                                    double* __restrict__ invb,
-                                                                   double* __restrict__ vnext) {
+                                                                   double* __restrict__ vnext,
+                                                                   unsigned int* __restrict__ gbar, int unroll2) {
   cg::grid_group grid = cg::this_grid();
+  auto gsync = [&] {  // gbar != null: ordinary launch (grid_barrier_flip), else cooperative
+    if (gbar) grid_barrier_flip(gbar);
+    else grid.sync();
+  };
   __shared__ double s_c[kStep3MaxJ + 1];
   __shared__ double red[kStep3MaxJ + 1][kStep3Threads / 32];
   pdl_wait();  // w comes from the matvec kernel before
@@ -618,14 +650,34 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
   // ---- pass A: c1 partials
 #pragma unroll
   for (int q = 0; q <= kStep3MaxJ; ++q) acc[q] = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kStep3Threads) {
+  // Two of the thread's elements per iteration: both elements' loads are issued before
+  // the FMAs (one block of 8 warps per SM leaves little else to hide their latency); each
+  // accumulator still adds element i before element i + kStep3Threads (same sums, bitwise).
+  int64_t i = lo + threadIdx.x;
+  if (unroll2) {
+    for (; i + kStep3Threads < hi; i += 2 * kStep3Threads) {
+      const int64_t i1 = i + kStep3Threads;
+      const double x0 = w[i], x1 = w[i1];
+      double v0[kStep3MaxJ], v1[kStep3MaxJ];
+#pragma unroll
+      for (int q = 0; q < kStep3MaxJ; ++q)
+        if (q < j) {
+          v0[q] = V[(int64_t)q * ldv + i];
+          v1[q] = V[(int64_t)q * ldv + i1];
+        }
+#pragma unroll
+      for (int q = 0; q < kStep3MaxJ; ++q)
+        if (q < j) acc[q] = fma(v1[q], x1, fma(v0[q], x0, acc[q]));
+    }
+  }
+  for (; i < hi; i += kStep3Threads) {
     const double x = w[i];
 #pragma unroll
     for (int q = 0; q < kStep3MaxJ; ++q)
       if (q < j) acc[q] = fma(V[(int64_t)q * ldv + i], x, acc[q]);
   }
   HEFF_STEP3_BLOCK_PARTIALS(acc, j, red, p1, G);
-  grid.sync();
+  gsync();
   grid_sums(p1, j, G, s_c);
   __syncthreads();
   if (blockIdx.x == 0)
@@ -634,7 +686,32 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
 #pragma unroll
   for (int q = 0; q <= kStep3MaxJ; ++q) acc[q] = 0.0;
   double nacc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kStep3Threads) {
+  i = lo + threadIdx.x;
+  if (unroll2) {
+    for (; i + kStep3Threads < hi; i += 2 * kStep3Threads) {
+      const int64_t i1 = i + kStep3Threads;
+      double v0[kStep3MaxJ], v1[kStep3MaxJ];
+#pragma unroll
+      for (int q = 0; q < kStep3MaxJ; ++q) {
+        v0[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
+        v1[q] = q < j ? V[(int64_t)q * ldv + i1] : 0.0;
+      }
+      double x0 = w[i], x1 = w[i1];
+#pragma unroll
+      for (int q = 0; q < kStep3MaxJ; ++q)
+        if (q < j) {
+          x0 = fma(-s_c[q], v0[q], x0);
+          x1 = fma(-s_c[q], v1[q], x1);
+        }
+      w[i] = x0;
+      w[i1] = x1;
+#pragma unroll
+      for (int q = 0; q < kStep3MaxJ; ++q)
+        if (q < j) acc[q] = fma(v1[q], x1, fma(v0[q], x0, acc[q]));
+      nacc = fma(x1, x1, fma(x0, x0, nacc));
+    }
+  }
+  for (; i < hi; i += kStep3Threads) {
     double v[kStep3MaxJ];
 #pragma unroll
     for (int q = 0; q < kStep3MaxJ; ++q) v[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
@@ -655,7 +732,7 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
     if ((threadIdx.x & 31) == 0) red[j][threadIdx.x >> 5] = v;
   }
   HEFF_STEP3_BLOCK_PARTIALS(acc, j + 1, red, p2, G);
-  grid.sync();
+  gsync();
   grid_sums(p2, j + 1, G, s_c);
   __syncthreads();
   if (blockIdx.x == 0)
@@ -670,7 +747,33 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
     invb[j - 1] = ib;
   }
   // ---- pass C: v_{j+1} = (w' - V c2) / beta   (or w = w'' without vnext)
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kStep3Threads) {
+  i = lo + threadIdx.x;
+  if (unroll2) {
+    for (; i + kStep3Threads < hi; i += 2 * kStep3Threads) {
+      const int64_t i1 = i + kStep3Threads;
+      double v0[kStep3MaxJ], v1[kStep3MaxJ];
+#pragma unroll
+      for (int q = 0; q < kStep3MaxJ; ++q) {
+        v0[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
+        v1[q] = q < j ? V[(int64_t)q * ldv + i1] : 0.0;
+      }
+      double x0 = w[i], x1 = w[i1];
+#pragma unroll
+      for (int q = 0; q < kStep3MaxJ; ++q)
+        if (q < j) {
+          x0 = fma(-s_c[q], v0[q], x0);
+          x1 = fma(-s_c[q], v1[q], x1);
+        }
+      if (vnext) {
+        vnext[i] = x0 * ib;
+        vnext[i1] = x1 * ib;
+      } else {
+        w[i] = x0;
+        w[i1] = x1;
+      }
+    }
+  }
+  for (; i < hi; i += kStep3Threads) {
     double v[kStep3MaxJ];
 #pragma unroll
     for (int q = 0; q < kStep3MaxJ; ++q) v[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;

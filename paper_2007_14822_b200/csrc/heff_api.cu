@@ -706,6 +706,7 @@ struct heff_plan_s {
   double* partial = nullptr;                // [(cap+1)][ldp]
   int ldp = 0;
   double* scal = nullptr;                   // c1[cap], c2[cap], alpha[cap], beta2/beta[cap], invb[cap], y[cap]
+  unsigned int* gbar = nullptr;             // grid barrier of the ordinary-launch CGS2 steps (zeroed once)
   // options
   int gemm_path = 0;
   int last_launches = 0;
@@ -921,7 +922,7 @@ extern "C" int heff_destroy(heff_plan p) {
   for (void* b : {(void*)p->T1, (void*)p->T3, (void*)p->V1, (void*)p->V3, (void*)p->stage_in, (void*)p->stage_out,
                   (void*)p->basis, (void*)p->work, (void*)p->full, (void*)p->gather, (void*)p->partial,
                   (void*)p->scal, (void*)p->Lp, (void*)p->Rp, (void*)p->Rperm, (void*)p->zin, (void*)p->zout, (void*)p->dense_in,
-                  (void*)p->dense_out})
+                  (void*)p->dense_out, (void*)p->gbar})
     ws_release(b);
   cudaFree(p->mpo_live);
   cudaFree(p->qn_idx);
@@ -2149,7 +2150,7 @@ static int lanczos_workspace(heff_plan_s* p, int cap, cudaStream_t s, LanczosLay
     p->ldp = reduce_grid(nr);
     const size_t pcols = std::max<size_t>((size_t)p->ldp, (size_t)8 * g_num_sms);  // also the fused step's grid
     CK(ws_malloc(&p->partial, sizeof(double) * (size_t)(2 * cap + 2 * kDotQ + 1) * pcols));
-    CK(ws_malloc(&p->scal, sizeof(double) * 9 * (size_t)(cap + 1)));  // + fused-gather timeout flag
+    CK(ws_malloc(&p->scal, sizeof(double) * 9 * (size_t)(cap + 1)));  // + fused-gather timeout flag, grid barrier
     p->basis_cap = fgather ? 0 : cap;  // a later non-fused call reallocates the full basis
     p->ldv = ldv;
   }
@@ -2163,6 +2164,10 @@ static int lanczos_workspace(heff_plan_s* p, int cap, cudaStream_t s, LanczosLay
     size_t bytes = 0;
     CK(pin_alloc(&p->hpin, &bytes, sizeof(double) * (size_t)(3 * cap + 4)));
     p->hpin_n = bytes / sizeof(double);
+  }
+  if (!p->gbar) {
+    CK(ws_malloc(&p->gbar, 256));
+    CK(cudaMemsetAsync(p->gbar, 0, 256, s));
   }
   if (!p->work || p->work_len < ldv) {
     CK(cudaStreamSynchronize(s));
@@ -2293,6 +2298,17 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
                                                              (n + kStep3Threads - 1) / kStep3Threads));
   }
   static const bool no_smem_step = getenv("HEFF_NO_SMEM_STEP") != nullptr;
+  // multi-block CGS2 steps as ordinary launches with a flip-counter grid barrier (p->gbar)
+  // instead of cooperative launches: measured 1.3-2.0 us less per Lanczos step (chain m = 64
+  // 45.8 -> 44.0 us, cylinder m = 64 46.5 -> 44.5 us, C2 90.0 -> 89.4 us), bitwise-equal
+  // results.  The grid is the occupancy-limited resident grid of the whole device; under MPS
+  // (a client may get fewer SMs than the device reports) the cooperative launch, which checks
+  // co-residency, stays.  HEFF_STEP_NONCOOP=0/1 overrides (read per call).
+  const bool step_noncoop = [] {
+    if (const char* e = getenv("HEFF_STEP_NONCOOP")) return atoi(e) != 0;
+    return getenv("CUDA_MPS_PIPE_DIRECTORY") == nullptr && getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE") == nullptr;
+  }();
+  unsigned int* d_gbar = p->gbar;
   std::vector<cudaEvent_t>* phase_ev = nullptr;  // HEFF_LANCZOS_TIMING >= 2 (fixed mode)
   auto step = [&](int j) -> int {  // j = 1-based step: v_j = V[j-1]
     double* vj = V + (int64_t)(j - 1) * ldv;
@@ -2335,7 +2351,15 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       }
       // j <= kStep3MaxJ: three passes over the basis (cgs2_step3_kernel), else four
       const bool three = j <= kStep3MaxJ && step_grid > 1 && getenv("HEFF_NO_STEP3") == nullptr;
-      void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &alpha, &beta, &invb, &vnext};
+      unsigned int* gbar = step_noncoop ? d_gbar : nullptr;
+      // cgs2_step3_kernel: two elements per thread per iteration when a thread owns >= 4
+      // (measured, B200: C2, 6.9 per thread, Lanczos step 90.8 -> 85.5 us; at 1.7 per thread,
+      // m = 128 chain / cylinder, 0.9-1.1 us slower); HEFF_STEP3_UNROLL=0/1 overrides
+      const int64_t per_thread = (n + (int64_t)step3_grid * kStep3Threads - 1) / ((int64_t)step3_grid * kStep3Threads);
+      int unroll2 = per_thread >= 4;
+      if (const char* e = getenv("HEFF_STEP3_UNROLL")) unroll2 = atoi(e) != 0;
+      void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &alpha, &beta, &invb, &vnext, &gbar,
+                      &unroll2};
       // cooperative (grid syncs) and, unless HEFF_NO_PDL, programmatic serialization: the
       // launch overlaps the matvec's last kernel, the body starts after griddepcontrol.wait
       cudaLaunchConfig_t cfg{};
@@ -2345,7 +2369,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       cfg.stream = s;
       cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeCooperative;
-      at[0].val.cooperative = step_grid > 1 ? 1 : 0;  // one block: an ordinary launch
+      at[0].val.cooperative = step_grid > 1 && !step_noncoop ? 1 : 0;  // one block: an ordinary launch
       at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[1].val.programmaticStreamSerializationAllowed = pdl_off ? 0 : 1;
       cfg.attrs = at;
@@ -2354,7 +2378,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
         cfg.dynamicSmemBytes = 0;
         cfg.gridDim = dim3(step3_grid);
         cfg.blockDim = dim3(kStep3Threads);
-        at[0].val.cooperative = step3_grid > 1 ? 1 : 0;
+        at[0].val.cooperative = step3_grid > 1 && !step_noncoop ? 1 : 0;
       }
       CK(cudaLaunchKernelExC(&cfg, three ? (const void*)cgs2_step3_kernel : (const void*)cgs2_step_kernel, args));
       ++p->total_launches;
@@ -2834,7 +2858,8 @@ extern "C" int heff_debug_launch_probe(int which, int64_t n, int j, int reps, fl
         double *c1 = sc, *c2 = sc + 4096, *al = sc + 8192, *be = sc + 12288, *ib = sc + 16384;
         double* vn = V + (int64_t)j * ldv;
         double* wp = w;
-        void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &al, &be, &ib, &vn};
+        unsigned int* gb = nullptr;
+        void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &al, &be, &ib, &vn, &gb};
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(G);
         cfg.blockDim = dim3(kStepThreads);
@@ -2851,7 +2876,8 @@ extern "C" int heff_debug_launch_probe(int which, int64_t n, int j, int reps, fl
       }
       default:
         cgs2_step_kernel<<<1, kStepThreads, sizeof(double) * (size_t)(j + 1), s>>>(
-            V, ldv, j, w, n, sc + 20480, 4096, sc, sc + 4096, sc + 8192, sc + 12288, sc + 16384, V + (int64_t)j * ldv);
+            V, ldv, j, w, n, sc + 20480, 4096, sc, sc + 4096, sc + 8192, sc + 12288, sc + 16384, V + (int64_t)j * ldv,
+            nullptr);
         return cudaGetLastError();
     }
   };

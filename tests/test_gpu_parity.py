@@ -211,6 +211,44 @@ def test_lanczos_fixed_without_thetas_is_exact(dev, name, steps):
     assert np.array_equal(v0, v1)
 
 
+@pytest.mark.parametrize("m", [128, 256])
+def test_lanczos_step3_unroll_is_bitwise(dev, m, monkeypatch):
+    """cgs2_step3_kernel with two elements per thread per iteration (the default at C2) keeps
+    every per-thread sum in element order: T_j and the Ritz vector are bitwise those of the
+    one-element loop, over 30 steps (three-pass kernel to j = 24, four-pass after)."""
+    from paper_2007_14822_b200 import Heff
+    xd = C.make("c2", m=m).to(dev)
+    out = {}
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        for flag in ("1", "0"):
+            monkeypatch.setenv("HEFF_STEP3_UNROLL", flag)
+            v = xd.psi.clone()
+            r = h.lanczos_ground(v, max_iter=30)
+            out[flag] = (r.energy, r.iters, tuple(r.alpha), tuple(r.beta), v.cpu().numpy().tobytes())
+    assert out["1"] == out["0"]
+
+
+@pytest.mark.parametrize("m", [128, 256])
+def test_lanczos_step_grid_barrier_matches_cooperative(dev, m, monkeypatch):
+    """The multi-block CGS2 steps launched as ordinary kernels (flip-counter grid barrier)
+    must give bitwise the cooperative launch's T_j and Ritz vector, over 30 steps (three-pass
+    kernel up to j = 24, four-pass kernel after), twice in a row on one plan (the barrier
+    counter is reused across launches and calls)."""
+    from paper_2007_14822_b200 import Heff
+    xd = C.make("c2", m=m).to(dev)
+    out = {}
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        for flag in ("1", "0", "1"):
+            monkeypatch.setenv("HEFF_STEP_NONCOOP", flag)
+            v = xd.psi.clone()
+            r = h.lanczos_ground(v, max_iter=30)
+            res = (r.energy, r.iters, tuple(r.alpha), tuple(r.beta), v.cpu().numpy().tobytes())
+            if flag in out:
+                assert out[flag] == res
+            out[flag] = res
+    assert out["1"] == out["0"]
+
+
 @pytest.mark.parametrize("name,tol", [("c1", 1e-10), ("c2", 1e-10), ("two_site", 1e-12), ("ragged_odd", 1e-9)])
 def test_lanczos_converge_batched_checks_are_exact(dev, name, tol, monkeypatch):
     """Converge mode on small vectors runs up to 3 steps ahead of the host's residual test;
