@@ -606,6 +606,7 @@ __global__ void __launch_bounds__(kSmemStepThreads) cgs2_step_smem_kernel(
 // fixed-order grid sums: deterministic.
 // ------------------------------------------------------------------------------------
 constexpr int kStep3MaxJ = 24;
+constexpr int kStep3SmallJ = 12;  // the two-blocks-per-SM instantiation
 constexpr int kStep3Threads = 256;  // 1 block per SM: up to 255 registers for the basis entries
 
 // acc[0..j) per thread (+ slot j already in red when nq = j + 1) -> pp[q * G + blockIdx.x] = the
@@ -613,7 +614,7 @@ constexpr int kStep3Threads = 256;  // 1 block per SM: up to 255 registers for t
 #define HEFF_STEP3_BLOCK_PARTIALS(acc, nq, red, pp, G)                      \
   do {                                                                       \
     const int warp_ = threadIdx.x >> 5, lane_ = threadIdx.x & 31;            \
-    _Pragma("unroll") for (int q_ = 0; q_ < kStep3MaxJ; ++q_) if (q_ < (nq) && q_ < j) { \
+    _Pragma("unroll") for (int q_ = 0; q_ < kJ; ++q_) if (q_ < (nq) && q_ < j) { \
       const double v_ = warp_sum(acc[q_]);                                   \
       if (lane_ == 0) red[q_][warp_] = v_;                                   \
     }                                                                        \
@@ -625,7 +626,11 @@ constexpr int kStep3Threads = 256;  // 1 block per SM: up to 255 registers for t
     }                                                                        \
   } while (0)
 
-__global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const double* __restrict__ V, int64_t ldv, int j,
+// JM: the largest j of the instantiation (the basis entries of a thread's element live in
+// registers); MINB resident blocks per SM (<24, 1>: up to 255 registers; <12, 2>: twice the
+// warps per SM for j <= 12, more loads in flight)
+template <int JM, int MINB>
+__global__ void __launch_bounds__(kStep3Threads, MINB) cgs2_step3_kernel(const double* __restrict__ V, int64_t ldv, int j,
                                                                    double* __restrict__ w, int64_t n,
                                                                    double* __restrict__ partial, int jmax,
                                                                    double* __restrict__ c1, double* __restrict__ c2,
@@ -633,23 +638,24 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
                                                                    double* __restrict__ invb,
                                                                    double* __restrict__ vnext,
                                                                    unsigned int* __restrict__ gbar, int unroll2) {
+  constexpr int kJ = JM;
   cg::grid_group grid = cg::this_grid();
   auto gsync = [&] {  // gbar != null: ordinary launch (grid_barrier_flip), else cooperative
     if (gbar) grid_barrier_flip(gbar);
     else grid.sync();
   };
-  __shared__ double s_c[kStep3MaxJ + 1];
-  __shared__ double red[kStep3MaxJ + 1][kStep3Threads / 32];
+  __shared__ double s_c[kJ + 1];
+  __shared__ double red[kJ + 1][kStep3Threads / 32];
   pdl_wait();  // w comes from the matvec kernel before
   const int G = gridDim.x;
   const int64_t chunk = ((n + G - 1) / G + 1) / 2 * 2;
   const int64_t lo = min(n, (int64_t)blockIdx.x * chunk), hi = min(n, lo + chunk);
   double* p1 = partial;
   double* p2 = partial + (int64_t)jmax * G;
-  double acc[kStep3MaxJ + 1];
+  double acc[kJ + 1];
   // ---- pass A: c1 partials
 #pragma unroll
-  for (int q = 0; q <= kStep3MaxJ; ++q) acc[q] = 0.0;
+  for (int q = 0; q <= kJ; ++q) acc[q] = 0.0;
   // Two of the thread's elements per iteration: both elements' loads are issued before
   // the FMAs (one block of 8 warps per SM leaves little else to hide their latency); each
   // accumulator still adds element i before element i + kStep3Threads (same sums, bitwise).
@@ -658,22 +664,22 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
     for (; i + kStep3Threads < hi; i += 2 * kStep3Threads) {
       const int64_t i1 = i + kStep3Threads;
       const double x0 = w[i], x1 = w[i1];
-      double v0[kStep3MaxJ], v1[kStep3MaxJ];
+      double v0[kJ], v1[kJ];
 #pragma unroll
-      for (int q = 0; q < kStep3MaxJ; ++q)
+      for (int q = 0; q < kJ; ++q)
         if (q < j) {
           v0[q] = V[(int64_t)q * ldv + i];
           v1[q] = V[(int64_t)q * ldv + i1];
         }
 #pragma unroll
-      for (int q = 0; q < kStep3MaxJ; ++q)
+      for (int q = 0; q < kJ; ++q)
         if (q < j) acc[q] = fma(v1[q], x1, fma(v0[q], x0, acc[q]));
     }
   }
   for (; i < hi; i += kStep3Threads) {
     const double x = w[i];
 #pragma unroll
-    for (int q = 0; q < kStep3MaxJ; ++q)
+    for (int q = 0; q < kJ; ++q)
       if (q < j) acc[q] = fma(V[(int64_t)q * ldv + i], x, acc[q]);
   }
   HEFF_STEP3_BLOCK_PARTIALS(acc, j, red, p1, G);
@@ -684,21 +690,21 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
     for (int q = threadIdx.x; q < j; q += kStep3Threads) c1[q] = s_c[q];
   // ---- pass B: w' = w - V c1; c2 partials and ||w'||^2 from the same basis entries
 #pragma unroll
-  for (int q = 0; q <= kStep3MaxJ; ++q) acc[q] = 0.0;
+  for (int q = 0; q <= kJ; ++q) acc[q] = 0.0;
   double nacc = 0.0;
   i = lo + threadIdx.x;
   if (unroll2) {
     for (; i + kStep3Threads < hi; i += 2 * kStep3Threads) {
       const int64_t i1 = i + kStep3Threads;
-      double v0[kStep3MaxJ], v1[kStep3MaxJ];
+      double v0[kJ], v1[kJ];
 #pragma unroll
-      for (int q = 0; q < kStep3MaxJ; ++q) {
+      for (int q = 0; q < kJ; ++q) {
         v0[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
         v1[q] = q < j ? V[(int64_t)q * ldv + i1] : 0.0;
       }
       double x0 = w[i], x1 = w[i1];
 #pragma unroll
-      for (int q = 0; q < kStep3MaxJ; ++q)
+      for (int q = 0; q < kJ; ++q)
         if (q < j) {
           x0 = fma(-s_c[q], v0[q], x0);
           x1 = fma(-s_c[q], v1[q], x1);
@@ -706,22 +712,22 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
       w[i] = x0;
       w[i1] = x1;
 #pragma unroll
-      for (int q = 0; q < kStep3MaxJ; ++q)
+      for (int q = 0; q < kJ; ++q)
         if (q < j) acc[q] = fma(v1[q], x1, fma(v0[q], x0, acc[q]));
       nacc = fma(x1, x1, fma(x0, x0, nacc));
     }
   }
   for (; i < hi; i += kStep3Threads) {
-    double v[kStep3MaxJ];
+    double v[kJ];
 #pragma unroll
-    for (int q = 0; q < kStep3MaxJ; ++q) v[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
+    for (int q = 0; q < kJ; ++q) v[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
     double x = w[i];
 #pragma unroll
-    for (int q = 0; q < kStep3MaxJ; ++q)
+    for (int q = 0; q < kJ; ++q)
       if (q < j) x = fma(-s_c[q], v[q], x);
     w[i] = x;
 #pragma unroll
-    for (int q = 0; q < kStep3MaxJ; ++q)
+    for (int q = 0; q < kJ; ++q)
       if (q < j) acc[q] = fma(v[q], x, acc[q]);
     nacc = fma(x, x, nacc);
   }
@@ -751,15 +757,15 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
   if (unroll2) {
     for (; i + kStep3Threads < hi; i += 2 * kStep3Threads) {
       const int64_t i1 = i + kStep3Threads;
-      double v0[kStep3MaxJ], v1[kStep3MaxJ];
+      double v0[kJ], v1[kJ];
 #pragma unroll
-      for (int q = 0; q < kStep3MaxJ; ++q) {
+      for (int q = 0; q < kJ; ++q) {
         v0[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
         v1[q] = q < j ? V[(int64_t)q * ldv + i1] : 0.0;
       }
       double x0 = w[i], x1 = w[i1];
 #pragma unroll
-      for (int q = 0; q < kStep3MaxJ; ++q)
+      for (int q = 0; q < kJ; ++q)
         if (q < j) {
           x0 = fma(-s_c[q], v0[q], x0);
           x1 = fma(-s_c[q], v1[q], x1);
@@ -774,12 +780,12 @@ __global__ void __launch_bounds__(kStep3Threads, 1) cgs2_step3_kernel(const doub
     }
   }
   for (; i < hi; i += kStep3Threads) {
-    double v[kStep3MaxJ];
+    double v[kJ];
 #pragma unroll
-    for (int q = 0; q < kStep3MaxJ; ++q) v[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
+    for (int q = 0; q < kJ; ++q) v[q] = q < j ? V[(int64_t)q * ldv + i] : 0.0;
     double x = w[i];
 #pragma unroll
-    for (int q = 0; q < kStep3MaxJ; ++q)
+    for (int q = 0; q < kJ; ++q)
       if (q < j) x = fma(-s_c[q], v[q], x);
     if (vnext)
       vnext[i] = x * ib;

@@ -2272,7 +2272,7 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
   // (launch-bound sizes only: above ~2M elements the separate vectorised kernels stream faster)
   const bool fused = !cplx && (p->comm == nullptr) && (cap <= 4096) &&
                      (n <= (int64_t(1) << 21) || getenv("HEFF_FUSED_STEP")) && getenv("HEFF_NO_FUSED_STEP") == nullptr;
-  int step_grid = 0, step3_grid = 0;
+  int step_grid = 0, step3_grid = 0, step3s_grid = 0;
   // vectors up to this length take the one-block step kernel when the grid is one block
   // (HEFF_SMALL_STEP_N overrides; 0 = never)
   static const int64_t small_step_max = [] {
@@ -2293,9 +2293,13 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
     const int64_t want = std::max<int64_t>(1, (n + (int64_t)ept * kStepThreads - 1) / ((int64_t)ept * kStepThreads));
     step_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * g_num_sms, want));
     int per_sm3 = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, cgs2_step3_kernel, kStep3Threads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, cgs2_step3_kernel<kStep3MaxJ, 1>, kStep3Threads, 0));
     step3_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm3 * g_num_sms,
                                                              (n + kStep3Threads - 1) / kStep3Threads));
+    int per_sm3s = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3s, cgs2_step3_kernel<kStep3SmallJ, 2>, kStep3Threads, 0));
+    step3s_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm3s * g_num_sms,
+                                                              (n + kStep3Threads - 1) / kStep3Threads));
   }
   static const bool no_smem_step = getenv("HEFF_NO_SMEM_STEP") != nullptr;
   // multi-block CGS2 steps as ordinary launches with a flip-counter grid barrier (p->gbar)
@@ -2355,7 +2359,12 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       // cgs2_step3_kernel: two elements per thread per iteration when a thread owns >= 4
       // (measured, B200: C2, 6.9 per thread, Lanczos step 90.8 -> 85.5 us; at 1.7 per thread,
       // m = 128 chain / cylinder, 0.9-1.1 us slower); HEFF_STEP3_UNROLL=0/1 overrides
-      const int64_t per_thread = (n + (int64_t)step3_grid * kStep3Threads - 1) / ((int64_t)step3_grid * kStep3Threads);
+      // j <= kStep3SmallJ: the <12, 2> instantiation (two blocks per SM; HEFF_STEP3_SMALLJ=0 off)
+      const char* e_sj = getenv("HEFF_STEP3_SMALLJ");  // (read per call)
+      const bool small_j_off = e_sj && atoi(e_sj) == 0;
+      const bool small_j = three && j <= kStep3SmallJ && step3s_grid > 1 && !small_j_off;
+      const int g3 = small_j ? step3s_grid : step3_grid;
+      const int64_t per_thread = (n + (int64_t)g3 * kStep3Threads - 1) / ((int64_t)g3 * kStep3Threads);
       int unroll2 = per_thread >= 4;
       if (const char* e = getenv("HEFF_STEP3_UNROLL")) unroll2 = atoi(e) != 0;
       void* args[] = {(void*)&Vc, &ldv_, &jj, &wp, &nn, &partial, &jmax, &c1, &c2, &alpha, &beta, &invb, &vnext, &gbar,
@@ -2376,11 +2385,14 @@ extern "C" int lanczos_ground(heff_plan p, double* psi, const heff_lanczos_opts*
       cfg.numAttrs = 2;
       if (three) {
         cfg.dynamicSmemBytes = 0;
-        cfg.gridDim = dim3(step3_grid);
+        cfg.gridDim = dim3(g3);
         cfg.blockDim = dim3(kStep3Threads);
-        at[0].val.cooperative = step3_grid > 1 && !step_noncoop ? 1 : 0;
+        at[0].val.cooperative = g3 > 1 && !step_noncoop ? 1 : 0;
       }
-      CK(cudaLaunchKernelExC(&cfg, three ? (const void*)cgs2_step3_kernel : (const void*)cgs2_step_kernel, args));
+      const void* kfn = !three ? (const void*)cgs2_step_kernel
+                               : small_j ? (const void*)cgs2_step3_kernel<kStep3SmallJ, 2>
+                                         : (const void*)cgs2_step3_kernel<kStep3MaxJ, 1>;
+      CK(cudaLaunchKernelExC(&cfg, kfn, args));
       ++p->total_launches;
       return HEFF_OK;
     }

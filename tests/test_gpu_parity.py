@@ -229,6 +229,31 @@ def test_lanczos_step3_unroll_is_bitwise(dev, m, monkeypatch):
 
 
 @pytest.mark.parametrize("m", [128, 256])
+def test_lanczos_step3_two_blocks_per_sm(dev, m, monkeypatch):
+    """j <= 12 steps on the two-blocks-per-SM step3 instantiation (a different grid, so
+    different partial sums): deterministic run to run, and T_j / energy / Ritz vector equal
+    to the one-block-per-SM kernel's to rounding (Lanczos parity vs the oracle runs the
+    default)."""
+    from paper_2007_14822_b200 import Heff
+    xd = C.make("c2", m=m).to(dev)
+    out = {}
+    with Heff(xd.L, xd.W1, xd.W2, xd.R) as h:
+        for flag in ("1", "0", "1"):
+            monkeypatch.setenv("HEFF_STEP3_SMALLJ", flag)
+            v = xd.psi.clone()
+            r = h.lanczos_ground(v, max_iter=20)
+            res = (r.energy, r.iters, np.array(r.alpha), np.array(r.beta), v.cpu().numpy())
+            if flag in out:
+                a = out[flag]
+                assert a[0] == res[0] and np.array_equal(a[2], res[2]) and np.array_equal(a[4], res[4])
+            out[flag] = res
+    a, b = out["1"], out["0"]
+    assert a[1] == b[1] and abs(a[0] - b[0]) <= 1e-12 * abs(b[0])
+    assert np.max(np.abs(a[2] - b[2])) <= 1e-10 and np.max(np.abs(a[3] - b[3])) <= 1e-10
+    assert abs(abs(float(np.dot(a[4].ravel(), b[4].ravel()))) - 1.0) <= 1e-9
+
+
+@pytest.mark.parametrize("m", [128, 256])
 def test_lanczos_step_grid_barrier_matches_cooperative(dev, m, monkeypatch):
     """The multi-block CGS2 steps launched as ordinary kernels (flip-counter grid barrier)
     must give bitwise the cooperative launch's T_j and Ritz vector, over 30 steps (three-pass
